@@ -1,0 +1,207 @@
+/*
+ * sparsla_c.h — C ABI of the B200-native sparse Krylov solve loop (libsparsla_b200.so).
+ *
+ * Drop-in boundary for the reference's sparse-tensor / solve API in proj/core
+ * (namespace sparsla, /root/reference/proj/core/include/sparsla/sparse.hpp:18-149 and
+ * the SPEC.md:122-544 contracts whose sources are missing from the reference tree).
+ * The C++ headers in include/sparsla/ are header-only wrappers over this ABI that keep
+ * the reference's signatures and exception classes (errors.hpp:9-62).
+ *
+ * Conventions
+ *   - Every function returns a sparsla_status (0 = OK).  The message of the last error on
+ *     the calling thread is sparsla_last_error_message().
+ *   - Index arrays use the reference layout (int64, sparse.hpp:20) unless the name ends in
+ *     _i32.  On the device the library stores int32 local indices and fp64 values.
+ *   - `mem` selects whether vector pointers are host (SPARSLA_MEM_HOST: copied in/out inside
+ *     the call) or device (SPARSLA_MEM_DEVICE: resident, zero-copy) memory.
+ *   - Each device handle binds one CUDA device and owns one non-default stream; calls on
+ *     distinct handles are reentrant.
+ *   - There is no CPU fallback: device entry points fail with SPARSLA_ERR_NO_DEVICE when no
+ *     CUDA device is visible.
+ */
+#ifndef SPARSLA_C_H
+#define SPARSLA_C_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* One code per exception class of errors.hpp:9-62, plus device/transport failures. */
+typedef enum {
+    SPARSLA_OK = 0,
+    SPARSLA_ERR_DIMENSION = 1,        /* DimensionError        errors.hpp:15-18 */
+    SPARSLA_ERR_BOUNDS = 2,           /* BoundsError           errors.hpp:21-24 */
+    SPARSLA_ERR_FORMAT = 3,           /* FormatError           errors.hpp:27-38 */
+    SPARSLA_ERR_SINGULAR = 4,         /* SingularMatrixError   errors.hpp:41-44 */
+    SPARSLA_ERR_UNSUPPORTED = 5,      /* UnsupportedInputError errors.hpp:48-51 */
+    SPARSLA_ERR_INVALID_ARGUMENT = 6, /* InvalidArgumentError  errors.hpp:53-56 */
+    SPARSLA_ERR_TRANSPORT = 7,        /* TransportError        errors.hpp:59-62 */
+    SPARSLA_ERR_CUDA = 8,             /* -> Error */
+    SPARSLA_ERR_NCCL = 9,             /* -> TransportError */
+    SPARSLA_ERR_NO_DEVICE = 10,       /* -> Error */
+    SPARSLA_ERR_INTERNAL = 11         /* -> Error */
+} sparsla_status;
+
+typedef enum { SPARSLA_MEM_HOST = 0, SPARSLA_MEM_DEVICE = 1 } sparsla_mem;
+typedef enum { SPARSLA_PRECOND_NONE = 0, SPARSLA_PRECOND_JACOBI = 1 } sparsla_precond;
+typedef enum { SPARSLA_BACKEND_CG = 0, SPARSLA_BACKEND_BICGSTAB = 1 } sparsla_backend;
+
+/* SolveOptions: atol >= 0, rtol >= 0, not both zero, max_iter >= 1. */
+typedef struct {
+    double atol;
+    double rtol;
+    int64_t max_iter;
+    int32_t preconditioner; /* sparsla_precond */
+    int32_t _pad;
+} sparsla_solve_options;
+
+/* SolveReport.  Non-convergence and breakdown are reported here, not
+ * returned as errors. */
+typedef struct {
+    int64_t iterations;
+    int64_t spmv_count;
+    double residual_norm;
+    int32_t converged;
+    int32_t backend; /* sparsla_backend */
+    char diagnostic[128];
+} sparsla_solve_report;
+
+const char* sparsla_last_error_message(void);
+int sparsla_version(void); /* major*10000 + minor*100 + patch */
+
+/* ======================= host-side sparse core (no GPU needed) ======================= */
+
+/* SparseCoo canonicalizing constructor (sparse.hpp:43-47, sparse.cpp:9-53): stable order
+ * by (row, col), duplicates summed in input order, explicit zeros kept.  Outputs have room
+ * for nnz entries; *out_nnz receives the canonical count. */
+int sparsla_coo_canonicalize(int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* rows,
+                             const int64_t* cols, const double* vals, int64_t* out_nnz,
+                             int64_t* rows_out, int64_t* cols_out, double* vals_out);
+/* CsrMatrix::from_coo (sparse.hpp:84, sparse.cpp:94-116), input must be canonical. */
+int sparsla_csr_from_coo(int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* rows,
+                         const int64_t* cols, const double* vals, int64_t* row_ptr,
+                         int64_t* col_idx, double* vals_out);
+/* CsrMatrix::to_coo (sparse.hpp:86-87, sparse.cpp:118-127): expands row ids. */
+int sparsla_csr_to_coo_rows(int64_t nrows, const int64_t* row_ptr, int64_t* rows_out);
+/* canonical A^T as CSR (transpose, sparse.hpp:141, sparse.cpp:176-182). */
+int sparsla_csr_transpose(int64_t nrows, int64_t ncols, const int64_t* row_ptr,
+                          const int64_t* col_idx, const double* vals, int64_t* t_row_ptr,
+                          int64_t* t_col_idx, double* t_vals);
+/* is_structurally_symmetric / is_symmetric (sparse.hpp:144-147, sparse.cpp:184-205) on a
+ * canonical CSR.  out = 0/1. */
+int sparsla_csr_symmetry(int64_t nrows, int64_t ncols, const int64_t* row_ptr,
+                         const int64_t* col_idx, const double* vals, double tol,
+                         int32_t* structurally_symmetric, int32_t* symmetric);
+
+/* Problem generators (SPEC.md:551-569 + SURVEY.md §8d), emitting canonical CSR rows
+ * [row_begin, row_end) directly (equal, bit for bit, to SparseCoo canonicalization of the
+ * element-order triplets).  kind: 0 poisson2d(N=p1), 1 poisson3d(N=p1),
+ * 2 convdiff3d(N=p1, c=fparam), 3 fem2d(m=p1, seed=p2).
+ * sparsla_gen_size: global n and the nnz of the row range.
+ * sparsla_gen_csr: row_ptr[row_end-row_begin+1] (starts at 0), col_idx/vals[nnz]. */
+int sparsla_gen_size(int32_t kind, int64_t p1, int64_t p2, double fparam, int64_t row_begin,
+                     int64_t row_end, int64_t* n_global, int64_t* nnz_range);
+int sparsla_gen_csr(int32_t kind, int64_t p1, int64_t p2, double fparam, int64_t row_begin,
+                    int64_t row_end, int64_t* row_ptr, int64_t* col_idx, double* vals);
+int sparsla_gen_csr_i32(int32_t kind, int64_t p1, int64_t p2, double fparam,
+                        int64_t row_begin, int64_t row_end, int32_t* row_ptr,
+                        int32_t* col_idx, double* vals);
+/* 2-D node coordinates (kind 0 grid, kind 3 FEM interior nodes) for partition_rcb. */
+int sparsla_gen_coords(int32_t kind, int64_t p1, int64_t p2, double* xs, double* ys);
+
+/* Partitioners. */
+int sparsla_partition_contiguous(int64_t n, int32_t nparts, int32_t* part_of);
+int sparsla_partition_rcb(int64_t n, const double* xs, const double* ys, int32_t nparts,
+                          int32_t* part_of);
+
+/* build_local for a structurally symmetric pattern, from this rank's
+ * owned rows only.  Inputs: part_of[n_global], the owned rows (ascending global ids) as a
+ * CSR with GLOBAL column ids.  The result handle exposes the SPEC-layout maps:
+ *   owned (ascending global), halo (ascending global), neighbors (ascending rank),
+ *   send_ptr/send_idx, recv_ptr/recv_idx (local positions in [owned | halo], canonical
+ *   global order), and the local matrix with columns relabelled to [owned | halo] while
+ *   every row keeps its global column order (so local SpMV reproduces serial row sums).
+ * sizes[0]=n_owned [1]=n_halo [2]=n_neighbors [3]=nnz_local [4]=total_send [5]=total_recv */
+typedef struct sparsla_local sparsla_local;
+int sparsla_local_build(int64_t n_global, const int32_t* part_of, int32_t nparts, int32_t rank,
+                        int64_t n_owned, const int64_t* owned, const int64_t* row_ptr,
+                        const int64_t* col_idx, const double* vals, sparsla_local** out);
+int sparsla_local_sizes(const sparsla_local* L, int64_t* sizes);
+int sparsla_local_get(const sparsla_local* L, int64_t* owned, int64_t* halo, int32_t* neighbors,
+                      int64_t* send_ptr, int64_t* send_idx, int64_t* recv_ptr,
+                      int64_t* recv_idx, int64_t* l_row_ptr, int64_t* l_col_idx,
+                      double* l_vals);
+int sparsla_local_destroy(sparsla_local* L);
+
+/* ============================ device CSR (one GPU) =================================== */
+typedef struct sparsla_dcsr sparsla_dcsr;
+
+int sparsla_device_count(int* count);
+/* Upload a canonical CSR (reference int64 layout) to `device`.  Rows must have strictly
+ * increasing columns (CsrMatrix invariant, sparse.hpp:76-78). */
+int sparsla_dcsr_create(int device, int64_t nrows, int64_t ncols, const int64_t* row_ptr,
+                        const int64_t* col_idx, const double* vals, sparsla_dcsr** out);
+/* Same with int32 host arrays (no index conversion on the host). */
+int sparsla_dcsr_create_i32(int device, int64_t nrows, int64_t ncols, const int32_t* row_ptr,
+                            const int32_t* col_idx, const double* vals, sparsla_dcsr** out);
+/* SparseCoo::with_values (sparse.hpp:58-61): same pattern, new values. */
+int sparsla_dcsr_set_values(sparsla_dcsr* A, const double* vals, int32_t mem);
+int sparsla_dcsr_destroy(sparsla_dcsr* A);
+/* info[0]=nrows [1]=ncols [2]=nnz [3]=device bytes of the matrix [4]=max nnz per 256-row
+ * block [5]=max row length [6]=kernel variant used by spmv (0 staged, 1 long-row) */
+int sparsla_dcsr_info(const sparsla_dcsr* A, int64_t* info);
+
+/* y = A x (sparse.cpp:135-154): rows accumulated left to right from 0.0, separate
+ * multiply and add — bitwise equal to the reference.  mem: see above. */
+int sparsla_spmv(sparsla_dcsr* A, const double* x, double* y, int32_t mem);
+/* y = A^T x (spmv_transpose, sparse.cpp:156-174), via an explicit canonical A^T kept on
+ * the device, bitwise equal to the reference scatter order. */
+int sparsla_spmv_transpose(sparsla_dcsr* A, const double* x, double* y, int32_t mem);
+/* canonical dot of two device/host vectors. */
+int sparsla_dot(int device, int64_t n, const double* a, const double* b, int32_t mem,
+                double* out);
+/* Jacobi inverse diagonal (jacobi_build). */
+int sparsla_jacobi(sparsla_dcsr* A, double* dinv, int32_t mem);
+
+/* cg_solve / bicgstab_solve, x0 = 0. */
+int sparsla_cg_solve(sparsla_dcsr* A, const double* b, double* x,
+                     const sparsla_solve_options* opts, sparsla_solve_report* report,
+                     int32_t mem);
+int sparsla_bicgstab_solve(sparsla_dcsr* A, const double* b, double* x,
+                           const sparsla_solve_options* opts, sparsla_solve_report* report,
+                           int32_t mem);
+
+/* solve_backward (Alg. 1): exactly one solve A^T lam = grad_x
+ * with `backend`; grad_b = lam; grad_vals[k] = -(lam[row_k] * x[col_k]) in CSR (= canonical
+ * COO) order.  A exactly-symmetric A is reused as its own transpose. */
+int sparsla_adjoint_backward(sparsla_dcsr* A, const double* x, const double* grad_x,
+                             int32_t backend, const sparsla_solve_options* opts,
+                             double* grad_b, double* grad_vals, sparsla_solve_report* report,
+                             int32_t mem);
+
+/* ============ bench / instrumentation hooks (persistent device-resident solver) ========= */
+/* A prepared solver keeps b, x and all work vectors resident and captures the iteration
+ * in a CUDA graph; `iterate` runs up to `iters` more iterations (stops early when the
+ * solve terminates).  Used by bench.py to time iterations with inputs resident in HBM. */
+typedef struct sparsla_solver sparsla_solver;
+int sparsla_solver_create(sparsla_dcsr* A, int32_t backend, const double* b, int32_t mem,
+                          const sparsla_solve_options* opts, sparsla_solver** out);
+int sparsla_solver_reset(sparsla_solver* S); /* x = 0, initial residual, state reset */
+int sparsla_solver_iterate(sparsla_solver* S, int64_t iters);
+int sparsla_solver_run(sparsla_solver* S); /* to termination */
+int sparsla_solver_report(sparsla_solver* S, sparsla_solve_report* report);
+int sparsla_solver_get_x(sparsla_solver* S, double* x, int32_t mem);
+/* device pointer of the handle's CUDA stream (cudaStream_t), for event timing */
+int sparsla_solver_stream(sparsla_solver* S, void** stream);
+/* number of kernel launches one iteration issues */
+int sparsla_solver_launches_per_iteration(sparsla_solver* S, int64_t* launches);
+int sparsla_solver_destroy(sparsla_solver* S);
+/* time `reps` SpMV launches on the handle stream, returns avg ms per launch */
+int sparsla_spmv_bench(sparsla_dcsr* A, int32_t reps, double* ms_per_launch);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPARSLA_C_H */

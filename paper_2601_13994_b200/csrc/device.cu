@@ -1,0 +1,753 @@
+// device.cu — device CSR handle, Krylov solver driver, adjoint backward and their C ABI.
+//
+// Single-GPU solve loop (per iteration, all on one stream, captured once into a CUDA graph):
+//   CG:        spmv<CG> (q = A p, p.q, alpha)   vec<CG_U1> (x, r, r.z, r.r, beta/conv)
+//              vec<CG_U2> (p = z + beta p)                               = 3 launches
+//   BiCGStab:  vec<BI_U1> spmv<BICG_V> vec<BI_U2> spmv<BICG_T> vec<BI_U3> = 5 launches
+// Every scalar decision is made on the device (kernels.cuh apply_scalar); once the solve
+// terminates every kernel exits at entry, so extra graph replays are no-ops and the host
+// only polls a pinned flag once per graph (G iterations) — never per iteration.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.hpp"
+#include "device.hpp"
+#include "kernels.cuh"
+
+namespace sparsla_b200 {
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(SPARSLA_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define CK(x) cuda_check((x), #x)
+
+DeviceGuard::DeviceGuard(int dev) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        fail(SPARSLA_ERR_NO_DEVICE, "no CUDA device visible (the sparsla B200 path has no CPU fallback)");
+    }
+    if (dev < 0 || dev >= n) fail(SPARSLA_ERR_INVALID_ARGUMENT, "device ordinal out of range");
+    CK(cudaGetDevice(&prev_));
+    if (prev_ != dev) CK(cudaSetDevice(dev));
+}
+DeviceGuard::~DeviceGuard() { cudaSetDevice(prev_); }
+
+template <class T>
+T* dalloc(size_t count) {
+    void* p = nullptr;
+    CK(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)));
+    return static_cast<T*>(p);
+}
+
+static inline unsigned grid_for(long long n, int per) { return (unsigned)((n + per - 1) / per); }
+static inline long long nchunks_of(long long n) { return (n + kChunk - 1) / kChunk; }
+
+// ------------------------------------------------------------------ DevCsr ---------
+DevCsr::~DevCsr() {
+    DeviceGuard g(device);
+    cudaFree(rp); cudaFree(ci); cudaFree(val); cudaFree(dinv); cudaFree(ones);
+    if (stream) cudaStreamDestroy(stream);
+    delete transpose;
+}
+
+static void configure_kernels_once(int device) {
+    static std::mutex mu;
+    static std::vector<int> done;
+    std::lock_guard<std::mutex> lk(mu);
+    if (std::find(done.begin(), done.end(), device) != done.end()) return;
+    const int max_smem = 160 * 1024;  // staged variant is chosen only up to 110 KB
+    CK(cudaFuncSetAttribute(spmv_kernel<SPMV_PLAIN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
+    CK(cudaFuncSetAttribute(spmv_kernel<SPMV_CG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
+    CK(cudaFuncSetAttribute(spmv_kernel<SPMV_BICG_V, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
+    CK(cudaFuncSetAttribute(spmv_kernel<SPMV_BICG_T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
+    done.push_back(device);
+}
+
+template <class I>
+DevCsr* DevCsr::create(int device, long long nrows, long long ncols, const I* h_rp, const I* h_ci,
+                       const double* h_val) {
+    if (nrows < 0 || ncols < 0) fail(SPARSLA_ERR_DIMENSION, "negative matrix shape");
+    validate_csr<I>(nrows, ncols, h_rp, h_ci);
+    const long long nnz = static_cast<long long>(h_rp[nrows]);
+    if (nrows >= (1LL << 31) || ncols >= (1LL << 31) || nnz >= (1LL << 31))
+        fail(SPARSLA_ERR_UNSUPPORTED,
+             "this build stores int32 row_ptr/col_idx per device: rows, cols and nnz must be < 2^31 "
+             "(shard larger matrices across GPUs)");
+    DeviceGuard g(device);
+    configure_kernels_once(device);
+    auto A = std::make_unique<DevCsr>();
+    A->device = device;
+    A->nrows = nrows; A->ncols = ncols; A->nnz = nnz;
+    CK(cudaStreamCreateWithFlags(&A->stream, cudaStreamNonBlocking));
+    // int32 device layout (+ padding for the bulk-copy over-read)
+    A->rp = dalloc<int32_t>(nrows + 1 + kRpCopy + 8);
+    A->ci = dalloc<int32_t>(nnz + 8);
+    A->val = dalloc<double>(nnz + 4);
+    CK(cudaMemset(A->rp, 0, (nrows + 1 + kRpCopy + 8) * sizeof(int32_t)));
+    CK(cudaMemset(A->ci + nnz, 0, 8 * sizeof(int32_t)));
+    CK(cudaMemset(A->val + nnz, 0, 4 * sizeof(double)));
+    if constexpr (sizeof(I) == 4) {
+        CK(cudaMemcpy(A->rp, h_rp, (nrows + 1) * sizeof(int32_t), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(A->ci, h_ci, nnz * sizeof(int32_t), cudaMemcpyHostToDevice));
+    } else {
+        std::vector<int32_t> tmp(static_cast<size_t>(std::max(nrows + 1, nnz)));
+        parallel_for(nrows + 1, [&](int64_t a, int64_t b) { for (int64_t i = a; i < b; ++i) tmp[i] = (int32_t)h_rp[i]; });
+        CK(cudaMemcpy(A->rp, tmp.data(), (nrows + 1) * sizeof(int32_t), cudaMemcpyHostToDevice));
+        parallel_for(nnz, [&](int64_t a, int64_t b) { for (int64_t i = a; i < b; ++i) tmp[i] = (int32_t)h_ci[i]; });
+        CK(cudaMemcpy(A->ci, tmp.data(), nnz * sizeof(int32_t), cudaMemcpyHostToDevice));
+    }
+    CK(cudaMemcpy(A->val, h_val, nnz * sizeof(double), cudaMemcpyHostToDevice));
+    // row-length statistics -> SpMV variant and staging capacity
+    long long mb = 0, mr = 0;
+    for (long long b = 0; b < nrows; b += kChunkSlots) {
+        const long long e = std::min(b + kChunkSlots, nrows);
+        mb = std::max<long long>(mb, (long long)h_rp[e] - (long long)h_rp[b]);
+    }
+    for (long long i = 0; i < nrows; ++i) mr = std::max<long long>(mr, (long long)h_rp[i + 1] - (long long)h_rp[i]);
+    A->max_block_nnz = mb;
+    A->max_row = mr;
+    A->cap_v = (int)(((mb + 2) + 1) & ~1LL);
+    A->cap_c = (int)(((mb + 6) + 3) & ~3LL);
+    const size_t vb = ((size_t)A->cap_v * 8 + 127) & ~size_t(127);
+    const size_t cb = ((size_t)A->cap_c * 4 + 127) & ~size_t(127);
+    const size_t rb = (kRpCopy * 4 + 127) & ~size_t(127);
+    A->smem_bytes = 128 + kStages * (vb + cb + rb);
+    A->staged = A->smem_bytes <= 110 * 1024;
+    CK(cudaDeviceSynchronize());
+    return A.release();
+}
+template DevCsr* DevCsr::create<int64_t>(int, long long, long long, const int64_t*, const int64_t*, const double*);
+template DevCsr* DevCsr::create<int32_t>(int, long long, long long, const int32_t*, const int32_t*, const double*);
+
+const double* DevCsr::jacobi_dinv() {
+    if (!dinv) {
+        DeviceGuard g(device);
+        if (nrows != ncols) fail(SPARSLA_ERR_DIMENSION, "jacobi_build requires a square matrix");
+        dinv = dalloc<double>(nrows + 2);
+        if (nrows > 0)
+            jacobi_kernel<<<grid_for(nrows, 256), 256, 0, stream>>>(rp, ci, val, nrows, 0, dinv);
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(stream));
+    }
+    return dinv;
+}
+
+const double* DevCsr::ones_vec() {
+    if (!ones) {
+        DeviceGuard g(device);
+        ones = dalloc<double>(nrows + 2);
+        if (nrows > 0) fill_kernel<<<grid_for(nrows, 256), 256, 0, stream>>>(ones, nrows, 1.0);
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(stream));
+    }
+    return ones;
+}
+
+bool DevCsr::exactly_symmetric() {
+    if (sym_checked < 0) {
+        DeviceGuard g(device);
+        if (nrows != ncols) { sym_checked = 0; return false; }
+        int* flags = dalloc<int>(2);
+        const int one[2] = {1, 1};
+        CK(cudaMemcpy(flags, one, sizeof(one), cudaMemcpyHostToDevice));
+        if (nrows > 0) symmetry_kernel<<<grid_for(nrows, 256), 256, 0, stream>>>(rp, ci, val, nrows, flags);
+        CK(cudaGetLastError());
+        int h[2];
+        CK(cudaMemcpyAsync(h, flags, sizeof(h), cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        cudaFree(flags);
+        sym_checked = h[1] ? 1 : 0;
+    }
+    return sym_checked == 1;
+}
+
+// canonical A^T (setup, nonsymmetric adjoint / spmv_transpose)
+DevCsr* DevCsr::get_transpose() {
+    if (!transpose) {
+        DeviceGuard g(device);
+        std::vector<int32_t> hrp(nrows + 1), hci(nnz);
+        std::vector<double> hv(nnz);
+        CK(cudaMemcpy(hrp.data(), rp, (nrows + 1) * 4, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(hci.data(), ci, nnz * 4, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(hv.data(), val, nnz * 8, cudaMemcpyDeviceToHost));
+        std::vector<int32_t> trp(ncols + 1, 0), tci(nnz);
+        std::vector<double> tv(nnz);
+        for (long long k = 0; k < nnz; ++k) ++trp[hci[k] + 1];
+        for (long long j = 0; j < ncols; ++j) trp[j + 1] += trp[j];
+        std::vector<int32_t> next(trp.begin(), trp.end() - 1);
+        for (long long i = 0; i < nrows; ++i)
+            for (int k = hrp[i]; k < hrp[i + 1]; ++k) {
+                const int pos = next[hci[k]]++;
+                tci[pos] = (int32_t)i;
+                tv[pos] = hv[k];
+            }
+        transpose = DevCsr::create<int32_t>(device, ncols, nrows, trp.data(), tci.data(), tv.data());
+    }
+    return transpose;
+}
+
+// ------------------------------------------------------------------ launches -------
+void launch_spmv(DevCsr* A, cudaStream_t s, int mode, const double* x, double* y, const double* aux,
+                 const RedParams& red, int check_done) {
+    if (A->nrows == 0) return;
+    SpmvParams P{};
+    P.rp = A->rp; P.ci = A->ci; P.val = A->val;
+    P.x = x; P.y = y; P.n = A->nrows; P.chunk0 = 0; P.aux = aux;
+    P.cap_v = A->cap_v; P.cap_c = A->cap_c;
+    P.check_done = check_done;
+    P.red = red;
+    P.red.nchunks = nchunks_of(A->nrows);
+    P.red.expected = (unsigned)P.red.nchunks;
+    const unsigned grid = (unsigned)nchunks_of(A->nrows);
+    const size_t smem = A->staged ? A->smem_bytes : 0;
+#define SPMV_CASE(M)                                                                     \
+    if (A->staged) spmv_kernel<M, true><<<grid, kSpmvThreads, smem, s>>>(P);            \
+    else spmv_kernel<M, false><<<grid, kSpmvThreads, 0, s>>>(P);
+    switch (mode) {
+        case SPMV_PLAIN: SPMV_CASE(SPMV_PLAIN) break;
+        case SPMV_CG: SPMV_CASE(SPMV_CG) break;
+        case SPMV_BICG_V: SPMV_CASE(SPMV_BICG_V) break;
+        case SPMV_BICG_T: SPMV_CASE(SPMV_BICG_T) break;
+    }
+#undef SPMV_CASE
+    CK(cudaGetLastError());
+}
+
+template <int OP>
+void launch_vec(cudaStream_t s, const VecParams& P0, RedParams red) {
+    if (P0.n == 0) return;
+    VecParams P = P0;
+    P.red = red;
+    P.red.nchunks = nchunks_of(P.n);
+    P.red.expected = (unsigned)P.red.nchunks;
+    vec_kernel<OP><<<(unsigned)nchunks_of(P.n), kVecThreads, 0, s>>>(P);
+    CK(cudaGetLastError());
+}
+
+// ------------------------------------------------------------------ Solver ---------
+Solver::Solver(DevCsr* A_, int backend_, const sparsla_solve_options& o) : A(A_), backend(backend_), opts(o) {
+    if (!(o.atol >= 0.0) || !(o.rtol >= 0.0) || (o.atol == 0.0 && o.rtol == 0.0))
+        fail(SPARSLA_ERR_INVALID_ARGUMENT, "SolveOptions: atol >= 0, rtol >= 0, not both zero (SPEC.md:129)");
+    if (o.max_iter < 1) fail(SPARSLA_ERR_INVALID_ARGUMENT, "SolveOptions: max_iter >= 1");
+    if (o.preconditioner != SPARSLA_PRECOND_NONE && o.preconditioner != SPARSLA_PRECOND_JACOBI)
+        fail(SPARSLA_ERR_INVALID_ARGUMENT, "SolveOptions: unknown preconditioner");
+    if (A->nrows != A->ncols) fail(SPARSLA_ERR_DIMENSION, "Krylov solve requires a square matrix");
+    DeviceGuard g(A->device);
+    n = A->nrows;
+    stream = A->stream;
+    dinv = o.preconditioner == SPARSLA_PRECOND_JACOBI ? A->jacobi_dinv() : A->ones_vec();
+    const long long m = std::max<long long>(1, nchunks_of(n));
+    const long long nv = n + 2;
+    x_own = dalloc<double>(nv); b_own = dalloc<double>(nv);
+    r = dalloc<double>(nv); p = dalloc<double>(nv); q = dalloc<double>(nv);
+    if (backend == SPARSLA_BACKEND_BICGSTAB) {
+        rh = dalloc<double>(nv); ph = dalloc<double>(nv); s = dalloc<double>(nv);
+        sh = dalloc<double>(nv); t = dalloc<double>(nv);
+    }
+    partials = dalloc<double>(3 * m);
+    tickets = dalloc<unsigned>(8);
+    CK(cudaMemset(tickets, 0, 8 * sizeof(unsigned)));
+    st = dalloc<KState>(1);
+    CK(cudaMallocHost(&h_st, sizeof(KState)));
+    CK(cudaMallocHost(&h_flag, 2 * sizeof(int)));
+    CK(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+    x = x_own; b = b_own;
+}
+
+Solver::~Solver() {
+    DeviceGuard g(A->device);
+    if (g_many) cudaGraphExecDestroy(g_many);
+    if (g_one) cudaGraphExecDestroy(g_one);
+    for (double* v : {x_own, b_own, r, p, q, rh, ph, s, sh, t}) cudaFree(v);
+    cudaFree(partials); cudaFree(tickets); cudaFree(st);
+    cudaFreeHost(h_st); cudaFreeHost(h_flag);
+    cudaEventDestroy(ev[0]); cudaEventDestroy(ev[1]);
+}
+
+RedParams Solver::red(int which, int slot) const {
+    RedParams R{};
+    R.partials = partials; R.ticket = tickets + slot; R.st = st; R.red_out = nullptr; R.scalar = which;
+    return R;
+}
+
+VecParams Solver::vparams() const {
+    VecParams P{};
+    P.n = n; P.d = dinv; P.x = x; P.r = r; P.p = p; P.q = q;
+    P.rh = rh; P.ph = ph; P.v = q; P.s = s; P.sh = sh; P.tt = t; P.b = b;
+    P.check_done = 1;
+    return P;
+}
+
+void Solver::enqueue_init() {
+    KState h{};
+    h.atol = opts.atol; h.rtol = opts.rtol; h.max_iter = opts.max_iter;
+    h.spmv_count = 1;
+    *h_st = h;
+    CK(cudaMemcpyAsync(st, h_st, sizeof(KState), cudaMemcpyHostToDevice, stream));
+    CK(cudaMemsetAsync(tickets, 0, 8 * sizeof(unsigned), stream));
+    CK(cudaMemsetAsync(x, 0, n * sizeof(double), stream));
+    RedParams none{};
+    VecParams P = vparams();
+    P.check_done = 0;
+    if (backend == SPARSLA_BACKEND_CG) {
+        launch_spmv(A, stream, SPMV_PLAIN, x, q, nullptr, none, 0);  // r0 = b - A x0
+        launch_vec<V_CG_INIT>(stream, P, red(SC_CG_INIT, 0));
+    } else {
+        launch_spmv(A, stream, SPMV_PLAIN, x, q, nullptr, none, 0);  // v = A x0
+        launch_vec<V_BI_INIT>(stream, P, red(SC_BI_INIT, 0));
+    }
+    if (n == 0) {  // empty system: converged with zero residual
+        KState z = h;
+        z.converged = 1; z.status = ST_CONVERGED; z.done = 1;
+        *h_st = z;
+        CK(cudaMemcpyAsync(st, h_st, sizeof(KState), cudaMemcpyHostToDevice, stream));
+    }
+}
+
+void Solver::enqueue_iteration() {
+    VecParams P = vparams();
+    if (backend == SPARSLA_BACKEND_CG) {
+        launch_spmv(A, stream, SPMV_CG, p, q, nullptr, red(SC_CG_PQ, 1), 1);
+        launch_vec<V_CG_U1>(stream, P, red(SC_CG_RR, 2));
+        launch_vec<V_CG_U2>(stream, P, red(SC_NONE, 3));
+    } else {
+        launch_vec<V_BI_U1>(stream, P, red(SC_NONE, 1));
+        launch_spmv(A, stream, SPMV_BICG_V, ph, q, rh, red(SC_BI_RV, 2), 1);
+        launch_vec<V_BI_U2>(stream, P, red(SC_NONE, 3));
+        launch_spmv(A, stream, SPMV_BICG_T, sh, t, s, red(SC_BI_T, 4), 1);
+        launch_vec<V_BI_U3>(stream, P, red(SC_BI_U3, 5));
+    }
+}
+
+long long Solver::launches_per_iteration() const { return backend == SPARSLA_BACKEND_CG ? 3 : 5; }
+
+void Solver::build_graphs() {
+    if (g_many) return;
+    auto capture = [&](int iters) {
+        cudaGraph_t graph;
+        CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+        for (int i = 0; i < iters; ++i) enqueue_iteration();
+        CK(cudaStreamEndCapture(stream, &graph));
+        cudaGraphExec_t exec;
+        CK(cudaGraphInstantiate(&exec, graph, 0));
+        CK(cudaGraphDestroy(graph));
+        return exec;
+    };
+    g_many = capture(kGraphIters);
+    g_one = capture(1);
+}
+
+void Solver::set_b(const double* src, int mem) {
+    DeviceGuard g(A->device);
+    if (mem == SPARSLA_MEM_DEVICE) b = src;
+    else { b = b_own; CK(cudaMemcpyAsync(b_own, src, n * sizeof(double), cudaMemcpyHostToDevice, stream)); }
+}
+
+void Solver::reset() {
+    DeviceGuard g(A->device);
+    build_graphs();
+    enqueue_init();
+}
+
+void Solver::iterate(long long iters) {
+    DeviceGuard g(A->device);
+    build_graphs();
+    while (iters >= kGraphIters) { CK(cudaGraphLaunch(g_many, stream)); iters -= kGraphIters; }
+    while (iters-- > 0) CK(cudaGraphLaunch(g_one, stream));
+}
+
+void Solver::run() {
+    DeviceGuard g(A->device);
+    build_graphs();
+    // Poll the device 'done' flag once per graph, one graph behind (no per-iteration sync).
+    const long long max_graphs = opts.max_iter / kGraphIters + 3;
+    h_flag[0] = h_flag[1] = 0;
+    for (long long i = 0; i < max_graphs; ++i) {
+        CK(cudaGraphLaunch(g_many, stream));
+        CK(cudaMemcpyAsync(h_flag + (i & 1), &st->done, sizeof(int), cudaMemcpyDeviceToHost, stream));
+        CK(cudaEventRecord(ev[i & 1], stream));
+        if (i > 0) {
+            CK(cudaEventSynchronize(ev[(i - 1) & 1]));
+            if (h_flag[(i - 1) & 1]) break;
+        }
+    }
+    CK(cudaStreamSynchronize(stream));
+}
+
+void Solver::report(sparsla_solve_report* rep) {
+    DeviceGuard g(A->device);
+    CK(cudaMemcpyAsync(h_st, st, sizeof(KState), cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    const KState& S = *h_st;
+    std::memset(rep, 0, sizeof(*rep));
+    rep->iterations = S.k;
+    rep->spmv_count = S.spmv_count;
+    rep->residual_norm = S.rnorm;
+    rep->converged = S.converged;
+    rep->backend = backend;
+    const long long k = S.breakdown_iter;
+    switch (S.status) {
+        case ST_CONVERGED: case ST_RUNNING: break;
+        case ST_MAXITER: std::snprintf(rep->diagnostic, 128, "max_iter reached"); break;
+        case ST_BD_PQ: std::snprintf(rep->diagnostic, 128, "breakdown: p^T A p <= 0 at iteration %lld", k); break;
+        case ST_BD_RHO: std::snprintf(rep->diagnostic, 128, "breakdown: |rho| < 1e-30*||b||^2 at iteration %lld", k); break;
+        case ST_BD_RV: std::snprintf(rep->diagnostic, 128, "breakdown: rhat^T v = 0 at iteration %lld", k); break;
+        case ST_BD_TT: std::snprintf(rep->diagnostic, 128, "breakdown: t^T t = 0 at iteration %lld", k); break;
+        case ST_BD_OMEGA: std::snprintf(rep->diagnostic, 128, "breakdown: omega = 0 at iteration %lld", k); break;
+    }
+    if (S.status == ST_RUNNING && !S.converged) std::snprintf(rep->diagnostic, 128, "running");
+}
+
+// canonical dot of device vectors (result on host); scratch is per thread and device
+struct DotScratch {
+    int device = -1;
+    long long cap = -1;
+    double* partials = nullptr;
+    unsigned* ticket = nullptr;
+    KState* st = nullptr;
+    cudaStream_t stream = nullptr;
+    ~DotScratch() {
+        if (device < 0) return;
+        cudaSetDevice(device);
+        cudaFree(partials); cudaFree(ticket); cudaFree(st);
+        cudaStreamDestroy(stream);
+    }
+};
+
+double device_dot(int device, long long n, const double* a, const double* b, cudaStream_t s) {
+    if (n == 0) return 0.0;
+    static thread_local DotScratch S;
+    const long long m = nchunks_of(n);
+    if (S.device != device || S.cap < m) {
+        S.~DotScratch();
+        new (&S) DotScratch();
+        S.device = device;
+        S.cap = m;
+        S.partials = dalloc<double>(m);
+        S.ticket = dalloc<unsigned>(1);
+        CK(cudaMemset(S.ticket, 0, sizeof(unsigned)));
+        S.st = dalloc<KState>(1);
+        CK(cudaStreamCreateWithFlags(&S.stream, cudaStreamNonBlocking));
+    }
+    (void)s;
+    DotParams P{};
+    P.n = n; P.a = a; P.b = b;
+    P.red.partials = S.partials;
+    P.red.nchunks = m;
+    P.red.expected = (unsigned)m;
+    P.red.ticket = S.ticket;
+    P.red.st = S.st;
+    P.red.scalar = SC_STORE;
+    CK(cudaDeviceSynchronize());
+    dot_kernel<<<(unsigned)m, kVecThreads, 0, S.stream>>>(P);
+    CK(cudaGetLastError());
+    double out;
+    CK(cudaMemcpyAsync(&out, &S.st->scratch[0], sizeof(double), cudaMemcpyDeviceToHost, S.stream));
+    CK(cudaStreamSynchronize(S.stream));
+    return out;
+}
+
+}  // namespace sparsla_b200
+
+// =============================================================== C ABI (device) ======
+using namespace sparsla_b200;
+
+struct sparsla_dcsr { DevCsr* A; };
+struct sparsla_solver { Solver* S; double* x_user; int x_mem; };
+
+namespace {
+// host/device staging of a vector argument
+struct VecArg {
+    const double* dptr = nullptr;
+    double* owned = nullptr;
+    VecArg(const double* src, long long n, int mem, cudaStream_t s) {
+        if (mem == SPARSLA_MEM_DEVICE) { dptr = src; return; }
+        if (mem != SPARSLA_MEM_HOST) fail(SPARSLA_ERR_INVALID_ARGUMENT, "mem must be SPARSLA_MEM_HOST or _DEVICE");
+        owned = dalloc<double>(n + 2);
+        if (n) CK(cudaMemcpyAsync(owned, src, n * sizeof(double), cudaMemcpyHostToDevice, s));
+        dptr = owned;
+    }
+    ~VecArg() { if (owned) cudaFree(owned); }
+};
+struct OutArg {
+    double* dptr = nullptr;
+    double* user;
+    long long n;
+    int mem;
+    cudaStream_t s;
+    OutArg(double* dst, long long n_, int mem_, cudaStream_t s_) : user(dst), n(n_), mem(mem_), s(s_) {
+        if (mem == SPARSLA_MEM_DEVICE) dptr = dst;
+        else dptr = dalloc<double>(n + 2);
+    }
+    void finish() {
+        if (mem != SPARSLA_MEM_DEVICE && n) CK(cudaMemcpyAsync(user, dptr, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+    }
+    ~OutArg() { if (mem != SPARSLA_MEM_DEVICE) cudaFree(dptr); }
+};
+void need(const void* p, const char* what) {
+    if (!p) fail(SPARSLA_ERR_INVALID_ARGUMENT, std::string(what) + " is null");
+}
+
+int krylov(sparsla_dcsr* H, int backend, const double* b, double* x, const sparsla_solve_options* o,
+           sparsla_solve_report* rep, int32_t mem) {
+    return guarded([&] {
+        need(H, "matrix"); need(o, "options"); need(rep, "report");
+        DevCsr* A = H->A;
+        DeviceGuard g(A->device);
+        Solver S(A, backend, *o);
+        S.set_b(b, mem);
+        if (mem == SPARSLA_MEM_DEVICE) S.x = x;
+        S.reset();
+        S.run();
+        S.report(rep);
+        if (mem != SPARSLA_MEM_DEVICE && A->nrows)
+            CK(cudaMemcpyAsync(x, S.x, A->nrows * sizeof(double), cudaMemcpyDeviceToHost, A->stream));
+        CK(cudaStreamSynchronize(A->stream));
+    });
+}
+}  // namespace
+
+extern "C" {
+
+int sparsla_device_count(int* count) {
+    return guarded([&] {
+        int n = 0;
+        if (cudaGetDeviceCount(&n) != cudaSuccess) { cudaGetLastError(); n = 0; }
+        *count = n;
+    });
+}
+
+int sparsla_dcsr_create(int device, int64_t nrows, int64_t ncols, const int64_t* rp, const int64_t* ci,
+                        const double* v, sparsla_dcsr** out) {
+    return guarded([&] {
+        need(rp, "row_ptr"); need(out, "out");
+        *out = new sparsla_dcsr{DevCsr::create<int64_t>(device, nrows, ncols, rp, ci, v)};
+    });
+}
+
+int sparsla_dcsr_create_i32(int device, int64_t nrows, int64_t ncols, const int32_t* rp, const int32_t* ci,
+                            const double* v, sparsla_dcsr** out) {
+    return guarded([&] {
+        need(rp, "row_ptr"); need(out, "out");
+        *out = new sparsla_dcsr{DevCsr::create<int32_t>(device, nrows, ncols, rp, ci, v)};
+    });
+}
+
+int sparsla_dcsr_set_values(sparsla_dcsr* H, const double* vals, int32_t mem) {
+    return guarded([&] {
+        need(H, "matrix");
+        DevCsr* A = H->A;
+        DeviceGuard g(A->device);
+        CK(cudaMemcpyAsync(A->val, vals, A->nnz * sizeof(double),
+                           mem == SPARSLA_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, A->stream));
+        CK(cudaStreamSynchronize(A->stream));
+        // value-dependent caches are invalid now
+        if (A->dinv) { cudaFree(A->dinv); A->dinv = nullptr; }
+        A->sym_checked = -1;
+        delete A->transpose;
+        A->transpose = nullptr;
+    });
+}
+
+int sparsla_dcsr_destroy(sparsla_dcsr* H) {
+    return guarded([&] {
+        if (!H) return;
+        delete H->A;
+        delete H;
+    });
+}
+
+int sparsla_dcsr_info(const sparsla_dcsr* H, int64_t* info) {
+    return guarded([&] {
+        need(H, "matrix");
+        const DevCsr* A = H->A;
+        info[0] = A->nrows; info[1] = A->ncols; info[2] = A->nnz;
+        info[3] = (A->nrows + 1) * 4 + A->nnz * 12;
+        info[4] = A->max_block_nnz; info[5] = A->max_row; info[6] = A->staged ? 0 : 1;
+    });
+}
+
+int sparsla_spmv(sparsla_dcsr* H, const double* x, double* y, int32_t mem) {
+    return guarded([&] {
+        need(H, "matrix");
+        DevCsr* A = H->A;
+        DeviceGuard g(A->device);
+        VecArg X(x, A->ncols, mem, A->stream);
+        OutArg Y(y, A->nrows, mem, A->stream);
+        RedParams none{};
+        launch_spmv(A, A->stream, SPMV_PLAIN, X.dptr, Y.dptr, nullptr, none, 0);
+        Y.finish();
+    });
+}
+
+int sparsla_spmv_transpose(sparsla_dcsr* H, const double* x, double* y, int32_t mem) {
+    return guarded([&] {
+        need(H, "matrix");
+        DevCsr* A = H->A;
+        DeviceGuard g(A->device);
+        DevCsr* T = A->get_transpose();
+        VecArg X(x, A->nrows, mem, T->stream);
+        OutArg Y(y, A->ncols, mem, T->stream);
+        RedParams none{};
+        launch_spmv(T, T->stream, SPMV_PLAIN, X.dptr, Y.dptr, nullptr, none, 0);
+        Y.finish();
+    });
+}
+
+int sparsla_dot(int device, int64_t n, const double* a, const double* b, int32_t mem, double* out) {
+    return guarded([&] {
+        DeviceGuard g(device);
+        if (n < 0) fail(SPARSLA_ERR_DIMENSION, "negative length");
+        VecArg A(a, n, mem, nullptr), B(b, n, mem, nullptr);
+        CK(cudaDeviceSynchronize());
+        *out = device_dot(device, n, A.dptr, B.dptr, nullptr);
+    });
+}
+
+int sparsla_jacobi(sparsla_dcsr* H, double* dinv, int32_t mem) {
+    return guarded([&] {
+        need(H, "matrix");
+        DevCsr* A = H->A;
+        DeviceGuard g(A->device);
+        const double* d = A->jacobi_dinv();
+        CK(cudaMemcpyAsync(dinv, d, A->nrows * sizeof(double),
+                           mem == SPARSLA_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, A->stream));
+        CK(cudaStreamSynchronize(A->stream));
+    });
+}
+
+int sparsla_cg_solve(sparsla_dcsr* A, const double* b, double* x, const sparsla_solve_options* o,
+                     sparsla_solve_report* rep, int32_t mem) {
+    return krylov(A, SPARSLA_BACKEND_CG, b, x, o, rep, mem);
+}
+
+int sparsla_bicgstab_solve(sparsla_dcsr* A, const double* b, double* x, const sparsla_solve_options* o,
+                           sparsla_solve_report* rep, int32_t mem) {
+    return krylov(A, SPARSLA_BACKEND_BICGSTAB, b, x, o, rep, mem);
+}
+
+int sparsla_adjoint_backward(sparsla_dcsr* H, const double* x, const double* grad_x, int32_t backend,
+                             const sparsla_solve_options* o, double* grad_b, double* grad_vals,
+                             sparsla_solve_report* rep, int32_t mem) {
+    return guarded([&] {
+        need(H, "matrix"); need(o, "options"); need(rep, "report");
+        DevCsr* A = H->A;
+        if (A->nrows != A->ncols) fail(SPARSLA_ERR_DIMENSION, "adjoint requires a square matrix");
+        if (backend != SPARSLA_BACKEND_CG && backend != SPARSLA_BACKEND_BICGSTAB)
+            fail(SPARSLA_ERR_INVALID_ARGUMENT, "unknown backend");
+        DeviceGuard g(A->device);
+        const long long n = A->nrows;
+        VecArg X(x, n, mem, A->stream), G(grad_x, n, mem, A->stream);
+        OutArg GB(grad_b, n, mem, A->stream), GV(grad_vals, A->nnz, mem, A->stream);
+        // grad_x == 0 exactly -> lambda = 0 short-circuit
+        bool all_zero = true;
+        {
+            std::vector<double> hg(n);
+            if (n) CK(cudaMemcpyAsync(hg.data(), G.dptr, n * sizeof(double), cudaMemcpyDeviceToHost, A->stream));
+            CK(cudaStreamSynchronize(A->stream));
+            for (double v : hg) if (v != 0.0) { all_zero = false; break; }
+        }
+        std::memset(rep, 0, sizeof(*rep));
+        rep->backend = backend;
+        if (all_zero) {
+            if (n) CK(cudaMemsetAsync(GB.dptr, 0, n * sizeof(double), A->stream));
+            rep->converged = 1;
+            std::snprintf(rep->diagnostic, 128, "grad_x == 0: short-circuit");
+        } else {
+            // exactly one solve with A^T (A itself when it is exactly symmetric: same bits)
+            DevCsr* AT = A->exactly_symmetric() ? A : A->get_transpose();
+            Solver S(AT, backend, *o);
+            S.set_b(G.dptr, SPARSLA_MEM_DEVICE);
+            S.x = GB.dptr;
+            S.reset();
+            S.run();
+            S.report(rep);
+            CK(cudaStreamSynchronize(AT->stream));
+        }
+        if (n) adjoint_gather_kernel<<<grid_for(n, 256), 256, 0, A->stream>>>(A->rp, A->ci, n, GB.dptr, X.dptr, GV.dptr);
+        CK(cudaGetLastError());
+        GB.finish();
+        GV.finish();
+    });
+}
+
+int sparsla_solver_create(sparsla_dcsr* H, int32_t backend, const double* b, int32_t mem,
+                          const sparsla_solve_options* o, sparsla_solver** out) {
+    return guarded([&] {
+        need(H, "matrix"); need(o, "options"); need(out, "out");
+        if (backend != SPARSLA_BACKEND_CG && backend != SPARSLA_BACKEND_BICGSTAB)
+            fail(SPARSLA_ERR_INVALID_ARGUMENT, "unknown backend");
+        auto S = std::make_unique<Solver>(H->A, backend, *o);
+        S->set_b(b, mem);
+        if (mem == SPARSLA_MEM_HOST) {  // keep a resident copy: b may be freed by the caller
+            DeviceGuard g(H->A->device);
+            CK(cudaStreamSynchronize(S->stream));
+        }
+        S->reset();
+        *out = new sparsla_solver{S.release(), nullptr, 0};
+    });
+}
+
+int sparsla_solver_reset(sparsla_solver* S) { return guarded([&] { S->S->reset(); }); }
+int sparsla_solver_iterate(sparsla_solver* S, int64_t iters) { return guarded([&] { S->S->iterate(iters); }); }
+int sparsla_solver_run(sparsla_solver* S) { return guarded([&] { S->S->run(); }); }
+int sparsla_solver_report(sparsla_solver* S, sparsla_solve_report* rep) {
+    return guarded([&] { S->S->report(rep); });
+}
+int sparsla_solver_get_x(sparsla_solver* S, double* x, int32_t mem) {
+    return guarded([&] {
+        Solver* s = S->S;
+        DeviceGuard g(s->A->device);
+        CK(cudaMemcpyAsync(x, s->x, s->n * sizeof(double),
+                           mem == SPARSLA_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s->stream));
+        CK(cudaStreamSynchronize(s->stream));
+    });
+}
+int sparsla_solver_stream(sparsla_solver* S, void** stream) {
+    return guarded([&] { *stream = reinterpret_cast<void*>(S->S->stream); });
+}
+int sparsla_solver_launches_per_iteration(sparsla_solver* S, int64_t* l) {
+    return guarded([&] { *l = S->S->launches_per_iteration(); });
+}
+int sparsla_solver_destroy(sparsla_solver* S) {
+    return guarded([&] {
+        if (!S) return;
+        delete S->S;
+        delete S;
+    });
+}
+
+int sparsla_spmv_bench(sparsla_dcsr* H, int32_t reps, double* ms) {
+    return guarded([&] {
+        DevCsr* A = H->A;
+        DeviceGuard g(A->device);
+        double* xin = dalloc<double>(A->ncols + 2);
+        double* y = dalloc<double>(A->nrows + 2);
+        if (A->ncols) fill_kernel<<<grid_for(A->ncols, 256), 256, 0, A->stream>>>(xin, A->ncols, 1.0);
+        RedParams none{};
+        launch_spmv(A, A->stream, SPMV_PLAIN, xin, y, nullptr, none, 0);
+        cudaEvent_t e0, e1;
+        CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1));
+        CK(cudaEventRecord(e0, A->stream));
+        for (int i = 0; i < reps; ++i) launch_spmv(A, A->stream, SPMV_PLAIN, xin, y, nullptr, none, 0);
+        CK(cudaEventRecord(e1, A->stream));
+        CK(cudaEventSynchronize(e1));
+        float t = 0;
+        CK(cudaEventElapsedTime(&t, e0, e1));
+        *ms = t / std::max(1, reps);
+        cudaEventDestroy(e0); cudaEventDestroy(e1);
+        cudaFree(xin); cudaFree(y);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,90 @@
+// device.hpp — device-side objects of libsparsla_b200 (host declarations).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels.cuh"
+#include "sparsla_c.h"
+
+namespace sparsla_b200 {
+
+void cuda_check(cudaError_t e, const char* what);
+
+struct DeviceGuard {
+    explicit DeviceGuard(int dev);
+    ~DeviceGuard();
+    int prev_ = 0;
+};
+
+// Device CSR: int32 row_ptr / col_idx (padded for the bulk-copy over-read), fp64 values.
+struct DevCsr {
+    int device = 0;
+    long long nrows = 0, ncols = 0, nnz = 0;
+    int32_t* rp = nullptr;
+    int32_t* ci = nullptr;
+    double* val = nullptr;
+    long long max_block_nnz = 0, max_row = 0;
+    int cap_v = 0, cap_c = 0;
+    size_t smem_bytes = 0;
+    bool staged = true;
+    double* dinv = nullptr;
+    double* ones = nullptr;
+    int sym_checked = -1;
+    DevCsr* transpose = nullptr;
+    cudaStream_t stream = nullptr;
+
+    template <class I>
+    static DevCsr* create(int device, long long nrows, long long ncols, const I* rp, const I* ci,
+                          const double* val);
+    ~DevCsr();
+    const double* jacobi_dinv();
+    const double* ones_vec();
+    bool exactly_symmetric();
+    DevCsr* get_transpose();
+};
+
+void launch_spmv(DevCsr* A, cudaStream_t s, int mode, const double* x, double* y, const double* aux,
+                 const RedParams& red, int check_done);
+
+// Jacobi-PCG / BiCGStab solver with device-resident state and graph-captured iterations.
+struct Solver {
+    static constexpr int kGraphIters = 16;
+    DevCsr* A;
+    int backend;
+    sparsla_solve_options opts;
+    long long n = 0;
+    cudaStream_t stream = nullptr;
+    const double* dinv = nullptr;
+    const double* b = nullptr;
+    double* x = nullptr;
+    double *x_own = nullptr, *b_own = nullptr;
+    double *r = nullptr, *p = nullptr, *q = nullptr;
+    double *rh = nullptr, *ph = nullptr, *s = nullptr, *sh = nullptr, *t = nullptr;
+    double* partials = nullptr;
+    unsigned* tickets = nullptr;
+    KState* st = nullptr;
+    KState* h_st = nullptr;
+    int* h_flag = nullptr;
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    cudaGraphExec_t g_many = nullptr, g_one = nullptr;
+
+    Solver(DevCsr* A, int backend, const sparsla_solve_options& o);
+    ~Solver();
+    void set_b(const double* src, int mem);
+    void reset();
+    void iterate(long long iters);
+    void run();
+    void report(sparsla_solve_report* rep);
+    long long launches_per_iteration() const;
+
+   private:
+    RedParams red(int which, int slot) const;
+    VecParams vparams() const;
+    void enqueue_init();
+    void enqueue_iteration();
+    void build_graphs();
+};
+
+}  // namespace sparsla_b200

@@ -1,0 +1,736 @@
+// kernels.cuh — sm_100a kernels of the sparse Krylov hot path.
+//
+//   spmv_kernel<MODE,STAGED>   y = A x, rows accumulated left to right from 0.0 with
+//                              separate multiply/add (__dmul_rn/__dadd_rn): bitwise equal to
+//                              the reference spmv (sparse.cpp:144-152).  STAGED: the CTA's
+//                              256-row round segments of row_ptr/col_idx/vals are streamed
+//                              into shared memory by the TMA bulk-copy engine
+//                              (cp.async.bulk + mbarrier, L2 evict_first), 4-stage ring;
+//                              x is gathered through the read-only path.  The epilogue fuses
+//                              the dot products the solver needs next (p.q for CG; rhat.v,
+//                              and t.t, t.s, s.s for BiCGStab).
+//   cg_* / bi_*                fused Jacobi-PCG / BiCGStab vector updates: every axpy of an
+//                              iteration step plus its dot products in one HBM pass.
+//   canonical reductions       every dot uses the fixed shape of DESIGN.md §3.2 (chunks of
+//                              2048 = 256 slots x 8 rounds, slot-pair binary tree, then a
+//                              1024-slot final stage done by the last CTA to finish), so
+//                              results are bitwise identical to the oracle and independent of
+//                              launch geometry.  Scalars (alpha, beta, omega, convergence)
+//                              are computed on the device by that last CTA: no host sync
+//                              inside the loop.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace sparsla_b200 {
+
+constexpr int kChunkSlots = 256;
+constexpr int kChunkRounds = 8;
+constexpr int64_t kChunk = kChunkSlots * kChunkRounds;  // 2048 rows / elements per chunk
+constexpr int kFinalSlots = 1024;
+constexpr int kSpmvThreads = 256;
+constexpr int kVecThreads = 128;
+constexpr int kStages = 4;
+constexpr int kRpCopy = 260;  // row_ptr entries staged per round (257 needed, 16B multiple)
+
+// ---------------------------------------------------------------- solver state -------
+enum Status : int {
+    ST_RUNNING = 0, ST_CONVERGED = 1, ST_MAXITER = 2, ST_BD_PQ = 3, ST_BD_RHO = 4,
+    ST_BD_RV = 5, ST_BD_TT = 6, ST_BD_OMEGA = 7
+};
+
+struct KState {
+    double atol, rtol;
+    long long max_iter;
+    double tol, bnorm, rnorm, rz, alpha, beta, omega, rho, rho_prev, rho_thr, ss;
+    long long k, spmv_count, breakdown_iter;
+    int done, converged, status, halfstep;
+    double scratch[8];  // plain dot outputs
+};
+
+enum Scalar : int {
+    SC_NONE = 0, SC_STORE = 1, SC_CG_INIT = 2, SC_CG_PQ = 3, SC_CG_RR = 4,
+    SC_BI_INIT = 5, SC_BI_RV = 6, SC_BI_T = 7, SC_BI_U3 = 8
+};
+
+__device__ __forceinline__ double dmax_ref(double a, double b) { return a < b ? b : a; }
+
+// Scalar bookkeeping after a reduction point (the same decisions, in the same order, as
+// the oracle's cg_core / bicgstab_core loops).
+__device__ inline void apply_scalar(int which, KState* st, const double* t) {
+    switch (which) {
+        case SC_STORE:
+            for (int j = 0; j < 3; ++j) st->scratch[j] = t[j];
+            break;
+        case SC_CG_INIT: {
+            st->rz = t[0];
+            const double rr = t[1];
+            st->bnorm = sqrt(t[2]);
+            st->tol = dmax_ref(st->atol, __dmul_rn(st->rtol, st->bnorm));
+            st->rnorm = sqrt(rr);
+            st->k = 0;
+            if (st->rnorm <= st->tol) { st->converged = 1; st->status = ST_CONVERGED; st->done = 1; }
+            break;
+        }
+        case SC_CG_PQ: {
+            st->spmv_count += 1;
+            const double pq = t[0];
+            if (!(pq > 0.0)) { st->status = ST_BD_PQ; st->breakdown_iter = st->k; st->done = 1; }
+            else st->alpha = st->rz / pq;
+            break;
+        }
+        case SC_CG_RR: {
+            const double rz_new = t[0], rr = t[1];
+            st->k += 1;
+            st->rnorm = sqrt(rr);
+            if (st->rnorm <= st->tol) { st->converged = 1; st->status = ST_CONVERGED; st->done = 1; }
+            else if (st->k >= st->max_iter) { st->status = ST_MAXITER; st->done = 1; }
+            else { st->beta = rz_new / st->rz; st->rz = rz_new; }
+            break;
+        }
+        case SC_BI_INIT: {
+            st->rho = t[0];
+            const double rr = t[1];
+            st->bnorm = sqrt(t[2]);
+            st->tol = dmax_ref(st->atol, __dmul_rn(st->rtol, st->bnorm));
+            st->rho_thr = __dmul_rn(1e-30, __dmul_rn(st->bnorm, st->bnorm));
+            st->rnorm = sqrt(rr);
+            st->k = 0;
+            st->rho_prev = 1.0; st->alpha = 1.0; st->omega = 1.0;
+            if (st->rnorm <= st->tol) { st->converged = 1; st->status = ST_CONVERGED; st->done = 1; }
+            else if (!(fabs(st->rho) >= st->rho_thr) || !isfinite(st->rho)) {
+                st->status = ST_BD_RHO; st->breakdown_iter = 0; st->done = 1;
+            }
+            break;
+        }
+        case SC_BI_RV: {
+            st->spmv_count += 1;
+            const double rv = t[0];
+            if (!(rv != 0.0) || !isfinite(rv)) { st->status = ST_BD_RV; st->breakdown_iter = st->k; st->done = 1; }
+            else st->alpha = st->rho / rv;
+            break;
+        }
+        case SC_BI_T: {
+            st->spmv_count += 1;
+            const double tt = t[0], ts = t[1], ss = t[2];
+            st->ss = ss;
+            if (sqrt(ss) <= st->tol) st->halfstep = 1;
+            else if (!(tt > 0.0)) { st->status = ST_BD_TT; st->breakdown_iter = st->k; st->done = 1; }
+            else st->omega = ts / tt;
+            break;
+        }
+        case SC_BI_U3: {
+            if (st->halfstep) {
+                st->k += 1;
+                st->rnorm = sqrt(st->ss);
+                st->converged = 1; st->status = ST_CONVERGED; st->done = 1;
+                break;
+            }
+            st->rho_prev = st->rho;
+            st->rho = t[0];
+            const double rr = t[1];
+            st->k += 1;
+            st->rnorm = sqrt(rr);
+            if (st->rnorm <= st->tol) { st->converged = 1; st->status = ST_CONVERGED; st->done = 1; }
+            else if (st->omega == 0.0) { st->status = ST_BD_OMEGA; st->breakdown_iter = st->k; st->done = 1; }
+            else if (st->k >= st->max_iter) { st->status = ST_MAXITER; st->done = 1; }
+            else if (!(fabs(st->rho) >= st->rho_thr) || !isfinite(st->rho)) {
+                st->status = ST_BD_RHO; st->breakdown_iter = st->k; st->done = 1;
+            } else {
+                st->beta = __dmul_rn(st->rho / st->rho_prev, st->alpha / st->omega);
+            }
+            break;
+        }
+        default: break;
+    }
+}
+
+// ------------------------------------------------------ canonical reduction helpers --
+// Binary tree over NW values in smem, left + right (matches the oracle's tree_reduce).
+template <int NW>
+__device__ __forceinline__ double tree_smem(volatile double* a) {
+#pragma unroll
+    for (int w = 1; w < NW; w *= 2)
+#pragma unroll
+        for (int i = 0; i + w < NW; i += 2 * w) a[i] = __dadd_rn(a[i], a[i + w]);
+    return a[0];
+}
+
+// Slot-group value per thread (thread t holds the group sum of slots [t*G, (t+1)*G)) ->
+// chunk partial on thread 0.  xor-butterfly levels 1..16 realise the pairwise tree over
+// consecutive groups (IEEE addition is commutative, so both lanes get the same bits).
+template <int NT, int NDOT>
+__device__ __forceinline__ void block_tree(double (&v)[NDOT], double* sred) {
+    constexpr int NW = NT / 32;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int d = 0; d < NDOT; ++d) {
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) v[d] = __dadd_rn(v[d], __shfl_xor_sync(0xffffffffu, v[d], off));
+        if (lane == 0) sred[d * NW + w] = v[d];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int d = 0; d < NDOT; ++d) v[d] = tree_smem<NW>(sred + d * NW);
+    }
+}
+
+// Level-2 reduction over m chunk partials per dot (layout [NDOT][m]); called by every
+// thread of the last CTA; result valid on thread 0.
+template <int NT, int NDOT>
+__device__ void final_reduce(const double* partials, long long m, double (&out)[NDOT], double* sred) {
+    constexpr int SPT = kFinalSlots / NT;  // consecutive slots per thread
+    const int t = threadIdx.x;
+#pragma unroll
+    for (int d = 0; d < NDOT; ++d) {
+        const double* P = partials + d * m;
+        double s[SPT];
+#pragma unroll
+        for (int j = 0; j < SPT; ++j) {
+            const long long slot = (long long)t * SPT + j;
+            double acc = 0.0;
+            long long c = slot;
+            for (; c + 3 * kFinalSlots < m; c += 4 * kFinalSlots) {
+                const double a0 = __ldcg(P + c), a1 = __ldcg(P + c + kFinalSlots);
+                const double a2 = __ldcg(P + c + 2 * kFinalSlots), a3 = __ldcg(P + c + 3 * kFinalSlots);
+                acc = __dadd_rn(acc, a0); acc = __dadd_rn(acc, a1);
+                acc = __dadd_rn(acc, a2); acc = __dadd_rn(acc, a3);
+            }
+            for (; c < m; c += kFinalSlots) acc = __dadd_rn(acc, __ldcg(P + c));
+            s[j] = acc;
+        }
+#pragma unroll
+        for (int w = 1; w < SPT; w *= 2)
+#pragma unroll
+            for (int i = 0; i + w < SPT; i += 2 * w) s[i] = __dadd_rn(s[i], s[i + w]);
+        out[d] = s[0];
+    }
+    block_tree<NT, NDOT>(out, sred);
+}
+
+// Publish this CTA's chunk partials; the last CTA (ticket) finishes the reduction and runs
+// the scalar step (or, distributed, writes the rank's totals for the all-gather).
+struct RedParams {
+    double* partials;     // [NDOT][nchunks]
+    long long nchunks;
+    unsigned* ticket;     // reset to 0 by the last CTA
+    unsigned expected;    // number of CTAs contributing (all launches of this point)
+    KState* st;
+    double* red_out;      // distributed: rank totals -> all-gather; else nullptr
+    int scalar;           // Scalar op applied by the last CTA (single rank)
+};
+
+template <int NT, int NDOT>
+__device__ void publish_and_finish(double (&part)[NDOT], long long chunk, const RedParams& R,
+                                   double* sred) {
+    __shared__ int s_last;
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int d = 0; d < NDOT; ++d) R.partials[d * R.nchunks + chunk] = part[d];
+        __threadfence();
+        const unsigned prev = atomicAdd(R.ticket, 1u);
+        s_last = (prev == R.expected - 1);
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    double tot[NDOT];
+    final_reduce<NT, NDOT>(R.partials, R.nchunks, tot, sred);
+    if (threadIdx.x == 0) {
+        if (R.red_out) {
+#pragma unroll
+            for (int d = 0; d < NDOT; ++d) R.red_out[d] = tot[d];
+        } else {
+            double t3[4] = {0, 0, 0, 0};
+#pragma unroll
+            for (int d = 0; d < NDOT; ++d) t3[d] = tot[d];
+            apply_scalar(R.scalar, R.st, t3);
+        }
+        *R.ticket = 0u;
+        __threadfence();
+    }
+}
+
+// ------------------------------------------------------------------ PTX helpers ------
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(ok)
+            : "r"(smem_addr(bar)), "r"(parity)
+            : "memory");
+    } while (!ok);
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+// TMA bulk copy global -> shared (non-tensor), completion on the mbarrier.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1], %2, [%3], %4;" ::"r"(smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(policy)
+        : "memory");
+}
+
+// ------------------------------------------------------------------------ SpMV -------
+enum SpmvMode : int { SPMV_PLAIN = 0, SPMV_CG = 1, SPMV_BICG_V = 2, SPMV_BICG_T = 3 };
+template <int MODE> struct SpmvDots { static constexpr int n = 0; };
+template <> struct SpmvDots<SPMV_CG> { static constexpr int n = 1; };
+template <> struct SpmvDots<SPMV_BICG_V> { static constexpr int n = 1; };
+template <> struct SpmvDots<SPMV_BICG_T> { static constexpr int n = 3; };
+
+struct SpmvParams {
+    const int32_t* rp;
+    const int32_t* ci;
+    const double* val;
+    const double* x;    // gathered input ([owned | halo] when distributed)
+    double* y;
+    long long n;        // rows
+    long long chunk0;   // first chunk index handled by this launch (interior/boundary split)
+    const double* aux;  // BICG_V: rhat, BICG_T: s
+    int cap_v, cap_c;   // staged capacities (elements) per round
+    int check_done;
+    RedParams red;
+};
+
+template <int MODE>
+__device__ __forceinline__ void spmv_epilogue(const SpmvParams& P, long long row, double y,
+                                              double (&acc)[SpmvDots<MODE>::n > 0 ? SpmvDots<MODE>::n : 1]) {
+    if constexpr (MODE == SPMV_CG) {
+        acc[0] = __dadd_rn(acc[0], __dmul_rn(__ldg(P.x + row), y));
+    } else if constexpr (MODE == SPMV_BICG_V) {
+        acc[0] = __dadd_rn(acc[0], __dmul_rn(__ldg(P.aux + row), y));
+    } else if constexpr (MODE == SPMV_BICG_T) {
+        const double s = __ldg(P.aux + row);
+        acc[0] = __dadd_rn(acc[0], __dmul_rn(y, y));
+        acc[1] = __dadd_rn(acc[1], __dmul_rn(y, s));
+        acc[2] = __dadd_rn(acc[2], __dmul_rn(s, s));
+    }
+}
+
+// Row-sequential accumulation over entries [kb, ke) read through accessor `ld(k, c, v)`.
+template <class LD>
+__device__ __forceinline__ double row_sum(int kb, int ke, const double* __restrict__ x, LD ld) {
+    double sum = 0.0;
+    for (int k = kb; k < ke; k += 8) {
+        double pr[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            if (k + u < ke) {
+                int c;
+                double v;
+                ld(k + u, c, v);
+                pr[u] = __dmul_rn(v, __ldg(x + c));
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (k + u < ke) sum = __dadd_rn(sum, pr[u]);
+    }
+    return sum;
+}
+
+// One CTA = one chunk of 2048 rows = 8 rounds of 256 rows; thread t owns row (round*256+t).
+template <int MODE, bool STAGED>
+__global__ void __launch_bounds__(kSpmvThreads, 2) spmv_kernel(SpmvParams P) {
+    constexpr int ND = SpmvDots<MODE>::n;
+    constexpr int NA = ND > 0 ? ND : 1;
+    if (P.check_done && P.red.st->done) return;
+    const int t = threadIdx.x;
+    const long long chunk = P.chunk0 + blockIdx.x;
+    const long long base = chunk * kChunk;
+    const long long rem_rounds = (P.n - base + kChunkSlots - 1) / kChunkSlots;
+    const int nrounds = rem_rounds < kChunkRounds ? (int)rem_rounds : kChunkRounds;
+    double acc[NA];
+#pragma unroll
+    for (int d = 0; d < NA; ++d) acc[d] = 0.0;
+
+    if constexpr (STAGED) {
+        extern __shared__ __align__(128) unsigned char smem[];
+        uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
+        const size_t vbytes = ((size_t)P.cap_v * 8 + 127) & ~size_t(127);
+        const size_t cbytes = ((size_t)P.cap_c * 4 + 127) & ~size_t(127);
+        const size_t rbytes = (kRpCopy * 4 + 127) & ~size_t(127);
+        const size_t stage_bytes = vbytes + cbytes + rbytes;
+        unsigned char* stage0 = smem + 128;
+        auto sv = [&](int s) { return reinterpret_cast<double*>(stage0 + s * stage_bytes); };
+        auto sc = [&](int s) { return reinterpret_cast<int32_t*>(stage0 + s * stage_bytes + vbytes); };
+        auto sr = [&](int s) { return reinterpret_cast<int32_t*>(stage0 + s * stage_bytes + vbytes + cbytes); };
+        if (t == 0) {
+            for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+            fence_mbar_init();
+        }
+        __syncthreads();
+        const uint64_t pol = policy_evict_first();
+        auto issue = [&](int r) {
+            const int s = r % kStages;
+            const long long rs = base + (long long)r * kChunkSlots;
+            const long long re = min(rs + kChunkSlots, P.n);
+            const int nz0 = __ldg(P.rp + rs), nz1 = __ldg(P.rp + re);
+            const int a0 = nz0 & ~1, a1 = (nz1 + 1) & ~1;
+            const int c0 = nz0 & ~3, c1 = (nz1 + 3) & ~3;
+            const uint32_t vb = (uint32_t)(a1 - a0) * 8u, cb = (uint32_t)(c1 - c0) * 4u;
+            mbar_arrive_expect_tx(&bars[s], (uint32_t)(kRpCopy * 4) + vb + cb);
+            bulk_g2s(sr(s), P.rp + rs, kRpCopy * 4, &bars[s], pol);
+            if (vb) bulk_g2s(sv(s), P.val + a0, vb, &bars[s], pol);
+            if (cb) bulk_g2s(sc(s), P.ci + c0, cb, &bars[s], pol);
+        };
+        if (t == 0)
+            for (int r = 0; r < kStages && r < nrounds; ++r) issue(r);
+        for (int r = 0; r < nrounds; ++r) {
+            const int s = r % kStages;
+            mbar_wait(&bars[s], (uint32_t)((r / kStages) & 1));
+            const long long row = base + (long long)r * kChunkSlots + t;
+            if (row < P.n) {
+                const int32_t* rps = sr(s);
+                const int nz0 = rps[0];
+                const int a0 = nz0 & ~1, c0 = nz0 & ~3;
+                const double* vs = sv(s);
+                const int32_t* cs = sc(s);
+                const double y = row_sum(rps[t], rps[t + 1], P.x, [&](int k, int& c, double& v) {
+                    c = cs[k - c0];
+                    v = vs[k - a0];
+                });
+                P.y[row] = y;
+                spmv_epilogue<MODE>(P, row, y, acc);
+            }
+            __syncthreads();  // stage s fully consumed
+            if (t == 0 && r + kStages < nrounds) {
+                fence_proxy_async_smem();
+                issue(r + kStages);
+            }
+        }
+    } else {
+        for (int r = 0; r < nrounds; ++r) {
+            const long long row = base + (long long)r * kChunkSlots + t;
+            if (row < P.n) {
+                const double y = row_sum(__ldg(P.rp + row), __ldg(P.rp + row + 1), P.x,
+                                         [&](int k, int& c, double& v) {
+                                             c = __ldg(P.ci + k);
+                                             v = __ldg(P.val + k);
+                                         });
+                P.y[row] = y;
+                spmv_epilogue<MODE>(P, row, y, acc);
+            }
+        }
+    }
+    if constexpr (ND > 0) {
+        __shared__ double sred[ND * (kSpmvThreads / 32)];
+        block_tree<kSpmvThreads, ND>(acc, sred);
+        publish_and_finish<kSpmvThreads, ND>(acc, chunk, P.red, sred);
+    }
+}
+
+// -------------------------------------------------------------- vector kernels -------
+// Thread t of a 128-thread CTA owns slots 2t and 2t+1 of each 256-element round (one
+// double2), rounds 0..7 of the CTA's 2048-element chunk.  Inputs of 4 rounds are loaded
+// before any arithmetic (ILP); all operations are separate IEEE mul/add/sub in the
+// oracle's order (no FMA).
+struct VecParams {
+    long long n;
+    const double* d;  // Jacobi inverse diagonal
+    double *x, *r, *p, *q;
+    double *rh, *ph, *v, *s, *sh, *tt;
+    const double* b;
+    int check_done;
+    RedParams red;
+};
+
+__device__ __forceinline__ double2 ld2(const double* p, long long i, long long n) {
+    if (i + 1 < n) return *reinterpret_cast<const double2*>(p + i);
+    double2 z;
+    z.x = i < n ? p[i] : 0.0;
+    z.y = 0.0;
+    return z;
+}
+__device__ __forceinline__ void st2(double* p, long long i, long long n, double2 v) {
+    if (i + 1 < n) *reinterpret_cast<double2*>(p + i) = v;
+    else if (i < n) p[i] = v.x;
+}
+__device__ __forceinline__ double lane(const double2& v, int e) { return e ? v.y : v.x; }
+__device__ __forceinline__ void set_lane(double2& v, int e, double x) { if (e) v.y = x; else v.x = x; }
+
+enum VecOp : int { V_CG_INIT, V_CG_U1, V_CG_U2, V_BI_INIT, V_BI_U1, V_BI_U2, V_BI_U3 };
+template <int OP> struct VecTraits;
+template <> struct VecTraits<V_CG_INIT> { static constexpr int nin = 3, ndot = 3; };  // b q d
+template <> struct VecTraits<V_CG_U1>   { static constexpr int nin = 5, ndot = 2; };  // x p r q d
+template <> struct VecTraits<V_CG_U2>   { static constexpr int nin = 3, ndot = 0; };  // d r p
+template <> struct VecTraits<V_BI_INIT> { static constexpr int nin = 2, ndot = 3; };  // b v
+template <> struct VecTraits<V_BI_U1>   { static constexpr int nin = 4, ndot = 0; };  // r p v d
+template <> struct VecTraits<V_BI_U2>   { static constexpr int nin = 3, ndot = 0; };  // r v d
+template <> struct VecTraits<V_BI_U3>   { static constexpr int nin = 6, ndot = 2; };  // x ph s sh t rh
+
+struct VecScalars {
+    double alpha, beta, omega;
+    int first, half;
+};
+
+template <int OP>
+__device__ __forceinline__ void vec_load(const VecParams& P, long long i, double2 (&in)[VecTraits<OP>::nin]) {
+    const long long n = P.n;
+    if constexpr (OP == V_CG_INIT) { in[0] = ld2(P.b, i, n); in[1] = ld2(P.q, i, n); in[2] = ld2(P.d, i, n); }
+    if constexpr (OP == V_CG_U1) {
+        in[0] = ld2(P.x, i, n); in[1] = ld2(P.p, i, n); in[2] = ld2(P.r, i, n);
+        in[3] = ld2(P.q, i, n); in[4] = ld2(P.d, i, n);
+    }
+    if constexpr (OP == V_CG_U2) { in[0] = ld2(P.d, i, n); in[1] = ld2(P.r, i, n); in[2] = ld2(P.p, i, n); }
+    if constexpr (OP == V_BI_INIT) { in[0] = ld2(P.b, i, n); in[1] = ld2(P.v, i, n); }
+    if constexpr (OP == V_BI_U1) {
+        in[0] = ld2(P.r, i, n); in[1] = ld2(P.p, i, n); in[2] = ld2(P.v, i, n); in[3] = ld2(P.d, i, n);
+    }
+    if constexpr (OP == V_BI_U2) { in[0] = ld2(P.r, i, n); in[1] = ld2(P.v, i, n); in[2] = ld2(P.d, i, n); }
+    if constexpr (OP == V_BI_U3) {
+        in[0] = ld2(P.x, i, n); in[1] = ld2(P.ph, i, n); in[2] = ld2(P.s, i, n);
+        in[3] = ld2(P.sh, i, n); in[4] = ld2(P.tt, i, n); in[5] = ld2(P.rh, i, n);
+    }
+}
+
+// Computes both lanes of the pair at i, stores outputs, returns per-lane dot products.
+template <int OP>
+__device__ __forceinline__ void vec_compute(const VecParams& P, const VecScalars& S, long long i,
+                                            const double2 (&in)[VecTraits<OP>::nin],
+                                            double (&pr)[VecTraits<OP>::ndot > 0 ? VecTraits<OP>::ndot : 1][2]) {
+    const long long n = P.n;
+    double2 o0 = make_double2(0.0, 0.0), o1 = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+        if constexpr (OP == V_CG_INIT) {  // r = b - q; z = d r; p = z; {r.z, r.r, b.b}
+            const double b = lane(in[0], e);
+            const double r = __dsub_rn(b, lane(in[1], e));
+            const double z = __dmul_rn(lane(in[2], e), r);
+            set_lane(o0, e, r); set_lane(o1, e, z);
+            pr[0][e] = __dmul_rn(r, z); pr[1][e] = __dmul_rn(r, r); pr[2][e] = __dmul_rn(b, b);
+        }
+        if constexpr (OP == V_CG_U1) {  // x += a p; r -= a q; z = d r; {r.z, r.r}
+            const double xn = __dadd_rn(lane(in[0], e), __dmul_rn(S.alpha, lane(in[1], e)));
+            const double rn = __dsub_rn(lane(in[2], e), __dmul_rn(S.alpha, lane(in[3], e)));
+            const double z = __dmul_rn(lane(in[4], e), rn);
+            set_lane(o0, e, xn); set_lane(o1, e, rn);
+            pr[0][e] = __dmul_rn(rn, z); pr[1][e] = __dmul_rn(rn, rn);
+        }
+        if constexpr (OP == V_CG_U2) {  // p = z + beta p, z = d r
+            const double z = __dmul_rn(lane(in[0], e), lane(in[1], e));
+            set_lane(o0, e, __dadd_rn(z, __dmul_rn(S.beta, lane(in[2], e))));
+        }
+        if constexpr (OP == V_BI_INIT) {  // r = b - v; rhat = r; {rh.r, r.r, b.b}
+            const double b = lane(in[0], e);
+            const double r = __dsub_rn(b, lane(in[1], e));
+            set_lane(o0, e, r);
+            pr[0][e] = __dmul_rn(r, r); pr[1][e] = __dmul_rn(r, r); pr[2][e] = __dmul_rn(b, b);
+        }
+        if constexpr (OP == V_BI_U1) {  // p = r + beta (p - omega v)  (p = r at k = 0); ph = d p
+            const double r = lane(in[0], e);
+            const double p = S.first ? r
+                : __dadd_rn(r, __dmul_rn(S.beta, __dsub_rn(lane(in[1], e), __dmul_rn(S.omega, lane(in[2], e)))));
+            set_lane(o0, e, p); set_lane(o1, e, __dmul_rn(lane(in[3], e), p));
+        }
+        if constexpr (OP == V_BI_U2) {  // s = r - alpha v; sh = d s
+            const double s = __dsub_rn(lane(in[0], e), __dmul_rn(S.alpha, lane(in[1], e)));
+            set_lane(o0, e, s); set_lane(o1, e, __dmul_rn(lane(in[2], e), s));
+        }
+        if constexpr (OP == V_BI_U3) {
+            if (S.half) {  // x += alpha ph; r = s
+                set_lane(o0, e, __dadd_rn(lane(in[0], e), __dmul_rn(S.alpha, lane(in[1], e))));
+                set_lane(o1, e, lane(in[2], e));
+                pr[0][e] = 0.0; pr[1][e] = 0.0;
+            } else {       // x = (x + alpha ph) + omega sh; r = s - omega t; {rh.r, r.r}
+                const double xn = __dadd_rn(__dadd_rn(lane(in[0], e), __dmul_rn(S.alpha, lane(in[1], e))),
+                                            __dmul_rn(S.omega, lane(in[3], e)));
+                const double rn = __dsub_rn(lane(in[2], e), __dmul_rn(S.omega, lane(in[4], e)));
+                set_lane(o0, e, xn); set_lane(o1, e, rn);
+                pr[0][e] = __dmul_rn(lane(in[5], e), rn); pr[1][e] = __dmul_rn(rn, rn);
+            }
+        }
+    }
+    if constexpr (OP == V_CG_INIT) { st2(P.r, i, n, o0); st2(P.p, i, n, o1); }
+    if constexpr (OP == V_CG_U1) { st2(P.x, i, n, o0); st2(P.r, i, n, o1); }
+    if constexpr (OP == V_CG_U2) { st2(P.p, i, n, o0); }
+    if constexpr (OP == V_BI_INIT) { st2(P.r, i, n, o0); st2(P.rh, i, n, o0); }
+    if constexpr (OP == V_BI_U1) { st2(P.p, i, n, o0); st2(P.ph, i, n, o1); }
+    if constexpr (OP == V_BI_U2) { st2(P.s, i, n, o0); st2(P.sh, i, n, o1); }
+    if constexpr (OP == V_BI_U3) { st2(P.x, i, n, o0); st2(P.r, i, n, o1); }
+}
+
+template <int OP>
+__global__ void __launch_bounds__(kVecThreads) vec_kernel(VecParams P) {
+    constexpr int NIN = VecTraits<OP>::nin;
+    constexpr int ND = VecTraits<OP>::ndot;
+    constexpr int NA = ND > 0 ? ND : 1;
+    const KState* st = P.red.st;
+    if (P.check_done && st->done) return;
+    VecScalars S;
+    if constexpr (OP == V_CG_U1 || OP == V_BI_U2) S.alpha = st->alpha;
+    if constexpr (OP == V_CG_U2) S.beta = st->beta;
+    if constexpr (OP == V_BI_U1) { S.beta = st->beta; S.omega = st->omega; S.first = st->k == 0; }
+    if constexpr (OP == V_BI_U3) { S.alpha = st->alpha; S.omega = st->omega; S.half = st->halfstep; }
+    const int t = threadIdx.x;
+    const long long chunk = blockIdx.x;
+    const long long base = chunk * kChunk;
+    double acc[NA][2];
+#pragma unroll
+    for (int d = 0; d < NA; ++d) acc[d][0] = acc[d][1] = 0.0;
+#pragma unroll
+    for (int g = 0; g < kChunkRounds; g += 4) {
+        double2 in[4][NIN];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) vec_load<OP>(P, base + (long long)(g + u) * kChunkSlots + 2 * t, in[u]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const long long i = base + (long long)(g + u) * kChunkSlots + 2 * t;
+            if (i >= P.n) continue;
+            double pr[NA][2];
+            vec_compute<OP>(P, S, i, in[u], pr);
+            if constexpr (ND > 0) {
+#pragma unroll
+                for (int d = 0; d < ND; ++d) {
+                    acc[d][0] = __dadd_rn(acc[d][0], pr[d][0]);
+                    if (i + 1 < P.n) acc[d][1] = __dadd_rn(acc[d][1], pr[d][1]);
+                }
+            }
+        }
+    }
+    if constexpr (ND > 0) {
+        __shared__ double sred[ND * (kVecThreads / 32)];
+        double v[ND];
+#pragma unroll
+        for (int d = 0; d < ND; ++d) v[d] = __dadd_rn(acc[d][0], acc[d][1]);  // slot pair
+        block_tree<kVecThreads, ND>(v, sred);
+        publish_and_finish<kVecThreads, ND>(v, chunk, P.red, sred);
+    }
+}
+
+// Generic canonical dot a.b (level 1 + last-CTA level 2), same chunk shape.
+struct DotParams {
+    long long n;
+    const double* a;
+    const double* b;
+    RedParams red;
+};
+__global__ void __launch_bounds__(kVecThreads) dot_kernel(DotParams P) {
+    const int t = threadIdx.x;
+    const long long chunk = blockIdx.x;
+    const long long base = chunk * kChunk;
+    double acc[2] = {0.0, 0.0};
+#pragma unroll
+    for (int rd = 0; rd < kChunkRounds; ++rd) {
+        const long long i = base + (long long)rd * kChunkSlots + 2 * t;
+        const double2 A = ld2(P.a, i, P.n), B = ld2(P.b, i, P.n);
+        if (i < P.n) acc[0] = __dadd_rn(acc[0], __dmul_rn(A.x, B.x));
+        if (i + 1 < P.n) acc[1] = __dadd_rn(acc[1], __dmul_rn(A.y, B.y));
+    }
+    __shared__ double sred[kVecThreads / 32];
+    double v[1] = {__dadd_rn(acc[0], acc[1])};
+    block_tree<kVecThreads, 1>(v, sred);
+    publish_and_finish<kVecThreads, 1>(v, chunk, P.red, sred);
+}
+
+// Distributed reduction points: rank totals were all-gathered into g[P][k]; sum in
+// ascending rank order starting from rank 0 and run the scalar step.
+__global__ void scalar_kernel(const double* g, int nranks, int k, int which, KState* st) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (st->done && which != SC_BI_U3) return;
+    if (st->done && which == SC_BI_U3 && !st->halfstep) return;
+    double t[4] = {0, 0, 0, 0};
+    for (int j = 0; j < k; ++j) {
+        double s = g[j];
+        for (int q = 1; q < nranks; ++q) s = __dadd_rn(s, g[q * 8 + j]);
+        t[j] = s;
+    }
+    apply_scalar(which, st, t);
+}
+
+// Jacobi inverse diagonal: 1/A_ii, or 1.0 when missing / zero / non-finite.
+__global__ void jacobi_kernel(const int32_t* rp, const int32_t* ci, const double* val, long long n,
+                              long long col_offset, double* dinv) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const long long g = i + col_offset;  // local column id of the diagonal
+    int lo = rp[i], hi = rp[i + 1];
+    double r = 1.0;
+    for (int k = lo; k < hi; ++k) {
+        if (ci[k] == g) {
+            const double a = val[k];
+            if (a != 0.0) {
+                const double inv = 1.0 / a;
+                if (isfinite(inv)) r = inv;
+            }
+            break;
+        }
+    }
+    dinv[i] = r;
+}
+
+// Exact value symmetry (A^T == A bitwise) for adjoint operator reuse.
+__global__ void symmetry_kernel(const int32_t* rp, const int32_t* ci, const double* val, long long n,
+                                int* flags) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    for (int k = rp[i]; k < rp[i + 1]; ++k) {
+        const int j = ci[k];
+        int lo = rp[j], hi = rp[j + 1];
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (ci[mid] < i) lo = mid + 1; else hi = mid;
+        }
+        if (lo == rp[j + 1] || ci[lo] != i) { flags[0] = 0; flags[1] = 0; return; }
+        if (val[lo] != val[k]) flags[1] = 0;
+    }
+}
+
+// Adjoint gradient gather (Eq. 3): grad_vals[k] = -(lam[row_k] * x[col_k]),
+// in CSR (= canonical COO) order; one thread per row.
+__global__ void adjoint_gather_kernel(const int32_t* rp, const int32_t* ci, long long n,
+                                      const double* lam, const double* x, double* gv) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double l = lam[i];
+    const int k1 = rp[i + 1];
+    for (int k = rp[i]; k < k1; ++k) gv[k] = -__dmul_rn(l, __ldg(x + ci[k]));
+}
+
+__global__ void fill_kernel(double* p, long long n, double v) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+
+__global__ void i64_to_i32_kernel(const long long* in, int32_t* out, long long n) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = (int32_t)in[i];
+}
+
+// Halo pack: sendbuf[j] = x[idx[j]] (canonical global order).
+__global__ void halo_pack_kernel(const double* x, const int32_t* idx, long long m, double* out) {
+    const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < m) out[j] = x[idx[j]];
+}
+// Halo unpack: x[idx[j]] = recvbuf[j].
+__global__ void halo_unpack_kernel(double* x, const int32_t* idx, long long m, const double* in) {
+    const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < m) x[idx[j]] = in[j];
+}
+
+}  // namespace sparsla_b200

@@ -1,0 +1,642 @@
+"""sparsla — Python mirror of the reference's proj/core API over libsparsla_b200.so (C ABI).
+
+Names, argument meaning and error behaviour follow the reference C++ API
+(/root/reference/proj/core/include/sparsla/sparse.hpp:18-149, errors.hpp:9-62) and the
+SPEC.md contracts of the missing solve / adjoint / distributed sources:
+
+    SparseCoo, CsrMatrix, Shape, spmv, spmv_transpose, transpose,
+    is_structurally_symmetric, is_symmetric                        (sparse.hpp)
+    SolveOptions, SolveReport, JacobiPreconditioner, jacobi_build,
+    cg_solve, bicgstab_solve
+    AdjointContext, GradientBundle, solve_forward, solve_backward
+    partition_contiguous, partition_rcb, build_local
+    poisson2d / poisson3d / convdiff3d / fem2d generators
+
+Every compute call runs the sm_100a kernels; there is no CPU fallback — without a CUDA
+device the device entry points raise sparsla.Error (SPARSLA_ERR_NO_DEVICE).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsparsla_b200.so")
+
+# ----------------------------------------------------------------------------- errors --
+class Error(RuntimeError):
+    """sparsla::Error (errors.hpp:9-12)."""
+
+
+class DimensionError(Error):
+    pass
+
+
+class BoundsError(Error):
+    pass
+
+
+class FormatError(Error):
+    pass
+
+
+class SingularMatrixError(Error):
+    pass
+
+
+class UnsupportedInputError(Error):
+    pass
+
+
+class InvalidArgumentError(Error):
+    pass
+
+
+class TransportError(Error):
+    pass
+
+
+_ERR = {1: DimensionError, 2: BoundsError, 3: FormatError, 4: SingularMatrixError,
+        5: UnsupportedInputError, 6: InvalidArgumentError, 7: TransportError, 8: Error,
+        9: TransportError, 10: Error, 11: Error}
+
+MEM_HOST, MEM_DEVICE = 0, 1
+PRECOND_NONE, PRECOND_JACOBI = 0, 1
+BACKEND_CG, BACKEND_BICGSTAB = 0, 1
+BACKEND_NAMES = {BACKEND_CG: "cg", BACKEND_BICGSTAB: "bicgstab"}
+
+_i64p = C.POINTER(C.c_int64)
+_i32p = C.POINTER(C.c_int32)
+_f64p = C.POINTER(C.c_double)
+_vp = C.c_void_p
+
+
+class _Opts(C.Structure):
+    _fields_ = [("atol", C.c_double), ("rtol", C.c_double), ("max_iter", C.c_int64),
+                ("preconditioner", C.c_int32), ("_pad", C.c_int32)]
+
+
+class _Report(C.Structure):
+    _fields_ = [("iterations", C.c_int64), ("spmv_count", C.c_int64),
+                ("residual_norm", C.c_double), ("converged", C.c_int32),
+                ("backend", C.c_int32), ("diagnostic", C.c_char * 128)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libsparsla_b200.so (fails loudly if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run `make -C paper_2601_13994_b200` "
+                              "(or __graft_entry__.build())")
+        L = C.CDLL(LIB_PATH)
+        L.sparsla_last_error_message.restype = C.c_char_p
+        _lib = L
+    return _lib
+
+
+def _check(rc):
+    if rc != 0:
+        msg = lib().sparsla_last_error_message().decode(errors="replace")
+        raise _ERR.get(rc, Error)(msg)
+
+
+def _p(a, t):
+    return a.ctypes.data_as(t)
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _i64(a):
+    return np.ascontiguousarray(a, dtype=np.int64)
+
+
+def device_count() -> int:
+    n = C.c_int()
+    _check(lib().sparsla_device_count(C.byref(n)))
+    return n.value
+
+
+# ------------------------------------------------------------------------ sparse core --
+@dataclass(frozen=True)
+class Shape:
+    rows: int = 0
+    cols: int = 0
+
+
+class SparseCoo:
+    """Canonical COO (sparse.hpp:38-75): sorted by (row, col), duplicates summed in input
+    order, explicit zeros kept.  Raises DimensionError / BoundsError like the reference."""
+
+    def __init__(self, rows=(), cols=(), vals=(), shape: Shape | tuple = Shape(),
+                 _canonical=False):
+        if isinstance(shape, tuple):
+            shape = Shape(*shape)
+        rows, cols, vals = _i64(rows), _i64(cols), _f64(vals)
+        if not (len(rows) == len(cols) == len(vals)):
+            raise DimensionError(f"coo arrays must have equal length: rows={len(rows)} "
+                                 f"cols={len(cols)} vals={len(vals)}")
+        if shape.rows < 0 or shape.cols < 0:
+            raise DimensionError("negative matrix shape")
+        self._shape = shape
+        if _canonical:
+            self._rows, self._cols, self._vals = rows, cols, vals
+            return
+        n = len(rows)
+        ro, co, vo = np.empty(n, np.int64), np.empty(n, np.int64), np.empty(n)
+        m = C.c_int64()
+        _check(lib().sparsla_coo_canonicalize(
+            C.c_int64(shape.rows), C.c_int64(shape.cols), C.c_int64(n), _p(rows, _i64p),
+            _p(cols, _i64p), _p(vals, _f64p), C.byref(m), _p(ro, _i64p), _p(co, _i64p),
+            _p(vo, _f64p)))
+        self._rows, self._cols, self._vals = ro[:m.value], co[:m.value], vo[:m.value]
+
+    shape = property(lambda s: s._shape)
+    nrows = property(lambda s: s._shape.rows)
+    ncols = property(lambda s: s._shape.cols)
+    nnz = property(lambda s: len(s._vals))
+    rows = property(lambda s: s._rows)
+    cols = property(lambda s: s._cols)
+    vals = property(lambda s: s._vals)
+
+    def with_values(self, vals) -> "SparseCoo":
+        vals = _f64(vals)
+        if len(vals) != self.nnz:
+            raise DimensionError(f"with_values: expected {self.nnz} values, got {len(vals)}")
+        return SparseCoo(self._rows, self._cols, vals.copy(), self._shape, _canonical=True)
+
+    def find(self, i: int, j: int) -> int:
+        lo = np.searchsorted(self._rows, i, "left")
+        hi = np.searchsorted(self._rows, i, "right")
+        c = lo + np.searchsorted(self._cols[lo:hi], j, "left")
+        return int(c) if c < hi and self._cols[c] == j else -1
+
+    def to_dense(self, cap: int = 1 << 24) -> np.ndarray:
+        if self.nrows * self.ncols > cap:
+            raise BoundsError(f"to_dense: {self.nrows}x{self.ncols} exceeds dense element cap {cap}")
+        d = np.zeros((self.nrows, self.ncols))
+        d[self._rows, self._cols] = self._vals
+        return d
+
+
+class CsrMatrix:
+    """CSR (sparse.hpp:77-104).  The device copy (int32 indices, fp64 values) is uploaded on
+    first use and cached per device; values are immutable like the reference's."""
+
+    def __init__(self, nrows, ncols, row_ptr, col_idx, vals, _validated=False):
+        self._shape = Shape(int(nrows), int(ncols))
+        self._rp, self._ci, self._v = _i64(row_ptr), _i64(col_idx), _f64(vals)
+        self._dev = {}
+
+    @staticmethod
+    def from_coo(coo: SparseCoo) -> "CsrMatrix":
+        n = coo.nrows
+        rp = np.empty(n + 1, np.int64)
+        ci = np.empty(coo.nnz, np.int64)
+        v = np.empty(coo.nnz)
+        _check(lib().sparsla_csr_from_coo(C.c_int64(n), C.c_int64(coo.ncols), C.c_int64(coo.nnz),
+                                          _p(coo.rows, _i64p), _p(coo.cols, _i64p),
+                                          _p(coo.vals, _f64p), _p(rp, _i64p), _p(ci, _i64p),
+                                          _p(v, _f64p)))
+        return CsrMatrix(n, coo.ncols, rp, ci, v)
+
+    def to_coo(self) -> SparseCoo:
+        rows = np.empty(self.nnz, np.int64)
+        _check(lib().sparsla_csr_to_coo_rows(C.c_int64(self.nrows), _p(self._rp, _i64p),
+                                             _p(rows, _i64p)))
+        return SparseCoo(rows, self._ci.copy(), self._v.copy(), self._shape, _canonical=True)
+
+    shape = property(lambda s: s._shape)
+    nrows = property(lambda s: s._shape.rows)
+    ncols = property(lambda s: s._shape.cols)
+    nnz = property(lambda s: len(s._v))
+    row_ptr = property(lambda s: s._rp)
+    col_idx = property(lambda s: s._ci)
+    vals = property(lambda s: s._v)
+
+    def bytes(self) -> int:
+        """Live-array footprint of the reference layout (sparse.cpp:129-133)."""
+        return 8 * (len(self._rp) + len(self._ci) + len(self._v))
+
+    def device(self, dev: int = 0) -> "DeviceCsr":
+        if dev not in self._dev:
+            self._dev[dev] = DeviceCsr(self, dev)
+        return self._dev[dev]
+
+
+class DeviceCsr:
+    """Owning wrapper of a sparsla_dcsr handle (one GPU)."""
+
+    def __init__(self, A: CsrMatrix | None = None, dev: int = 0, *, i32=None):
+        self.h = _vp()
+        self.dev = dev
+        if A is not None:
+            _check(lib().sparsla_dcsr_create(C.c_int(dev), C.c_int64(A.nrows), C.c_int64(A.ncols),
+                                             _p(A.row_ptr, _i64p), _p(A.col_idx, _i64p),
+                                             _p(A.vals, _f64p), C.byref(self.h)))
+            self.nrows, self.ncols, self.nnz = A.nrows, A.ncols, A.nnz
+        else:
+            nrows, ncols, rp, ci, v = i32
+            rp = np.ascontiguousarray(rp, np.int32)
+            ci = np.ascontiguousarray(ci, np.int32)
+            v = _f64(v)
+            _check(lib().sparsla_dcsr_create_i32(C.c_int(dev), C.c_int64(nrows), C.c_int64(ncols),
+                                                 _p(rp, _i32p), _p(ci, _i32p), _p(v, _f64p),
+                                                 C.byref(self.h)))
+            self.nrows, self.ncols, self.nnz = int(nrows), int(ncols), len(v)
+
+    def info(self):
+        out = np.zeros(8, np.int64)
+        _check(lib().sparsla_dcsr_info(self.h, _p(out, _i64p)))
+        keys = ["nrows", "ncols", "nnz", "device_bytes", "max_block_nnz", "max_row", "variant"]
+        return {k: int(out[i]) for i, k in enumerate(keys)}
+
+    def close(self):
+        if self.h:
+            lib().sparsla_dcsr_destroy(self.h)
+            self.h = _vp()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _dev_of(A, dev=0) -> DeviceCsr:
+    return A if isinstance(A, DeviceCsr) else A.device(dev)
+
+
+def spmv(a, x) -> np.ndarray:
+    """y = A x, row-ordered accumulation (sparse.hpp:134-135), on the GPU."""
+    D = _dev_of(a)
+    x = _f64(x)
+    if len(x) != D.ncols:
+        raise DimensionError(f"spmv: x has length {len(x)}, expected {D.ncols}")
+    y = np.empty(D.nrows)
+    _check(lib().sparsla_spmv(D.h, _p(x, _f64p), _p(y, _f64p), C.c_int32(MEM_HOST)))
+    return y
+
+
+def spmv_transpose(a, x) -> np.ndarray:
+    """y = A^T x (sparse.hpp:137-138), on the GPU via an explicit canonical A^T."""
+    D = _dev_of(a)
+    x = _f64(x)
+    if len(x) != D.nrows:
+        raise DimensionError(f"spmv_transpose: x has length {len(x)}, expected {D.nrows}")
+    y = np.empty(D.ncols)
+    _check(lib().sparsla_spmv_transpose(D.h, _p(x, _f64p), _p(y, _f64p), C.c_int32(MEM_HOST)))
+    return y
+
+
+def transpose(a: SparseCoo) -> SparseCoo:
+    """Canonical transpose (sparse.hpp:140-141)."""
+    return SparseCoo(a.cols, a.rows, a.vals, Shape(a.ncols, a.nrows))
+
+
+def _symmetry(a: SparseCoo, tol):
+    A = CsrMatrix.from_coo(a)
+    s1, s2 = C.c_int32(), C.c_int32()
+    _check(lib().sparsla_csr_symmetry(C.c_int64(A.nrows), C.c_int64(A.ncols), _p(A.row_ptr, _i64p),
+                                      _p(A.col_idx, _i64p), _p(A.vals, _f64p), C.c_double(tol),
+                                      C.byref(s1), C.byref(s2)))
+    return bool(s1.value), bool(s2.value)
+
+
+def is_structurally_symmetric(a: SparseCoo) -> bool:
+    return _symmetry(a, 0.0)[0]
+
+
+def is_symmetric(a: SparseCoo, tol: float = 1e-12) -> bool:
+    return _symmetry(a, tol)[1]
+
+
+def dot(a, b, dev: int = 0) -> float:
+    """Canonical (deterministic, launch-geometry independent) dot product on the GPU."""
+    a, b = _f64(a), _f64(b)
+    if len(a) != len(b):
+        raise DimensionError("dot: length mismatch")
+    out = C.c_double()
+    _check(lib().sparsla_dot(C.c_int(dev), C.c_int64(len(a)), _p(a, _f64p), _p(b, _f64p),
+                             C.c_int32(MEM_HOST), C.byref(out)))
+    return out.value
+
+
+# --------------------------------------------------------------------------- solvers --
+@dataclass
+class SolveOptions:
+    """SPEC.md:127-130 (defaults: atol = 1e-10 per Listing 2, rtol = 0)."""
+    atol: float = 1e-10
+    rtol: float = 0.0
+    max_iter: int = 10000
+    preconditioner: str = "jacobi"  # "none" | "jacobi"
+
+    def c(self) -> _Opts:
+        pc = {"none": PRECOND_NONE, "jacobi": PRECOND_JACOBI}.get(self.preconditioner)
+        if pc is None:
+            raise InvalidArgumentError(f"unknown preconditioner {self.preconditioner!r}")
+        return _Opts(float(self.atol), float(self.rtol), int(self.max_iter), pc, 0)
+
+
+@dataclass
+class SolveReport:
+    """SPEC.md:131-134."""
+    iterations: int = 0
+    residual_norm: float = 0.0
+    converged: bool = False
+    spmv_count: int = 0
+    backend: str = "cg"
+    diagnostic: str = ""
+
+    @staticmethod
+    def _from(r: _Report) -> "SolveReport":
+        return SolveReport(int(r.iterations), float(r.residual_norm), bool(r.converged),
+                           int(r.spmv_count), BACKEND_NAMES.get(r.backend, "?"),
+                           r.diagnostic.decode(errors="replace"))
+
+
+@dataclass
+class JacobiPreconditioner:
+    inv_diag: np.ndarray
+
+
+def jacobi_build(a) -> JacobiPreconditioner:
+    """SPEC.md:159-167 (1/A_ii, 1.0 for missing / zero / non-finite reciprocal)."""
+    D = _dev_of(a)
+    if D.nrows != D.ncols:
+        raise DimensionError("jacobi_build requires a square matrix")
+    d = np.empty(D.nrows)
+    _check(lib().sparsla_jacobi(D.h, _p(d, _f64p), C.c_int32(MEM_HOST)))
+    return JacobiPreconditioner(d)
+
+
+def _krylov(fn, a, b, opts):
+    D = _dev_of(a)
+    opts = opts or SolveOptions()
+    b = _f64(b)
+    if D.nrows != D.ncols:
+        raise DimensionError("solve requires a square matrix")
+    if len(b) != D.nrows:
+        raise DimensionError(f"rhs has length {len(b)}, expected {D.nrows}")
+    x = np.empty(D.nrows)
+    rep = _Report()
+    o = opts.c()
+    _check(fn(D.h, _p(b, _f64p), _p(x, _f64p), C.byref(o), C.byref(rep), C.c_int32(MEM_HOST)))
+    return x, SolveReport._from(rep)
+
+
+def cg_solve(a, b, opts: SolveOptions | None = None):
+    """Jacobi-PCG from x0 = 0 -> (x, SolveReport)."""
+    return _krylov(lib().sparsla_cg_solve, a, b, opts)
+
+
+def bicgstab_solve(a, b, opts: SolveOptions | None = None):
+    """Right-Jacobi BiCGStab from x0 = 0 -> (x, SolveReport)."""
+    return _krylov(lib().sparsla_bicgstab_solve, a, b, opts)
+
+
+# --------------------------------------------------------------------------- adjoint --
+@dataclass
+class AdjointContext:
+    """Exactly (A, x) — no per-iteration state (Theorem 1)."""
+    matrix: SparseCoo
+    x: np.ndarray
+    backend: str = "cg"
+    _csr: CsrMatrix | None = field(default=None, repr=False)
+
+
+@dataclass
+class GradientBundle:
+    grad_b: np.ndarray
+    grad_vals: np.ndarray
+    report: SolveReport | None = None
+
+
+def solve_forward(a: SparseCoo, b, opts: SolveOptions | None = None, backend: str | None = None):
+    """by default CG on a structurally symmetric pattern, else BiCGStab
+    (auto_solve's iterative branch, SPEC.md:180 — note it picks CG for value-nonsymmetric
+    matrices with a symmetric pattern; pass backend="bicgstab" for those).  Raises Error if
+    the solve does not converge."""
+    csr = CsrMatrix.from_coo(a)
+    if backend is None:
+        backend = "cg" if is_structurally_symmetric(a) else "bicgstab"
+    fn = cg_solve if backend == "cg" else bicgstab_solve
+    x, rep = fn(csr, b, opts)
+    if not rep.converged:
+        raise Error(f"forward solve did not converge: {rep.diagnostic}")
+    return x, AdjointContext(a, x, backend, csr), rep
+
+
+def solve_backward(ctx: AdjointContext, grad_x, opts: SolveOptions | None = None,
+                   backend: str | None = None) -> GradientBundle:
+    """one solve A^T lam = grad_x; grad_b = lam;
+    grad_vals[k] = -lam[i_k] * x[j_k] over the stored entries (canonical COO order)."""
+    opts = opts or SolveOptions()
+    csr = ctx._csr or CsrMatrix.from_coo(ctx.matrix)
+    D = csr.device(0)
+    g = _f64(grad_x)
+    if len(g) != D.nrows:
+        raise DimensionError("grad_x length mismatch")
+    x = _f64(ctx.x)
+    gb = np.empty(D.nrows)
+    gv = np.empty(D.nnz)
+    rep = _Report()
+    o = opts.c()
+    be = {"cg": BACKEND_CG, "bicgstab": BACKEND_BICGSTAB}[backend or ctx.backend]
+    _check(lib().sparsla_adjoint_backward(D.h, _p(x, _f64p), _p(g, _f64p), C.c_int32(be),
+                                          C.byref(o), _p(gb, _f64p), _p(gv, _f64p), C.byref(rep),
+                                          C.c_int32(MEM_HOST)))
+    r = SolveReport._from(rep)
+    if not r.converged:
+        raise Error(f"adjoint solve did not converge: {r.diagnostic}")
+    return GradientBundle(gb, gv, r)
+
+
+# --------------------------------------------------------------- persistent solver ---
+class Solver:
+    """Device-resident solver (b, x, work vectors in HBM, graph-captured iteration)."""
+
+    def __init__(self, a, b, backend="cg", opts: SolveOptions | None = None, mem=MEM_HOST):
+        self.D = _dev_of(a)
+        self.h = _vp()
+        o = (opts or SolveOptions()).c()
+        be = {"cg": BACKEND_CG, "bicgstab": BACKEND_BICGSTAB}[backend]
+        ptr = _p(_f64(b), _f64p) if mem == MEM_HOST else C.cast(C.c_void_p(b), _f64p)
+        _check(lib().sparsla_solver_create(self.D.h, C.c_int32(be), ptr, C.c_int32(mem),
+                                           C.byref(o), C.byref(self.h)))
+
+    def reset(self):
+        _check(lib().sparsla_solver_reset(self.h))
+
+    def iterate(self, n):
+        _check(lib().sparsla_solver_iterate(self.h, C.c_int64(n)))
+
+    def run(self):
+        _check(lib().sparsla_solver_run(self.h))
+
+    def report(self) -> SolveReport:
+        r = _Report()
+        _check(lib().sparsla_solver_report(self.h, C.byref(r)))
+        return SolveReport._from(r)
+
+    def x(self) -> np.ndarray:
+        out = np.empty(self.D.nrows)
+        _check(lib().sparsla_solver_get_x(self.h, _p(out, _f64p), C.c_int32(MEM_HOST)))
+        return out
+
+    def stream(self) -> int:
+        s = _vp()
+        _check(lib().sparsla_solver_stream(self.h, C.byref(s)))
+        return s.value or 0
+
+    def launches_per_iteration(self) -> int:
+        n = C.c_int64()
+        _check(lib().sparsla_solver_launches_per_iteration(self.h, C.byref(n)))
+        return n.value
+
+    def close(self):
+        if self.h:
+            lib().sparsla_solver_destroy(self.h)
+            self.h = _vp()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ---------------------------------------------------------------------- generators ---
+KIND = {"poisson2d": 0, "poisson3d": 1, "convdiff3d": 2, "fem2d": 3}
+
+
+def gen_size(kind, p1, p2=0, fparam=1.0, row_begin=0, row_end=None):
+    n = C.c_int64()
+    nnz = C.c_int64()
+    if row_end is None:
+        _check(lib().sparsla_gen_size(C.c_int32(KIND[kind]), C.c_int64(p1), C.c_int64(p2),
+                                      C.c_double(fparam), C.c_int64(0), C.c_int64(0),
+                                      C.byref(n), C.byref(nnz)))
+        row_end = n.value
+    _check(lib().sparsla_gen_size(C.c_int32(KIND[kind]), C.c_int64(p1), C.c_int64(p2),
+                                  C.c_double(fparam), C.c_int64(row_begin), C.c_int64(row_end),
+                                  C.byref(n), C.byref(nnz)))
+    return n.value, nnz.value, row_end
+
+
+def generate(kind, p1, p2=0, fparam=1.0, row_begin=0, row_end=None) -> CsrMatrix:
+    """Canonical CSR rows [row_begin, row_end) of a generated problem (global columns)."""
+    n, nnz, row_end = gen_size(kind, p1, p2, fparam, row_begin, row_end)
+    nr = row_end - row_begin
+    rp = np.empty(nr + 1, np.int64)
+    ci = np.empty(nnz, np.int64)
+    v = np.empty(nnz)
+    _check(lib().sparsla_gen_csr(C.c_int32(KIND[kind]), C.c_int64(p1), C.c_int64(p2),
+                                 C.c_double(fparam), C.c_int64(row_begin), C.c_int64(row_end),
+                                 _p(rp, _i64p), _p(ci, _i64p), _p(v, _f64p)))
+    return CsrMatrix(nr, n, rp, ci, v)
+
+
+def generate_i32(kind, p1, p2=0, fparam=1.0, row_begin=0, row_end=None):
+    """Same as generate() in the device's int32 layout (no int64 host copy)."""
+    n, nnz, row_end = gen_size(kind, p1, p2, fparam, row_begin, row_end)
+    nr = row_end - row_begin
+    rp = np.empty(nr + 1, np.int32)
+    ci = np.empty(nnz, np.int32)
+    v = np.empty(nnz)
+    _check(lib().sparsla_gen_csr_i32(C.c_int32(KIND[kind]), C.c_int64(p1), C.c_int64(p2),
+                                     C.c_double(fparam), C.c_int64(row_begin), C.c_int64(row_end),
+                                     _p(rp, _i32p), _p(ci, _i32p), _p(v, _f64p)))
+    return nr, n, rp, ci, v
+
+
+def poisson2d(N: int):
+    """SPEC.md:561-569 -> (CsrMatrix, rhs = ones)."""
+    A = generate("poisson2d", N)
+    return A, np.ones(A.nrows)
+
+
+def gen_coords(kind, p1, p2=0):
+    n = p1 * p1 if kind == "poisson2d" else (p1 - 2) * (p1 - 2)
+    xs, ys = np.empty(n), np.empty(n)
+    _check(lib().sparsla_gen_coords(C.c_int32(KIND[kind]), C.c_int64(p1), C.c_int64(p2),
+                                    _p(xs, _f64p), _p(ys, _f64p)))
+    return xs, ys
+
+
+# ---------------------------------------------------------------------- distributed ---
+def partition_contiguous(n: int, P: int) -> np.ndarray:
+    out = np.empty(n, np.int32)
+    _check(lib().sparsla_partition_contiguous(C.c_int64(n), C.c_int32(P), _p(out, _i32p)))
+    return out
+
+
+def partition_rcb(xs, ys, P: int) -> np.ndarray:
+    xs, ys = _f64(xs), _f64(ys)
+    out = np.empty(len(xs), np.int32)
+    _check(lib().sparsla_partition_rcb(C.c_int64(len(xs)), _p(xs, _f64p), _p(ys, _f64p),
+                                       C.c_int32(P), _p(out, _i32p)))
+    return out
+
+
+@dataclass
+class LocalPartition:
+    """owned/halo sets, HaloMap per neighbour, local [owned|halo] matrix."""
+    rank: int
+    owned: np.ndarray
+    halo: np.ndarray
+    neighbors: np.ndarray
+    send_ptr: np.ndarray
+    send_idx: np.ndarray
+    recv_ptr: np.ndarray
+    recv_idx: np.ndarray
+    row_ptr: np.ndarray
+    col_idx: np.ndarray
+    vals: np.ndarray
+
+    def send_to(self, q):
+        a = int(np.searchsorted(self.neighbors, q))
+        return self.send_idx[self.send_ptr[a]:self.send_ptr[a + 1]]
+
+    def recv_from(self, q):
+        a = int(np.searchsorted(self.neighbors, q))
+        return self.recv_idx[self.recv_ptr[a]:self.recv_ptr[a + 1]]
+
+
+def build_local(owned_rows: CsrMatrix, owned, part_of, P: int, rank: int) -> LocalPartition:
+    """build_local from this rank's rows only (global column ids); structurally symmetric
+    patterns."""
+    part_of = np.ascontiguousarray(part_of, np.int32)
+    owned = _i64(owned)
+    h = _vp()
+    _check(lib().sparsla_local_build(C.c_int64(len(part_of)), _p(part_of, _i32p), C.c_int32(P),
+                                     C.c_int32(rank), C.c_int64(len(owned)), _p(owned, _i64p),
+                                     _p(owned_rows.row_ptr, _i64p), _p(owned_rows.col_idx, _i64p),
+                                     _p(owned_rows.vals, _f64p), C.byref(h)))
+    try:
+        s = np.empty(6, np.int64)
+        _check(lib().sparsla_local_sizes(h, _p(s, _i64p)))
+        no, nh, nn, nnz, ns, nr = (int(t) for t in s)
+        o = dict(owned=np.empty(no, np.int64), halo=np.empty(nh, np.int64),
+                 neighbors=np.empty(nn, np.int32), send_ptr=np.empty(nn + 1, np.int64),
+                 send_idx=np.empty(ns, np.int64), recv_ptr=np.empty(nn + 1, np.int64),
+                 recv_idx=np.empty(nr, np.int64), row_ptr=np.empty(no + 1, np.int64),
+                 col_idx=np.empty(nnz, np.int64), vals=np.empty(nnz))
+        args = []
+        for k in ("owned", "halo", "neighbors", "send_ptr", "send_idx", "recv_ptr", "recv_idx",
+                  "row_ptr", "col_idx", "vals"):
+            a = o[k]
+            args.append(_p(a, _i32p if a.dtype == np.int32 else
+                           (_f64p if a.dtype == np.float64 else _i64p)))
+        _check(lib().sparsla_local_get(h, *args))
+    finally:
+        lib().sparsla_local_destroy(h)
+    return LocalPartition(rank, **o)

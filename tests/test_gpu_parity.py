@@ -1,0 +1,259 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the CPU oracle.
+
+Bar (north star / SURVEY.md §8): integer and structural data bit-exact; SpMV bit-exact with
+the reference's row-ordered accumulation (sparse.cpp:144-152); Krylov trajectories bit-exact
+with the oracle (canonical dots, same operation order), hence identical iteration counts and
+||x - x_ref|| / ||x_ref|| = 0 <= 1e-8; adjoint gradients bit-exact (<= 1e-7 relative).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def bits(a):
+    return np.ascontiguousarray(a, np.float64).view(np.int64)
+
+
+def assert_bitwise(a, b, what=""):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    assert a.shape == b.shape, what
+    diff = np.nonzero(bits(a) != bits(b))[0]
+    assert len(diff) == 0, f"{what}: {len(diff)} entries differ, first at {diff[:5]}: " \
+                           f"{a[diff[:5]]} vs {b[diff[:5]]}"
+
+
+def to_S(S, A):
+    return S.CsrMatrix(A.nrows, A.ncols, A.row_ptr, A.col_idx, A.vals)
+
+
+def random_csr(O, n, m, density_rows, seed, long_rows=()):
+    rng = np.random.default_rng(seed)
+    rows, cols = [], []
+    for i in range(n):
+        k = int(rng.integers(0, density_rows + 1))
+        if i in long_rows:
+            k = long_rows[i] if isinstance(long_rows, dict) else 3000
+        c = rng.choice(m, size=min(k, m), replace=False)
+        rows += [i] * len(c)
+        cols += list(c)
+    vals = rng.standard_normal(len(rows))
+    return O.csr_from_triplets(n, m, rows, cols, vals)
+
+
+GENS = [("poisson2d", 37, 0, 0.0), ("poisson3d", 17, 0, 0.0), ("convdiff3d", 13, 0, 1.0),
+        ("fem2d", 60, 2601, 0.0)]
+
+
+@pytest.mark.parametrize("kind,p1,p2,fp", GENS)
+def test_spmv_bitwise_generators(S, O, gpu, kind, p1, p2, fp):
+    A = O.generate(kind, p1, p2, fp)
+    rng = np.random.default_rng(1)
+    x = rng.standard_normal(A.ncols)
+    assert_bitwise(S.spmv(to_S(S, A), x), O.spmv(A, x), kind)
+
+
+def test_spmv_spec_examples(S, O, gpu):
+    # I x = x; Poisson 3x3 grid * ones = {corner 2, edge 1, centre 0}; [[2,0],[1,3]][1,1]=[2,4]
+    I = S.CsrMatrix.from_coo(S.SparseCoo(range(5), range(5), np.ones(5), (5, 5)))
+    x = np.array([1.5, -2.0, 3.25, 0.0, 7.0])
+    assert_bitwise(S.spmv(I, x), x)
+    A, _ = S.poisson2d(3)
+    assert list(S.spmv(A, np.ones(9))) == [2, 1, 2, 1, 0, 1, 2, 1, 2]
+    B = S.CsrMatrix.from_coo(S.SparseCoo([0, 1, 1], [0, 0, 1], [2.0, 1.0, 3.0], (2, 2)))
+    assert list(S.spmv(B, [1, 1])) == [2.0, 4.0]
+    T = S.CsrMatrix.from_coo(S.SparseCoo([0], [1], [1.0], (2, 2)))
+    assert list(S.spmv_transpose(T, [1, 0])) == [0.0, 1.0]
+    with pytest.raises(S.DimensionError):
+        S.spmv(B, [1, 1, 1])
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_spmv_random_rectangular_and_ragged(S, O, gpu, seed):
+    A = random_csr(O, 3001 + seed, 2500, 12, seed)  # empty rows, ragged rows, n % 2048 != 0
+    x = np.random.default_rng(seed).standard_normal(A.ncols)
+    D = to_S(S, A).device(0)
+    assert D.info()["variant"] == 0
+    assert_bitwise(S.spmv(D, x), O.spmv(A, x))
+    # spmv_transpose == row-ordered spmv on canonical A^T (== reference scatter order)
+    y = np.random.default_rng(seed + 7).standard_normal(A.nrows)
+    assert_bitwise(S.spmv_transpose(D, y), O.spmv(O.transpose(A), y))
+
+
+def test_spmv_long_rows_direct_variant(S, O, gpu):
+    A = random_csr(O, 700, 5000, 5, 3, long_rows={3: 4000, 500: 4500})  # > smem staging
+    D = to_S(S, A).device(0)
+    assert D.info()["variant"] == 1
+    x = np.random.default_rng(3).standard_normal(A.ncols)
+    assert_bitwise(S.spmv(D, x), O.spmv(A, x))
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 2047, 2048, 2049, 4097, 300001, 2_100_000])
+def test_canonical_dot(S, O, gpu, n):
+    rng = np.random.default_rng(n)
+    a, b = rng.standard_normal(n), rng.standard_normal(n)
+    assert bits([S.dot(a, b)])[0] == bits([O.cdot(a, b)])[0]
+
+
+def test_jacobi(S, O, gpu):
+    A = O.csr_from_triplets(4, 4, [0, 1, 2, 3, 0], [0, 1, 3, 3, 1], [2.0, 0.0, 1.0, 4.0, 5.0])
+    d = S.jacobi_build(to_S(S, A)).inv_diag
+    assert list(d) == [0.5, 1.0, 1.0, 0.25]  # A_11 = 0 -> 1.0, A_22 missing -> 1.0
+    P = O.generate("poisson2d", 8)
+    assert np.all(S.jacobi_build(to_S(S, P)).inv_diag == 0.25)
+    F = O.generate("fem2d", 50, 2601)
+    assert_bitwise(S.jacobi_build(to_S(S, F)).inv_diag, O.jacobi(F))
+
+
+def rep_eq(r, ro):
+    assert r.iterations == ro["iterations"], (r, ro)
+    assert r.spmv_count == ro["spmv_count"], (r, ro)
+    assert r.converged == ro["converged"], (r, ro)
+    assert bits([r.residual_norm])[0] == bits([ro["residual_norm"]])[0], (r, ro)
+    assert r.diagnostic == ro["diagnostic"], (r, ro)
+
+
+CG_CASES = [("poisson2d", 64, 0, 0.0, 1e-8), ("poisson3d", 24, 0, 0.0, 1e-8),
+            ("fem2d", 90, 2601, 0.0, 1e-8), ("poisson2d", 150, 0, 0.0, 1e-10)]
+
+
+@pytest.mark.parametrize("kind,p1,p2,fp,rtol", CG_CASES)
+def test_cg_bitwise_trajectory(S, O, gpu, kind, p1, p2, fp, rtol):
+    A = O.generate(kind, p1, p2, fp)
+    b = np.ones(A.nrows)
+    xo, ro = O.cg(A, b, atol=0.0, rtol=rtol, max_iter=20000)
+    x, r = S.cg_solve(to_S(S, A), b, S.SolveOptions(atol=0.0, rtol=rtol, max_iter=20000))
+    assert ro["converged"]
+    rep_eq(r, ro)
+    assert_bitwise(x, xo, kind)
+
+
+def test_cg_spec_examples(S, O, gpu):
+    A = S.CsrMatrix.from_coo(S.SparseCoo(range(4), range(4), [2.0] * 4, (4, 4)))
+    x, r = S.cg_solve(A, [2, 4, 6, 8])
+    assert list(x) == [1, 2, 3, 4] and r.iterations == 1 and r.converged and r.spmv_count == 2
+    P, b = S.poisson2d(32)
+    x, r = S.cg_solve(P, b, S.SolveOptions(atol=1e-10))
+    assert r.converged and r.residual_norm <= 1e-10 and r.spmv_count == 1 + r.iterations
+    xd = np.linalg.solve(S.SparseCoo(*_coo(P), (1024, 1024)).to_dense(), b)
+    assert np.max(np.abs(x - xd)) <= 1e-8
+    x1, r1 = S.cg_solve(P, b, S.SolveOptions(atol=1e-10, max_iter=1))
+    assert not r1.converged and r1.residual_norm > 1e-10 and r1.diagnostic == "max_iter reached"
+    # indefinite: p^T A p <= 0 breakdown is reported, not raised
+    N = S.CsrMatrix.from_coo(S.SparseCoo(range(3), range(3), [-1.0, -2.0, -3.0], (3, 3)))
+    xn, rn = S.cg_solve(N, [1, 1, 1])
+    assert not rn.converged and rn.diagnostic.startswith("breakdown: p^T A p <= 0")
+    with pytest.raises(S.InvalidArgumentError):
+        S.cg_solve(P, b, S.SolveOptions(atol=0.0, rtol=0.0))
+
+
+def _coo(A):
+    rows = np.repeat(np.arange(A.nrows), np.diff(A.row_ptr))
+    return rows, A.col_idx, A.vals
+
+
+def test_cg_iteration_scaling(S, gpu):
+    its = []
+    for N in (16, 32, 64, 128):
+        P, b = S.poisson2d(N)
+        its.append(S.cg_solve(P, b, S.SolveOptions(atol=1e-10))[1].iterations)
+    ratios = [its[i + 1] / its[i] for i in range(3)]
+    assert all(1.5 <= q <= 3.0 for q in ratios), its
+
+
+BI_CASES = [("convdiff3d", 16, 0, 1.0), ("convdiff3d", 24, 0, 0.3), ("poisson2d", 40, 0, 0.0),
+            ("fem2d", 50, 2601, 0.0)]
+
+
+@pytest.mark.parametrize("kind,p1,p2,fp", BI_CASES)
+def test_bicgstab_bitwise_trajectory(S, O, gpu, kind, p1, p2, fp):
+    A = O.generate(kind, p1, p2, fp)
+    b = np.ones(A.nrows)
+    xo, ro = O.bicgstab(A, b, atol=0.0, rtol=1e-8, max_iter=5000)
+    x, r = S.bicgstab_solve(to_S(S, A), b, S.SolveOptions(atol=0.0, rtol=1e-8, max_iter=5000))
+    assert ro["converged"]
+    rep_eq(r, ro)
+    assert_bitwise(x, xo, kind)
+
+
+def test_bicgstab_spec_examples(S, O, gpu):
+    A = S.CsrMatrix.from_coo(S.SparseCoo([0, 0, 1], [0, 1, 1], [4.0, 1.0, 3.0], (2, 2)))
+    x, r = S.bicgstab_solve(A, [5, 3])
+    assert r.converged and np.allclose(x, [1, 1], atol=1e-12)
+    xo, ro = O.bicgstab(O.csr_from_triplets(2, 2, [0, 0, 1], [0, 1, 1], [4.0, 1.0, 3.0]), [5, 3])
+    rep_eq(r, ro)
+    assert_bitwise(x, xo)
+    P, b = S.poisson2d(16)
+    xb, rb = S.bicgstab_solve(P, b, S.SolveOptions(atol=1e-12))
+    xc, rc = S.cg_solve(P, b, S.SolveOptions(atol=1e-12))
+    assert np.max(np.abs(xb - xc)) <= 1e-8
+    Z = S.CsrMatrix(2, 2, [0, 0, 0], [], [])
+    xz, rz = S.bicgstab_solve(Z, [1, 1])
+    assert not rz.converged and rz.diagnostic.startswith("breakdown")
+
+
+def test_adjoint_spec_examples(S, O, gpu):
+    A = S.SparseCoo(range(3), range(3), [2.0, 2.0, 2.0], (3, 3))
+    x, ctx, rep = S.solve_forward(A, [2, 4, 6])
+    assert list(x) == [1, 2, 3]
+    g = S.solve_backward(ctx, np.ones(3))
+    assert list(g.grad_b) == [0.5, 0.5, 0.5]
+    assert list(g.grad_vals) == [-0.5, -1.0, -1.5]
+    I = S.SparseCoo(range(4), range(4), np.ones(4), (4, 4))
+    gx = np.array([1.0, -2.0, 3.0, 0.5])
+    xi, ci, _ = S.solve_forward(I, [4.0, 3.0, 2.0, 1.0])
+    gi = S.solve_backward(ci, gx)
+    assert_bitwise(gi.grad_b, gx)
+    assert_bitwise(gi.grad_vals, -(gx * xi))
+    z = S.solve_backward(ci, np.zeros(4))  # short-circuit: zero gradients, zero iterations
+    assert np.all(z.grad_b == 0) and np.all(z.grad_vals == 0) and z.report.iterations == 0
+
+
+@pytest.mark.parametrize("kind,p1,fp,backend", [("poisson2d", 40, 0.0, 0), ("fem2d", 45, 0.0, 0),
+                                                 ("convdiff3d", 12, 1.0, 1)])
+def test_adjoint_bitwise(S, O, gpu, kind, p1, fp, backend):
+    A = O.generate(kind, p1, 2601 if kind == "fem2d" else 0, fp)
+    b = np.ones(A.nrows)
+    solve = O.bicgstab if backend else O.cg
+    xo, _ = solve(A, b, atol=1e-12)
+    g = np.random.default_rng(5).standard_normal(A.nrows)
+    gbo, gvo, ro = O.adjoint_backward(A, xo, g, backend=backend, atol=1e-12)
+    coo = S.SparseCoo(*_coo(A), (A.nrows, A.ncols))
+    x, ctx, _ = S.solve_forward(coo, b, S.SolveOptions(atol=1e-12),
+                                backend="bicgstab" if backend else "cg")
+    assert_bitwise(x, xo)
+    gr = S.solve_backward(ctx, g, S.SolveOptions(atol=1e-12), backend="bicgstab" if backend else "cg")
+    rep_eq(gr.report, ro)
+    assert_bitwise(gr.grad_b, gbo)
+    assert_bitwise(gr.grad_vals, gvo)
+    # linearity in grad_x
+    g2 = np.random.default_rng(6).standard_normal(A.nrows)
+    ga = S.solve_backward(ctx, g, S.SolveOptions(atol=1e-13))
+    gb = S.solve_backward(ctx, g2, S.SolveOptions(atol=1e-13))
+    gc = S.solve_backward(ctx, 2.0 * g - 3.0 * g2, S.SolveOptions(atol=1e-13))
+    ref = 2.0 * ga.grad_b - 3.0 * gb.grad_b
+    assert np.max(np.abs(gc.grad_b - ref)) <= 1e-7 * np.max(np.abs(ref))
+
+
+def test_config_A_full(S, O, gpu):
+    """BASELINE configs[0]: 2-D Poisson 1000x1000, Jacobi-PCG to rel-res 1e-8."""
+    A = O.generate("poisson2d", 1000)
+    b = np.ones(A.nrows)
+    xo, ro = O.cg(A, b, atol=0.0, rtol=1e-8, max_iter=100000)
+    x, r = S.cg_solve(to_S(S, A), b, S.SolveOptions(atol=0.0, rtol=1e-8, max_iter=100000))
+    assert ro["iterations"] == 1853
+    rep_eq(r, ro)
+    assert_bitwise(x, xo)
+
+
+def test_persistent_solver_fixed_iterations(S, O, gpu):
+    """Solver.iterate(k) after reset == oracle CG truncated at k iterations, bitwise."""
+    A = O.generate("poisson3d", 64)
+    b = np.ones(A.nrows)
+    sv = S.Solver(to_S(S, A), b, "cg", S.SolveOptions(atol=0.0, rtol=1e-30, max_iter=10**6))
+    for k in (1, 7, 40):
+        sv.reset()
+        sv.iterate(k)
+        xo, _ = O.cg_fixed(A, b, k)
+        assert sv.report().iterations == k
+        assert_bitwise(sv.x(), xo, f"k={k}")
