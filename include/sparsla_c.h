@@ -197,6 +197,9 @@ int sparsla_solver_get_x(sparsla_solver* S, double* x, int32_t mem);
 int sparsla_solver_stream(sparsla_solver* S, void** stream);
 /* number of kernel launches one iteration issues */
 int sparsla_solver_launches_per_iteration(sparsla_solver* S, int64_t* launches);
+/* run `iters` iterations launched individually with CUDA events around every kernel; ms[k]
+ * = average duration of the k-th kernel of an iteration (launches_per_iteration entries) */
+int sparsla_solver_kernel_times(sparsla_solver* S, int64_t iters, double* ms);
 int sparsla_solver_destroy(sparsla_solver* S);
 /* time `reps` SpMV launches on the handle stream, returns avg ms per launch */
 int sparsla_spmv_bench(sparsla_dcsr* A, int32_t reps, double* ms_per_launch);

@@ -64,10 +64,10 @@ static void configure_kernels_once(int device) {
     std::lock_guard<std::mutex> lk(mu);
     if (std::find(done.begin(), done.end(), device) != done.end()) return;
     const int max_smem = 160 * 1024;  // staged variant is chosen only up to 110 KB
-    CK(cudaFuncSetAttribute(spmv_kernel<SPMV_PLAIN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
-    CK(cudaFuncSetAttribute(spmv_kernel<SPMV_CG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
-    CK(cudaFuncSetAttribute(spmv_kernel<SPMV_BICG_V, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
-    CK(cudaFuncSetAttribute(spmv_kernel<SPMV_BICG_T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
+    CK(cudaFuncSetAttribute(spmv_ws_kernel<SPMV_PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
+    CK(cudaFuncSetAttribute(spmv_ws_kernel<SPMV_CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
+    CK(cudaFuncSetAttribute(spmv_ws_kernel<SPMV_BICG_V>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
+    CK(cudaFuncSetAttribute(spmv_ws_kernel<SPMV_BICG_T>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
     done.push_back(device);
 }
 
@@ -116,11 +116,16 @@ DevCsr* DevCsr::create(int device, long long nrows, long long ncols, const I* h_
     A->max_row = mr;
     A->cap_v = (int)(((mb + 2) + 1) & ~1LL);
     A->cap_c = (int)(((mb + 6) + 3) & ~3LL);
-    const size_t vb = ((size_t)A->cap_v * 8 + 127) & ~size_t(127);
-    const size_t cb = ((size_t)A->cap_c * 4 + 127) & ~size_t(127);
-    const size_t rb = (kRpCopy * 4 + 127) & ~size_t(127);
-    A->smem_bytes = 128 + kStages * (vb + cb + rb);
+    const StageLayout SL(A->cap_v, A->cap_c);
+    A->smem_bytes = 128 + kStages * SL.stage;
     A->staged = A->smem_bytes <= 110 * 1024;
+    {
+        int sms = 0, per_sm = 0;
+        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, spmv_ws_kernel<SPMV_CG>, kWsThreads,
+                                                         A->smem_bytes));
+        A->ws_ctas = sms * std::max(1, per_sm);
+    }
     CK(cudaDeviceSynchronize());
     return A.release();
 }
@@ -201,23 +206,34 @@ void launch_spmv(DevCsr* A, cudaStream_t s, int mode, const double* x, double* y
     SpmvParams P{};
     P.rp = A->rp; P.ci = A->ci; P.val = A->val;
     P.x = x; P.y = y; P.n = A->nrows; P.chunk0 = 0; P.aux = aux;
+    P.nch = nchunks_of(A->nrows);
     P.cap_v = A->cap_v; P.cap_c = A->cap_c;
     P.check_done = check_done;
     P.red = red;
     P.red.nchunks = nchunks_of(A->nrows);
-    P.red.expected = (unsigned)P.red.nchunks;
-    const unsigned grid = (unsigned)nchunks_of(A->nrows);
-    const size_t smem = A->staged ? A->smem_bytes : 0;
-#define SPMV_CASE(M)                                                                     \
-    if (A->staged) spmv_kernel<M, true><<<grid, kSpmvThreads, smem, s>>>(P);            \
-    else spmv_kernel<M, false><<<grid, kSpmvThreads, 0, s>>>(P);
-    switch (mode) {
-        case SPMV_PLAIN: SPMV_CASE(SPMV_PLAIN) break;
-        case SPMV_CG: SPMV_CASE(SPMV_CG) break;
-        case SPMV_BICG_V: SPMV_CASE(SPMV_BICG_V) break;
-        case SPMV_BICG_T: SPMV_CASE(SPMV_BICG_T) break;
+    if (A->staged) {
+        const unsigned grid = (unsigned)std::min<long long>(P.nch, (long long)A->ws_ctas);
+        P.red.expected = grid;
+#define WS_CASE(M) spmv_ws_kernel<M><<<grid, kWsThreads, A->smem_bytes, s>>>(P);
+        switch (mode) {
+            case SPMV_PLAIN: WS_CASE(SPMV_PLAIN) break;
+            case SPMV_CG: WS_CASE(SPMV_CG) break;
+            case SPMV_BICG_V: WS_CASE(SPMV_BICG_V) break;
+            case SPMV_BICG_T: WS_CASE(SPMV_BICG_T) break;
+        }
+#undef WS_CASE
+    } else {
+        const unsigned grid = (unsigned)P.nch;
+        P.red.expected = grid;
+#define DIRECT_CASE(M) spmv_direct_kernel<M><<<grid, kSpmvThreads, 0, s>>>(P);
+        switch (mode) {
+            case SPMV_PLAIN: DIRECT_CASE(SPMV_PLAIN) break;
+            case SPMV_CG: DIRECT_CASE(SPMV_CG) break;
+            case SPMV_BICG_V: DIRECT_CASE(SPMV_BICG_V) break;
+            case SPMV_BICG_T: DIRECT_CASE(SPMV_BICG_T) break;
+        }
+#undef DIRECT_CASE
     }
-#undef SPMV_CASE
     CK(cudaGetLastError());
 }
 
@@ -313,19 +329,39 @@ void Solver::enqueue_init() {
     }
 }
 
-void Solver::enqueue_iteration() {
+void Solver::enqueue_iteration(cudaEvent_t* evs) {
+    // evs (optional): launches_per_iteration()+1 events recorded around every kernel
+    auto mark = [&](int i) { if (evs) CK(cudaEventRecord(evs[i], stream)); };
     VecParams P = vparams();
+    mark(0);
     if (backend == SPARSLA_BACKEND_CG) {
-        launch_spmv(A, stream, SPMV_CG, p, q, nullptr, red(SC_CG_PQ, 1), 1);
-        launch_vec<V_CG_U1>(stream, P, red(SC_CG_RR, 2));
-        launch_vec<V_CG_U2>(stream, P, red(SC_NONE, 3));
+        launch_spmv(A, stream, SPMV_CG, p, q, nullptr, red(SC_CG_PQ, 1), 1); mark(1);
+        launch_vec<V_CG_U1>(stream, P, red(SC_CG_RR, 2)); mark(2);
+        launch_vec<V_CG_U2>(stream, P, red(SC_NONE, 3)); mark(3);
     } else {
-        launch_vec<V_BI_U1>(stream, P, red(SC_NONE, 1));
-        launch_spmv(A, stream, SPMV_BICG_V, ph, q, rh, red(SC_BI_RV, 2), 1);
-        launch_vec<V_BI_U2>(stream, P, red(SC_NONE, 3));
-        launch_spmv(A, stream, SPMV_BICG_T, sh, t, s, red(SC_BI_T, 4), 1);
-        launch_vec<V_BI_U3>(stream, P, red(SC_BI_U3, 5));
+        launch_vec<V_BI_U1>(stream, P, red(SC_NONE, 1)); mark(1);
+        launch_spmv(A, stream, SPMV_BICG_V, ph, q, rh, red(SC_BI_RV, 2), 1); mark(2);
+        launch_vec<V_BI_U2>(stream, P, red(SC_NONE, 3)); mark(3);
+        launch_spmv(A, stream, SPMV_BICG_T, sh, t, s, red(SC_BI_T, 4), 1); mark(4);
+        launch_vec<V_BI_U3>(stream, P, red(SC_BI_U3, 5)); mark(5);
     }
+}
+
+void Solver::kernel_times(long long iters, double* ms) {
+    DeviceGuard g(A->device);
+    const int L = (int)launches_per_iteration();
+    std::vector<cudaEvent_t> evs((size_t)iters * (L + 1));
+    for (auto& e : evs) CK(cudaEventCreate(&e));
+    for (long long it = 0; it < iters; ++it) enqueue_iteration(evs.data() + it * (L + 1));
+    CK(cudaStreamSynchronize(stream));
+    for (int k = 0; k < L; ++k) ms[k] = 0.0;
+    for (long long it = 0; it < iters; ++it)
+        for (int k = 0; k < L; ++k) {
+            float t = 0;
+            CK(cudaEventElapsedTime(&t, evs[it * (L + 1) + k], evs[it * (L + 1) + k + 1]));
+            ms[k] += t / (double)iters;
+        }
+    for (auto& e : evs) cudaEventDestroy(e);
 }
 
 long long Solver::launches_per_iteration() const { return backend == SPARSLA_BACKEND_CG ? 3 : 5; }
@@ -718,6 +754,12 @@ int sparsla_solver_stream(sparsla_solver* S, void** stream) {
 }
 int sparsla_solver_launches_per_iteration(sparsla_solver* S, int64_t* l) {
     return guarded([&] { *l = S->S->launches_per_iteration(); });
+}
+int sparsla_solver_kernel_times(sparsla_solver* S, int64_t iters, double* ms) {
+    return guarded([&] {
+        if (iters < 1) fail(SPARSLA_ERR_INVALID_ARGUMENT, "iters >= 1");
+        S->S->kernel_times(iters, ms);
+    });
 }
 int sparsla_solver_destroy(sparsla_solver* S) {
     return guarded([&] {

@@ -29,6 +29,7 @@ struct DevCsr {
     int cap_v = 0, cap_c = 0;
     size_t smem_bytes = 0;
     bool staged = true;
+    int ws_ctas = 0;  // persistent grid of the staged SpMV (SMs x resident CTAs)
     double* dinv = nullptr;
     double* ones = nullptr;
     int sym_checked = -1;
@@ -78,12 +79,13 @@ struct Solver {
     void run();
     void report(sparsla_solve_report* rep);
     long long launches_per_iteration() const;
+    void kernel_times(long long iters, double* ms);
 
    private:
     RedParams red(int which, int slot) const;
     VecParams vparams() const;
     void enqueue_init();
-    void enqueue_iteration();
+    void enqueue_iteration(cudaEvent_t* evs = nullptr);
     void build_graphs();
 };
 

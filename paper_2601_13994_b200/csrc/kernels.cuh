@@ -160,7 +160,14 @@ __device__ __forceinline__ double tree_smem(volatile double* a) {
 // Slot-group value per thread (thread t holds the group sum of slots [t*G, (t+1)*G)) ->
 // chunk partial on thread 0.  xor-butterfly levels 1..16 realise the pairwise tree over
 // consecutive groups (IEEE addition is commutative, so both lanes get the same bits).
-template <int NT, int NDOT>
+// CTA (BAR == 0) or named-barrier (BAR > 0, the first NT threads) synchronisation.
+template <int BAR, int NT>
+__device__ __forceinline__ void group_sync() {
+    if constexpr (BAR == 0) __syncthreads();
+    else asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(NT) : "memory");
+}
+
+template <int NT, int NDOT, int BAR = 0>
 __device__ __forceinline__ void block_tree(double (&v)[NDOT], double* sred) {
     constexpr int NW = NT / 32;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -170,16 +177,17 @@ __device__ __forceinline__ void block_tree(double (&v)[NDOT], double* sred) {
         for (int off = 1; off < 32; off <<= 1) v[d] = __dadd_rn(v[d], __shfl_xor_sync(0xffffffffu, v[d], off));
         if (lane == 0) sred[d * NW + w] = v[d];
     }
-    __syncthreads();
+    group_sync<BAR, NT>();
     if (threadIdx.x == 0) {
 #pragma unroll
         for (int d = 0; d < NDOT; ++d) v[d] = tree_smem<NW>(sred + d * NW);
     }
+    group_sync<BAR, NT>();  // sred reusable afterwards
 }
 
 // Level-2 reduction over m chunk partials per dot (layout [NDOT][m]); called by every
 // thread of the last CTA; result valid on thread 0.
-template <int NT, int NDOT>
+template <int NT, int NDOT, int BAR = 0>
 __device__ void final_reduce(const double* partials, long long m, double (&out)[NDOT], double* sred) {
     constexpr int SPT = kFinalSlots / NT;  // consecutive slots per thread
     const int t = threadIdx.x;
@@ -207,7 +215,7 @@ __device__ void final_reduce(const double* partials, long long m, double (&out)[
             for (int i = 0; i + w < SPT; i += 2 * w) s[i] = __dadd_rn(s[i], s[i + w]);
         out[d] = s[0];
     }
-    block_tree<NT, NDOT>(out, sred);
+    block_tree<NT, NDOT, BAR>(out, sred);
 }
 
 // Publish this CTA's chunk partials; the last CTA (ticket) finishes the reduction and runs
@@ -253,6 +261,35 @@ __device__ void publish_and_finish(double (&part)[NDOT], long long chunk, const 
     }
 }
 
+// Persistent kernels: each CTA publishes several chunk partials, then takes ONE ticket;
+// the last CTA to finish reduces all chunks (same canonical result as publish_and_finish).
+template <int NT, int NDOT, int BAR>
+__device__ void ticket_and_finish(const RedParams& R, double* sred, int* s_flag) {
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned prev = atomicAdd(R.ticket, 1u);
+        *s_flag = (prev == R.expected - 1);
+    }
+    group_sync<BAR, NT>();
+    if (!*s_flag) return;
+    __threadfence();
+    double tot[NDOT];
+    final_reduce<NT, NDOT, BAR>(R.partials, R.nchunks, tot, sred);
+    if (threadIdx.x == 0) {
+        if (R.red_out) {
+#pragma unroll
+            for (int d = 0; d < NDOT; ++d) R.red_out[d] = tot[d];
+        } else {
+            double t3[4] = {0, 0, 0, 0};
+#pragma unroll
+            for (int d = 0; d < NDOT; ++d) t3[d] = tot[d];
+            apply_scalar(R.scalar, R.st, t3);
+        }
+        *R.ticket = 0u;
+        __threadfence();
+    }
+}
+
 // ------------------------------------------------------------------ PTX helpers ------
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -269,6 +306,9 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
                  : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     uint32_t ok;
@@ -311,6 +351,7 @@ struct SpmvParams {
     double* y;
     long long n;        // rows
     long long chunk0;   // first chunk index handled by this launch (interior/boundary split)
+    long long nch;      // number of chunks handled by this launch
     const double* aux;  // BICG_V: rhat, BICG_T: s
     int cap_v, cap_c;   // staged capacities (elements) per round
     int check_done;
@@ -354,9 +395,11 @@ __device__ __forceinline__ double row_sum(int kb, int ke, const double* __restri
     return sum;
 }
 
-// One CTA = one chunk of 2048 rows = 8 rounds of 256 rows; thread t owns row (round*256+t).
-template <int MODE, bool STAGED>
-__global__ void __launch_bounds__(kSpmvThreads, 2) spmv_kernel(SpmvParams P) {
+// Direct variant (rows too long for shared-memory staging): one CTA = one chunk of 2048
+// rows = 8 rounds of 256 rows; thread t owns row (round*256 + t); vals/cols via the
+// read-only path.
+template <int MODE>
+__global__ void __launch_bounds__(kSpmvThreads, 2) spmv_direct_kernel(SpmvParams P) {
     constexpr int ND = SpmvDots<MODE>::n;
     constexpr int NA = ND > 0 ? ND : 1;
     if (P.check_done && P.red.st->done) return;
@@ -368,74 +411,16 @@ __global__ void __launch_bounds__(kSpmvThreads, 2) spmv_kernel(SpmvParams P) {
     double acc[NA];
 #pragma unroll
     for (int d = 0; d < NA; ++d) acc[d] = 0.0;
-
-    if constexpr (STAGED) {
-        extern __shared__ __align__(128) unsigned char smem[];
-        uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
-        const size_t vbytes = ((size_t)P.cap_v * 8 + 127) & ~size_t(127);
-        const size_t cbytes = ((size_t)P.cap_c * 4 + 127) & ~size_t(127);
-        const size_t rbytes = (kRpCopy * 4 + 127) & ~size_t(127);
-        const size_t stage_bytes = vbytes + cbytes + rbytes;
-        unsigned char* stage0 = smem + 128;
-        auto sv = [&](int s) { return reinterpret_cast<double*>(stage0 + s * stage_bytes); };
-        auto sc = [&](int s) { return reinterpret_cast<int32_t*>(stage0 + s * stage_bytes + vbytes); };
-        auto sr = [&](int s) { return reinterpret_cast<int32_t*>(stage0 + s * stage_bytes + vbytes + cbytes); };
-        if (t == 0) {
-            for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
-            fence_mbar_init();
-        }
-        __syncthreads();
-        const uint64_t pol = policy_evict_first();
-        auto issue = [&](int r) {
-            const int s = r % kStages;
-            const long long rs = base + (long long)r * kChunkSlots;
-            const long long re = min(rs + kChunkSlots, P.n);
-            const int nz0 = __ldg(P.rp + rs), nz1 = __ldg(P.rp + re);
-            const int a0 = nz0 & ~1, a1 = (nz1 + 1) & ~1;
-            const int c0 = nz0 & ~3, c1 = (nz1 + 3) & ~3;
-            const uint32_t vb = (uint32_t)(a1 - a0) * 8u, cb = (uint32_t)(c1 - c0) * 4u;
-            mbar_arrive_expect_tx(&bars[s], (uint32_t)(kRpCopy * 4) + vb + cb);
-            bulk_g2s(sr(s), P.rp + rs, kRpCopy * 4, &bars[s], pol);
-            if (vb) bulk_g2s(sv(s), P.val + a0, vb, &bars[s], pol);
-            if (cb) bulk_g2s(sc(s), P.ci + c0, cb, &bars[s], pol);
-        };
-        if (t == 0)
-            for (int r = 0; r < kStages && r < nrounds; ++r) issue(r);
-        for (int r = 0; r < nrounds; ++r) {
-            const int s = r % kStages;
-            mbar_wait(&bars[s], (uint32_t)((r / kStages) & 1));
-            const long long row = base + (long long)r * kChunkSlots + t;
-            if (row < P.n) {
-                const int32_t* rps = sr(s);
-                const int nz0 = rps[0];
-                const int a0 = nz0 & ~1, c0 = nz0 & ~3;
-                const double* vs = sv(s);
-                const int32_t* cs = sc(s);
-                const double y = row_sum(rps[t], rps[t + 1], P.x, [&](int k, int& c, double& v) {
-                    c = cs[k - c0];
-                    v = vs[k - a0];
-                });
-                P.y[row] = y;
-                spmv_epilogue<MODE>(P, row, y, acc);
-            }
-            __syncthreads();  // stage s fully consumed
-            if (t == 0 && r + kStages < nrounds) {
-                fence_proxy_async_smem();
-                issue(r + kStages);
-            }
-        }
-    } else {
-        for (int r = 0; r < nrounds; ++r) {
-            const long long row = base + (long long)r * kChunkSlots + t;
-            if (row < P.n) {
-                const double y = row_sum(__ldg(P.rp + row), __ldg(P.rp + row + 1), P.x,
-                                         [&](int k, int& c, double& v) {
-                                             c = __ldg(P.ci + k);
-                                             v = __ldg(P.val + k);
-                                         });
-                P.y[row] = y;
-                spmv_epilogue<MODE>(P, row, y, acc);
-            }
+    for (int r = 0; r < nrounds; ++r) {
+        const long long row = base + (long long)r * kChunkSlots + t;
+        if (row < P.n) {
+            const double y = row_sum(__ldg(P.rp + row), __ldg(P.rp + row + 1), P.x,
+                                     [&](int k, int& c, double& v) {
+                                         c = __ldg(P.ci + k);
+                                         v = __ldg(P.val + k);
+                                     });
+            P.y[row] = y;
+            spmv_epilogue<MODE>(P, row, y, acc);
         }
     }
     if constexpr (ND > 0) {
@@ -443,6 +428,145 @@ __global__ void __launch_bounds__(kSpmvThreads, 2) spmv_kernel(SpmvParams P) {
         block_tree<kSpmvThreads, ND>(acc, sred);
         publish_and_finish<kSpmvThreads, ND>(acc, chunk, P.red, sred);
     }
+}
+
+// Staged variant: persistent, warp-specialised.  Warp 8 (one elected lane) is the
+// producer: it walks this CTA's (chunk, round) sequence and streams each round's
+// row_ptr / col_idx / vals segment into a kStages-deep shared-memory ring with TMA bulk
+// copies (cp.async.bulk, L2 evict_first), signalling full[s] through the mbarrier
+// transaction count.  Warps 0-7 consume two rounds at a time (two rows per thread, all
+// x gathers of both rows in flight together), release the stages through empty[s]
+// (one arrive per warp), and never wait on a CTA-wide barrier inside the loop.
+constexpr int kConsumerWarps = 8;
+constexpr int kWsThreads = (kConsumerWarps + 1) * 32;
+
+struct StageLayout {
+    size_t vbytes, cbytes, rbytes, stage;
+    __host__ __device__ StageLayout(int cap_v, int cap_c) {
+        vbytes = ((size_t)cap_v * 8 + 127) & ~size_t(127);
+        cbytes = ((size_t)cap_c * 4 + 127) & ~size_t(127);
+        rbytes = (kRpCopy * 4 + 127) & ~size_t(127);
+        stage = vbytes + cbytes + rbytes;
+    }
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(kWsThreads, 2) spmv_ws_kernel(SpmvParams P) {
+    constexpr int ND = SpmvDots<MODE>::n;
+    constexpr int NA = ND > 0 ? ND : 1;
+    if (P.check_done && P.red.st->done) return;
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+    uint64_t* empty = full + kStages;
+    const StageLayout L(P.cap_v, P.cap_c);
+    unsigned char* stage0 = smem + 128;
+    const int t = threadIdx.x;
+    const int warp = t >> 5, lane = t & 31;
+    if (t == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kConsumerWarps);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    if (warp == kConsumerWarps) {  // ------------------------------- producer warp ----
+        if (lane == 0) {
+            const uint64_t pol = policy_evict_first();
+            long long g = 0;
+            for (long long c = blockIdx.x; c < P.nch; c += gridDim.x) {
+                const long long base = (P.chunk0 + c) * kChunk;
+                const long long rem = (P.n - base + kChunkSlots - 1) / kChunkSlots;
+                const int nr = rem < kChunkRounds ? (int)rem : kChunkRounds;
+                for (int r = 0; r < nr; ++r, ++g) {
+                    const int s = (int)(g % kStages);
+                    mbar_wait(&empty[s], (uint32_t)(((g / kStages) & 1) ^ 1));
+                    const long long rs = base + (long long)r * kChunkSlots;
+                    const long long re = min(rs + kChunkSlots, P.n);
+                    const int nz0 = __ldg(P.rp + rs), nz1 = __ldg(P.rp + re);
+                    const int a0 = nz0 & ~1, a1 = (nz1 + 1) & ~1;
+                    const int c0 = nz0 & ~3, c1 = (nz1 + 3) & ~3;
+                    const uint32_t vb = (uint32_t)(a1 - a0) * 8u, cb = (uint32_t)(c1 - c0) * 4u;
+                    unsigned char* st = stage0 + s * L.stage;
+                    mbar_arrive_expect_tx(&full[s], (uint32_t)(kRpCopy * 4) + vb + cb);
+                    bulk_g2s(st + L.vbytes + L.cbytes, P.rp + rs, kRpCopy * 4, &full[s], pol);
+                    if (vb) bulk_g2s(st, P.val + a0, vb, &full[s], pol);
+                    if (cb) bulk_g2s(st + L.vbytes, P.ci + c0, cb, &full[s], pol);
+                }
+            }
+        }
+        return;
+    }
+
+    // ------------------------------------------------------------------ consumers ----
+    __shared__ double sred[NA * kConsumerWarps];
+    __shared__ int s_flag;
+    long long g = 0;
+    for (long long c = blockIdx.x; c < P.nch; c += gridDim.x) {
+        const long long chunk = P.chunk0 + c;
+        const long long base = chunk * kChunk;
+        const long long rem = (P.n - base + kChunkSlots - 1) / kChunkSlots;
+        const int nr = rem < kChunkRounds ? (int)rem : kChunkRounds;
+        double acc[NA];
+#pragma unroll
+        for (int d = 0; d < NA; ++d) acc[d] = 0.0;
+        for (int r = 0; r < nr; r += 2) {
+            const bool two = r + 1 < nr;
+            const int s0 = (int)(g % kStages), s1 = (int)((g + 1) % kStages);
+            mbar_wait(&full[s0], (uint32_t)((g / kStages) & 1));
+            if (two) mbar_wait(&full[s1], (uint32_t)(((g + 1) / kStages) & 1));
+            const unsigned char* A = stage0 + s0 * L.stage;
+            const unsigned char* B = stage0 + s1 * L.stage;
+            const int32_t* rpa = reinterpret_cast<const int32_t*>(A + L.vbytes + L.cbytes);
+            const int32_t* rpb = reinterpret_cast<const int32_t*>(B + L.vbytes + L.cbytes);
+            const double* va = reinterpret_cast<const double*>(A);
+            const double* vb = reinterpret_cast<const double*>(B);
+            const int32_t* ca = reinterpret_cast<const int32_t*>(A + L.vbytes);
+            const int32_t* cb = reinterpret_cast<const int32_t*>(B + L.vbytes);
+            const long long rowa = base + (long long)r * kChunkSlots + t;
+            const long long rowb = rowa + kChunkSlots;
+            const bool ha = rowa < P.n, hb = two && rowb < P.n;
+            int ka = 0, kea = 0, kb = 0, keb = 0;
+            int oa_v = 0, oa_c = 0, ob_v = 0, ob_c = 0;
+            if (ha) { ka = rpa[t]; kea = rpa[t + 1]; oa_v = rpa[0] & ~1; oa_c = rpa[0] & ~3; }
+            if (hb) { kb = rpb[t]; keb = rpb[t + 1]; ob_v = rpb[0] & ~1; ob_c = rpb[0] & ~3; }
+            double ya = 0.0, yb = 0.0;
+            while (ka < kea || kb < keb) {
+                double pa[8], pb[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (ka + u < kea) pa[u] = __dmul_rn(va[ka + u - oa_v], __ldg(P.x + ca[ka + u - oa_c]));
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (kb + u < keb) pb[u] = __dmul_rn(vb[kb + u - ob_v], __ldg(P.x + cb[kb + u - ob_c]));
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (ka + u < kea) ya = __dadd_rn(ya, pa[u]);
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (kb + u < keb) yb = __dadd_rn(yb, pb[u]);
+                ka += 8;
+                kb += 8;
+            }
+            __syncwarp();
+            if (lane == 0) {  // stage contents fully read by this warp
+                mbar_arrive(&empty[s0]);
+                if (two) mbar_arrive(&empty[s1]);
+            }
+            if (ha) { P.y[rowa] = ya; spmv_epilogue<MODE>(P, rowa, ya, acc); }
+            if (hb) { P.y[rowb] = yb; spmv_epilogue<MODE>(P, rowb, yb, acc); }
+            g += two ? 2 : 1;
+        }
+        if constexpr (ND > 0) {
+            block_tree<kConsumerWarps * 32, ND, 1>(acc, sred);
+            if (t == 0) {
+#pragma unroll
+                for (int d = 0; d < ND; ++d) P.red.partials[d * P.red.nchunks + chunk] = acc[d];
+            }
+        }
+    }
+    if constexpr (ND > 0) ticket_and_finish<kConsumerWarps * 32, ND, 1>(P.red, sred, &s_flag);
 }
 
 // -------------------------------------------------------------- vector kernels -------

@@ -497,6 +497,13 @@ class Solver:
         _check(lib().sparsla_solver_stream(self.h, C.byref(s)))
         return s.value or 0
 
+    def kernel_times(self, iters: int) -> list:
+        """Average duration (ms) of each kernel of an iteration, CUDA events per kernel."""
+        L = self.launches_per_iteration()
+        out = np.zeros(L)
+        _check(lib().sparsla_solver_kernel_times(self.h, C.c_int64(iters), _p(out, _f64p)))
+        return list(out)
+
     def launches_per_iteration(self) -> int:
         n = C.c_int64()
         _check(lib().sparsla_solver_launches_per_iteration(self.h, C.byref(n)))
