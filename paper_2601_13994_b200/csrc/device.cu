@@ -50,6 +50,50 @@ T* dalloc(size_t count) {
 static inline unsigned grid_for(long long n, int per) { return (unsigned)((n + per - 1) / per); }
 static inline long long nchunks_of(long long n) { return (n + kChunk - 1) / kChunk; }
 
+// Staged SpMV variants (RPT rows in flight per thread, STG-deep ring, MINB CTAs/SM).
+// Variant 0 is the default; SPARSLA_WS_VARIANT selects another for sweeps.
+struct WsVariant {
+    int rpt, stg, minb;
+    const void* fn[4];  // per SpmvMode
+};
+#define WSV(R, S, M, E)                                                                           \
+    {R, S, M, {(const void*)spmv_ws_kernel<SPMV_PLAIN, R, S, M, E>, (const void*)spmv_ws_kernel<SPMV_CG, R, S, M, E>, \
+               (const void*)spmv_ws_kernel<SPMV_BICG_V, R, S, M, E>, (const void*)spmv_ws_kernel<SPMV_BICG_T, R, S, M, E>}}
+#define WPV(D, M)                                                                                 \
+    {0, D, M, {(const void*)spmv_wp_kernel<SPMV_PLAIN, D, M>, (const void*)spmv_wp_kernel<SPMV_CG, D, M>,  \
+               (const void*)spmv_wp_kernel<SPMV_BICG_V, D, M>, (const void*)spmv_wp_kernel<SPMV_BICG_T, D, M>}}
+// rpt == 0 marks the warp-pipelined kernel (stg = per-warp ring depth)
+// Measured on B200 (tools/spmv_sweep.py, profiles/r01_spmv_sweep.md): variant 0 is the
+// fastest on both the 7-point stencil (6.2 TB/s) and the P1 FEM matrix (5.4 TB/s).
+static const WsVariant kWsVariants[] = {WSV(1, 3, 3, true), WSV(1, 4, 2, true), WSV(1, 4, 2, false),
+                                        WSV(2, 4, 2, false), WPV(2, 3)};
+#undef WSV
+#undef WPV
+constexpr int kNumWsVariants = sizeof(kWsVariants) / sizeof(kWsVariants[0]);
+
+static int ws_variant() {
+    static int v = [] {
+        const char* e = getenv("SPARSLA_WS_VARIANT");
+        int x = e ? atoi(e) : 0;
+        return (x >= 0 && x < kNumWsVariants) ? x : 0;
+    }();
+    return v;
+}
+
+size_t ws_smem_bytes(const DevCsr* A, int variant) {
+    const WsVariant& V = kWsVariants[variant];
+    if (V.rpt == 0) return 1024 + (size_t)(kSpmvThreads / 32) * V.stg * WarpStage(A->cap_v32, A->cap_c32).stage;
+    return 256 + (size_t)V.stg * StageLayout(A->cap_v, A->cap_c).stage;
+}
+
+static void configure_ws_variants(int device) {
+    for (int v = 0; v < kNumWsVariants; ++v)
+        for (int m = 0; m < 4; ++m)
+            CK(cudaFuncSetAttribute(kWsVariants[v].fn[m], cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    (void)device;
+}
+
+
 // ------------------------------------------------------------------ DevCsr ---------
 DevCsr::~DevCsr() {
     DeviceGuard g(device);
@@ -63,11 +107,7 @@ static void configure_kernels_once(int device) {
     static std::vector<int> done;
     std::lock_guard<std::mutex> lk(mu);
     if (std::find(done.begin(), done.end(), device) != done.end()) return;
-    const int max_smem = 160 * 1024;  // staged variant is chosen only up to 110 KB
-    CK(cudaFuncSetAttribute(spmv_ws_kernel<SPMV_PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
-    CK(cudaFuncSetAttribute(spmv_ws_kernel<SPMV_CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
-    CK(cudaFuncSetAttribute(spmv_ws_kernel<SPMV_BICG_V>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
-    CK(cudaFuncSetAttribute(spmv_ws_kernel<SPMV_BICG_T>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
+    configure_ws_variants(device);
     done.push_back(device);
 }
 
@@ -112,19 +152,34 @@ DevCsr* DevCsr::create(int device, long long nrows, long long ncols, const I* h_
         mb = std::max<long long>(mb, (long long)h_rp[e] - (long long)h_rp[b]);
     }
     for (long long i = 0; i < nrows; ++i) mr = std::max<long long>(mr, (long long)h_rp[i + 1] - (long long)h_rp[i]);
+    long long mb32 = 0;
+    for (long long b = 0; b < nrows; b += 32) {
+        const long long e = std::min(b + 32, nrows);
+        mb32 = std::max<long long>(mb32, (long long)h_rp[e] - (long long)h_rp[b]);
+    }
+    A->cap_v32 = (int)(((mb32 + 2) + 1) & ~1LL);
+    A->cap_c32 = (int)(((mb32 + 6) + 3) & ~3LL);
     A->max_block_nnz = mb;
     A->max_row = mr;
     A->cap_v = (int)(((mb + 2) + 1) & ~1LL);
     A->cap_c = (int)(((mb + 6) + 3) & ~3LL);
-    const StageLayout SL(A->cap_v, A->cap_c);
-    A->smem_bytes = 128 + kStages * SL.stage;
-    A->staged = A->smem_bytes <= 110 * 1024;
+    A->smem_bytes = ws_smem_bytes(A.get(), ws_variant());
+    A->staged = A->smem_bytes <= 200 * 1024;
     {
-        int sms = 0, per_sm = 0;
+        size_t smax = 0;
+        for (int v = 0; v < kNumWsVariants; ++v) smax = std::max(smax, ws_smem_bytes(A.get(), v));
+        if (smax > 200 * 1024) A->staged = false;  // keep every variant launchable
+    }
+    {
+        int sms = 0;
         CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, spmv_ws_kernel<SPMV_CG>, kWsThreads,
-                                                         A->smem_bytes));
-        A->ws_ctas = sms * std::max(1, per_sm);
+        for (int v = 0; v < kNumWsVariants; ++v) {
+            int per_sm = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                &per_sm, kWsVariants[v].fn[SPMV_CG], kWsVariants[v].rpt == 0 ? kSpmvThreads : kWsThreads,
+                ws_smem_bytes(A.get(), v)));
+            A->ws_ctas[v] = sms * std::max(1, per_sm);
+        }
     }
     CK(cudaDeviceSynchronize());
     return A.release();
@@ -212,16 +267,14 @@ void launch_spmv(DevCsr* A, cudaStream_t s, int mode, const double* x, double* y
     P.red = red;
     P.red.nchunks = nchunks_of(A->nrows);
     if (A->staged) {
-        const unsigned grid = (unsigned)std::min<long long>(P.nch, (long long)A->ws_ctas);
+        const int v = ws_variant();
+        const unsigned grid = (unsigned)std::min<long long>(P.nch, (long long)A->ws_ctas[v]);
         P.red.expected = grid;
-#define WS_CASE(M) spmv_ws_kernel<M><<<grid, kWsThreads, A->smem_bytes, s>>>(P);
-        switch (mode) {
-            case SPMV_PLAIN: WS_CASE(SPMV_PLAIN) break;
-            case SPMV_CG: WS_CASE(SPMV_CG) break;
-            case SPMV_BICG_V: WS_CASE(SPMV_BICG_V) break;
-            case SPMV_BICG_T: WS_CASE(SPMV_BICG_T) break;
-        }
-#undef WS_CASE
+        const bool wp = kWsVariants[v].rpt == 0;
+        if (wp) { P.cap_v = A->cap_v32; P.cap_c = A->cap_c32; }
+        void* args[] = {&P};
+        CK(cudaLaunchKernel(kWsVariants[v].fn[mode], dim3(grid), dim3(wp ? kSpmvThreads : kWsThreads), args,
+                            ws_smem_bytes(A, v), s));
     } else {
         const unsigned grid = (unsigned)P.nch;
         P.red.expected = grid;

@@ -26,10 +26,11 @@ struct DevCsr {
     int32_t* ci = nullptr;
     double* val = nullptr;
     long long max_block_nnz = 0, max_row = 0;
-    int cap_v = 0, cap_c = 0;
+    int cap_v = 0, cap_c = 0;      // per 256-row round (+alignment slack)
+    int cap_v32 = 0, cap_c32 = 0;  // per 32-row warp segment
     size_t smem_bytes = 0;
     bool staged = true;
-    int ws_ctas = 0;  // persistent grid of the staged SpMV (SMs x resident CTAs)
+    int ws_ctas[8] = {0};  // persistent grid per staged-SpMV variant (SMs x resident CTAs)
     double* dinv = nullptr;
     double* ones = nullptr;
     int sym_checked = -1;

@@ -450,20 +450,22 @@ struct StageLayout {
     }
 };
 
-template <int MODE>
-__global__ void __launch_bounds__(kWsThreads, 2) spmv_ws_kernel(SpmvParams P) {
+// RPT: rounds (= rows per consumer thread) in flight together; STG: ring depth;
+// MINB: resident CTAs per SM requested from ptxas (register budget).
+template <int MODE, int RPT, int STG, int MINB, bool EARLY>
+__global__ void __launch_bounds__(kWsThreads, MINB) spmv_ws_kernel(SpmvParams P) {
     constexpr int ND = SpmvDots<MODE>::n;
     constexpr int NA = ND > 0 ? ND : 1;
     if (P.check_done && P.red.st->done) return;
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);
-    uint64_t* empty = full + kStages;
+    uint64_t* empty = full + STG;
     const StageLayout L(P.cap_v, P.cap_c);
-    unsigned char* stage0 = smem + 128;
+    unsigned char* stage0 = smem + 256;
     const int t = threadIdx.x;
     const int warp = t >> 5, lane = t & 31;
     if (t == 0) {
-        for (int s = 0; s < kStages; ++s) {
+        for (int s = 0; s < STG; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], kConsumerWarps);
         }
@@ -480,8 +482,8 @@ __global__ void __launch_bounds__(kWsThreads, 2) spmv_ws_kernel(SpmvParams P) {
                 const long long rem = (P.n - base + kChunkSlots - 1) / kChunkSlots;
                 const int nr = rem < kChunkRounds ? (int)rem : kChunkRounds;
                 for (int r = 0; r < nr; ++r, ++g) {
-                    const int s = (int)(g % kStages);
-                    mbar_wait(&empty[s], (uint32_t)(((g / kStages) & 1) ^ 1));
+                    const int s = (int)(g % STG);
+                    mbar_wait(&empty[s], (uint32_t)(((g / STG) & 1) ^ 1));
                     const long long rs = base + (long long)r * kChunkSlots;
                     const long long re = min(rs + kChunkSlots, P.n);
                     const int nz0 = __ldg(P.rp + rs), nz1 = __ldg(P.rp + re);
@@ -511,52 +513,122 @@ __global__ void __launch_bounds__(kWsThreads, 2) spmv_ws_kernel(SpmvParams P) {
         double acc[NA];
 #pragma unroll
         for (int d = 0; d < NA; ++d) acc[d] = 0.0;
-        for (int r = 0; r < nr; r += 2) {
-            const bool two = r + 1 < nr;
-            const int s0 = (int)(g % kStages), s1 = (int)((g + 1) % kStages);
-            mbar_wait(&full[s0], (uint32_t)((g / kStages) & 1));
-            if (two) mbar_wait(&full[s1], (uint32_t)(((g + 1) / kStages) & 1));
-            const unsigned char* A = stage0 + s0 * L.stage;
-            const unsigned char* B = stage0 + s1 * L.stage;
-            const int32_t* rpa = reinterpret_cast<const int32_t*>(A + L.vbytes + L.cbytes);
-            const int32_t* rpb = reinterpret_cast<const int32_t*>(B + L.vbytes + L.cbytes);
-            const double* va = reinterpret_cast<const double*>(A);
-            const double* vb = reinterpret_cast<const double*>(B);
-            const int32_t* ca = reinterpret_cast<const int32_t*>(A + L.vbytes);
-            const int32_t* cb = reinterpret_cast<const int32_t*>(B + L.vbytes);
-            const long long rowa = base + (long long)r * kChunkSlots + t;
-            const long long rowb = rowa + kChunkSlots;
-            const bool ha = rowa < P.n, hb = two && rowb < P.n;
-            int ka = 0, kea = 0, kb = 0, keb = 0;
-            int oa_v = 0, oa_c = 0, ob_v = 0, ob_c = 0;
-            if (ha) { ka = rpa[t]; kea = rpa[t + 1]; oa_v = rpa[0] & ~1; oa_c = rpa[0] & ~3; }
-            if (hb) { kb = rpb[t]; keb = rpb[t + 1]; ob_v = rpb[0] & ~1; ob_c = rpb[0] & ~3; }
-            double ya = 0.0, yb = 0.0;
-            while (ka < kea || kb < keb) {
-                double pa[8], pb[8];
+        for (int r = 0; r < nr; r += RPT) {
+            const int cnt = nr - r < RPT ? nr - r : RPT;
+            int k[RPT], ke[RPT], ov[RPT], oc[RPT];
+            const double* vs[RPT];
+            const int32_t* cs[RPT];
+            double y[RPT];
 #pragma unroll
-                for (int u = 0; u < 8; ++u)
-                    if (ka + u < kea) pa[u] = __dmul_rn(va[ka + u - oa_v], __ldg(P.x + ca[ka + u - oa_c]));
+            for (int j = 0; j < RPT; ++j) {
+                k[j] = 0; ke[j] = 0; ov[j] = 0; oc[j] = 0; y[j] = 0.0;
+                const int s = (int)((g + j) % STG);
+                const unsigned char* A = stage0 + s * L.stage;
+                vs[j] = reinterpret_cast<const double*>(A);
+                cs[j] = reinterpret_cast<const int32_t*>(A + L.vbytes);
+                if (j < cnt) {
+                    mbar_wait(&full[s], (uint32_t)(((g + j) / STG) & 1));
+                    const long long row = base + (long long)(r + j) * kChunkSlots + t;
+                    if (row < P.n) {
+                        const int32_t* rps = reinterpret_cast<const int32_t*>(A + L.vbytes + L.cbytes);
+                        k[j] = rps[t]; ke[j] = rps[t + 1];
+                        ov[j] = rps[0] & ~1; oc[j] = rps[0] & ~3;
+                    }
+                }
+            }
+            if constexpr (EARLY) {
+                // Copy the first 8 entries of every row to registers and release the stages
+                // before the x gathers: the ring is held only for one shared-memory read.
+                int cc[RPT][8];
+                double vv[RPT][8];
+                bool fits = true;
 #pragma unroll
-                for (int u = 0; u < 8; ++u)
-                    if (kb + u < keb) pb[u] = __dmul_rn(vb[kb + u - ob_v], __ldg(P.x + cb[kb + u - ob_c]));
+                for (int j = 0; j < RPT; ++j) {
 #pragma unroll
-                for (int u = 0; u < 8; ++u)
-                    if (ka + u < kea) ya = __dadd_rn(ya, pa[u]);
+                    for (int u = 0; u < 8; ++u) {
+                        if (k[j] + u < ke[j]) { cc[j][u] = cs[j][k[j] + u - oc[j]]; vv[j][u] = vs[j][k[j] + u - ov[j]]; }
+                    }
+                    fits &= ke[j] - k[j] <= 8;
+                }
+                fits = __all_sync(0xffffffffu, fits);
+                if (fits) {
+                    __syncwarp();
+                    if (lane == 0) {
 #pragma unroll
-                for (int u = 0; u < 8; ++u)
-                    if (kb + u < keb) yb = __dadd_rn(yb, pb[u]);
-                ka += 8;
-                kb += 8;
+                        for (int j = 0; j < RPT; ++j)
+                            if (j < cnt) mbar_arrive(&empty[(g + j) % STG]);
+                    }
+                }
+                double pr[RPT][8];
+#pragma unroll
+                for (int j = 0; j < RPT; ++j)
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        if (k[j] + u < ke[j]) pr[j][u] = __dmul_rn(vv[j][u], __ldg(P.x + cc[j][u]));
+#pragma unroll
+                for (int j = 0; j < RPT; ++j)
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        if (k[j] + u < ke[j]) y[j] = __dadd_rn(y[j], pr[j][u]);
+                if (!fits) {  // long rows: finish from the (still held) stages, then release
+                    bool more = false;
+#pragma unroll
+                    for (int j = 0; j < RPT; ++j) { k[j] += 8; more |= k[j] < ke[j]; }
+                    while (more) {
+#pragma unroll
+                        for (int j = 0; j < RPT; ++j)
+#pragma unroll
+                            for (int u = 0; u < 8; ++u)
+                                if (k[j] + u < ke[j])
+                                    pr[j][u] = __dmul_rn(vs[j][k[j] + u - ov[j]], __ldg(P.x + cs[j][k[j] + u - oc[j]]));
+#pragma unroll
+                        for (int j = 0; j < RPT; ++j)
+#pragma unroll
+                            for (int u = 0; u < 8; ++u)
+                                if (k[j] + u < ke[j]) y[j] = __dadd_rn(y[j], pr[j][u]);
+                        more = false;
+#pragma unroll
+                        for (int j = 0; j < RPT; ++j) { k[j] += 8; more |= k[j] < ke[j]; }
+                    }
+                    __syncwarp();
+                    if (lane == 0) {
+#pragma unroll
+                        for (int j = 0; j < RPT; ++j)
+                            if (j < cnt) mbar_arrive(&empty[(g + j) % STG]);
+                    }
+                }
+            } else {
+            bool more = true;
+            while (more) {
+                double pr[RPT][8];
+#pragma unroll
+                for (int j = 0; j < RPT; ++j)
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        if (k[j] + u < ke[j])
+                            pr[j][u] = __dmul_rn(vs[j][k[j] + u - ov[j]], __ldg(P.x + cs[j][k[j] + u - oc[j]]));
+#pragma unroll
+                for (int j = 0; j < RPT; ++j)
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        if (k[j] + u < ke[j]) y[j] = __dadd_rn(y[j], pr[j][u]);
+                more = false;
+#pragma unroll
+                for (int j = 0; j < RPT; ++j) { k[j] += 8; more |= k[j] < ke[j]; }
             }
             __syncwarp();
             if (lane == 0) {  // stage contents fully read by this warp
-                mbar_arrive(&empty[s0]);
-                if (two) mbar_arrive(&empty[s1]);
+#pragma unroll
+                for (int j = 0; j < RPT; ++j)
+                    if (j < cnt) mbar_arrive(&empty[(g + j) % STG]);
             }
-            if (ha) { P.y[rowa] = ya; spmv_epilogue<MODE>(P, rowa, ya, acc); }
-            if (hb) { P.y[rowb] = yb; spmv_epilogue<MODE>(P, rowb, yb, acc); }
-            g += two ? 2 : 1;
+            }
+#pragma unroll
+            for (int j = 0; j < RPT; ++j) {
+                const long long row = base + (long long)(r + j) * kChunkSlots + t;
+                if (j < cnt && row < P.n) { P.y[row] = y[j]; spmv_epilogue<MODE>(P, row, y[j], acc); }
+            }
+            g += cnt;
         }
         if constexpr (ND > 0) {
             block_tree<kConsumerWarps * 32, ND, 1>(acc, sred);
@@ -567,6 +639,140 @@ __global__ void __launch_bounds__(kWsThreads, 2) spmv_ws_kernel(SpmvParams P) {
         }
     }
     if constexpr (ND > 0) ticket_and_finish<kConsumerWarps * 32, ND, 1>(P.red, sred, &s_flag);
+}
+
+// Warp-pipelined staged variant (persistent, no producer/consumer hand-off).  Each warp
+// owns slots [32w, 32w+32) of every round, so it streams its own 32-row segments
+// (row_ptr, col_idx, vals) through a private D-deep shared-memory ring with TMA bulk
+// copies; lane 0 re-arms a stage right after the warp has read it.  Only 3 KB of shared
+// memory is held per segment being consumed, so almost all of it is in flight.  Segment
+// boundaries (row_ptr at the segment ends) are prefetched one issue ahead so the
+// issuing lane never stalls on a dependent global load.
+struct WarpStage {
+    int vbytes, cbytes, stage;
+    __host__ __device__ WarpStage(int cap_v, int cap_c) {
+        vbytes = (cap_v * 8 + 127) & ~127;
+        cbytes = (cap_c * 4 + 127) & ~127;
+        stage = vbytes + cbytes + 256;  // + row_ptr[36]
+    }
+};
+constexpr int kWarpRp = 36;
+
+template <int MODE, int D, int MINB>
+__global__ void __launch_bounds__(kSpmvThreads, MINB) spmv_wp_kernel(SpmvParams P) {
+    constexpr int ND = SpmvDots<MODE>::n;
+    constexpr int NA = ND > 0 ? ND : 1;
+    constexpr int NW = kSpmvThreads / 32;
+    if (P.check_done && P.red.st->done) return;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const WarpStage L(P.cap_v, P.cap_c);
+    const int t = threadIdx.x, w = t >> 5, lane = t & 31;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem) + w * D;
+    unsigned char* ring = smem + 1024 + (size_t)w * D * L.stage;
+    __shared__ double sred[NA * NW];
+    __shared__ int s_flag;
+    if (lane == 0) {
+        for (int s = 0; s < D; ++s) mbar_init(&bars[s], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    // issue iterator over this CTA's (chunk, round) sequence
+    long long ic = blockIdx.x;
+    int ir = 0;
+    auto nrounds = [&](long long c) {
+        const long long base = (P.chunk0 + c) * kChunk;
+        const long long rem = (P.n - base + kChunkSlots - 1) / kChunkSlots;
+        return rem < kChunkRounds ? (int)rem : kChunkRounds;
+    };
+    // segment row range for (c, r) of this warp
+    auto seg = [&](long long c, int r, long long& rs, long long& re) {
+        rs = (P.chunk0 + c) * kChunk + (long long)r * kChunkSlots + 32 * w;
+        re = min(rs + 32, P.n);
+    };
+    uint64_t pol = 0;
+    int nz0n = 0, nz1n = 0;  // prefetched boundaries of the next segment to issue
+    bool have_next = ic < P.nch;
+    if (lane == 0) {
+        pol = policy_evict_first();
+        if (have_next) {
+            long long rs, re;
+            seg(ic, ir, rs, re);
+            if (rs < re) { nz0n = __ldg(P.rp + rs); nz1n = __ldg(P.rp + re); }
+        }
+    }
+    long long issued = 0;
+    auto issue_next = [&]() {  // lane 0 only
+        if (!have_next) return;
+        const int s = (int)(issued % D);
+        long long rs, re;
+        seg(ic, ir, rs, re);
+        unsigned char* st = ring + s * L.stage;
+        if (rs < re) {
+            const int nz0 = nz0n, nz1 = nz1n;
+            const int a0 = nz0 & ~1, a1 = (nz1 + 1) & ~1;
+            const int c0 = nz0 & ~3, c1 = (nz1 + 3) & ~3;
+            const uint32_t vb = (uint32_t)(a1 - a0) * 8u, cb = (uint32_t)(c1 - c0) * 4u;
+            mbar_arrive_expect_tx(&bars[s], (uint32_t)(kWarpRp * 4) + vb + cb);
+            bulk_g2s(st + L.vbytes + L.cbytes, P.rp + rs, kWarpRp * 4, &bars[s], pol);
+            if (vb) bulk_g2s(st, P.val + a0, vb, &bars[s], pol);
+            if (cb) bulk_g2s(st + L.vbytes, P.ci + c0, cb, &bars[s], pol);
+        } else {
+            mbar_arrive_expect_tx(&bars[s], 0);  // empty segment (tail): complete the phase
+        }
+        ++issued;
+        if (++ir >= nrounds(ic)) { ir = 0; ic += gridDim.x; }
+        have_next = ic < P.nch;
+        if (have_next) {  // prefetch the following segment's boundaries
+            seg(ic, ir, rs, re);
+            if (rs < re) { nz0n = __ldg(P.rp + rs); nz1n = __ldg(P.rp + re); }
+        }
+    };
+    if (lane == 0)
+        for (int s = 0; s < D; ++s) issue_next();
+
+    long long g = 0;
+    for (long long c = blockIdx.x; c < P.nch; c += gridDim.x) {
+        const long long chunk = P.chunk0 + c;
+        const long long base = chunk * kChunk;
+        const int nr = nrounds(c);
+        double acc[NA];
+#pragma unroll
+        for (int d = 0; d < NA; ++d) acc[d] = 0.0;
+        for (int r = 0; r < nr; ++r, ++g) {
+            const int s = (int)(g % D);
+            mbar_wait(&bars[s], (uint32_t)((g / D) & 1));
+            const unsigned char* st = ring + s * L.stage;
+            const int32_t* rps = reinterpret_cast<const int32_t*>(st + L.vbytes + L.cbytes);
+            const double* vs = reinterpret_cast<const double*>(st);
+            const int32_t* cs = reinterpret_cast<const int32_t*>(st + L.vbytes);
+            const long long row = base + (long long)r * kChunkSlots + t;
+            double y = 0.0;
+            if (row < P.n) {
+                const int ov = rps[0] & ~1, oc = rps[0] & ~3;
+                y = row_sum(rps[lane], rps[lane + 1], P.x, [&](int k, int& cc, double& v) {
+                    cc = cs[k - oc];
+                    v = vs[k - ov];
+                });
+            }
+            __syncwarp();
+            if (lane == 0) {
+                fence_proxy_async_smem();
+                issue_next();
+            }
+            if (row < P.n) {
+                P.y[row] = y;
+                spmv_epilogue<MODE>(P, row, y, acc);
+            }
+        }
+        if constexpr (ND > 0) {
+            block_tree<kSpmvThreads, ND, 1>(acc, sred);
+            if (t == 0) {
+#pragma unroll
+                for (int d = 0; d < ND; ++d) P.red.partials[d * P.red.nchunks + chunk] = acc[d];
+            }
+        }
+    }
+    if constexpr (ND > 0) ticket_and_finish<kSpmvThreads, ND, 1>(P.red, sred, &s_flag);
 }
 
 // -------------------------------------------------------------- vector kernels -------
