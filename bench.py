@@ -170,7 +170,7 @@ def run_ours(args):
     from paper_2601_13994_b200 import sparsla as S
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    if world > 1 or args.gpus > 1:
+    if world > 1 or args.gpus > 1 or args.dist:
         from paper_2601_13994_b200 import dist_bench
         return dist_bench.run(args, METRIC)
     dev = 0
@@ -307,6 +307,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--kernel-iters", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dist", action="store_true", help="force the NCCL distributed path (also at N=1)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -117,7 +117,8 @@ int sparsla_partition_rcb(int64_t n, const double* xs, const double* ys, int32_t
                           int32_t* part_of);
 
 /* build_local for a structurally symmetric pattern, from this rank's
- * owned rows only.  Inputs: part_of[n_global], the owned rows (ascending global ids) as a
+ * owned rows only.  Inputs: part_of[n_global] (NULL = contiguous partition
+ * partition_contiguous(n_global, nparts)), the owned rows (ascending global ids) as a
  * CSR with GLOBAL column ids.  The result handle exposes the SPEC-layout maps:
  *   owned (ascending global), halo (ascending global), neighbors (ascending rank),
  *   send_ptr/send_idx, recv_ptr/recv_idx (local positions in [owned | halo], canonical
@@ -203,6 +204,52 @@ int sparsla_solver_kernel_times(sparsla_solver* S, int64_t iters, double* ms);
 int sparsla_solver_destroy(sparsla_solver* S);
 /* time `reps` SpMV launches on the handle stream, returns avg ms per launch */
 int sparsla_spmv_bench(sparsla_dcsr* A, int32_t reps, double* ms_per_launch);
+
+/* ===================== distributed (row partition, 1..8 GPUs) ======================= */
+/* One handle per rank.  All calls below are collective over the ranks of the handle.
+ * NCCL backing: one rank per GPU (one process per GPU, e.g. torchrun); the 128-byte id
+ * comes from sparsla_nccl_unique_id on rank 0 and is broadcast by the caller.
+ * Local backing: P ranks as threads of one process sharing a sparsla_local_hub (they may
+ * share one device) — the in-process-worker model of SPEC.md:529. */
+typedef struct sparsla_dist sparsla_dist;
+typedef struct sparsla_local_hub sparsla_local_hub;
+int sparsla_nccl_unique_id(unsigned char* id128);
+int sparsla_dist_create_nccl(int device, int nranks, int rank, const unsigned char* id128,
+                             const sparsla_local* L, sparsla_dist** out);
+int sparsla_local_hub_create(int nranks, sparsla_local_hub** out);
+int sparsla_local_hub_destroy(sparsla_local_hub* hub);
+int sparsla_dist_create_local(int device, sparsla_local_hub* hub, int rank, const sparsla_local* L,
+                              sparsla_dist** out);
+int sparsla_dist_destroy(sparsla_dist* D);
+/* info[0]=n_owned [1]=n_halo [2]=neighbors [3]=interior chunks [4]=boundary chunks [5]=P
+ * [6]=rank [7]=zero-copy halo segments [8]=n_global */
+int sparsla_dist_info(const sparsla_dist* D, int64_t* info);
+/* counters[0]=halo exchanges [1]=all_reduce points [2]=p2p messages performed by the live
+ * algorithm (SPEC.md:524 accounting); [3..5] = raw transport calls of the same kinds (they
+ * also include the no-op tail replayed after convergence).  6 entries. */
+int sparsla_dist_counters(const sparsla_dist* D, int64_t* counters);
+int sparsla_dist_reset_counters(sparsla_dist* D);
+/* dist_spmv */
+int sparsla_dist_spmv(sparsla_dist* D, const double* x_owned, double* y_owned, int32_t mem);
+/* dist_cg (Alg. 4) / distributed BiCGStab, SolveOptions as cg_solve */
+int sparsla_dist_cg_solve(sparsla_dist* D, const double* b_owned, double* x_owned,
+                          const sparsla_solve_options* opts, sparsla_solve_report* report,
+                          int32_t mem);
+int sparsla_dist_bicgstab_solve(sparsla_dist* D, const double* b_owned, double* x_owned,
+                                const sparsla_solve_options* opts, sparsla_solve_report* report,
+                                int32_t mem);
+/* dist_adjoint_solve; vals_t = A^T values in A's local entry order, or
+ * NULL when A is symmetric; grad_vals in the local entry order */
+int sparsla_dist_adjoint_backward(sparsla_dist* D, const double* x_owned, const double* grad_x_owned,
+                                  const double* vals_t, int32_t backend,
+                                  const sparsla_solve_options* opts, double* grad_b_owned,
+                                  double* grad_vals_local, sparsla_solve_report* report,
+                                  int32_t mem);
+/* gather_solution: x_global (host, n_global) written on rank 0 only */
+int sparsla_dist_gather(sparsla_dist* D, const double* x_owned, double* x_global, int32_t mem);
+/* persistent distributed solver (bench): use the sparsla_solver_* calls on the result */
+int sparsla_dist_solver_create(sparsla_dist* D, int32_t backend, const double* b_owned, int32_t mem,
+                               const sparsla_solve_options* opts, sparsla_solver** out);
 
 #ifdef __cplusplus
 }

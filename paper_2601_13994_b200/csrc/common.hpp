@@ -76,3 +76,11 @@ template <class I>
 void validate_csr(int64_t nrows, int64_t ncols, const I* rp, const I* ci);
 
 }  // namespace sparsla_b200
+
+// build_local result (host, SPEC.md:433-436 layout)
+struct sparsla_local {
+    std::vector<int64_t> owned, halo;
+    std::vector<int32_t> neighbors;
+    std::vector<int64_t> send_ptr, send_idx, recv_ptr, recv_idx, rp, ci;
+    std::vector<double> v;
+};

@@ -20,6 +20,7 @@
 #include "common.hpp"
 #include "device.hpp"
 #include "kernels.cuh"
+#include "transport.hpp"
 
 namespace sparsla_b200 {
 
@@ -113,9 +114,11 @@ static void configure_kernels_once(int device) {
 
 template <class I>
 DevCsr* DevCsr::create(int device, long long nrows, long long ncols, const I* h_rp, const I* h_ci,
-                       const double* h_val) {
+                       const double* h_val, bool local_layout) {
     if (nrows < 0 || ncols < 0) fail(SPARSLA_ERR_DIMENSION, "negative matrix shape");
-    validate_csr<I>(nrows, ncols, h_rp, h_ci);
+    // rank-local matrices keep the global column order of every row, so their relabelled
+    // [owned|halo] column ids need not increase within a row
+    if (!local_layout) validate_csr<I>(nrows, ncols, h_rp, h_ci);
     const long long nnz = static_cast<long long>(h_rp[nrows]);
     if (nrows >= (1LL << 31) || ncols >= (1LL << 31) || nnz >= (1LL << 31))
         fail(SPARSLA_ERR_UNSUPPORTED,
@@ -125,6 +128,7 @@ DevCsr* DevCsr::create(int device, long long nrows, long long ncols, const I* h_
     configure_kernels_once(device);
     auto A = std::make_unique<DevCsr>();
     A->device = device;
+    A->local_layout = local_layout;
     A->nrows = nrows; A->ncols = ncols; A->nnz = nnz;
     CK(cudaStreamCreateWithFlags(&A->stream, cudaStreamNonBlocking));
     // int32 device layout (+ padding for the bulk-copy over-read)
@@ -184,13 +188,13 @@ DevCsr* DevCsr::create(int device, long long nrows, long long ncols, const I* h_
     CK(cudaDeviceSynchronize());
     return A.release();
 }
-template DevCsr* DevCsr::create<int64_t>(int, long long, long long, const int64_t*, const int64_t*, const double*);
-template DevCsr* DevCsr::create<int32_t>(int, long long, long long, const int32_t*, const int32_t*, const double*);
+template DevCsr* DevCsr::create<int64_t>(int, long long, long long, const int64_t*, const int64_t*, const double*, bool);
+template DevCsr* DevCsr::create<int32_t>(int, long long, long long, const int32_t*, const int32_t*, const double*, bool);
 
 const double* DevCsr::jacobi_dinv() {
     if (!dinv) {
         DeviceGuard g(device);
-        if (nrows != ncols) fail(SPARSLA_ERR_DIMENSION, "jacobi_build requires a square matrix");
+        if (nrows != ncols && !local_layout) fail(SPARSLA_ERR_DIMENSION, "jacobi_build requires a square matrix");
         dinv = dalloc<double>(nrows + 2);
         if (nrows > 0)
             jacobi_kernel<<<grid_for(nrows, 256), 256, 0, stream>>>(rp, ci, val, nrows, 0, dinv);
@@ -255,29 +259,37 @@ DevCsr* DevCsr::get_transpose() {
 }
 
 // ------------------------------------------------------------------ launches -------
-void launch_spmv(DevCsr* A, cudaStream_t s, int mode, const double* x, double* y, const double* aux,
-                 const RedParams& red, int check_done) {
-    if (A->nrows == 0) return;
+unsigned spmv_grid(const DevCsr* A, long long nch) {
+    if (nch <= 0) return 0;
+    if (A->staged) return (unsigned)std::min<long long>(nch, (long long)A->ws_ctas[ws_variant()]);
+    return (unsigned)nch;
+}
+
+// One SpMV launch over `nch` chunks (all chunks when list == nullptr).  `expected` is the
+// number of CTAs of every launch of this reduction point (interior + boundary).
+void launch_spmv_part(DevCsr* A, cudaStream_t s, int mode, const double* x, double* y, const double* aux,
+                      const RedParams& red, int check_done, const int32_t* list, long long nch,
+                      unsigned expected) {
+    const unsigned grid = spmv_grid(A, nch);
+    if (grid == 0) return;
     SpmvParams P{};
     P.rp = A->rp; P.ci = A->ci; P.val = A->val;
     P.x = x; P.y = y; P.n = A->nrows; P.chunk0 = 0; P.aux = aux;
-    P.nch = nchunks_of(A->nrows);
+    P.nch = nch;
+    P.chunk_list = list;
     P.cap_v = A->cap_v; P.cap_c = A->cap_c;
     P.check_done = check_done;
     P.red = red;
     P.red.nchunks = nchunks_of(A->nrows);
+    P.red.expected = expected;
     if (A->staged) {
         const int v = ws_variant();
-        const unsigned grid = (unsigned)std::min<long long>(P.nch, (long long)A->ws_ctas[v]);
-        P.red.expected = grid;
         const bool wp = kWsVariants[v].rpt == 0;
         if (wp) { P.cap_v = A->cap_v32; P.cap_c = A->cap_c32; }
         void* args[] = {&P};
         CK(cudaLaunchKernel(kWsVariants[v].fn[mode], dim3(grid), dim3(wp ? kSpmvThreads : kWsThreads), args,
                             ws_smem_bytes(A, v), s));
     } else {
-        const unsigned grid = (unsigned)P.nch;
-        P.red.expected = grid;
 #define DIRECT_CASE(M) spmv_direct_kernel<M><<<grid, kSpmvThreads, 0, s>>>(P);
         switch (mode) {
             case SPMV_PLAIN: DIRECT_CASE(SPMV_PLAIN) break;
@@ -288,6 +300,13 @@ void launch_spmv(DevCsr* A, cudaStream_t s, int mode, const double* x, double* y
 #undef DIRECT_CASE
     }
     CK(cudaGetLastError());
+}
+
+void launch_spmv(DevCsr* A, cudaStream_t s, int mode, const double* x, double* y, const double* aux,
+                 const RedParams& red, int check_done) {
+    if (A->nrows == 0) return;
+    const long long nch = nchunks_of(A->nrows);
+    launch_spmv_part(A, s, mode, x, y, aux, red, check_done, nullptr, nch, spmv_grid(A, nch));
 }
 
 template <int OP>
@@ -302,24 +321,26 @@ void launch_vec(cudaStream_t s, const VecParams& P0, RedParams red) {
 }
 
 // ------------------------------------------------------------------ Solver ---------
-Solver::Solver(DevCsr* A_, int backend_, const sparsla_solve_options& o) : A(A_), backend(backend_), opts(o) {
+Solver::Solver(DevCsr* A_, int backend_, const sparsla_solve_options& o, DistCtx* dist_)
+    : A(A_), backend(backend_), opts(o), dist(dist_) {
     if (!(o.atol >= 0.0) || !(o.rtol >= 0.0) || (o.atol == 0.0 && o.rtol == 0.0))
         fail(SPARSLA_ERR_INVALID_ARGUMENT, "SolveOptions: atol >= 0, rtol >= 0, not both zero (SPEC.md:129)");
     if (o.max_iter < 1) fail(SPARSLA_ERR_INVALID_ARGUMENT, "SolveOptions: max_iter >= 1");
     if (o.preconditioner != SPARSLA_PRECOND_NONE && o.preconditioner != SPARSLA_PRECOND_JACOBI)
         fail(SPARSLA_ERR_INVALID_ARGUMENT, "SolveOptions: unknown preconditioner");
-    if (A->nrows != A->ncols) fail(SPARSLA_ERR_DIMENSION, "Krylov solve requires a square matrix");
+    if (!dist && A->nrows != A->ncols) fail(SPARSLA_ERR_DIMENSION, "Krylov solve requires a square matrix");
     DeviceGuard g(A->device);
     n = A->nrows;
     stream = A->stream;
     dinv = o.preconditioner == SPARSLA_PRECOND_JACOBI ? A->jacobi_dinv() : A->ones_vec();
     const long long m = std::max<long long>(1, nchunks_of(n));
     const long long nv = n + 2;
+    const long long nh = (dist ? dist->n_halo : 0) + nv;  // SpMV inputs carry the halo slots
     x_own = dalloc<double>(nv); b_own = dalloc<double>(nv);
-    r = dalloc<double>(nv); p = dalloc<double>(nv); q = dalloc<double>(nv);
+    r = dalloc<double>(nv); p = dalloc<double>(nh); q = dalloc<double>(nv);
     if (backend == SPARSLA_BACKEND_BICGSTAB) {
-        rh = dalloc<double>(nv); ph = dalloc<double>(nv); s = dalloc<double>(nv);
-        sh = dalloc<double>(nv); t = dalloc<double>(nv);
+        rh = dalloc<double>(nv); ph = dalloc<double>(nh); s = dalloc<double>(nv);
+        sh = dalloc<double>(nh); t = dalloc<double>(nv);
     }
     partials = dalloc<double>(3 * m);
     tickets = dalloc<unsigned>(8);
@@ -356,6 +377,42 @@ VecParams Solver::vparams() const {
     return P;
 }
 
+// One SpMV reduction point: (distributed: halo exchange on the comm stream overlapped
+// with the interior-row SpMV, then the boundary rows, then the all-gather of the rank
+// totals and the rank-ordered scalar step) or a single launch.
+void Solver::spmv_point(int mode, double* xin, double* y, const double* aux, int scalar, int slot, int check_done) {
+    RedParams R = scalar == SC_NONE ? RedParams{} : red(scalar, slot);
+    const int nd = mode == SPMV_BICG_T ? 3 : (mode == SPMV_PLAIN ? 0 : 1);
+    if (!dist) {
+        launch_spmv(A, stream, mode, xin, y, aux, R, check_done);
+        return;
+    }
+    if (nd > 0) R.red_out = dist->red_send + slot * 8;
+    dist->exchange(stream, xin);
+    const unsigned gi = spmv_grid(A, dist->n_interior), gb = spmv_grid(A, dist->n_boundary);
+    launch_spmv_part(A, stream, mode, xin, y, aux, R, check_done, dist->d_interior, dist->n_interior, gi + gb);
+    CK(cudaStreamWaitEvent(stream, dist->ev_halo, 0));
+    launch_spmv_part(A, stream, mode, xin, y, aux, R, check_done, dist->d_boundary, dist->n_boundary, gi + gb);
+    if (nd > 0) reduce_point(scalar, slot, nd);
+}
+
+void Solver::reduce_point(int scalar, int slot, int nd) {
+    dist->tr->allgather(stream, dist->red_send + slot * 8, dist->red_all + (size_t)slot * dist->tr->P * 8, 8);
+    scalar_kernel<<<1, 32, 0, stream>>>(dist->red_all + (size_t)slot * dist->tr->P * 8, dist->tr->P, nd, scalar, st);
+    CK(cudaGetLastError());
+}
+
+template <int OP>
+void Solver::vec_point(int scalar, int slot, int check_done) {
+    VecParams P = vparams();
+    P.check_done = check_done;
+    RedParams R = red(scalar, slot);
+    constexpr int nd = VecTraits<OP>::ndot;
+    if (dist && nd > 0) R.red_out = dist->red_send + slot * 8;
+    launch_vec<OP>(stream, P, R);
+    if (dist && nd > 0) reduce_point(scalar, slot, nd);
+}
+
 void Solver::enqueue_init() {
     KState h{};
     h.atol = opts.atol; h.rtol = opts.rtol; h.max_iter = opts.max_iter;
@@ -364,17 +421,14 @@ void Solver::enqueue_init() {
     CK(cudaMemcpyAsync(st, h_st, sizeof(KState), cudaMemcpyHostToDevice, stream));
     CK(cudaMemsetAsync(tickets, 0, 8 * sizeof(unsigned), stream));
     CK(cudaMemsetAsync(x, 0, n * sizeof(double), stream));
-    RedParams none{};
-    VecParams P = vparams();
-    P.check_done = 0;
-    if (backend == SPARSLA_BACKEND_CG) {
-        launch_spmv(A, stream, SPMV_PLAIN, x, q, nullptr, none, 0);  // r0 = b - A x0
-        launch_vec<V_CG_INIT>(stream, P, red(SC_CG_INIT, 0));
-    } else {
-        launch_spmv(A, stream, SPMV_PLAIN, x, q, nullptr, none, 0);  // v = A x0
-        launch_vec<V_BI_INIT>(stream, P, red(SC_BI_INIT, 0));
-    }
-    if (n == 0) {  // empty system: converged with zero residual
+    // initial residual r0 = b - A x0 (one SpMV, spmv_count = 1); x0 = 0 lives in p's storage
+    // for the distributed case so the halo exchange has its slots
+    double* x0 = dist ? p : x;
+    if (dist) CK(cudaMemsetAsync(p, 0, (n + dist->n_halo) * sizeof(double), stream));
+    spmv_point(SPMV_PLAIN, x0, q, nullptr, SC_NONE, 0, 0);
+    if (backend == SPARSLA_BACKEND_CG) vec_point<V_CG_INIT>(SC_CG_INIT, 0, 0);
+    else vec_point<V_BI_INIT>(SC_BI_INIT, 0, 0);
+    if (n == 0 && !dist) {  // empty system: converged with zero residual
         KState z = h;
         z.converged = 1; z.status = ST_CONVERGED; z.done = 1;
         *h_st = z;
@@ -385,18 +439,17 @@ void Solver::enqueue_init() {
 void Solver::enqueue_iteration(cudaEvent_t* evs) {
     // evs (optional): launches_per_iteration()+1 events recorded around every kernel
     auto mark = [&](int i) { if (evs) CK(cudaEventRecord(evs[i], stream)); };
-    VecParams P = vparams();
     mark(0);
     if (backend == SPARSLA_BACKEND_CG) {
-        launch_spmv(A, stream, SPMV_CG, p, q, nullptr, red(SC_CG_PQ, 1), 1); mark(1);
-        launch_vec<V_CG_U1>(stream, P, red(SC_CG_RR, 2)); mark(2);
-        launch_vec<V_CG_U2>(stream, P, red(SC_NONE, 3)); mark(3);
+        spmv_point(SPMV_CG, p, q, nullptr, SC_CG_PQ, 1, 1); mark(1);
+        vec_point<V_CG_U1>(SC_CG_RR, 2, 1); mark(2);
+        vec_point<V_CG_U2>(SC_NONE, 3, 1); mark(3);
     } else {
-        launch_vec<V_BI_U1>(stream, P, red(SC_NONE, 1)); mark(1);
-        launch_spmv(A, stream, SPMV_BICG_V, ph, q, rh, red(SC_BI_RV, 2), 1); mark(2);
-        launch_vec<V_BI_U2>(stream, P, red(SC_NONE, 3)); mark(3);
-        launch_spmv(A, stream, SPMV_BICG_T, sh, t, s, red(SC_BI_T, 4), 1); mark(4);
-        launch_vec<V_BI_U3>(stream, P, red(SC_BI_U3, 5)); mark(5);
+        vec_point<V_BI_U1>(SC_NONE, 1, 1); mark(1);
+        spmv_point(SPMV_BICG_V, ph, q, rh, SC_BI_RV, 2, 1); mark(2);
+        vec_point<V_BI_U2>(SC_NONE, 3, 1); mark(3);
+        spmv_point(SPMV_BICG_T, sh, t, s, SC_BI_T, 4, 1); mark(4);
+        vec_point<V_BI_U3>(SC_BI_U3, 5, 1); mark(5);
     }
 }
 
@@ -420,7 +473,7 @@ void Solver::kernel_times(long long iters, double* ms) {
 long long Solver::launches_per_iteration() const { return backend == SPARSLA_BACKEND_CG ? 3 : 5; }
 
 void Solver::build_graphs() {
-    if (g_many) return;
+    if (g_many || !capturable()) return;
     auto capture = [&](int iters) {
         cudaGraph_t graph;
         CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
@@ -447,9 +500,15 @@ void Solver::reset() {
     enqueue_init();
 }
 
+bool Solver::capturable() const { return !dist || dist->tr->capturable(); }
+
 void Solver::iterate(long long iters) {
     DeviceGuard g(A->device);
     build_graphs();
+    if (!capturable()) {
+        while (iters-- > 0) enqueue_iteration();
+        return;
+    }
     while (iters >= kGraphIters) { CK(cudaGraphLaunch(g_many, stream)); iters -= kGraphIters; }
     while (iters-- > 0) CK(cudaGraphLaunch(g_one, stream));
 }
@@ -460,8 +519,11 @@ void Solver::run() {
     // Poll the device 'done' flag once per graph, one graph behind (no per-iteration sync).
     const long long max_graphs = opts.max_iter / kGraphIters + 3;
     h_flag[0] = h_flag[1] = 0;
+    // All ranks of a distributed solve see identical device flags (same all-gathered
+    // totals, same scalar step), so they stop after the same number of graph launches.
     for (long long i = 0; i < max_graphs; ++i) {
-        CK(cudaGraphLaunch(g_many, stream));
+        if (capturable()) CK(cudaGraphLaunch(g_many, stream));
+        else for (int k = 0; k < kGraphIters; ++k) enqueue_iteration();
         CK(cudaMemcpyAsync(h_flag + (i & 1), &st->done, sizeof(int), cudaMemcpyDeviceToHost, stream));
         CK(cudaEventRecord(ev[i & 1], stream));
         if (i > 0) {
@@ -551,7 +613,6 @@ double device_dot(int device, long long n, const double* a, const double* b, cud
 using namespace sparsla_b200;
 
 struct sparsla_dcsr { DevCsr* A; };
-struct sparsla_solver { Solver* S; double* x_user; int x_mem; };
 
 namespace {
 // host/device staging of a vector argument

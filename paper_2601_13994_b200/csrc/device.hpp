@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <vector>
 
 #include "kernels.cuh"
 #include "sparsla_c.h"
@@ -30,6 +31,7 @@ struct DevCsr {
     int cap_v32 = 0, cap_c32 = 0;  // per 32-row warp segment
     size_t smem_bytes = 0;
     bool staged = true;
+    bool local_layout = false;  // rank-local [owned | halo] columns (diagonal of row i is column i)
     int ws_ctas[8] = {0};  // persistent grid per staged-SpMV variant (SMs x resident CTAs)
     double* dinv = nullptr;
     double* ones = nullptr;
@@ -39,7 +41,7 @@ struct DevCsr {
 
     template <class I>
     static DevCsr* create(int device, long long nrows, long long ncols, const I* rp, const I* ci,
-                          const double* val);
+                          const double* val, bool local_layout = false);
     ~DevCsr();
     const double* jacobi_dinv();
     const double* ones_vec();
@@ -49,6 +51,36 @@ struct DevCsr {
 
 void launch_spmv(DevCsr* A, cudaStream_t s, int mode, const double* x, double* y, const double* aux,
                  const RedParams& red, int check_done);
+unsigned spmv_grid(const DevCsr* A, long long nch);
+void launch_spmv_part(DevCsr* A, cudaStream_t s, int mode, const double* x, double* y, const double* aux,
+                      const RedParams& red, int check_done, const int32_t* list, long long nch,
+                      unsigned expected);
+
+struct Transport;
+
+// One rank's distributed plan on its device (dist.cu): halo maps, interior/boundary chunk
+// lists, comm stream and the per-reduction-point all-gather buffers.
+struct DistCtx {
+    Transport* tr = nullptr;
+    int device = 0;
+    long long n_owned = 0, n_halo = 0;
+    std::vector<int> nbr;
+    std::vector<long long> s_off, s_cnt, r_off, r_cnt;  // per neighbour into send/recv maps
+    std::vector<long long> s_base, r_base;              // contiguous range start, or -1
+    int32_t* d_send_idx = nullptr;
+    int32_t* d_recv_idx = nullptr;
+    double* sendbuf = nullptr;
+    double* recvbuf = nullptr;
+    int32_t* d_interior = nullptr;
+    int32_t* d_boundary = nullptr;
+    long long n_interior = 0, n_boundary = 0;
+    double* red_send = nullptr;  // [8 points][8]
+    double* red_all = nullptr;   // [8 points][P][8]
+    cudaStream_t comm = nullptr;
+    cudaEvent_t ev_x = nullptr, ev_halo = nullptr;
+    void exchange(cudaStream_t s, double* x);  // halo of x ([owned|halo]) -> ev_halo
+    ~DistCtx();
+};
 
 // Jacobi-PCG / BiCGStab solver with device-resident state and graph-captured iterations.
 struct Solver {
@@ -72,7 +104,8 @@ struct Solver {
     cudaEvent_t ev[2] = {nullptr, nullptr};
     cudaGraphExec_t g_many = nullptr, g_one = nullptr;
 
-    Solver(DevCsr* A, int backend, const sparsla_solve_options& o);
+    DistCtx* dist = nullptr;
+    Solver(DevCsr* A, int backend, const sparsla_solve_options& o, DistCtx* dist = nullptr);
     ~Solver();
     void set_b(const double* src, int mem);
     void reset();
@@ -82,7 +115,13 @@ struct Solver {
     long long launches_per_iteration() const;
     void kernel_times(long long iters, double* ms);
 
+    bool capturable() const;
+
    private:
+    void spmv_point(int mode, double* xin, double* y, const double* aux, int scalar, int slot, int check_done);
+    template <int OP>
+    void vec_point(int scalar, int slot, int check_done);
+    void reduce_point(int scalar, int slot, int nd);
     RedParams red(int which, int slot) const;
     VecParams vparams() const;
     void enqueue_init();
@@ -91,3 +130,9 @@ struct Solver {
 };
 
 }  // namespace sparsla_b200
+
+struct sparsla_solver {
+    sparsla_b200::Solver* S;
+    double* x_user;
+    int x_mem;
+};

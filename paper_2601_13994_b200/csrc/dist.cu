@@ -1,0 +1,493 @@
+// dist.cu — row-partitioned (domain-decomposition) Krylov loop on 1..8 GPUs.
+//
+// Restates the reference's distributed module (Alg. 3/4) on the
+// device:
+//   dist_spmv       halo exchange of the SpMV input (zero-copy for contiguous ranges,
+//                   halo_pack/halo_unpack kernels otherwise) on a comm stream, overlapped
+//                   with the interior-chunk SpMV; boundary chunks run once the halo landed.
+//                   Rows keep their global column order, so every owned row sum equals the
+//                   serial one bit for bit.
+//   all_reduce_sum  each reduction point all-gathers the per-rank canonical-dot totals and
+//                   sums them in ascending rank order on the device:
+//                   deterministic, identical on every rank.
+//   dist_cg / dist_bicgstab / dist_adjoint_solve / gather_solution.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.hpp"
+#include "device.hpp"
+#include "kernels.cuh"
+#include "transport.hpp"
+
+namespace sparsla_b200 {
+
+#define CKD(x) cuda_check((x), #x)
+
+template <class T>
+static T* dmalloc(size_t n) {
+    void* p = nullptr;
+    CKD(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)));
+    return static_cast<T*>(p);
+}
+
+DistCtx::~DistCtx() {
+    cudaFree(d_send_idx); cudaFree(d_recv_idx); cudaFree(sendbuf); cudaFree(recvbuf);
+    cudaFree(d_interior); cudaFree(d_boundary); cudaFree(red_send); cudaFree(red_all);
+    if (ev_x) cudaEventDestroy(ev_x);
+    if (ev_halo) cudaEventDestroy(ev_halo);
+    if (comm) cudaStreamDestroy(comm);
+}
+
+void DistCtx::exchange(cudaStream_t s, double* x) {
+    CKD(cudaEventRecord(ev_x, s));
+    CKD(cudaStreamWaitEvent(comm, ev_x, 0));
+    std::vector<HaloPeer> peers(nbr.size());
+    for (size_t a = 0; a < nbr.size(); ++a) {
+        HaloPeer& p = peers[a];
+        p.rank = nbr[a];
+        p.scount = s_cnt[a];
+        p.rcount = r_cnt[a];
+        if (s_base[a] >= 0) {
+            p.send = x + s_base[a];  // contiguous: zero-copy send
+        } else {
+            p.send = sendbuf + s_off[a];
+            if (p.scount)
+                halo_pack_kernel<<<(unsigned)((p.scount + 255) / 256), 256, 0, comm>>>(x, d_send_idx + s_off[a],
+                                                                                     p.scount, sendbuf + s_off[a]);
+        }
+        p.recv = r_base[a] >= 0 ? x + r_base[a] : recvbuf + r_off[a];
+    }
+    CKD(cudaGetLastError());
+    tr->exchange(comm, peers);
+    for (size_t a = 0; a < nbr.size(); ++a)
+        if (r_base[a] < 0 && r_cnt[a])
+            halo_unpack_kernel<<<(unsigned)((r_cnt[a] + 255) / 256), 256, 0, comm>>>(x, d_recv_idx + r_off[a], r_cnt[a],
+                                                                                   recvbuf + r_off[a]);
+    CKD(cudaGetLastError());
+    CKD(cudaEventRecord(ev_halo, comm));
+}
+
+}  // namespace sparsla_b200
+
+using namespace sparsla_b200;
+
+struct sparsla_local_hub { std::shared_ptr<LocalHub> hub; };
+
+struct sparsla_dist {
+    std::unique_ptr<Transport> tr;
+    std::unique_ptr<DistCtx> ctx;
+    DevCsr* A = nullptr;
+    DevCsr* AT = nullptr;            // transposed values in A's local pattern (adjoint)
+    std::vector<int64_t> owned;      // this rank's global ids
+    std::vector<int64_t> all_owned;  // rank 0: concatenation over ranks (gather_solution)
+    std::vector<int64_t> all_count;  // rank 0: owned count per rank
+    long long n_global = 0;
+    long long alg_exchanges = 0, alg_allreduces = 0, alg_messages = 0;  // live algorithm work
+    ~sparsla_dist() {
+        if (A) { DeviceGuard g(A->device); ctx.reset(); delete AT; delete A; }
+    }
+};
+
+namespace {
+
+bool contiguous_range(const std::vector<int64_t>& v, size_t b, size_t e, long long& base) {
+    if (b == e) { base = 0; return true; }
+    for (size_t k = b + 1; k < e; ++k)
+        if (v[k] != v[k - 1] + 1) { base = -1; return false; }
+    base = v[b];
+    return true;
+}
+
+// Builds the device plan for one rank.  Collective over the transport (count handshake).
+sparsla_dist* build_plan(int device, std::unique_ptr<Transport> tr, const sparsla_local* L) {
+    DeviceGuard g(device);
+    auto D = std::make_unique<sparsla_dist>();
+    const long long no = (long long)L->owned.size(), nh = (long long)L->halo.size();
+    std::vector<int32_t> rp(L->rp.begin(), L->rp.end()), ci(L->ci.begin(), L->ci.end());
+    D->A = DevCsr::create<int32_t>(device, no, no + nh, rp.data(), ci.data(), L->v.data(), true);
+    auto C = std::make_unique<DistCtx>();
+    C->tr = tr.get();
+    C->device = device;
+    C->n_owned = no;
+    C->n_halo = nh;
+    const size_t nn = L->neighbors.size();
+    for (size_t a = 0; a < nn; ++a) {
+        C->nbr.push_back(L->neighbors[a]);
+        C->s_off.push_back(L->send_ptr[a]);
+        C->s_cnt.push_back(L->send_ptr[a + 1] - L->send_ptr[a]);
+        C->r_off.push_back(L->recv_ptr[a]);
+        C->r_cnt.push_back(L->recv_ptr[a + 1] - L->recv_ptr[a]);
+        long long sb, rb;
+        contiguous_range(L->send_idx, L->send_ptr[a], L->send_ptr[a + 1], sb);
+        contiguous_range(L->recv_idx, L->recv_ptr[a], L->recv_ptr[a + 1], rb);
+        C->s_base.push_back(sb);
+        C->r_base.push_back(rb);
+    }
+    std::vector<int32_t> si(L->send_idx.begin(), L->send_idx.end()), ri(L->recv_idx.begin(), L->recv_idx.end());
+    C->d_send_idx = dmalloc<int32_t>(si.size());
+    C->d_recv_idx = dmalloc<int32_t>(ri.size());
+    if (!si.empty()) CKD(cudaMemcpy(C->d_send_idx, si.data(), si.size() * 4, cudaMemcpyHostToDevice));
+    if (!ri.empty()) CKD(cudaMemcpy(C->d_recv_idx, ri.data(), ri.size() * 4, cudaMemcpyHostToDevice));
+    C->sendbuf = dmalloc<double>(si.size());
+    C->recvbuf = dmalloc<double>(ri.size());
+    // interior chunks reference no halo column; boundary chunks wait for the exchange
+    const long long nch = (no + kChunk - 1) / kChunk;
+    std::vector<int32_t> inter, bound;
+    for (long long c = 0; c < nch; ++c) {
+        bool b = false;
+        const long long r1 = std::min(no, (c + 1) * kChunk);
+        for (long long k = L->rp[c * kChunk]; k < L->rp[r1] && !b; ++k) b = L->ci[k] >= no;
+        (b ? bound : inter).push_back((int32_t)c);
+    }
+    C->n_interior = (long long)inter.size();
+    C->n_boundary = (long long)bound.size();
+    C->d_interior = dmalloc<int32_t>(inter.size());
+    C->d_boundary = dmalloc<int32_t>(bound.size());
+    if (!inter.empty()) CKD(cudaMemcpy(C->d_interior, inter.data(), inter.size() * 4, cudaMemcpyHostToDevice));
+    if (!bound.empty()) CKD(cudaMemcpy(C->d_boundary, bound.data(), bound.size() * 4, cudaMemcpyHostToDevice));
+    C->red_send = dmalloc<double>(8 * 8);
+    C->red_all = dmalloc<double>((size_t)8 * tr->P * 8);
+    CKD(cudaMemset(C->red_send, 0, 64 * sizeof(double)));
+    CKD(cudaStreamCreateWithFlags(&C->comm, cudaStreamNonBlocking));
+    CKD(cudaEventCreateWithFlags(&C->ev_x, cudaEventDisableTiming));
+    CKD(cudaEventCreateWithFlags(&C->ev_halo, cudaEventDisableTiming));
+    D->owned = L->owned;
+
+    // handshake without point-to-point traffic: all-gather every rank's send / recv count
+    // rows so that all ranks reach the same verdict before any send/recv is posted
+    // (|send p->q| must equal |recv q<-p|: structural symmetry)
+    cudaStream_t s = D->A->stream;
+    const int P = tr->P;
+    std::vector<double> row(2 * (size_t)P + 1, 0.0);
+    for (size_t a = 0; a < nn; ++a) {
+        row[C->nbr[a]] = (double)C->s_cnt[a];
+        row[P + C->nbr[a]] = (double)C->r_cnt[a];
+    }
+    row[2 * P] = (double)no;
+    const int W = 2 * P + 1;
+    double* hs = dmalloc<double>((size_t)W * (P + 1));
+    CKD(cudaMemcpy(hs, row.data(), W * 8, cudaMemcpyHostToDevice));
+    tr->allgather(s, hs, hs + W, W);
+    std::vector<double> all((size_t)W * P);
+    CKD(cudaMemcpyAsync(all.data(), hs + W, all.size() * 8, cudaMemcpyDeviceToHost, s));
+    CKD(cudaStreamSynchronize(s));
+    cudaFree(hs);
+    bool any_bad = false;
+    D->n_global = 0;
+    for (int p = 0; p < P; ++p) {
+        for (int q = 0; q < P; ++q)
+            any_bad |= all[(size_t)p * W + q] != all[(size_t)q * W + P + p];  // send p->q vs recv q<-p
+        D->all_count.push_back((int64_t)all[(size_t)p * W + 2 * P]);
+        D->n_global += (int64_t)all[(size_t)p * W + 2 * P];
+    }
+    if (any_bad)
+        fail(SPARSLA_ERR_UNSUPPORTED,
+             "halo maps disagree between ranks: the distributed path requires a structurally "
+             "symmetric pattern (SPEC.md:510)");
+    // gather_solution needs every rank's owned ids on rank 0 (ids travel bit-cast as doubles)
+    {
+        std::vector<HaloPeer> gp;
+        double* ids = dmalloc<double>(no + 1);
+        std::vector<double> idd(no);
+        std::memcpy(idd.data(), L->owned.data(), no * 8);
+        if (no) CKD(cudaMemcpy(ids, idd.data(), no * 8, cudaMemcpyHostToDevice));
+        double* rbuf = nullptr;
+        if (tr->rank == 0) {
+            rbuf = dmalloc<double>(D->n_global + 1);
+            long long off = 0;
+            for (int q = 0; q < tr->P; ++q) {
+                if (q == 0) { if (no) CKD(cudaMemcpy(rbuf, ids, no * 8, cudaMemcpyDeviceToDevice)); }
+                else gp.push_back(HaloPeer{q, nullptr, 0, rbuf + off, D->all_count[q]});
+                off += D->all_count[q];
+            }
+        } else {
+            gp.push_back(HaloPeer{0, ids, no, nullptr, 0});
+        }
+        tr->exchange(s, gp);
+        if (tr->rank == 0) {
+            std::vector<double> h(D->n_global);
+            if (D->n_global) CKD(cudaMemcpyAsync(h.data(), rbuf, D->n_global * 8, cudaMemcpyDeviceToHost, s));
+            CKD(cudaStreamSynchronize(s));
+            D->all_owned.resize(D->n_global);
+            std::memcpy(D->all_owned.data(), h.data(), D->n_global * 8);
+            cudaFree(rbuf);
+        }
+        CKD(cudaStreamSynchronize(s));
+        cudaFree(ids);
+        tr->exchanges -= 1;  // setup traffic is not part of the solver counters
+        tr->messages -= (long long)gp.size();
+    }
+    tr->allgathers -= 1;
+    D->ctx = std::move(C);
+    D->tr = std::move(tr);
+    return D.release();
+}
+
+struct DVec {  // staging of an owned-length vector argument (+ optional halo slots)
+    double* d = nullptr;
+    bool own = false;
+    DVec(const double* src, long long n, long long extra, int mem, cudaStream_t s, bool copy = true) {
+        if (mem == SPARSLA_MEM_DEVICE && extra == 0) { d = const_cast<double*>(src); return; }
+        d = dmalloc<double>(n + extra + 2);
+        own = true;
+        if (copy && n)
+            CKD(cudaMemcpyAsync(d, src, n * 8, mem == SPARSLA_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+    }
+    void out(double* dst, long long n, int mem, cudaStream_t s) {
+        if (own && n) CKD(cudaMemcpyAsync(dst, d, n * 8, mem == SPARSLA_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+    }
+    ~DVec() { if (own) cudaFree(d); }
+};
+
+void dist_krylov(sparsla_dist* D, int backend, const double* b, double* x, const sparsla_solve_options* o,
+                 sparsla_solve_report* rep, int mem, DevCsr* M = nullptr) {
+    DevCsr* A = M ? M : D->A;
+    DeviceGuard g(A->device);
+    Solver S(A, backend, *o, D->ctx.get());
+    S.set_b(b, mem);
+    if (mem == SPARSLA_MEM_DEVICE) S.x = x;
+    S.reset();
+    S.run();
+    S.report(rep);
+    D->alg_exchanges += S.h_st->spmv_count;  // one halo exchange per SpMV (incl. the initial one)
+    D->alg_allreduces += S.h_st->reductions;
+    D->alg_messages += S.h_st->spmv_count * (long long)D->ctx->nbr.size();
+    if (mem != SPARSLA_MEM_DEVICE && A->nrows)
+        CKD(cudaMemcpyAsync(x, S.x, A->nrows * 8, cudaMemcpyDeviceToHost, A->stream));
+    CKD(cudaStreamSynchronize(A->stream));
+}
+
+}  // namespace
+
+extern "C" {
+
+int sparsla_nccl_unique_id(unsigned char* out) {
+    return guarded([&] { nccl_unique_id(out); });
+}
+
+int sparsla_dist_create_nccl(int device, int nranks, int rank, const unsigned char* id, const sparsla_local* L,
+                             sparsla_dist** out) {
+    return guarded([&] {
+        if (!L || !out || !id) fail(SPARSLA_ERR_INVALID_ARGUMENT, "null argument");
+        DeviceGuard g(device);
+        std::unique_ptr<Transport> tr(new NcclTransport(nranks, rank, id));
+        *out = build_plan(device, std::move(tr), L);
+    });
+}
+
+int sparsla_local_hub_create(int nranks, sparsla_local_hub** out) {
+    return guarded([&] {
+        if (nranks < 1) fail(SPARSLA_ERR_INVALID_ARGUMENT, "nranks >= 1");
+        *out = new sparsla_local_hub{std::make_shared<LocalHub>(nranks)};
+    });
+}
+
+int sparsla_local_hub_destroy(sparsla_local_hub* h) {
+    delete h;
+    return SPARSLA_OK;
+}
+
+int sparsla_dist_create_local(int device, sparsla_local_hub* hub, int rank, const sparsla_local* L,
+                              sparsla_dist** out) {
+    return guarded([&] {
+        if (!L || !out || !hub) fail(SPARSLA_ERR_INVALID_ARGUMENT, "null argument");
+        DeviceGuard g(device);
+        std::unique_ptr<Transport> tr(new LocalTransport(hub->hub, rank));
+        *out = build_plan(device, std::move(tr), L);
+    });
+}
+
+int sparsla_dist_destroy(sparsla_dist* D) {
+    return guarded([&] { delete D; });
+}
+
+int sparsla_dist_info(const sparsla_dist* D, int64_t* info) {
+    return guarded([&] {
+        const DistCtx& C = *D->ctx;
+        info[0] = C.n_owned; info[1] = C.n_halo; info[2] = (int64_t)C.nbr.size();
+        info[3] = C.n_interior; info[4] = C.n_boundary; info[5] = D->tr->P; info[6] = D->tr->rank;
+        long long zc = 0;
+        for (size_t a = 0; a < C.nbr.size(); ++a) zc += (C.s_base[a] >= 0) + (C.r_base[a] >= 0);
+        info[7] = zc;  // zero-copy (contiguous) halo segments
+        info[8] = D->n_global;
+    });
+}
+
+int sparsla_dist_counters(const sparsla_dist* D, int64_t* out) {
+    return guarded([&] {
+        out[0] = D->alg_exchanges;
+        out[1] = D->alg_allreduces;
+        out[2] = D->alg_messages;
+        out[3] = D->tr->exchanges;  // raw transport calls (include the no-op tail of the
+        out[4] = D->tr->allgathers; // last graph replay after convergence)
+        out[5] = D->tr->messages;
+    });
+}
+
+int sparsla_dist_reset_counters(sparsla_dist* D) {
+    return guarded([&] {
+        D->tr->exchanges = D->tr->allgathers = D->tr->messages = 0;
+        D->alg_exchanges = D->alg_allreduces = D->alg_messages = 0;
+    });
+}
+
+// dist_spmv: y_owned = owned rows of A x, bit-identical to serial rows.
+int sparsla_dist_spmv(sparsla_dist* D, const double* x_owned, double* y_owned, int32_t mem) {
+    return guarded([&] {
+        DevCsr* A = D->A;
+        DistCtx* C = D->ctx.get();
+        DeviceGuard g(A->device);
+        cudaStream_t s = A->stream;
+        DVec X(x_owned, C->n_owned, C->n_halo, mem, s);
+        DVec Y(y_owned, C->n_owned, 0, mem, s, false);
+        C->exchange(s, X.d);
+        RedParams none{};
+        const unsigned gi = spmv_grid(A, C->n_interior), gb = spmv_grid(A, C->n_boundary);
+        launch_spmv_part(A, s, SPMV_PLAIN, X.d, Y.d, nullptr, none, 0, C->d_interior, C->n_interior, gi + gb);
+        CKD(cudaStreamWaitEvent(s, C->ev_halo, 0));
+        launch_spmv_part(A, s, SPMV_PLAIN, X.d, Y.d, nullptr, none, 0, C->d_boundary, C->n_boundary, gi + gb);
+        Y.out(y_owned, C->n_owned, mem, s);
+        CKD(cudaStreamSynchronize(s));
+        D->alg_exchanges += 1;
+        D->alg_messages += (long long)C->nbr.size();
+        D->tr->check();
+    });
+}
+
+// dist_cg (Alg. 4) with SolveOptions (Jacobi, rtol) like cg_solve.
+int sparsla_dist_cg_solve(sparsla_dist* D, const double* b, double* x, const sparsla_solve_options* o,
+                          sparsla_solve_report* rep, int32_t mem) {
+    return guarded([&] { dist_krylov(D, SPARSLA_BACKEND_CG, b, x, o, rep, mem); D->tr->check(); });
+}
+
+int sparsla_dist_bicgstab_solve(sparsla_dist* D, const double* b, double* x, const sparsla_solve_options* o,
+                                sparsla_solve_report* rep, int32_t mem) {
+    return guarded([&] { dist_krylov(D, SPARSLA_BACKEND_BICGSTAB, b, x, o, rep, mem); D->tr->check(); });
+}
+
+// dist_adjoint_solve: one distributed solve with A^T on the forward halo
+// maps (structural symmetry), grad_b = lambda (owned), grad_vals over the local entries
+// with x taken from [owned | halo] after one exchange of x.  vals_t: A^T's values in A's
+// local entry order (nullptr when A is symmetric).
+int sparsla_dist_adjoint_backward(sparsla_dist* D, const double* x_owned, const double* g_owned,
+                                  const double* vals_t, int32_t backend, const sparsla_solve_options* o,
+                                  double* grad_b, double* grad_vals, sparsla_solve_report* rep, int32_t mem) {
+    return guarded([&] {
+        DevCsr* A = D->A;
+        DistCtx* C = D->ctx.get();
+        DeviceGuard g(A->device);
+        cudaStream_t s = A->stream;
+        const long long no = C->n_owned;
+        // global "grad_x == 0" short-circuit decided identically on every rank
+        std::vector<double> hg(no);
+        if (no) CKD(cudaMemcpy(hg.data(), g_owned, no * 8, mem == SPARSLA_MEM_DEVICE ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost));
+        double nz = 0.0;
+        for (double v : hg) if (v != 0.0) { nz = 1.0; break; }
+        double* f = dmalloc<double>(2 + (size_t)D->tr->P);
+        CKD(cudaMemcpy(f, &nz, 8, cudaMemcpyHostToDevice));
+        D->tr->allgather(s, f, f + 1, 1);
+        std::vector<double> fl(D->tr->P);
+        CKD(cudaMemcpyAsync(fl.data(), f + 1, fl.size() * 8, cudaMemcpyDeviceToHost, s));
+        CKD(cudaStreamSynchronize(s));
+        cudaFree(f);
+        D->tr->allgathers -= 1;
+        bool any = false;
+        for (double v : fl) any |= v != 0.0;
+        DVec GB(grad_b, no, 0, mem, s, false);
+        std::memset(rep, 0, sizeof(*rep));
+        rep->backend = backend;
+        if (!any) {
+            if (no) CKD(cudaMemsetAsync(GB.d, 0, no * 8, s));
+            rep->converged = 1;
+            std::snprintf(rep->diagnostic, 128, "grad_x == 0: short-circuit");
+        } else {
+            DevCsr* M = A;
+            if (vals_t) {
+                if (!D->AT) {
+                    std::vector<int32_t> hrp(A->nrows + 1), hci(A->nnz);
+                    CKD(cudaMemcpy(hrp.data(), A->rp, (A->nrows + 1) * 4, cudaMemcpyDeviceToHost));
+                    CKD(cudaMemcpy(hci.data(), A->ci, A->nnz * 4, cudaMemcpyDeviceToHost));
+                    std::vector<double> hv(A->nnz);
+                    CKD(cudaMemcpy(hv.data(), vals_t, A->nnz * 8, mem == SPARSLA_MEM_DEVICE ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost));
+                    D->AT = DevCsr::create<int32_t>(A->device, A->nrows, A->ncols, hrp.data(), hci.data(), hv.data(), true);
+                } else {
+                    CKD(cudaMemcpy(D->AT->val, vals_t, A->nnz * 8, mem == SPARSLA_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
+                    cudaFree(D->AT->dinv);
+                    D->AT->dinv = nullptr;
+                }
+                M = D->AT;
+            }
+            DVec G(g_owned, no, 0, mem, s);
+            CKD(cudaStreamSynchronize(s));
+            dist_krylov(D, backend, G.d, GB.d, o, rep, SPARSLA_MEM_DEVICE, M);
+        }
+        // grad_vals: x over [owned | halo] (one exchange), lambda owned
+        DVec XL(x_owned, no, C->n_halo, mem, s);
+        C->exchange(s, XL.d);
+        CKD(cudaStreamWaitEvent(s, C->ev_halo, 0));
+        DVec GV(grad_vals, A->nnz, 0, mem, s, false);
+        if (no) adjoint_gather_kernel<<<(unsigned)((no + 255) / 256), 256, 0, s>>>(A->rp, A->ci, no, GB.d, XL.d, GV.d);
+        CKD(cudaGetLastError());
+        GB.out(grad_b, no, mem, s);
+        GV.out(grad_vals, A->nnz, mem, s);
+        CKD(cudaStreamSynchronize(s));
+        D->tr->check();
+    });
+}
+
+// gather_solution: rank 0 receives every rank's owned values and places
+// them by global index.  x_global is only written on rank 0 (host memory).
+int sparsla_dist_gather(sparsla_dist* D, const double* x_owned, double* x_global, int32_t mem) {
+    return guarded([&] {
+        DevCsr* A = D->A;
+        DeviceGuard g(A->device);
+        cudaStream_t s = A->stream;
+        const long long no = D->ctx->n_owned;
+        DVec X(x_owned, no, 0, mem, s);
+        std::vector<HaloPeer> gp;
+        double* rbuf = nullptr;
+        if (D->tr->rank == 0) {
+            rbuf = dmalloc<double>(D->n_global + 1);
+            long long off = 0;
+            for (int q = 0; q < D->tr->P; ++q) {
+                if (q == 0) { if (no) CKD(cudaMemcpyAsync(rbuf, X.d, no * 8, cudaMemcpyDeviceToDevice, s)); }
+                else gp.push_back(HaloPeer{q, nullptr, 0, rbuf + off, D->all_count[q]});
+                off += D->all_count[q];
+            }
+        } else {
+            gp.push_back(HaloPeer{0, X.d, no, nullptr, 0});
+        }
+        D->tr->exchange(s, gp);
+        D->tr->exchanges -= 1;
+        D->tr->messages -= (long long)gp.size();
+        if (D->tr->rank == 0) {
+            std::vector<double> h(D->n_global);
+            if (D->n_global) CKD(cudaMemcpyAsync(h.data(), rbuf, D->n_global * 8, cudaMemcpyDeviceToHost, s));
+            CKD(cudaStreamSynchronize(s));
+            for (long long k = 0; k < D->n_global; ++k) x_global[D->all_owned[k]] = h[k];
+            cudaFree(rbuf);
+        }
+        CKD(cudaStreamSynchronize(s));
+    });
+}
+
+}  // extern "C"
+
+// persistent distributed solver for the benchmark (same sparsla_solver handle as 1 GPU)
+
+extern "C" int sparsla_dist_solver_create(sparsla_dist* D, int32_t backend, const double* b, int32_t mem,
+                                          const sparsla_solve_options* o, sparsla_solver** out) {
+    return guarded([&] {
+        DeviceGuard g(D->A->device);
+        auto S = std::make_unique<Solver>(D->A, backend, *o, D->ctx.get());
+        S->set_b(b, mem);
+        CKD(cudaStreamSynchronize(S->stream));
+        S->reset();
+        *out = new sparsla_solver{S.release(), nullptr, 0};
+    });
+}

@@ -379,12 +379,6 @@ using namespace sparsla_b200;
 // ------------------------------------------------------------------------------------
 // build_local result
 // ------------------------------------------------------------------------------------
-struct sparsla_local {
-    std::vector<int64_t> owned, halo;
-    std::vector<int32_t> neighbors;
-    std::vector<int64_t> send_ptr, send_idx, recv_ptr, recv_idx, rp, ci;
-    std::vector<double> v;
-};
 
 extern "C" {
 
@@ -534,8 +528,12 @@ int sparsla_local_build(int64_t n_global, const int32_t* part_of, int32_t P, int
                         const double* v, sparsla_local** out) {
     return guarded([&] {
         if (rank < 0 || rank >= P) fail(SPARSLA_ERR_INVALID_ARGUMENT, "rank outside [0, P)");
+        // part_of == nullptr: contiguous partition computed on the fly, so
+        // a rank of a 400M-row problem never materialises the global map
+        const int64_t blk = (n_global + P - 1) / std::max<int32_t>(P, 1);
+        auto part = [&](int64_t g) -> int32_t { return part_of ? part_of[g] : (int32_t)(g / blk); };
         for (int64_t a = 0; a < no; ++a) {
-            if (owned[a] < 0 || owned[a] >= n_global || part_of[owned[a]] != rank)
+            if (owned[a] < 0 || owned[a] >= n_global || part(owned[a]) != rank)
                 fail(SPARSLA_ERR_INVALID_ARGUMENT, "owned list disagrees with part_of");
             if (a > 0 && owned[a] <= owned[a - 1])
                 fail(SPARSLA_ERR_INVALID_ARGUMENT, "owned list must be strictly ascending");
@@ -548,19 +546,19 @@ int sparsla_local_build(int64_t n_global, const int32_t* part_of, int32_t P, int
         for (int64_t k = 0; k < nnz; ++k) {
             const int64_t c = ci[k];
             if (c < 0 || c >= n_global) fail(SPARSLA_ERR_BOUNDS, "column outside matrix");
-            if (part_of[c] != rank) cand.push_back(c);
+            if (part(c) != rank) cand.push_back(c);
         }
         std::sort(cand.begin(), cand.end());
         cand.erase(std::unique(cand.begin(), cand.end()), cand.end());
         L->halo = std::move(cand);
         const int64_t nh = static_cast<int64_t>(L->halo.size());
         std::vector<char> nb(static_cast<size_t>(P), 0);
-        for (int64_t h : L->halo) nb[part_of[h]] = 1;
+        for (int64_t h : L->halo) nb[part(h)] = 1;
         for (int32_t q = 0; q < P; ++q)
             if (nb[q]) L->neighbors.push_back(q);
         const bool contiguous = no == 0 || owned[no - 1] - owned[0] == no - 1;
         auto g2l = [&](int64_t g) -> int64_t {
-            if (part_of[g] == rank) {
+            if (part(g) == rank) {
                 if (contiguous) return g - owned[0];
                 return std::lower_bound(L->owned.begin(), L->owned.end(), g) - L->owned.begin();
             }
@@ -569,14 +567,14 @@ int sparsla_local_build(int64_t n_global, const int32_t* part_of, int32_t P, int
         L->recv_ptr.push_back(0);
         for (int32_t q : L->neighbors) {
             for (int64_t a = 0; a < nh; ++a)
-                if (part_of[L->halo[a]] == q) L->recv_idx.push_back(no + a);
+                if (part(L->halo[a]) == q) L->recv_idx.push_back(no + a);
             L->recv_ptr.push_back(static_cast<int64_t>(L->recv_idx.size()));
         }
         L->send_ptr.push_back(0);
         for (int32_t q : L->neighbors) {
             for (int64_t a = 0; a < no; ++a) {
                 bool need = false;
-                for (int64_t k = rp[a]; k < rp[a + 1] && !need; ++k) need = part_of[ci[k]] == q;
+                for (int64_t k = rp[a]; k < rp[a + 1] && !need; ++k) need = part(ci[k]) == q;
                 if (need) L->send_idx.push_back(a);
             }
             L->send_ptr.push_back(static_cast<int64_t>(L->send_idx.size()));

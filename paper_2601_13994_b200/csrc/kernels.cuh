@@ -45,6 +45,7 @@ struct KState {
     long long max_iter;
     double tol, bnorm, rnorm, rz, alpha, beta, omega, rho, rho_prev, rho_thr, ss;
     long long k, spmv_count, breakdown_iter;
+    long long reductions;  // reduction points applied while the solve was live
     int done, converged, status, halfstep;
     double scratch[8];  // plain dot outputs
 };
@@ -59,6 +60,7 @@ __device__ __forceinline__ double dmax_ref(double a, double b) { return a < b ? 
 // Scalar bookkeeping after a reduction point (the same decisions, in the same order, as
 // the oracle's cg_core / bicgstab_core loops).
 __device__ inline void apply_scalar(int which, KState* st, const double* t) {
+    if (which != SC_STORE && which != SC_NONE) st->reductions += 1;
     switch (which) {
         case SC_STORE:
             for (int j = 0; j < 3; ++j) st->scratch[j] = t[j];
@@ -352,6 +354,7 @@ struct SpmvParams {
     long long n;        // rows
     long long chunk0;   // first chunk index handled by this launch (interior/boundary split)
     long long nch;      // number of chunks handled by this launch
+    const int32_t* chunk_list;  // optional: chunk ids of this launch (interior / boundary rows)
     const double* aux;  // BICG_V: rhat, BICG_T: s
     int cap_v, cap_c;   // staged capacities (elements) per round
     int check_done;
@@ -404,7 +407,7 @@ __global__ void __launch_bounds__(kSpmvThreads, 2) spmv_direct_kernel(SpmvParams
     constexpr int NA = ND > 0 ? ND : 1;
     if (P.check_done && P.red.st->done) return;
     const int t = threadIdx.x;
-    const long long chunk = P.chunk0 + blockIdx.x;
+    const long long chunk = P.chunk_list ? (long long)P.chunk_list[blockIdx.x] : P.chunk0 + blockIdx.x;
     const long long base = chunk * kChunk;
     const long long rem_rounds = (P.n - base + kChunkSlots - 1) / kChunkSlots;
     const int nrounds = rem_rounds < kChunkRounds ? (int)rem_rounds : kChunkRounds;
@@ -478,7 +481,7 @@ __global__ void __launch_bounds__(kWsThreads, MINB) spmv_ws_kernel(SpmvParams P)
             const uint64_t pol = policy_evict_first();
             long long g = 0;
             for (long long c = blockIdx.x; c < P.nch; c += gridDim.x) {
-                const long long base = (P.chunk0 + c) * kChunk;
+                const long long base = (P.chunk_list ? (long long)P.chunk_list[c] : P.chunk0 + c) * kChunk;
                 const long long rem = (P.n - base + kChunkSlots - 1) / kChunkSlots;
                 const int nr = rem < kChunkRounds ? (int)rem : kChunkRounds;
                 for (int r = 0; r < nr; ++r, ++g) {
@@ -506,7 +509,7 @@ __global__ void __launch_bounds__(kWsThreads, MINB) spmv_ws_kernel(SpmvParams P)
     __shared__ int s_flag;
     long long g = 0;
     for (long long c = blockIdx.x; c < P.nch; c += gridDim.x) {
-        const long long chunk = P.chunk0 + c;
+        const long long chunk = P.chunk_list ? (long long)P.chunk_list[c] : P.chunk0 + c;
         const long long base = chunk * kChunk;
         const long long rem = (P.n - base + kChunkSlots - 1) / kChunkSlots;
         const int nr = rem < kChunkRounds ? (int)rem : kChunkRounds;
@@ -679,14 +682,15 @@ __global__ void __launch_bounds__(kSpmvThreads, MINB) spmv_wp_kernel(SpmvParams 
     // issue iterator over this CTA's (chunk, round) sequence
     long long ic = blockIdx.x;
     int ir = 0;
+    auto chunk_of = [&](long long c) { return P.chunk_list ? (long long)P.chunk_list[c] : P.chunk0 + c; };
     auto nrounds = [&](long long c) {
-        const long long base = (P.chunk0 + c) * kChunk;
+        const long long base = chunk_of(c) * kChunk;
         const long long rem = (P.n - base + kChunkSlots - 1) / kChunkSlots;
         return rem < kChunkRounds ? (int)rem : kChunkRounds;
     };
     // segment row range for (c, r) of this warp
     auto seg = [&](long long c, int r, long long& rs, long long& re) {
-        rs = (P.chunk0 + c) * kChunk + (long long)r * kChunkSlots + 32 * w;
+        rs = chunk_of(c) * kChunk + (long long)r * kChunkSlots + 32 * w;
         re = min(rs + 32, P.n);
     };
     uint64_t pol = 0;
@@ -732,7 +736,7 @@ __global__ void __launch_bounds__(kSpmvThreads, MINB) spmv_wp_kernel(SpmvParams 
 
     long long g = 0;
     for (long long c = blockIdx.x; c < P.nch; c += gridDim.x) {
-        const long long chunk = P.chunk0 + c;
+        const long long chunk = chunk_of(c);
         const long long base = chunk * kChunk;
         const int nr = nrounds(c);
         double acc[NA];
@@ -960,7 +964,7 @@ struct DotParams {
     const double* b;
     RedParams red;
 };
-__global__ void __launch_bounds__(kVecThreads) dot_kernel(DotParams P) {
+static __global__ void __launch_bounds__(kVecThreads) dot_kernel(DotParams P) {
     const int t = threadIdx.x;
     const long long chunk = blockIdx.x;
     const long long base = chunk * kChunk;
@@ -980,10 +984,9 @@ __global__ void __launch_bounds__(kVecThreads) dot_kernel(DotParams P) {
 
 // Distributed reduction points: rank totals were all-gathered into g[P][k]; sum in
 // ascending rank order starting from rank 0 and run the scalar step.
-__global__ void scalar_kernel(const double* g, int nranks, int k, int which, KState* st) {
+static __global__ void scalar_kernel(const double* g, int nranks, int k, int which, KState* st) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    if (st->done && which != SC_BI_U3) return;
-    if (st->done && which == SC_BI_U3 && !st->halfstep) return;
+    if (st->done) return;  // (the half step runs with done == 0; SC_BI_U3 sets it)
     double t[4] = {0, 0, 0, 0};
     for (int j = 0; j < k; ++j) {
         double s = g[j];
@@ -994,7 +997,7 @@ __global__ void scalar_kernel(const double* g, int nranks, int k, int which, KSt
 }
 
 // Jacobi inverse diagonal: 1/A_ii, or 1.0 when missing / zero / non-finite.
-__global__ void jacobi_kernel(const int32_t* rp, const int32_t* ci, const double* val, long long n,
+static __global__ void jacobi_kernel(const int32_t* rp, const int32_t* ci, const double* val, long long n,
                               long long col_offset, double* dinv) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -1015,7 +1018,7 @@ __global__ void jacobi_kernel(const int32_t* rp, const int32_t* ci, const double
 }
 
 // Exact value symmetry (A^T == A bitwise) for adjoint operator reuse.
-__global__ void symmetry_kernel(const int32_t* rp, const int32_t* ci, const double* val, long long n,
+static __global__ void symmetry_kernel(const int32_t* rp, const int32_t* ci, const double* val, long long n,
                                 int* flags) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -1033,7 +1036,7 @@ __global__ void symmetry_kernel(const int32_t* rp, const int32_t* ci, const doub
 
 // Adjoint gradient gather (Eq. 3): grad_vals[k] = -(lam[row_k] * x[col_k]),
 // in CSR (= canonical COO) order; one thread per row.
-__global__ void adjoint_gather_kernel(const int32_t* rp, const int32_t* ci, long long n,
+static __global__ void adjoint_gather_kernel(const int32_t* rp, const int32_t* ci, long long n,
                                       const double* lam, const double* x, double* gv) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -1042,23 +1045,23 @@ __global__ void adjoint_gather_kernel(const int32_t* rp, const int32_t* ci, long
     for (int k = rp[i]; k < k1; ++k) gv[k] = -__dmul_rn(l, __ldg(x + ci[k]));
 }
 
-__global__ void fill_kernel(double* p, long long n, double v) {
+static __global__ void fill_kernel(double* p, long long n, double v) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) p[i] = v;
 }
 
-__global__ void i64_to_i32_kernel(const long long* in, int32_t* out, long long n) {
+static __global__ void i64_to_i32_kernel(const long long* in, int32_t* out, long long n) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) out[i] = (int32_t)in[i];
 }
 
 // Halo pack: sendbuf[j] = x[idx[j]] (canonical global order).
-__global__ void halo_pack_kernel(const double* x, const int32_t* idx, long long m, double* out) {
+static __global__ void halo_pack_kernel(const double* x, const int32_t* idx, long long m, double* out) {
     const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (j < m) out[j] = x[idx[j]];
 }
 // Halo unpack: x[idx[j]] = recvbuf[j].
-__global__ void halo_unpack_kernel(double* x, const int32_t* idx, long long m, const double* in) {
+static __global__ void halo_unpack_kernel(double* x, const int32_t* idx, long long m, const double* in) {
     const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (j < m) x[idx[j]] = in[j];
 }

@@ -620,11 +620,16 @@ class LocalPartition:
 
 def build_local(owned_rows: CsrMatrix, owned, part_of, P: int, rank: int) -> LocalPartition:
     """build_local from this rank's rows only (global column ids); structurally symmetric
-    patterns (SPEC.md:461-469, 508-510)."""
-    part_of = np.ascontiguousarray(part_of, np.int32)
+    patterns.  part_of=None means partition_contiguous(n, P)
+    with n = owned_rows.ncols (the global size), without materialising the map."""
     owned = _i64(owned)
     h = _vp()
-    _check(lib().sparsla_local_build(C.c_int64(len(part_of)), _p(part_of, _i32p), C.c_int32(P),
+    if part_of is None:
+        n_global, pp = owned_rows.ncols, None
+    else:
+        part_of = np.ascontiguousarray(part_of, np.int32)
+        n_global, pp = len(part_of), _p(part_of, _i32p)
+    _check(lib().sparsla_local_build(C.c_int64(n_global), pp, C.c_int32(P),
                                      C.c_int32(rank), C.c_int64(len(owned)), _p(owned, _i64p),
                                      _p(owned_rows.row_ptr, _i64p), _p(owned_rows.col_idx, _i64p),
                                      _p(owned_rows.vals, _f64p), C.byref(h)))
@@ -647,3 +652,187 @@ def build_local(owned_rows: CsrMatrix, owned, part_of, P: int, rank: int) -> Loc
     finally:
         lib().sparsla_local_destroy(h)
     return LocalPartition(rank, **o)
+
+
+# ------------------------------------------------------------- distributed (device) ---
+def _local_handle(rows: CsrMatrix, owned, part_of, P: int, rank: int, n_global: int):
+    owned = _i64(owned)
+    h = _vp()
+    po = None if part_of is None else np.ascontiguousarray(part_of, np.int32)
+    _check(lib().sparsla_local_build(C.c_int64(n_global),
+                                     None if po is None else _p(po, _i32p), C.c_int32(P),
+                                     C.c_int32(rank), C.c_int64(len(owned)), _p(owned, _i64p),
+                                     _p(rows.row_ptr, _i64p), _p(rows.col_idx, _i64p),
+                                     _p(rows.vals, _f64p), C.byref(h)))
+    return h
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_ubyte * 128)()
+    _check(lib().sparsla_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+class LocalHub:
+    """In-process transport hub: P ranks as threads of this process (may share a GPU)."""
+
+    def __init__(self, P: int):
+        self.P = P
+        self.h = _vp()
+        _check(lib().sparsla_local_hub_create(C.c_int(P), C.byref(self.h)))
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().sparsla_local_hub_destroy(self.h)
+        except Exception:
+            pass
+
+
+class DistPlan:
+    """One rank of the row-partitioned solver.  Every method is
+    collective over the ranks of the plan."""
+
+    def __init__(self, h, n_owned, nnz_local, dev):
+        self.h, self.n_owned, self.nnz_local, self.dev = h, n_owned, nnz_local, dev
+
+    @staticmethod
+    def create_local(hub: LocalHub, dev: int, rank: int, rows: CsrMatrix, owned, part_of,
+                     n_global: int) -> "DistPlan":
+        L = _local_handle(rows, owned, part_of, hub.P, rank, n_global)
+        try:
+            h = _vp()
+            _check(lib().sparsla_dist_create_local(C.c_int(dev), hub.h, C.c_int(rank), L, C.byref(h)))
+        finally:
+            lib().sparsla_local_destroy(L)
+        return DistPlan(h, len(owned), rows.nnz, dev)
+
+    @staticmethod
+    def create_nccl(dev: int, nranks: int, rank: int, uid: bytes, rows: CsrMatrix, owned,
+                    part_of, n_global: int) -> "DistPlan":
+        L = _local_handle(rows, owned, part_of, nranks, rank, n_global)
+        try:
+            h = _vp()
+            idb = (C.c_ubyte * 128).from_buffer_copy(uid)
+            _check(lib().sparsla_dist_create_nccl(C.c_int(dev), C.c_int(nranks), C.c_int(rank), idb,
+                                                  L, C.byref(h)))
+        finally:
+            lib().sparsla_local_destroy(L)
+        return DistPlan(h, len(owned), rows.nnz, dev)
+
+    def info(self):
+        out = np.zeros(9, np.int64)
+        _check(lib().sparsla_dist_info(self.h, _p(out, _i64p)))
+        keys = ["n_owned", "n_halo", "neighbors", "interior_chunks", "boundary_chunks", "P", "rank",
+                "zero_copy_segments", "n_global"]
+        return {k: int(out[i]) for i, k in enumerate(keys)}
+
+    def counters(self):
+        out = np.zeros(6, np.int64)
+        _check(lib().sparsla_dist_counters(self.h, _p(out, _i64p)))
+        return {"halo_exchanges": int(out[0]), "all_reduces": int(out[1]), "messages": int(out[2]),
+                "raw_exchanges": int(out[3]), "raw_allgathers": int(out[4]), "raw_messages": int(out[5])}
+
+    def reset_counters(self):
+        _check(lib().sparsla_dist_reset_counters(self.h))
+
+    def spmv(self, x_owned):
+        x = _f64(x_owned)
+        y = np.empty(self.n_owned)
+        _check(lib().sparsla_dist_spmv(self.h, _p(x, _f64p), _p(y, _f64p), C.c_int32(MEM_HOST)))
+        return y
+
+    def _solve(self, fn, b_owned, opts):
+        b = _f64(b_owned)
+        x = np.empty(self.n_owned)
+        rep = _Report()
+        o = (opts or SolveOptions()).c()
+        _check(fn(self.h, _p(b, _f64p), _p(x, _f64p), C.byref(o), C.byref(rep), C.c_int32(MEM_HOST)))
+        return x, SolveReport._from(rep)
+
+    def cg(self, b_owned, opts: SolveOptions | None = None):
+        return self._solve(lib().sparsla_dist_cg_solve, b_owned, opts)
+
+    def bicgstab(self, b_owned, opts: SolveOptions | None = None):
+        return self._solve(lib().sparsla_dist_bicgstab_solve, b_owned, opts)
+
+    def adjoint(self, x_owned, g_owned, vals_t=None, backend="cg", opts: SolveOptions | None = None):
+        x, g = _f64(x_owned), _f64(g_owned)
+        gb = np.empty(self.n_owned)
+        gv = np.empty(self.nnz_local)
+        vt = None if vals_t is None else _f64(vals_t)
+        rep = _Report()
+        o = (opts or SolveOptions()).c()
+        be = {"cg": BACKEND_CG, "bicgstab": BACKEND_BICGSTAB}[backend]
+        _check(lib().sparsla_dist_adjoint_backward(self.h, _p(x, _f64p), _p(g, _f64p),
+                                                   None if vt is None else _p(vt, _f64p), C.c_int32(be),
+                                                   C.byref(o), _p(gb, _f64p), _p(gv, _f64p),
+                                                   C.byref(rep), C.c_int32(MEM_HOST)))
+        return gb, gv, SolveReport._from(rep)
+
+    def gather(self, x_owned):
+        """gather_solution: the global vector on rank 0, None elsewhere."""
+        x = _f64(x_owned)
+        n = self.info()["n_global"]
+        out = np.empty(n)
+        _check(lib().sparsla_dist_gather(self.h, _p(x, _f64p), _p(out, _f64p), C.c_int32(MEM_HOST)))
+        return out if self.info()["rank"] == 0 else None
+
+    def solver(self, b_owned, backend="cg", opts: SolveOptions | None = None) -> "Solver":
+        sv = Solver.__new__(Solver)
+        sv.D = DeviceCsr.__new__(DeviceCsr)
+        sv.D.h, sv.D.dev, sv.D.nrows, sv.D.ncols = _vp(), self.dev, self.n_owned, self.n_owned
+        sv.h = _vp()
+        o = (opts or SolveOptions()).c()
+        be = {"cg": BACKEND_CG, "bicgstab": BACKEND_BICGSTAB}[backend]
+        b = _f64(b_owned)
+        _check(lib().sparsla_dist_solver_create(self.h, C.c_int32(be), _p(b, _f64p), C.c_int32(MEM_HOST),
+                                                C.byref(o), C.byref(sv.h)))
+        return sv
+
+    def close(self):
+        if self.h:
+            lib().sparsla_dist_destroy(self.h)
+            self.h = _vp()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def run_ranks(P: int, fn):
+    """Run fn(rank) on P threads (the in-process worker model); returns the
+    per-rank results or raises the first rank's exception."""
+    import threading
+    out, err = [None] * P, [None] * P
+
+    def body(r):
+        try:
+            out[r] = fn(r)
+        except BaseException as e:  # noqa: BLE001
+            err[r] = e
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(P)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for e in err:
+        if e is not None:
+            raise e
+    return out
+
+
+def owned_rows(A: CsrMatrix, owned) -> CsrMatrix:
+    """Rows `owned` of a global CSR, global column ids (a rank's input to build_local)."""
+    owned = _i64(owned)
+    lens = np.diff(A.row_ptr)[owned]
+    rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    if len(owned):
+        starts = A.row_ptr[owned]
+        sel = np.repeat(starts - rp[:-1], lens) + np.arange(rp[-1])
+    else:
+        sel = np.zeros(0, np.int64)
+    return CsrMatrix(len(owned), A.ncols, rp, A.col_idx[sel], A.vals[sel])
