@@ -27,6 +27,8 @@ def run(args, metric):
     local = int(os.environ.get("LOCAL_RANK", str(rank)))
     torch.cuda.set_device(local)
     if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")  # --dist at N=1 outside torchrun
+        os.environ.setdefault("MASTER_PORT", "29533")
         dist.init_process_group("gloo", rank=rank, world_size=world)
     t0 = time.time()
     plan, owned, n = bootstrap.nccl_plan("poisson3d", args.size, 0, 0.0, rank, world, local)
