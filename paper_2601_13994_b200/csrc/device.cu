@@ -29,7 +29,12 @@ void cuda_check(cudaError_t e, const char* what) {
 }
 #define CK(x) cuda_check((x), #x)
 
-DeviceGuard::DeviceGuard(int dev) {
+DeviceGuard::DeviceGuard(int dev, bool nothrow) {
+    if (nothrow) {  // destructors: never throw (the runtime may already be shut down)
+        if (cudaGetDevice(&prev_) != cudaSuccess) { cudaGetLastError(); prev_ = dev; return; }
+        if (prev_ != dev && cudaSetDevice(dev) != cudaSuccess) cudaGetLastError();
+        return;
+    }
     int n = 0;
     if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
         cudaGetLastError();
@@ -97,7 +102,7 @@ static void configure_ws_variants(int device) {
 
 // ------------------------------------------------------------------ DevCsr ---------
 DevCsr::~DevCsr() {
-    DeviceGuard g(device);
+    DeviceGuard g(device, true);
     cudaFree(rp); cudaFree(ci); cudaFree(val); cudaFree(dinv); cudaFree(ones);
     if (stream) cudaStreamDestroy(stream);
     delete transpose;
@@ -354,7 +359,7 @@ Solver::Solver(DevCsr* A_, int backend_, const sparsla_solve_options& o, DistCtx
 }
 
 Solver::~Solver() {
-    DeviceGuard g(A->device);
+    DeviceGuard g(A->device, true);
     if (g_many) cudaGraphExecDestroy(g_many);
     if (g_one) cudaGraphExecDestroy(g_one);
     for (double* v : {x_own, b_own, r, p, q, rh, ph, s, sh, t}) cudaFree(v);

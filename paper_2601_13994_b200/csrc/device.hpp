@@ -14,7 +14,7 @@ namespace sparsla_b200 {
 void cuda_check(cudaError_t e, const char* what);
 
 struct DeviceGuard {
-    explicit DeviceGuard(int dev);
+    explicit DeviceGuard(int dev, bool nothrow = false);
     ~DeviceGuard();
     int prev_ = 0;
 };

@@ -89,7 +89,7 @@ struct sparsla_dist {
     long long n_global = 0;
     long long alg_exchanges = 0, alg_allreduces = 0, alg_messages = 0;  // live algorithm work
     ~sparsla_dist() {
-        if (A) { DeviceGuard g(A->device); ctx.reset(); delete AT; delete A; }
+        if (A) { DeviceGuard g(A->device, true); ctx.reset(); delete AT; delete A; }
     }
 };
 
