@@ -102,9 +102,12 @@ def gen_config(args):
 
 
 def iteration_bytes(n, nnz):
+    """Algorithmic bytes of THIS implementation's CG iteration (x += a p moved into update 2
+    so p is streamed once: 12 nnz + 100 n + 4; SURVEY.md's canonical 3-pass accounting is
+    12 nnz + 108 n + 4, reported beside it)."""
     spmv = 12 * nnz + 4 * (n + 1) + 8 * n + 8 * n  # vals+cols, row_ptr, p (once), q write
-    u1 = 56 * n                                     # read x p r q d, write x r
-    u2 = 32 * n                                     # read r d p, write p
+    u1 = 32 * n                                     # read r q d, write r
+    u2 = 48 * n                                     # read x p r d, write x p
     return spmv, u1, u2
 
 
@@ -273,6 +276,8 @@ def run_ours(args):
         "spmv_gbs": spmv_gbs,
         "iteration_gbs": it_bytes / (ms / args.steps * 1e-3) / 1e9,
         "bytes_per_iteration": it_bytes,
+        "canonical_bytes_per_iteration": 12 * nnz + 108 * n + 4,
+        "canonical_iteration_gbs": (12 * nnz + 108 * n + 4) / (ms / args.steps * 1e-3) / 1e9,
         "kernel_ms": {"spmv_cg": kms[0], "cg_update1": kms[1], "cg_update2": kms[2]},
         "roofline": {"bound": "hbm", "kernel": "spmv_kernel<SPMV_CG,staged>", "achieved": spmv_gbs,
                      "peak": peak, "unit": "GB/s", "frac": spmv_gbs / peak, "traffic": traffic,

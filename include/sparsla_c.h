@@ -151,7 +151,8 @@ int sparsla_dcsr_create_i32(int device, int64_t nrows, int64_t ncols, const int3
 int sparsla_dcsr_set_values(sparsla_dcsr* A, const double* vals, int32_t mem);
 int sparsla_dcsr_destroy(sparsla_dcsr* A);
 /* info[0]=nrows [1]=ncols [2]=nnz [3]=device bytes of the matrix [4]=max nnz per 256-row
- * block [5]=max row length [6]=kernel variant used by spmv (0 staged, 1 long-row) */
+ * block [5]=max row length [6]=kernel variant used by spmv (0 staged, 1 long-row)
+ * [7]=staged-SpMV variant index (8 entries) */
 int sparsla_dcsr_info(const sparsla_dcsr* A, int64_t* info);
 
 /* y = A x (sparse.cpp:135-154): rows accumulated left to right from 0.0, separate

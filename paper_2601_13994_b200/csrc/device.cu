@@ -62,9 +62,10 @@ struct WsVariant {
     int rpt, stg, minb;
     const void* fn[4];  // per SpmvMode
 };
-#define WSV(R, S, M, E)                                                                           \
-    {R, S, M, {(const void*)spmv_ws_kernel<SPMV_PLAIN, R, S, M, E>, (const void*)spmv_ws_kernel<SPMV_CG, R, S, M, E>, \
-               (const void*)spmv_ws_kernel<SPMV_BICG_V, R, S, M, E>, (const void*)spmv_ws_kernel<SPMV_BICG_T, R, S, M, E>}}
+#define WSVW(R, S, M, E, W)                                                                        \
+    {R, S, M, {(const void*)spmv_ws_kernel<SPMV_PLAIN, R, S, M, E, W>, (const void*)spmv_ws_kernel<SPMV_CG, R, S, M, E, W>, \
+               (const void*)spmv_ws_kernel<SPMV_BICG_V, R, S, M, E, W>, (const void*)spmv_ws_kernel<SPMV_BICG_T, R, S, M, E, W>}}
+#define WSV(R, S, M, E) WSVW(R, S, M, E, 8)
 #define WPV(D, M)                                                                                 \
     {0, D, M, {(const void*)spmv_wp_kernel<SPMV_PLAIN, D, M>, (const void*)spmv_wp_kernel<SPMV_CG, D, M>,  \
                (const void*)spmv_wp_kernel<SPMV_BICG_V, D, M>, (const void*)spmv_wp_kernel<SPMV_BICG_T, D, M>}}
@@ -72,18 +73,24 @@ struct WsVariant {
 // Measured on B200 (tools/spmv_sweep.py, profiles/r01_spmv_sweep.md): variant 0 is the
 // fastest on both the 7-point stencil (6.2 TB/s) and the P1 FEM matrix (5.4 TB/s).
 static const WsVariant kWsVariants[] = {WSV(1, 3, 3, true), WSV(1, 4, 2, true), WSV(1, 4, 2, false),
-                                        WSV(2, 4, 2, false), WPV(2, 3)};
+                                        WSV(2, 4, 2, false), WPV(2, 3), WSVW(1, 3, 3, true, 12),
+                                        WSVW(1, 4, 2, true, 12)};
 #undef WSV
+#undef WSVW
 #undef WPV
 constexpr int kNumWsVariants = sizeof(kWsVariants) / sizeof(kWsVariants[0]);
 
-static int ws_variant() {
-    static int v = [] {
-        const char* e = getenv("SPARSLA_WS_VARIANT");
-        int x = e ? atoi(e) : 0;
-        return (x >= 0 && x < kNumWsVariants) ? x : 0;
-    }();
-    return v;
+// Per-matrix choice (measured, profiles/r01_spmv_sweep.md): rows of <= 8 entries -> the
+// 8-wide register variant at 3 CTAs/SM; <= 12 -> the 12-wide variant at 2 CTAs/SM (FEM);
+// longer -> 8-wide with the held-stage tail path.  SPARSLA_WS_VARIANT overrides (sweeps).
+static int choose_ws_variant(long long max_row) {
+    if (const char* e = getenv("SPARSLA_WS_VARIANT")) {
+        const int x = atoi(e);
+        if (x >= 0 && x < kNumWsVariants) return x;
+    }
+    if (max_row <= 8) return 0;
+    if (max_row <= 12) return 6;
+    return 1;
 }
 
 size_t ws_smem_bytes(const DevCsr* A, int variant) {
@@ -172,7 +179,18 @@ DevCsr* DevCsr::create(int device, long long nrows, long long ncols, const I* h_
     A->max_row = mr;
     A->cap_v = (int)(((mb + 2) + 1) & ~1LL);
     A->cap_c = (int)(((mb + 6) + 3) & ~3LL);
-    A->smem_bytes = ws_smem_bytes(A.get(), ws_variant());
+    {
+        // Keep the matrix stream in L2 (evict_last) when matrix + Krylov vectors fit in it;
+        // stream it evict_first otherwise so x's reuse lines survive.  SPARSLA_L2_KEEP=0/1
+        // overrides (sweeps).
+        int l2 = 0;
+        CK(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device));
+        const double ws = 12.0 * nnz + 4.0 * nrows + 48.0 * nrows;
+        A->l2_keep = ws <= 0.9 * l2 ? 1 : 0;
+        if (const char* e = getenv("SPARSLA_L2_KEEP")) A->l2_keep = atoi(e) ? 1 : 0;
+    }
+    A->ws_var = choose_ws_variant(mr);
+    A->smem_bytes = ws_smem_bytes(A.get(), A->ws_var);
     A->staged = A->smem_bytes <= 200 * 1024;
     {
         size_t smax = 0;
@@ -266,7 +284,7 @@ DevCsr* DevCsr::get_transpose() {
 // ------------------------------------------------------------------ launches -------
 unsigned spmv_grid(const DevCsr* A, long long nch) {
     if (nch <= 0) return 0;
-    if (A->staged) return (unsigned)std::min<long long>(nch, (long long)A->ws_ctas[ws_variant()]);
+    if (A->staged) return (unsigned)std::min<long long>(nch, (long long)A->ws_ctas[A->ws_var]);
     return (unsigned)nch;
 }
 
@@ -283,12 +301,13 @@ void launch_spmv_part(DevCsr* A, cudaStream_t s, int mode, const double* x, doub
     P.nch = nch;
     P.chunk_list = list;
     P.cap_v = A->cap_v; P.cap_c = A->cap_c;
+    P.l2_keep = A->l2_keep;
     P.check_done = check_done;
     P.red = red;
     P.red.nchunks = nchunks_of(A->nrows);
     P.red.expected = expected;
     if (A->staged) {
-        const int v = ws_variant();
+        const int v = A->ws_var;
         const bool wp = kWsVariants[v].rpt == 0;
         if (wp) { P.cap_v = A->cap_v32; P.cap_c = A->cap_c32; }
         void* args[] = {&P};
@@ -314,6 +333,22 @@ void launch_spmv(DevCsr* A, cudaStream_t s, int mode, const double* x, double* y
     launch_spmv_part(A, s, mode, x, y, aux, red, check_done, nullptr, nch, spmv_grid(A, nch));
 }
 
+static int u1_group() {
+    static int g = [] {
+        const char* e = getenv("SPARSLA_U1_GROUP");
+        return e ? atoi(e) : 4;
+    }();
+    return g;
+}
+
+static bool vec_persist() {
+    static bool p = [] {
+        const char* e = getenv("SPARSLA_VEC_PERSIST");
+        return e ? atoi(e) != 0 : false;
+    }();
+    return p;
+}
+
 template <int OP>
 void launch_vec(cudaStream_t s, const VecParams& P0, RedParams red) {
     if (P0.n == 0) return;
@@ -321,7 +356,19 @@ void launch_vec(cudaStream_t s, const VecParams& P0, RedParams red) {
     P.red = red;
     P.red.nchunks = nchunks_of(P.n);
     P.red.expected = (unsigned)P.red.nchunks;
-    vec_kernel<OP><<<(unsigned)nchunks_of(P.n), kVecThreads, 0, s>>>(P);
+    const unsigned grid = (unsigned)nchunks_of(P.n);
+    if (vec_persist()) {
+        static int per_sm = -1, sms = 0;
+        if (per_sm < 0) {
+            CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, vec_kernel<OP, 4, true>, kVecThreads, 0));
+        }
+        const unsigned pg = (unsigned)std::min<long long>(grid, (long long)sms * std::max(1, per_sm));
+        P.red.expected = pg;
+        vec_kernel<OP, 4, true><<<pg, kVecThreads, 0, s>>>(P);
+    } else if (OP == V_CG_U1 && u1_group() == 2) vec_kernel<OP, 2><<<grid, kVecThreads, 0, s>>>(P);
+    else if (OP == V_CG_U1 && u1_group() == 8) vec_kernel<OP, 8><<<grid, kVecThreads, 0, s>>>(P);
+    else vec_kernel<OP><<<grid, kVecThreads, 0, s>>>(P);
     CK(cudaGetLastError());
 }
 
@@ -411,7 +458,7 @@ template <int OP>
 void Solver::vec_point(int scalar, int slot, int check_done) {
     VecParams P = vparams();
     P.check_done = check_done;
-    RedParams R = red(scalar, slot);
+    RedParams R = red(scalar, slot);  // (CG_U2 uses the slot's ticket to clear pending_x)
     constexpr int nd = VecTraits<OP>::ndot;
     if (dist && nd > 0) R.red_out = dist->red_send + slot * 8;
     launch_vec<OP>(stream, P, R);
@@ -729,6 +776,7 @@ int sparsla_dcsr_info(const sparsla_dcsr* H, int64_t* info) {
         info[0] = A->nrows; info[1] = A->ncols; info[2] = A->nnz;
         info[3] = (A->nrows + 1) * 4 + A->nnz * 12;
         info[4] = A->max_block_nnz; info[5] = A->max_row; info[6] = A->staged ? 0 : 1;
+        info[7] = A->ws_var;
     });
 }
 

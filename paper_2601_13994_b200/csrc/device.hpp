@@ -31,6 +31,8 @@ struct DevCsr {
     int cap_v32 = 0, cap_c32 = 0;  // per 32-row warp segment
     size_t smem_bytes = 0;
     bool staged = true;
+    int l2_keep = 0;  // matrix stream L2 policy (see DevCsr::create)
+    int ws_var = 0;   // staged-SpMV variant (choose_ws_variant)
     bool local_layout = false;  // rank-local [owned | halo] columns (diagonal of row i is column i)
     int ws_ctas[8] = {0};  // persistent grid per staged-SpMV variant (SMs x resident CTAs)
     double* dinv = nullptr;

@@ -46,6 +46,7 @@ struct KState {
     double tol, bnorm, rnorm, rz, alpha, beta, omega, rho, rho_prev, rho_thr, ss;
     long long k, spmv_count, breakdown_iter;
     long long reductions;  // reduction points applied while the solve was live
+    int pending_x;         // CG: alpha of this iteration computed, x += alpha p still to apply
     int done, converged, status, halfstep;
     double scratch[8];  // plain dot outputs
 };
@@ -79,7 +80,7 @@ __device__ inline void apply_scalar(int which, KState* st, const double* t) {
             st->spmv_count += 1;
             const double pq = t[0];
             if (!(pq > 0.0)) { st->status = ST_BD_PQ; st->breakdown_iter = st->k; st->done = 1; }
-            else st->alpha = st->rz / pq;
+            else { st->alpha = st->rz / pq; st->pending_x = 1; }
             break;
         }
         case SC_CG_RR: {
@@ -328,6 +329,11 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
 // TMA bulk copy global -> shared (non-tensor), completion on the mbarrier.
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
                                          uint64_t policy) {
@@ -357,6 +363,7 @@ struct SpmvParams {
     const int32_t* chunk_list;  // optional: chunk ids of this launch (interior / boundary rows)
     const double* aux;  // BICG_V: rhat, BICG_T: s
     int cap_v, cap_c;   // staged capacities (elements) per round
+    int l2_keep;        // 1: matrix stream evict_last (working set fits L2), 0: evict_first
     int check_done;
     RedParams red;
 };
@@ -455,7 +462,7 @@ struct StageLayout {
 
 // RPT: rounds (= rows per consumer thread) in flight together; STG: ring depth;
 // MINB: resident CTAs per SM requested from ptxas (register budget).
-template <int MODE, int RPT, int STG, int MINB, bool EARLY>
+template <int MODE, int RPT, int STG, int MINB, bool EARLY, int W = 8>
 __global__ void __launch_bounds__(kWsThreads, MINB) spmv_ws_kernel(SpmvParams P) {
     constexpr int ND = SpmvDots<MODE>::n;
     constexpr int NA = ND > 0 ? ND : 1;
@@ -478,7 +485,7 @@ __global__ void __launch_bounds__(kWsThreads, MINB) spmv_ws_kernel(SpmvParams P)
 
     if (warp == kConsumerWarps) {  // ------------------------------- producer warp ----
         if (lane == 0) {
-            const uint64_t pol = policy_evict_first();
+            const uint64_t pol = P.l2_keep ? policy_evict_last() : policy_evict_first();
             long long g = 0;
             for (long long c = blockIdx.x; c < P.nch; c += gridDim.x) {
                 const long long base = (P.chunk_list ? (long long)P.chunk_list[c] : P.chunk0 + c) * kChunk;
@@ -542,16 +549,16 @@ __global__ void __launch_bounds__(kWsThreads, MINB) spmv_ws_kernel(SpmvParams P)
             if constexpr (EARLY) {
                 // Copy the first 8 entries of every row to registers and release the stages
                 // before the x gathers: the ring is held only for one shared-memory read.
-                int cc[RPT][8];
-                double vv[RPT][8];
+                int cc[RPT][W];
+                double vv[RPT][W];
                 bool fits = true;
 #pragma unroll
                 for (int j = 0; j < RPT; ++j) {
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) {
+                    for (int u = 0; u < W; ++u) {
                         if (k[j] + u < ke[j]) { cc[j][u] = cs[j][k[j] + u - oc[j]]; vv[j][u] = vs[j][k[j] + u - ov[j]]; }
                     }
-                    fits &= ke[j] - k[j] <= 8;
+                    fits &= ke[j] - k[j] <= W;
                 }
                 fits = __all_sync(0xffffffffu, fits);
                 if (fits) {
@@ -562,36 +569,36 @@ __global__ void __launch_bounds__(kWsThreads, MINB) spmv_ws_kernel(SpmvParams P)
                             if (j < cnt) mbar_arrive(&empty[(g + j) % STG]);
                     }
                 }
-                double pr[RPT][8];
+                double pr[RPT][W];
 #pragma unroll
                 for (int j = 0; j < RPT; ++j)
 #pragma unroll
-                    for (int u = 0; u < 8; ++u)
+                    for (int u = 0; u < W; ++u)
                         if (k[j] + u < ke[j]) pr[j][u] = __dmul_rn(vv[j][u], __ldg(P.x + cc[j][u]));
 #pragma unroll
                 for (int j = 0; j < RPT; ++j)
 #pragma unroll
-                    for (int u = 0; u < 8; ++u)
+                    for (int u = 0; u < W; ++u)
                         if (k[j] + u < ke[j]) y[j] = __dadd_rn(y[j], pr[j][u]);
                 if (!fits) {  // long rows: finish from the (still held) stages, then release
                     bool more = false;
 #pragma unroll
-                    for (int j = 0; j < RPT; ++j) { k[j] += 8; more |= k[j] < ke[j]; }
+                    for (int j = 0; j < RPT; ++j) { k[j] += W; more |= k[j] < ke[j]; }
                     while (more) {
 #pragma unroll
                         for (int j = 0; j < RPT; ++j)
 #pragma unroll
-                            for (int u = 0; u < 8; ++u)
+                            for (int u = 0; u < W; ++u)
                                 if (k[j] + u < ke[j])
                                     pr[j][u] = __dmul_rn(vs[j][k[j] + u - ov[j]], __ldg(P.x + cs[j][k[j] + u - oc[j]]));
 #pragma unroll
                         for (int j = 0; j < RPT; ++j)
 #pragma unroll
-                            for (int u = 0; u < 8; ++u)
+                            for (int u = 0; u < W; ++u)
                                 if (k[j] + u < ke[j]) y[j] = __dadd_rn(y[j], pr[j][u]);
                         more = false;
 #pragma unroll
-                        for (int j = 0; j < RPT; ++j) { k[j] += 8; more |= k[j] < ke[j]; }
+                        for (int j = 0; j < RPT; ++j) { k[j] += W; more |= k[j] < ke[j]; }
                     }
                     __syncwarp();
                     if (lane == 0) {
@@ -809,10 +816,14 @@ __device__ __forceinline__ double lane(const double2& v, int e) { return e ? v.y
 __device__ __forceinline__ void set_lane(double2& v, int e, double x) { if (e) v.y = x; else v.x = x; }
 
 enum VecOp : int { V_CG_INIT, V_CG_U1, V_CG_U2, V_BI_INIT, V_BI_U1, V_BI_U2, V_BI_U3 };
+// CG iteration split used by the solver: U1 = r -= a q, z = d r, {r.z, r.r} (reads r q d);
+// U2 = x += a p, then p = z + b p unless the solve just terminated (reads x p r d).  p is
+// streamed once per iteration instead of twice (100 n instead of 108 n bytes); the x update
+// is the oracle's x + a p, only applied one kernel later.
 template <int OP> struct VecTraits;
 template <> struct VecTraits<V_CG_INIT> { static constexpr int nin = 3, ndot = 3; };  // b q d
-template <> struct VecTraits<V_CG_U1>   { static constexpr int nin = 5, ndot = 2; };  // x p r q d
-template <> struct VecTraits<V_CG_U2>   { static constexpr int nin = 3, ndot = 0; };  // d r p
+template <> struct VecTraits<V_CG_U1>   { static constexpr int nin = 3, ndot = 2; };  // r q d
+template <> struct VecTraits<V_CG_U2>   { static constexpr int nin = 4, ndot = 0; };  // x p r d
 template <> struct VecTraits<V_BI_INIT> { static constexpr int nin = 2, ndot = 3; };  // b v
 template <> struct VecTraits<V_BI_U1>   { static constexpr int nin = 4, ndot = 0; };  // r p v d
 template <> struct VecTraits<V_BI_U2>   { static constexpr int nin = 3, ndot = 0; };  // r v d
@@ -820,18 +831,17 @@ template <> struct VecTraits<V_BI_U3>   { static constexpr int nin = 6, ndot = 2
 
 struct VecScalars {
     double alpha, beta, omega;
-    int first, half;
+    int first, half, live;
 };
 
 template <int OP>
 __device__ __forceinline__ void vec_load(const VecParams& P, long long i, double2 (&in)[VecTraits<OP>::nin]) {
     const long long n = P.n;
     if constexpr (OP == V_CG_INIT) { in[0] = ld2(P.b, i, n); in[1] = ld2(P.q, i, n); in[2] = ld2(P.d, i, n); }
-    if constexpr (OP == V_CG_U1) {
-        in[0] = ld2(P.x, i, n); in[1] = ld2(P.p, i, n); in[2] = ld2(P.r, i, n);
-        in[3] = ld2(P.q, i, n); in[4] = ld2(P.d, i, n);
+    if constexpr (OP == V_CG_U1) { in[0] = ld2(P.r, i, n); in[1] = ld2(P.q, i, n); in[2] = ld2(P.d, i, n); }
+    if constexpr (OP == V_CG_U2) {
+        in[0] = ld2(P.x, i, n); in[1] = ld2(P.p, i, n); in[2] = ld2(P.r, i, n); in[3] = ld2(P.d, i, n);
     }
-    if constexpr (OP == V_CG_U2) { in[0] = ld2(P.d, i, n); in[1] = ld2(P.r, i, n); in[2] = ld2(P.p, i, n); }
     if constexpr (OP == V_BI_INIT) { in[0] = ld2(P.b, i, n); in[1] = ld2(P.v, i, n); }
     if constexpr (OP == V_BI_U1) {
         in[0] = ld2(P.r, i, n); in[1] = ld2(P.p, i, n); in[2] = ld2(P.v, i, n); in[3] = ld2(P.d, i, n);
@@ -859,16 +869,16 @@ __device__ __forceinline__ void vec_compute(const VecParams& P, const VecScalars
             set_lane(o0, e, r); set_lane(o1, e, z);
             pr[0][e] = __dmul_rn(r, z); pr[1][e] = __dmul_rn(r, r); pr[2][e] = __dmul_rn(b, b);
         }
-        if constexpr (OP == V_CG_U1) {  // x += a p; r -= a q; z = d r; {r.z, r.r}
-            const double xn = __dadd_rn(lane(in[0], e), __dmul_rn(S.alpha, lane(in[1], e)));
-            const double rn = __dsub_rn(lane(in[2], e), __dmul_rn(S.alpha, lane(in[3], e)));
-            const double z = __dmul_rn(lane(in[4], e), rn);
-            set_lane(o0, e, xn); set_lane(o1, e, rn);
+        if constexpr (OP == V_CG_U1) {  // r -= a q; z = d r; {r.z, r.r}
+            const double rn = __dsub_rn(lane(in[0], e), __dmul_rn(S.alpha, lane(in[1], e)));
+            const double z = __dmul_rn(lane(in[2], e), rn);
+            set_lane(o1, e, rn);
             pr[0][e] = __dmul_rn(rn, z); pr[1][e] = __dmul_rn(rn, rn);
         }
-        if constexpr (OP == V_CG_U2) {  // p = z + beta p, z = d r
-            const double z = __dmul_rn(lane(in[0], e), lane(in[1], e));
-            set_lane(o0, e, __dadd_rn(z, __dmul_rn(S.beta, lane(in[2], e))));
+        if constexpr (OP == V_CG_U2) {  // x += a p (old p); then p = z + beta p, z = d r
+            set_lane(o0, e, __dadd_rn(lane(in[0], e), __dmul_rn(S.alpha, lane(in[1], e))));
+            const double z = __dmul_rn(lane(in[3], e), lane(in[2], e));
+            set_lane(o1, e, __dadd_rn(z, __dmul_rn(S.beta, lane(in[1], e))));
         }
         if constexpr (OP == V_BI_INIT) {  // r = b - v; rhat = r; {rh.r, r.r, b.b}
             const double b = lane(in[0], e);
@@ -901,39 +911,50 @@ __device__ __forceinline__ void vec_compute(const VecParams& P, const VecScalars
         }
     }
     if constexpr (OP == V_CG_INIT) { st2(P.r, i, n, o0); st2(P.p, i, n, o1); }
-    if constexpr (OP == V_CG_U1) { st2(P.x, i, n, o0); st2(P.r, i, n, o1); }
-    if constexpr (OP == V_CG_U2) { st2(P.p, i, n, o0); }
+    if constexpr (OP == V_CG_U1) { st2(P.r, i, n, o1); }
+    if constexpr (OP == V_CG_U2) {
+        st2(P.x, i, n, o0);
+        if (S.live) st2(P.p, i, n, o1);  // the solve continues: new direction
+    }
     if constexpr (OP == V_BI_INIT) { st2(P.r, i, n, o0); st2(P.rh, i, n, o0); }
     if constexpr (OP == V_BI_U1) { st2(P.p, i, n, o0); st2(P.ph, i, n, o1); }
     if constexpr (OP == V_BI_U2) { st2(P.s, i, n, o0); st2(P.sh, i, n, o1); }
     if constexpr (OP == V_BI_U3) { st2(P.x, i, n, o0); st2(P.r, i, n, o1); }
 }
 
-template <int OP>
+template <int OP, int G = 4, bool PERSIST = false>
 __global__ void __launch_bounds__(kVecThreads) vec_kernel(VecParams P) {
     constexpr int NIN = VecTraits<OP>::nin;
     constexpr int ND = VecTraits<OP>::ndot;
     constexpr int NA = ND > 0 ? ND : 1;
-    const KState* st = P.red.st;
-    if (P.check_done && st->done) return;
+    KState* st = P.red.st;
+    if constexpr (OP == V_CG_U2) {
+        if (!st->pending_x) return;  // runs once more after termination to apply x += a p
+    } else {
+        if (P.check_done && st->done) return;
+    }
     VecScalars S;
     if constexpr (OP == V_CG_U1 || OP == V_BI_U2) S.alpha = st->alpha;
-    if constexpr (OP == V_CG_U2) S.beta = st->beta;
+    if constexpr (OP == V_CG_U2) { S.alpha = st->alpha; S.beta = st->beta; S.live = !st->done; }
     if constexpr (OP == V_BI_U1) { S.beta = st->beta; S.omega = st->omega; S.first = st->k == 0; }
     if constexpr (OP == V_BI_U3) { S.alpha = st->alpha; S.omega = st->omega; S.half = st->halfstep; }
     const int t = threadIdx.x;
-    const long long chunk = blockIdx.x;
+    __shared__ double sred[NA * (kVecThreads / 32)];
+    __shared__ int s_flag;
+    const long long nchunks = P.red.nchunks;
+    // PERSIST: a resident grid loops over chunks (one ticket per CTA); else one chunk per CTA
+    for (long long chunk = blockIdx.x; chunk < nchunks; chunk += PERSIST ? gridDim.x : nchunks) {
     const long long base = chunk * kChunk;
     double acc[NA][2];
 #pragma unroll
     for (int d = 0; d < NA; ++d) acc[d][0] = acc[d][1] = 0.0;
 #pragma unroll
-    for (int g = 0; g < kChunkRounds; g += 4) {
-        double2 in[4][NIN];
+    for (int g = 0; g < kChunkRounds; g += G) {
+        double2 in[G][NIN];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) vec_load<OP>(P, base + (long long)(g + u) * kChunkSlots + 2 * t, in[u]);
+        for (int u = 0; u < G; ++u) vec_load<OP>(P, base + (long long)(g + u) * kChunkSlots + 2 * t, in[u]);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < G; ++u) {
             const long long i = base + (long long)(g + u) * kChunkSlots + 2 * t;
             if (i >= P.n) continue;
             double pr[NA][2];
@@ -948,12 +969,33 @@ __global__ void __launch_bounds__(kVecThreads) vec_kernel(VecParams P) {
         }
     }
     if constexpr (ND > 0) {
-        __shared__ double sred[ND * (kVecThreads / 32)];
         double v[ND];
 #pragma unroll
         for (int d = 0; d < ND; ++d) v[d] = __dadd_rn(acc[d][0], acc[d][1]);  // slot pair
         block_tree<kVecThreads, ND>(v, sred);
-        publish_and_finish<kVecThreads, ND>(v, chunk, P.red, sred);
+        if constexpr (PERSIST) {
+            if (t == 0) {
+#pragma unroll
+                for (int d = 0; d < ND; ++d) P.red.partials[d * P.red.nchunks + chunk] = v[d];
+            }
+        } else {
+            publish_and_finish<kVecThreads, ND>(v, chunk, P.red, sred);
+        }
+    }
+    }  // chunk loop
+    if constexpr (ND > 0 && PERSIST) {
+        ticket_and_finish<kVecThreads, ND, 0>(P.red, sred, &s_flag);
+    } else if constexpr (OP == V_CG_U2) {
+        // the last CTA clears pending_x once every CTA has read it
+        __syncthreads();
+        if (t == 0) {
+            __threadfence();
+            if (atomicAdd(P.red.ticket, 1u) == P.red.expected - 1) {
+                st->pending_x = 0;
+                *P.red.ticket = 0u;
+                __threadfence();
+            }
+        }
     }
 }
 

@@ -256,7 +256,7 @@ class DeviceCsr:
     def info(self):
         out = np.zeros(8, np.int64)
         _check(lib().sparsla_dcsr_info(self.h, _p(out, _i64p)))
-        keys = ["nrows", "ncols", "nnz", "device_bytes", "max_block_nnz", "max_row", "variant"]
+        keys = ["nrows", "ncols", "nnz", "device_bytes", "max_block_nnz", "max_row", "variant", "ws_variant"]
         return {k: int(out[i]) for i, k in enumerate(keys)}
 
     def close(self):
