@@ -307,6 +307,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--size", type=int, default=464)
+    ap.add_argument("--config", default="B", choices=["B", "E"],
+                    help="B: 464^3 strong-scaled over N GPUs; E: 368^2 x (368 N) weak scaling (368^3 per GPU)")
     ap.add_argument("--rtol", type=float, default=1e-8)
     ap.add_argument("--max-iter", type=int, default=100000)
     ap.add_argument("--e2e-steps", type=int, default=1)

@@ -98,7 +98,8 @@ int sparsla_csr_symmetry(int64_t nrows, int64_t ncols, const int64_t* row_ptr,
 /* Problem generators (SPEC.md:551-569 + SURVEY.md §8d), emitting canonical CSR rows
  * [row_begin, row_end) directly (equal, bit for bit, to SparseCoo canonicalization of the
  * element-order triplets).  kind: 0 poisson2d(N=p1), 1 poisson3d(N=p1),
- * 2 convdiff3d(N=p1, c=fparam), 3 fem2d(m=p1, seed=p2).
+ * 2 convdiff3d(N=p1, c=fparam), 3 fem2d(m=p1, seed=p2), 4 poisson3d box N x N x Nz
+ * (N=p1, Nz=p2; the weak-scaling slabs of config E).
  * sparsla_gen_size: global n and the nnz of the row range.
  * sparsla_gen_csr: row_ptr[row_end-row_begin+1] (starts at 0), col_idx/vals[nnz]. */
 int sparsla_gen_size(int32_t kind, int64_t p1, int64_t p2, double fparam, int64_t row_begin,

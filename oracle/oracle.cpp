@@ -785,6 +785,22 @@ int orc_gen_triplets(int32_t kind, int64_t p1, int64_t p2, double fparam, int64_
                     if (y < N - 1) emit(k, k + N, -1.0);
                     if (z < N - 1) emit(k, k + N * N, -1.0);
                 }
+    } else if (kind == 4) {  // 3-D 7-pt Poisson box N x N x Nz (config E weak-scaling slabs)
+        const int64_t N = p1, Nz = p2;
+        if (N < 2 || Nz < 2) return 6;
+        *n_out = N * N * Nz;
+        for (int64_t z = 0; z < Nz; ++z)
+            for (int64_t y = 0; y < N; ++y)
+                for (int64_t x = 0; x < N; ++x) {
+                    int64_t k = (z * N + y) * N + x;
+                    if (z > 0) emit(k, k - N * N, -1.0);
+                    if (y > 0) emit(k, k - N, -1.0);
+                    if (x > 0) emit(k, k - 1, -1.0);
+                    emit(k, k, 6.0);
+                    if (x < N - 1) emit(k, k + 1, -1.0);
+                    if (y < N - 1) emit(k, k + N, -1.0);
+                    if (z < Nz - 1) emit(k, k + N * N, -1.0);
+                }
     } else if (kind == 3) {  // P1 FEM on jittered lattice, element order
         const int64_t m = p1;
         if (m < 3) return 6;

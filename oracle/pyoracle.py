@@ -229,7 +229,7 @@ def adjoint_backward(A: Csr, x, g, backend=0, atol=1e-10, rtol=0.0, max_iter=100
 
 
 # ---------------- generators ----------------
-KIND = {"poisson2d": 0, "poisson3d": 1, "convdiff3d": 2, "fem2d": 3}
+KIND = {"poisson2d": 0, "poisson3d": 1, "convdiff3d": 2, "fem2d": 3, "poisson3d_box": 4}
 
 
 def gen_triplets(kind, p1, p2=0, fparam=1.0):

@@ -38,3 +38,9 @@ def nccl_plan(kind: str, p1: int, p2: int, fparam: float, rank: int, world: int,
     rows, owned, n = local_rows(kind, p1, p2, fparam, world, rank)
     uid = share_unique_id(rank)
     return S.DistPlan.create_nccl(device, world, rank, uid, rows, owned, None, n), owned, n
+
+
+def nccl_plan_box(nx: int, ny: int, nz: int, rank: int, world: int, device: int):
+    """Config E: N x N x Nz 7-point Poisson box (nx == ny) in z-slabs, one per rank."""
+    assert nx == ny
+    return nccl_plan("poisson3d_box", nx, nz, 0.0, rank, world, device)

@@ -249,12 +249,14 @@ struct Spec {
             case 0: return p1 * p1;
             case 1: case 2: return p1 * p1 * p1;
             case 3: return (p1 - 2) * (p1 - 2);
+            case 4: return p1 * p1 * p2;
         }
         return -1;
     }
     void check() const {
-        if (kind < 0 || kind > 3) fail(SPARSLA_ERR_INVALID_ARGUMENT, "unknown generator kind");
-        if ((kind <= 2 && p1 < 2) || (kind == 3 && p1 < 3))
+        if (kind < 0 || kind > 4) fail(SPARSLA_ERR_INVALID_ARGUMENT, "unknown generator kind");
+        if (kind == 4 && p2 < 2) fail(SPARSLA_ERR_INVALID_ARGUMENT, "generator size too small (Nz >= 2)");
+        if ((kind <= 2 && p1 < 2) || (kind == 3 && p1 < 3) || (kind == 4 && p1 < 2))
             fail(SPARSLA_ERR_INVALID_ARGUMENT, "generator size too small (N >= 2, m >= 3)");
     }
     // entries of global row k, canonical order; returns count (<= 9)
@@ -268,6 +270,15 @@ struct Spec {
             put(k, 4.0);
             if (j < N - 1) put(k + 1, -1.0);
             if (i < N - 1) put(k + N, -1.0);
+        } else if (kind == 4) {  // N x N x Nz box (weak-scaling slabs, config E)
+            const int64_t N = p1, NN = N * N, Nz = p2, z = k / NN, y = (k / N) % N, x = k % N;
+            if (z > 0) put(k - NN, -1.0);
+            if (y > 0) put(k - N, -1.0);
+            if (x > 0) put(k - 1, -1.0);
+            put(k, 6.0);
+            if (x < N - 1) put(k + 1, -1.0);
+            if (y < N - 1) put(k + N, -1.0);
+            if (z < Nz - 1) put(k + NN, -1.0);
         } else if (kind == 1 || kind == 2) {
             const int64_t N = p1, NN = N * N, z = k / NN, y = (k / N) % N, x = k % N;
             const double c = fparam;
@@ -320,6 +331,19 @@ int64_t count(const Spec& s, int64_t r0, int64_t r1) {
             t += 1 + (i > 0) + (j > 0) + (j < N - 1) + (i < N - 1);
         }
         return t;
+    }
+    if (s.kind == 4) {
+        const int64_t N = s.p1, Nz = s.p2;
+        std::atomic<int64_t> tot{0};
+        parallel_for(r1 - r0, [&](int64_t a, int64_t b) {
+            int64_t t = 0;
+            for (int64_t k = r0 + a; k < r0 + b; ++k) {
+                const int64_t z = k / (N * N), y = (k / N) % N, x = k % N;
+                t += 1 + (z > 0) + (y > 0) + (x > 0) + (x < N - 1) + (y < N - 1) + (z < Nz - 1);
+            }
+            tot += t;
+        });
+        return tot.load();
     }
     if (s.kind == 1 || s.kind == 2) {
         const int64_t N = s.p1;

@@ -31,7 +31,10 @@ def run(args, metric):
         os.environ.setdefault("MASTER_PORT", "29533")
         dist.init_process_group("gloo", rank=rank, world_size=world)
     t0 = time.time()
-    plan, owned, n = bootstrap.nccl_plan("poisson3d", args.size, 0, 0.0, rank, world, local)
+    if getattr(args, "config", "B") == "E":  # weak scaling: 368 x 368 x (368 P) z-slab grid
+        plan, owned, n = bootstrap.nccl_plan_box(368, 368, 368 * world, rank, world, local)
+    else:
+        plan, owned, n = bootstrap.nccl_plan("poisson3d", args.size, 0, 0.0, rank, world, local)
     tsetup = time.time() - t0
     info = plan.info()
     opts = S.SolveOptions(atol=0.0, rtol=args.rtol, max_iter=args.max_iter)
@@ -94,9 +97,12 @@ def run(args, metric):
         line = {
             "metric": metric, "value": args.steps / (ms / 1e3), "unit": "it/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "weak" if getattr(args, "config", "B") == "E" else "strong",
+            "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (generated 3-D Poisson, b = ones)",
-            "config": {"workload": f"B: 3-D 7-pt Poisson {args.size}^3 ({n} DOF), Jacobi-PCG rtol {args.rtol}",
+            "config": {"workload": (f"E: 3-D 7-pt Poisson 368x368x{368 * world} ({n} DOF, 368^3 per GPU)"
+                                    if getattr(args, "config", "B") == "E" else
+                                    f"B: 3-D 7-pt Poisson {args.size}^3 ({n} DOF)") + f", Jacobi-PCG rtol {args.rtol}",
                        "n": n, "partition": f"contiguous z-slabs x{world}", "parallelism": f"dp{world} (row partition)",
                        "n_owned_rank0": no, "halo_rank0": nh, "interior_chunks": info["interior_chunks"],
                        "boundary_chunks": info["boundary_chunks"],

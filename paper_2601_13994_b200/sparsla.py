@@ -522,7 +522,7 @@ class Solver:
 
 
 # ---------------------------------------------------------------------- generators ---
-KIND = {"poisson2d": 0, "poisson3d": 1, "convdiff3d": 2, "fem2d": 3}
+KIND = {"poisson2d": 0, "poisson3d": 1, "convdiff3d": 2, "fem2d": 3, "poisson3d_box": 4}
 
 
 def gen_size(kind, p1, p2=0, fparam=1.0, row_begin=0, row_end=None):

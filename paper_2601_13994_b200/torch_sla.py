@@ -1,0 +1,147 @@
+"""torch-sla style autograd binding.
+
+    A = SparseTensor(values, row, col, (n, n))      # values: torch tensor (requires_grad ok)
+    x = A.solve(b, atol=..., rtol=...)              # differentiable w.r.t. values and b
+    loss(x).backward()                              # one adjoint solve (Alg. 1, Eq. 3)
+
+Forward and backward run on the sm_100a Krylov loop through the C ABI with zero-copy device
+pointers (SPARSLA_MEM_DEVICE).  Backward is exactly one transposed solve plus the per-entry
+gather grad_vals[k] = -lambda[row_k] * x[col_k] (solve_backward); the
+saved state is (pattern, values, x) only — no per-iteration tape (Theorem 1).  Input
+triplets may be unsorted / duplicated: the pattern is canonicalised like SparseCoo
+(sparse.cpp:9-53, duplicates summed in input order on the host-defined permutation) and the
+gradient of every duplicate is the gradient of its canonical entry.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import sparsla as S
+
+
+class SparseTensor:
+    def __init__(self, values: torch.Tensor, row, col, shape, device: int | None = None):
+        row = np.ascontiguousarray(torch.as_tensor(row).cpu().numpy(), np.int64)
+        col = np.ascontiguousarray(torch.as_tensor(col).cpu().numpy(), np.int64)
+        if values.dim() != 1 or values.numel() != len(row) or len(row) != len(col):
+            raise S.DimensionError("values, row and col must be 1-D of equal length")
+        if values.dtype != torch.float64:
+            raise S.InvalidArgumentError("torch-sla B200 path computes in float64")
+        n, m = int(shape[0]), int(shape[1])
+        # canonical pattern + map input entry -> canonical entry (host, SparseCoo order)
+        order = np.lexsort((np.arange(len(row)), col, row))  # stable by (row, col, input index)
+        r_s, c_s = row[order], col[order]
+        new = np.ones(len(order), bool)
+        if len(order):
+            new[1:] = (r_s[1:] != r_s[:-1]) | (c_s[1:] != c_s[:-1])
+        group = np.cumsum(new) - 1
+        self._group_of_input = np.empty(len(row), np.int64)
+        self._group_of_input[order] = group
+        self._order = order
+        coo = S.SparseCoo(r_s[new], c_s[new], np.zeros(int(new.sum())), (n, m))  # pattern check
+        self.csr = S.CsrMatrix.from_coo(coo)
+        self.shape = (n, m)
+        self.values = values
+        self.device = values.device.index if values.is_cuda else (device or 0)
+        self._dup = bool((~new).any())
+        self._order_t = None
+        self._group_t = None
+
+    @property
+    def nnz(self):
+        return self.csr.nnz
+
+    def canonical_values(self) -> torch.Tensor:
+        """Values in canonical entry order; duplicates summed in input order (SparseCoo)."""
+        v = self.values
+        if not v.is_cuda:
+            v = v.to(f"cuda:{self.device}")
+        if not self._dup:
+            if self._order_t is None:
+                self._order_t = torch.as_tensor(self._order, device=v.device)
+            return v[self._order_t]
+        # duplicates: sequential per-entry sums in input order (deterministic, exact order)
+        return _DupSum.apply(v, self)
+
+    def solve(self, b: torch.Tensor, atol: float = 1e-10, rtol: float = 0.0, max_iter: int = 10000,
+              preconditioner: str = "jacobi", backend: str = "auto") -> torch.Tensor:
+        if backend == "auto":
+            backend = "cg" if S.is_structurally_symmetric(self.csr.to_coo()) else "bicgstab"
+        opts = S.SolveOptions(atol=atol, rtol=rtol, max_iter=max_iter, preconditioner=preconditioner)
+        return _Solve.apply(self.canonical_values(), b, self, opts, backend)
+
+
+class _DupSum(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, v, A):
+        order = A._order
+        grp = A._group_of_input[order]
+        vs = v.detach().cpu().numpy()[order]
+        out = np.empty(A.nnz)
+        k = -1
+        for i, g in enumerate(grp):  # vals_.back() += vals[p] in stable (row, col, input) order
+            if g != k:
+                out[g] = vs[i]
+                k = g
+            else:
+                out[g] += vs[i]
+        ctx.A = A
+        return torch.as_tensor(out, device=v.device)
+
+    @staticmethod
+    def backward(ctx, g):
+        idx = torch.as_tensor(ctx.A._group_of_input, device=g.device)
+        return g[idx], None
+
+
+def _ptr(t: torch.Tensor):
+    return C.cast(C.c_void_p(t.data_ptr()), S._f64p)
+
+
+class _Solve(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, vals, b, A: SparseTensor, opts: S.SolveOptions, backend: str):
+        dev = A.device
+        vals = vals.detach().to(f"cuda:{dev}", torch.float64).contiguous()
+        b = b.detach().to(f"cuda:{dev}", torch.float64).contiguous()
+        if b.numel() != A.shape[0]:
+            raise S.DimensionError("rhs length mismatch")
+        D = A.csr.device(dev)
+        torch.cuda.current_stream(dev).synchronize()  # the library runs on its own stream
+        S._check(S.lib().sparsla_dcsr_set_values(D.h, _ptr(vals), C.c_int32(S.MEM_DEVICE)))
+        x = torch.empty_like(b)
+        rep = S._Report()
+        o = opts.c()
+        fn = S.lib().sparsla_cg_solve if backend == "cg" else S.lib().sparsla_bicgstab_solve
+        S._check(fn(D.h, _ptr(b), _ptr(x), C.byref(o), C.byref(rep), C.c_int32(S.MEM_DEVICE)))
+        r = S.SolveReport._from(rep)
+        if not r.converged:
+            raise S.Error(f"solve did not converge: {r.diagnostic}")
+        ctx.A, ctx.opts, ctx.backend = A, opts, backend
+        ctx.save_for_backward(vals, x)
+        ctx.report = r
+        return x
+
+    @staticmethod
+    def backward(ctx, gx):
+        vals, x = ctx.saved_tensors
+        A = ctx.A
+        D = A.csr.device(A.device)
+        gx = gx.detach().to(x.device, torch.float64).contiguous()
+        torch.cuda.current_stream(A.device).synchronize()
+        # the matrix handle may hold other values since forward: restore this solve's A
+        S._check(S.lib().sparsla_dcsr_set_values(D.h, _ptr(vals), C.c_int32(S.MEM_DEVICE)))
+        gb = torch.empty_like(x)
+        gv = torch.empty(A.nnz, dtype=torch.float64, device=x.device)
+        rep = S._Report()
+        o = ctx.opts.c()
+        be = S.BACKEND_CG if ctx.backend == "cg" else S.BACKEND_BICGSTAB
+        S._check(S.lib().sparsla_adjoint_backward(D.h, _ptr(x), _ptr(gx), C.c_int32(be), C.byref(o), _ptr(gb),
+                                                  _ptr(gv), C.byref(rep), C.c_int32(S.MEM_DEVICE)))
+        r = S.SolveReport._from(rep)
+        if not r.converged:
+            raise S.Error(f"adjoint solve did not converge: {r.diagnostic}")
+        return gv, gb, None, None, None

@@ -94,7 +94,7 @@ def coo_of(A):
 @pytest.mark.parametrize("kind,p1,p2,fp", [("poisson2d", 33, 0, 0.0), ("poisson3d", 11, 0, 0.0),
                                            ("convdiff3d", 9, 0, 1.0), ("convdiff3d", 7, 0, 0.37),
                                            ("fem2d", 3, 2601, 0.0), ("fem2d", 57, 2601, 0.0),
-                                           ("fem2d", 40, 7, 0.0)])
+                                           ("fem2d", 40, 7, 0.0), ("poisson3d_box", 6, 17, 0.0)])
 def test_generators_bitwise_vs_oracle(S, O, kind, p1, p2, fp):
     A = S.generate(kind, p1, p2, fp)
     B = O.generate(kind, p1, p2, fp)
