@@ -137,6 +137,19 @@ int sparsla_local_get(const sparsla_local* L, int64_t* owned, int64_t* halo, int
                       double* l_vals);
 int sparsla_local_destroy(sparsla_local* L);
 
+/* Matrix Market coordinate I/O (matrix_market.hpp:10-20): real
+ * general|symmetric, '%' comments, 1-based -> 0-based, symmetric expanded, result
+ * canonical (SparseCoo).  SPARSLA_ERR_FORMAT with "(line N)" on malformed input.  The writer
+ * emits coordinate/real/general with 17 significant digits (bit-exact round trip). */
+typedef struct sparsla_coo sparsla_coo;
+int sparsla_mtx_read(const char* path, sparsla_coo** out);
+int sparsla_mtx_read_buffer(const char* data, int64_t len, sparsla_coo** out);
+int sparsla_coo_sizes(const sparsla_coo* coo, int64_t* nrows, int64_t* ncols, int64_t* nnz);
+int sparsla_coo_get(const sparsla_coo* coo, int64_t* rows, int64_t* cols, double* vals);
+int sparsla_coo_destroy(sparsla_coo* coo);
+int sparsla_mtx_write(const char* path, int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* rows,
+                      const int64_t* cols, const double* vals);
+
 /* ============================ device CSR (one GPU) =================================== */
 typedef struct sparsla_dcsr sparsla_dcsr;
 

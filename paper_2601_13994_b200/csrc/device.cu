@@ -60,14 +60,19 @@ static inline long long nchunks_of(long long n) { return (n + kChunk - 1) / kChu
 // Variant 0 is the default; SPARSLA_WS_VARIANT selects another for sweeps.
 struct WsVariant {
     int rpt, stg, minb;
-    const void* fn[4];  // per SpmvMode
+    const void* fn[4];      // per SpmvMode
+    const void* fn_hub[4];  // same, with the oversized-round bypass compiled in
 };
 #define WSVW(R, S, M, E, W)                                                                        \
     {R, S, M, {(const void*)spmv_ws_kernel<SPMV_PLAIN, R, S, M, E, W>, (const void*)spmv_ws_kernel<SPMV_CG, R, S, M, E, W>, \
-               (const void*)spmv_ws_kernel<SPMV_BICG_V, R, S, M, E, W>, (const void*)spmv_ws_kernel<SPMV_BICG_T, R, S, M, E, W>}}
+               (const void*)spmv_ws_kernel<SPMV_BICG_V, R, S, M, E, W>, (const void*)spmv_ws_kernel<SPMV_BICG_T, R, S, M, E, W>}, \
+              {(const void*)spmv_ws_kernel<SPMV_PLAIN, R, S, M, E, W, true>, (const void*)spmv_ws_kernel<SPMV_CG, R, S, M, E, W, true>, \
+               (const void*)spmv_ws_kernel<SPMV_BICG_V, R, S, M, E, W, true>, (const void*)spmv_ws_kernel<SPMV_BICG_T, R, S, M, E, W, true>}}
 #define WSV(R, S, M, E) WSVW(R, S, M, E, 8)
 #define WPV(D, M)                                                                                 \
     {0, D, M, {(const void*)spmv_wp_kernel<SPMV_PLAIN, D, M>, (const void*)spmv_wp_kernel<SPMV_CG, D, M>,  \
+               (const void*)spmv_wp_kernel<SPMV_BICG_V, D, M>, (const void*)spmv_wp_kernel<SPMV_BICG_T, D, M>}, \
+              {(const void*)spmv_wp_kernel<SPMV_PLAIN, D, M>, (const void*)spmv_wp_kernel<SPMV_CG, D, M>,  \
                (const void*)spmv_wp_kernel<SPMV_BICG_V, D, M>, (const void*)spmv_wp_kernel<SPMV_BICG_T, D, M>}}
 // rpt == 0 marks the warp-pipelined kernel (stg = per-warp ring depth)
 // Measured on B200 (tools/spmv_sweep.py, profiles/r01_spmv_sweep.md): variant 0 is the
@@ -101,8 +106,10 @@ size_t ws_smem_bytes(const DevCsr* A, int variant) {
 
 static void configure_ws_variants(int device) {
     for (int v = 0; v < kNumWsVariants; ++v)
-        for (int m = 0; m < 4; ++m)
+        for (int m = 0; m < 4; ++m) {
             CK(cudaFuncSetAttribute(kWsVariants[v].fn[m], cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+            CK(cudaFuncSetAttribute(kWsVariants[v].fn_hub[m], cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        }
     (void)device;
 }
 
@@ -179,6 +186,23 @@ DevCsr* DevCsr::create(int device, long long nrows, long long ncols, const I* h_
     A->max_row = mr;
     A->cap_v = (int)(((mb + 2) + 1) & ~1LL);
     A->cap_c = (int)(((mb + 6) + 3) & ~3LL);
+    A->ws_var = choose_ws_variant(mr);
+    {
+        // Size the ring for the chosen variant's occupancy; rounds above the resulting
+        // capacity (hub rows) bypass the ring inside the kernel instead of demoting the
+        // whole matrix to the direct kernel.
+        const WsVariant& V = kWsVariants[A->ws_var];
+        if (V.rpt != 0) {
+            const long long per_cta = 227LL * 1024 / V.minb - 1024 - 256 - 256;
+            const long long stage_budget = per_cta / V.stg;
+            const long long cap = (stage_budget - 2 * 128 - ((kRpCopy + 1) * 4 + 127)) / 12;
+            if (cap < A->cap_v) {
+                A->cap_v = (int)(cap & ~1LL);
+                A->cap_c = (int)(cap & ~3LL);
+                A->has_hub = true;  // some rounds exceed the stage: use the bypass kernels
+            }
+        }
+    }
     {
         // Keep the matrix stream in L2 (evict_last) when matrix + Krylov vectors fit in it;
         // stream it evict_first otherwise so x's reuse lines survive.  SPARSLA_L2_KEEP=0/1
@@ -189,14 +213,9 @@ DevCsr* DevCsr::create(int device, long long nrows, long long ncols, const I* h_
         A->l2_keep = ws <= 0.9 * l2 ? 1 : 0;
         if (const char* e = getenv("SPARSLA_L2_KEEP")) A->l2_keep = atoi(e) ? 1 : 0;
     }
-    A->ws_var = choose_ws_variant(mr);
     A->smem_bytes = ws_smem_bytes(A.get(), A->ws_var);
-    A->staged = A->smem_bytes <= 200 * 1024;
-    {
-        size_t smax = 0;
-        for (int v = 0; v < kNumWsVariants; ++v) smax = std::max(smax, ws_smem_bytes(A.get(), v));
-        if (smax > 200 * 1024) A->staged = false;  // keep every variant launchable
-    }
+    A->staged = A->cap_v >= 512 && A->smem_bytes <= 200 * 1024;  // else: direct kernel
+    if (const char* e = getenv("SPARSLA_SPMV_DIRECT")) if (atoi(e)) A->staged = false;
     {
         int sms = 0;
         CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
@@ -311,8 +330,8 @@ void launch_spmv_part(DevCsr* A, cudaStream_t s, int mode, const double* x, doub
         const bool wp = kWsVariants[v].rpt == 0;
         if (wp) { P.cap_v = A->cap_v32; P.cap_c = A->cap_c32; }
         void* args[] = {&P};
-        CK(cudaLaunchKernel(kWsVariants[v].fn[mode], dim3(grid), dim3(wp ? kSpmvThreads : kWsThreads), args,
-                            ws_smem_bytes(A, v), s));
+        const void* fn = A->has_hub ? kWsVariants[v].fn_hub[mode] : kWsVariants[v].fn[mode];
+        CK(cudaLaunchKernel(fn, dim3(grid), dim3(wp ? kSpmvThreads : kWsThreads), args, ws_smem_bytes(A, v), s));
     } else {
 #define DIRECT_CASE(M) spmv_direct_kernel<M><<<grid, kSpmvThreads, 0, s>>>(P);
         switch (mode) {

@@ -33,6 +33,7 @@ struct DevCsr {
     bool staged = true;
     int l2_keep = 0;  // matrix stream L2 policy (see DevCsr::create)
     int ws_var = 0;   // staged-SpMV variant (choose_ws_variant)
+    bool has_hub = false;  // rounds above the stage capacity exist (bypass kernels)
     bool local_layout = false;  // rank-local [owned | halo] columns (diagonal of row i is column i)
     int ws_ctas[8] = {0};  // persistent grid per staged-SpMV variant (SMs x resident CTAs)
     double* dinv = nullptr;

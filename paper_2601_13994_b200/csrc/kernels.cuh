@@ -462,7 +462,7 @@ struct StageLayout {
 
 // RPT: rounds (= rows per consumer thread) in flight together; STG: ring depth;
 // MINB: resident CTAs per SM requested from ptxas (register budget).
-template <int MODE, int RPT, int STG, int MINB, bool EARLY, int W = 8>
+template <int MODE, int RPT, int STG, int MINB, bool EARLY, int W = 8, bool HUB = false>
 __global__ void __launch_bounds__(kWsThreads, MINB) spmv_ws_kernel(SpmvParams P) {
     constexpr int ND = SpmvDots<MODE>::n;
     constexpr int NA = ND > 0 ? ND : 1;
@@ -499,8 +499,13 @@ __global__ void __launch_bounds__(kWsThreads, MINB) spmv_ws_kernel(SpmvParams P)
                     const int nz0 = __ldg(P.rp + rs), nz1 = __ldg(P.rp + re);
                     const int a0 = nz0 & ~1, a1 = (nz1 + 1) & ~1;
                     const int c0 = nz0 & ~3, c1 = (nz1 + 3) & ~3;
-                    const uint32_t vb = (uint32_t)(a1 - a0) * 8u, cb = (uint32_t)(c1 - c0) * 4u;
+                    // rounds larger than the ring's stage (hub rows of irregular matrices)
+                    // bypass it: only row_ptr is staged, col/val are read from global
+                    const bool big = HUB && (a1 - a0 > P.cap_v || c1 - c0 > P.cap_c);
+                    const uint32_t vb = big ? 0u : (uint32_t)(a1 - a0) * 8u;
+                    const uint32_t cb = big ? 0u : (uint32_t)(c1 - c0) * 4u;
                     unsigned char* st = stage0 + s * L.stage;
+                    reinterpret_cast<int32_t*>(st + L.vbytes + L.cbytes)[kRpCopy] = big ? 1 : 0;
                     mbar_arrive_expect_tx(&full[s], (uint32_t)(kRpCopy * 4) + vb + cb);
                     bulk_g2s(st + L.vbytes + L.cbytes, P.rp + rs, kRpCopy * 4, &full[s], pol);
                     if (vb) bulk_g2s(st, P.val + a0, vb, &full[s], pol);
@@ -526,12 +531,13 @@ __global__ void __launch_bounds__(kWsThreads, MINB) spmv_ws_kernel(SpmvParams P)
         for (int r = 0; r < nr; r += RPT) {
             const int cnt = nr - r < RPT ? nr - r : RPT;
             int k[RPT], ke[RPT], ov[RPT], oc[RPT];
+            bool big[RPT];
             const double* vs[RPT];
             const int32_t* cs[RPT];
             double y[RPT];
 #pragma unroll
             for (int j = 0; j < RPT; ++j) {
-                k[j] = 0; ke[j] = 0; ov[j] = 0; oc[j] = 0; y[j] = 0.0;
+                k[j] = 0; ke[j] = 0; ov[j] = 0; oc[j] = 0; y[j] = 0.0; big[j] = false;
                 const int s = (int)((g + j) % STG);
                 const unsigned char* A = stage0 + s * L.stage;
                 vs[j] = reinterpret_cast<const double*>(A);
@@ -539,8 +545,9 @@ __global__ void __launch_bounds__(kWsThreads, MINB) spmv_ws_kernel(SpmvParams P)
                 if (j < cnt) {
                     mbar_wait(&full[s], (uint32_t)(((g + j) / STG) & 1));
                     const long long row = base + (long long)(r + j) * kChunkSlots + t;
+                    const int32_t* rps = reinterpret_cast<const int32_t*>(A + L.vbytes + L.cbytes);
+                    if constexpr (HUB) big[j] = rps[kRpCopy] != 0;  // oversized round: col/val from global
                     if (row < P.n) {
-                        const int32_t* rps = reinterpret_cast<const int32_t*>(A + L.vbytes + L.cbytes);
                         k[j] = rps[t]; ke[j] = rps[t + 1];
                         ov[j] = rps[0] & ~1; oc[j] = rps[0] & ~3;
                     }
@@ -554,9 +561,14 @@ __global__ void __launch_bounds__(kWsThreads, MINB) spmv_ws_kernel(SpmvParams P)
                 bool fits = true;
 #pragma unroll
                 for (int j = 0; j < RPT; ++j) {
+                    if (!HUB || !big[j]) {
 #pragma unroll
-                    for (int u = 0; u < W; ++u) {
-                        if (k[j] + u < ke[j]) { cc[j][u] = cs[j][k[j] + u - oc[j]]; vv[j][u] = vs[j][k[j] + u - ov[j]]; }
+                        for (int u = 0; u < W; ++u)
+                            if (k[j] + u < ke[j]) { cc[j][u] = cs[j][k[j] + u - oc[j]]; vv[j][u] = vs[j][k[j] + u - ov[j]]; }
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < W; ++u)
+                            if (k[j] + u < ke[j]) { cc[j][u] = __ldg(P.ci + k[j] + u); vv[j][u] = __ldg(P.val + k[j] + u); }
                     }
                     fits &= ke[j] - k[j] <= W;
                 }
@@ -589,8 +601,12 @@ __global__ void __launch_bounds__(kWsThreads, MINB) spmv_ws_kernel(SpmvParams P)
                         for (int j = 0; j < RPT; ++j)
 #pragma unroll
                             for (int u = 0; u < W; ++u)
-                                if (k[j] + u < ke[j])
-                                    pr[j][u] = __dmul_rn(vs[j][k[j] + u - ov[j]], __ldg(P.x + cs[j][k[j] + u - oc[j]]));
+                                if (k[j] + u < ke[j]) {
+                                    const int kk = k[j] + u;
+                                    const double vvv = (HUB && big[j]) ? __ldg(P.val + kk) : vs[j][kk - ov[j]];
+                                    const int ccc = (HUB && big[j]) ? __ldg(P.ci + kk) : cs[j][kk - oc[j]];
+                                    pr[j][u] = __dmul_rn(vvv, __ldg(P.x + ccc));
+                                }
 #pragma unroll
                         for (int j = 0; j < RPT; ++j)
 #pragma unroll
@@ -615,8 +631,12 @@ __global__ void __launch_bounds__(kWsThreads, MINB) spmv_ws_kernel(SpmvParams P)
                 for (int j = 0; j < RPT; ++j)
 #pragma unroll
                     for (int u = 0; u < 8; ++u)
-                        if (k[j] + u < ke[j])
-                            pr[j][u] = __dmul_rn(vs[j][k[j] + u - ov[j]], __ldg(P.x + cs[j][k[j] + u - oc[j]]));
+                        if (k[j] + u < ke[j]) {
+                            const int kk = k[j] + u;
+                            const double vvv = (HUB && big[j]) ? __ldg(P.val + kk) : vs[j][kk - ov[j]];
+                            const int ccc = (HUB && big[j]) ? __ldg(P.ci + kk) : cs[j][kk - oc[j]];
+                            pr[j][u] = __dmul_rn(vvv, __ldg(P.x + ccc));
+                        }
 #pragma unroll
                 for (int j = 0; j < RPT; ++j)
 #pragma unroll

@@ -311,6 +311,35 @@ def _symmetry(a: SparseCoo, tol):
     return bool(s1.value), bool(s2.value)
 
 
+def _coo_from_handle(h) -> SparseCoo:
+    nr, nc, nz = C.c_int64(), C.c_int64(), C.c_int64()
+    try:
+        _check(lib().sparsla_coo_sizes(h, C.byref(nr), C.byref(nc), C.byref(nz)))
+        r, c, v = np.empty(nz.value, np.int64), np.empty(nz.value, np.int64), np.empty(nz.value)
+        _check(lib().sparsla_coo_get(h, _p(r, _i64p), _p(c, _i64p), _p(v, _f64p)))
+    finally:
+        lib().sparsla_coo_destroy(h)
+    return SparseCoo(r, c, v, Shape(nr.value, nc.value), _canonical=True)
+
+
+def read_matrix_market(src) -> SparseCoo:
+    """read_matrix_market (matrix_market.hpp:10-15): a path, or a text/bytes buffer."""
+    h = _vp()
+    if isinstance(src, (bytes, bytearray)) or (isinstance(src, str) and src.startswith("%%MatrixMarket")):
+        data = src.encode() if isinstance(src, str) else bytes(src)
+        _check(lib().sparsla_mtx_read_buffer(data, C.c_int64(len(data)), C.byref(h)))
+    else:
+        _check(lib().sparsla_mtx_read(os.fsencode(src), C.byref(h)))
+    return _coo_from_handle(h)
+
+
+def write_matrix_market(a: SparseCoo, path):
+    """write_matrix_market (matrix_market.hpp:17-20): coordinate/real/general, %.17g."""
+    _check(lib().sparsla_mtx_write(os.fsencode(path), C.c_int64(a.nrows), C.c_int64(a.ncols),
+                                   C.c_int64(a.nnz), _p(_i64(a.rows), _i64p), _p(_i64(a.cols), _i64p),
+                                   _p(_f64(a.vals), _f64p)))
+
+
 def is_structurally_symmetric(a: SparseCoo) -> bool:
     return _symmetry(a, 0.0)[0]
 

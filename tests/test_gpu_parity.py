@@ -80,12 +80,30 @@ def test_spmv_random_rectangular_and_ragged(S, O, gpu, seed):
     assert_bitwise(S.spmv_transpose(D, y), O.spmv(O.transpose(A), y))
 
 
-def test_spmv_long_rows_direct_variant(S, O, gpu):
-    A = random_csr(O, 700, 5000, 5, 3, long_rows={3: 4000, 500: 4500})  # > smem staging
+def test_spmv_long_rows_hub_bypass(S, O, gpu):
+    """Rounds larger than a ring stage (hub rows) bypass the smem ring inside the staged
+    kernel; everything stays bit-exact, incl. the fused dot and CG."""
+    A = random_csr(O, 5000, 5000, 5, 3, long_rows={3: 4000, 500: 4500, 4999: 3000})
     D = to_S(S, A).device(0)
-    assert D.info()["variant"] == 1
+    assert D.info()["variant"] == 0
     x = np.random.default_rng(3).standard_normal(A.ncols)
     assert_bitwise(S.spmv(D, x), O.spmv(A, x))
+
+
+def test_spmv_direct_kernel(S, O, gpu, monkeypatch):
+    monkeypatch.setenv("SPARSLA_SPMV_DIRECT", "1")
+    A = random_csr(O, 3100, 3000, 9, 4, long_rows={7: 2500})
+    D = to_S(S, A).device(0)
+    assert D.info()["variant"] == 1
+    x = np.random.default_rng(4).standard_normal(A.ncols)
+    assert_bitwise(S.spmv(D, x), O.spmv(A, x))
+    P = O.generate("poisson2d", 50)
+    DP = to_S(S, P).device(0)
+    b = np.ones(P.nrows)
+    xo, ro = O.cg(P, b, atol=0.0, rtol=1e-9)
+    xg, rg = S.cg_solve(DP, b, S.SolveOptions(atol=0.0, rtol=1e-9))
+    rep_eq(rg, ro)
+    assert_bitwise(xg, xo)
 
 
 @pytest.mark.parametrize("n", [1, 2, 3, 2047, 2048, 2049, 4097, 300001, 2_100_000])
