@@ -234,6 +234,7 @@ template DevCsr* DevCsr::create<int64_t>(int, long long, long long, const int64_
 template DevCsr* DevCsr::create<int32_t>(int, long long, long long, const int32_t*, const int32_t*, const double*, bool);
 
 const double* DevCsr::jacobi_dinv() {
+    std::lock_guard<std::mutex> lk(lazy_mu);
     if (!dinv) {
         DeviceGuard g(device);
         if (nrows != ncols && !local_layout) fail(SPARSLA_ERR_DIMENSION, "jacobi_build requires a square matrix");
@@ -247,6 +248,7 @@ const double* DevCsr::jacobi_dinv() {
 }
 
 const double* DevCsr::ones_vec() {
+    std::lock_guard<std::mutex> lk(lazy_mu);
     if (!ones) {
         DeviceGuard g(device);
         ones = dalloc<double>(nrows + 2);
@@ -258,6 +260,7 @@ const double* DevCsr::ones_vec() {
 }
 
 bool DevCsr::exactly_symmetric() {
+    std::lock_guard<std::mutex> lk(lazy_mu);
     if (sym_checked < 0) {
         DeviceGuard g(device);
         if (nrows != ncols) { sym_checked = 0; return false; }
@@ -277,6 +280,7 @@ bool DevCsr::exactly_symmetric() {
 
 // canonical A^T (setup, nonsymmetric adjoint / spmv_transpose)
 DevCsr* DevCsr::get_transpose() {
+    std::lock_guard<std::mutex> lk(lazy_mu);
     if (!transpose) {
         DeviceGuard g(device);
         std::vector<int32_t> hrp(nrows + 1), hci(nnz);
@@ -377,11 +381,10 @@ void launch_vec(cudaStream_t s, const VecParams& P0, RedParams red) {
     P.red.expected = (unsigned)P.red.nchunks;
     const unsigned grid = (unsigned)nchunks_of(P.n);
     if (vec_persist()) {
-        static int per_sm = -1, sms = 0;
-        if (per_sm < 0) {
-            CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, vec_kernel<OP, 4, true>, kVecThreads, 0));
-        }
+        int dev = 0, per_sm = 0, sms = 0;
+        CK(cudaGetDevice(&dev));
+        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, vec_kernel<OP, 4, true>, kVecThreads, 0));
         const unsigned pg = (unsigned)std::min<long long>(grid, (long long)sms * std::max(1, per_sm));
         P.red.expected = pg;
         vec_kernel<OP, 4, true><<<pg, kVecThreads, 0, s>>>(P);
@@ -407,6 +410,7 @@ Solver::Solver(DevCsr* A_, int backend_, const sparsla_solve_options& o, DistCtx
     const long long m = std::max<long long>(1, nchunks_of(n));
     const long long nv = n + 2;
     const long long nh = (dist ? dist->n_halo : 0) + nv;  // SpMV inputs carry the halo slots
+    try {
     x_own = dalloc<double>(nv); b_own = dalloc<double>(nv);
     r = dalloc<double>(nv); p = dalloc<double>(nh); q = dalloc<double>(nv);
     if (backend == SPARSLA_BACKEND_BICGSTAB) {
@@ -414,6 +418,18 @@ Solver::Solver(DevCsr* A_, int backend_, const sparsla_solve_options& o, DistCtx
         sh = dalloc<double>(nh); t = dalloc<double>(nv);
     }
     partials = dalloc<double>(3 * m);
+    // small single-GPU CG problems: whole iterations in one cooperative kernel
+    if (!dist && backend == SPARSLA_BACKEND_CG && n > 0) {
+        int coop = 0, sms = 0, per_sm = 0;
+        CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, A->device));
+        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, A->device));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cg_fused_kernel, kSpmvThreads, 0));
+        const long long cap = (long long)sms * per_sm;
+        fused_grid = (int)std::min<long long>(m, cap);
+        fused = coop && cap > 0 && m <= cap;  // one chunk per CTA (measured: 2 per CTA ~ break-even)
+        if (const char* e = getenv("SPARSLA_FUSED")) fused = coop && cap > 0 && atoi(e) != 0;
+        if (fused) { fused_bar = dalloc<unsigned>(1); }
+    }
     tickets = dalloc<unsigned>(8);
     CK(cudaMemset(tickets, 0, 8 * sizeof(unsigned)));
     st = dalloc<KState>(1);
@@ -421,18 +437,31 @@ Solver::Solver(DevCsr* A_, int backend_, const sparsla_solve_options& o, DistCtx
     CK(cudaMallocHost(&h_flag, 2 * sizeof(int)));
     CK(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+    } catch (...) {
+        release();  // a constructor that throws runs no destructor: free what was allocated
+        throw;
+    }
     x = x_own; b = b_own;
 }
 
-Solver::~Solver() {
+void Solver::release() noexcept {
     DeviceGuard g(A->device, true);
     if (g_many) cudaGraphExecDestroy(g_many);
     if (g_one) cudaGraphExecDestroy(g_one);
     for (double* v : {x_own, b_own, r, p, q, rh, ph, s, sh, t}) cudaFree(v);
-    cudaFree(partials); cudaFree(tickets); cudaFree(st);
-    cudaFreeHost(h_st); cudaFreeHost(h_flag);
-    cudaEventDestroy(ev[0]); cudaEventDestroy(ev[1]);
+    cudaFree(partials); cudaFree(tickets); cudaFree(st); cudaFree(fused_bar);
+    if (h_st) cudaFreeHost(h_st);
+    if (h_flag) cudaFreeHost(h_flag);
+    if (ev[0]) cudaEventDestroy(ev[0]);
+    if (ev[1]) cudaEventDestroy(ev[1]);
+    g_many = g_one = nullptr;
+    x_own = b_own = r = p = q = rh = ph = s = sh = t = nullptr;
+    partials = nullptr; tickets = nullptr; st = nullptr; fused_bar = nullptr;
+    h_st = nullptr; h_flag = nullptr; ev[0] = ev[1] = nullptr;
+    cudaGetLastError();
 }
+
+Solver::~Solver() { release(); }
 
 RedParams Solver::red(int which, int slot) const {
     RedParams R{};
@@ -527,6 +556,20 @@ void Solver::enqueue_iteration(cudaEvent_t* evs) {
 void Solver::kernel_times(long long iters, double* ms) {
     DeviceGuard g(A->device);
     const int L = (int)launches_per_iteration();
+    if (fused) {  // one kernel runs whole iterations: report the per-iteration time in ms[0]
+        cudaEvent_t e0, e1;
+        CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1));
+        CK(cudaEventRecord(e0, stream));
+        enqueue_fused(iters);
+        CK(cudaEventRecord(e1, stream));
+        CK(cudaEventSynchronize(e1));
+        float t = 0;
+        CK(cudaEventElapsedTime(&t, e0, e1));
+        for (int k = 0; k < L; ++k) ms[k] = 0.0;
+        ms[0] = t / (double)iters;
+        cudaEventDestroy(e0); cudaEventDestroy(e1);
+        return;
+    }
     std::vector<cudaEvent_t> evs((size_t)iters * (L + 1));
     for (auto& e : evs) CK(cudaEventCreate(&e));
     for (long long it = 0; it < iters; ++it) enqueue_iteration(evs.data() + it * (L + 1));
@@ -571,11 +614,31 @@ void Solver::reset() {
     enqueue_init();
 }
 
-bool Solver::capturable() const { return !dist || dist->tr->capturable(); }
+bool Solver::capturable() const { return !fused && (!dist || dist->tr->capturable()); }
+
+void Solver::enqueue_fused(long long iters) {
+    FusedParams F{};
+    F.rp = A->rp; F.ci = A->ci; F.val = A->val; F.d = dinv;
+    F.x = x; F.r = r; F.p = p; F.q = q;
+    F.n = n; F.nch = nchunks_of(n);
+    F.partials = partials; F.bar = fused_bar; F.st = st;
+    while (iters > 0) {
+        F.iters = (int)std::min<long long>(iters, 1 << 20);
+        CK(cudaMemsetAsync(fused_bar, 0, sizeof(unsigned), stream));
+        void* args[] = {&F};
+        CK(cudaLaunchCooperativeKernel((const void*)cg_fused_kernel, dim3(fused_grid), dim3(kSpmvThreads), args, 0,
+                                       stream));
+        iters -= F.iters;
+    }
+}
 
 void Solver::iterate(long long iters) {
     DeviceGuard g(A->device);
     build_graphs();
+    if (fused) {
+        enqueue_fused(iters);
+        return;
+    }
     if (!capturable()) {
         while (iters-- > 0) enqueue_iteration();
         return;
@@ -588,12 +651,13 @@ void Solver::run() {
     DeviceGuard g(A->device);
     build_graphs();
     // Poll the device 'done' flag once per graph, one graph behind (no per-iteration sync).
-    const long long max_graphs = opts.max_iter / kGraphIters + 3;
+    const long long max_graphs = opts.max_iter / kGraphIters + 3;  // (fused: 4x more per launch)
     h_flag[0] = h_flag[1] = 0;
     // All ranks of a distributed solve see identical device flags (same all-gathered
     // totals, same scalar step), so they stop after the same number of graph launches.
     for (long long i = 0; i < max_graphs; ++i) {
-        if (capturable()) CK(cudaGraphLaunch(g_many, stream));
+        if (fused) enqueue_fused(4 * kGraphIters);
+        else if (capturable()) CK(cudaGraphLaunch(g_many, stream));
         else for (int k = 0; k < kGraphIters; ++k) enqueue_iteration();
         CK(cudaMemcpyAsync(h_flag + (i & 1), &st->done, sizeof(int), cudaMemcpyDeviceToHost, stream));
         CK(cudaEventRecord(ev[i & 1], stream));

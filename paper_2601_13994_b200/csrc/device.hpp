@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <mutex>
 #include <vector>
 
 #include "kernels.cuh"
@@ -41,6 +42,7 @@ struct DevCsr {
     int sym_checked = -1;
     DevCsr* transpose = nullptr;
     cudaStream_t stream = nullptr;
+    std::mutex lazy_mu;  // guards the lazily built caches (dinv, ones, symmetry, transpose)
 
     template <class I>
     static DevCsr* create(int device, long long nrows, long long ncols, const I* rp, const I* ci,
@@ -106,10 +108,14 @@ struct Solver {
     int* h_flag = nullptr;
     cudaEvent_t ev[2] = {nullptr, nullptr};
     cudaGraphExec_t g_many = nullptr, g_one = nullptr;
+    bool fused = false;          // small CG: cg_fused_kernel runs whole iterations
+    int fused_grid = 0;
+    unsigned* fused_bar = nullptr;
 
     DistCtx* dist = nullptr;
     Solver(DevCsr* A, int backend, const sparsla_solve_options& o, DistCtx* dist = nullptr);
     ~Solver();
+    void release() noexcept;
     void set_b(const double* src, int mem);
     void reset();
     void iterate(long long iters);
@@ -128,6 +134,7 @@ struct Solver {
     RedParams red(int which, int slot) const;
     VecParams vparams() const;
     void enqueue_init();
+    void enqueue_fused(long long iters);
     void enqueue_iteration(cudaEvent_t* evs = nullptr);
     void build_graphs();
 };

@@ -1019,6 +1019,160 @@ __global__ void __launch_bounds__(kVecThreads) vec_kernel(VecParams P) {
     }
 }
 
+// ------------------------------------------------ fused small-problem CG kernel -------
+// Whole Jacobi-PCG iterations in ONE cooperative persistent kernel (problems whose chunks
+// fit the co-resident grid, e.g. config A): per iteration
+//   SpMV + p.q chunk partials | grid barrier | every CTA finishes the canonical reduction
+//   and the scalar step itself (identical inputs -> identical decisions) | update 1 +
+//   {r.z, r.r} partials | grid barrier | reduction + scalar step | update 2 | grid barrier.
+// Same canonical slot / round / tree order as the multi-kernel path, so the trajectory is
+// bit-identical.  Vectors written inside the kernel are read with ld.global.cg (L2) so no
+// SM sees a stale L1 line of another CTA's rows.
+struct FusedParams {
+    const int32_t* rp;
+    const int32_t* ci;
+    const double* val;
+    const double* d;
+    double *x, *r, *p, *q;
+    long long n, nch;
+    double* partials;  // [3][nch]
+    unsigned* bar;     // grid barrier counter, zeroed before every launch
+    KState* st;
+    int iters;         // iterations this launch (stops earlier when the solve terminates)
+};
+
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned& epoch) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned target = (epoch + 1) * gridDim.x;
+        atomicAdd(bar, 1u);
+        unsigned v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+            if (v < target) __nanosleep(20);
+        } while (v < target);
+    }
+    ++epoch;
+    __syncthreads();
+}
+
+template <int ND>
+__device__ __forceinline__ void fused_total(const double* partials, long long m, double* out, double* sred,
+                                            volatile double* sbc) {
+    double tot[ND];
+    final_reduce<kSpmvThreads, ND>(partials, m, tot, sred);
+    if (threadIdx.x == 0)
+        for (int d = 0; d < ND; ++d) sbc[d] = tot[d];
+    __syncthreads();
+    for (int d = 0; d < ND; ++d) out[d] = sbc[d];
+    __syncthreads();
+}
+
+static __global__ void __launch_bounds__(kSpmvThreads, 4) cg_fused_kernel(FusedParams P) {
+    __shared__ KState S;
+    __shared__ double sred[3 * (kSpmvThreads / 32)];
+    __shared__ double sbc[4];
+    const int t = threadIdx.x;
+    if (t == 0) S = *P.st;
+    __syncthreads();
+    if (S.done) return;
+    unsigned epoch = 0;
+    const long long m = P.nch;
+    for (int it = 0; it < P.iters; ++it) {
+        // ---- SpMV q = A p (thread per row, L2-coherent gathers) + p.q chunk partials
+        for (long long c = blockIdx.x; c < m; c += gridDim.x) {
+            const long long base = c * kChunk;
+            double acc[1] = {0.0};
+            int kk = 0, ke = 0;
+            long long row = base + t;
+            if (row < P.n) { kk = __ldg(P.rp + row); ke = __ldg(P.rp + row + 1); }
+#pragma unroll 1
+            for (int r = 0; r < kChunkRounds; ++r) {
+                // prefetch the next round's row bounds while this row's gathers are in flight
+                const long long nrow = row + kChunkSlots;
+                int nk = 0, nke = 0;
+                if (r + 1 < kChunkRounds && nrow < P.n) { nk = __ldg(P.rp + nrow); nke = __ldg(P.rp + nrow + 1); }
+                if (row < P.n) {
+                    double y = 0.0;
+                    for (int k0 = kk; k0 < ke; k0 += 8) {
+                        double pr[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u)
+                            if (k0 + u < ke) pr[u] = __dmul_rn(__ldg(P.val + k0 + u), __ldcg(P.p + __ldg(P.ci + k0 + u)));
+#pragma unroll
+                        for (int u = 0; u < 8; ++u)
+                            if (k0 + u < ke) y = __dadd_rn(y, pr[u]);
+                    }
+                    P.q[row] = y;
+                    acc[0] = __dadd_rn(acc[0], __dmul_rn(__ldcg(P.p + row), y));
+                }
+                row = nrow; kk = nk; ke = nke;
+            }
+            block_tree<kSpmvThreads, 1>(acc, sred);
+            if (t == 0) P.partials[c] = acc[0];
+        }
+        grid_barrier(P.bar, epoch);
+        double pq[1];
+        fused_total<1>(P.partials, m, pq, sred, sbc);
+        if (t == 0) apply_scalar(SC_CG_PQ, &S, pq);
+        __syncthreads();
+        if (S.done) break;  // p^T A p <= 0: breakdown (uniform decision)
+        const double alpha = S.alpha;
+        // ---- update 1: r -= alpha q; z = d r; {r.z, r.r}
+        for (long long c = blockIdx.x; c < m; c += gridDim.x) {
+            const long long base = c * kChunk;
+            double acc[2] = {0.0, 0.0};
+#pragma unroll
+            for (int r = 0; r < kChunkRounds; ++r) {
+                const long long i = base + (long long)r * kChunkSlots + t;
+                if (i < P.n) {
+                    const double rn = __dsub_rn(__ldcg(P.r + i), __dmul_rn(alpha, __ldcg(P.q + i)));
+                    const double z = __dmul_rn(__ldg(P.d + i), rn);
+                    P.r[i] = rn;
+                    acc[0] = __dadd_rn(acc[0], __dmul_rn(rn, z));
+                    acc[1] = __dadd_rn(acc[1], __dmul_rn(rn, rn));
+                }
+            }
+            block_tree<kSpmvThreads, 2>(acc, sred);
+            if (t == 0) { P.partials[m + c] = acc[0]; P.partials[2 * m + c] = acc[1]; }
+        }
+        grid_barrier(P.bar, epoch);
+        double rr2[2];
+        {
+            double a[1], b2[1];
+            fused_total<1>(P.partials + m, m, a, sred, sbc);
+            fused_total<1>(P.partials + 2 * m, m, b2, sred, sbc);
+            rr2[0] = a[0];
+            rr2[1] = b2[0];
+        }
+        if (t == 0) apply_scalar(SC_CG_RR, &S, rr2);
+        __syncthreads();
+        const bool live = !S.done;
+        const double beta = S.beta;
+        // ---- update 2: x += alpha p; p = z + beta p (own rows only)
+        for (long long c = blockIdx.x; c < m; c += gridDim.x) {
+            const long long base = c * kChunk;
+#pragma unroll
+            for (int r = 0; r < kChunkRounds; ++r) {
+                const long long i = base + (long long)r * kChunkSlots + t;
+                if (i < P.n) {
+                    const double pv = __ldcg(P.p + i);
+                    P.x[i] = __dadd_rn(__ldcg(P.x + i), __dmul_rn(alpha, pv));
+                    if (live) P.p[i] = __dadd_rn(__dmul_rn(__ldg(P.d + i), __ldcg(P.r + i)), __dmul_rn(beta, pv));
+                }
+            }
+        }
+        if (!live) break;
+        grid_barrier(P.bar, epoch);
+    }
+    if (blockIdx.x == 0 && t == 0) {
+        S.pending_x = 0;
+        *P.st = S;
+        __threadfence();
+    }
+}
+
 // Generic canonical dot a.b (level 1 + last-CTA level 2), same chunk shape.
 struct DotParams {
     long long n;
