@@ -231,6 +231,17 @@ typedef struct sparsla_local_hub sparsla_local_hub;
 int sparsla_nccl_unique_id(unsigned char* id128);
 int sparsla_dist_create_nccl(int device, int nranks, int rank, const unsigned char* id128,
                              const sparsla_local* L, sparsla_dist** out);
+/* Host-callback backing (setup / init traffic through caller-provided collectives, e.g.
+ * torch.distributed gloo; host buffers, synchronous).  Combined with sparsla_dist_set_fused
+ * the iterations use cudaIpc peer memory only, so several processes may share one GPU. */
+typedef struct {
+    void* user;
+    int (*allgather)(void* user, const double* send, double* recv, int64_t count);
+    int (*exchange)(void* user, int32_t npeers, const int32_t* ranks, const double* const* sbuf,
+                    const int64_t* scount, double* const* rbuf, const int64_t* rcount);
+} sparsla_host_transport;
+int sparsla_dist_create_host(int device, int nranks, int rank, const sparsla_host_transport* T,
+                             const sparsla_local* L, sparsla_dist** out);
 int sparsla_local_hub_create(int nranks, sparsla_local_hub** out);
 int sparsla_local_hub_destroy(sparsla_local_hub* hub);
 int sparsla_dist_create_local(int device, sparsla_local_hub* hub, int rank, const sparsla_local* L,
@@ -244,6 +255,12 @@ int sparsla_dist_info(const sparsla_dist* D, int64_t* info);
  * also include the no-op tail replayed after convergence).  6 entries. */
 int sparsla_dist_counters(const sparsla_dist* D, int64_t* counters);
 int sparsla_dist_reset_counters(sparsla_dist* D);
+/* Fused peer-memory collectives for distributed CG (default off; SPARSLA_P2P=1 also
+ * enables): per iteration no NCCL call — reduction totals and halo values are stored by
+ * the kernels straight into the peers' memory (NVLink / cudaIpc, or same-device for
+ * in-process ranks) with release/acquire epoch flags.  Must be set identically on all
+ * ranks before a solve. */
+int sparsla_dist_set_fused(sparsla_dist* D, int32_t on);
 /* dist_spmv */
 int sparsla_dist_spmv(sparsla_dist* D, const double* x_owned, double* y_owned, int32_t mem);
 /* dist_cg (Alg. 4) / distributed BiCGStab, SolveOptions as cg_solve */

@@ -158,16 +158,16 @@ DevCsr* DevCsr::create(int device, long long nrows, long long ncols, const I* h_
     CK(cudaMemset(A->ci + nnz, 0, 8 * sizeof(int32_t)));
     CK(cudaMemset(A->val + nnz, 0, 4 * sizeof(double)));
     if constexpr (sizeof(I) == 4) {
-        CK(cudaMemcpy(A->rp, h_rp, (nrows + 1) * sizeof(int32_t), cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(A->ci, h_ci, nnz * sizeof(int32_t), cudaMemcpyHostToDevice));
+        CK(memcpy_sync(A->rp, h_rp, (nrows + 1) * sizeof(int32_t), cudaMemcpyHostToDevice));
+        CK(memcpy_sync(A->ci, h_ci, nnz * sizeof(int32_t), cudaMemcpyHostToDevice));
     } else {
         std::vector<int32_t> tmp(static_cast<size_t>(std::max(nrows + 1, nnz)));
         parallel_for(nrows + 1, [&](int64_t a, int64_t b) { for (int64_t i = a; i < b; ++i) tmp[i] = (int32_t)h_rp[i]; });
-        CK(cudaMemcpy(A->rp, tmp.data(), (nrows + 1) * sizeof(int32_t), cudaMemcpyHostToDevice));
+        CK(memcpy_sync(A->rp, tmp.data(), (nrows + 1) * sizeof(int32_t), cudaMemcpyHostToDevice));
         parallel_for(nnz, [&](int64_t a, int64_t b) { for (int64_t i = a; i < b; ++i) tmp[i] = (int32_t)h_ci[i]; });
-        CK(cudaMemcpy(A->ci, tmp.data(), nnz * sizeof(int32_t), cudaMemcpyHostToDevice));
+        CK(memcpy_sync(A->ci, tmp.data(), nnz * sizeof(int32_t), cudaMemcpyHostToDevice));
     }
-    CK(cudaMemcpy(A->val, h_val, nnz * sizeof(double), cudaMemcpyHostToDevice));
+    CK(memcpy_sync(A->val, h_val, nnz * sizeof(double), cudaMemcpyHostToDevice));
     // row-length statistics -> SpMV variant and staging capacity
     long long mb = 0, mr = 0;
     for (long long b = 0; b < nrows; b += kChunkSlots) {
@@ -266,7 +266,7 @@ bool DevCsr::exactly_symmetric() {
         if (nrows != ncols) { sym_checked = 0; return false; }
         int* flags = dalloc<int>(2);
         const int one[2] = {1, 1};
-        CK(cudaMemcpy(flags, one, sizeof(one), cudaMemcpyHostToDevice));
+        CK(memcpy_sync(flags, one, sizeof(one), cudaMemcpyHostToDevice));
         if (nrows > 0) symmetry_kernel<<<grid_for(nrows, 256), 256, 0, stream>>>(rp, ci, val, nrows, flags);
         CK(cudaGetLastError());
         int h[2];
@@ -285,9 +285,9 @@ DevCsr* DevCsr::get_transpose() {
         DeviceGuard g(device);
         std::vector<int32_t> hrp(nrows + 1), hci(nnz);
         std::vector<double> hv(nnz);
-        CK(cudaMemcpy(hrp.data(), rp, (nrows + 1) * 4, cudaMemcpyDeviceToHost));
-        CK(cudaMemcpy(hci.data(), ci, nnz * 4, cudaMemcpyDeviceToHost));
-        CK(cudaMemcpy(hv.data(), val, nnz * 8, cudaMemcpyDeviceToHost));
+        CK(memcpy_sync(hrp.data(), rp, (nrows + 1) * 4, cudaMemcpyDeviceToHost));
+        CK(memcpy_sync(hci.data(), ci, nnz * 4, cudaMemcpyDeviceToHost));
+        CK(memcpy_sync(hv.data(), val, nnz * 8, cudaMemcpyDeviceToHost));
         std::vector<int32_t> trp(ncols + 1, 0), tci(nnz);
         std::vector<double> tv(nnz);
         for (long long k = 0; k < nnz; ++k) ++trp[hci[k] + 1];
@@ -315,7 +315,7 @@ unsigned spmv_grid(const DevCsr* A, long long nch) {
 // number of CTAs of every launch of this reduction point (interior + boundary).
 void launch_spmv_part(DevCsr* A, cudaStream_t s, int mode, const double* x, double* y, const double* aux,
                       const RedParams& red, int check_done, const int32_t* list, long long nch,
-                      unsigned expected) {
+                      unsigned expected, const P2PCtx* p2p, long long n_interior, int halo_v) {
     const unsigned grid = spmv_grid(A, nch);
     if (grid == 0) return;
     SpmvParams P{};
@@ -323,6 +323,9 @@ void launch_spmv_part(DevCsr* A, cudaStream_t s, int mode, const double* x, doub
     P.x = x; P.y = y; P.n = A->nrows; P.chunk0 = 0; P.aux = aux;
     P.nch = nch;
     P.chunk_list = list;
+    P.p2p = p2p;
+    P.n_interior = n_interior;
+    P.halo_v = halo_v;
     P.cap_v = A->cap_v; P.cap_c = A->cap_c;
     P.l2_keep = A->l2_keep;
     P.check_done = check_done;
@@ -409,7 +412,7 @@ Solver::Solver(DevCsr* A_, int backend_, const sparsla_solve_options& o, DistCtx
     dinv = o.preconditioner == SPARSLA_PRECOND_JACOBI ? A->jacobi_dinv() : A->ones_vec();
     const long long m = std::max<long long>(1, nchunks_of(n));
     const long long nv = n + 2;
-    const long long nh = (dist ? dist->n_halo : 0) + nv;  // SpMV inputs carry the halo slots
+    const long long nh = (dist ? dist->vec_len : n) + 2;  // SpMV inputs: [owned | gap | halo]
     try {
     x_own = dalloc<double>(nv); b_own = dalloc<double>(nv);
     r = dalloc<double>(nv); p = dalloc<double>(nh); q = dalloc<double>(nv);
@@ -437,6 +440,7 @@ Solver::Solver(DevCsr* A_, int backend_, const sparsla_solve_options& o, DistCtx
     CK(cudaMallocHost(&h_flag, 2 * sizeof(int)));
     CK(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+    if (dist && dist->p2p_enabled && backend == SPARSLA_BACKEND_CG) p2p_setup();
     } catch (...) {
         release();  // a constructor that throws runs no destructor: free what was allocated
         throw;
@@ -446,6 +450,7 @@ Solver::Solver(DevCsr* A_, int backend_, const sparsla_solve_options& o, DistCtx
 
 void Solver::release() noexcept {
     DeviceGuard g(A->device, true);
+    p2p_release();
     if (g_many) cudaGraphExecDestroy(g_many);
     if (g_one) cudaGraphExecDestroy(g_one);
     for (double* v : {x_own, b_own, r, p, q, rh, ph, s, sh, t}) cudaFree(v);
@@ -487,6 +492,14 @@ void Solver::spmv_point(int mode, double* xin, double* y, const double* aux, int
         launch_spmv(A, stream, mode, xin, y, aux, R, check_done);
         return;
     }
+    if (d_p2p && check_done) {  // fused peer collectives: one launch, halo pushed by the producer
+        R.p2p = d_p2p;
+        R.point = slot;
+        const unsigned gall = spmv_grid(A, dist->n_interior + dist->n_boundary);
+        launch_spmv_part(A, stream, mode, xin, y, aux, R, check_done, dist->d_all_chunks,
+                         dist->n_interior + dist->n_boundary, gall, d_p2p, dist->n_interior, 0);
+        return;
+    }
     if (nd > 0) R.red_out = dist->red_send + slot * 8;
     dist->exchange(stream, xin);
     const unsigned gi = spmv_grid(A, dist->n_interior), gb = spmv_grid(A, dist->n_boundary);
@@ -508,6 +521,16 @@ void Solver::vec_point(int scalar, int slot, int check_done) {
     P.check_done = check_done;
     RedParams R = red(scalar, slot);  // (CG_U2 uses the slot's ticket to clear pending_x)
     constexpr int nd = VecTraits<OP>::ndot;
+    if (d_p2p && (OP == V_CG_U1 || OP == V_CG_U2)) {
+        // consume the previous reduction point in-kernel; U1 pushes its own totals
+        P.p2p = d_p2p;
+        P.consume_point = OP == V_CG_U1 ? 1 : 2;
+        P.consume_scalar = OP == V_CG_U1 ? SC_CG_PQ : SC_CG_RR;
+        P.consume_k = OP == V_CG_U1 ? 1 : 2;
+        R.point = slot;
+        launch_vec<OP>(stream, P, R);
+        return;
+    }
     if (dist && nd > 0) R.red_out = dist->red_send + slot * 8;
     launch_vec<OP>(stream, P, R);
     if (dist && nd > 0) reduce_point(scalar, slot, nd);
@@ -524,10 +547,18 @@ void Solver::enqueue_init() {
     // initial residual r0 = b - A x0 (one SpMV, spmv_count = 1); x0 = 0 lives in p's storage
     // for the distributed case so the halo exchange has its slots
     double* x0 = dist ? p : x;
-    if (dist) CK(cudaMemsetAsync(p, 0, (n + dist->n_halo) * sizeof(double), stream));
+    if (dist) CK(cudaMemsetAsync(p, 0, dist->vec_len * sizeof(double), stream));
+    if (d_p2p) {  // fused-collective epochs restart at 0 on every rank (ordered by the init all-gather)
+        CK(cudaMemsetAsync(p2p_allocs[1], 0, 8 * dist->tr->P * sizeof(unsigned long long), stream));
+        CK(cudaMemsetAsync(p2p_allocs[2], 0, 4 * dist->tr->P * sizeof(unsigned long long), stream));
+    }
     spmv_point(SPMV_PLAIN, x0, q, nullptr, SC_NONE, 0, 0);
     if (backend == SPARSLA_BACKEND_CG) vec_point<V_CG_INIT>(SC_CG_INIT, 0, 0);
     else vec_point<V_BI_INIT>(SC_BI_INIT, 0, 0);
+    if (d_p2p) {  // halo of p0 through the transport once; later iterations push it in-kernel
+        dist->exchange(stream, p);
+        CK(cudaStreamWaitEvent(stream, dist->ev_halo, 0));
+    }
     if (n == 0 && !dist) {  // empty system: converged with zero residual
         KState z = h;
         z.converged = 1; z.status = ST_CONVERGED; z.done = 1;

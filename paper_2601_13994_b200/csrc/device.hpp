@@ -7,6 +7,7 @@
 #include <mutex>
 #include <vector>
 
+#include "copy_sync.hpp"
 #include "kernels.cuh"
 #include "sparsla_c.h"
 
@@ -59,7 +60,8 @@ void launch_spmv(DevCsr* A, cudaStream_t s, int mode, const double* x, double* y
 unsigned spmv_grid(const DevCsr* A, long long nch);
 void launch_spmv_part(DevCsr* A, cudaStream_t s, int mode, const double* x, double* y, const double* aux,
                       const RedParams& red, int check_done, const int32_t* list, long long nch,
-                      unsigned expected);
+                      unsigned expected, const P2PCtx* p2p = nullptr, long long n_interior = 0,
+                      int halo_v = 0);
 
 struct Transport;
 
@@ -69,6 +71,7 @@ struct DistCtx {
     Transport* tr = nullptr;
     int device = 0;
     long long n_owned = 0, n_halo = 0;
+    long long halo_base = 0, vec_len = 0;  // device layout [owned | gap | halo]
     std::vector<int> nbr;
     std::vector<long long> s_off, s_cnt, r_off, r_cnt;  // per neighbour into send/recv maps
     std::vector<long long> s_base, r_base;              // contiguous range start, or -1
@@ -83,6 +86,8 @@ struct DistCtx {
     double* red_all = nullptr;   // [8 points][P][8]
     cudaStream_t comm = nullptr;
     cudaEvent_t ev_x = nullptr, ev_halo = nullptr;
+    bool p2p_enabled = false;     // fused peer-memory collectives for CG (sparsla_dist_set_fused)
+    int32_t* d_all_chunks = nullptr;  // [interior | boundary] for the single fused-mode launch
     void exchange(cudaStream_t s, double* x);  // halo of x ([owned|halo]) -> ev_halo
     ~DistCtx();
 };
@@ -109,6 +114,9 @@ struct Solver {
     cudaEvent_t ev[2] = {nullptr, nullptr};
     cudaGraphExec_t g_many = nullptr, g_one = nullptr;
     bool fused = false;          // small CG: cg_fused_kernel runs whole iterations
+    // fused peer-memory collectives (distributed CG)
+    P2PCtx* d_p2p = nullptr;
+    std::vector<void*> p2p_allocs, p2p_ipc_opened;
     int fused_grid = 0;
     unsigned* fused_bar = nullptr;
 
@@ -134,6 +142,8 @@ struct Solver {
     RedParams red(int which, int slot) const;
     VecParams vparams() const;
     void enqueue_init();
+    void p2p_setup();     // collective (dist.cu)
+    void p2p_release() noexcept;
     void enqueue_fused(long long iters);
     void enqueue_iteration(cudaEvent_t* evs = nullptr);
     void build_graphs();

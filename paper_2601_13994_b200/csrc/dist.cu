@@ -12,6 +12,7 @@
 //                   deterministic, identical on every rank.
 //   dist_cg / dist_bicgstab / dist_adjoint_solve / gather_solution.
 #include <cuda_runtime.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <cstring>
@@ -34,8 +35,15 @@ static T* dmalloc(size_t n) {
     CKD(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)));
     return static_cast<T*>(p);
 }
+template <class T>
+static T* dalloc_zero(size_t n) {
+    T* p = dmalloc<T>(n);
+    CKD(cudaMemset(p, 0, std::max<size_t>(n, 1) * sizeof(T)));
+    return p;
+}
 
 DistCtx::~DistCtx() {
+    cudaFree(d_all_chunks);
     cudaFree(d_send_idx); cudaFree(d_recv_idx); cudaFree(sendbuf); cudaFree(recvbuf);
     cudaFree(d_interior); cudaFree(d_boundary); cudaFree(red_send); cudaFree(red_all);
     if (ev_x) cudaEventDestroy(ev_x);
@@ -70,6 +78,153 @@ void DistCtx::exchange(cudaStream_t s, double* x) {
                                                                                    recvbuf + r_off[a]);
     CKD(cudaGetLastError());
     CKD(cudaEventRecord(ev_halo, comm));
+}
+
+// ---------------------------------------------- fused peer-memory collectives setup ----
+// Collective over the plan's transport.  Every rank publishes (pid, raw pointers, cudaIpc
+// handles) of its mailbox, flags and SpMV-input vector; peers in the same process use the
+// raw pointers (peer access enabled across devices), peers in other processes open the IPC
+// handles.  Then each rank learns where its send values land in every neighbour's vector
+// and builds per-chunk push tables for the in-kernel halo push.
+void Solver::p2p_setup() {
+    DistCtx* C = dist;
+    Transport* tr = C->tr;
+    const int P = tr->P, me = tr->rank;
+    cudaStream_t s0 = stream;
+    double* mail = dalloc_zero<double>((size_t)8 * P * 8);
+    auto* mflag = dalloc_zero<unsigned long long>((size_t)8 * P);
+    auto* hflag = dalloc_zero<unsigned long long>((size_t)4 * P);
+    p2p_allocs = {mail, mflag, hflag};
+    void* mine[4] = {mail, mflag, hflag, p};
+    constexpr int W = 40;  // doubles per rank: pid, device, 4 pointers, 4 x 64-byte handles
+    std::vector<double> blob(W, 0.0);
+    blob[0] = (double)getpid();
+    blob[1] = (double)A->device;
+    for (int i = 0; i < 4; ++i) std::memcpy(&blob[2 + i], &mine[i], 8);
+    std::string ipc_err;
+    for (int i = 0; i < 4; ++i) {
+        cudaIpcMemHandle_t hd;
+        const cudaError_t e = cudaIpcGetMemHandle(&hd, mine[i]);
+        if (e == cudaSuccess) std::memcpy(&blob[6 + 8 * i], &hd, 64);
+        else { ipc_err = cudaGetErrorString(e); cudaGetLastError(); }  // in-process peers do not need it
+    }
+    double* dblob = dalloc_zero<double>((size_t)W * (P + 1));
+    CKD(memcpy_sync(dblob, blob.data(), W * 8, cudaMemcpyHostToDevice));
+    tr->allgather(s0, dblob, dblob + W, W);
+    std::vector<double> all((size_t)W * P);
+    CKD(cudaMemcpyAsync(all.data(), dblob + W, all.size() * 8, cudaMemcpyDeviceToHost, s0));
+    CKD(cudaStreamSynchronize(s0));
+    cudaFree(dblob);
+    tr->allgathers -= 1;
+    std::vector<void*> peer[4];
+    for (int q = 0; q < P; ++q) {
+        const double* bq = &all[(size_t)q * W];
+        for (int i = 0; i < 4; ++i) {
+            void* ptr = nullptr;
+            if (q == me) {
+                ptr = mine[i];
+            } else if ((long long)bq[0] == (long long)getpid()) {
+                std::memcpy(&ptr, &bq[2 + i], 8);
+                const int pdev = (int)bq[1];
+                if (pdev != A->device) {
+                    int can = 0;
+                    CKD(cudaDeviceCanAccessPeer(&can, A->device, pdev));
+                    if (!can) fail(SPARSLA_ERR_UNSUPPORTED, "fused collectives need peer access between GPUs");
+                    cudaError_t e = cudaDeviceEnablePeerAccess(pdev, 0);
+                    if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+                    else CKD(e);
+                }
+            } else {
+                cudaIpcMemHandle_t hd;
+                std::memcpy(&hd, &bq[6 + 8 * i], 64);
+                const cudaError_t e = cudaIpcOpenMemHandle(&ptr, hd, cudaIpcMemLazyEnablePeerAccess);
+                if (e != cudaSuccess) {
+                    cudaGetLastError();
+                    unsigned sum = 0;
+                    for (int b = 0; b < 64; ++b) sum += (unsigned char)hd.reserved[b];
+                    fail(SPARSLA_ERR_CUDA, std::string("cudaIpcOpenMemHandle(rank ") + std::to_string(q) + ", buffer " +
+                                               std::to_string(i) + "): " + cudaGetErrorString(e) +
+                                               " (handle byte sum " + std::to_string(sum) + "; local GetMemHandle: " +
+                                               (ipc_err.empty() ? "ok" : ipc_err) + ")");
+                }
+                p2p_ipc_opened.push_back(ptr);
+            }
+            peer[i].push_back(ptr);
+        }
+    }
+    // where my send values land: each neighbour tells me its recv positions for me
+    const size_t nn = C->nbr.size();
+    std::vector<long long> rpos_cnt(nn);
+    long long tot_recv = 0, tot_send = 0;
+    for (size_t a = 0; a < nn; ++a) { tot_recv += C->r_cnt[a]; tot_send += C->s_cnt[a]; }
+    std::vector<int32_t> my_recv(tot_recv);
+    if (tot_recv) CKD(memcpy_sync(my_recv.data(), C->d_recv_idx, tot_recv * 4, cudaMemcpyDeviceToHost));
+    std::vector<double> recv_d(my_recv.begin(), my_recv.end());
+    double* dbuf = dalloc_zero<double>((size_t)tot_recv + tot_send + 2);
+    if (tot_recv) CKD(memcpy_sync(dbuf, recv_d.data(), tot_recv * 8, cudaMemcpyHostToDevice));
+    std::vector<HaloPeer> hp(nn);
+    for (size_t a = 0; a < nn; ++a)
+        hp[a] = HaloPeer{C->nbr[a], dbuf + C->r_off[a], C->r_cnt[a], dbuf + tot_recv + C->s_off[a], C->s_cnt[a]};
+    tr->exchange(s0, hp);
+    tr->exchanges -= 1;
+    tr->messages -= (long long)nn;
+    std::vector<double> remote(tot_send);
+    if (tot_send) CKD(cudaMemcpyAsync(remote.data(), dbuf + tot_recv, tot_send * 8, cudaMemcpyDeviceToHost, s0));
+    CKD(cudaStreamSynchronize(s0));
+    cudaFree(dbuf);
+    std::vector<int32_t> my_send(tot_send);
+    if (tot_send) CKD(memcpy_sync(my_send.data(), C->d_send_idx, tot_send * 4, cudaMemcpyDeviceToHost));
+    // non-contiguous send lists live in d_send_idx; contiguous ones were not uploaded there
+    // as positions, so rebuild the send rows from the plan: row = s_base + j when contiguous
+    struct E { int32_t row, nbr; long long pos; };
+    std::vector<E> ent;
+    ent.reserve(tot_send);
+    for (size_t a = 0; a < nn; ++a)
+        for (long long j = 0; j < C->s_cnt[a]; ++j) {
+            const int32_t row = C->s_base[a] >= 0 ? (int32_t)(C->s_base[a] + j) : my_send[C->s_off[a] + j];
+            ent.push_back(E{row, (int32_t)a, (long long)remote[C->s_off[a] + j]});
+        }
+    const long long nch = (n + kChunk - 1) / kChunk;
+    std::stable_sort(ent.begin(), ent.end(), [](const E& u, const E& v) { return u.row / kChunk < v.row / kChunk; });
+    std::vector<int32_t> pptr(nch + 1, 0), prow(ent.size()), pnbr(ent.size());
+    std::vector<long long> ppos(ent.size());
+    for (size_t e = 0; e < ent.size(); ++e) {
+        ++pptr[ent[e].row / kChunk + 1];
+        prow[e] = ent[e].row; pnbr[e] = ent[e].nbr; ppos[e] = ent[e].pos;
+    }
+    for (long long c = 0; c < nch; ++c) pptr[c + 1] += pptr[c];
+    auto upload = [&](const void* src, size_t bytes) {
+        void* dst = nullptr;
+        CKD(cudaMalloc(&dst, std::max<size_t>(bytes, 8)));
+        if (bytes) CKD(memcpy_sync(dst, src, bytes, cudaMemcpyHostToDevice));
+        p2p_allocs.push_back(dst);
+        return dst;
+    };
+    std::vector<double*> pv(nn);
+    std::vector<int32_t> nr(nn);
+    for (size_t a = 0; a < nn; ++a) { pv[a] = static_cast<double*>(peer[3][C->nbr[a]]); nr[a] = C->nbr[a]; }
+    P2PCtx X{};
+    X.P = P; X.me = me; X.nnbr = (int)nn;
+    X.peer_mail = (double**)upload(peer[0].data(), P * sizeof(void*));
+    X.peer_mflag = (unsigned long long**)upload(peer[1].data(), P * sizeof(void*));
+    X.peer_hflag = (unsigned long long**)upload(peer[2].data(), P * sizeof(void*));
+    X.my_mail = mail; X.my_mflag = mflag; X.my_hflag = hflag;
+    X.nbr_rank = (const int32_t*)upload(nr.data(), nn * 4);
+    X.push_ptr = (const int32_t*)upload(pptr.data(), pptr.size() * 4);
+    X.push_row = (const int32_t*)upload(prow.data(), prow.size() * 4);
+    X.push_nbr = (const int32_t*)upload(pnbr.data(), pnbr.size() * 4);
+    X.push_pos = (const long long*)upload(ppos.data(), ppos.size() * 8);
+    X.peer_vec = (double**)upload(pv.data(), nn * sizeof(void*));
+    d_p2p = (P2PCtx*)upload(&X, sizeof(X));
+}
+
+void Solver::p2p_release() noexcept {
+    for (void* p2 : p2p_ipc_opened) cudaIpcCloseMemHandle(p2);
+    for (void* p2 : p2p_allocs) cudaFree(p2);
+    p2p_ipc_opened.clear();
+    p2p_allocs.clear();
+    d_p2p = nullptr;
+    cudaGetLastError();
 }
 
 }  // namespace sparsla_b200
@@ -108,13 +263,21 @@ sparsla_dist* build_plan(int device, std::unique_ptr<Transport> tr, const sparsl
     DeviceGuard g(device);
     auto D = std::make_unique<sparsla_dist>();
     const long long no = (long long)L->owned.size(), nh = (long long)L->halo.size();
-    std::vector<int32_t> rp(L->rp.begin(), L->rp.end()), ci(L->ci.begin(), L->ci.end());
-    D->A = DevCsr::create<int32_t>(device, no, no + nh, rp.data(), ci.data(), L->v.data(), true);
+    // device layout of SpMV inputs: [owned | gap | halo], the halo starting on its own
+    // 128-byte lines (>= 16 doubles after the last owned value): halo values may be written
+    // by peers while this rank's SpMV already streams owned lines through the read-only
+    // cache, so no line may mix owned and halo data.  SPEC-layout maps stay n_owned-based.
+    const long long hb = ((no + 16 + 15) / 16) * 16;
+    std::vector<int32_t> rp(L->rp.begin(), L->rp.end()), ci(L->ci.size());
+    for (size_t k = 0; k < ci.size(); ++k) ci[k] = (int32_t)(L->ci[k] < no ? L->ci[k] : L->ci[k] - no + hb);
+    D->A = DevCsr::create<int32_t>(device, no, hb + nh, rp.data(), ci.data(), L->v.data(), true);
     auto C = std::make_unique<DistCtx>();
     C->tr = tr.get();
     C->device = device;
     C->n_owned = no;
     C->n_halo = nh;
+    C->halo_base = hb;
+    C->vec_len = hb + nh;
     const size_t nn = L->neighbors.size();
     for (size_t a = 0; a < nn; ++a) {
         C->nbr.push_back(L->neighbors[a]);
@@ -125,14 +288,16 @@ sparsla_dist* build_plan(int device, std::unique_ptr<Transport> tr, const sparsl
         long long sb, rb;
         contiguous_range(L->send_idx, L->send_ptr[a], L->send_ptr[a + 1], sb);
         contiguous_range(L->recv_idx, L->recv_ptr[a], L->recv_ptr[a + 1], rb);
+        if (rb >= 0 && L->recv_ptr[a + 1] > L->recv_ptr[a]) rb = rb - no + hb;
         C->s_base.push_back(sb);
         C->r_base.push_back(rb);
     }
-    std::vector<int32_t> si(L->send_idx.begin(), L->send_idx.end()), ri(L->recv_idx.begin(), L->recv_idx.end());
+    std::vector<int32_t> si(L->send_idx.begin(), L->send_idx.end()), ri(L->recv_idx.size());
+    for (size_t k = 0; k < ri.size(); ++k) ri[k] = (int32_t)(L->recv_idx[k] - no + hb);
     C->d_send_idx = dmalloc<int32_t>(si.size());
     C->d_recv_idx = dmalloc<int32_t>(ri.size());
-    if (!si.empty()) CKD(cudaMemcpy(C->d_send_idx, si.data(), si.size() * 4, cudaMemcpyHostToDevice));
-    if (!ri.empty()) CKD(cudaMemcpy(C->d_recv_idx, ri.data(), ri.size() * 4, cudaMemcpyHostToDevice));
+    if (!si.empty()) CKD(memcpy_sync(C->d_send_idx, si.data(), si.size() * 4, cudaMemcpyHostToDevice));
+    if (!ri.empty()) CKD(memcpy_sync(C->d_recv_idx, ri.data(), ri.size() * 4, cudaMemcpyHostToDevice));
     C->sendbuf = dmalloc<double>(si.size());
     C->recvbuf = dmalloc<double>(ri.size());
     // interior chunks reference no halo column; boundary chunks wait for the exchange
@@ -141,15 +306,22 @@ sparsla_dist* build_plan(int device, std::unique_ptr<Transport> tr, const sparsl
     for (long long c = 0; c < nch; ++c) {
         bool b = false;
         const long long r1 = std::min(no, (c + 1) * kChunk);
-        for (long long k = L->rp[c * kChunk]; k < L->rp[r1] && !b; ++k) b = L->ci[k] >= no;
+        for (long long k = L->rp[c * kChunk]; k < L->rp[r1] && !b; ++k) b = L->ci[k] >= no;  // SPEC-layout ids
         (b ? bound : inter).push_back((int32_t)c);
     }
     C->n_interior = (long long)inter.size();
     C->n_boundary = (long long)bound.size();
+    {
+        std::vector<int32_t> all(inter);
+        all.insert(all.end(), bound.begin(), bound.end());
+        C->d_all_chunks = dmalloc<int32_t>(all.size());
+        if (!all.empty()) CKD(memcpy_sync(C->d_all_chunks, all.data(), all.size() * 4, cudaMemcpyHostToDevice));
+    }
+    if (const char* e = getenv("SPARSLA_P2P")) C->p2p_enabled = atoi(e) != 0;
     C->d_interior = dmalloc<int32_t>(inter.size());
     C->d_boundary = dmalloc<int32_t>(bound.size());
-    if (!inter.empty()) CKD(cudaMemcpy(C->d_interior, inter.data(), inter.size() * 4, cudaMemcpyHostToDevice));
-    if (!bound.empty()) CKD(cudaMemcpy(C->d_boundary, bound.data(), bound.size() * 4, cudaMemcpyHostToDevice));
+    if (!inter.empty()) CKD(memcpy_sync(C->d_interior, inter.data(), inter.size() * 4, cudaMemcpyHostToDevice));
+    if (!bound.empty()) CKD(memcpy_sync(C->d_boundary, bound.data(), bound.size() * 4, cudaMemcpyHostToDevice));
     C->red_send = dmalloc<double>(8 * 8);
     C->red_all = dmalloc<double>((size_t)8 * tr->P * 8);
     CKD(cudaMemset(C->red_send, 0, 64 * sizeof(double)));
@@ -171,7 +343,7 @@ sparsla_dist* build_plan(int device, std::unique_ptr<Transport> tr, const sparsl
     row[2 * P] = (double)no;
     const int W = 2 * P + 1;
     double* hs = dmalloc<double>((size_t)W * (P + 1));
-    CKD(cudaMemcpy(hs, row.data(), W * 8, cudaMemcpyHostToDevice));
+    CKD(memcpy_sync(hs, row.data(), W * 8, cudaMemcpyHostToDevice));
     tr->allgather(s, hs, hs + W, W);
     std::vector<double> all((size_t)W * P);
     CKD(cudaMemcpyAsync(all.data(), hs + W, all.size() * 8, cudaMemcpyDeviceToHost, s));
@@ -185,6 +357,12 @@ sparsla_dist* build_plan(int device, std::unique_ptr<Transport> tr, const sparsl
         D->all_count.push_back((int64_t)all[(size_t)p * W + 2 * P]);
         D->n_global += (int64_t)all[(size_t)p * W + 2 * P];
     }
+    if (D->all_count[tr->rank] != no) {
+        std::string got;
+        for (int p = 0; p < P; ++p) got += " " + std::to_string(D->all_count[p]);
+        fail(SPARSLA_ERR_TRANSPORT, "handshake all-gather returned inconsistent owned counts (own " +
+                                        std::to_string(no) + ", gathered" + got + ")");
+    }
     if (any_bad)
         fail(SPARSLA_ERR_UNSUPPORTED,
              "halo maps disagree between ranks: the distributed path requires a structurally "
@@ -195,13 +373,13 @@ sparsla_dist* build_plan(int device, std::unique_ptr<Transport> tr, const sparsl
         double* ids = dmalloc<double>(no + 1);
         std::vector<double> idd(no);
         std::memcpy(idd.data(), L->owned.data(), no * 8);
-        if (no) CKD(cudaMemcpy(ids, idd.data(), no * 8, cudaMemcpyHostToDevice));
+        if (no) CKD(memcpy_sync(ids, idd.data(), no * 8, cudaMemcpyHostToDevice));
         double* rbuf = nullptr;
         if (tr->rank == 0) {
             rbuf = dmalloc<double>(D->n_global + 1);
             long long off = 0;
             for (int q = 0; q < tr->P; ++q) {
-                if (q == 0) { if (no) CKD(cudaMemcpy(rbuf, ids, no * 8, cudaMemcpyDeviceToDevice)); }
+                if (q == 0) { if (no) CKD(memcpy_sync(rbuf, ids, no * 8, cudaMemcpyDeviceToDevice)); }
                 else gp.push_back(HaloPeer{q, nullptr, 0, rbuf + off, D->all_count[q]});
                 off += D->all_count[q];
             }
@@ -280,6 +458,17 @@ int sparsla_dist_create_nccl(int device, int nranks, int rank, const unsigned ch
     });
 }
 
+int sparsla_dist_create_host(int device, int nranks, int rank, const sparsla_host_transport* T,
+                             const sparsla_local* L, sparsla_dist** out) {
+    return guarded([&] {
+        if (!L || !out || !T || !T->allgather || !T->exchange) fail(SPARSLA_ERR_INVALID_ARGUMENT, "null argument");
+        DeviceGuard g(device);
+        HostCallbacks cb{T->user, T->allgather, T->exchange};
+        std::unique_ptr<Transport> tr(new HostTransport(nranks, rank, cb));
+        *out = build_plan(device, std::move(tr), L);
+    });
+}
+
 int sparsla_local_hub_create(int nranks, sparsla_local_hub** out) {
     return guarded([&] {
         if (nranks < 1) fail(SPARSLA_ERR_INVALID_ARGUMENT, "nranks >= 1");
@@ -318,6 +507,10 @@ int sparsla_dist_info(const sparsla_dist* D, int64_t* info) {
     });
 }
 
+int sparsla_dist_set_fused(sparsla_dist* D, int32_t on) {
+    return guarded([&] { D->ctx->p2p_enabled = on != 0; });
+}
+
 int sparsla_dist_counters(const sparsla_dist* D, int64_t* out) {
     return guarded([&] {
         out[0] = D->alg_exchanges;
@@ -343,7 +536,7 @@ int sparsla_dist_spmv(sparsla_dist* D, const double* x_owned, double* y_owned, i
         DistCtx* C = D->ctx.get();
         DeviceGuard g(A->device);
         cudaStream_t s = A->stream;
-        DVec X(x_owned, C->n_owned, C->n_halo, mem, s);
+        DVec X(x_owned, C->n_owned, C->vec_len - C->n_owned, mem, s);
         DVec Y(y_owned, C->n_owned, 0, mem, s, false);
         C->exchange(s, X.d);
         RedParams none{};
@@ -385,11 +578,11 @@ int sparsla_dist_adjoint_backward(sparsla_dist* D, const double* x_owned, const 
         const long long no = C->n_owned;
         // global "grad_x == 0" short-circuit decided identically on every rank
         std::vector<double> hg(no);
-        if (no) CKD(cudaMemcpy(hg.data(), g_owned, no * 8, mem == SPARSLA_MEM_DEVICE ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost));
+        if (no) CKD(memcpy_sync(hg.data(), g_owned, no * 8, mem == SPARSLA_MEM_DEVICE ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost));
         double nz = 0.0;
         for (double v : hg) if (v != 0.0) { nz = 1.0; break; }
         double* f = dmalloc<double>(2 + (size_t)D->tr->P);
-        CKD(cudaMemcpy(f, &nz, 8, cudaMemcpyHostToDevice));
+        CKD(memcpy_sync(f, &nz, 8, cudaMemcpyHostToDevice));
         D->tr->allgather(s, f, f + 1, 1);
         std::vector<double> fl(D->tr->P);
         CKD(cudaMemcpyAsync(fl.data(), f + 1, fl.size() * 8, cudaMemcpyDeviceToHost, s));
@@ -410,13 +603,13 @@ int sparsla_dist_adjoint_backward(sparsla_dist* D, const double* x_owned, const 
             if (vals_t) {
                 if (!D->AT) {
                     std::vector<int32_t> hrp(A->nrows + 1), hci(A->nnz);
-                    CKD(cudaMemcpy(hrp.data(), A->rp, (A->nrows + 1) * 4, cudaMemcpyDeviceToHost));
-                    CKD(cudaMemcpy(hci.data(), A->ci, A->nnz * 4, cudaMemcpyDeviceToHost));
+                    CKD(memcpy_sync(hrp.data(), A->rp, (A->nrows + 1) * 4, cudaMemcpyDeviceToHost));
+                    CKD(memcpy_sync(hci.data(), A->ci, A->nnz * 4, cudaMemcpyDeviceToHost));
                     std::vector<double> hv(A->nnz);
-                    CKD(cudaMemcpy(hv.data(), vals_t, A->nnz * 8, mem == SPARSLA_MEM_DEVICE ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost));
+                    CKD(memcpy_sync(hv.data(), vals_t, A->nnz * 8, mem == SPARSLA_MEM_DEVICE ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost));
                     D->AT = DevCsr::create<int32_t>(A->device, A->nrows, A->ncols, hrp.data(), hci.data(), hv.data(), true);
                 } else {
-                    CKD(cudaMemcpy(D->AT->val, vals_t, A->nnz * 8, mem == SPARSLA_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
+                    CKD(memcpy_sync(D->AT->val, vals_t, A->nnz * 8, mem == SPARSLA_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
                     cudaFree(D->AT->dinv);
                     D->AT->dinv = nullptr;
                 }
@@ -427,7 +620,7 @@ int sparsla_dist_adjoint_backward(sparsla_dist* D, const double* x_owned, const 
             dist_krylov(D, backend, G.d, GB.d, o, rep, SPARSLA_MEM_DEVICE, M);
         }
         // grad_vals: x over [owned | halo] (one exchange), lambda owned
-        DVec XL(x_owned, no, C->n_halo, mem, s);
+        DVec XL(x_owned, no, C->vec_len - no, mem, s);
         C->exchange(s, XL.d);
         CKD(cudaStreamWaitEvent(s, C->ev_halo, 0));
         DVec GV(grad_vals, A->nnz, 0, mem, s, false);

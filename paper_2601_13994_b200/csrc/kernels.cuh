@@ -47,6 +47,8 @@ struct KState {
     long long k, spmv_count, breakdown_iter;
     long long reductions;  // reduction points applied while the solve was live
     int pending_x;         // CG: alpha of this iteration computed, x += alpha p still to apply
+    unsigned long long ep[8];       // fused peer collectives: epochs pushed per reduction point
+    unsigned long long ep_halo[4];  // ... and per halo-pushed vector
     int done, converged, status, halfstep;
     double scratch[8];  // plain dot outputs
 };
@@ -221,6 +223,80 @@ __device__ void final_reduce(const double* partials, long long m, double (&out)[
     block_tree<NT, NDOT, BAR>(out, sred);
 }
 
+// ------------------------------------------ fused peer-memory collectives (N>1) ----
+// Distributed CG without per-iteration NCCL calls: the last CTA of a reduction kernel
+// stores the rank's totals straight into every rank's mailbox (NVLink peer stores, or
+// same-device stores for in-process ranks), fences at system scope and release-stores an
+// epoch flag; the consuming kernel's CTAs acquire-wait on all P flags, sum the totals in
+// ascending rank order and run the scalar step themselves.  The producer of the next SpMV
+// input pushes its boundary values into the neighbours' halo slots inside the same kernel
+// and raises a halo flag; the SpMV waits for it only before its first boundary chunk.
+// Mailboxes are single-buffered: a rank can only overwrite a slot after the reader has
+// pushed its own next contribution, which it does after consuming the slot.
+struct P2PCtx {
+    int P, me, nnbr;
+    double** peer_mail;                // [P] -> rank q's mailbox [8 points][P][8]
+    unsigned long long** peer_mflag;   // [P] -> rank q's flags [8 points][P]
+    unsigned long long** peer_hflag;   // [P] -> rank q's halo flags [4][P]
+    double* my_mail;
+    unsigned long long* my_mflag;
+    unsigned long long* my_hflag;
+    const int32_t* nbr_rank;           // [nnbr]
+    const int32_t* push_ptr;           // [nchunks+1]: halo-push entries of each chunk
+    const int32_t* push_row;           // local owned row
+    const int32_t* push_nbr;           // neighbour index (0..nnbr-1)
+    const long long* push_pos;         // element offset in that neighbour's vector
+    double** peer_vec;                 // [nnbr] -> neighbour's SpMV-input vector
+};
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ double ld_relaxed_sys(const double* p) {
+    double v;
+    asm volatile("ld.relaxed.sys.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// last CTA of a producer kernel (single thread)
+__device__ inline void p2p_push_totals(const P2PCtx* X, KState* st, int point, const double* tot, int k) {
+    const unsigned long long e = ++st->ep[point];
+    for (int q = 0; q < X->P; ++q) {
+        double* dst = X->peer_mail[q] + ((size_t)point * X->P + X->me) * 8;
+        for (int j = 0; j < k; ++j) dst[j] = tot[j];
+    }
+    __threadfence_system();
+    for (int q = 0; q < X->P; ++q) st_release_sys(X->peer_mflag[q] + point * X->P + X->me, e);
+}
+
+// one thread per CTA of a consumer kernel: wait for every rank's totals of `point`, sum
+// them in ascending rank order and apply the scalar step to S
+__device__ inline void p2p_consume(const P2PCtx* X, KState* S, int point, int k, int which) {
+    const unsigned long long e = S->ep[point];
+    for (int q = 0; q < X->P; ++q)
+        while (ld_acquire_sys(X->my_mflag + point * X->P + q) < e) __nanosleep(32);
+    double t[4] = {0, 0, 0, 0};
+    for (int j = 0; j < k; ++j) {
+        double s = ld_relaxed_sys(X->my_mail + ((size_t)point * X->P) * 8 + j);
+        for (int q = 1; q < X->P; ++q) s = __dadd_rn(s, ld_relaxed_sys(X->my_mail + ((size_t)point * X->P + q) * 8 + j));
+        t[j] = s;
+    }
+    apply_scalar(which, S, t);
+}
+
+// wait until every neighbour has pushed this epoch's halo of vector v
+__device__ inline void p2p_wait_halo(const P2PCtx* X, int v, unsigned long long e) {
+    for (int a = 0; a < X->nnbr; ++a) {
+        const int q = X->nbr_rank[a];
+        while (ld_acquire_sys(X->my_hflag + v * X->P + q) < e) __nanosleep(32);
+    }
+}
+
 // Publish this CTA's chunk partials; the last CTA (ticket) finishes the reduction and runs
 // the scalar step (or, distributed, writes the rank's totals for the all-gather).
 struct RedParams {
@@ -231,6 +307,9 @@ struct RedParams {
     KState* st;
     double* red_out;      // distributed: rank totals -> all-gather; else nullptr
     int scalar;           // Scalar op applied by the last CTA (single rank)
+    const P2PCtx* p2p;    // fused peer collectives: push the totals of `point` instead
+    int point;
+    const KState* s_loc;  // consumer kernels: CTA-local scalar state to write back first
 };
 
 template <int NT, int NDOT>
@@ -250,7 +329,15 @@ __device__ void publish_and_finish(double (&part)[NDOT], long long chunk, const 
     double tot[NDOT];
     final_reduce<NT, NDOT>(R.partials, R.nchunks, tot, sred);
     if (threadIdx.x == 0) {
-        if (R.red_out) {
+        if (R.p2p) {
+            if (R.s_loc) *R.st = *R.s_loc;
+            if (!R.st->done) {
+                double t3[4] = {0, 0, 0, 0};
+#pragma unroll
+                for (int d = 0; d < NDOT; ++d) t3[d] = tot[d];
+                p2p_push_totals(R.p2p, R.st, R.point, t3, NDOT);
+            }
+        } else if (R.red_out) {
 #pragma unroll
             for (int d = 0; d < NDOT; ++d) R.red_out[d] = tot[d];
         } else {
@@ -279,7 +366,15 @@ __device__ void ticket_and_finish(const RedParams& R, double* sred, int* s_flag)
     double tot[NDOT];
     final_reduce<NT, NDOT, BAR>(R.partials, R.nchunks, tot, sred);
     if (threadIdx.x == 0) {
-        if (R.red_out) {
+        if (R.p2p) {
+            if (R.s_loc) *R.st = *R.s_loc;
+            if (!R.st->done) {
+                double t3[4] = {0, 0, 0, 0};
+#pragma unroll
+                for (int d = 0; d < NDOT; ++d) t3[d] = tot[d];
+                p2p_push_totals(R.p2p, R.st, R.point, t3, NDOT);
+            }
+        } else if (R.red_out) {
 #pragma unroll
             for (int d = 0; d < NDOT; ++d) R.red_out[d] = tot[d];
         } else {
@@ -361,6 +456,9 @@ struct SpmvParams {
     long long chunk0;   // first chunk index handled by this launch (interior/boundary split)
     long long nch;      // number of chunks handled by this launch
     const int32_t* chunk_list;  // optional: chunk ids of this launch (interior / boundary rows)
+    const P2PCtx* p2p;          // fused peer collectives: list = [interior | boundary] in ONE launch,
+    long long n_interior;       //   consumers wait for the halo before list index n_interior
+    int halo_v;
     const double* aux;  // BICG_V: rhat, BICG_T: s
     int cap_v, cap_c;   // staged capacities (elements) per round
     int l2_keep;        // 1: matrix stream evict_last (working set fits L2), 0: evict_first
@@ -414,6 +512,10 @@ __global__ void __launch_bounds__(kSpmvThreads, 2) spmv_direct_kernel(SpmvParams
     constexpr int NA = ND > 0 ? ND : 1;
     if (P.check_done && P.red.st->done) return;
     const int t = threadIdx.x;
+    if (P.p2p && (long long)blockIdx.x >= P.n_interior) {
+        if (t == 0) p2p_wait_halo(P.p2p, P.halo_v, P.red.st->ep_halo[P.halo_v]);
+        __syncthreads();
+    }
     const long long chunk = P.chunk_list ? (long long)P.chunk_list[blockIdx.x] : P.chunk0 + blockIdx.x;
     const long long base = chunk * kChunk;
     const long long rem_rounds = (P.n - base + kChunkSlots - 1) / kChunkSlots;
@@ -520,7 +622,13 @@ __global__ void __launch_bounds__(kWsThreads, MINB) spmv_ws_kernel(SpmvParams P)
     __shared__ double sred[NA * kConsumerWarps];
     __shared__ int s_flag;
     long long g = 0;
+    bool halo_ready = P.p2p == nullptr;
     for (long long c = blockIdx.x; c < P.nch; c += gridDim.x) {
+        if (!halo_ready && c >= P.n_interior) {  // first boundary chunk: neighbours' pushes landed
+            if (lane == 0) p2p_wait_halo(P.p2p, P.halo_v, P.red.st->ep_halo[P.halo_v]);
+            __syncwarp();
+            halo_ready = true;
+        }
         const long long chunk = P.chunk_list ? (long long)P.chunk_list[c] : P.chunk0 + c;
         const long long base = chunk * kChunk;
         const long long rem = (P.n - base + kChunkSlots - 1) / kChunkSlots;
@@ -819,6 +927,10 @@ struct VecParams {
     const double* b;
     int check_done;
     RedParams red;
+    // fused peer collectives (distributed CG): consume reduction point `consume_point`
+    // (scalar op consume_scalar over consume_k totals) at entry; CG_U2 also pushes the halo
+    const P2PCtx* p2p;
+    int consume_point, consume_scalar, consume_k;
 };
 
 __device__ __forceinline__ double2 ld2(const double* p, long long i, long long n) {
@@ -953,9 +1065,23 @@ __global__ void __launch_bounds__(kVecThreads) vec_kernel(VecParams P) {
     } else {
         if (P.check_done && st->done) return;
     }
+    __shared__ KState s_loc;  // fused peer collectives: this CTA's copy of the scalar state
+    const KState* sc = st;
+    bool skip = false;
+    if constexpr (OP == V_CG_U1 || OP == V_CG_U2) {
+        if (P.p2p) {
+            if (threadIdx.x == 0) {
+                s_loc = *st;
+                p2p_consume(P.p2p, &s_loc, P.consume_point, P.consume_k, P.consume_scalar);
+            }
+            __syncthreads();
+            sc = &s_loc;
+            if constexpr (OP == V_CG_U1) skip = s_loc.done != 0;  // p^T A p breakdown
+        }
+    }
     VecScalars S;
-    if constexpr (OP == V_CG_U1 || OP == V_BI_U2) S.alpha = st->alpha;
-    if constexpr (OP == V_CG_U2) { S.alpha = st->alpha; S.beta = st->beta; S.live = !st->done; }
+    if constexpr (OP == V_CG_U1 || OP == V_BI_U2) S.alpha = sc->alpha;
+    if constexpr (OP == V_CG_U2) { S.alpha = sc->alpha; S.beta = sc->beta; S.live = !sc->done; }
     if constexpr (OP == V_BI_U1) { S.beta = st->beta; S.omega = st->omega; S.first = st->k == 0; }
     if constexpr (OP == V_BI_U3) { S.alpha = st->alpha; S.omega = st->omega; S.half = st->halfstep; }
     const int t = threadIdx.x;
@@ -976,7 +1102,7 @@ __global__ void __launch_bounds__(kVecThreads) vec_kernel(VecParams P) {
 #pragma unroll
         for (int u = 0; u < G; ++u) {
             const long long i = base + (long long)(g + u) * kChunkSlots + 2 * t;
-            if (i >= P.n) continue;
+            if (i >= P.n || skip) continue;
             double pr[NA][2];
             vec_compute<OP>(P, S, i, in[u], pr);
             if constexpr (ND > 0) {
@@ -986,6 +1112,16 @@ __global__ void __launch_bounds__(kVecThreads) vec_kernel(VecParams P) {
                     if (i + 1 < P.n) acc[d][1] = __dadd_rn(acc[d][1], pr[d][1]);
                 }
             }
+        }
+    }
+    if constexpr (OP == V_CG_U2) {
+        // fused halo push: this chunk's boundary values of the new p go straight into the
+        // neighbours' halo slots (written above by this CTA; visible after the barrier)
+        if (P.p2p && S.live) {
+            __syncthreads();
+            const P2PCtx* X = P.p2p;
+            for (int e = X->push_ptr[chunk] + t; e < X->push_ptr[chunk + 1]; e += kVecThreads)
+                X->peer_vec[X->push_nbr[e]][X->push_pos[e]] = P.p[X->push_row[e]];
         }
     }
     if constexpr (ND > 0) {
@@ -999,19 +1135,35 @@ __global__ void __launch_bounds__(kVecThreads) vec_kernel(VecParams P) {
                 for (int d = 0; d < ND; ++d) P.red.partials[d * P.red.nchunks + chunk] = v[d];
             }
         } else {
-            publish_and_finish<kVecThreads, ND>(v, chunk, P.red, sred);
+            RedParams R = P.red;
+            if (P.p2p) { R.p2p = P.p2p; R.s_loc = &s_loc; }
+            publish_and_finish<kVecThreads, ND>(v, chunk, R, sred);
         }
     }
     }  // chunk loop
     if constexpr (ND > 0 && PERSIST) {
         ticket_and_finish<kVecThreads, ND, 0>(P.red, sred, &s_flag);
     } else if constexpr (OP == V_CG_U2) {
-        // the last CTA clears pending_x once every CTA has read it
+        // the last CTA clears pending_x once every CTA has read it; with fused peer
+        // collectives it also publishes this rank's scalar step and raises the halo flags
         __syncthreads();
         if (t == 0) {
-            __threadfence();
+            if (P.p2p) __threadfence_system();  // order this CTA's peer halo stores first
+            else __threadfence();
             if (atomicAdd(P.red.ticket, 1u) == P.red.expected - 1) {
-                st->pending_x = 0;
+                if (P.p2p) {
+                    __threadfence_system();
+                    *st = s_loc;
+                    st->pending_x = 0;
+                    if (S.live) {
+                        const P2PCtx* X = P.p2p;
+                        const unsigned long long e = ++st->ep_halo[0];
+                        for (int a = 0; a < X->nnbr; ++a)
+                            st_release_sys(X->peer_hflag[X->nbr_rank[a]] + 0 * X->P + X->me, e);
+                    }
+                } else {
+                    st->pending_x = 0;
+                }
                 *P.red.ticket = 0u;
                 __threadfence();
             }

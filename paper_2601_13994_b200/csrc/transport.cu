@@ -105,6 +105,41 @@ void NcclTransport::allgather(cudaStream_t s, const double* send, double* recv, 
     ++allgathers;
 }
 
+// ----------------------------------------------------------------------- host ----
+void HostTransport::exchange(cudaStream_t s, const std::vector<HaloPeer>& peers) {
+    CKT(cudaStreamSynchronize(s));
+    std::vector<std::vector<double>> sb(peers.size()), rb(peers.size());
+    std::vector<const double*> sp(peers.size());
+    std::vector<double*> rp(peers.size());
+    std::vector<int32_t> rk(peers.size());
+    std::vector<int64_t> sc(peers.size()), rc(peers.size());
+    for (size_t a = 0; a < peers.size(); ++a) {
+        sb[a].resize((size_t)peers[a].scount);
+        rb[a].resize((size_t)peers[a].rcount);
+        if (peers[a].scount)
+            CKT(memcpy_sync(sb[a].data(), peers[a].send, peers[a].scount * 8, cudaMemcpyDeviceToHost));
+        sp[a] = sb[a].data(); rp[a] = rb[a].data(); rk[a] = peers[a].rank;
+        sc[a] = peers[a].scount; rc[a] = peers[a].rcount;
+    }
+    if (cb.exchange(cb.user, (int32_t)peers.size(), rk.data(), sp.data(), sc.data(), rp.data(), rc.data()) != 0)
+        fail(SPARSLA_ERR_TRANSPORT, "host transport exchange callback failed");
+    for (size_t a = 0; a < peers.size(); ++a)
+        if (peers[a].rcount)
+            CKT(memcpy_sync(peers[a].recv, rb[a].data(), peers[a].rcount * 8, cudaMemcpyHostToDevice));
+    ++exchanges;
+    messages += (long long)peers.size();
+}
+
+void HostTransport::allgather(cudaStream_t s, const double* send, double* recv, int count) {
+    CKT(cudaStreamSynchronize(s));
+    std::vector<double> h(count), all((size_t)count * P);
+    CKT(memcpy_sync(h.data(), send, count * 8, cudaMemcpyDeviceToHost));
+    if (cb.allgather(cb.user, h.data(), all.data(), count) != 0)
+        fail(SPARSLA_ERR_TRANSPORT, "host transport allgather callback failed");
+    CKT(memcpy_sync(recv, all.data(), all.size() * 8, cudaMemcpyHostToDevice));
+    ++allgathers;
+}
+
 // ---------------------------------------------------------------------- local ----
 void TimedBarrier::arrive_and_wait() {
     static const double timeout_s = [] {

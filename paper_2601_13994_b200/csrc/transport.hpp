@@ -57,6 +57,26 @@ struct NcclTransport : Transport {
     void check() override;
 };
 
+// ---- host callbacks (caller-provided collectives, e.g. torch.distributed gloo) ----
+// Setup / init traffic only: device buffers are staged through host memory and the
+// callbacks run synchronously on the calling thread.  With fused peer collectives the
+// iteration itself never calls the transport, so this backing also lets several processes
+// share ONE GPU (cudaIpc peers) — which NCCL refuses.
+struct HostCallbacks {
+    void* user;
+    int (*allgather)(void* user, const double* send, double* recv, int64_t count);
+    int (*exchange)(void* user, int32_t npeers, const int32_t* ranks, const double* const* sbuf,
+                    const int64_t* scount, double* const* rbuf, const int64_t* rcount);
+};
+
+struct HostTransport : Transport {
+    HostCallbacks cb;
+    HostTransport(int nranks, int r, const HostCallbacks& c) : cb(c) { P = nranks; rank = r; }
+    void exchange(cudaStream_t s, const std::vector<HaloPeer>& peers) override;
+    void allgather(cudaStream_t s, const double* send, double* recv, int count) override;
+    bool capturable() const override { return false; }
+};
+
 // ---- in-process (threads) ----
 // Barrier with the reference's collective timeout (default 30 s,
 // SPARSLA_TRANSPORT_TIMEOUT seconds): a rank missing from a collective surfaces as

@@ -702,6 +702,60 @@ def nccl_unique_id() -> bytes:
     return bytes(buf)
 
 
+_AG_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int64)
+_EX_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.POINTER(C.c_double)),
+                     C.POINTER(C.c_int64), C.POINTER(C.POINTER(C.c_double)), C.POINTER(C.c_int64))
+
+
+class _HostTransportC(C.Structure):
+    _fields_ = [("user", C.c_void_p), ("allgather", _AG_FN), ("exchange", _EX_FN)]
+
+
+def torch_host_transport(nranks: int, group=None) -> _HostTransportC:
+    """sparsla_host_transport whose collectives run on torch.distributed (gloo) — setup and
+    init traffic only when the plan uses fused peer collectives."""
+    import traceback
+
+    import torch
+    import torch.distributed as dist
+
+    def ag(user, send, recv, count):
+        try:
+            t = torch.from_numpy(np.ctypeslib.as_array(send, shape=(count,)).copy())
+            outs = [torch.empty(count, dtype=torch.float64) for _ in range(nranks)]
+            dist.all_gather(outs, t, group=group)
+            np.ctypeslib.as_array(recv, shape=(count * nranks,))[:] = torch.cat(outs).numpy()
+            return 0
+        except Exception:  # noqa: BLE001
+            traceback.print_exc()
+            return 1
+
+    def ex(user, npeers, ranks, sbuf, scount, rbuf, rcount):
+        try:
+            reqs, outs = [], []
+            for a in range(npeers):
+                q = int(ranks[a])
+                if scount[a]:
+                    t = torch.from_numpy(np.ctypeslib.as_array(sbuf[a], shape=(scount[a],)).copy())
+                    reqs.append(dist.isend(t, q, group=group))
+                if rcount[a]:
+                    r = torch.empty(int(rcount[a]), dtype=torch.float64)
+                    reqs.append(dist.irecv(r, q, group=group))
+                    outs.append((a, r))
+            for rq in reqs:
+                rq.wait()
+            for a, r in outs:
+                np.ctypeslib.as_array(rbuf[a], shape=(int(rcount[a]),))[:] = r.numpy()
+            return 0
+        except Exception:  # noqa: BLE001
+            traceback.print_exc()
+            return 1
+
+    T = _HostTransportC(None, _AG_FN(ag), _EX_FN(ex))
+    T._keep = (ag, ex)
+    return T
+
+
 class LocalHub:
     """In-process transport hub: P ranks as threads of this process (may share a GPU)."""
 
@@ -737,6 +791,20 @@ class DistPlan:
         return DistPlan(h, len(owned), rows.nnz, dev)
 
     @staticmethod
+    def create_host(dev: int, nranks: int, rank: int, transport: _HostTransportC, rows: CsrMatrix, owned,
+                    part_of, n_global: int) -> "DistPlan":
+        L = _local_handle(rows, owned, part_of, nranks, rank, n_global)
+        try:
+            h = _vp()
+            _check(lib().sparsla_dist_create_host(C.c_int(dev), C.c_int(nranks), C.c_int(rank), C.byref(transport),
+                                                  L, C.byref(h)))
+        finally:
+            lib().sparsla_local_destroy(L)
+        plan = DistPlan(h, len(owned), rows.nnz, dev)
+        plan._transport = transport  # callbacks must outlive the plan
+        return plan
+
+    @staticmethod
     def create_nccl(dev: int, nranks: int, rank: int, uid: bytes, rows: CsrMatrix, owned,
                     part_of, n_global: int) -> "DistPlan":
         L = _local_handle(rows, owned, part_of, nranks, rank, n_global)
@@ -764,6 +832,10 @@ class DistPlan:
 
     def reset_counters(self):
         _check(lib().sparsla_dist_reset_counters(self.h))
+
+    def set_fused(self, on: bool = True):
+        """Fused peer-memory collectives for CG (no NCCL call per iteration)."""
+        _check(lib().sparsla_dist_set_fused(self.h, C.c_int32(1 if on else 0)))
 
     def spmv(self, x_owned):
         x = _f64(x_owned)

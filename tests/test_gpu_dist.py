@@ -141,3 +141,33 @@ def test_dist_rejects_nonsymmetric_pattern(S, gpu):
     owned = [np.nonzero(po == r)[0] for r in range(2)]
     with pytest.raises(S.UnsupportedInputError):
         S.run_ranks(2, lambda r: S.DistPlan.create_local(hub, 0, r, S.owned_rows(A, owned[r]), owned[r], po, n))
+
+
+@pytest.mark.parametrize("kind,p1,P,part", [("poisson3d", 20, 2, "contig"), ("poisson3d", 24, 4, "contig"),
+                                            ("fem2d", 60, 4, "rcb"), ("poisson2d", 90, 3, "contig")])
+def test_dist_cg_fused_peer_collectives_bitwise(S, O, gpu, kind, p1, P, part):
+    """Fused mode: reductions and halos pushed by the kernels into peer memory (same-device
+    pointers for in-process ranks); no transport call per iteration."""
+    A = S.generate(kind, p1, 2601 if kind == "fem2d" else 0)
+    po = partition(S, kind, p1, A, P, part)
+    hub, plans, owned = make_plans(S, A, po, P)
+    for p in plans:
+        p.set_fused(True)
+        p.reset_counters()
+    b = np.ones(A.nrows)
+    opts = S.SolveOptions(atol=0.0, rtol=1e-10, max_iter=5000)
+    for rep_i in range(2):  # twice: epochs / flags restart cleanly per solve
+        res = S.run_ranks(P, lambda r: plans[r].cg(b[owned[r]], opts))
+        xd = np.empty(A.nrows)
+        for r in range(P):
+            xd[owned[r]] = res[r][0]
+        xo, ro, co = O.dist_solve(Ocsr(O, A), b, po, P, atol=0.0, rtol=1e-10, max_iter=5000)
+        rep = res[0][1]
+        assert rep.converged and rep.iterations == ro["iterations"]
+        assert bits([rep.residual_norm])[0] == bits([ro["residual_norm"]])[0]
+        assert np.array_equal(bits(xd), bits(xo))
+    c = plans[0].counters()
+    k = rep.iterations
+    assert c["halo_exchanges"] == 2 * (1 + k) and c["all_reduces"] == 2 * (1 + 2 * k)
+    # transport calls: only the setup / init ones, none per iteration
+    assert c["raw_allgathers"] <= 2 * 2 and c["raw_exchanges"] <= 2 * 2
