@@ -197,6 +197,43 @@ int sparsla_adjoint_backward(sparsla_dcsr* A, const double* x, const double* gra
                              double* grad_b, double* grad_vals, sparsla_solve_report* report,
                              int32_t mem);
 
+/* ===================== eigen-solver (Eq. 4) ================== */
+/* eig_smallest options: a pair converges when ||A v - lambda v||_2 <= tol. */
+typedef struct {
+    double tol;
+    int64_t max_iter;
+    uint64_t seed;          /* initial block, counter-based hash; e.g. 2601 */
+    int32_t preconditioner; /* sparsla_precond: JACOBI or NONE */
+    int32_t _pad;
+} sparsla_eig_options;
+
+/* EigenResult.report.  Non-convergence is reported with per-pair flags,
+ * not returned as an error. */
+typedef struct {
+    int64_t iterations;
+    int64_t spmm_count;      /* block SpMV launches */
+    int64_t converged_pairs;
+    int32_t converged;       /* all k pairs converged */
+    int32_t method;          /* 0 = LOBPCG, 1 = dense Rayleigh-Ritz on the full space */
+    char diagnostic[128];
+} sparsla_eig_report;
+
+/* eig_smallest: the k smallest eigenpairs of a symmetric A (pattern and
+ * values checked to 1e-12, else SPARSLA_ERR_UNSUPPORTED), 1 <= k <= 16 and k <= n/4 above
+ * the dense threshold (64 rows; env SPARSLA_EIG_DENSE_THRESHOLD).  Jacobi-preconditioned
+ * LOBPCG on the GPU.  lambdas[k] ascending; vectors row-major n x k (column m = v_m,
+ * ||v_m|| = 1, largest-magnitude component positive); residual_norms[k] and
+ * pair_converged[k] may be NULL. */
+int sparsla_eig_smallest(sparsla_dcsr* A, int64_t k, const sparsla_eig_options* opts,
+                         double* lambdas, double* vectors, double* residual_norms,
+                         int32_t* pair_converged, sparsla_eig_report* report, int32_t mem);
+/* eig_backward (Eq. 4): grad_vals[e] = sum_m grad_lambdas[m] v_m[i_e] v_m[j_e]
+ * in CSR (= canonical COO) order, no linear solves.  Degenerate eigenvalues (consecutive gap
+ * <= 1e-8) -> SPARSLA_ERR_UNSUPPORTED.  lambdas and grad_lambdas are host arrays; vectors
+ * (n x k) and grad_vals (nnz) follow `mem`. */
+int sparsla_eig_backward(sparsla_dcsr* A, int64_t k, const double* lambdas, const double* vectors,
+                         const double* grad_lambdas, double* grad_vals, int32_t mem);
+
 /* ============ bench / instrumentation hooks (persistent device-resident solver) ========= */
 /* A prepared solver keeps b, x and all work vectors resident and captures the iteration
  * in a CUDA graph; `iterate` runs up to `iters` more iterations (stops early when the

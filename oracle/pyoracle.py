@@ -420,3 +420,51 @@ def ref_symmetry(nrows, ncols, rows, cols, vals, tol=1e-12):
     if rc:
         raise RefError(rc, R.ref_last_error().decode())
     return bool(s1.value), bool(s2.value)
+
+
+# ------------------------------------------------------------------ eigen-solver oracle --
+# SPEC.md:274-327 has no executable reference; its own oracle is a dense symmetric
+# eigensolver and central finite differences for Eq. 4.
+def eig_sign(V):
+    """largest-magnitude component of each column positive (first index on ties)."""
+    V = np.array(V, dtype=np.float64, copy=True)
+    for j in range(V.shape[1]):
+        i = int(np.argmax(np.abs(V[:, j])))
+        if V[i, j] < 0:
+            V[:, j] = -V[:, j]
+    return V
+
+
+def eig_dense(A: Csr, k: int):
+    """k smallest eigenpairs of the dense symmetric matrix (LAPACK syevd via numpy)."""
+    w, U = np.linalg.eigh(A.dense())
+    return w[:k], eig_sign(U[:, :k])
+
+
+def eig_backward(A: Csr, V, g):
+    """Eq. 4: grad_vals[e] = sum_m g_m v_m[i_e] v_m[j_e], stored-entry order."""
+    rows = np.repeat(np.arange(A.nrows), np.diff(A.row_ptr))
+    cols = np.asarray(A.col_idx)
+    V = np.asarray(V)
+    return np.einsum("em,em,m->e", V[rows], V[cols], np.asarray(g, dtype=np.float64))
+
+
+def eig_fd(A: Csr, k: int, g, eps=1e-5, entries=None):
+    """Central finite differences of sum_m g_m lambda_m, perturbing one STORED entry at a
+    time ((i,j) and (j,i) are separate parameters).  A single-entry
+    perturbation E makes A nonsymmetric; to first order d(lambda) = v^T E v, which equals
+    that of its symmetric part (E + E^T)/2, so eps/2 is applied at (i,j) and (j,i) and the
+    symmetric eigensolver is used (same derivative, real spectrum)."""
+    Ad = A.dense()
+    rows = np.repeat(np.arange(A.nrows), np.diff(A.row_ptr))
+    cols = np.asarray(A.col_idx)
+    idx = range(len(cols)) if entries is None else entries
+    out = []
+    for e in idx:
+        i, j = rows[e], cols[e]
+        Ap = Ad.copy(); Ap[i, j] += eps / 2; Ap[j, i] += eps / 2
+        Am = Ad.copy(); Am[i, j] -= eps / 2; Am[j, i] -= eps / 2
+        lp = np.linalg.eigvalsh(Ap)[:k]
+        lm = np.linalg.eigvalsh(Am)[:k]
+        out.append(float(np.dot(g, (lp - lm) / (2 * eps))))
+    return np.array(out)

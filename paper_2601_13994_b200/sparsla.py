@@ -9,6 +9,7 @@ SPEC.md contracts of the missing solve / adjoint / distributed sources:
     SolveOptions, SolveReport, JacobiPreconditioner, jacobi_build,
     cg_solve, bicgstab_solve                                       (SPEC.md:122-206)
     AdjointContext, GradientBundle, solve_forward, solve_backward  (SPEC.md:208-272)
+    EigenResult, eig_smallest, eig_backward                        (SPEC.md:274-327)
     partition_contiguous, partition_rcb, build_local               (SPEC.md:417-469)
     poisson2d / poisson3d / convdiff3d / fem2d generators
 
@@ -487,6 +488,93 @@ def solve_backward(ctx: AdjointContext, grad_x, opts: SolveOptions | None = None
     if not r.converged:
         raise Error(f"adjoint solve did not converge: {r.diagnostic}")
     return GradientBundle(gb, gv, r)
+
+
+# ---------------------------------------------------------------------- eigen-solver --
+class _EigOpts(C.Structure):
+    _fields_ = [("tol", C.c_double), ("max_iter", C.c_int64), ("seed", C.c_uint64),
+                ("preconditioner", C.c_int32), ("_pad", C.c_int32)]
+
+
+class _EigReport(C.Structure):
+    _fields_ = [("iterations", C.c_int64), ("spmm_count", C.c_int64),
+                ("converged_pairs", C.c_int64), ("converged", C.c_int32),
+                ("method", C.c_int32), ("diagnostic", C.c_char * 128)]
+
+
+@dataclass
+class EigenReport:
+    """EigenResult.report: iterations, per-pair residual norms and flags."""
+    iterations: int = 0
+    residual_norms: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    pair_converged: np.ndarray = field(default_factory=lambda: np.zeros(0, dtype=bool))
+    converged: bool = False
+    spmm_count: int = 0
+    method: str = "lobpcg"
+    diagnostic: str = ""
+
+
+@dataclass
+class EigenResult:
+    """lambdas ascending (k), vectors n x k (column m = v_m, unit norm,
+    largest-magnitude component positive), report."""
+    lambdas: np.ndarray
+    vectors: np.ndarray
+    report: EigenReport
+
+
+def eig_smallest(a, k: int, tol: float = 1e-8, max_iter: int = 10000, seed: int = 2601,
+                 preconditioner: str = "jacobi") -> EigenResult:
+    """k smallest eigenpairs of a symmetric sparse matrix: Jacobi-
+    preconditioned LOBPCG on the GPU (dense Rayleigh-Ritz on the full space below the dense
+    threshold).  Non-symmetric input raises UnsupportedInputError; non-convergence returns
+    the partial result with per-pair flags."""
+    if isinstance(a, SparseCoo):
+        a = CsrMatrix.from_coo(a)
+    D = _dev_of(a)
+    pc = {"none": PRECOND_NONE, "jacobi": PRECOND_JACOBI}.get(preconditioner)
+    if pc is None:
+        raise InvalidArgumentError(f"unknown preconditioner {preconditioner!r}")
+    k = int(k)
+    n = D.nrows
+    if k < 1 or k > max(n, 0):
+        raise InvalidArgumentError("eig_smallest: need 1 <= k <= n")
+    lam = np.empty(k)
+    V = np.empty((n, k))
+    res = np.empty(k)
+    conv = np.empty(k, dtype=np.int32)
+    o = _EigOpts(float(tol), int(max_iter), int(seed) & ((1 << 64) - 1), pc, 0)
+    rep = _EigReport()
+    _check(lib().sparsla_eig_smallest(D.h, C.c_int64(k), C.byref(o), _p(lam, _f64p), _p(V, _f64p),
+                                      _p(res, _f64p), _p(conv, _i32p), C.byref(rep),
+                                      C.c_int32(MEM_HOST)))
+    r = EigenReport(int(rep.iterations), res, conv.astype(bool), bool(rep.converged),
+                    int(rep.spmm_count), "dense" if rep.method == 1 else "lobpcg",
+                    rep.diagnostic.decode(errors="replace"))
+    return EigenResult(lam, V, r)
+
+
+def eig_backward(result: EigenResult, a_pattern, grad_lambdas) -> np.ndarray:
+    """Eq. 4: grad_vals[e] = sum_m grad_lambdas[m] v_m[i_e] v_m[j_e] over
+    the stored entries of a_pattern (canonical COO order); no linear solves.  Requires all
+    pairs converged and simple eigenvalues (gap > 1e-8), else raises."""
+    if isinstance(a_pattern, SparseCoo):
+        a_pattern = CsrMatrix.from_coo(a_pattern)
+    D = _dev_of(a_pattern)
+    lam = _f64(result.lambdas)
+    k = len(lam)
+    g = _f64(grad_lambdas)
+    if len(g) != k:
+        raise DimensionError(f"grad_lambdas has length {len(g)}, expected {k}")
+    V = _f64(result.vectors)
+    if V.shape != (D.nrows, k):
+        raise DimensionError(f"vectors shape {V.shape}, expected {(D.nrows, k)}")
+    if not bool(np.all(result.report.pair_converged)):
+        raise InvalidArgumentError("eig_backward: not all eigenpairs converged")
+    gv = np.empty(D.nnz)
+    _check(lib().sparsla_eig_backward(D.h, C.c_int64(k), _p(lam, _f64p), _p(V, _f64p), _p(g, _f64p),
+                                      _p(gv, _f64p), C.c_int32(MEM_HOST)))
+    return gv
 
 
 # --------------------------------------------------------------- persistent solver ---

@@ -1,0 +1,170 @@
+"""GPU parity of the eigen-solver: LOBPCG on sm_100a against the dense
+symmetric eigensolver oracle and the closed-form Poisson spectrum, plus Eq. 4's gradient
+against the oracle gather and central finite differences.  Tolerances are SPEC's:
+eigenvalues 1e-8 absolute, ||v|| = 1 +- 1e-10, |v_p.v_q| <= 1e-8,
+residual <= tol, FD relative error < 1e-5."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def ocsr(O, A):
+    return O.Csr(A.nrows, A.ncols, A.row_ptr, A.col_idx, A.vals)
+
+
+def from_dense(S, D):
+    D = np.asarray(D, dtype=np.float64)
+    r, c = np.nonzero(D)
+    return S.CsrMatrix.from_coo(S.SparseCoo(r, c, D[r, c], (D.shape[0], D.shape[1])))
+
+
+def poisson_spectrum(dims, N):
+    t = 2.0 - 2.0 * np.cos(np.pi * np.arange(1, N + 1) / (N + 1))
+    if dims == 2:
+        return np.sort(np.add.outer(t, t).ravel())
+    return np.sort(np.add.outer(np.add.outer(t, t), t).ravel())
+
+
+def check_invariants(O, A, res, tol):
+    lam, V = res.lambdas, res.vectors
+    n, k = V.shape
+    assert np.all(np.diff(lam) >= 0)
+    assert np.max(np.abs(np.linalg.norm(V, axis=0) - 1.0)) <= 1e-10
+    G = V.T @ V - np.eye(k)
+    assert np.max(np.abs(G)) <= 1e-8
+    Ao = ocsr(O, A)
+    for m in range(k):
+        r = O.spmv(Ao, V[:, m]) - lam[m] * V[:, m]
+        assert np.linalg.norm(r) <= tol * (1 + 1e-6), (m, np.linalg.norm(r))
+        i = int(np.argmax(np.abs(V[:, m])))
+        assert V[i, m] > 0
+    assert res.report.converged and np.all(res.report.pair_converged)
+
+
+def test_spec_examples_dense_path(S, O, gpu):
+    A = from_dense(S, np.diag([1.0, 2.0, 3.0, 4.0]))
+    r = S.eig_smallest(A, 2, tol=1e-10)
+    assert r.report.method == "dense"
+    assert np.allclose(r.lambdas, [1.0, 2.0], atol=1e-14)
+    assert np.allclose(r.vectors, np.eye(4)[:, :2], atol=1e-14)
+    B = from_dense(S, [[2.0, 1.0], [1.0, 2.0]])
+    r = S.eig_smallest(B, 1, tol=1e-10)
+    assert abs(r.lambdas[0] - 1.0) < 1e-14
+    assert np.allclose(r.vectors[:, 0], np.array([1.0, -1.0]) / np.sqrt(2), atol=1e-14)
+    g = S.eig_backward(r, B, [1.0])
+    assert np.allclose(g, [0.5, -0.5, -0.5, 0.5], atol=1e-14)
+    assert np.all(S.eig_backward(r, B, [0.0]) == 0.0)
+
+
+def test_poisson16_k6_lobpcg_vs_dense(S, O, gpu):
+    A = S.generate("poisson2d", 16)
+    r = S.eig_smallest(A, 6, tol=1e-9)
+    assert r.report.method == "lobpcg"
+    w, _ = O.eig_dense(ocsr(O, A), 6)
+    assert np.max(np.abs(r.lambdas - w)) <= 1e-8
+    assert np.max(np.abs(r.lambdas - poisson_spectrum(2, 16)[:6])) <= 1e-8
+    check_invariants(O, A, r, 1e-9)
+
+
+@pytest.mark.parametrize("seed", [1, 2601])
+def test_random_symmetric_vs_dense(S, O, gpu, seed):
+    rng = np.random.default_rng(seed)
+    n, k = 256, 5
+    M = rng.standard_normal((n, n)) * (rng.random((n, n)) < 0.03)
+    M = M + M.T + np.diag(np.linspace(1.0, 50.0, n))
+    A = from_dense(S, M)
+    r = S.eig_smallest(A, k, tol=1e-9, seed=seed)
+    w, U = O.eig_dense(ocsr(O, A), k)
+    assert np.max(np.abs(r.lambdas - w)) <= 1e-8
+    check_invariants(O, A, r, 1e-9)
+    # simple spectrum: vectors equal the oracle's under the sign convention
+    assert np.max(np.abs(r.vectors - U)) <= 1e-6
+
+
+def test_dense_and_lobpcg_paths_agree(S, O, gpu, monkeypatch):
+    A = S.generate("poisson2d", 9)  # n = 81
+    r1 = S.eig_smallest(A, 4, tol=1e-10)
+    monkeypatch.setenv("SPARSLA_EIG_DENSE_THRESHOLD", "128")
+    r2 = S.eig_smallest(A, 4, tol=1e-10)
+    assert (r1.report.method, r2.report.method) == ("lobpcg", "dense")
+    assert np.max(np.abs(r1.lambdas - r2.lambdas)) <= 1e-12
+
+
+def test_trace_consistency_dense(S, O, gpu):
+    A = S.generate("poisson2d", 4)
+    r = S.eig_smallest(A, A.nrows, tol=1e-10)
+    assert abs(r.lambdas.sum() - 4.0 * A.nrows) < 1e-9
+
+
+@pytest.mark.parametrize("dims,N,k", [(3, 32, 6), (2, 100, 6), (3, 20, 16)])
+def test_poisson_closed_form(S, O, gpu, dims, N, k):
+    A = S.generate("poisson3d" if dims == 3 else "poisson2d", N)
+    r = S.eig_smallest(A, k, tol=1e-8, max_iter=5000)
+    assert r.report.converged, r.report.diagnostic
+    assert np.max(np.abs(r.lambdas - poisson_spectrum(dims, N)[:k])) <= 1e-8
+    check_invariants(O, A, r, 1e-8)
+
+
+def test_fem_matrix(S, O, gpu):
+    A = S.generate("fem2d", 40)
+    r = S.eig_smallest(A, 6, tol=1e-8, max_iter=5000)
+    w, _ = O.eig_dense(ocsr(O, A), 6)
+    assert np.max(np.abs(r.lambdas - w)) <= 1e-8
+    check_invariants(O, A, r, 1e-8)
+
+
+def test_nonsymmetric_rejected(S, gpu):
+    A = S.generate("convdiff3d", 6, 0, 1.0)
+    with pytest.raises(S.UnsupportedInputError):
+        S.eig_smallest(A, 2)
+    with pytest.raises(S.InvalidArgumentError):
+        S.eig_smallest(S.generate("poisson2d", 3), 10)  # k > n
+    with pytest.raises(S.InvalidArgumentError):
+        S.eig_smallest(S.generate("poisson2d", 16), 0)
+    with pytest.raises(S.UnsupportedInputError):
+        S.eig_smallest(S.generate("poisson2d", 16), 17)  # GPU block limit
+
+
+def test_nonconvergence_partial_result(S, gpu):
+    A = S.generate("poisson2d", 40)
+    r = S.eig_smallest(A, 4, tol=1e-12, max_iter=2)
+    assert not r.report.converged and r.report.iterations == 2
+    assert len(r.report.pair_converged) == 4
+    with pytest.raises(S.InvalidArgumentError):
+        S.eig_backward(r, A, np.ones(4))
+
+
+def test_eig_backward_degenerate_rejected(S, gpu):
+    A = S.generate("poisson2d", 16)  # lambda(1,2) == lambda(2,1)
+    r = S.eig_smallest(A, 3, tol=1e-10)
+    with pytest.raises(S.UnsupportedInputError):
+        S.eig_backward(r, A, np.ones(3))
+
+
+def test_eig_backward_fd_n1024(S, O, gpu):
+    """SPEC.md:306 / PAPER Table 4 'Eigenvalue (k=6)': n = 1024, random grad_lambdas,
+    FD relative error < 1e-5.  A 2-D Poisson 32x32 with a graded diagonal (simple spectrum)."""
+    P = S.generate("poisson2d", 32)
+    n = P.nrows
+    vals = P.vals.copy()
+    rows = np.repeat(np.arange(n), np.diff(P.row_ptr))
+    diag = rows == P.col_idx
+    vals[diag] += 0.5 * np.arange(n) / n
+    A = S.CsrMatrix(n, n, P.row_ptr, P.col_idx, vals)
+    r = S.eig_smallest(A, 6, tol=1e-11, max_iter=5000)
+    assert r.report.converged
+    Ao = ocsr(O, A)
+    w, _ = O.eig_dense(Ao, 6)
+    assert np.max(np.abs(r.lambdas - w)) <= 1e-8 and np.all(np.diff(w) > 1e-8)
+    g = np.random.default_rng(2601).standard_normal(6)
+    gv = S.eig_backward(r, A, g)
+    ref = O.eig_backward(Ao, r.vectors, g)
+    assert np.max(np.abs(gv - ref)) <= 1e-14 * max(1.0, np.max(np.abs(ref)))
+    ent = list(range(0, A.nnz, A.nnz // 12))
+    fd = O.eig_fd(Ao, 6, g, entries=ent)
+    assert np.max(np.abs(fd - gv[ent])) / np.max(np.abs(gv[ent])) < 1e-5
+    # linearity in grad_lambdas
+    g2 = np.random.default_rng(7).standard_normal(6)
+    lin = S.eig_backward(r, A, 2.0 * g + g2)
+    assert np.max(np.abs(lin - (2.0 * gv + S.eig_backward(r, A, g2)))) <= 1e-12 * np.max(np.abs(lin))
