@@ -43,8 +43,6 @@ constexpr int kMaxK = 16;             // block size limit of the GPU LOBPCG
 constexpr int kMaxQ = 3 * kMaxK;      // basis columns [X | W | P]
 constexpr int kRedCTAs = 296;         // fixed reduction grid (device-independent result)
 constexpr int kT = 256;
-constexpr int kGramTile = 32;         // rows per shared-memory tile in gram_kernel
-constexpr int kGramR = 3;             // 3x3 register tile of the Gram matrix per thread
 
 template <class T>
 T* dalloc(size_t count) {
@@ -58,8 +56,8 @@ struct Cols {  // column list of a row-major block buffer (kernel parameter)
     unsigned char c[kMaxQ] = {};
 };
 
-struct Mat {  // small dense coefficient matrix a x c (row-major), kernel parameter
-    double v[kMaxQ * kMaxK];
+struct Mat {  // small dense coefficient matrix a x c (row-major, c <= 2 kMaxK), kernel parameter
+    double v[kMaxQ * 2 * kMaxK];
 };
 
 // Copy a column list into shared memory with constant indices (a dynamically indexed
@@ -106,8 +104,11 @@ __global__ void eye_kernel(double* S, long long n, int ld) {
     for (int j = 0; j < ld; ++j) S[i * ld + j] = (j == i) ? 1.0 : 0.0;
 }
 
-// Block SpMV: Y[i, out_j] = sum_k A_ik S[c_k, in_j] for the listed columns, 8 columns per
-// pass over the row (the matrix row is re-read from L1 for wider blocks).
+// Block SpMV: Y[i, out_j] = sum_k A_ik S[c_k, in_j] for NW listed columns (one thread per
+// row, all NW accumulators in registers).  VEC: the columns are one contiguous, even-aligned
+// range (the usual case), so every gathered row segment and every output row segment moves
+// as 16-byte double2 accesses.
+template <int NW, bool VEC>
 __global__ void __launch_bounds__(kT) spmm_kernel(const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
                                                   const double* __restrict__ val, long long n,
                                                   const double* __restrict__ S, int lds, Cols in, double* Y,
@@ -118,73 +119,144 @@ __global__ void __launch_bounds__(kT) spmm_kernel(const int32_t* __restrict__ rp
     __syncthreads();
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
+    int col[NW];
+#pragma unroll
+    for (int j = 0; j < NW; ++j) col[j] = s_in[j];
     const int kb = __ldg(rp + i), ke = __ldg(rp + i + 1);
-    for (int g = 0; g < in.n; g += 8) {
-        const int w = min(8, in.n - g);
-        int col[8];
+    double acc[NW];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) col[j] = j < w ? s_in[g + j] : 0;
-        double acc[8];
+    for (int j = 0; j < NW; ++j) acc[j] = 0.0;
+    for (int k = kb; k < ke; ++k) {
+        const double v = __ldg(val + k);
+        const double* srow = S + (size_t)__ldg(ci + k) * lds;
+        if constexpr (VEC) {
+            const double2* s2 = reinterpret_cast<const double2*>(srow + col[0]);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[j] = 0.0;
-        for (int k = kb; k < ke; ++k) {
-            const double v = __ldg(val + k);
-            const double* s = S + (size_t)__ldg(ci + k) * lds;
+            for (int j = 0; j < NW / 2; ++j) {
+                const double2 x = __ldg(s2 + j);
+                acc[2 * j] = fma(v, x.x, acc[2 * j]);
+                acc[2 * j + 1] = fma(v, x.y, acc[2 * j + 1]);
+            }
+        } else {
 #pragma unroll
-            for (int j = 0; j < 8; ++j)
-                if (j < w) acc[j] = fma(v, __ldg(s + col[j]), acc[j]);
+            for (int j = 0; j < NW; ++j) acc[j] = fma(v, __ldg(srow + col[j]), acc[j]);
         }
+    }
+    double* yrow = Y + i * ldy;
+    if constexpr (VEC) {
+        double2* y2 = reinterpret_cast<double2*>(yrow + s_out[0]);
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
-            if (j < w) Y[i * ldy + s_out[g + j]] = acc[j];
+        for (int j = 0; j < NW / 2; ++j) y2[j] = make_double2(acc[2 * j], acc[2 * j + 1]);
+    } else {
+#pragma unroll
+        for (int j = 0; j < NW; ++j) yrow[s_out[j]] = acc[j];
     }
 }
 
-// Gram block G = U_uc^T V_vc (a x b) over the CTA's row range: rows are staged through
-// shared memory 32 at a time; each thread owns a 3x3 register tile of G and a residue
-// class of the tile's rows; groups are combined in a fixed order.  One partial per CTA.
-__global__ void __launch_bounds__(kT) gram_kernel(const double* __restrict__ U, int ldu, Cols uc,
-                                                  const double* __restrict__ V, int ldv, Cols vc, long long n,
-                                                  double* partial) {
-    constexpr int TR = kGramTile, R = kGramR, LDS = kMaxQ + 1;
-    __shared__ double sh[2 * TR * LDS];
-    __shared__ int s_uc[kMaxQ], s_vc[kMaxQ];
+#define SPARSLA_FOR_1_32(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16) \
+    X(17) X(18) X(19) X(20) X(21) X(22) X(23) X(24) X(25) X(26) X(27) X(28) X(29) X(30) X(31) X(32)
+
+// ------------------------------------------------- row-tile staging (TMA bulk) ----
+// The block kernels below stream whole basis rows: a tile of kTR consecutive rows of a
+// row-major buffer is one contiguous range (kTR * ld doubles, ld even -> 16-byte multiple),
+// copied into shared memory by one cp.async.bulk per buffer with mbarrier completion.  Each
+// CTA walks the tiles t = blockIdx.x + j * gridDim.x through a kEStages-deep ring; thread 0
+// re-arms a stage right after the CTA barrier that ends its use.  Outputs are assembled in
+// shared memory and written back by bulk stores (cp.async.bulk.global.shared::cta).
+constexpr int kTR = 64;    // Gram tiles
+constexpr int kTRa = 128;  // apply tiles (one thread per row)
+constexpr int kEStages = 3;
+constexpr int kTileR = 6;  // 6x6 register tile of the Gram matrix per thread
+
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* dst, const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                 ::"l"(dst), "r"(smem_addr(src)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+template <int TR>
+struct TileWalk {
+    long long n, ntiles, mine;
+    int ld;
+    __device__ TileWalk(long long n_, int ld_) : n(n_), ld(ld_) {
+        ntiles = (n + TR - 1) / TR;
+        mine = (long long)blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    }
+    __device__ long long row0(long long j) const { return ((long long)blockIdx.x + j * gridDim.x) * TR; }
+    __device__ int rows(long long j) const { return (int)min((long long)TR, n - row0(j)); }
+    // thread 0: load tile j of up to two buffers into stage s
+    __device__ void issue(long long j, int s, uint64_t* bar, double* stage, const double* A, const double* B) const {
+        const long long r0 = row0(j);
+        const uint32_t bytes = (uint32_t)rows(j) * (uint32_t)ld * 8u;
+        const size_t te = (size_t)TR * ld;
+        mbar_arrive_expect_tx(&bar[s], B ? 2 * bytes : bytes);
+        bulk_load(stage, A + r0 * ld, bytes, &bar[s]);
+        if (B) bulk_load(stage + te, B + r0 * ld, bytes, &bar[s]);
+    }
+};
+
+// Gram block G = U_uc^T V_vc (a x b <= 48 x 48).  Each thread owns a 6x6 register tile of G
+// and a residue class of every tile's rows; row groups are combined in ascending order, CTA
+// partials land in `partial`, and the last CTA (ticket) sums them in CTA order into `out`.
+// The grid is fixed (kRedCTAs), so the result is deterministic and device-independent.
+__global__ void __launch_bounds__(kT) gram_kernel(const double* __restrict__ U, const double* __restrict__ V, int ld,
+                                                  Cols uc, Cols vc, long long n, double* partial,
+                                                  unsigned* ticket, double* out, int nst) {
+    constexpr int R = kTileR;
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem);  // [nst <= 8]
+    int* s_uc = reinterpret_cast<int*>(smem + 64);
+    int* s_vc = s_uc + kMaxQ;
+    double* red = reinterpret_cast<double*>(smem + 512);
+    double* ring = red + kMaxQ * kMaxQ;
+    const bool two = U != V;
+    const size_t te = (size_t)kTR * ld, st_el = two ? 2 * te : te;
+    const int a = uc.n, b = vc.n, ab = a * b;
+    const int TI = (a + R - 1) / R, TJ = (b + R - 1) / R, tiles = TI * TJ;
+    const int ngroups = min(kTR, max(1, kT / tiles));
+    const int tid = threadIdx.x, grp = tid / tiles, tt = tid - grp * tiles;
+    const bool act = grp < ngroups;
+    const int ti = tt / TJ, tj = tt - ti * TJ;
     stage_cols(uc, s_uc);
     stage_cols(vc, s_vc);
-    double* Us = sh;
-    double* Vs = sh + TR * LDS;
-    const int a = uc.n, b = vc.n;
-    const int TI = (a + R - 1) / R, TJ = (b + R - 1) / R, tiles = TI * TJ;
-    const int ngroups = max(1, kT / tiles);
-    const int tid = threadIdx.x, grp = tid / tiles, tt = tid % tiles;
-    const bool act = grp < ngroups;
-    const int ti = tt / TJ, tj = tt % TJ;
+    const TileWalk<kTR> W(n, ld);
+    if (tid == 0) {
+        for (int s = 0; s < nst; ++s) mbar_init(&bar[s], 1);
+        fence_mbar_init();
+        for (long long j = 0; j < min((long long)nst, W.mine); ++j)
+            W.issue(j, (int)j, bar, ring + j * st_el, U, two ? V : nullptr);
+    }
+    __syncthreads();
+    int cu[R], cv[R];
+#pragma unroll
+    for (int x = 0; x < R; ++x) {
+        cu[x] = ti * R + x < a ? s_uc[ti * R + x] : 0;
+        cv[x] = tj * R + x < b ? s_vc[tj * R + x] : 0;
+    }
     double acc[R][R];
 #pragma unroll
     for (int x = 0; x < R; ++x)
 #pragma unroll
         for (int y = 0; y < R; ++y) acc[x][y] = 0.0;
-    long long r0, r1;
-    cta_rows(n, r0, r1);
-    __syncthreads();
-    for (long long base = r0; base < r1; base += TR) {
-        const int nr = (int)min((long long)TR, r1 - base);
-        for (int e = tid; e < nr * a; e += kT) {
-            const int r = e / a, l = e - r * a;
-            Us[r * LDS + l] = __ldg(U + (base + r) * ldu + s_uc[l]);
-        }
-        for (int e = tid; e < nr * b; e += kT) {
-            const int r = e / b, l = e - r * b;
-            Vs[r * LDS + l] = __ldg(V + (base + r) * ldv + s_vc[l]);
-        }
-        __syncthreads();
+    for (long long j = 0; j < W.mine; ++j) {
+        const int s = (int)(j % nst);
+        mbar_wait(&bar[s], (uint32_t)((j / nst) & 1));
+        const double* Ut = ring + s * st_el;
+        const double* Vt = two ? Ut + te : Ut;
+        const int nr = W.rows(j);
         if (act) {
             for (int r = grp; r < nr; r += ngroups) {
                 double u[R], v[R];
 #pragma unroll
-                for (int x = 0; x < R; ++x) u[x] = ti * R + x < a ? Us[r * LDS + ti * R + x] : 0.0;
+                for (int x = 0; x < R; ++x) u[x] = Ut[r * ld + cu[x]];
 #pragma unroll
-                for (int y = 0; y < R; ++y) v[y] = tj * R + y < b ? Vs[r * LDS + tj * R + y] : 0.0;
+                for (int y = 0; y < R; ++y) v[y] = Vt[r * ld + cv[y]];
 #pragma unroll
                 for (int x = 0; x < R; ++x)
 #pragma unroll
@@ -192,34 +264,208 @@ __global__ void __launch_bounds__(kT) gram_kernel(const double* __restrict__ U, 
             }
         }
         __syncthreads();
+        if (tid == 0 && j + nst < W.mine) {
+            fence_proxy_async_smem();
+            W.issue(j + nst, s, bar, ring + s * st_el, U, two ? V : nullptr);
+        }
     }
-    // combine the row groups in ascending group order (ngroups * a * b <= 9 * 256 doubles)
-    const int ab = a * b;
+    // row groups in ascending order: every group's tile into the drained ring
+    // (ngroups * ab <= 36 * 256 doubles), then one ordered sum per entry
+    double* gbuf = ring;
     if (act) {
 #pragma unroll
         for (int x = 0; x < R; ++x)
 #pragma unroll
             for (int y = 0; y < R; ++y) {
-                const int i = ti * R + x, j = tj * R + y;
-                if (i < a && j < b) sh[grp * ab + i * b + j] = acc[x][y];
+                const int i = ti * R + x, k = tj * R + y;
+                if (i < a && k < b) gbuf[(size_t)grp * ab + i * b + k] = acc[x][y];
             }
     }
     __syncthreads();
     for (int e = tid; e < ab; e += kT) {
-        double s = 0.0;
-        for (int g = 0; g < ngroups; ++g) s += sh[g * ab + e];
-        partial[(size_t)blockIdx.x * ab + e] = s;
+        double sum = 0.0;
+        for (int g = 0; g < ngroups; ++g) sum += gbuf[(size_t)g * ab + e];
+        red[e] = sum;
     }
+    __syncthreads();
+    for (int e = tid; e < ab; e += kT) partial[(size_t)blockIdx.x * ab + e] = red[e];
+    __shared__ int s_last;
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    const int P = gridDim.x;
+    for (int e = tid; e < ab; e += kT) {
+        double sum = 0.0;
+        int p = 0;
+        for (; p + 8 <= P; p += 8) {
+            double t[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) t[q] = __ldcg(partial + (size_t)(p + q) * ab + e);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) sum += t[q];
+        }
+        for (; p < P; ++p) sum += __ldcg(partial + (size_t)p * ab + e);
+        out[e] = sum;
+    }
+    if (tid == 0) *ticket = 0u;
 }
 
-// Sum of the per-CTA partials in CTA order (one thread per entry).
-__global__ void partial_sum_kernel(const double* partial, int nparts, int ab, double* out) {
-    const int e = blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= ab) return;
-    double s = 0.0;
-    for (int p = 0; p < nparts; ++p) s += partial[(size_t)p * ab + e];
-    out[e] = s;
+// In-place block transform of whole rows: S[:, out_j] = sum_l S[:, in_l] M[l, j]
+// (a = in.n <= 48 inputs, c = out.n <= 32 outputs).  One thread per row (kTRa rows per
+// tile): the coefficients are warp-uniform constant-bank reads; the row's inputs are read
+// from the staged tile before its outputs are written back into it, then the whole rows
+// are bulk-stored.
+template <int C>
+__global__ void __launch_bounds__(kTRa) apply_kernel(double* S, int ld, Cols in, Cols out, long long n, const Mat M) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+    int* s_in = reinterpret_cast<int*>(smem + 64);
+    int* s_out = s_in + kMaxQ;
+    double* ring = reinterpret_cast<double*>(smem + 512);
+    const size_t te = (size_t)kTRa * ld;
+    const int a = in.n;
+    stage_cols(in, s_in);
+    stage_cols(out, s_out);
+    const TileWalk<kTRa> W(n, ld);
+    const int row = threadIdx.x;
+    if (row == 0) {
+        for (int s = 0; s < kEStages; ++s) mbar_init(&bar[s], 1);
+        fence_mbar_init();
+        for (long long j = 0; j < min((long long)kEStages, W.mine); ++j)
+            W.issue(j, (int)j, bar, ring + j * te, S, nullptr);
+    }
+    __syncthreads();
+    for (long long j = 0; j < W.mine; ++j) {
+        const int s = (int)(j % kEStages);
+        mbar_wait(&bar[s], (uint32_t)((j / kEStages) & 1));
+        double* T = ring + s * te;
+        const int nr = W.rows(j);
+        if (row < nr) {
+            double* t = T + row * ld;
+            double acc[C];
+#pragma unroll
+            for (int q = 0; q < C; ++q) acc[q] = 0.0;
+            for (int l = 0; l < a; ++l) {  // warp-uniform coefficient row l
+                const double u = t[s_in[l]];
+                const double* Ml = M.v + l * C;
+#pragma unroll
+                for (int q = 0; q < C; ++q) acc[q] = fma(u, Ml[q], acc[q]);
+            }
+#pragma unroll
+            for (int q = 0; q < C; ++q) t[s_out[q]] = acc[q];
+        }
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (row == 0) {
+            bulk_store(S + W.row0(j) * ld, T, (uint32_t)nr * ld * 8u);
+            bulk_commit();
+            if (j + kEStages < W.mine) {
+                bulk_wait_read();  // the store has read the stage
+                W.issue(j + kEStages, s, bar, T, S, nullptr);
+            }
+        }
+    }
+    if (row == 0) bulk_wait_all();
 }
+
+// Rayleigh-Ritz update of whole rows from the basis B = [X | Z] (q = B.n) with C (q x m):
+//   P' = S_Z C_Z,   X' = P' + S_X C_X,   AX' = AS_B C     into Sn (X, P slots) and ASn (X slot).
+// One thread per row; S and AS tiles are staged together (kRRStages deep); the two output
+// tiles are single-buffered in shared memory and bulk-stored (the W slot of Sn and the W, P
+// slots of ASn carry don't-care values, rewritten before they are read).
+constexpr int kRRStages = 2;
+template <int TR>
+__global__ void __launch_bounds__(TR) rr_apply_kernel(const double* S, const double* AS, double* Sn, double* ASn,
+                                                      int ld, Cols B, int m, long long n, const Mat C) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+    int* s_b = reinterpret_cast<int*>(smem + 64);
+    double* outS = reinterpret_cast<double*>(smem + 512);
+    const size_t te = (size_t)TR * ld;
+    double* outA = outS + te;
+    double* ring = outA + te;
+    const int q = B.n;
+    stage_cols(B, s_b);
+    const TileWalk<TR> W(n, ld);
+    const int row = threadIdx.x;
+    if (row == 0) {
+        for (int s = 0; s < kRRStages; ++s) mbar_init(&bar[s], 1);
+        fence_mbar_init();
+        for (long long j = 0; j < min((long long)kRRStages, W.mine); ++j)
+            W.issue(j, (int)j, bar, ring + j * 2 * te, S, AS);
+    }
+    __syncthreads();
+    for (long long j = 0; j < W.mine; ++j) {
+        const int s = (int)(j % kRRStages);
+        mbar_wait(&bar[s], (uint32_t)((j / kRRStages) & 1));
+        const double* Ts = ring + s * 2 * te;
+        const double* Ta = Ts + te;
+        const int nr = W.rows(j);
+        double xs[kMaxK], xa[kMaxK];
+#pragma unroll
+        for (int k = 0; k < kMaxK; ++k) { xs[k] = 0.0; xa[k] = 0.0; }
+        if (row < nr) {
+            const double* ts = Ts + row * ld;
+            const double* ta = Ta + row * ld;
+            for (int l = m; l < q; ++l) {  // Z part first: P'
+                const double u = ts[s_b[l]], v = ta[s_b[l]];
+#pragma unroll
+                for (int k = 0; k < kMaxK; ++k)
+                    if (k < m) {
+                        xs[k] = fma(u, C.v[l * m + k], xs[k]);
+                        xa[k] = fma(v, C.v[l * m + k], xa[k]);
+                    }
+            }
+        }
+        if (row == 0) bulk_wait_read();  // the previous tile's stores have read the out tiles
+        __syncthreads();
+        if (row < nr) {
+            const double* ts = Ts + row * ld;
+            const double* ta = Ta + row * ld;
+#pragma unroll
+            for (int k = 0; k < kMaxK; ++k)
+                if (k < m) outS[row * ld + 2 * m + k] = xs[k];
+            for (int l = 0; l < m; ++l) {
+                const double u = ts[s_b[l]], v = ta[s_b[l]];
+#pragma unroll
+                for (int k = 0; k < kMaxK; ++k)
+                    if (k < m) {
+                        xs[k] = fma(u, C.v[l * m + k], xs[k]);
+                        xa[k] = fma(v, C.v[l * m + k], xa[k]);
+                    }
+            }
+#pragma unroll
+            for (int k = 0; k < kMaxK; ++k)
+                if (k < m) { outS[row * ld + k] = xs[k]; outA[row * ld + k] = xa[k]; }
+        }
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (row == 0) {
+            const uint32_t bytes = (uint32_t)nr * ld * 8u;
+            bulk_store(Sn + W.row0(j) * ld, outS, bytes);
+            bulk_store(ASn + W.row0(j) * ld, outA, bytes);
+            bulk_commit();
+            if (j + kRRStages < W.mine) W.issue(j + kRRStages, s, bar, ring + s * 2 * te, S, AS);
+        }
+    }
+    if (row == 0) bulk_wait_all();
+}
+
+// The ring doubles as the row-group reduction buffer after the tile loop.
+int gram_stages(int, bool) { return kEStages; }  // deeper rings measured slower (profiles/)
+size_t gram_smem(int ld, bool two, int a, int b) {
+    const int tiles = ((a + kTileR - 1) / kTileR) * ((b + kTileR - 1) / kTileR);
+    const int ngroups = std::min(kTR, std::max(1, kT / std::max(1, tiles)));
+    const size_t ring = (size_t)gram_stages(ld, two) * kTR * ld * 8 * (two ? 2 : 1);
+    return 512 + kMaxQ * kMaxQ * 8 + std::max(ring, (size_t)ngroups * a * b * 8);
+}
+size_t apply_smem(int ld) { return 512 + (size_t)kEStages * kTRa * ld * 8; }
+// 128-row tiles up to ld = 24 (k <= 8), 64-row tiles above (shared-memory limit)
+int rr_rows(int ld) { return ld <= 24 ? 128 : 64; }
+size_t rr_apply_smem(int ld) { return 512 + (size_t)(2 + 2 * kRRStages) * rr_rows(ld) * ld * 8; }
 
 // O[i, oc_j] = (add ? O[i, oc_j] : 0) + sum_l U[i, uc_l] M[l, j]  (c = oc.n <= kMaxK).
 // The coefficient matrix lives in the kernel's constant bank (uniform broadcast reads);
@@ -365,6 +611,36 @@ __global__ void sym_tol_kernel(const int32_t* rp, const int32_t* ci, const doubl
     if (md > 0.0) atomicMax(maxdiff_bits, (unsigned long long)__double_as_longlong(md));
 }
 
+// Y[:, out] = A X[:, in] in groups of <= 16 columns (templated register blocks).
+void launch_spmm(const DevCsr* A, const double* X, int ldx, const Cols& in, double* Y, int ldy, const Cols& out,
+                 cudaStream_t st) {
+    const long long n = A->nrows;
+    const unsigned g = (unsigned)((n + kT - 1) / kT);
+    for (int b = 0; b < in.n; b += 16) {
+        Cols ci, co;
+        ci.n = co.n = std::min(16, in.n - b);
+        bool contig = ci.n % 2 == 0 && in.c[b] % 2 == 0 && out.c[b] % 2 == 0 && ldx % 2 == 0 && ldy % 2 == 0;
+        for (int j = 0; j < ci.n; ++j) {
+            ci.c[j] = in.c[b + j];
+            co.c[j] = out.c[b + j];
+            if (j && (ci.c[j] != ci.c[j - 1] + 1 || co.c[j] != co.c[j - 1] + 1)) contig = false;
+        }
+        switch (ci.n * 2 + (contig ? 1 : 0)) {
+#define SPARSLA_SPMM(W) \
+    case 2 * W: spmm_kernel<W, false><<<g, kT, 0, st>>>(A->rp, A->ci, A->val, n, X, ldx, ci, Y, ldy, co); break;
+#define SPARSLA_SPMM2(W) \
+    SPARSLA_SPMM(W) case 2 * W + 1: spmm_kernel<W, true><<<g, kT, 0, st>>>(A->rp, A->ci, A->val, n, X, ldx, ci, Y, ldy, co); break;
+            SPARSLA_SPMM(1) SPARSLA_SPMM2(2) SPARSLA_SPMM(3) SPARSLA_SPMM2(4) SPARSLA_SPMM(5) SPARSLA_SPMM2(6)
+            SPARSLA_SPMM(7) SPARSLA_SPMM2(8) SPARSLA_SPMM(9) SPARSLA_SPMM2(10) SPARSLA_SPMM(11) SPARSLA_SPMM2(12)
+            SPARSLA_SPMM(13) SPARSLA_SPMM2(14) SPARSLA_SPMM(15) SPARSLA_SPMM2(16)
+#undef SPARSLA_SPMM2
+#undef SPARSLA_SPMM
+            default: fail(SPARSLA_ERR_INTERNAL, "spmm: bad column count");
+        }
+        CK(cudaGetLastError());
+    }
+}
+
 // ------------------------------------------------------------ host dense algebra ----
 // Cyclic Jacobi eigendecomposition of a symmetric q x q matrix (row-major).  Returns
 // eigenvalues ascending in w and the matching orthonormal eigenvectors as the COLUMNS of
@@ -441,54 +717,83 @@ struct Lobpcg {
     double *S = nullptr, *AS = nullptr, *Sn = nullptr, *ASn = nullptr;
     double* partial = nullptr;  // [kRedCTAs][kMaxQ*kMaxQ]
     double* gout = nullptr;     // [kMaxQ*kMaxQ]
+    unsigned* ticket = nullptr;
     double* h_pin = nullptr;    // pinned [kMaxQ*kMaxQ]
     long long* ipart = nullptr;
     long long spmm_count = 0;
 
-    Lobpcg(DevCsr* A_, int m_) : A(A_), s(A_->stream), n(A_->nrows), m(m_), ld(3 * m_) {
-        const size_t bytes = (size_t)n * ld;
-        S = dalloc<double>(bytes); AS = dalloc<double>(bytes);
-        Sn = dalloc<double>(bytes); ASn = dalloc<double>(bytes);
-        CK(cudaMemsetAsync(S, 0, bytes * 8, s)); CK(cudaMemsetAsync(AS, 0, bytes * 8, s));
-        CK(cudaMemsetAsync(Sn, 0, bytes * 8, s)); CK(cudaMemsetAsync(ASn, 0, bytes * 8, s));
+    Lobpcg(DevCsr* A_, int m_) : A(A_), s(A_->stream), n(A_->nrows), m(m_), ld((3 * m_ + 1) & ~1) {
+        const size_t el = (size_t)n * ld + 2;
+        S = dalloc<double>(el); AS = dalloc<double>(el);
+        Sn = dalloc<double>(el); ASn = dalloc<double>(el);
+        CK(cudaMemsetAsync(S, 0, el * 8, s)); CK(cudaMemsetAsync(AS, 0, el * 8, s));
+        CK(cudaMemsetAsync(Sn, 0, el * 8, s)); CK(cudaMemsetAsync(ASn, 0, el * 8, s));
         partial = dalloc<double>((size_t)kRedCTAs * kMaxQ * kMaxQ);
         gout = dalloc<double>((size_t)kMaxQ * kMaxQ);
+        ticket = dalloc<unsigned>(1);
+        CK(cudaMemsetAsync(ticket, 0, sizeof(unsigned), s));
         ipart = dalloc<long long>((size_t)kRedCTAs * kMaxK);
         CK(cudaMallocHost(&h_pin, sizeof(double) * kMaxQ * kMaxQ));
+        // dynamic shared memory up to the opt-in limit minus each kernel's static part
+        auto allow = [&](const void* f, const char* what) {
+            int optin = 0;
+            cuda_check(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, A->device), what);
+            cudaFuncAttributes fa{};
+            cuda_check(cudaFuncGetAttributes(&fa, f), what);
+            cuda_check(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            optin - (int)fa.sharedSizeBytes), what);
+        };
+        allow((const void*)gram_kernel, "gram smem");
+#define SPARSLA_ALLOW(C) allow((const void*)apply_kernel<C>, "apply smem");
+        SPARSLA_FOR_1_32(SPARSLA_ALLOW)
+#undef SPARSLA_ALLOW
+        allow((const void*)rr_apply_kernel<128>, "rr smem");
+        allow((const void*)rr_apply_kernel<64>, "rr smem");
     }
     ~Lobpcg() {
         DeviceGuard g(A->device, true);
         cudaFree(S); cudaFree(AS); cudaFree(Sn); cudaFree(ASn);
-        cudaFree(partial); cudaFree(gout); cudaFree(ipart);
+        cudaFree(partial); cudaFree(gout); cudaFree(ticket); cudaFree(ipart);
         if (h_pin) cudaFreeHost(h_pin);
     }
     unsigned grid() const { return (unsigned)((n + kT - 1) / kT); }
+    unsigned tile_grid() const {  // persistent over row tiles, 4 CTAs per SM
+        const long long nt = (n + kTRa - 1) / kTRa;
+        return (unsigned)std::max<long long>(1, std::min<long long>(nt, 4LL * 148));
+    }
 
-    // G = U_uc^T V_vc (host, row-major a x b)
+    // G = U_uc^T V_vc (host, row-major a x b); U, V are S / AS buffers (row stride ld)
     std::vector<double> gram(const double* U, const Cols& uc, const double* V, const Cols& vc) {
         const int ab = uc.n * vc.n;
         std::vector<double> G(ab, 0.0);
-        if (ab == 0) return G;
-        gram_kernel<<<kRedCTAs, kT, 0, s>>>(U, ld, uc, V, ld, vc, n, partial);
-        partial_sum_kernel<<<(ab + 127) / 128, 128, 0, s>>>(partial, kRedCTAs, ab, gout);
+        if (ab == 0 || n == 0) return G;
+        gram_kernel<<<kRedCTAs, kT, gram_smem(ld, U != V, uc.n, vc.n), s>>>(U, V, ld, uc, vc, n, partial, ticket, gout,
+                                                                      gram_stages(ld, U != V));
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(h_pin, gout, ab * sizeof(double), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         std::memcpy(G.data(), h_pin, ab * sizeof(double));
         return G;
     }
-    void combine(double* O, const Cols& oc, bool add, const double* U, const Cols& uc, const std::vector<double>& M) {
-        if (oc.n == 0 || n == 0) return;
+    // in place: S[:, out] = S[:, in] M
+    void apply(const Cols& in, const Cols& out, const std::vector<double>& M) {
+        if (out.n == 0 || n == 0) return;
         Mat Mt;
         std::memset(&Mt, 0, sizeof(Mt));
         std::copy(M.begin(), M.end(), Mt.v);
-        combine_kernel<<<grid(), kT, 0, s>>>(O, ld, oc, add ? 1 : 0, U, ld, uc, n, Mt);
+        const unsigned g = tile_grid();
+        const size_t sm = apply_smem(ld);
+        switch (out.n) {
+#define SPARSLA_APPLY(C) case C: apply_kernel<C><<<g, kTRa, sm, s>>>(S, ld, in, out, n, Mt); break;
+            SPARSLA_FOR_1_32(SPARSLA_APPLY)
+#undef SPARSLA_APPLY
+            default: fail(SPARSLA_ERR_INTERNAL, "apply: more than 32 output columns");
+        }
         CK(cudaGetLastError());
     }
     void spmm(const double* X, const Cols& in, double* Y) {
         if (in.n == 0 || n == 0) return;
-        spmm_kernel<<<grid(), kT, 0, s>>>(A->rp, A->ci, A->val, n, X, ld, in, Y, ld, in);
-        CK(cudaGetLastError());
+        launch_spmm(A, X, ld, in, Y, ld, in, s);
         ++spmm_count;
     }
     std::vector<double> resid(const std::vector<double>& lam, const double* dinv) {
@@ -506,62 +811,70 @@ struct Lobpcg {
         return r;
     }
 
-    // Z -= B (B^T Z): classical Gram-Schmidt of block Z against the orthonormal block B
-    void orth_against(const Cols& B, const Cols& Z) {
-        if (B.n == 0 || Z.n == 0) return;
-        std::vector<double> Y = gram(S, B, S, Z);  // B.n x Z.n
-        for (auto& v : Y) v = -v;
-        combine(S, Z, true, S, B, Y);
-    }
-    // SVQB (Stathopoulos & Wu): Z <- Z D U diag(sigma)^-1/2 on the columns whose normalised
-    // Gram eigenvalue survives the drop rule (norm after orthogonalisation
-    // below 1e-12 relative -> dropped).  Returns the surviving columns (a prefix of Z).
-    Cols svqb(const Cols& Z) {
-        const int w = Z.n;
-        if (w == 0) return Z;
-        std::vector<double> G = gram(S, Z, S, Z);
-        double dmax = 0.0;
-        for (int i = 0; i < w; ++i) dmax = std::max(dmax, G[(size_t)i * w + i]);
-        std::vector<double> D(w, 0.0);
-        for (int i = 0; i < w; ++i) {
-            const double d = G[(size_t)i * w + i];
-            if (d > 1e-300 && d > 1e-28 * dmax && std::isfinite(d)) D[i] = 1.0 / std::sqrt(d);
-        }
-        std::vector<double> H((size_t)w * w);
-        for (int i = 0; i < w; ++i)
-            for (int j = 0; j < w; ++j) H[(size_t)i * w + j] = D[i] * G[(size_t)i * w + j] * D[j];
-        for (int i = 0; i < w; ++i)
-            for (int j = i + 1; j < w; ++j) {
-                const double h = 0.5 * (H[(size_t)i * w + j] + H[(size_t)j * w + i]);
-                H[(size_t)i * w + j] = H[(size_t)j * w + i] = h;
-            }
-        std::vector<double> sig, U;
-        sym_eig(w, H, sig, U);
-        const double smax = std::max(sig.empty() ? 0.0 : sig.back(), 0.0);
-        std::vector<int> keep;
-        for (int j = w - 1; j >= 0; --j)  // largest first: best-conditioned directions
-            if (sig[j] > 1e-24 * smax && sig[j] > 0.0) keep.push_back(j);
-        const int w2 = (int)keep.size();
-        std::vector<double> T((size_t)w * w2, 0.0);
-        for (int i = 0; i < w; ++i)
-            for (int c = 0; c < w2; ++c)
-                T[(size_t)i * w2 + c] = D[i] * U[(size_t)i * w + keep[c]] / std::sqrt(sig[keep[c]]);
-        Cols out = Z;
-        out.n = w2;
-        combine(S, out, false, S, Z, T);
-        return out;
-    }
-    Cols orthonormalize(const Cols& B, const Cols& Z) {
+    // Orthonormalise the columns Z of S against the orthonormal columns B and among
+    // themselves.  One pass = ONE Gram launch ([B Z]^T Z) + ONE in-place apply launch:
+    // the block Gram-Schmidt step Z - B Y (Y = B^T Z) and the SVQB step (Stathopoulos & Wu)
+    // are composed in the small space, Gram(Z - B Y) = Z^T Z - Y^T Y, T = D U sigma^-1/2, and
+    // applied at once as Z' = [B Z] [[-Y T]; [T]].  Two passes (CGS2 + SVQB2): the second
+    // pass sees an almost orthonormal block, so its Gram has no cancellation.  Directions
+    // whose norm after orthogonalisation falls below the drop rule are removed;
+    // the survivors are a prefix of Z's column slots.
+    Cols ortho(const Cols& B, const Cols& Z) {
         Cols z = Z;
-        for (int pass = 0; pass < 2; ++pass) {
-            orth_against(B, z);
-            z = svqb(z);
+        for (int pass = 0; pass < 2 && z.n > 0; ++pass) {
+            const int b = B.n, w = z.n;
+            const Cols BZ = cols_cat(B, z);
+            const std::vector<double> G = gram(S, BZ, S, z);  // (b + w) x w
+            std::vector<double> H((size_t)w * w);
+            for (int i = 0; i < w; ++i)
+                for (int j = 0; j < w; ++j) {
+                    double h = G[(size_t)(b + i) * w + j];
+                    for (int l = 0; l < b; ++l) h -= G[(size_t)l * w + i] * G[(size_t)l * w + j];
+                    H[(size_t)i * w + j] = h;
+                }
+            // pass 0 subtracts B's component in the small space (cancellation ~ eps / rho^2
+            // for a relative remaining norm rho): drop rho < 1e-7 there; pass 1 applies the
+            // SPEC rule (norm after orthogonalisation < 1e-12 relative)
+            const double rel = pass == 0 ? 1e-14 : 1e-24;
+            std::vector<double> D(w, 0.0);
+            for (int i = 0; i < w; ++i) {
+                const double h0 = G[(size_t)(b + i) * w + i], h = H[(size_t)i * w + i];
+                if (std::isfinite(h) && h > 1e-300 && h > rel * h0) D[i] = 1.0 / std::sqrt(h);
+            }
+            std::vector<double> K((size_t)w * w);
+            for (int i = 0; i < w; ++i)
+                for (int j = 0; j < w; ++j)
+                    K[(size_t)i * w + j] = D[i] * 0.5 * (H[(size_t)i * w + j] + H[(size_t)j * w + i]) * D[j];
+            std::vector<double> sig, U;
+            sym_eig(w, K, sig, U);
+            const double smax = std::max(sig.empty() ? 0.0 : sig.back(), 0.0);
+            std::vector<int> keep;
+            for (int j = w - 1; j >= 0; --j)
+                if (sig[j] > rel * smax && sig[j] > 0.0) keep.push_back(j);
+            const int w2 = (int)keep.size();
+            std::vector<double> T((size_t)w * w2);
+            for (int i = 0; i < w; ++i)
+                for (int c = 0; c < w2; ++c) T[(size_t)i * w2 + c] = D[i] * U[(size_t)i * w + keep[c]] / std::sqrt(sig[keep[c]]);
+            std::vector<double> M((size_t)(b + w) * w2, 0.0);
+            for (int l = 0; l < b; ++l)  // -Y T
+                for (int c = 0; c < w2; ++c) {
+                    double v = 0.0;
+                    for (int i = 0; i < w; ++i) v += G[(size_t)l * w + i] * T[(size_t)i * w2 + c];
+                    M[(size_t)l * w2 + c] = -v;
+                }
+            for (int i = 0; i < w; ++i)
+                for (int c = 0; c < w2; ++c) M[(size_t)(b + i) * w2 + c] = T[(size_t)i * w2 + c];
+            Cols out = z;
+            out.n = w2;
+            apply(BZ, out, M);
+            z = out;
         }
         return z;
     }
 
-    // Rayleigh-Ritz on the orthonormal basis S_B (AS_B = A S_B): X, AX, P into Sn / ASn.
-    void rayleigh_ritz(const Cols& B, const Cols& WP, std::vector<double>& lam) {
+    // Rayleigh-Ritz on the orthonormal basis S_B, B = [X | Z] (AS_B = A S_B): one Gram launch
+    // and one fused update launch writing X', AX', P' into Sn / ASn, then swap.
+    void rayleigh_ritz(const Cols& B, std::vector<double>& lam) {
         const int q = B.n;
         std::vector<double> G = gram(S, B, AS, B);
         for (int i = 0; i < q; ++i)
@@ -571,15 +884,16 @@ struct Lobpcg {
             }
         std::vector<double> th, U;
         sym_eig(q, G, th, U);
-        std::vector<double> C((size_t)q * m);
+        Mat C;
+        std::memset(&C, 0, sizeof(C));
         for (int i = 0; i < q; ++i)
-            for (int j = 0; j < m; ++j) C[(size_t)i * m + j] = U[(size_t)i * q + j];
-        const Cols Xc = cols_range(0, m);
-        combine(Sn, Xc, false, S, B, C);
-        combine(ASn, Xc, false, AS, B, C);
-        if (WP.n > 0) {  // P' = S_{W,P} C_{W,P}: rows m.. of C
-            std::vector<double> Cp(C.begin() + (size_t)m * m, C.end());
-            combine(Sn, cols_range(2 * m, 3 * m), false, S, WP, Cp);
+            for (int j = 0; j < m; ++j) C.v[i * m + j] = U[(size_t)i * q + j];
+        if (n > 0) {
+            if (rr_rows(ld) == 128)
+                rr_apply_kernel<128><<<tile_grid(), 128, rr_apply_smem(ld), s>>>(S, AS, Sn, ASn, ld, B, m, n, C);
+            else
+                rr_apply_kernel<64><<<tile_grid(), 64, rr_apply_smem(ld), s>>>(S, AS, Sn, ASn, ld, B, m, n, C);
+            CK(cudaGetLastError());
         }
         std::swap(S, Sn);
         std::swap(AS, ASn);
@@ -665,7 +979,7 @@ void eig_smallest(DevCsr* A, int k, double tol, long long max_iter, uint64_t see
         eye_kernel<<<(nn + 127) / 128, 128, 0, A->stream>>>(E, nn, nn);
         for (int b = 0; b < nn; b += kMaxQ) {
             const Cols c = cols_range(b, std::min(nn, b + kMaxQ));
-            spmm_kernel<<<(nn + kT - 1) / kT, kT, 0, A->stream>>>(A->rp, A->ci, A->val, nn, E, nn, c, AE, nn, c);
+            launch_spmm(A, E, nn, c, AE, nn, c, A->stream);
         }
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(Ad.data(), AE, Ad.size() * 8, cudaMemcpyDeviceToHost, A->stream));
@@ -689,33 +1003,28 @@ void eig_smallest(DevCsr* A, int k, double tol, long long max_iter, uint64_t see
     const Cols Xc = cols_range(0, m);
     eig_init_kernel<<<L.grid(), kT, 0, L.s>>>(L.S, n, L.ld, m, seed);
     CK(cudaGetLastError());
-    Cols x0 = L.orthonormalize(Cols{}, Xc);
-    if (x0.n < m) fail(SPARSLA_ERR_INTERNAL, "eig_smallest: initial block is rank deficient");
+    if (L.ortho(Cols{}, Xc).n < m) fail(SPARSLA_ERR_INTERNAL, "eig_smallest: initial block is rank deficient");
     L.spmm(L.S, Xc, L.AS);
     std::vector<double> lam;
-    L.rayleigh_ritz(Xc, Cols{}, lam);
+    L.rayleigh_ritz(Xc, lam);
     bool have_p = false;
     long long it = 0;
     std::vector<double> res;
     for (;; ++it) {
-        res = L.resid(lam, dinv);
-        Cols act;
-        for (int j = 0; j < m; ++j)
-            if (!(res[j] <= tol)) act.c[act.n++] = (unsigned char)j;
-        if (act.n == 0 || it >= max_iter) break;
-        Cols Wc, Pc;
-        for (int t = 0; t < act.n; ++t) {
-            Wc.c[Wc.n++] = (unsigned char)(m + act.c[t]);
-            if (have_p) Pc.c[Pc.n++] = (unsigned char)(2 * m + act.c[t]);
+        res = L.resid(lam, dinv);  // also W = |D|^-1 R into the W slot
+        Cols Z;
+        for (int j = 0; j < m; ++j)  // soft locking: only unconverged pairs add directions
+            if (!(res[j] <= tol)) Z.c[Z.n++] = (unsigned char)(m + j);
+        if (Z.n == 0 || it >= max_iter) break;
+        if (have_p) {
+            const int nw = Z.n;
+            for (int t = 0; t < nw; ++t) Z.c[Z.n++] = (unsigned char)(m + Z.c[t]);  // P slot = W slot + m
         }
-        Wc = L.orthonormalize(Xc, Wc);
-        const Cols XW = cols_cat(Xc, Wc);
-        Pc = L.orthonormalize(XW, Pc);
-        const Cols WP = cols_cat(Wc, Pc);
-        L.spmm(L.S, WP, L.AS);
-        L.rayleigh_ritz(cols_cat(Xc, WP), WP, lam);
-        have_p = WP.n > 0;
-        if (WP.n == 0) break;  // no new directions: the block cannot improve
+        Z = L.ortho(Xc, Z);
+        L.spmm(L.S, Z, L.AS);
+        L.rayleigh_ritz(cols_cat(Xc, Z), lam);
+        have_p = Z.n > 0;
+        if (Z.n == 0) break;  // no new directions: the block cannot improve
     }
     o.iters = it;
     o.lam = lam;

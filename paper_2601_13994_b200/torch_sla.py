@@ -3,6 +3,7 @@
     A = SparseTensor(values, row, col, (n, n))      # values: torch tensor (requires_grad ok)
     x = A.solve(b, atol=..., rtol=...)              # differentiable w.r.t. values and b
     loss(x).backward()                              # one adjoint solve (Alg. 1, Eq. 3)
+    lam, V = A.eigsh(k=6)                           # LOBPCG; d(lam)/d(values) by Eq. 4
 
 Forward and backward run on the sm_100a Krylov loop through the C ABI with zero-copy device
 pointers (SPARSLA_MEM_DEVICE).  Backward is exactly one transposed solve plus the per-entry
@@ -72,6 +73,12 @@ class SparseTensor:
             backend = "cg" if S.is_structurally_symmetric(self.csr.to_coo()) else "bicgstab"
         opts = S.SolveOptions(atol=atol, rtol=rtol, max_iter=max_iter, preconditioner=preconditioner)
         return _Solve.apply(self.canonical_values(), b, self, opts, backend)
+
+    def eigsh(self, k: int = 6, tol: float = 1e-8, max_iter: int = 10000, seed: int = 2601):
+        """k smallest eigenpairs.  Returns (lambdas,
+        vectors n x k); lambdas are differentiable w.r.t. the values (Eq. 4, no solves),
+        the eigenvectors are not (eigenvector gradients are a non-goal)."""
+        return _Eigsh.apply(self.canonical_values(), self, int(k), float(tol), int(max_iter), int(seed))
 
 
 class _DupSum(torch.autograd.Function):
@@ -145,3 +152,41 @@ class _Solve(torch.autograd.Function):
         if not r.converged:
             raise S.Error(f"adjoint solve did not converge: {r.diagnostic}")
         return gv, gb, None, None, None
+
+
+class _Eigsh(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, vals, A: SparseTensor, k: int, tol: float, max_iter: int, seed: int):
+        dev = A.device
+        vals = vals.detach().to(f"cuda:{dev}", torch.float64).contiguous()
+        n = A.shape[0]
+        D = A.csr.device(dev)
+        torch.cuda.current_stream(dev).synchronize()
+        S._check(S.lib().sparsla_dcsr_set_values(D.h, _ptr(vals), C.c_int32(S.MEM_DEVICE)))
+        lam = np.empty(k)
+        res = np.empty(k)
+        conv = np.empty(k, dtype=np.int32)
+        V = torch.empty((n, k), dtype=torch.float64, device=vals.device)
+        o = S._EigOpts(tol, max_iter, seed & ((1 << 64) - 1), S.PRECOND_JACOBI, 0)
+        rep = S._EigReport()
+        S._check(S.lib().sparsla_eig_smallest(D.h, C.c_int64(k), C.byref(o), S._p(lam, S._f64p), _ptr(V),
+                                              S._p(res, S._f64p), S._p(conv, S._i32p), C.byref(rep),
+                                              C.c_int32(S.MEM_DEVICE)))
+        if not rep.converged:
+            raise S.Error("eigsh did not converge: " + rep.diagnostic.decode(errors="replace"))
+        ctx.A, ctx.lam = A, lam
+        ctx.save_for_backward(vals, V)
+        ctx.mark_non_differentiable(V)
+        return torch.as_tensor(lam, device=vals.device), V
+
+    @staticmethod
+    def backward(ctx, glam, _gV):
+        vals, V = ctx.saved_tensors
+        A = ctx.A
+        D = A.csr.device(A.device)
+        g = np.ascontiguousarray(glam.detach().cpu().numpy(), np.float64)
+        gv = torch.empty(A.nnz, dtype=torch.float64, device=vals.device)
+        torch.cuda.current_stream(A.device).synchronize()
+        S._check(S.lib().sparsla_eig_backward(D.h, C.c_int64(len(g)), S._p(ctx.lam, S._f64p), _ptr(V),
+                                              S._p(g, S._f64p), _ptr(gv), C.c_int32(S.MEM_DEVICE)))
+        return gv, None, None, None, None, None

@@ -7,6 +7,7 @@
 
 #include "sparsla/adjoint.hpp"
 #include "sparsla/distributed.hpp"
+#include "sparsla/eigen.hpp"
 #include "sparsla/solve.hpp"
 #include "sparsla/sparse.hpp"
 
@@ -81,6 +82,15 @@ int main(int argc, char** argv) {
     auto [x3, ctx] = solve_forward(I2, b3);
     auto grads = solve_backward(ctx, g3);
     CHECK(grads.grad_b[0] == 0.5 && grads.grad_vals[2] == -1.5);
+    // eigen-solver: [[2,1],[1,2]], k = 1 -> lambda = 1, dlambda/dA = v v^T
+    SparseCoo E({0, 0, 1, 1}, {0, 1, 0, 1}, {2.0, 1.0, 1.0, 2.0}, Shape{2, 2});
+    auto ev = eig_smallest(E, 1, 1e-10);
+    CHECK(std::fabs(ev.lambdas[0] - 1.0) < 1e-14 && ev.vectors[0] > 0 && ev.report.converged);
+    std::vector<double> gl = {1.0};
+    auto ge = eig_backward(ev, E, gl);
+    CHECK(std::fabs(ge[0] - 0.5) < 1e-14 && std::fabs(ge[1] + 0.5) < 1e-14);
+    auto ep = eig_smallest(P, 6, 1e-9);  // 2-D Poisson 16x16 through LOBPCG
+    CHECK(ep.report.converged && std::fabs(ep.lambdas[0] - 2.0 * (2.0 - 2.0 * std::cos(M_PI / 17))) < 1e-8);
     std::printf("dropin gpu ok\n");
     return 0;
 }

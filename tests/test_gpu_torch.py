@@ -71,3 +71,27 @@ def test_autograd_nonsymmetric_bicgstab(S, O, gpu):
     gbo, gvo, _ = O.adjoint_backward(A, xo, np.ones(A.nrows), backend=1, atol=1e-12)
     assert np.array_equal(bits(b.grad.cpu().numpy()), bits(gbo))
     assert np.array_equal(bits(vals.grad.cpu().numpy()), bits(gvo))
+
+
+def test_eigsh_autograd_eq4(S, O, gpu):
+    """SparseTensor.eigsh: LOBPCG forward, Eq. 4 backward (no solves) equals the oracle's
+    gather sum_m g_m v_m[i] v_m[j] on the returned vectors; FD on a few stored entries."""
+    import torch
+    from paper_2601_13994_b200.torch_sla import SparseTensor
+    P = O.generate("poisson2d", 20)
+    rows = np.repeat(np.arange(P.nrows), np.diff(P.row_ptr))
+    v0 = P.vals.copy()
+    v0[rows == P.col_idx] += 0.3 * np.arange(P.nrows) / P.nrows  # simple spectrum
+    vals = torch.tensor(v0, dtype=torch.float64, device="cuda:0", requires_grad=True)
+    T = SparseTensor(vals, rows, P.col_idx, (P.nrows, P.ncols))
+    lam, V = T.eigsh(k=4, tol=1e-11)
+    g = torch.tensor([1.0, -0.5, 0.25, 2.0], dtype=torch.float64, device="cuda:0")
+    (lam * g).sum().backward()
+    A = O.Csr(P.nrows, P.ncols, P.row_ptr, P.col_idx, v0)
+    w, _ = O.eig_dense(A, 4)
+    assert np.max(np.abs(lam.detach().cpu().numpy() - w)) <= 1e-8
+    ref = O.eig_backward(A, V.cpu().numpy(), g.cpu().numpy())
+    assert np.max(np.abs(vals.grad.cpu().numpy() - ref)) <= 1e-14
+    ent = [0, 7, 100, len(v0) - 1]
+    fd = O.eig_fd(A, 4, g.cpu().numpy(), entries=ent)
+    assert np.max(np.abs(fd - ref[ent])) / np.max(np.abs(ref[ent])) < 1e-5
