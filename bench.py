@@ -101,13 +101,16 @@ def gen_config(args):
     return n, rp, ci, v, time.time() - t0
 
 
-def iteration_bytes(n, nnz):
-    """Algorithmic bytes of THIS implementation's CG iteration (x += a p moved into update 2
-    so p is streamed once: 12 nnz + 100 n + 4; SURVEY.md's canonical 3-pass accounting is
-    12 nnz + 108 n + 4, reported beside it)."""
-    spmv = 12 * nnz + 4 * (n + 1) + 8 * n + 8 * n  # vals+cols, row_ptr, p (once), q write
-    u1 = 32 * n                                     # read r q d, write r
-    u2 = 48 * n                                     # read x p r d, write x p
+def iteration_bytes(n, nnz, value_dict=False, uniform_diag=False):
+    """Algorithmic bytes of THIS implementation's CG iteration in the storage format the
+    library chose (x += a p moved into update 2 so p is streamed once).  Plain CSR:
+    12 nnz + 100 n + 4; with the value dictionary the matrix stream is 5 nnz (+ a 2 KB
+    table); with a constant Jacobi diagonal the two vector passes skip d (-16 n).
+    SURVEY.md's canonical 3-pass CSR accounting, 12 nnz + 108 n + 4, is reported beside it."""
+    mat = (5 * nnz + 2048) if value_dict else 12 * nnz
+    spmv = mat + 4 * (n + 1) + 8 * n + 8 * n        # matrix, row_ptr, p (once), q write
+    u1 = (24 if uniform_diag else 32) * n           # read r q (d), write r
+    u2 = (40 if uniform_diag else 48) * n           # read x p r (d), write x p
     return spmv, u1, u2
 
 
@@ -185,6 +188,7 @@ def run_ours(args):
     D = S.DeviceCsr(None, dev, i32=(n, n, rp, ci, v))
     tup = time.time() - t0
     info = D.info()
+    fmt = D.format()
     b_host = torch.ones(n, dtype=torch.float64).pin_memory()
     x_host = torch.empty(n, dtype=torch.float64).pin_memory()
     opts = S.SolveOptions(atol=0.0, rtol=args.rtol, max_iter=args.max_iter)
@@ -253,9 +257,39 @@ def run_ours(args):
     sv.reset()
     sv.iterate(5)
     kms = sv.kernel_times(args.kernel_iters)
-    spmv_b, u1_b, u2_b = iteration_bytes(n, nnz)
+    spmv_b, u1_b, u2_b = iteration_bytes(n, nnz, fmt["value_dict"], fmt["uniform_diag"])
     it_bytes = spmv_b + u1_b + u2_b
     spmv_gbs = spmv_b / (kms[0] * 1e-3) / 1e9
+    sv.close()
+    # plain-CSR reference point of the same loop (value dictionary and scalar diagonal off)
+    plain = None
+    if args.plain_steps > 0:
+        os.environ["SPARSLA_VALUE_DICT"] = "0"
+        os.environ["SPARSLA_UNIFORM_DIAG"] = "0"
+        try:
+            Dp = S.DeviceCsr(None, dev, i32=(n, n, rp, ci, v))
+            svp = S.Solver(Dp, b_host.numpy(), "cg", opts)
+            sp = torch.cuda.ExternalStream(svp.stream())
+            svp.reset()
+            svp.iterate(5)
+            torch.cuda.synchronize()
+            q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            q0.record(sp)
+            svp.iterate(args.plain_steps)
+            q1.record(sp)
+            q1.synchronize()
+            pms = q0.elapsed_time(q1) / args.plain_steps
+            pk = svp.kernel_times(10)
+            ps_b, pu1, pu2 = iteration_bytes(n, nnz)
+            plain = {"value": 1e3 / pms, "unit": "it/s", "steps": args.plain_steps, "ms_per_step": pms,
+                     "kernel_ms": {"spmv_cg": pk[0], "cg_update1": pk[1], "cg_update2": pk[2]},
+                     "spmv_gbs": ps_b / (pk[0] * 1e-3) / 1e9,
+                     "iteration_gbs": (ps_b + pu1 + pu2) / (pms * 1e-3) / 1e9,
+                     "format": "plain CSR (int32 col, fp64 val), streamed Jacobi diagonal"}
+            svp.close()
+            del Dp
+        finally:
+            del os.environ["SPARSLA_VALUE_DICT"], os.environ["SPARSLA_UNIFORM_DIAG"]
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "spmv_traffic.json")) as f:
@@ -272,17 +306,24 @@ def run_ours(args):
         "config": {"workload": f"B: 3-D 7-pt Poisson {args.size}^3 ({n} DOF, nnz {nnz}), Jacobi-PCG "
                                f"rtol {args.rtol}, x0 = 0", "n": n, "nnz": nnz, "partition": "single GPU",
                    "l2": "no flush: matrix + vectors (>12 GB) exceed the 126 MB L2",
-                   "spmv_variant": "tma-bulk-staged" if info["variant"] == 0 else "direct"},
+                   "spmv_variant": "tma-bulk-staged" if info["variant"] == 0 else "direct",
+                   "storage": ("value dictionary (1-byte index into %d distinct fp64 values) + int32 col"
+                               % fmt["distinct_values"]) if fmt["value_dict"] else "CSR int32 col + fp64 val",
+                   "jacobi_diag": "constant (scalar)" if fmt["uniform_diag"] else "streamed"},
         "spmv_gbs": spmv_gbs,
         "iteration_gbs": it_bytes / (ms / args.steps * 1e-3) / 1e9,
         "bytes_per_iteration": it_bytes,
         "canonical_bytes_per_iteration": 12 * nnz + 108 * n + 4,
         "canonical_iteration_gbs": (12 * nnz + 108 * n + 4) / (ms / args.steps * 1e-3) / 1e9,
         "kernel_ms": {"spmv_cg": kms[0], "cg_update1": kms[1], "cg_update2": kms[2]},
-        "roofline": {"bound": "hbm", "kernel": "spmv_kernel<SPMV_CG,staged>", "achieved": spmv_gbs,
+        "csr_equivalent_spmv_gbs": (12 * nnz + 20 * n + 4) / (kms[0] * 1e-3) / 1e9,
+        "plain_csr": plain,
+        "roofline": {"bound": "hbm", "kernel": "spmv_ws_kernel<SPMV_CG,staged%s>" % (",value-dict" if fmt["value_dict"] else ""), "achieved": spmv_gbs,
                      "peak": peak, "unit": "GB/s", "frac": spmv_gbs / peak, "traffic": traffic,
                      "peak_source": peak_src, "frac_of_spec_8tbs": spmv_gbs / SPEC_PEAK_GBS,
                      "algorithmic_bytes_per_launch": spmv_b,
+                     "bytes_basis": "bytes of the stored format (value dictionary: 5 B/entry)" if fmt["value_dict"]
+                                    else "CSR 12 B/entry",
                      "iteration_frac": (it_bytes / (ms / args.steps * 1e-3) / 1e9) / peak},
         "time_to_tolerance_s": e2e_t / len(reps), "iterations_to_tolerance": k_tol,
         "e2e": {"value": e2e_its / e2e_t, "unit": "it/s", "h2d_bytes_per_step": 8 * n,
@@ -313,6 +354,7 @@ def main():
     ap.add_argument("--max-iter", type=int, default=100000)
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--kernel-iters", type=int, default=20)
+    ap.add_argument("--plain-steps", type=int, default=100, help="plain-CSR comparison run (0: skip)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dist", action="store_true", help="force the NCCL distributed path (also at N=1)")
     args = ap.parse_args()

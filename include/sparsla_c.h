@@ -168,6 +168,11 @@ int sparsla_dcsr_destroy(sparsla_dcsr* A);
  * block [5]=max row length [6]=kernel variant used by spmv (0 staged, 1 long-row)
  * [7]=staged-SpMV variant index (8 entries) */
 int sparsla_dcsr_info(const sparsla_dcsr* A, int64_t* info);
+/* Storage format chosen for the SpMV stream: fmt[0]=1 when the value dictionary is in use
+ * (<= 256 distinct values: 1-byte index per entry instead of the 8-byte value), fmt[1]=number
+ * of distinct values in it (0 otherwise), fmt[2]=1 when the Jacobi inverse diagonal is
+ * constant (the CG/BiCGStab vector kernels then take it as a scalar). */
+int sparsla_dcsr_format(sparsla_dcsr* A, int64_t* fmt);
 
 /* y = A x (sparse.cpp:135-154): rows accumulated left to right from 0.0, separate
  * multiply and add — bitwise equal to the reference.  mem: see above. */

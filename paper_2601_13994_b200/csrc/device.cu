@@ -10,6 +10,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <thread>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -77,6 +79,32 @@ struct WsVariant {
 // rpt == 0 marks the warp-pipelined kernel (stg = per-warp ring depth)
 // Measured on B200 (tools/spmv_sweep.py, profiles/r01_spmv_sweep.md): variant 0 is the
 // fastest on both the 7-point stencil (6.2 TB/s) and the P1 FEM matrix (5.4 TB/s).
+// Value-dictionary kernels (for matrices that use staged variant 0: rows of <= 8 entries),
+// indexed [hub][mode].  The matrix stream is 5 instead of 12 bytes per entry, so more rows
+// must be in flight per SM to keep HBM busy: the variants trade ring depth and CTAs per
+// SM (2 rows per thread spilled and ran 2x slower).  SPARSLA_VD_VARIANT selects one (sweeps).
+struct VdVariant {
+    int rpt, stg, minb;
+    const void* fn[4];  // per SpmvMode
+};
+#define VDV(R, S, M)                                                                                 \
+    {R, S, M, {(const void*)spmv_ws_kernel<SPMV_PLAIN, R, S, M, true, 8, false, true>,                \
+               (const void*)spmv_ws_kernel<SPMV_CG, R, S, M, true, 8, false, true>,                   \
+               (const void*)spmv_ws_kernel<SPMV_BICG_V, R, S, M, true, 8, false, true>,               \
+               (const void*)spmv_ws_kernel<SPMV_BICG_T, R, S, M, true, 8, false, true>}}
+// Measured on config B (tools/vd_sweep.py, profiles/r01_value_dict.md): 3 CTAs/SM at 72
+// registers (no spills) is the best point; 4 CTAs/SM (56 registers) spills.
+static const VdVariant kVdVariants[] = {VDV(1, 3, 3), VDV(1, 4, 3), VDV(1, 3, 4)};
+#undef VDV
+constexpr int kNumVdVariants = sizeof(kVdVariants) / sizeof(kVdVariants[0]);
+static int vd_variant() {
+    if (const char* e = getenv("SPARSLA_VD_VARIANT")) {
+        const int x = atoi(e);
+        if (x >= 0 && x < kNumVdVariants) return x;
+    }
+    return 0;
+}
+
 static const WsVariant kWsVariants[] = {WSV(1, 3, 3, true), WSV(1, 4, 2, true), WSV(1, 4, 2, false),
                                         WSV(2, 4, 2, false), WPV(2, 3), WSVW(1, 3, 3, true, 12),
                                         WSVW(1, 4, 2, true, 12)};
@@ -98,7 +126,8 @@ static int choose_ws_variant(long long max_row) {
     return 1;
 }
 
-size_t ws_smem_bytes(const DevCsr* A, int variant) {
+size_t ws_smem_bytes(const DevCsr* A, int variant, bool vd = false) {
+    if (vd) return 256 + (size_t)kVdVariants[A->vd_var].stg * StageLayout(A->cap_v, A->cap_c, true).stage;
     const WsVariant& V = kWsVariants[variant];
     if (V.rpt == 0) return 1024 + (size_t)(kSpmvThreads / 32) * V.stg * WarpStage(A->cap_v32, A->cap_c32).stage;
     return 256 + (size_t)V.stg * StageLayout(A->cap_v, A->cap_c).stage;
@@ -110,6 +139,9 @@ static void configure_ws_variants(int device) {
             CK(cudaFuncSetAttribute(kWsVariants[v].fn[m], cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
             CK(cudaFuncSetAttribute(kWsVariants[v].fn_hub[m], cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         }
+    for (int v = 0; v < kNumVdVariants; ++v)
+        for (int m = 0; m < 4; ++m)
+            CK(cudaFuncSetAttribute(kVdVariants[v].fn[m], cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     (void)device;
 }
 
@@ -118,6 +150,7 @@ static void configure_ws_variants(int device) {
 DevCsr::~DevCsr() {
     DeviceGuard g(device, true);
     cudaFree(rp); cudaFree(ci); cudaFree(val); cudaFree(dinv); cudaFree(ones);
+    cudaFree(vidx); cudaFree(vtab);
     if (stream) cudaStreamDestroy(stream);
     delete transpose;
 }
@@ -129,6 +162,78 @@ static void configure_kernels_once(int device) {
     if (std::find(done.begin(), done.end(), device) != done.end()) return;
     configure_ws_variants(device);
     done.push_back(device);
+}
+
+// Value dictionary: when the matrix has at most 256 distinct values (bit patterns), the
+// staged SpMV streams a 1-byte index per entry instead of the 8-byte value (constant-
+// coefficient stencils: {6, -1}).  The table holds the exact fp64 values, so every product
+// and sum is bit-identical.  SPARSLA_VALUE_DICT=0 disables.
+static void drop_value_dictionary(DevCsr* A) {
+    cudaFree(A->vidx); cudaFree(A->vtab);
+    A->vidx = nullptr; A->vtab = nullptr; A->vd = false;
+}
+
+static void build_value_dictionary(DevCsr* A, const double* h_val) {
+    drop_value_dictionary(A);
+    if (const char* e = getenv("SPARSLA_VALUE_DICT")) if (atoi(e) == 0) return;
+    const long long nnz = A->nnz;
+    if (nnz == 0) return;
+    // distinct bit patterns, per thread, abandoned past 256
+    const int nt = std::max(1, host_threads());
+    std::vector<std::vector<uint64_t>> seen(nt);
+    std::atomic<bool> too_many{false};
+    {
+        std::vector<std::thread> th;
+        const long long per = (nnz + nt - 1) / nt;
+        for (int t = 0; t < nt; ++t)
+            th.emplace_back([&, t] {
+                const long long b = t * per, e = std::min(nnz, b + per);
+                auto& S = seen[t];
+                uint64_t last = 0;
+                bool have_last = false;
+                for (long long k = b; k < e && !too_many.load(std::memory_order_relaxed); ++k) {
+                    uint64_t u;
+                    std::memcpy(&u, h_val + k, 8);
+                    if (have_last && u == last) continue;
+                    if (std::find(S.begin(), S.end(), u) == S.end()) {
+                        if (S.size() >= 256) { too_many = true; break; }
+                        S.push_back(u);
+                    }
+                    last = u;
+                    have_last = true;
+                }
+            });
+        for (auto& x : th) x.join();
+    }
+    if (too_many) return;
+    std::vector<uint64_t> tab;
+    for (auto& S : seen) tab.insert(tab.end(), S.begin(), S.end());
+    std::sort(tab.begin(), tab.end());
+    tab.erase(std::unique(tab.begin(), tab.end()), tab.end());
+    if (tab.size() > 256) return;
+    std::vector<uint8_t> idx((size_t)nnz);
+    parallel_for(nnz, [&](int64_t b, int64_t e) {
+        uint64_t last = ~0ULL;
+        uint8_t li = 0;
+        for (int64_t k = b; k < e; ++k) {
+            uint64_t u;
+            std::memcpy(&u, h_val + k, 8);
+            if (u != last) {
+                li = (uint8_t)(std::lower_bound(tab.begin(), tab.end(), u) - tab.begin());
+                last = u;
+            }
+            idx[(size_t)k] = li;
+        }
+    });
+    std::vector<double> vt(256, 0.0);
+    for (size_t i = 0; i < tab.size(); ++i) std::memcpy(&vt[i], &tab[i], 8);
+    A->vidx = dalloc<uint8_t>(nnz + 32);
+    A->vtab = dalloc<double>(256);
+    CK(cudaMemset(A->vidx + nnz, 0, 32));
+    CK(memcpy_sync(A->vidx, idx.data(), nnz, cudaMemcpyHostToDevice));
+    CK(memcpy_sync(A->vtab, vt.data(), 256 * 8, cudaMemcpyHostToDevice));
+    A->vd = true;
+    A->nvals = (int)tab.size();
 }
 
 template <class I>
@@ -168,6 +273,8 @@ DevCsr* DevCsr::create(int device, long long nrows, long long ncols, const I* h_
         CK(memcpy_sync(A->ci, tmp.data(), nnz * sizeof(int32_t), cudaMemcpyHostToDevice));
     }
     CK(memcpy_sync(A->val, h_val, nnz * sizeof(double), cudaMemcpyHostToDevice));
+    A->vd_var = vd_variant();
+    build_value_dictionary(A.get(), h_val);
     // row-length statistics -> SpMV variant and staging capacity
     long long mb = 0, mr = 0;
     for (long long b = 0; b < nrows; b += kChunkSlots) {
@@ -213,7 +320,9 @@ DevCsr* DevCsr::create(int device, long long nrows, long long ncols, const I* h_
         A->l2_keep = ws <= 0.9 * l2 ? 1 : 0;
         if (const char* e = getenv("SPARSLA_L2_KEEP")) A->l2_keep = atoi(e) ? 1 : 0;
     }
-    A->smem_bytes = ws_smem_bytes(A.get(), A->ws_var);
+    // dictionary kernels: variant 0 (rows of <= 8 entries) without oversized rounds only
+    if (A->ws_var != 0 || A->has_hub) drop_value_dictionary(A.get());
+    A->smem_bytes = ws_smem_bytes(A.get(), A->ws_var, A->vd);
     A->staged = A->cap_v >= 512 && A->smem_bytes <= 200 * 1024;  // else: direct kernel
     if (const char* e = getenv("SPARSLA_SPMV_DIRECT")) if (atoi(e)) A->staged = false;
     {
@@ -221,9 +330,10 @@ DevCsr* DevCsr::create(int device, long long nrows, long long ncols, const I* h_
         CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
         for (int v = 0; v < kNumWsVariants; ++v) {
             int per_sm = 0;
+            const bool vd = A->vd && v == 0;
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                &per_sm, kWsVariants[v].fn[SPMV_CG], kWsVariants[v].rpt == 0 ? kSpmvThreads : kWsThreads,
-                ws_smem_bytes(A.get(), v)));
+                &per_sm, vd ? kVdVariants[A->vd_var].fn[SPMV_CG] : kWsVariants[v].fn[SPMV_CG],
+                kWsVariants[v].rpt == 0 ? kSpmvThreads : kWsThreads, ws_smem_bytes(A.get(), v, vd)));
             A->ws_ctas[v] = sms * std::max(1, per_sm);
         }
     }
@@ -245,6 +355,36 @@ const double* DevCsr::jacobi_dinv() {
         CK(cudaStreamSynchronize(stream));
     }
     return dinv;
+}
+
+// every d[i] bit-identical to d[0]?  (flag cleared by any mismatch)
+static __global__ void uniform_kernel(const double* d, long long n, int* flag) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n && __double_as_longlong(d[i]) != __double_as_longlong(d[0])) *flag = 0;
+}
+
+bool DevCsr::jacobi_uniform(double* value) {
+    const double* d = jacobi_dinv();
+    std::lock_guard<std::mutex> lk(lazy_mu);
+    if (dinv_uniform < 0) {
+        DeviceGuard g(device);
+        dinv_uniform = 0;
+        if (nrows > 0) {
+            int* flag = dalloc<int>(1);
+            const int one = 1;
+            CK(cudaMemcpyAsync(flag, &one, sizeof one, cudaMemcpyHostToDevice, stream));
+            uniform_kernel<<<grid_for(nrows, 256), 256, 0, stream>>>(d, nrows, flag);
+            CK(cudaGetLastError());
+            int h = 0;
+            CK(cudaMemcpyAsync(&h, flag, sizeof h, cudaMemcpyDeviceToHost, stream));
+            CK(cudaMemcpyAsync(&dinv_value, d, sizeof(double), cudaMemcpyDeviceToHost, stream));
+            CK(cudaStreamSynchronize(stream));
+            cudaFree(flag);
+            dinv_uniform = h;
+        }
+    }
+    *value = dinv_value;
+    return dinv_uniform == 1;
 }
 
 const double* DevCsr::ones_vec() {
@@ -320,6 +460,7 @@ void launch_spmv_part(DevCsr* A, cudaStream_t s, int mode, const double* x, doub
     if (grid == 0) return;
     SpmvParams P{};
     P.rp = A->rp; P.ci = A->ci; P.val = A->val;
+    P.vidx = A->vidx; P.vtab = A->vtab;
     P.x = x; P.y = y; P.n = A->nrows; P.chunk0 = 0; P.aux = aux;
     P.nch = nch;
     P.chunk_list = list;
@@ -337,8 +478,10 @@ void launch_spmv_part(DevCsr* A, cudaStream_t s, int mode, const double* x, doub
         const bool wp = kWsVariants[v].rpt == 0;
         if (wp) { P.cap_v = A->cap_v32; P.cap_c = A->cap_c32; }
         void* args[] = {&P};
-        const void* fn = A->has_hub ? kWsVariants[v].fn_hub[mode] : kWsVariants[v].fn[mode];
-        CK(cudaLaunchKernel(fn, dim3(grid), dim3(wp ? kSpmvThreads : kWsThreads), args, ws_smem_bytes(A, v), s));
+        const bool vd = A->vd && v == 0;
+        const void* fn = vd ? kVdVariants[A->vd_var].fn[mode]
+                            : (A->has_hub ? kWsVariants[v].fn_hub[mode] : kWsVariants[v].fn[mode]);
+        CK(cudaLaunchKernel(fn, dim3(grid), dim3(wp ? kSpmvThreads : kWsThreads), args, ws_smem_bytes(A, v, vd), s));
     } else {
 #define DIRECT_CASE(M) spmv_direct_kernel<M><<<grid, kSpmvThreads, 0, s>>>(P);
         switch (mode) {
@@ -410,6 +553,16 @@ Solver::Solver(DevCsr* A_, int backend_, const sparsla_solve_options& o, DistCtx
     n = A->nrows;
     stream = A->stream;
     dinv = o.preconditioner == SPARSLA_PRECOND_JACOBI ? A->jacobi_dinv() : A->ones_vec();
+    // A constant Jacobi diagonal (constant-coefficient stencils; the identity when
+    // unpreconditioned) is passed as a scalar instead of being streamed: 16 bytes per row
+    // less per CG iteration, same operands, same bits.  SPARSLA_UNIFORM_DIAG=0 disables.
+    {
+        const char* e = getenv("SPARSLA_UNIFORM_DIAG");
+        if (!e || atoi(e) != 0) {
+            if (o.preconditioner == SPARSLA_PRECOND_JACOBI) d_is_uniform = A->jacobi_uniform(&d_uniform);
+            else { d_is_uniform = true; d_uniform = 1.0; }
+        }
+    }
     const long long m = std::max<long long>(1, nchunks_of(n));
     const long long nv = n + 2;
     const long long nh = (dist ? dist->vec_len : n) + 2;  // SpMV inputs: [owned | gap | halo]
@@ -476,7 +629,7 @@ RedParams Solver::red(int which, int slot) const {
 
 VecParams Solver::vparams() const {
     VecParams P{};
-    P.n = n; P.d = dinv; P.x = x; P.r = r; P.p = p; P.q = q;
+    P.n = n; P.d = d_is_uniform ? nullptr : dinv; P.d_uni = d_uniform; P.x = x; P.r = r; P.p = p; P.q = q;
     P.rh = rh; P.ph = ph; P.v = q; P.s = s; P.sh = sh; P.tt = t; P.b = b;
     P.check_done = 1;
     return P;
@@ -868,7 +1021,22 @@ int sparsla_dcsr_set_values(sparsla_dcsr* H, const double* vals, int32_t mem) {
                            mem == SPARSLA_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, A->stream));
         CK(cudaStreamSynchronize(A->stream));
         // value-dependent caches are invalid now
+        // value dictionary: rebuilt from host values (the scan stops at the 257th distinct
+        // value); device values are only downloaded when the matrix had a dictionary
+        if (A->ws_var == 0 && !A->has_hub && (mem != SPARSLA_MEM_DEVICE || A->vd)) {
+            if (mem != SPARSLA_MEM_DEVICE) {
+                build_value_dictionary(A, vals);
+            } else {
+                std::vector<double> hv((size_t)A->nnz);
+                CK(memcpy_sync(hv.data(), A->val, A->nnz * sizeof(double), cudaMemcpyDeviceToHost));
+                build_value_dictionary(A, hv.data());
+            }
+        } else {
+            drop_value_dictionary(A);
+        }
+        A->smem_bytes = ws_smem_bytes(A, A->ws_var, A->vd);
         if (A->dinv) { cudaFree(A->dinv); A->dinv = nullptr; }
+        A->dinv_uniform = -1;
         A->sym_checked = -1;
         delete A->transpose;
         A->transpose = nullptr;
@@ -891,6 +1059,18 @@ int sparsla_dcsr_info(const sparsla_dcsr* H, int64_t* info) {
         info[3] = (A->nrows + 1) * 4 + A->nnz * 12;
         info[4] = A->max_block_nnz; info[5] = A->max_row; info[6] = A->staged ? 0 : 1;
         info[7] = A->ws_var;
+    });
+}
+
+int sparsla_dcsr_format(sparsla_dcsr* H, int64_t* fmt) {
+    return guarded([&] {
+        need(H, "matrix");
+        DevCsr* A = H->A;
+        DeviceGuard g(A->device);
+        fmt[0] = A->vd ? 1 : 0;
+        fmt[1] = A->vd ? A->nvals : 0;
+        double v = 0.0;
+        fmt[2] = (A->nrows == A->ncols || A->local_layout) && A->jacobi_uniform(&v) ? 1 : 0;
     });
 }
 

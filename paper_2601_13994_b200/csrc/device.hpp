@@ -40,6 +40,13 @@ struct DevCsr {
     int ws_ctas[8] = {0};  // persistent grid per staged-SpMV variant (SMs x resident CTAs)
     double* dinv = nullptr;
     double* ones = nullptr;
+    uint8_t* vidx = nullptr;  // value dictionary (<= 256 distinct values): 1-byte index per entry
+    double* vtab = nullptr;   // [256] distinct values
+    bool vd = false;          // staged SpMV streams vidx instead of val
+    int nvals = 0;            // distinct values in vtab
+    int vd_var = 0;           // value-dictionary kernel variant
+    int dinv_uniform = -1;    // 1: every dinv entry has the same bits (dinv_value); -1: unknown
+    double dinv_value = 0.0;
     int sym_checked = -1;
     DevCsr* transpose = nullptr;
     cudaStream_t stream = nullptr;
@@ -50,6 +57,7 @@ struct DevCsr {
                           const double* val, bool local_layout = false);
     ~DevCsr();
     const double* jacobi_dinv();
+    bool jacobi_uniform(double* value);  // constant Jacobi diagonal? (checked once per values)
     const double* ones_vec();
     bool exactly_symmetric();
     DevCsr* get_transpose();
@@ -101,6 +109,8 @@ struct Solver {
     long long n = 0;
     cudaStream_t stream = nullptr;
     const double* dinv = nullptr;
+    bool d_is_uniform = false;   // constant diagonal: the vector kernels take d_uniform, not dinv
+    double d_uniform = 0.0;
     const double* b = nullptr;
     double* x = nullptr;
     double *x_own = nullptr, *b_own = nullptr;

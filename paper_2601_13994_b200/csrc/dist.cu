@@ -612,6 +612,7 @@ int sparsla_dist_adjoint_backward(sparsla_dist* D, const double* x_owned, const 
                     CKD(memcpy_sync(D->AT->val, vals_t, A->nnz * 8, mem == SPARSLA_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
                     cudaFree(D->AT->dinv);
                     D->AT->dinv = nullptr;
+                    D->AT->dinv_uniform = -1;
                 }
                 M = D->AT;
             }

@@ -460,6 +460,8 @@ struct SpmvParams {
     long long n_interior;       //   consumers wait for the halo before list index n_interior
     int halo_v;
     const double* aux;  // BICG_V: rhat, BICG_T: s
+    const uint8_t* vidx;  // value-dictionary kernels: 1-byte value index per entry ...
+    const double* vtab;   // ... into this table of the matrix's <= 256 distinct values
     int cap_v, cap_c;   // staged capacities (elements) per round
     int l2_keep;        // 1: matrix stream evict_last (working set fits L2), 0: evict_first
     int check_done;
@@ -554,8 +556,9 @@ constexpr int kWsThreads = (kConsumerWarps + 1) * 32;
 
 struct StageLayout {
     size_t vbytes, cbytes, rbytes, stage;
-    __host__ __device__ StageLayout(int cap_v, int cap_c) {
-        vbytes = ((size_t)cap_v * 8 + 127) & ~size_t(127);
+    // vd: value-dictionary stream (1 byte per entry + 16-byte copy granule slack)
+    __host__ __device__ StageLayout(int cap_v, int cap_c, bool vd = false) {
+        vbytes = ((size_t)cap_v * (vd ? 1 : 8) + (vd ? 32 : 0) + 127) & ~size_t(127);
         cbytes = ((size_t)cap_c * 4 + 127) & ~size_t(127);
         rbytes = (kRpCopy * 4 + 127) & ~size_t(127);
         stage = vbytes + cbytes + rbytes;
@@ -564,15 +567,24 @@ struct StageLayout {
 
 // RPT: rounds (= rows per consumer thread) in flight together; STG: ring depth;
 // MINB: resident CTAs per SM requested from ptxas (register budget).
-template <int MODE, int RPT, int STG, int MINB, bool EARLY, int W = 8, bool HUB = false>
+// VD (value dictionary): the value stream is one byte per entry indexing a table of the
+// matrix's distinct values (<= 256, e.g. {6, -1} for the 7-point Laplacian) held in shared
+// memory, so the matrix costs 5 instead of 12 bytes per entry; the products use the same
+// fp64 values in the same order, so results are bit-identical to the plain kernel.
+template <int MODE, int RPT, int STG, int MINB, bool EARLY, int W = 8, bool HUB = false, bool VD = false>
 __global__ void __launch_bounds__(kWsThreads, MINB) spmv_ws_kernel(SpmvParams P) {
     constexpr int ND = SpmvDots<MODE>::n;
     constexpr int NA = ND > 0 ? ND : 1;
+    constexpr int VALIGN = VD ? 16 : 2;  // value-stream copy granule (16 bytes)
     if (P.check_done && P.red.st->done) return;
     extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ double s_vtab[VD ? 256 : 1];
+    if constexpr (VD) {
+        for (int i = threadIdx.x; i < 256; i += blockDim.x) s_vtab[i] = P.vtab[i];
+    }
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);
     uint64_t* empty = full + STG;
-    const StageLayout L(P.cap_v, P.cap_c);
+    const StageLayout L(P.cap_v, P.cap_c, VD);
     unsigned char* stage0 = smem + 256;
     const int t = threadIdx.x;
     const int warp = t >> 5, lane = t & 31;
@@ -599,18 +611,22 @@ __global__ void __launch_bounds__(kWsThreads, MINB) spmv_ws_kernel(SpmvParams P)
                     const long long rs = base + (long long)r * kChunkSlots;
                     const long long re = min(rs + kChunkSlots, P.n);
                     const int nz0 = __ldg(P.rp + rs), nz1 = __ldg(P.rp + re);
-                    const int a0 = nz0 & ~1, a1 = (nz1 + 1) & ~1;
+                    const int a0 = nz0 & ~(VALIGN - 1), a1 = (nz1 + VALIGN - 1) & ~(VALIGN - 1);
                     const int c0 = nz0 & ~3, c1 = (nz1 + 3) & ~3;
                     // rounds larger than the ring's stage (hub rows of irregular matrices)
                     // bypass it: only row_ptr is staged, col/val are read from global
                     const bool big = HUB && (a1 - a0 > P.cap_v || c1 - c0 > P.cap_c);
-                    const uint32_t vb = big ? 0u : (uint32_t)(a1 - a0) * 8u;
+                    const uint32_t vb = big ? 0u : (uint32_t)(a1 - a0) * (VD ? 1u : 8u);
                     const uint32_t cb = big ? 0u : (uint32_t)(c1 - c0) * 4u;
                     unsigned char* st = stage0 + s * L.stage;
                     reinterpret_cast<int32_t*>(st + L.vbytes + L.cbytes)[kRpCopy] = big ? 1 : 0;
                     mbar_arrive_expect_tx(&full[s], (uint32_t)(kRpCopy * 4) + vb + cb);
                     bulk_g2s(st + L.vbytes + L.cbytes, P.rp + rs, kRpCopy * 4, &full[s], pol);
-                    if (vb) bulk_g2s(st, P.val + a0, vb, &full[s], pol);
+                    if constexpr (VD) {
+                        if (vb) bulk_g2s(st, P.vidx + a0, vb, &full[s], pol);
+                    } else {
+                        if (vb) bulk_g2s(st, P.val + a0, vb, &full[s], pol);
+                    }
                     if (cb) bulk_g2s(st + L.vbytes, P.ci + c0, cb, &full[s], pol);
                 }
             }
@@ -621,6 +637,84 @@ __global__ void __launch_bounds__(kWsThreads, MINB) spmv_ws_kernel(SpmvParams P)
     // ------------------------------------------------------------------ consumers ----
     __shared__ double sred[NA * kConsumerWarps];
     __shared__ int s_flag;
+    static_assert(!VD || (RPT == 1 && !HUB), "value-dictionary kernels use the lean consumer");
+    if constexpr (VD) {
+        // Lean consumer of the value-dictionary stream: one row per thread per round, the
+        // ring position kept incrementally, row segments addressed once per round, entries
+        // read with immediate offsets.  Rows of <= W entries issue their x gathers straight
+        // from the staged columns, keep the 1-byte value indices, and release the stage
+        // while the gathers are in flight; a round with a longer row finishes from the held
+        // stage (same left-to-right order).
+        int s = 0;
+        uint32_t ph = 0;
+        bool halo_ok = P.p2p == nullptr;
+        for (long long c = blockIdx.x; c < P.nch; c += gridDim.x) {
+            if (!halo_ok && c >= P.n_interior) {
+                if (lane == 0) p2p_wait_halo(P.p2p, P.halo_v, P.red.st->ep_halo[P.halo_v]);
+                __syncwarp();
+                halo_ok = true;
+            }
+            const long long chunk = P.chunk_list ? (long long)P.chunk_list[c] : P.chunk0 + c;
+            const long long base = chunk * kChunk;
+            const long long rem = (P.n - base + kChunkSlots - 1) / kChunkSlots;
+            const int nr = rem < kChunkRounds ? (int)rem : kChunkRounds;
+            double acc[NA];
+#pragma unroll
+            for (int d = 0; d < NA; ++d) acc[d] = 0.0;
+            for (int r = 0; r < nr; ++r) {
+                mbar_wait(&full[s], ph);
+                const unsigned char* A = stage0 + s * L.stage;
+                const int32_t* rps = reinterpret_cast<const int32_t*>(A + L.vbytes + L.cbytes);
+                const long long row = base + (long long)r * kChunkSlots + t;
+                const bool live = row < P.n;
+                const int o0 = rps[0];
+                const int kb = live ? rps[t] : o0, ke = live ? rps[t + 1] : o0;
+                const int len = ke - kb;
+                const int32_t* cp = reinterpret_cast<const int32_t*>(A + L.vbytes) + (kb - (o0 & ~3));
+                const uint8_t* vp = A + (kb - (o0 & ~(VALIGN - 1)));
+                double y = 0.0;
+                if (__all_sync(0xffffffffu, len <= W)) {
+                    // issue every gather straight from the staged columns; the stage is
+                    // released once the gathers are in flight (their addresses consumed)
+                    double xv[W];
+                    uint32_t vi[(W + 3) / 4];  // value indices, 4 per register
+#pragma unroll
+                    for (int q = 0; q < (W + 3) / 4; ++q) vi[q] = 0u;
+#pragma unroll
+                    for (int u = 0; u < W; ++u)
+                        if (u < len) { xv[u] = __ldg(P.x + cp[u]); vi[u / 4] |= (uint32_t)vp[u] << (8 * (u % 4)); }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&empty[s]);
+#pragma unroll
+                    for (int u = 0; u < W; ++u)
+                        if (u < len) y = __dadd_rn(y, __dmul_rn(s_vtab[(vi[u / 4] >> (8 * (u % 4))) & 0xffu], xv[u]));
+                } else {
+                    for (int k0 = 0; k0 < len; k0 += W) {
+                        double pr[W];
+#pragma unroll
+                        for (int u = 0; u < W; ++u)
+                            if (k0 + u < len) pr[u] = __dmul_rn(s_vtab[vp[k0 + u]], __ldg(P.x + cp[k0 + u]));
+#pragma unroll
+                        for (int u = 0; u < W; ++u)
+                            if (k0 + u < len) y = __dadd_rn(y, pr[u]);
+                    }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&empty[s]);
+                }
+                if (live) { P.y[row] = y; spmv_epilogue<MODE>(P, row, y, acc); }
+                if (++s == STG) { s = 0; ph ^= 1u; }
+            }
+            if constexpr (ND > 0) {
+                block_tree<kConsumerWarps * 32, ND, 1>(acc, sred);
+                if (t == 0) {
+#pragma unroll
+                    for (int d = 0; d < ND; ++d) P.red.partials[d * P.red.nchunks + chunk] = acc[d];
+                }
+            }
+        }
+        if constexpr (ND > 0) ticket_and_finish<kConsumerWarps * 32, ND, 1>(P.red, sred, &s_flag);
+        return;
+    }
     long long g = 0;
     bool halo_ready = P.p2p == nullptr;
     for (long long c = blockIdx.x; c < P.nch; c += gridDim.x) {
@@ -657,7 +751,7 @@ __global__ void __launch_bounds__(kWsThreads, MINB) spmv_ws_kernel(SpmvParams P)
                     if constexpr (HUB) big[j] = rps[kRpCopy] != 0;  // oversized round: col/val from global
                     if (row < P.n) {
                         k[j] = rps[t]; ke[j] = rps[t + 1];
-                        ov[j] = rps[0] & ~1; oc[j] = rps[0] & ~3;
+                        ov[j] = rps[0] & ~(VALIGN - 1); oc[j] = rps[0] & ~3;
                     }
                 }
             }
@@ -921,7 +1015,8 @@ __global__ void __launch_bounds__(kSpmvThreads, MINB) spmv_wp_kernel(SpmvParams 
 // oracle's order (no FMA).
 struct VecParams {
     long long n;
-    const double* d;  // Jacobi inverse diagonal
+    const double* d;  // Jacobi inverse diagonal; nullptr: uniform diagonal d_uni (not streamed)
+    double d_uni;
     double *x, *r, *p, *q;
     double *rh, *ph, *v, *s, *sh, *tt;
     const double* b;
@@ -943,6 +1038,11 @@ __device__ __forceinline__ double2 ld2(const double* p, long long i, long long n
 __device__ __forceinline__ void st2(double* p, long long i, long long n, double2 v) {
     if (i + 1 < n) *reinterpret_cast<double2*>(p + i) = v;
     else if (i < n) p[i] = v.x;
+}
+// Jacobi inverse diagonal pair: streamed, or the uniform value of a constant diagonal
+// (Poisson / constant-coefficient stencils, and the identity when unpreconditioned).
+__device__ __forceinline__ double2 ldd(const double* d, double d_uni, long long i, long long n) {
+    return d ? ld2(d, i, n) : make_double2(d_uni, d_uni);
 }
 __device__ __forceinline__ double lane(const double2& v, int e) { return e ? v.y : v.x; }
 __device__ __forceinline__ void set_lane(double2& v, int e, double x) { if (e) v.y = x; else v.x = x; }
@@ -969,16 +1069,16 @@ struct VecScalars {
 template <int OP>
 __device__ __forceinline__ void vec_load(const VecParams& P, long long i, double2 (&in)[VecTraits<OP>::nin]) {
     const long long n = P.n;
-    if constexpr (OP == V_CG_INIT) { in[0] = ld2(P.b, i, n); in[1] = ld2(P.q, i, n); in[2] = ld2(P.d, i, n); }
-    if constexpr (OP == V_CG_U1) { in[0] = ld2(P.r, i, n); in[1] = ld2(P.q, i, n); in[2] = ld2(P.d, i, n); }
+    if constexpr (OP == V_CG_INIT) { in[0] = ld2(P.b, i, n); in[1] = ld2(P.q, i, n); in[2] = ldd(P.d, P.d_uni, i, n); }
+    if constexpr (OP == V_CG_U1) { in[0] = ld2(P.r, i, n); in[1] = ld2(P.q, i, n); in[2] = ldd(P.d, P.d_uni, i, n); }
     if constexpr (OP == V_CG_U2) {
-        in[0] = ld2(P.x, i, n); in[1] = ld2(P.p, i, n); in[2] = ld2(P.r, i, n); in[3] = ld2(P.d, i, n);
+        in[0] = ld2(P.x, i, n); in[1] = ld2(P.p, i, n); in[2] = ld2(P.r, i, n); in[3] = ldd(P.d, P.d_uni, i, n);
     }
     if constexpr (OP == V_BI_INIT) { in[0] = ld2(P.b, i, n); in[1] = ld2(P.v, i, n); }
     if constexpr (OP == V_BI_U1) {
-        in[0] = ld2(P.r, i, n); in[1] = ld2(P.p, i, n); in[2] = ld2(P.v, i, n); in[3] = ld2(P.d, i, n);
+        in[0] = ld2(P.r, i, n); in[1] = ld2(P.p, i, n); in[2] = ld2(P.v, i, n); in[3] = ldd(P.d, P.d_uni, i, n);
     }
-    if constexpr (OP == V_BI_U2) { in[0] = ld2(P.r, i, n); in[1] = ld2(P.v, i, n); in[2] = ld2(P.d, i, n); }
+    if constexpr (OP == V_BI_U2) { in[0] = ld2(P.r, i, n); in[1] = ld2(P.v, i, n); in[2] = ldd(P.d, P.d_uni, i, n); }
     if constexpr (OP == V_BI_U3) {
         in[0] = ld2(P.x, i, n); in[1] = ld2(P.ph, i, n); in[2] = ld2(P.s, i, n);
         in[3] = ld2(P.sh, i, n); in[4] = ld2(P.tt, i, n); in[5] = ld2(P.rh, i, n);

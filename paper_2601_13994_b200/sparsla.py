@@ -260,6 +260,12 @@ class DeviceCsr:
         keys = ["nrows", "ncols", "nnz", "device_bytes", "max_block_nnz", "max_row", "variant", "ws_variant"]
         return {k: int(out[i]) for i, k in enumerate(keys)}
 
+    def format(self):
+        """SpMV storage format: value dictionary on / distinct values / constant Jacobi diagonal."""
+        out = np.zeros(3, np.int64)
+        _check(lib().sparsla_dcsr_format(self.h, _p(out, _i64p)))
+        return {"value_dict": bool(out[0]), "distinct_values": int(out[1]), "uniform_diag": bool(out[2])}
+
     def close(self):
         if self.h:
             lib().sparsla_dcsr_destroy(self.h)

@@ -275,3 +275,52 @@ def test_persistent_solver_fixed_iterations(S, O, gpu):
         xo, _ = O.cg_fixed(A, b, k)
         assert sv.report().iterations == k
         assert_bitwise(sv.x(), xo, f"k={k}")
+
+
+@pytest.mark.parametrize("kind,p1,p2,fp,backend", [("poisson3d", 40, 0, 0.0, "cg"), ("poisson2d", 200, 0, 0.0, "cg"),
+                                                   ("convdiff3d", 24, 0, 0.1, "bicgstab")])
+def test_value_dictionary_and_scalar_diagonal_bitwise(S, O, gpu, monkeypatch, kind, p1, p2, fp, backend):
+    """Stored-format choices are invisible in the results: the 1-byte value dictionary
+    (<= 256 distinct values) and the scalar constant Jacobi diagonal give the same bits as
+    plain CSR with a streamed diagonal, and as the oracle."""
+    A = O.generate(kind, p1, p2, fp)
+    b = np.random.default_rng(5).standard_normal(A.nrows)
+    opts = S.SolveOptions(atol=0.0, rtol=1e-9, max_iter=20000)
+    fn = S.cg_solve if backend == "cg" else S.bicgstab_solve
+    D1 = to_S(S, A).device(0)
+    f1 = D1.format()
+    assert f1["value_dict"] and f1["distinct_values"] <= 4 and f1["uniform_diag"], f1
+    x1, r1 = fn(D1, b, opts)
+    y1 = S.spmv(D1, b)
+    monkeypatch.setenv("SPARSLA_VALUE_DICT", "0")
+    monkeypatch.setenv("SPARSLA_UNIFORM_DIAG", "0")
+    D2 = to_S(S, A).device(0)
+    assert not D2.format()["value_dict"]
+    x2, r2 = fn(D2, b, opts)
+    assert r1.iterations == r2.iterations and r1.converged
+    assert_bitwise(x1, x2, "dictionary/scalar-diagonal vs plain solve")
+    assert_bitwise(y1, S.spmv(D2, b), "dictionary vs plain spmv")
+    assert_bitwise(y1, O.spmv(A, b), "dictionary spmv vs oracle")
+    xo, ro = (O.cg if backend == "cg" else O.bicgstab)(A, b, atol=0.0, rtol=1e-9, max_iter=20000)
+    assert ro["iterations"] == r1.iterations
+    assert_bitwise(x1, xo, "vs oracle")
+
+
+def test_value_dictionary_rebuilt_by_set_values(S, O, gpu):
+    """set_values (= SparseCoo::with_values) rebuilds the dictionary; more than 256 distinct
+    values fall back to the plain value stream, still bit-exact."""
+    A = O.generate("poisson3d", 20)
+    D = to_S(S, A).device(0)
+    assert D.format()["value_dict"]
+    rng = np.random.default_rng(9)
+    v2 = A.vals * (1.0 + 0.01 * rng.random(len(A.vals)))  # all distinct
+    S.lib().sparsla_dcsr_set_values(D.h, v2.ctypes.data_as(S._f64p), 0)
+    assert not D.format()["value_dict"]
+    x = rng.standard_normal(A.ncols)
+    A2 = O.Csr(A.nrows, A.ncols, A.row_ptr, A.col_idx, v2)
+    assert_bitwise(S.spmv(D, x), O.spmv(A2, x))
+    v3 = np.where(A.vals > 0, 7.5, -1.25)
+    S.lib().sparsla_dcsr_set_values(D.h, v3.ctypes.data_as(S._f64p), 0)
+    assert D.format()["value_dict"] and D.format()["distinct_values"] == 2
+    A3 = O.Csr(A.nrows, A.ncols, A.row_ptr, A.col_idx, v3)
+    assert_bitwise(S.spmv(D, x), O.spmv(A3, x))
