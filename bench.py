@@ -295,7 +295,7 @@ def run_ours(args):
         with open(os.path.join(ROOT, "profiles", "spmv_traffic.json")) as f:
             tj = json.load(f)
         if tj.get("size") == args.size:
-            traffic = tj["dram_bytes_per_launch"]
+            traffic = tj["value_dict" if fmt["value_dict"] else "plain"]["dram_bytes_per_launch"]
     except Exception:
         pass
     line = {

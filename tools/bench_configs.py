@@ -46,11 +46,16 @@ def solve_cfg(name, kind, p1, p2, fp, backend, rtol, extra=None):
     sv.reset()
     sv.iterate(3)
     kms = sv.kernel_times(10)
+    fmt = D.format()
+    mat = 5 * nnz + 2048 if fmt["value_dict"] else 12 * nnz  # stored matrix stream per SpMV
+    dn = 0 if fmt["uniform_diag"] else 8 * n                  # one streamed-diagonal read
     if backend == "cg":
-        it_bytes = 12 * nnz + 108 * n + 4
+        it_bytes = 12 * nnz + 108 * n + 4                     # SURVEY canonical (CSR, 3 passes)
+        stored_bytes = mat + 4 * (n + 1) + 16 * n + 32 * n - (8 * n - dn) + 48 * n - (8 * n - dn)
         names = ["spmv_cg", "cg_update1", "cg_update2"]
     else:
         it_bytes = 24 * nnz + 208 * n + 8
+        stored_bytes = 2 * mat + 8 * (n + 1) + 208 * n - 2 * (8 * n - dn)
         names = ["bicg_update1", "spmv_v", "bicg_update2", "spmv_t", "bicg_update3"]
     per_it = sum(kms)
     out = {"config": name, "kind": kind, "n": n, "nnz": nnz, "backend": backend, "rtol": rtol,
@@ -61,6 +66,8 @@ def solve_cfg(name, kind, p1, p2, fp, backend, rtol, extra=None):
            "iteration_gbs_from_kernels": it_bytes / (per_it * 1e-3) / 1e9,
            "iteration_frac_of_measured_peak": it_bytes / (per_it * 1e-3) / 1e9 / PEAK,
            "iteration_gbs_wall": it_bytes * rep.iterations / (ms * 1e-3) / 1e9,
+           "format": fmt, "stored_bytes_per_iteration": stored_bytes,
+           "stored_iteration_frac_of_measured_peak": stored_bytes / (per_it * 1e-3) / 1e9 / PEAK,
            "generate_s": tgen, "device_info": D.info()}
     if extra:
         out.update(extra(D, sv, n, nnz, opts))
