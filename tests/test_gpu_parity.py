@@ -324,3 +324,25 @@ def test_value_dictionary_rebuilt_by_set_values(S, O, gpu):
     assert D.format()["value_dict"] and D.format()["distinct_values"] == 2
     A3 = O.Csr(A.nrows, A.ncols, A.row_ptr, A.col_idx, v3)
     assert_bitwise(S.spmv(D, x), O.spmv(A3, x))
+
+
+@pytest.mark.parametrize("nvals", [1, 255, 256, 257])
+def test_value_dictionary_limits_and_signed_zero(S, O, gpu, nvals):
+    """Dictionary selection is by bit pattern: 256 distinct values use it, 257 fall back;
+    -0.0 and +0.0 are distinct entries, and either way the SpMV is bitwise the oracle's."""
+    A = O.generate("poisson3d", 14)
+    nnz = len(A.vals)
+    pool = np.linspace(-3.0, 3.0, nvals)
+    if nvals >= 2:
+        pool[0], pool[1] = 0.0, -0.0
+    vals = pool[np.arange(nnz) % nvals]
+    B = O.Csr(A.nrows, A.ncols, A.row_ptr, A.col_idx, vals)
+    D = to_S(S, B).device(0)
+    f = D.format()
+    distinct = len(np.unique(pool.view(np.int64)))
+    assert f["value_dict"] == (distinct <= 256), f
+    if f["value_dict"]:
+        assert f["distinct_values"] == distinct
+    x = np.random.default_rng(nvals).standard_normal(A.ncols)
+    x[::7] = -x[::7]
+    assert_bitwise(S.spmv(D, x), O.spmv(B, x), f"{nvals} values")
