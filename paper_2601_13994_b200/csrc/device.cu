@@ -593,7 +593,7 @@ Solver::Solver(DevCsr* A_, int backend_, const sparsla_solve_options& o, DistCtx
     CK(cudaMallocHost(&h_flag, 2 * sizeof(int)));
     CK(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
-    if (dist && dist->p2p_enabled && backend == SPARSLA_BACKEND_CG) p2p_setup();
+    if (dist && dist->p2p_enabled) p2p_setup();
     } catch (...) {
         release();  // a constructor that throws runs no destructor: free what was allocated
         throw;
@@ -650,7 +650,8 @@ void Solver::spmv_point(int mode, double* xin, double* y, const double* aux, int
         R.point = slot;
         const unsigned gall = spmv_grid(A, dist->n_interior + dist->n_boundary);
         launch_spmv_part(A, stream, mode, xin, y, aux, R, check_done, dist->d_all_chunks,
-                         dist->n_interior + dist->n_boundary, gall, d_p2p, dist->n_interior, 0);
+                         dist->n_interior + dist->n_boundary, gall, d_p2p, dist->n_interior,
+                         mode == SPMV_BICG_T ? 1 : 0);  // halo flag: p / p-hat = 0, s-hat = 1
         return;
     }
     if (nd > 0) R.red_out = dist->red_send + slot * 8;
@@ -674,12 +675,18 @@ void Solver::vec_point(int scalar, int slot, int check_done) {
     P.check_done = check_done;
     RedParams R = red(scalar, slot);  // (CG_U2 uses the slot's ticket to clear pending_x)
     constexpr int nd = VecTraits<OP>::ndot;
-    if (d_p2p && (OP == V_CG_U1 || OP == V_CG_U2)) {
-        // consume the previous reduction point in-kernel; U1 pushes its own totals
+    if (d_p2p && (OP == V_CG_U1 || OP == V_CG_U2 || OP == V_BI_U1 || OP == V_BI_U2 || OP == V_BI_U3)) {
+        // consume the previous reduction point in-kernel (CG: U1 <- p.q, U2 <- r.z/r.r;
+        // BiCGStab: U1 <- previous U3's rho/r.r, U2 <- rhat.v, U3 <- t.t/t.s/s.s); kernels
+        // with dot products push their own totals as point `slot`
         P.p2p = d_p2p;
-        P.consume_point = OP == V_CG_U1 ? 1 : 2;
-        P.consume_scalar = OP == V_CG_U1 ? SC_CG_PQ : SC_CG_RR;
-        P.consume_k = OP == V_CG_U1 ? 1 : 2;
+        switch (OP) {
+            case V_CG_U1: P.consume_point = 1; P.consume_scalar = SC_CG_PQ; P.consume_k = 1; break;
+            case V_CG_U2: P.consume_point = 2; P.consume_scalar = SC_CG_RR; P.consume_k = 2; break;
+            case V_BI_U1: P.consume_point = 5; P.consume_scalar = SC_BI_U3; P.consume_k = 2; break;
+            case V_BI_U2: P.consume_point = 2; P.consume_scalar = SC_BI_RV; P.consume_k = 1; break;
+            default: P.consume_point = 4; P.consume_scalar = SC_BI_T; P.consume_k = 3; break;
+        }
         R.point = slot;
         launch_vec<OP>(stream, P, R);
         return;
@@ -708,8 +715,8 @@ void Solver::enqueue_init() {
     spmv_point(SPMV_PLAIN, x0, q, nullptr, SC_NONE, 0, 0);
     if (backend == SPARSLA_BACKEND_CG) vec_point<V_CG_INIT>(SC_CG_INIT, 0, 0);
     else vec_point<V_BI_INIT>(SC_BI_INIT, 0, 0);
-    if (d_p2p) {  // halo of p0 through the transport once; later iterations push it in-kernel
-        dist->exchange(stream, p);
+    if (d_p2p && backend == SPARSLA_BACKEND_CG) {  // halo of p0 through the transport once;
+        dist->exchange(stream, p);                    // later iterations push it in-kernel
         CK(cudaStreamWaitEvent(stream, dist->ev_halo, 0));
     }
     if (n == 0 && !dist) {  // empty system: converged with zero residual

@@ -95,17 +95,20 @@ void Solver::p2p_setup() {
     auto* mflag = dalloc_zero<unsigned long long>((size_t)8 * P);
     auto* hflag = dalloc_zero<unsigned long long>((size_t)4 * P);
     p2p_allocs = {mail, mflag, hflag};
-    void* mine[4] = {mail, mflag, hflag, p};
-    constexpr int W = 40;  // doubles per rank: pid, device, 4 pointers, 4 x 64-byte handles
+    // the SpMV inputs whose halos the kernels push: CG p; BiCGStab p-hat and s-hat
+    const bool bicg = backend == SPARSLA_BACKEND_BICGSTAB;
+    constexpr int NB = 5;
+    void* mine[NB] = {mail, mflag, hflag, bicg ? (void*)ph : (void*)p, bicg ? (void*)sh : (void*)p};
+    constexpr int W = 2 + NB + 8 * NB;  // doubles per rank: pid, device, pointers, 64-byte handles
     std::vector<double> blob(W, 0.0);
     blob[0] = (double)getpid();
     blob[1] = (double)A->device;
-    for (int i = 0; i < 4; ++i) std::memcpy(&blob[2 + i], &mine[i], 8);
+    for (int i = 0; i < NB; ++i) std::memcpy(&blob[2 + i], &mine[i], 8);
     std::string ipc_err;
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < NB; ++i) {
         cudaIpcMemHandle_t hd;
         const cudaError_t e = cudaIpcGetMemHandle(&hd, mine[i]);
-        if (e == cudaSuccess) std::memcpy(&blob[6 + 8 * i], &hd, 64);
+        if (e == cudaSuccess) std::memcpy(&blob[2 + NB + 8 * i], &hd, 64);
         else { ipc_err = cudaGetErrorString(e); cudaGetLastError(); }  // in-process peers do not need it
     }
     double* dblob = dalloc_zero<double>((size_t)W * (P + 1));
@@ -116,10 +119,10 @@ void Solver::p2p_setup() {
     CKD(cudaStreamSynchronize(s0));
     cudaFree(dblob);
     tr->allgathers -= 1;
-    std::vector<void*> peer[4];
+    std::vector<void*> peer[NB];
     for (int q = 0; q < P; ++q) {
         const double* bq = &all[(size_t)q * W];
-        for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < NB; ++i) {
             void* ptr = nullptr;
             if (q == me) {
                 ptr = mine[i];
@@ -136,7 +139,7 @@ void Solver::p2p_setup() {
                 }
             } else {
                 cudaIpcMemHandle_t hd;
-                std::memcpy(&hd, &bq[6 + 8 * i], 64);
+                std::memcpy(&hd, &bq[2 + NB + 8 * i], 64);
                 const cudaError_t e = cudaIpcOpenMemHandle(&ptr, hd, cudaIpcMemLazyEnablePeerAccess);
                 if (e != cudaSuccess) {
                     cudaGetLastError();
@@ -200,9 +203,13 @@ void Solver::p2p_setup() {
         p2p_allocs.push_back(dst);
         return dst;
     };
-    std::vector<double*> pv(nn);
+    std::vector<double*> pv(nn), pv2(nn);
     std::vector<int32_t> nr(nn);
-    for (size_t a = 0; a < nn; ++a) { pv[a] = static_cast<double*>(peer[3][C->nbr[a]]); nr[a] = C->nbr[a]; }
+    for (size_t a = 0; a < nn; ++a) {
+        pv[a] = static_cast<double*>(peer[3][C->nbr[a]]);
+        pv2[a] = static_cast<double*>(peer[4][C->nbr[a]]);
+        nr[a] = C->nbr[a];
+    }
     P2PCtx X{};
     X.P = P; X.me = me; X.nnbr = (int)nn;
     X.peer_mail = (double**)upload(peer[0].data(), P * sizeof(void*));
@@ -215,6 +222,7 @@ void Solver::p2p_setup() {
     X.push_nbr = (const int32_t*)upload(pnbr.data(), pnbr.size() * 4);
     X.push_pos = (const long long*)upload(ppos.data(), ppos.size() * 8);
     X.peer_vec = (double**)upload(pv.data(), nn * sizeof(void*));
+    X.peer_vec2 = (double**)upload(pv2.data(), nn * sizeof(void*));
     d_p2p = (P2PCtx*)upload(&X, sizeof(X));
 }
 

@@ -246,8 +246,10 @@ struct P2PCtx {
     const int32_t* push_row;           // local owned row
     const int32_t* push_nbr;           // neighbour index (0..nnbr-1)
     const long long* push_pos;         // element offset in that neighbour's vector
-    double** peer_vec;                 // [nnbr] -> neighbour's SpMV-input vector
+    double** peer_vec;                 // [nnbr] -> neighbour's SpMV-input vector (p / BiCGStab p-hat)
+    double** peer_vec2;                // [nnbr] -> neighbour's second SpMV input (BiCGStab s-hat)
 };
+
 
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
     unsigned long long v;
@@ -287,6 +289,18 @@ __device__ inline void p2p_consume(const P2PCtx* X, KState* S, int point, int k,
         t[j] = s;
     }
     apply_scalar(which, S, t);
+}
+
+// this CTA's chunk of boundary values of v straight into the neighbours' halo slots
+__device__ __forceinline__ void p2p_push_halo_chunk(const P2PCtx* X, long long chunk, const double* v,
+                                                    double* const* peers) {
+    for (int e = X->push_ptr[chunk] + threadIdx.x; e < X->push_ptr[chunk + 1]; e += blockDim.x)
+        peers[X->push_nbr[e]][X->push_pos[e]] = v[X->push_row[e]];
+}
+// last CTA of the producer: raise halo flag v on every neighbour (after a system fence)
+__device__ inline void p2p_raise_halo(const P2PCtx* X, KState* st, int v) {
+    const unsigned long long e = ++st->ep_halo[v];
+    for (int a = 0; a < X->nnbr; ++a) st_release_sys(X->peer_hflag[X->nbr_rank[a]] + v * X->P + X->me, e);
 }
 
 // wait until every neighbour has pushed this epoch's halo of vector v
@@ -1168,22 +1182,29 @@ __global__ void __launch_bounds__(kVecThreads) vec_kernel(VecParams P) {
     __shared__ KState s_loc;  // fused peer collectives: this CTA's copy of the scalar state
     const KState* sc = st;
     bool skip = false;
-    if constexpr (OP == V_CG_U1 || OP == V_CG_U2) {
+    constexpr bool CONSUMES = OP == V_CG_U1 || OP == V_CG_U2 || OP == V_BI_U1 || OP == V_BI_U2 || OP == V_BI_U3;
+    if constexpr (CONSUMES) {
         if (P.p2p) {
             if (threadIdx.x == 0) {
                 s_loc = *st;
-                p2p_consume(P.p2p, &s_loc, P.consume_point, P.consume_k, P.consume_scalar);
+                // BiCGStab U1 consumes the previous iteration's U3 totals (flagged in
+                // pending_x by that U3; there are none before the first iteration)
+                if (OP != V_BI_U1 || s_loc.pending_x) {
+                    p2p_consume(P.p2p, &s_loc, P.consume_point, P.consume_k, P.consume_scalar);
+                    if constexpr (OP == V_BI_U1) s_loc.pending_x = 0;
+                }
+                if constexpr (OP == V_BI_U3) s_loc.pending_x = !s_loc.done;  // its totals follow
             }
             __syncthreads();
             sc = &s_loc;
-            if constexpr (OP == V_CG_U1) skip = s_loc.done != 0;  // p^T A p breakdown
+            if constexpr (OP != V_CG_U2) skip = s_loc.done != 0;  // breakdown / convergence decided here
         }
     }
     VecScalars S;
     if constexpr (OP == V_CG_U1 || OP == V_BI_U2) S.alpha = sc->alpha;
     if constexpr (OP == V_CG_U2) { S.alpha = sc->alpha; S.beta = sc->beta; S.live = !sc->done; }
-    if constexpr (OP == V_BI_U1) { S.beta = st->beta; S.omega = st->omega; S.first = st->k == 0; }
-    if constexpr (OP == V_BI_U3) { S.alpha = st->alpha; S.omega = st->omega; S.half = st->halfstep; }
+    if constexpr (OP == V_BI_U1) { S.beta = sc->beta; S.omega = sc->omega; S.first = sc->k == 0; }
+    if constexpr (OP == V_BI_U3) { S.alpha = sc->alpha; S.omega = sc->omega; S.half = sc->halfstep; }
     const int t = threadIdx.x;
     __shared__ double sred[NA * (kVecThreads / 32)];
     __shared__ int s_flag;
@@ -1214,14 +1235,18 @@ __global__ void __launch_bounds__(kVecThreads) vec_kernel(VecParams P) {
             }
         }
     }
-    if constexpr (OP == V_CG_U2) {
-        // fused halo push: this chunk's boundary values of the new p go straight into the
-        // neighbours' halo slots (written above by this CTA; visible after the barrier)
-        if (P.p2p && S.live) {
+    if constexpr (OP == V_CG_U2 || OP == V_BI_U1 || OP == V_BI_U2) {
+        // fused halo push: this chunk's boundary values of the next SpMV input (p; p-hat;
+        // s-hat) go straight into the neighbours' halo slots (written above by this CTA,
+        // visible after the barrier)
+        bool push = P.p2p != nullptr;
+        if constexpr (OP == V_CG_U2) push = push && S.live;
+        else push = push && !skip;
+        if (push) {
             __syncthreads();
-            const P2PCtx* X = P.p2p;
-            for (int e = X->push_ptr[chunk] + t; e < X->push_ptr[chunk + 1]; e += kVecThreads)
-                X->peer_vec[X->push_nbr[e]][X->push_pos[e]] = P.p[X->push_row[e]];
+            if constexpr (OP == V_CG_U2) p2p_push_halo_chunk(P.p2p, chunk, P.p, P.p2p->peer_vec);
+            if constexpr (OP == V_BI_U1) p2p_push_halo_chunk(P.p2p, chunk, P.ph, P.p2p->peer_vec);
+            if constexpr (OP == V_BI_U2) p2p_push_halo_chunk(P.p2p, chunk, P.sh, P.p2p->peer_vec2);
         }
     }
     if constexpr (ND > 0) {
@@ -1243,6 +1268,22 @@ __global__ void __launch_bounds__(kVecThreads) vec_kernel(VecParams P) {
     }  // chunk loop
     if constexpr (ND > 0 && PERSIST) {
         ticket_and_finish<kVecThreads, ND, 0>(P.red, sred, &s_flag);
+    } else if constexpr (OP == V_BI_U1 || OP == V_BI_U2) {
+        // fused peer collectives: the last CTA publishes the consumed scalar state and
+        // raises this vector's halo flag once every CTA's peer stores are ordered before it
+        if (P.p2p) {
+            __syncthreads();
+            if (t == 0) {
+                __threadfence_system();
+                if (atomicAdd(P.red.ticket, 1u) == P.red.expected - 1) {
+                    __threadfence_system();
+                    *st = s_loc;
+                    if (!s_loc.done) p2p_raise_halo(P.p2p, st, OP == V_BI_U1 ? 0 : 1);
+                    *P.red.ticket = 0u;
+                    __threadfence();
+                }
+            }
+        }
     } else if constexpr (OP == V_CG_U2) {
         // the last CTA clears pending_x once every CTA has read it; with fused peer
         // collectives it also publishes this rank's scalar step and raises the halo flags
@@ -1255,12 +1296,7 @@ __global__ void __launch_bounds__(kVecThreads) vec_kernel(VecParams P) {
                     __threadfence_system();
                     *st = s_loc;
                     st->pending_x = 0;
-                    if (S.live) {
-                        const P2PCtx* X = P.p2p;
-                        const unsigned long long e = ++st->ep_halo[0];
-                        for (int a = 0; a < X->nnbr; ++a)
-                            st_release_sys(X->peer_hflag[X->nbr_rank[a]] + 0 * X->P + X->me, e);
-                    }
+                    if (S.live) p2p_raise_halo(P.p2p, st, 0);
                 } else {
                     st->pending_x = 0;
                 }

@@ -171,3 +171,35 @@ def test_dist_cg_fused_peer_collectives_bitwise(S, O, gpu, kind, p1, P, part):
     assert c["halo_exchanges"] == 2 * (1 + k) and c["all_reduces"] == 2 * (1 + 2 * k)
     # transport calls: only the setup / init ones, none per iteration
     assert c["raw_allgathers"] <= 2 * 2 and c["raw_exchanges"] <= 2 * 2
+
+
+@pytest.mark.parametrize("kind,p1,P,part,c", [("convdiff3d", 16, 2, "contig", 0.1), ("convdiff3d", 20, 4, "contig", 0.3),
+                                              ("fem2d", 40, 4, "rcb", 0.0), ("convdiff3d", 24, 3, "contig", 1.0)])
+def test_dist_bicgstab_fused_peer_collectives_bitwise(S, O, gpu, kind, p1, P, part, c):
+    """Fused mode for BiCGStab: the SpMVs push r-hat.v and t.t/t.s/s.s, U3 pushes rho/r.r,
+    U1 / U2 push the p-hat / s-hat halos straight into the neighbours' vectors, and each
+    consumer kernel sums the rank totals in rank order itself — bit-identical to the
+    transport path and to the oracle, with no transport call per iteration (including a
+    breakdown case: c = 1.0 hits |rho| < 1e-30 ||b||^2 like the oracle)."""
+    A = S.generate(kind, p1, 2601 if kind == "fem2d" else 0, c)
+    po = partition(S, kind, p1, A, P, part)
+    hub, plans, owned = make_plans(S, A, po, P)
+    for p in plans:
+        p.set_fused(True)
+        p.reset_counters()
+    b = np.ones(A.nrows)
+    opts = S.SolveOptions(atol=0.0, rtol=1e-8, max_iter=3000)
+    for rep_i in range(2):
+        res = S.run_ranks(P, lambda r: plans[r].bicgstab(b[owned[r]], opts))
+        xd = np.empty(A.nrows)
+        for r in range(P):
+            xd[owned[r]] = res[r][0]
+        xo, ro, co = O.dist_solve(Ocsr(O, A), b, po, P, kind="bicgstab", atol=0.0, rtol=1e-8, max_iter=3000)
+        reps = [res[r][1] for r in range(P)]
+        assert all(rp.iterations == reps[0].iterations and rp.converged == reps[0].converged for rp in reps)
+        assert reps[0].iterations == ro["iterations"] and reps[0].converged == ro["converged"], (reps[0], ro)
+        assert bits([reps[0].residual_norm])[0] == bits([ro["residual_norm"]])[0]
+        assert np.array_equal(bits(xd), bits(xo))
+    c0 = plans[0].counters()
+    # transport calls: only the setup / init ones, none per iteration
+    assert c0["raw_allgathers"] <= 2 * 2 and c0["raw_exchanges"] <= 2 * 2, c0

@@ -22,19 +22,20 @@ def _port():
     return p
 
 
-def _rank(rank, world, port, kind, p1, fused, outq):
+def _rank(rank, world, port, kind, p1, fused, outq, backend="cg", c=0.0):
     try:
         sys.path.insert(0, ROOT)
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
         import torch.distributed as dist
         from paper_2601_13994_b200 import bootstrap, sparsla as S
         dist.init_process_group("gloo", rank=rank, world_size=world)
-        rows, owned, n = bootstrap.local_rows(kind, p1, 0, 0.0, world, rank)
+        rows, owned, n = bootstrap.local_rows(kind, p1, 0, c, world, rank)
         T = S.torch_host_transport(world)
         plan = S.DistPlan.create_host(0, world, rank, T, rows, owned, None, n)
         plan.set_fused(fused)
-        x, rep = plan.cg(np.ones(len(owned)), S.SolveOptions(atol=0.0, rtol=1e-10, max_iter=5000))
-        x2, rep2 = plan.cg(np.ones(len(owned)), S.SolveOptions(atol=0.0, rtol=1e-10, max_iter=5000))
+        solve = plan.cg if backend == "cg" else plan.bicgstab
+        x, rep = solve(np.ones(len(owned)), S.SolveOptions(atol=0.0, rtol=1e-10, max_iter=5000))
+        x2, rep2 = solve(np.ones(len(owned)), S.SolveOptions(atol=0.0, rtol=1e-10, max_iter=5000))
         c = plan.counters()
         outq.put((rank, owned, x, rep.iterations, rep.residual_norm, np.array_equal(x, x2), c))
         dist.barrier()
@@ -72,4 +73,32 @@ def test_two_processes_one_gpu(O, gpu, fused):
             assert c["raw_exchanges"] <= 4 and c["raw_allgathers"] <= 4, c
         else:
             assert c["raw_exchanges"] >= 2 * ro["iterations"], c
+    assert np.array_equal(x.view(np.int64), xo.view(np.int64))
+
+
+def test_two_processes_one_gpu_bicgstab_fused(O, gpu):
+    """BiCGStab through cross-process fused peer collectives (p-hat / s-hat halo pushes and
+    three reduction points per iteration over cudaIpc memory)."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_rank, args=(r, 2, port, "convdiff3d", 20, True, q, "bicgstab", 0.3))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+    for r in res:
+        assert not isinstance(r[1], str), r[2]
+    A = O.generate("convdiff3d", 20, 0, 0.3)
+    b = np.ones(A.nrows)
+    xo, ro, _ = O.dist_solve(A, b, O.partition_contiguous(A.nrows, 2), 2, kind="bicgstab", atol=0.0,
+                             rtol=1e-10, max_iter=5000)
+    x = np.empty(A.nrows)
+    for rank, owned, xr, k, rn, same, c in res:
+        x[owned] = xr
+        assert k == ro["iterations"] and same
+        assert c["raw_exchanges"] <= 4 and c["raw_allgathers"] <= 4, c
     assert np.array_equal(x.view(np.int64), xo.view(np.int64))
