@@ -357,6 +357,8 @@ def main():
     ap.add_argument("--plain-steps", type=int, default=100, help="plain-CSR comparison run (0: skip)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dist", action="store_true", help="force the NCCL distributed path (also at N=1)")
+    ap.add_argument("--fused", action="store_true",
+                    help="N>1: fused peer-memory collectives inside the kernels instead of NCCL calls")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

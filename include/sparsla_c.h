@@ -292,6 +292,8 @@ int sparsla_dist_destroy(sparsla_dist* D);
 /* info[0]=n_owned [1]=n_halo [2]=neighbors [3]=interior chunks [4]=boundary chunks [5]=P
  * [6]=rank [7]=zero-copy halo segments [8]=n_global */
 int sparsla_dist_info(const sparsla_dist* D, int64_t* info);
+/* this rank's local-matrix storage format (same fields as sparsla_dcsr_format) */
+int sparsla_dist_format(sparsla_dist* D, int64_t* fmt);
 /* counters[0]=halo exchanges [1]=all_reduce points [2]=p2p messages performed by the live
  * algorithm (SPEC.md:524 accounting); [3..5] = raw transport calls of the same kinds (they
  * also include the no-op tail replayed after convergence).  6 entries. */

@@ -515,6 +515,17 @@ int sparsla_dist_info(const sparsla_dist* D, int64_t* info) {
     });
 }
 
+int sparsla_dist_format(sparsla_dist* D, int64_t* fmt) {
+    return guarded([&] {
+        DevCsr* A = D->A;
+        DeviceGuard g(A->device);
+        fmt[0] = A->vd ? 1 : 0;
+        fmt[1] = A->vd ? A->nvals : 0;
+        double v = 0.0;
+        fmt[2] = A->jacobi_uniform(&v) ? 1 : 0;
+    });
+}
+
 int sparsla_dist_set_fused(sparsla_dist* D, int32_t on) {
     return guarded([&] { D->ctx->p2p_enabled = on != 0; });
 }

@@ -927,6 +927,12 @@ class DistPlan:
     def reset_counters(self):
         _check(lib().sparsla_dist_reset_counters(self.h))
 
+    def format(self):
+        """This rank's local-matrix storage format (see DeviceCsr.format)."""
+        out = np.zeros(3, np.int64)
+        _check(lib().sparsla_dist_format(self.h, _p(out, _i64p)))
+        return {"value_dict": bool(out[0]), "distinct_values": int(out[1]), "uniform_diag": bool(out[2])}
+
     def set_fused(self, on: bool = True):
         """Fused peer-memory collectives for CG (no NCCL call per iteration)."""
         _check(lib().sparsla_dist_set_fused(self.h, C.c_int32(1 if on else 0)))
