@@ -147,7 +147,13 @@ static void configure_ws_variants(int device) {
 
 
 // ------------------------------------------------------------------ DevCsr ---------
+void DevCsr::drop_parked() noexcept {
+    std::lock_guard<std::mutex> lk(solver_mu);
+    for (auto*& p : parked) { delete p; p = nullptr; }
+}
+
 DevCsr::~DevCsr() {
+    drop_parked();
     DeviceGuard g(device, true);
     cudaFree(rp); cudaFree(ci); cudaFree(val); cudaFree(dinv); cudaFree(ones);
     cudaFree(vidx); cudaFree(vtab);
@@ -541,14 +547,18 @@ void launch_vec(cudaStream_t s, const VecParams& P0, RedParams red) {
 }
 
 // ------------------------------------------------------------------ Solver ---------
-Solver::Solver(DevCsr* A_, int backend_, const sparsla_solve_options& o, DistCtx* dist_)
-    : A(A_), backend(backend_), opts(o), dist(dist_) {
+void Solver::validate(const sparsla_solve_options& o, bool square) {
     if (!(o.atol >= 0.0) || !(o.rtol >= 0.0) || (o.atol == 0.0 && o.rtol == 0.0))
         fail(SPARSLA_ERR_INVALID_ARGUMENT, "SolveOptions: atol >= 0, rtol >= 0, not both zero (SPEC.md:129)");
     if (o.max_iter < 1) fail(SPARSLA_ERR_INVALID_ARGUMENT, "SolveOptions: max_iter >= 1");
     if (o.preconditioner != SPARSLA_PRECOND_NONE && o.preconditioner != SPARSLA_PRECOND_JACOBI)
         fail(SPARSLA_ERR_INVALID_ARGUMENT, "SolveOptions: unknown preconditioner");
-    if (!dist && A->nrows != A->ncols) fail(SPARSLA_ERR_DIMENSION, "Krylov solve requires a square matrix");
+    if (!square) fail(SPARSLA_ERR_DIMENSION, "Krylov solve requires a square matrix");
+}
+
+Solver::Solver(DevCsr* A_, int backend_, const sparsla_solve_options& o, DistCtx* dist_)
+    : A(A_), backend(backend_), opts(o), dist(dist_) {
+    validate(o, dist || A->nrows == A->ncols);
     DeviceGuard g(A->device);
     n = A->nrows;
     stream = A->stream;
@@ -974,21 +984,46 @@ void need(const void* p, const char* what) {
     if (!p) fail(SPARSLA_ERR_INVALID_ARGUMENT, std::string(what) + " is null");
 }
 
+bool solver_cache_on() {
+    static const bool on = [] { const char* e = getenv("SPARSLA_SOLVER_CACHE"); return !e || atoi(e) != 0; }();
+    return on;
+}
+
 int krylov(sparsla_dcsr* H, int backend, const double* b, double* x, const sparsla_solve_options* o,
            sparsla_solve_report* rep, int32_t mem) {
     return guarded([&] {
         need(H, "matrix"); need(o, "options"); need(rep, "report");
         DevCsr* A = H->A;
         DeviceGuard g(A->device);
-        Solver S(A, backend, *o);
-        S.set_b(b, mem);
-        if (mem == SPARSLA_MEM_DEVICE) S.x = x;
-        S.reset();
-        S.run();
-        S.report(rep);
+        // Host-buffer calls reuse the matrix's parked solver of this backend (workspace and
+        // captured graphs address only solver-owned vectors); device-buffer calls bind the
+        // caller's x into the graphs and get their own.
+        std::unique_ptr<Solver> S;
+        const bool cache = mem != SPARSLA_MEM_DEVICE && solver_cache_on();
+        if (cache) {
+            Solver::validate(*o, A->nrows == A->ncols);
+            std::lock_guard<std::mutex> lk(A->solver_mu);
+            Solver*& slot = A->parked[backend == SPARSLA_BACKEND_CG ? 0 : 1];
+            if (slot && slot->opts.preconditioner == o->preconditioner) {
+                S.reset(slot);
+                slot = nullptr;
+                S->opts = *o;  // tolerances / max_iter enter through reset() (KState)
+            }
+        }
+        if (!S) S = std::make_unique<Solver>(A, backend, *o);
+        S->set_b(b, mem);
+        if (mem == SPARSLA_MEM_DEVICE) S->x = x;
+        S->reset();
+        S->run();
+        S->report(rep);
         if (mem != SPARSLA_MEM_DEVICE && A->nrows)
-            CK(cudaMemcpyAsync(x, S.x, A->nrows * sizeof(double), cudaMemcpyDeviceToHost, A->stream));
+            CK(cudaMemcpyAsync(x, S->x, A->nrows * sizeof(double), cudaMemcpyDeviceToHost, A->stream));
         CK(cudaStreamSynchronize(A->stream));
+        if (cache) {
+            std::lock_guard<std::mutex> lk(A->solver_mu);
+            Solver*& slot = A->parked[backend == SPARSLA_BACKEND_CG ? 0 : 1];
+            if (!slot) slot = S.release();
+        }
     });
 }
 }  // namespace
@@ -1027,7 +1062,8 @@ int sparsla_dcsr_set_values(sparsla_dcsr* H, const double* vals, int32_t mem) {
         CK(cudaMemcpyAsync(A->val, vals, A->nnz * sizeof(double),
                            mem == SPARSLA_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, A->stream));
         CK(cudaStreamSynchronize(A->stream));
-        // value-dependent caches are invalid now
+        // value-dependent caches are invalid now (parked solvers hold the old diagonal)
+        A->drop_parked();
         // value dictionary: rebuilt from host values (the scan stops at the 257th distinct
         // value); device values are only downloaded when the matrix had a dictionary
         if (A->ws_var == 0 && !A->has_hub && (mem != SPARSLA_MEM_DEVICE || A->vd)) {

@@ -51,6 +51,11 @@ struct DevCsr {
     DevCsr* transpose = nullptr;
     cudaStream_t stream = nullptr;
     std::mutex lazy_mu;  // guards the lazily built caches (dinv, ones, symmetry, transpose)
+    // one parked host-buffer Krylov solver per backend (workspace + captured graphs), reused
+    // by the next cg_solve / bicgstab_solve call with host buffers (SPARSLA_SOLVER_CACHE=0: off)
+    std::mutex solver_mu;
+    struct Solver* parked[2] = {nullptr, nullptr};
+    void drop_parked() noexcept;
 
     template <class I>
     static DevCsr* create(int device, long long nrows, long long ncols, const I* rp, const I* ci,
@@ -103,6 +108,7 @@ struct DistCtx {
 // Jacobi-PCG / BiCGStab solver with device-resident state and graph-captured iterations.
 struct Solver {
     static constexpr int kGraphIters = 16;
+    static void validate(const sparsla_solve_options& o, bool square);
     DevCsr* A;
     int backend;
     sparsla_solve_options opts;

@@ -346,3 +346,32 @@ def test_value_dictionary_limits_and_signed_zero(S, O, gpu, nvals):
     x = np.random.default_rng(nvals).standard_normal(A.ncols)
     x[::7] = -x[::7]
     assert_bitwise(S.spmv(D, x), O.spmv(B, x), f"{nvals} values")
+
+
+def test_parked_solver_reuse_bitwise(S, O, gpu, monkeypatch):
+    """Host-buffer solves on one matrix handle reuse its parked solver (workspace + graphs):
+    different tolerances, right-hand sides and backends, then new values — every result is
+    bit-identical to a fresh solver (SPARSLA_SOLVER_CACHE=0) and to the oracle."""
+    A = O.generate("convdiff3d", 18, 0, 0.2)
+    D = to_S(S, A).device(0)
+    rng = np.random.default_rng(3)
+    runs = [("bicgstab", 1e-6), ("bicgstab", 1e-10), ("cg", 1e-8), ("bicgstab", 1e-8)]
+    out = []
+    for be, rtol in runs:
+        b = rng.standard_normal(A.nrows)
+        fn = S.cg_solve if be == "cg" else S.bicgstab_solve
+        x, r = fn(D, b, S.SolveOptions(atol=0.0, rtol=rtol, max_iter=3000))
+        out.append((be, rtol, b, x, r))
+    v2 = np.where(A.vals > 0, A.vals * 1.5, A.vals)
+    S.lib().sparsla_dcsr_set_values(D.h, v2.ctypes.data_as(S._f64p), 0)
+    b = rng.standard_normal(A.nrows)
+    x2, r2 = S.bicgstab_solve(D, b, S.SolveOptions(atol=0.0, rtol=1e-9, max_iter=3000))
+    out.append(("bicgstab", 1e-9, b, x2, r2, v2))
+    monkeypatch.setenv("SPARSLA_SOLVER_CACHE", "0")
+    for item in out:
+        be, rtol, b, x, r = item[:5]
+        vals = item[5] if len(item) > 5 else A.vals
+        Ao = O.Csr(A.nrows, A.ncols, A.row_ptr, A.col_idx, vals)
+        xo, ro = (O.cg if be == "cg" else O.bicgstab)(Ao, b, atol=0.0, rtol=rtol, max_iter=3000)
+        assert r.iterations == ro["iterations"], (be, rtol)
+        assert_bitwise(x, xo, f"{be} rtol={rtol}")
