@@ -11,12 +11,13 @@
 // row (144 B at m = 6) is contiguous, so the SpMM gathers S[col] as whole 16-byte lines.
 //
 // Per LOBPCG iteration (m = k block vectors):
-//   resid_kernel   R = AX - X diag(lambda), ||R_j||, W = |D|^-1 R         1 pass
+//   (R = AX - X diag(lambda), ||R_j||, W = |D|^-1 R come out of the previous RR update)
 //   W: twice { Y = X^T W (gram), W -= X Y (combine), SVQB(W) }           orthonormal W
 //   P: twice { Y = [X W]^T P, P -= [X W] Y, SVQB(P) }                    orthonormal P
 //   spmm_kernel    AS[:, W P] = A S[:, W P]                               1 SpMM of <= 2m columns
 //   gram           G = S_B^T AS_B, B = X u W u P (q <= 3m)               host: eig(G)
-//   combine        X' = S_B C, AX' = AS_B C, P' = S_{W,P} C_{W,P}        (Hetmaniuk-Lehoucq P)
+//   rr_apply       X' = S_B C, AX' = AS_B C, P' = S_{W,P} C_{W,P}        (Hetmaniuk-Lehoucq P)
+//                  + R' = AX' - X' Lambda', ||R'_j||, W' = |D|^-1 R'      1 fused pass
 // Reductions use a fixed grid (kRedCTAs) and fixed in-CTA orders, so a run is
 // deterministic.  Parity is tolerance-based (eigenvalues to 1e-8 against
 // a dense symmetric eigensolver) — there is no bitwise reference for this module.
@@ -379,7 +380,9 @@ __global__ void __launch_bounds__(kTRa) apply_kernel(double* S, int ld, Cols in,
 constexpr int kRRStages = 2;
 template <int TR>
 __global__ void __launch_bounds__(TR) rr_apply_kernel(const double* S, const double* AS, double* Sn, double* ASn,
-                                                      int ld, Cols B, int m, long long n, const Mat C) {
+                                                      int ld, Cols B, int m, long long n, const Mat C,
+                                                      const Vec16 lam, const double* __restrict__ dinv,
+                                                      double* rpart) {
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
     int* s_b = reinterpret_cast<int*>(smem + 64);
@@ -391,6 +394,9 @@ __global__ void __launch_bounds__(TR) rr_apply_kernel(const double* S, const dou
     stage_cols(B, s_b);
     const TileWalk<TR> W(n, ld);
     const int row = threadIdx.x;
+    double racc[kMaxK];  // ||R_k||^2 over this thread's rows
+#pragma unroll
+    for (int k = 0; k < kMaxK; ++k) racc[k] = 0.0;
     if (row == 0) {
         for (int s = 0; s < kRRStages; ++s) mbar_init(&bar[s], 1);
         fence_mbar_init();
@@ -437,9 +443,18 @@ __global__ void __launch_bounds__(TR) rr_apply_kernel(const double* S, const dou
                         xa[k] = fma(v, C.v[l * m + k], xa[k]);
                     }
             }
+            // fused residual of the new Ritz pairs: R = AX' - X' diag(lambda), its norms, and
+            // the Jacobi-preconditioned W = |D|^-1 R for the next iteration (W slot)
+            const double d = dinv ? fabs(__ldg(dinv + W.row0(j) + row)) : 1.0;
 #pragma unroll
             for (int k = 0; k < kMaxK; ++k)
-                if (k < m) { outS[row * ld + k] = xs[k]; outA[row * ld + k] = xa[k]; }
+                if (k < m) {
+                    outS[row * ld + k] = xs[k];
+                    outA[row * ld + k] = xa[k];
+                    const double r = fma(-lam.v[k], xs[k], xa[k]);
+                    racc[k] = fma(r, r, racc[k]);
+                    outS[row * ld + m + k] = d * r;
+                }
         }
         fence_proxy_async_smem();
         __syncthreads();
@@ -450,6 +465,23 @@ __global__ void __launch_bounds__(TR) rr_apply_kernel(const double* S, const dou
             bulk_commit();
             if (j + kRRStages < W.mine) W.issue(j + kRRStages, s, bar, ring + s * 2 * te, S, AS);
         }
+    }
+    // per-CTA residual partials: warp trees, then warps in order
+    __shared__ double rred[TR / 32][kMaxK];
+    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < kMaxK; ++k) {
+        if (k >= m) break;
+        double v = racc[k];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+        if (lane == 0) rred[wp][k] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < m) {
+        double v = 0.0;
+        for (int q2 = 0; q2 < TR / 32; ++q2) v += rred[q2][threadIdx.x];
+        rpart[(size_t)blockIdx.x * m + threadIdx.x] = v;
     }
     if (row == 0) bulk_wait_all();
 }
@@ -873,8 +905,9 @@ struct Lobpcg {
     }
 
     // Rayleigh-Ritz on the orthonormal basis S_B, B = [X | Z] (AS_B = A S_B): one Gram launch
-    // and one fused update launch writing X', AX', P' into Sn / ASn, then swap.
-    void rayleigh_ritz(const Cols& B, std::vector<double>& lam) {
+    // and one fused update launch writing X', AX', P' into Sn / ASn — plus the new pairs'
+    // residual norms and W = |D|^-1 (AX' - X' Lambda) for the next iteration — then swap.
+    void rayleigh_ritz(const Cols& B, std::vector<double>& lam, const double* dinv, std::vector<double>& res) {
         const int q = B.n;
         std::vector<double> G = gram(S, B, AS, B);
         for (int i = 0; i < q; ++i)
@@ -888,12 +921,23 @@ struct Lobpcg {
         std::memset(&C, 0, sizeof(C));
         for (int i = 0; i < q; ++i)
             for (int j = 0; j < m; ++j) C.v[i * m + j] = U[(size_t)i * q + j];
+        Vec16 L{};
+        for (int j = 0; j < m; ++j) L.v[j] = th[j];
+        res.assign(m, 0.0);
         if (n > 0) {
-            if (rr_rows(ld) == 128)
-                rr_apply_kernel<128><<<tile_grid(), 128, rr_apply_smem(ld), s>>>(S, AS, Sn, ASn, ld, B, m, n, C);
+            const int tr = rr_rows(ld);
+            const unsigned g = (unsigned)std::max<long long>(1, std::min<long long>((n + tr - 1) / tr, 4LL * 148));
+            if (tr == 128)
+                rr_apply_kernel<128><<<g, 128, rr_apply_smem(ld), s>>>(S, AS, Sn, ASn, ld, B, m, n, C, L, dinv, partial);
             else
-                rr_apply_kernel<64><<<tile_grid(), 64, rr_apply_smem(ld), s>>>(S, AS, Sn, ASn, ld, B, m, n, C);
+                rr_apply_kernel<64><<<g, 64, rr_apply_smem(ld), s>>>(S, AS, Sn, ASn, ld, B, m, n, C, L, dinv, partial);
             CK(cudaGetLastError());
+            std::vector<double> h((size_t)g * m);
+            CK(cudaMemcpyAsync(h.data(), partial, h.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            for (unsigned p = 0; p < g; ++p)
+                for (int j = 0; j < m; ++j) res[j] += h[(size_t)p * m + j];
+            for (auto& v : res) v = std::sqrt(v);
         }
         std::swap(S, Sn);
         std::swap(AS, ASn);
@@ -1005,13 +1049,11 @@ void eig_smallest(DevCsr* A, int k, double tol, long long max_iter, uint64_t see
     CK(cudaGetLastError());
     if (L.ortho(Cols{}, Xc).n < m) fail(SPARSLA_ERR_INTERNAL, "eig_smallest: initial block is rank deficient");
     L.spmm(L.S, Xc, L.AS);
-    std::vector<double> lam;
-    L.rayleigh_ritz(Xc, lam);
+    std::vector<double> lam, res;
+    L.rayleigh_ritz(Xc, lam, dinv, res);  // also ||R_j|| and W = |D|^-1 R into the W slot
     bool have_p = false;
     long long it = 0;
-    std::vector<double> res;
     for (;; ++it) {
-        res = L.resid(lam, dinv);  // also W = |D|^-1 R into the W slot
         Cols Z;
         for (int j = 0; j < m; ++j)  // soft locking: only unconverged pairs add directions
             if (!(res[j] <= tol)) Z.c[Z.n++] = (unsigned char)(m + j);
@@ -1022,7 +1064,7 @@ void eig_smallest(DevCsr* A, int k, double tol, long long max_iter, uint64_t see
         }
         Z = L.ortho(Xc, Z);
         L.spmm(L.S, Z, L.AS);
-        L.rayleigh_ritz(cols_cat(Xc, Z), lam);
+        L.rayleigh_ritz(cols_cat(Xc, Z), lam, dinv, res);
         have_p = Z.n > 0;
         if (Z.n == 0) break;  // no new directions: the block cannot improve
     }
