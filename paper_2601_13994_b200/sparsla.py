@@ -537,14 +537,14 @@ def eig_smallest(a, k: int, tol: float = 1e-8, max_iter: int = 10000, seed: int 
     the partial result with per-pair flags."""
     if isinstance(a, SparseCoo):
         a = CsrMatrix.from_coo(a)
-    D = _dev_of(a)
     pc = {"none": PRECOND_NONE, "jacobi": PRECOND_JACOBI}.get(preconditioner)
     if pc is None:
         raise InvalidArgumentError(f"unknown preconditioner {preconditioner!r}")
     k = int(k)
-    n = D.nrows
+    n = a.nrows
     if k < 1 or k > max(n, 0):
         raise InvalidArgumentError("eig_smallest: need 1 <= k <= n")
+    D = _dev_of(a)
     lam = np.empty(k)
     V = np.empty((n, k))
     res = np.empty(k)
@@ -566,17 +566,17 @@ def eig_backward(result: EigenResult, a_pattern, grad_lambdas) -> np.ndarray:
     pairs converged and simple eigenvalues (gap > 1e-8), else raises."""
     if isinstance(a_pattern, SparseCoo):
         a_pattern = CsrMatrix.from_coo(a_pattern)
-    D = _dev_of(a_pattern)
     lam = _f64(result.lambdas)
     k = len(lam)
     g = _f64(grad_lambdas)
     if len(g) != k:
         raise DimensionError(f"grad_lambdas has length {len(g)}, expected {k}")
     V = _f64(result.vectors)
-    if V.shape != (D.nrows, k):
-        raise DimensionError(f"vectors shape {V.shape}, expected {(D.nrows, k)}")
+    if V.shape != (a_pattern.nrows, k):
+        raise DimensionError(f"vectors shape {V.shape}, expected {(a_pattern.nrows, k)}")
     if not bool(np.all(result.report.pair_converged)):
         raise InvalidArgumentError("eig_backward: not all eigenpairs converged")
+    D = _dev_of(a_pattern)
     gv = np.empty(D.nnz)
     _check(lib().sparsla_eig_backward(D.h, C.c_int64(k), _p(lam, _f64p), _p(V, _f64p), _p(g, _f64p),
                                       _p(gv, _f64p), C.c_int32(MEM_HOST)))

@@ -202,6 +202,25 @@ def test_device_calls_fail_loudly_without_gpu(S):
         S.cg_solve(A, b)
     with pytest.raises(S.Error, match="no CUDA device"):
         S.spmv(A, b)
+    with pytest.raises(S.Error, match="no CUDA device"):
+        S.eig_smallest(A, 2)
+    with pytest.raises(S.InvalidArgumentError):
+        S.eig_smallest(A, 0)  # argument checks come first
+
+
+def test_eig_backward_argument_checks(S):
+    """eig_backward validates shapes and convergence flags before any device work."""
+    A, _ = S.poisson2d(4)
+    n = A.nrows
+    rep = S.EigenReport(iterations=1, residual_norms=np.zeros(2), pair_converged=np.array([True, False]))
+    res = S.EigenResult(np.array([1.0, 2.0]), np.zeros((n, 2)), rep)
+    with pytest.raises(S.DimensionError):
+        S.eig_backward(res, A, [1.0])
+    with pytest.raises(S.InvalidArgumentError):
+        S.eig_backward(res, A, [1.0, 1.0])
+    bad = S.EigenResult(np.array([1.0, 2.0]), np.zeros((n + 1, 2)), rep)
+    with pytest.raises(S.DimensionError):
+        S.eig_backward(bad, A, [1.0, 1.0])
 
 
 def test_options_validation(S):
