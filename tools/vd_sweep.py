@@ -18,7 +18,7 @@ sv = S.Solver(D, np.ones(n), "cg", S.SolveOptions(atol=0.0, rtol=1e-30, max_iter
 sv.iterate(3)
 ms = sv.kernel_times(20)
 fmt = D.format()
-b = ((1 if fmt["value_dict"] else 8) + (1 if fmt["col_dict"] else 4)) * nnz + 20 * n + 4
+b = ((1 if fmt["value_dict"] else 8) + (1 if fmt.get("col_dict") else 4)) * nnz + 20 * n + 4
 print(json.dumps({"spmv_ms": ms[0], "stored_gbs": b / ms[0] / 1e6, "csr_equiv_gbs": (12 * nnz + 20 * n + 4) / ms[0] / 1e6,
                   "u1_ms": ms[1], "u2_ms": ms[2], "fmt": fmt}))
 '''
