@@ -687,6 +687,10 @@ __global__ void __launch_bounds__(kWsThreads, MINB) spmv_ws_kernel(SpmvParams P)
                 const int32_t* cp = reinterpret_cast<const int32_t*>(A + L.vbytes) + (kb - (o0 & ~3));
                 const uint8_t* vp = A + (kb - (o0 & ~(VALIGN - 1)));
                 double y = 0.0;
+                double eop = 0.0;
+                if constexpr (MODE == SPMV_BICG_V || MODE == SPMV_BICG_T) {
+                    if (!__all_sync(0xffffffffu, len <= W)) eop = live ? __ldg(P.aux + row) : 0.0;
+                }
                 if (__all_sync(0xffffffffu, len <= W)) {
                     // issue every gather straight from the staged columns; the stage is
                     // released once the gathers are in flight (their addresses consumed)
@@ -697,6 +701,9 @@ __global__ void __launch_bounds__(kWsThreads, MINB) spmv_ws_kernel(SpmvParams P)
 #pragma unroll
                     for (int u = 0; u < W; ++u)
                         if (u < len) { xv[u] = __ldg(P.x + cp[u]); vi[u / 4] |= (uint32_t)vp[u] << (8 * (u % 4)); }
+                    // BiCGStab epilogues stream a second vector (r-hat / s): its load joins the
+                    // gathers instead of adding a dependent DRAM round trip at the end
+                    if constexpr (MODE == SPMV_BICG_V || MODE == SPMV_BICG_T) eop = live ? __ldg(P.aux + row) : 0.0;
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&empty[s]);
 #pragma unroll
@@ -715,7 +722,18 @@ __global__ void __launch_bounds__(kWsThreads, MINB) spmv_ws_kernel(SpmvParams P)
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&empty[s]);
                 }
-                if (live) { P.y[row] = y; spmv_epilogue<MODE>(P, row, y, acc); }
+                if (live) {
+                    P.y[row] = y;
+                    if constexpr (MODE == SPMV_BICG_V) {
+                        acc[0] = __dadd_rn(acc[0], __dmul_rn(eop, y));
+                    } else if constexpr (MODE == SPMV_BICG_T) {
+                        acc[0] = __dadd_rn(acc[0], __dmul_rn(y, y));
+                        acc[1] = __dadd_rn(acc[1], __dmul_rn(y, eop));
+                        acc[2] = __dadd_rn(acc[2], __dmul_rn(eop, eop));
+                    } else {
+                        spmv_epilogue<MODE>(P, row, y, acc);
+                    }
+                }
                 if (++s == STG) { s = 0; ph ^= 1u; }
             }
             if constexpr (ND > 0) {
