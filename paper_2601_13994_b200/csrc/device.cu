@@ -532,7 +532,11 @@ void launch_vec(cudaStream_t s, const VecParams& P0, RedParams red) {
     P.red.nchunks = nchunks_of(P.n);
     P.red.expected = (unsigned)P.red.nchunks;
     const unsigned grid = (unsigned)nchunks_of(P.n);
-    if (vec_persist()) {
+    // fused peer collectives with every peer on another GPU: a resident grid, so the per-CTA
+    // consume of the reduction point and the system-scope fences run once per CTA slot, not
+    // once per 2048-row chunk.  (With a peer rank on the same GPU a resident grid spinning on
+    // its flags could keep that peer's producer kernel off the SMs.)
+    if (vec_persist() || P.resident) {
         int dev = 0, per_sm = 0, sms = 0;
         CK(cudaGetDevice(&dev));
         CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -690,6 +694,7 @@ void Solver::vec_point(int scalar, int slot, int check_done) {
         // BiCGStab: U1 <- previous U3's rho/r.r, U2 <- rhat.v, U3 <- t.t/t.s/s.s); kernels
         // with dot products push their own totals as point `slot`
         P.p2p = d_p2p;
+        P.resident = dist->p2p_shared_device ? 0 : 1;
         switch (OP) {
             case V_CG_U1: P.consume_point = 1; P.consume_scalar = SC_CG_PQ; P.consume_k = 1; break;
             case V_CG_U2: P.consume_point = 2; P.consume_scalar = SC_CG_RR; P.consume_k = 2; break;

@@ -99,7 +99,8 @@ struct DistCtx {
     double* red_all = nullptr;   // [8 points][P][8]
     cudaStream_t comm = nullptr;
     cudaEvent_t ev_x = nullptr, ev_halo = nullptr;
-    bool p2p_enabled = false;     // fused peer-memory collectives for CG (sparsla_dist_set_fused)
+    bool p2p_enabled = false;     // fused peer-memory collectives (sparsla_dist_set_fused)
+    bool p2p_shared_device = false;  // a peer rank runs on this GPU: its kernels compete for the SMs
     int32_t* d_all_chunks = nullptr;  // [interior | boundary] for the single fused-mode launch
     void exchange(cudaStream_t s, double* x);  // halo of x ([owned|halo]) -> ev_halo
     ~DistCtx();

@@ -120,8 +120,12 @@ void Solver::p2p_setup() {
     cudaFree(dblob);
     tr->allgathers -= 1;
     std::vector<void*> peer[NB];
+    C->p2p_shared_device = false;
     for (int q = 0; q < P; ++q) {
         const double* bq = &all[(size_t)q * W];
+        // same ordinal = same GPU for in-process peers; processes with different
+        // CUDA_VISIBLE_DEVICES mappings are treated conservatively the same way
+        if (q != me && (int)bq[1] == A->device) C->p2p_shared_device = true;
         for (int i = 0; i < NB; ++i) {
             void* ptr = nullptr;
             if (q == me) {

@@ -1058,6 +1058,7 @@ struct VecParams {
     // (scalar op consume_scalar over consume_k totals) at entry; CG_U2 also pushes the halo
     const P2PCtx* p2p;
     int consume_point, consume_scalar, consume_k;
+    int resident;  // host: launch a resident (persistent) grid
 };
 
 __device__ __forceinline__ double2 ld2(const double* p, long long i, long long n) {
@@ -1285,7 +1286,9 @@ __global__ void __launch_bounds__(kVecThreads) vec_kernel(VecParams P) {
     }
     }  // chunk loop
     if constexpr (ND > 0 && PERSIST) {
-        ticket_and_finish<kVecThreads, ND, 0>(P.red, sred, &s_flag);
+        RedParams R = P.red;
+        if (P.p2p) { R.p2p = P.p2p; R.s_loc = &s_loc; }
+        ticket_and_finish<kVecThreads, ND, 0>(R, sred, &s_flag);
     } else if constexpr (OP == V_BI_U1 || OP == V_BI_U2) {
         // fused peer collectives: the last CTA publishes the consumed scalar state and
         // raises this vector's halo flag once every CTA's peer stores are ordered before it
