@@ -704,6 +704,7 @@ __global__ void __launch_bounds__(kWsThreads, MINB) spmv_ws_kernel(SpmvParams P)
                     // BiCGStab epilogues stream a second vector (r-hat / s): its load joins the
                     // gathers instead of adding a dependent DRAM round trip at the end
                     if constexpr (MODE == SPMV_BICG_V || MODE == SPMV_BICG_T) eop = live ? __ldg(P.aux + row) : 0.0;
+                    if constexpr (MODE == SPMV_CG) eop = live ? __ldg(P.x + row) : 0.0;
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&empty[s]);
 #pragma unroll
@@ -724,7 +725,9 @@ __global__ void __launch_bounds__(kWsThreads, MINB) spmv_ws_kernel(SpmvParams P)
                 }
                 if (live) {
                     P.y[row] = y;
-                    if constexpr (MODE == SPMV_BICG_V) {
+                    if constexpr (MODE == SPMV_CG) {
+                        acc[0] = __dadd_rn(acc[0], __dmul_rn(__all_sync(0xffffffffu, len <= W) ? eop : __ldg(P.x + row), y));
+                    } else if constexpr (MODE == SPMV_BICG_V) {
                         acc[0] = __dadd_rn(acc[0], __dmul_rn(eop, y));
                     } else if constexpr (MODE == SPMV_BICG_T) {
                         acc[0] = __dadd_rn(acc[0], __dmul_rn(y, y));
