@@ -79,6 +79,13 @@ int sparsla_version(void); /* major*10000 + minor*100 + patch */
 int sparsla_coo_canonicalize(int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* rows,
                              const int64_t* cols, const double* vals, int64_t* out_nnz,
                              int64_t* rows_out, int64_t* cols_out, double* vals_out);
+/* The same canonicalization on a GPU (radix sort of (row*ncols + col, input position), duplicate
+ * sums in input order): bit-identical outputs and errors; nnz < 2^31; `mem` selects host or
+ * device pointers for inputs and outputs alike. */
+int sparsla_coo_canonicalize_device(int device, int64_t nrows, int64_t ncols, int64_t nnz,
+                                    const int64_t* rows, const int64_t* cols, const double* vals,
+                                    int32_t mem, int64_t* out_nnz, int64_t* rows_out,
+                                    int64_t* cols_out, double* vals_out);
 /* CsrMatrix::from_coo (sparse.hpp:84, sparse.cpp:94-116), input must be canonical. */
 int sparsla_csr_from_coo(int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* rows,
                          const int64_t* cols, const double* vals, int64_t* row_ptr,

@@ -1,0 +1,171 @@
+// coo_device.cu — SparseCoo canonicalization on the GPU (
+// reference sparse.cpp:9-53): bounds check, stable order by (row, col), duplicates summed in
+// input order, explicit zeros kept.  The reference sorts a permutation with a two-key
+// comparator on one core (12.2 s at 117M entries, SURVEY probe P1); here the keys
+// row * ncols + col are radix-sorted with their input positions (LSD radix sort is stable,
+// so equal keys keep their input order), segment heads are flagged and scanned, and one
+// thread per output entry sums its duplicates left to right — the reference's
+// vals_.back() += vals[p] order, so the result is bit-identical to the host path.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <string>
+
+#include "common.hpp"
+#include "device.hpp"
+
+namespace sparsla_b200 {
+namespace {
+
+#define CK(x) cuda_check((x), #x)
+
+template <class T>
+struct DBuf {  // device buffer owned for the duration of a call
+    T* p = nullptr;
+    explicit DBuf(size_t n) { CK(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T))); }
+    ~DBuf() { cudaFree(p); }
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+};
+
+// first entry (in input order) outside the shape -> bad[0] (atomicMin)
+__global__ void coo_bounds_kernel(const int64_t* rows, const int64_t* cols, long long nnz, int64_t nrows,
+                                  int64_t ncols, unsigned long long* bad) {
+    const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= nnz) return;
+    const int64_t r = rows[k], c = cols[k];
+    if (r < 0 || r >= nrows || c < 0 || c >= ncols) atomicMin(bad, (unsigned long long)k);
+}
+
+__global__ void coo_keys_kernel(const int64_t* rows, const int64_t* cols, long long nnz, int64_t ncols,
+                                unsigned long long* keys, int32_t* idx) {
+    const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= nnz) return;
+    keys[k] = (unsigned long long)rows[k] * (unsigned long long)ncols + (unsigned long long)cols[k];
+    idx[k] = (int32_t)k;
+}
+
+__global__ void coo_heads_kernel(const unsigned long long* keys, long long nnz, int32_t* head) {
+    const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= nnz) return;
+    head[k] = (k == 0 || keys[k] != keys[k - 1]) ? 1 : 0;
+}
+
+// one thread per segment head: output entry seg[k] - 1 = (row, col, sum of its duplicates
+// in sorted = input order)
+__global__ void coo_emit_kernel(const unsigned long long* keys, const int32_t* idx, const int32_t* seg,
+                                const double* vals, long long nnz, int64_t ncols, int64_t* ro, int64_t* co,
+                                double* vo) {
+    const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= nnz) return;
+    const unsigned long long key = keys[k];
+    if (k > 0 && keys[k - 1] == key) return;
+    double s = vals[idx[k]];
+    for (long long j = k + 1; j < nnz && keys[j] == key; ++j) s = __dadd_rn(s, vals[idx[j]]);
+    const long long o = (long long)seg[k] - 1;
+    ro[o] = (int64_t)(key / (unsigned long long)ncols);
+    co[o] = (int64_t)(key % (unsigned long long)ncols);
+    vo[o] = s;
+}
+
+int key_bits(unsigned long long maxkey) {
+    int b = 1;
+    while (b < 64 && (maxkey >> b) != 0) ++b;
+    return b;
+}
+
+}  // namespace
+}  // namespace sparsla_b200
+
+using namespace sparsla_b200;
+
+extern "C" int sparsla_coo_canonicalize_device(int device, int64_t nrows, int64_t ncols, int64_t nnz,
+                                               const int64_t* rows, const int64_t* cols, const double* vals,
+                                               int32_t mem, int64_t* out_nnz, int64_t* rows_out,
+                                               int64_t* cols_out, double* vals_out) {
+    return guarded([&] {
+        if (nrows < 0 || ncols < 0) fail(SPARSLA_ERR_DIMENSION, "negative matrix shape");
+        if (nnz < 0) fail(SPARSLA_ERR_DIMENSION, "negative nnz");
+        if (nnz >= (1LL << 31)) fail(SPARSLA_ERR_UNSUPPORTED, "device canonicalization: nnz must be < 2^31");
+        if (mem != SPARSLA_MEM_HOST && mem != SPARSLA_MEM_DEVICE) fail(SPARSLA_ERR_INVALID_ARGUMENT, "bad mem");
+        if (!out_nnz) fail(SPARSLA_ERR_INVALID_ARGUMENT, "out_nnz is null");
+        if (nrows > 0 && ncols > 0 && (unsigned long long)nrows > ~0ULL / (unsigned long long)ncols)
+            fail(SPARSLA_ERR_UNSUPPORTED, "device canonicalization: nrows * ncols must fit 64 bits");
+        DeviceGuard g(device);
+        *out_nnz = 0;
+        if (nnz == 0) return;
+        cudaStream_t s = nullptr;
+        CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        struct StreamGuard { cudaStream_t s; ~StreamGuard() { cudaStreamDestroy(s); } } sg{s};
+        const size_t n = (size_t)nnz;
+        const unsigned grid = (unsigned)((nnz + 255) / 256);
+        // inputs on the device
+        const int64_t *dr = rows, *dc = cols;
+        const double* dv = vals;
+        DBuf<int64_t> hr(mem == SPARSLA_MEM_HOST ? n : 0), hc(mem == SPARSLA_MEM_HOST ? n : 0);
+        DBuf<double> hv(mem == SPARSLA_MEM_HOST ? n : 0);
+        if (mem == SPARSLA_MEM_HOST) {
+            CK(cudaMemcpyAsync(hr.p, rows, n * 8, cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(hc.p, cols, n * 8, cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(hv.p, vals, n * 8, cudaMemcpyHostToDevice, s));
+            dr = hr.p; dc = hc.p; dv = hv.p;
+        }
+        // bounds (the first offending entry in input order, as the host path reports it)
+        DBuf<unsigned long long> bad(1);
+        const unsigned long long none = ~0ULL;
+        CK(cudaMemcpyAsync(bad.p, &none, 8, cudaMemcpyHostToDevice, s));
+        coo_bounds_kernel<<<grid, 256, 0, s>>>(dr, dc, nnz, nrows, ncols, bad.p);
+        CK(cudaGetLastError());
+        unsigned long long hb = 0;
+        CK(cudaMemcpyAsync(&hb, bad.p, 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (hb != none) {
+            int64_t r = 0, c = 0;
+            CK(cudaMemcpy(&r, dr + hb, 8, mem == SPARSLA_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDefault));
+            CK(cudaMemcpy(&c, dc + hb, 8, mem == SPARSLA_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDefault));
+            fail(SPARSLA_ERR_BOUNDS, "coo index (" + std::to_string(r) + ", " + std::to_string(c) + ") outside shape (" +
+                                         std::to_string(nrows) + ", " + std::to_string(ncols) + ") at entry " +
+                                         std::to_string(hb));
+        }
+        // stable radix sort of (key, input position)
+        DBuf<unsigned long long> k0(n), k1(n);
+        DBuf<int32_t> i0(n), i1(n);
+        coo_keys_kernel<<<grid, 256, 0, s>>>(dr, dc, nnz, ncols, k0.p, i0.p);
+        CK(cudaGetLastError());
+        const int bits = key_bits((unsigned long long)(nrows > 0 ? nrows : 1) * (unsigned long long)(ncols > 0 ? ncols : 1));
+        cub::DoubleBuffer<unsigned long long> kb(k0.p, k1.p);
+        cub::DoubleBuffer<int32_t> ib(i0.p, i1.p);
+        size_t tmp_bytes = 0;
+        CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, kb, ib, (int)nnz, 0, bits, s));
+        DBuf<unsigned char> tmp(tmp_bytes);
+        CK(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, kb, ib, (int)nnz, 0, bits, s));
+        // segment heads -> output positions
+        DBuf<int32_t> head(n), seg(n);
+        coo_heads_kernel<<<grid, 256, 0, s>>>(kb.Current(), nnz, head.p);
+        CK(cudaGetLastError());
+        size_t scan_bytes = 0;
+        CK(cub::DeviceScan::InclusiveSum(nullptr, scan_bytes, head.p, seg.p, (int)nnz, s));
+        DBuf<unsigned char> stmp(scan_bytes);
+        CK(cub::DeviceScan::InclusiveSum(stmp.p, scan_bytes, head.p, seg.p, (int)nnz, s));
+        int32_t nout = 0;
+        CK(cudaMemcpyAsync(&nout, seg.p + (n - 1), 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        // outputs
+        int64_t *orr = rows_out, *occ = cols_out;
+        double* ovv = vals_out;
+        DBuf<int64_t> tr(mem == SPARSLA_MEM_HOST ? (size_t)nout : 0), tc(mem == SPARSLA_MEM_HOST ? (size_t)nout : 0);
+        DBuf<double> tv(mem == SPARSLA_MEM_HOST ? (size_t)nout : 0);
+        if (mem == SPARSLA_MEM_HOST) { orr = tr.p; occ = tc.p; ovv = tv.p; }
+        coo_emit_kernel<<<grid, 256, 0, s>>>(kb.Current(), ib.Current(), seg.p, dv, nnz, ncols, orr, occ, ovv);
+        CK(cudaGetLastError());
+        if (mem == SPARSLA_MEM_HOST) {
+            CK(cudaMemcpyAsync(rows_out, tr.p, (size_t)nout * 8, cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(cols_out, tc.p, (size_t)nout * 8, cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(vals_out, tv.p, (size_t)nout * 8, cudaMemcpyDeviceToHost, s));
+        }
+        CK(cudaStreamSynchronize(s));
+        *out_nnz = nout;
+    });
+}

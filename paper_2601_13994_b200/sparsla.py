@@ -138,7 +138,9 @@ class SparseCoo:
     order, explicit zeros kept.  Raises DimensionError / BoundsError like the reference."""
 
     def __init__(self, rows=(), cols=(), vals=(), shape: Shape | tuple = Shape(),
-                 _canonical=False):
+                 _canonical=False, device: int | None = None):
+        """device: canonicalize on that GPU (radix sort, bit-identical result) instead of the
+        host; the inputs are copied in and the canonical arrays copied back."""
         if isinstance(shape, tuple):
             shape = Shape(*shape)
         rows, cols, vals = _i64(rows), _i64(cols), _f64(vals)
@@ -154,10 +156,16 @@ class SparseCoo:
         n = len(rows)
         ro, co, vo = np.empty(n, np.int64), np.empty(n, np.int64), np.empty(n)
         m = C.c_int64()
-        _check(lib().sparsla_coo_canonicalize(
-            C.c_int64(shape.rows), C.c_int64(shape.cols), C.c_int64(n), _p(rows, _i64p),
-            _p(cols, _i64p), _p(vals, _f64p), C.byref(m), _p(ro, _i64p), _p(co, _i64p),
-            _p(vo, _f64p)))
+        if device is None:
+            _check(lib().sparsla_coo_canonicalize(
+                C.c_int64(shape.rows), C.c_int64(shape.cols), C.c_int64(n), _p(rows, _i64p),
+                _p(cols, _i64p), _p(vals, _f64p), C.byref(m), _p(ro, _i64p), _p(co, _i64p),
+                _p(vo, _f64p)))
+        else:
+            _check(lib().sparsla_coo_canonicalize_device(
+                C.c_int(device), C.c_int64(shape.rows), C.c_int64(shape.cols), C.c_int64(n),
+                _p(rows, _i64p), _p(cols, _i64p), _p(vals, _f64p), C.c_int32(MEM_HOST), C.byref(m),
+                _p(ro, _i64p), _p(co, _i64p), _p(vo, _f64p)))
         self._rows, self._cols, self._vals = ro[:m.value], co[:m.value], vo[:m.value]
 
     shape = property(lambda s: s._shape)
