@@ -688,10 +688,11 @@ __global__ void __launch_bounds__(kWsThreads, MINB) spmv_ws_kernel(SpmvParams P)
                 const uint8_t* vp = A + (kb - (o0 & ~(VALIGN - 1)));
                 double y = 0.0;
                 double eop = 0.0;
+                const bool fits = __all_sync(0xffffffffu, len <= W);  // warp-uniform
                 if constexpr (MODE == SPMV_BICG_V || MODE == SPMV_BICG_T) {
-                    if (!__all_sync(0xffffffffu, len <= W)) eop = live ? __ldg(P.aux + row) : 0.0;
+                    if (!fits) eop = live ? __ldg(P.aux + row) : 0.0;
                 }
-                if (__all_sync(0xffffffffu, len <= W)) {
+                if (fits) {
                     // issue every gather straight from the staged columns; the stage is
                     // released once the gathers are in flight (their addresses consumed)
                     double xv[W];
@@ -726,7 +727,7 @@ __global__ void __launch_bounds__(kWsThreads, MINB) spmv_ws_kernel(SpmvParams P)
                 if (live) {
                     P.y[row] = y;
                     if constexpr (MODE == SPMV_CG) {
-                        acc[0] = __dadd_rn(acc[0], __dmul_rn(__all_sync(0xffffffffu, len <= W) ? eop : __ldg(P.x + row), y));
+                        acc[0] = __dadd_rn(acc[0], __dmul_rn(fits ? eop : __ldg(P.x + row), y));
                     } else if constexpr (MODE == SPMV_BICG_V) {
                         acc[0] = __dadd_rn(acc[0], __dmul_rn(eop, y));
                     } else if constexpr (MODE == SPMV_BICG_T) {

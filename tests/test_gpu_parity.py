@@ -278,7 +278,10 @@ def test_persistent_solver_fixed_iterations(S, O, gpu):
 
 
 @pytest.mark.parametrize("kind,p1,p2,fp,backend", [("poisson3d", 40, 0, 0.0, "cg"), ("poisson2d", 200, 0, 0.0, "cg"),
-                                                   ("convdiff3d", 24, 0, 0.1, "bicgstab")])
+                                                   ("convdiff3d", 24, 0, 0.1, "bicgstab"),
+                                                   # row counts that leave idle lanes in the last round
+                                                   ("poisson3d", 13, 0, 0.0, "cg"), ("poisson2d", 37, 0, 0.0, "cg"),
+                                                   ("convdiff3d", 11, 0, 0.3, "bicgstab")])
 def test_value_dictionary_and_scalar_diagonal_bitwise(S, O, gpu, monkeypatch, kind, p1, p2, fp, backend):
     """Stored-format choices are invisible in the results: the 1-byte value dictionary
     (<= 256 distinct values) and the scalar constant Jacobi diagonal give the same bits as

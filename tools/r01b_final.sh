@@ -2,7 +2,7 @@
 # Round-1 final measurements on one B200: tests, smoke, bench (+reference arm), launch list,
 # ncu captures, all configs, LOBPCG.
 cd "$GRAFT_REPO_ROOT"
-timeout 1500 python -m pytest tests -m gpu -q --timeout 900 > gpurun_out/f_pytest.log 2>&1; echo "pytest exit $?" >> gpurun_out/f_pytest.log
+timeout 1500 python -m pytest tests -m gpu -q --timeout 300 > gpurun_out/f_pytest.log 2>&1; echo "pytest exit $?" >> gpurun_out/f_pytest.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/f_smoke.log 2>&1
 timeout 900 python bench.py > gpurun_out/f_bench.json 2> gpurun_out/f_bench.err
 timeout 900 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/f_bench_ref.json 2> gpurun_out/f_bench_ref.err
