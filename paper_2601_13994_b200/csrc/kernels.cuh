@@ -687,12 +687,8 @@ __global__ void __launch_bounds__(kWsThreads, MINB) spmv_ws_kernel(SpmvParams P)
                 const int32_t* cp = reinterpret_cast<const int32_t*>(A + L.vbytes) + (kb - (o0 & ~3));
                 const uint8_t* vp = A + (kb - (o0 & ~(VALIGN - 1)));
                 double y = 0.0;
-                double eop = 0.0;
-                const bool fits = __all_sync(0xffffffffu, len <= W);  // warp-uniform
-                if constexpr (MODE == SPMV_BICG_V || MODE == SPMV_BICG_T) {
-                    if (!fits) eop = live ? __ldg(P.aux + row) : 0.0;
-                }
-                if (fits) {
+                double eop = 0.0;  // the fused dot's operand (p[row] / r-hat[row] / s[row])
+                if (__all_sync(0xffffffffu, len <= W)) {
                     // issue every gather straight from the staged columns; the stage is
                     // released once the gathers are in flight (their addresses consumed)
                     double xv[W];
@@ -712,6 +708,8 @@ __global__ void __launch_bounds__(kWsThreads, MINB) spmv_ws_kernel(SpmvParams P)
                     for (int u = 0; u < W; ++u)
                         if (u < len) y = __dadd_rn(y, __dmul_rn(s_vtab[(vi[u / 4] >> (8 * (u % 4))) & 0xffu], xv[u]));
                 } else {
+                    if constexpr (MODE == SPMV_BICG_V || MODE == SPMV_BICG_T) eop = live ? __ldg(P.aux + row) : 0.0;
+                    if constexpr (MODE == SPMV_CG) eop = live ? __ldg(P.x + row) : 0.0;
                     for (int k0 = 0; k0 < len; k0 += W) {
                         double pr[W];
 #pragma unroll
@@ -727,7 +725,7 @@ __global__ void __launch_bounds__(kWsThreads, MINB) spmv_ws_kernel(SpmvParams P)
                 if (live) {
                     P.y[row] = y;
                     if constexpr (MODE == SPMV_CG) {
-                        acc[0] = __dadd_rn(acc[0], __dmul_rn(fits ? eop : __ldg(P.x + row), y));
+                        acc[0] = __dadd_rn(acc[0], __dmul_rn(eop, y));
                     } else if constexpr (MODE == SPMV_BICG_V) {
                         acc[0] = __dadd_rn(acc[0], __dmul_rn(eop, y));
                     } else if constexpr (MODE == SPMV_BICG_T) {
