@@ -70,6 +70,28 @@ __global__ void coo_emit_kernel(const unsigned long long* keys, const int32_t* i
     vo[o] = s;
 }
 
+__global__ void csr_rows_kernel(const int32_t* rp, long long n, int32_t* rows) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    for (int k = rp[i]; k < rp[i + 1]; ++k) rows[k] = (int32_t)i;
+}
+
+__global__ void iota_hist_kernel(const int32_t* ci, long long nnz, int32_t* idx, int32_t* count) {
+    const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= nnz) return;
+    idx[k] = (int32_t)k;
+    atomicAdd(count + ci[k], 1);
+}
+
+__global__ void transpose_emit_kernel(const int32_t* idx, const int32_t* rows, const double* val, long long nnz,
+                                      int32_t* tci, double* tv) {
+    const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= nnz) return;
+    const int32_t k = idx[j];
+    tci[j] = rows[k];
+    tv[j] = val[k];
+}
+
 int key_bits(unsigned long long maxkey) {
     int b = 1;
     while (b < 64 && (maxkey >> b) != 0) ++b;
@@ -77,6 +99,47 @@ int key_bits(unsigned long long maxkey) {
 }
 
 }  // namespace
+
+// Canonical A^T of a device CSR (sparse.cpp:176-182 / the reference's spmv_transpose scatter
+// order): entries stably radix-sorted by column keep their row-major order, so every row of
+// A^T lists its columns (A's rows) ascending.  Results land in host arrays trp[ncols+1],
+// tci[nnz], tv[nnz] (the device handle of A^T is built from them).
+void csr_transpose_device(int device, long long nrows, long long ncols, long long nnz, const int32_t* rp,
+                          const int32_t* ci, const double* val, int32_t* trp, int32_t* tci, double* tv) {
+    DeviceGuard g(device);
+    cudaStream_t s = nullptr;
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    struct StreamGuard { cudaStream_t s; ~StreamGuard() { cudaStreamDestroy(s); } } sg{s};
+    const size_t n = (size_t)std::max<long long>(nnz, 1);
+    DBuf<int32_t> rows(n), cnt((size_t)ncols + 1), k0(n), k1(n), i0(n), i1(n), otc(n), orp((size_t)ncols + 1);
+    DBuf<double> otv(n);
+    CK(cudaMemsetAsync(cnt.p, 0, ((size_t)ncols + 1) * 4, s));
+    if (nrows > 0) csr_rows_kernel<<<(unsigned)((nrows + 255) / 256), 256, 0, s>>>(rp, nrows, rows.p);
+    if (nnz > 0) {
+        iota_hist_kernel<<<(unsigned)((nnz + 255) / 256), 256, 0, s>>>(ci, nnz, i0.p, cnt.p);
+        CK(cudaMemcpyAsync(k0.p, ci, (size_t)nnz * 4, cudaMemcpyDeviceToDevice, s));
+        const int bits = key_bits((unsigned long long)std::max<long long>(ncols, 1));
+        cub::DoubleBuffer<int32_t> kb(k0.p, k1.p), ib(i0.p, i1.p);
+        size_t tb = 0;
+        CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, kb, ib, (int)nnz, 0, bits, s));
+        DBuf<unsigned char> tmp(tb);
+        CK(cub::DeviceRadixSort::SortPairs(tmp.p, tb, kb, ib, (int)nnz, 0, bits, s));
+        transpose_emit_kernel<<<(unsigned)((nnz + 255) / 256), 256, 0, s>>>(ib.Current(), rows.p, val, nnz, otc.p,
+                                                                           otv.p);
+    }
+    CK(cudaGetLastError());
+    size_t sb = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, sb, cnt.p, orp.p, (int)(ncols + 1), s));
+    DBuf<unsigned char> stmp(sb);
+    CK(cub::DeviceScan::ExclusiveSum(stmp.p, sb, cnt.p, orp.p, (int)(ncols + 1), s));
+    CK(cudaMemcpyAsync(trp, orp.p, ((size_t)ncols + 1) * 4, cudaMemcpyDeviceToHost, s));
+    if (nnz > 0) {
+        CK(cudaMemcpyAsync(tci, otc.p, (size_t)nnz * 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(tv, otv.p, (size_t)nnz * 8, cudaMemcpyDeviceToHost, s));
+    }
+    CK(cudaStreamSynchronize(s));
+}
+
 }  // namespace sparsla_b200
 
 using namespace sparsla_b200;

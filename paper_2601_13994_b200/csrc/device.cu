@@ -429,22 +429,10 @@ DevCsr* DevCsr::get_transpose() {
     std::lock_guard<std::mutex> lk(lazy_mu);
     if (!transpose) {
         DeviceGuard g(device);
-        std::vector<int32_t> hrp(nrows + 1), hci(nnz);
-        std::vector<double> hv(nnz);
-        CK(memcpy_sync(hrp.data(), rp, (nrows + 1) * 4, cudaMemcpyDeviceToHost));
-        CK(memcpy_sync(hci.data(), ci, nnz * 4, cudaMemcpyDeviceToHost));
-        CK(memcpy_sync(hv.data(), val, nnz * 8, cudaMemcpyDeviceToHost));
-        std::vector<int32_t> trp(ncols + 1, 0), tci(nnz);
-        std::vector<double> tv(nnz);
-        for (long long k = 0; k < nnz; ++k) ++trp[hci[k] + 1];
-        for (long long j = 0; j < ncols; ++j) trp[j + 1] += trp[j];
-        std::vector<int32_t> next(trp.begin(), trp.end() - 1);
-        for (long long i = 0; i < nrows; ++i)
-            for (int k = hrp[i]; k < hrp[i + 1]; ++k) {
-                const int pos = next[hci[k]]++;
-                tci[pos] = (int32_t)i;
-                tv[pos] = hv[k];
-            }
+        CK(cudaStreamSynchronize(stream));  // the values may have just been (re)written
+        std::vector<int32_t> trp(ncols + 1, 0), tci(std::max<long long>(nnz, 1));
+        std::vector<double> tv(std::max<long long>(nnz, 1));
+        csr_transpose_device(device, nrows, ncols, nnz, rp, ci, val, trp.data(), tci.data(), tv.data());
         transpose = DevCsr::create<int32_t>(device, ncols, nrows, trp.data(), tci.data(), tv.data());
     }
     return transpose;

@@ -68,6 +68,10 @@ struct DevCsr {
     DevCsr* get_transpose();
 };
 
+// canonical A^T of a device CSR into host arrays (coo_device.cu)
+void csr_transpose_device(int device, long long nrows, long long ncols, long long nnz, const int32_t* rp,
+                          const int32_t* ci, const double* val, int32_t* trp, int32_t* tci, double* tv);
+
 void launch_spmv(DevCsr* A, cudaStream_t s, int mode, const double* x, double* y, const double* aux,
                  const RedParams& red, int check_done);
 unsigned spmv_grid(const DevCsr* A, long long nch);
