@@ -1003,6 +1003,12 @@ void finish(Lobpcg& L, int k, double tol, const double* dinv, EigOut& o, double*
     o.spmm = L.spmm_count;
 }
 
+int eig_guard(int k) {
+    if (const char* e = std::getenv("SPARSLA_EIG_GUARD")) return std::max(0, std::atoi(e));
+    (void)k;
+    return 0;
+}
+
 int dense_threshold() {
     const char* e = std::getenv("SPARSLA_EIG_DENSE_THRESHOLD");
     return e ? std::max(0, std::atoi(e)) : 64;
@@ -1012,7 +1018,7 @@ void eig_smallest(DevCsr* A, int k, double tol, long long max_iter, uint64_t see
                   EigOut& o) {
     const long long n = A->nrows;
     const double* dinv = precond == SPARSLA_PRECOND_JACOBI ? A->jacobi_dinv() : nullptr;
-    const int m = k;
+    int m = k;
     if (n <= dense_threshold()) {
         // Rayleigh-Ritz on the whole space (S = I): A is formed column block by column
         // block with the same SpMM kernel, then the n x n symmetric problem is solved.
@@ -1043,6 +1049,13 @@ void eig_smallest(DevCsr* A, int k, double tol, long long max_iter, uint64_t see
         o.diag = "dense Rayleigh-Ritz on the full space (n <= dense threshold)";
         return;
     }
+    // guard vectors: the block carries g extra Ritz pairs so the k wanted ones converge at the
+    // rate of the gap to lambda_{k+g+1} (SPARSLA_EIG_GUARD overrides the default)
+    {
+        int g = eig_guard(k);
+        g = (int)std::min<long long>(g, std::min<long long>(kMaxK - k, n / 4 - k));
+        m = k + std::max(0, g);
+    }
     Lobpcg L(A, m);
     const Cols Xc = cols_range(0, m);
     eig_init_kernel<<<L.grid(), kT, 0, L.s>>>(L.S, n, L.ld, m, seed);
@@ -1055,9 +1068,12 @@ void eig_smallest(DevCsr* A, int k, double tol, long long max_iter, uint64_t see
     long long it = 0;
     for (;; ++it) {
         Cols Z;
-        for (int j = 0; j < m; ++j)  // soft locking: only unconverged pairs add directions
+        bool wanted_done = true;  // the first k (wanted) pairs decide termination
+        for (int j = 0; j < m; ++j) {  // soft locking: only unconverged pairs add directions
             if (!(res[j] <= tol)) Z.c[Z.n++] = (unsigned char)(m + j);
-        if (Z.n == 0 || it >= max_iter) break;
+            if (j < k && !(res[j] <= tol)) wanted_done = false;
+        }
+        if (wanted_done || Z.n == 0 || it >= max_iter) break;
         if (have_p) {
             const int nw = Z.n;
             for (int t = 0; t < nw; ++t) Z.c[Z.n++] = (unsigned char)(m + Z.c[t]);  // P slot = W slot + m
@@ -1072,7 +1088,7 @@ void eig_smallest(DevCsr* A, int k, double tol, long long max_iter, uint64_t see
     o.lam = lam;
     finish(L, k, tol, dinv, o, V);
     char buf[128];
-    std::snprintf(buf, sizeof buf, "lobpcg: %lld iterations, block %d, %s", it, m,
+    std::snprintf(buf, sizeof buf, "lobpcg: %lld iterations, block %d (k %d), %s", it, m, k,
                   o.all_conv ? "all pairs converged" : "not all pairs converged");
     o.diag = buf;
 }
