@@ -374,15 +374,18 @@ __global__ void __launch_bounds__(kTRa) apply_kernel(double* S, int ld, Cols in,
 
 // Rayleigh-Ritz update of whole rows from the basis B = [X | Z] (q = B.n) with C (q x m):
 //   P' = S_Z C_Z,   X' = P' + S_X C_X,   AX' = AS_B C     into Sn (X, P slots) and ASn (X slot).
-// One thread per row; S and AS tiles are staged together (kRRStages deep); the two output
-// tiles are single-buffered in shared memory and bulk-stored (the W slot of Sn and the W, P
-// slots of ASn carry don't-care values, rewritten before they are read).
+// Two threads per row, each owning the output columns k = half, half + 2, ... (the row's
+// inputs are broadcast reads of the staged tiles); S and AS tiles are staged together
+// (kRRStages deep); the two output tiles are single-buffered in shared memory and
+// bulk-stored (the W slot of Sn and the W, P slots of ASn carry don't-care values, rewritten
+// before they are read).
 constexpr int kRRStages = 2;
+constexpr int kHalfK = kMaxK / 2;
 template <int TR>
-__global__ void __launch_bounds__(TR) rr_apply_kernel(const double* S, const double* AS, double* Sn, double* ASn,
-                                                      int ld, Cols B, int m, long long n, const Mat C,
-                                                      const Vec16 lam, const double* __restrict__ dinv,
-                                                      double* rpart) {
+__global__ void __launch_bounds__(2 * TR) rr_apply_kernel(const double* S, const double* AS, double* Sn, double* ASn,
+                                                          int ld, Cols B, int m, long long n, const Mat C,
+                                                          const Vec16 lam, const double* __restrict__ dinv,
+                                                          double* rpart) {
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
     int* s_b = reinterpret_cast<int*>(smem + 64);
@@ -393,11 +396,14 @@ __global__ void __launch_bounds__(TR) rr_apply_kernel(const double* S, const dou
     const int q = B.n;
     stage_cols(B, s_b);
     const TileWalk<TR> W(n, ld);
-    const int row = threadIdx.x;
-    double racc[kMaxK];  // ||R_k||^2 over this thread's rows
+    const int row = threadIdx.x >> 1, half = threadIdx.x & 1;
+    double lk[kHalfK];  // lambda of this thread's columns (constant-index parameter reads)
 #pragma unroll
-    for (int k = 0; k < kMaxK; ++k) racc[k] = 0.0;
-    if (row == 0) {
+    for (int i = 0; i < kHalfK; ++i) lk[i] = half ? lam.v[2 * i + 1] : lam.v[2 * i];
+    double racc[kHalfK];  // ||R_k||^2 of this thread's columns over its rows
+#pragma unroll
+    for (int i = 0; i < kHalfK; ++i) racc[i] = 0.0;
+    if (threadIdx.x == 0) {
         for (int s = 0; s < kRRStages; ++s) mbar_init(&bar[s], 1);
         fence_mbar_init();
         for (long long j = 0; j < min((long long)kRRStages, W.mine); ++j)
@@ -410,55 +416,63 @@ __global__ void __launch_bounds__(TR) rr_apply_kernel(const double* S, const dou
         const double* Ts = ring + s * 2 * te;
         const double* Ta = Ts + te;
         const int nr = W.rows(j);
-        double xs[kMaxK], xa[kMaxK];
+        double xs[kHalfK], xa[kHalfK];
 #pragma unroll
-        for (int k = 0; k < kMaxK; ++k) { xs[k] = 0.0; xa[k] = 0.0; }
+        for (int i = 0; i < kHalfK; ++i) { xs[i] = 0.0; xa[i] = 0.0; }
         if (row < nr) {
             const double* ts = Ts + row * ld;
             const double* ta = Ta + row * ld;
             for (int l = m; l < q; ++l) {  // Z part first: P'
                 const double u = ts[s_b[l]], v = ta[s_b[l]];
 #pragma unroll
-                for (int k = 0; k < kMaxK; ++k)
+                for (int i = 0; i < kHalfK; ++i) {
+                    const int k = half + 2 * i;
                     if (k < m) {
-                        xs[k] = fma(u, C.v[l * m + k], xs[k]);
-                        xa[k] = fma(v, C.v[l * m + k], xa[k]);
+                        xs[i] = fma(u, C.v[l * m + k], xs[i]);
+                        xa[i] = fma(v, C.v[l * m + k], xa[i]);
                     }
+                }
             }
         }
-        if (row == 0) bulk_wait_read();  // the previous tile's stores have read the out tiles
+        if (threadIdx.x == 0) bulk_wait_read();  // the previous tile's stores have read the out tiles
         __syncthreads();
         if (row < nr) {
             const double* ts = Ts + row * ld;
             const double* ta = Ta + row * ld;
 #pragma unroll
-            for (int k = 0; k < kMaxK; ++k)
-                if (k < m) outS[row * ld + 2 * m + k] = xs[k];
+            for (int i = 0; i < kHalfK; ++i) {
+                const int k = half + 2 * i;
+                if (k < m) outS[row * ld + 2 * m + k] = xs[i];
+            }
             for (int l = 0; l < m; ++l) {
                 const double u = ts[s_b[l]], v = ta[s_b[l]];
 #pragma unroll
-                for (int k = 0; k < kMaxK; ++k)
+                for (int i = 0; i < kHalfK; ++i) {
+                    const int k = half + 2 * i;
                     if (k < m) {
-                        xs[k] = fma(u, C.v[l * m + k], xs[k]);
-                        xa[k] = fma(v, C.v[l * m + k], xa[k]);
+                        xs[i] = fma(u, C.v[l * m + k], xs[i]);
+                        xa[i] = fma(v, C.v[l * m + k], xa[i]);
                     }
+                }
             }
             // fused residual of the new Ritz pairs: R = AX' - X' diag(lambda), its norms, and
             // the Jacobi-preconditioned W = |D|^-1 R for the next iteration (W slot)
             const double d = dinv ? fabs(__ldg(dinv + W.row0(j) + row)) : 1.0;
 #pragma unroll
-            for (int k = 0; k < kMaxK; ++k)
+            for (int i = 0; i < kHalfK; ++i) {
+                const int k = half + 2 * i;
                 if (k < m) {
-                    outS[row * ld + k] = xs[k];
-                    outA[row * ld + k] = xa[k];
-                    const double r = fma(-lam.v[k], xs[k], xa[k]);
-                    racc[k] = fma(r, r, racc[k]);
+                    outS[row * ld + k] = xs[i];
+                    outA[row * ld + k] = xa[i];
+                    const double r = fma(-lk[i], xs[i], xa[i]);
+                    racc[i] = fma(r, r, racc[i]);
                     outS[row * ld + m + k] = d * r;
                 }
+            }
         }
         fence_proxy_async_smem();
         __syncthreads();
-        if (row == 0) {
+        if (threadIdx.x == 0) {
             const uint32_t bytes = (uint32_t)nr * ld * 8u;
             bulk_store(Sn + W.row0(j) * ld, outS, bytes);
             bulk_store(ASn + W.row0(j) * ld, outA, bytes);
@@ -466,24 +480,25 @@ __global__ void __launch_bounds__(TR) rr_apply_kernel(const double* S, const dou
             if (j + kRRStages < W.mine) W.issue(j + kRRStages, s, bar, ring + s * 2 * te, S, AS);
         }
     }
-    // per-CTA residual partials: warp trees, then warps in order
-    __shared__ double rred[TR / 32][kMaxK];
+    // per-CTA residual partials: same-parity lanes folded by shuffles (even offsets), lane 0
+    // / 1 hold the warp's even / odd columns, then warps in order
+    __shared__ double rred[2 * TR / 32][kMaxK];
     const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
 #pragma unroll
-    for (int k = 0; k < kMaxK; ++k) {
-        if (k >= m) break;
-        double v = racc[k];
+    for (int i = 0; i < kHalfK; ++i) {
+        double v = racc[i];
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
-        if (lane == 0) rred[wp][k] = v;
+        for (int off = 16; off > 1; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+        const int k = lane + 2 * i;
+        if (lane < 2 && k < m) rred[wp][k] = v;
     }
     __syncthreads();
     if (threadIdx.x < m) {
         double v = 0.0;
-        for (int q2 = 0; q2 < TR / 32; ++q2) v += rred[q2][threadIdx.x];
+        for (int q2 = 0; q2 < 2 * TR / 32; ++q2) v += rred[q2][threadIdx.x];
         rpart[(size_t)blockIdx.x * m + threadIdx.x] = v;
     }
-    if (row == 0) bulk_wait_all();
+    if (threadIdx.x == 0) bulk_wait_all();
 }
 
 // The ring doubles as the row-group reduction buffer after the tile loop.
@@ -928,9 +943,9 @@ struct Lobpcg {
             const int tr = rr_rows(ld);
             const unsigned g = (unsigned)std::max<long long>(1, std::min<long long>((n + tr - 1) / tr, 4LL * 148));
             if (tr == 128)
-                rr_apply_kernel<128><<<g, 128, rr_apply_smem(ld), s>>>(S, AS, Sn, ASn, ld, B, m, n, C, L, dinv, partial);
+                rr_apply_kernel<128><<<g, 256, rr_apply_smem(ld), s>>>(S, AS, Sn, ASn, ld, B, m, n, C, L, dinv, partial);
             else
-                rr_apply_kernel<64><<<g, 64, rr_apply_smem(ld), s>>>(S, AS, Sn, ASn, ld, B, m, n, C, L, dinv, partial);
+                rr_apply_kernel<64><<<g, 128, rr_apply_smem(ld), s>>>(S, AS, Sn, ASn, ld, B, m, n, C, L, dinv, partial);
             CK(cudaGetLastError());
             std::vector<double> h((size_t)g * m);
             CK(cudaMemcpyAsync(h.data(), partial, h.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
