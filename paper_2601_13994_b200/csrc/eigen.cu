@@ -756,6 +756,11 @@ Cols cols_cat(const Cols& x, const Cols& y) {
 }
 
 // --------------------------------------------------------------- LOBPCG driver ------
+bool cgs2_always() {
+    static const bool on = [] { const char* e = std::getenv("SPARSLA_EIG_CGS2"); return e && std::atoi(e) != 0; }();
+    return on;
+}
+
 struct Lobpcg {
     DevCsr* A;
     cudaStream_t s;
@@ -915,6 +920,19 @@ struct Lobpcg {
             out.n = w2;
             apply(BZ, out, M);
             z = out;
+            // "Twice is enough" (Kahan / Parlett): when no column lost more than half of its
+            // norm to B and the normalised Gram is well conditioned, the first pass is already
+            // orthonormal to working precision and the second is skipped (SPARSLA_EIG_CGS2=1
+            // forces it).
+            if (pass == 0 && !cgs2_always()) {
+                double worst = 1.0;
+                for (int i = 0; i < w; ++i) {
+                    const double h0 = G[(size_t)(b + i) * w + i], h = H[(size_t)i * w + i];
+                    worst = std::min(worst, h0 > 0 ? h / h0 : 0.0);
+                }
+                const double smin = sig.empty() ? 0.0 : sig.front();
+                if (w2 == w && worst > 0.25 && smin > 1e-6 * smax) break;
+            }
         }
         return z;
     }
@@ -1017,6 +1035,7 @@ void finish(Lobpcg& L, int k, double tol, const double* dinv, EigOut& o, double*
     CK(cudaStreamSynchronize(L.s));
     o.spmm = L.spmm_count;
 }
+
 
 int eig_guard(int k) {
     if (const char* e = std::getenv("SPARSLA_EIG_GUARD")) return std::max(0, std::atoi(e));
