@@ -812,7 +812,8 @@ bool Solver::capturable() const { return !fused && (!dist || dist->tr->capturabl
 
 void Solver::enqueue_fused(long long iters) {
     FusedParams F{};
-    F.rp = A->rp; F.ci = A->ci; F.val = A->val; F.d = dinv;
+    F.rp = A->rp; F.ci = A->ci; F.val = A->val; F.d = d_is_uniform ? nullptr : dinv; F.d_uni = d_uniform;
+    F.vidx = A->vd ? A->vidx : nullptr; F.vtab = A->vtab;
     F.x = x; F.r = r; F.p = p; F.q = q;
     F.n = n; F.nch = nchunks_of(n);
     F.partials = partials; F.bar = fused_bar; F.st = st;

@@ -1343,7 +1343,10 @@ struct FusedParams {
     const int32_t* rp;
     const int32_t* ci;
     const double* val;
-    const double* d;
+    const uint8_t* vidx;  // value dictionary (or nullptr: val)
+    const double* vtab;
+    const double* d;      // nullptr: constant diagonal d_uni
+    double d_uni;
     double *x, *r, *p, *q;
     long long n, nch;
     double* partials;  // [3][nch]
@@ -1384,10 +1387,13 @@ static __global__ void __launch_bounds__(kSpmvThreads, 4) cg_fused_kernel(FusedP
     __shared__ KState S;
     __shared__ double sred[3 * (kSpmvThreads / 32)];
     __shared__ double sbc[4];
+    __shared__ double s_vtab[256];
     const int t = threadIdx.x;
     if (t == 0) S = *P.st;
+    if (P.vidx) s_vtab[t] = P.vtab[t];  // kSpmvThreads == 256
     __syncthreads();
     if (S.done) return;
+    const uint8_t* __restrict__ vidx = P.vidx;
     unsigned epoch = 0;
     const long long m = P.nch;
     for (int it = 0; it < P.iters; ++it) {
@@ -1410,7 +1416,9 @@ static __global__ void __launch_bounds__(kSpmvThreads, 4) cg_fused_kernel(FusedP
                         double pr[8];
 #pragma unroll
                         for (int u = 0; u < 8; ++u)
-                            if (k0 + u < ke) pr[u] = __dmul_rn(__ldg(P.val + k0 + u), __ldcg(P.p + __ldg(P.ci + k0 + u)));
+                            if (k0 + u < ke)
+                                pr[u] = __dmul_rn(vidx ? s_vtab[__ldg(vidx + k0 + u)] : __ldg(P.val + k0 + u),
+                                                  __ldcg(P.p + __ldg(P.ci + k0 + u)));
 #pragma unroll
                         for (int u = 0; u < 8; ++u)
                             if (k0 + u < ke) y = __dadd_rn(y, pr[u]);
@@ -1439,7 +1447,7 @@ static __global__ void __launch_bounds__(kSpmvThreads, 4) cg_fused_kernel(FusedP
                 const long long i = base + (long long)r * kChunkSlots + t;
                 if (i < P.n) {
                     const double rn = __dsub_rn(__ldcg(P.r + i), __dmul_rn(alpha, __ldcg(P.q + i)));
-                    const double z = __dmul_rn(__ldg(P.d + i), rn);
+                    const double z = __dmul_rn(P.d ? __ldg(P.d + i) : P.d_uni, rn);
                     P.r[i] = rn;
                     acc[0] = __dadd_rn(acc[0], __dmul_rn(rn, z));
                     acc[1] = __dadd_rn(acc[1], __dmul_rn(rn, rn));
@@ -1470,7 +1478,7 @@ static __global__ void __launch_bounds__(kSpmvThreads, 4) cg_fused_kernel(FusedP
                 if (i < P.n) {
                     const double pv = __ldcg(P.p + i);
                     P.x[i] = __dadd_rn(__ldcg(P.x + i), __dmul_rn(alpha, pv));
-                    if (live) P.p[i] = __dadd_rn(__dmul_rn(__ldg(P.d + i), __ldcg(P.r + i)), __dmul_rn(beta, pv));
+                    if (live) P.p[i] = __dadd_rn(__dmul_rn(P.d ? __ldg(P.d + i) : P.d_uni, __ldcg(P.r + i)), __dmul_rn(beta, pv));
                 }
             }
         }
