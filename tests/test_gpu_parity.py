@@ -378,3 +378,21 @@ def test_parked_solver_reuse_bitwise(S, O, gpu, monkeypatch):
         xo, ro = (O.cg if be == "cg" else O.bicgstab)(Ao, b, atol=0.0, rtol=rtol, max_iter=3000)
         assert r.iterations == ro["iterations"], (be, rtol)
         assert_bitwise(x, xo, f"{be} rtol={rtol}")
+
+
+def test_value_dictionary_empty_rows_and_partial_rounds(S, O, gpu):
+    """Dictionary SpMV on a stencil with emptied rows and a row count that ends mid-round:
+    empty rows give exactly 0.0, every other row the oracle's bits."""
+    A = O.generate("poisson3d", 19)  # 6859 rows: the last 256-row round is partial
+    n = A.nrows
+    keep = np.ones(A.nnz, bool)
+    rows = np.repeat(np.arange(n), np.diff(A.row_ptr))
+    keep[(rows % 7) == 3] = False
+    B = O.csr_from_triplets(n, n, rows[keep], A.col_idx[keep], A.vals[keep])
+    assert (np.diff(B.row_ptr) == 0).sum() > 0
+    D = to_S(S, B).device(0)
+    assert D.format()["value_dict"]
+    x = np.random.default_rng(4).standard_normal(n)
+    y = S.spmv(D, x)
+    assert_bitwise(y, O.spmv(B, x))
+    assert np.all(y[np.diff(B.row_ptr) == 0] == 0.0)
