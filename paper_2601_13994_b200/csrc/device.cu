@@ -150,6 +150,7 @@ static void configure_ws_variants(int device) {
 void DevCsr::drop_parked() noexcept {
     std::lock_guard<std::mutex> lk(solver_mu);
     for (auto*& p : parked) { delete p; p = nullptr; }
+    ++values_version;  // solvers still running on the old values must not park afterwards
 }
 
 DevCsr::~DevCsr() {
@@ -1004,7 +1005,15 @@ int krylov(sparsla_dcsr* H, int backend, const double* b, double* x, const spars
                 S->opts = *o;  // tolerances / max_iter enter through reset() (KState)
             }
         }
-        if (!S) S = std::make_unique<Solver>(A, backend, *o);
+        if (!S) {
+            long long ver;
+            {
+                std::lock_guard<std::mutex> lk(A->solver_mu);
+                ver = A->values_version;
+            }
+            S = std::make_unique<Solver>(A, backend, *o);
+            S->values_version = ver;
+        }
         S->set_b(b, mem);
         if (mem == SPARSLA_MEM_DEVICE) S->x = x;
         S->reset();
@@ -1016,7 +1025,7 @@ int krylov(sparsla_dcsr* H, int backend, const double* b, double* x, const spars
         if (cache) {
             std::lock_guard<std::mutex> lk(A->solver_mu);
             Solver*& slot = A->parked[backend == SPARSLA_BACKEND_CG ? 0 : 1];
-            if (!slot) slot = S.release();
+            if (!slot && S->values_version == A->values_version) slot = S.release();
         }
     });
 }

@@ -55,6 +55,7 @@ struct DevCsr {
     // by the next cg_solve / bicgstab_solve call with host buffers (SPARSLA_SOLVER_CACHE=0: off)
     std::mutex solver_mu;
     struct Solver* parked[2] = {nullptr, nullptr};
+    long long values_version = 0;  // bumped by set_values: a solver built before never parks
     void drop_parked() noexcept;
 
     template <class I>
@@ -135,6 +136,7 @@ struct Solver {
     cudaEvent_t ev[2] = {nullptr, nullptr};
     cudaGraphExec_t g_many = nullptr, g_one = nullptr;
     bool fused = false;          // small CG: cg_fused_kernel runs whole iterations
+    long long values_version = 0;  // A->values_version when this solver was built
     // fused peer-memory collectives (distributed CG)
     P2PCtx* d_p2p = nullptr;
     std::vector<void*> p2p_allocs, p2p_ipc_opened;
