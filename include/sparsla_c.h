@@ -86,6 +86,12 @@ int sparsla_coo_canonicalize_device(int device, int64_t nrows, int64_t ncols, in
                                     const int64_t* rows, const int64_t* cols, const double* vals,
                                     int32_t mem, int64_t* out_nnz, int64_t* rows_out,
                                     int64_t* cols_out, double* vals_out);
+/* The canonicalization's permutation on a GPU: order[j] = input entry at sorted position j
+ * (stable by (row, col)), group[j] = the canonical entry it is summed into (ascending from 0);
+ * *out_nnz = number of canonical entries.  Bounds errors as above. */
+int sparsla_coo_sort_device(int device, int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* rows,
+                            const int64_t* cols, int32_t mem, int64_t* out_nnz, int64_t* order,
+                            int64_t* group);
 /* CsrMatrix::from_coo (sparse.hpp:84, sparse.cpp:94-116), input must be canonical. */
 int sparsla_csr_from_coo(int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* rows,
                          const int64_t* cols, const double* vals, int64_t* row_ptr,

@@ -70,6 +70,14 @@ __global__ void coo_emit_kernel(const unsigned long long* keys, const int32_t* i
     vo[o] = s;
 }
 
+// sorted position j: order[j] = input entry, group[j] = its canonical entry
+__global__ void coo_perm_kernel(const int32_t* idx, const int32_t* seg, long long nnz, int64_t* order, int64_t* group) {
+    const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= nnz) return;
+    order[j] = idx[j];
+    group[j] = (int64_t)seg[j] - 1;
+}
+
 __global__ void csr_rows_kernel(const int32_t* rp, long long n, int32_t* rows) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -144,10 +152,12 @@ void csr_transpose_device(int device, long long nrows, long long ncols, long lon
 
 using namespace sparsla_b200;
 
-extern "C" int sparsla_coo_canonicalize_device(int device, int64_t nrows, int64_t ncols, int64_t nnz,
-                                               const int64_t* rows, const int64_t* cols, const double* vals,
-                                               int32_t mem, int64_t* out_nnz, int64_t* rows_out,
-                                               int64_t* cols_out, double* vals_out) {
+namespace {
+// Shared by both entry points: vals == nullptr -> permutation outputs (order, group) instead
+// of the canonical COO.
+int coo_device_impl(int device, int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* rows, const int64_t* cols,
+                    const double* vals, int32_t mem, int64_t* out_nnz, int64_t* rows_out, int64_t* cols_out,
+                    double* vals_out, int64_t* order, int64_t* group) {
     return guarded([&] {
         if (nrows < 0 || ncols < 0) fail(SPARSLA_ERR_DIMENSION, "negative matrix shape");
         if (nnz < 0) fail(SPARSLA_ERR_DIMENSION, "negative nnz");
@@ -168,12 +178,12 @@ extern "C" int sparsla_coo_canonicalize_device(int device, int64_t nrows, int64_
         const int64_t *dr = rows, *dc = cols;
         const double* dv = vals;
         DBuf<int64_t> hr(mem == SPARSLA_MEM_HOST ? n : 0), hc(mem == SPARSLA_MEM_HOST ? n : 0);
-        DBuf<double> hv(mem == SPARSLA_MEM_HOST ? n : 0);
+        DBuf<double> hv(mem == SPARSLA_MEM_HOST && vals ? n : 0);
         if (mem == SPARSLA_MEM_HOST) {
             CK(cudaMemcpyAsync(hr.p, rows, n * 8, cudaMemcpyHostToDevice, s));
             CK(cudaMemcpyAsync(hc.p, cols, n * 8, cudaMemcpyHostToDevice, s));
-            CK(cudaMemcpyAsync(hv.p, vals, n * 8, cudaMemcpyHostToDevice, s));
-            dr = hr.p; dc = hc.p; dv = hv.p;
+            if (vals) CK(cudaMemcpyAsync(hv.p, vals, n * 8, cudaMemcpyHostToDevice, s));
+            dr = hr.p; dc = hc.p; dv = vals ? hv.p : nullptr;
         }
         // bounds (the first offending entry in input order, as the host path reports it)
         DBuf<unsigned long long> bad(1);
@@ -215,6 +225,20 @@ extern "C" int sparsla_coo_canonicalize_device(int device, int64_t nrows, int64_
         int32_t nout = 0;
         CK(cudaMemcpyAsync(&nout, seg.p + (n - 1), 4, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
+        if (!vals) {  // permutation outputs
+            int64_t *oo = order, *og = group;
+            DBuf<int64_t> to(mem == SPARSLA_MEM_HOST ? n : 0), tg(mem == SPARSLA_MEM_HOST ? n : 0);
+            if (mem == SPARSLA_MEM_HOST) { oo = to.p; og = tg.p; }
+            coo_perm_kernel<<<grid, 256, 0, s>>>(ib.Current(), seg.p, nnz, oo, og);
+            CK(cudaGetLastError());
+            if (mem == SPARSLA_MEM_HOST) {
+                CK(cudaMemcpyAsync(order, to.p, n * 8, cudaMemcpyDeviceToHost, s));
+                CK(cudaMemcpyAsync(group, tg.p, n * 8, cudaMemcpyDeviceToHost, s));
+            }
+            CK(cudaStreamSynchronize(s));
+            *out_nnz = nout;
+            return;
+        }
         // outputs
         int64_t *orr = rows_out, *occ = cols_out;
         double* ovv = vals_out;
@@ -231,4 +255,29 @@ extern "C" int sparsla_coo_canonicalize_device(int device, int64_t nrows, int64_
         CK(cudaStreamSynchronize(s));
         *out_nnz = nout;
     });
+}
+}  // namespace
+
+extern "C" int sparsla_coo_canonicalize_device(int device, int64_t nrows, int64_t ncols, int64_t nnz,
+                                               const int64_t* rows, const int64_t* cols, const double* vals,
+                                               int32_t mem, int64_t* out_nnz, int64_t* rows_out,
+                                               int64_t* cols_out, double* vals_out) {
+    if (!vals && nnz > 0) {
+        set_last_error("vals is null");
+        return SPARSLA_ERR_INVALID_ARGUMENT;
+    }
+    static const double dummy = 0.0;
+    return coo_device_impl(device, nrows, ncols, nnz, rows, cols, nnz > 0 ? vals : &dummy, mem, out_nnz, rows_out,
+                           cols_out, vals_out, nullptr, nullptr);
+}
+
+extern "C" int sparsla_coo_sort_device(int device, int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* rows,
+                                       const int64_t* cols, int32_t mem, int64_t* out_nnz, int64_t* order,
+                                       int64_t* group) {
+    if (nnz > 0 && (!order || !group)) {
+        set_last_error("order / group is null");
+        return SPARSLA_ERR_INVALID_ARGUMENT;
+    }
+    return coo_device_impl(device, nrows, ncols, nnz, rows, cols, nullptr, mem, out_nnz, nullptr, nullptr, nullptr,
+                           order, group);
 }

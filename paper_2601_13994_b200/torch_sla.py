@@ -32,13 +32,28 @@ class SparseTensor:
         if values.dtype != torch.float64:
             raise S.InvalidArgumentError("torch-sla B200 path computes in float64")
         n, m = int(shape[0]), int(shape[1])
-        # canonical pattern + map input entry -> canonical entry (host, SparseCoo order)
-        order = np.lexsort((np.arange(len(row)), col, row))  # stable by (row, col, input index)
-        r_s, c_s = row[order], col[order]
-        new = np.ones(len(order), bool)
-        if len(order):
-            new[1:] = (r_s[1:] != r_s[:-1]) | (c_s[1:] != c_s[:-1])
-        group = np.cumsum(new) - 1
+        # canonical pattern + map input entry -> canonical entry (SparseCoo order: stable by
+        # (row, col, input index)); large inputs are sorted on the GPU (radix sort, same order)
+        dev = values.device.index if values.is_cuda else (device or 0)
+        if len(row) >= (1 << 17):
+            order = np.empty(len(row), np.int64)
+            group = np.empty(len(row), np.int64)
+            m_out = C.c_int64()
+            S._check(S.lib().sparsla_coo_sort_device(
+                C.c_int(dev), C.c_int64(int(shape[0])), C.c_int64(int(shape[1])), C.c_int64(len(row)),
+                S._p(row, S._i64p), S._p(col, S._i64p), C.c_int32(S.MEM_HOST), C.byref(m_out),
+                S._p(order, S._i64p), S._p(group, S._i64p)))
+            new = np.ones(len(order), bool)
+            if len(order):
+                new[1:] = group[1:] != group[:-1]
+            r_s, c_s = row[order], col[order]
+        else:
+            order = np.lexsort((np.arange(len(row)), col, row))
+            r_s, c_s = row[order], col[order]
+            new = np.ones(len(order), bool)
+            if len(order):
+                new[1:] = (r_s[1:] != r_s[:-1]) | (c_s[1:] != c_s[:-1])
+            group = np.cumsum(new) - 1
         self._group_of_input = np.empty(len(row), np.int64)
         self._group_of_input[order] = group
         self._order = order
@@ -46,7 +61,7 @@ class SparseTensor:
         self.csr = S.CsrMatrix.from_coo(coo)
         self.shape = (n, m)
         self.values = values
-        self.device = values.device.index if values.is_cuda else (device or 0)
+        self.device = dev
         self._dup = bool((~new).any())
         self._order_t = None
         self._group_t = None

@@ -66,3 +66,50 @@ def test_generator_triplets_at_scale(S, O, gpu):
     A = S.generate("fem2d", 300, 2601)
     assert np.array_equal(a.cols, A.col_idx) and np.array_equal(bits(a.vals), bits(A.vals))
     assert np.array_equal(np.repeat(np.arange(n), np.diff(A.row_ptr)), a.rows)
+
+
+def test_sort_permutation_matches_host_order(S, gpu):
+    """sparsla_coo_sort_device: the stable (row, col, input) order and the canonical entry of
+    every sorted position, as numpy's lexsort gives them."""
+    import ctypes as C
+    rng = np.random.default_rng(11)
+    n, nnz = 5000, 400000
+    rows, cols = rng.integers(0, n, nnz), rng.integers(0, n // 50, nnz)
+    order = np.empty(nnz, np.int64)
+    group = np.empty(nnz, np.int64)
+    m = C.c_int64()
+    S._check(S.lib().sparsla_coo_sort_device(C.c_int(0), C.c_int64(n), C.c_int64(n), C.c_int64(nnz),
+                                             S._p(rows, S._i64p), S._p(cols, S._i64p), C.c_int32(0), C.byref(m),
+                                             S._p(order, S._i64p), S._p(group, S._i64p)))
+    ref = np.lexsort((np.arange(nnz), cols, rows))
+    assert np.array_equal(order, ref)
+    r_s, c_s = rows[ref], cols[ref]
+    new = np.ones(nnz, bool)
+    new[1:] = (r_s[1:] != r_s[:-1]) | (c_s[1:] != c_s[:-1])
+    assert np.array_equal(group, np.cumsum(new) - 1) and m.value == int(new.sum())
+
+
+def test_torch_sparse_tensor_large_unsorted_input(S, O, gpu):
+    """SparseTensor from 300K shuffled triplets with duplicates (GPU sort path): the solve
+    and its gradients equal those of the canonical matrix."""
+    import torch
+    from paper_2601_13994_b200.torch_sla import SparseTensor
+    A = O.generate("poisson2d", 120)
+    rows = np.repeat(np.arange(A.nrows), np.diff(A.row_ptr))
+    # duplicates: every entry split into halves, then shuffled
+    r = np.concatenate([rows, rows])
+    c = np.concatenate([A.col_idx, A.col_idx])
+    v = np.concatenate([A.vals * 0.5, A.vals * 0.5])
+    perm = np.random.default_rng(5).permutation(len(r))
+    vals = torch.tensor(v[perm], dtype=torch.float64, device="cuda:0", requires_grad=True)
+    T = SparseTensor(vals, r[perm], c[perm], (A.nrows, A.ncols))
+    assert len(r) >= (1 << 17) and T.nnz == A.nnz
+    b = torch.ones(A.nrows, dtype=torch.float64, device="cuda:0")
+    x = T.solve(b, atol=1e-12)
+    xo, _ = O.cg(A, np.ones(A.nrows), atol=1e-12)
+    assert np.max(np.abs(x.detach().cpu().numpy() - xo)) <= 1e-12 * np.max(np.abs(xo))
+    x.sum().backward()
+    g = vals.grad.cpu().numpy()
+    # both halves of an entry get the gradient of their canonical entry
+    inv = np.empty_like(perm); inv[perm] = np.arange(len(perm))
+    assert np.array_equal(g[inv[:len(rows)]], g[inv[len(rows):]])
