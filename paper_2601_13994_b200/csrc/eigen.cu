@@ -154,6 +154,33 @@ __global__ void __launch_bounds__(kT) spmm_kernel(const int32_t* __restrict__ rp
     }
 }
 
+// Coalesced block SpMV for a contiguous, even-aligned column range of NW columns: L = NW/2
+// lanes share a row (each owns one double2 column pair), 32/L rows per warp.  Every gathered
+// row segment S[c, in:in+NW] is one contiguous NW*8-byte access by the row's lanes (one or two
+// L1 wavefronts instead of NW/2 scattered 16-byte requests), the row's (col, val) pairs are
+// broadcast loads, and the outputs are contiguous double2 stores.
+template <int NW>
+__global__ void __launch_bounds__(kT) spmm_lanes_kernel(const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                                        const double* __restrict__ val, long long n,
+                                                        const double* __restrict__ S, int lds, int c_in,
+                                                        double* Y, int ldy, int c_out) {
+    constexpr int L = NW / 2, RPW = 32 / L;
+    const int lane = threadIdx.x & 31, sub = lane / L, part = lane - sub * L;
+    const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long i = warp * RPW + sub;
+    if (sub >= RPW || i >= n) return;
+    const int kb = __ldg(rp + i), ke = __ldg(rp + i + 1);
+    double2 acc = make_double2(0.0, 0.0);
+    const double* base = S + c_in + 2 * part;
+    for (int k = kb; k < ke; ++k) {
+        const double v = __ldg(val + k);
+        const double2 x = __ldg(reinterpret_cast<const double2*>(base + (size_t)__ldg(ci + k) * lds));
+        acc.x = fma(v, x.x, acc.x);
+        acc.y = fma(v, x.y, acc.y);
+    }
+    *reinterpret_cast<double2*>(Y + i * ldy + c_out + 2 * part) = acc;
+}
+
 #define SPARSLA_FOR_1_32(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16) \
     X(17) X(18) X(19) X(20) X(21) X(22) X(23) X(24) X(25) X(26) X(27) X(28) X(29) X(30) X(31) X(32)
 
@@ -659,6 +686,11 @@ __global__ void sym_tol_kernel(const int32_t* rp, const int32_t* ci, const doubl
 }
 
 // Y[:, out] = A X[:, in] in groups of <= 16 columns (templated register blocks).
+bool lanes_off() {
+    static const bool off = [] { const char* e = std::getenv("SPARSLA_SPMM_LANES"); return e && std::atoi(e) == 0; }();
+    return off;
+}
+
 void launch_spmm(const DevCsr* A, const double* X, int ldx, const Cols& in, double* Y, int ldy, const Cols& out,
                  cudaStream_t st) {
     const long long n = A->nrows;
@@ -671,6 +703,20 @@ void launch_spmm(const DevCsr* A, const double* X, int ldx, const Cols& in, doub
             ci.c[j] = in.c[b + j];
             co.c[j] = out.c[b + j];
             if (j && (ci.c[j] != ci.c[j - 1] + 1 || co.c[j] != co.c[j - 1] + 1)) contig = false;
+        }
+        if (contig && ci.n >= 4 && !lanes_off()) {  // coalesced lanes-per-row kernel
+            const long long rpw = 32 / (ci.n / 2);
+            const unsigned gl = (unsigned)((n + rpw * (kT / 32) - 1) / (rpw * (kT / 32)));
+            switch (ci.n) {
+#define SPARSLA_SPMML(W) \
+    case W: spmm_lanes_kernel<W><<<gl, kT, 0, st>>>(A->rp, A->ci, A->val, n, X, ldx, ci.c[0], Y, ldy, co.c[0]); break;
+                SPARSLA_SPMML(4) SPARSLA_SPMML(6) SPARSLA_SPMML(8) SPARSLA_SPMML(10) SPARSLA_SPMML(12)
+                SPARSLA_SPMML(14) SPARSLA_SPMML(16)
+#undef SPARSLA_SPMML
+                default: fail(SPARSLA_ERR_INTERNAL, "spmm: bad column count");
+            }
+            CK(cudaGetLastError());
+            continue;
         }
         switch (ci.n * 2 + (contig ? 1 : 0)) {
 #define SPARSLA_SPMM(W) \
