@@ -255,12 +255,24 @@ struct sparsla_dist {
     std::vector<int64_t> all_count;  // rank 0: owned count per rank
     long long n_global = 0;
     long long alg_exchanges = 0, alg_allreduces = 0, alg_messages = 0;  // live algorithm work
+    // parked host-buffer solvers per backend (workspace, graphs, fused-collective mappings),
+    // reused by the next collective solve with the same preconditioner and fused setting
+    Solver* parked[2] = {nullptr, nullptr};
+    bool parked_fused[2] = {false, false};
     ~sparsla_dist() {
-        if (A) { DeviceGuard g(A->device, true); ctx.reset(); delete AT; delete A; }
+        if (A) {
+            DeviceGuard g(A->device, true);
+            for (auto*& p : parked) { delete p; p = nullptr; }
+            ctx.reset(); delete AT; delete A;
+        }
     }
 };
 
 namespace {
+bool solver_cache_enabled() {
+    static const bool on = [] { const char* e = getenv("SPARSLA_SOLVER_CACHE"); return !e || atoi(e) != 0; }();
+    return on;
+}
 
 bool contiguous_range(const std::vector<int64_t>& v, size_t b, size_t e, long long& base) {
     if (b == e) { base = 0; return true; }
@@ -438,7 +450,22 @@ void dist_krylov(sparsla_dist* D, int backend, const double* b, double* x, const
                  sparsla_solve_report* rep, int mem, DevCsr* M = nullptr) {
     DevCsr* A = M ? M : D->A;
     DeviceGuard g(A->device);
-    Solver S(A, backend, *o, D->ctx.get());
+    // every rank makes the same parking decisions (same call sequence), so collective setup
+    // inside a new Solver happens on all ranks or on none
+    const int slot = backend == SPARSLA_BACKEND_CG ? 0 : 1;
+    const bool cache = !M && mem != SPARSLA_MEM_DEVICE && solver_cache_enabled();
+    std::unique_ptr<Solver> Sp;
+    if (cache && D->parked[slot] && D->parked[slot]->opts.preconditioner == o->preconditioner &&
+        D->parked_fused[slot] == D->ctx->p2p_enabled) {
+        Solver::validate(*o, true);
+        Sp.reset(D->parked[slot]);
+        D->parked[slot] = nullptr;
+        Sp->opts = *o;
+    } else {
+        if (cache && D->parked[slot]) { delete D->parked[slot]; D->parked[slot] = nullptr; }
+        Sp = std::make_unique<Solver>(A, backend, *o, D->ctx.get());
+    }
+    Solver& S = *Sp;
     S.set_b(b, mem);
     if (mem == SPARSLA_MEM_DEVICE) S.x = x;
     S.reset();
@@ -450,6 +477,10 @@ void dist_krylov(sparsla_dist* D, int backend, const double* b, double* x, const
     if (mem != SPARSLA_MEM_DEVICE && A->nrows)
         CKD(cudaMemcpyAsync(x, S.x, A->nrows * 8, cudaMemcpyDeviceToHost, A->stream));
     CKD(cudaStreamSynchronize(A->stream));
+    if (cache) {
+        D->parked_fused[slot] = D->ctx->p2p_enabled;
+        D->parked[slot] = Sp.release();
+    }
 }
 
 }  // namespace

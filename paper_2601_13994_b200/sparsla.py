@@ -951,19 +951,19 @@ class DistPlan:
         _check(lib().sparsla_dist_spmv(self.h, _p(x, _f64p), _p(y, _f64p), C.c_int32(MEM_HOST)))
         return y
 
-    def _solve(self, fn, b_owned, opts):
+    def _solve(self, fn, b_owned, opts, out=None):
         b = _f64(b_owned)
-        x = np.empty(self.n_owned)
+        x = np.empty(self.n_owned) if out is None else out  # out: e.g. a pinned host buffer
         rep = _Report()
         o = (opts or SolveOptions()).c()
         _check(fn(self.h, _p(b, _f64p), _p(x, _f64p), C.byref(o), C.byref(rep), C.c_int32(MEM_HOST)))
         return x, SolveReport._from(rep)
 
-    def cg(self, b_owned, opts: SolveOptions | None = None):
-        return self._solve(lib().sparsla_dist_cg_solve, b_owned, opts)
+    def cg(self, b_owned, opts: SolveOptions | None = None, out=None):
+        return self._solve(lib().sparsla_dist_cg_solve, b_owned, opts, out)
 
-    def bicgstab(self, b_owned, opts: SolveOptions | None = None):
-        return self._solve(lib().sparsla_dist_bicgstab_solve, b_owned, opts)
+    def bicgstab(self, b_owned, opts: SolveOptions | None = None, out=None):
+        return self._solve(lib().sparsla_dist_bicgstab_solve, b_owned, opts, out)
 
     def adjoint(self, x_owned, g_owned, vals_t=None, backend="cg", opts: SolveOptions | None = None):
         x, g = _f64(x_owned), _f64(g_owned)
