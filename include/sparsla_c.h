@@ -92,6 +92,11 @@ int sparsla_coo_canonicalize_device(int device, int64_t nrows, int64_t ncols, in
 int sparsla_coo_sort_device(int device, int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* rows,
                             const int64_t* cols, int32_t mem, int64_t* out_nnz, int64_t* order,
                             int64_t* group);
+/* SparseCoo::with_values for triplets that carried duplicates (sparse.hpp:58-61 over the
+ * pattern sparse.cpp:9-53 built): DEVICE arrays order/group from sparsla_coo_sort_device and
+ * input-order vals[nnz] -> canonical vals_out[nout], each sum left to right in input order. */
+int sparsla_coo_group_sum_device(int device, int64_t nnz, int64_t nout, const int64_t* order,
+                                 const int64_t* group, const double* vals, double* vals_out);
 /* CsrMatrix::from_coo (sparse.hpp:84, sparse.cpp:94-116), input must be canonical. */
 int sparsla_csr_from_coo(int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* rows,
                          const int64_t* cols, const double* vals, int64_t* row_ptr,

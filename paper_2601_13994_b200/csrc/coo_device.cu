@@ -78,6 +78,19 @@ __global__ void coo_perm_kernel(const int32_t* idx, const int32_t* seg, long lon
     group[j] = (int64_t)seg[j] - 1;
 }
 
+// one thread per group head in sorted order: out[group[j]] = vals[order[j]] + ... left to right
+// over the group's sorted positions (the reference's vals_.back() += vals[p], sparse.cpp:45-47)
+__global__ void group_sum_kernel(const int64_t* order, const int64_t* group, const double* vals, long long nnz,
+                                 double* out) {
+    const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= nnz) return;
+    const int64_t g = group[j];
+    if (j > 0 && group[j - 1] == g) return;
+    double s = vals[order[j]];
+    for (long long i = j + 1; i < nnz && group[i] == g; ++i) s = __dadd_rn(s, vals[order[i]]);
+    out[g] = s;
+}
+
 __global__ void csr_rows_kernel(const int32_t* rp, long long n, int32_t* rows) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -280,4 +293,24 @@ extern "C" int sparsla_coo_sort_device(int device, int64_t nrows, int64_t ncols,
     }
     return coo_device_impl(device, nrows, ncols, nnz, rows, cols, nullptr, mem, out_nnz, nullptr, nullptr, nullptr,
                            order, group);
+}
+
+// Values of a canonicalised pattern from new input-order values (the with_values step of a
+// differentiable SparseCoo whose triplets carry duplicates): device arrays order[nnz],
+// group[nnz] from sparsla_coo_sort_device, vals[nnz] in input order -> vals_out[nout].
+extern "C" int sparsla_coo_group_sum_device(int device, int64_t nnz, int64_t nout, const int64_t* order,
+                                            const int64_t* group, const double* vals, double* vals_out) {
+    return guarded([&] {
+        if (nnz < 0 || nout < 0 || nout > nnz) fail(SPARSLA_ERR_DIMENSION, "bad nnz / nout");
+        if (nnz >= (1LL << 31)) fail(SPARSLA_ERR_UNSUPPORTED, "group sum: nnz must be < 2^31");
+        if (nnz > 0 && (!order || !group || !vals || !vals_out)) fail(SPARSLA_ERR_INVALID_ARGUMENT, "null pointer");
+        if (nnz == 0) return;
+        DeviceGuard g(device);
+        cudaStream_t s = nullptr;
+        CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        struct StreamGuard { cudaStream_t s; ~StreamGuard() { cudaStreamDestroy(s); } } sg{s};
+        group_sum_kernel<<<(unsigned)((nnz + 255) / 256), 256, 0, s>>>(order, group, vals, nnz, vals_out);
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(s));
+    });
 }

@@ -5,6 +5,11 @@
     loss(x).backward()                              # one adjoint solve (Alg. 1, Eq. 3)
     lam, V = A.eigsh(k=6)                           # LOBPCG; d(lam)/d(values) by Eq. 4
 
+    # one process per GPU: this rank's partition of the same triplets
+    D = DSparseMatrix.from_global(values, row, col, (n, n), num_partitions=P, my_partition=rank)
+    x_local = D.solve(b_local, atol=1e-10)           # distributed CG / BiCGStab, halo exchange
+    x_local.sum().backward()                         # one distributed adjoint solve
+
 Forward and backward run on the sm_100a Krylov loop through the C ABI with zero-copy device
 pointers (SPARSLA_MEM_DEVICE).  Backward is exactly one transposed solve plus the per-entry
 gather grad_vals[k] = -lambda[row_k] * x[col_k] (solve_backward); the
@@ -97,21 +102,24 @@ class SparseTensor:
 
 
 class _DupSum(torch.autograd.Function):
+    """Canonical values of triplets with duplicates: each canonical entry is the left-to-right
+    sum of its duplicates in input order (sparse.cpp:45-47), one GPU thread per entry."""
+
     @staticmethod
     def forward(ctx, v, A):
-        order = A._order
-        grp = A._group_of_input[order]
-        vs = v.detach().cpu().numpy()[order]
-        out = np.empty(A.nnz)
-        k = -1
-        for i, g in enumerate(grp):  # vals_.back() += vals[p] in stable (row, col, input) order
-            if g != k:
-                out[g] = vs[i]
-                k = g
-            else:
-                out[g] += vs[i]
+        v = v.detach().to(torch.float64).contiguous()
+        if A._group_t is None or A._order_t.device != v.device:
+            A._order_t = torch.as_tensor(A._order, device=v.device)
+            A._group_t = torch.as_tensor(A._group_of_input[A._order], device=v.device)
+        out = torch.empty(A.nnz, dtype=torch.float64, device=v.device)
+        torch.cuda.current_stream(v.device).synchronize()  # the library runs on its own stream
+        i64 = C.POINTER(C.c_int64)
+        S._check(S.lib().sparsla_coo_group_sum_device(
+            C.c_int(v.device.index), C.c_int64(v.numel()), C.c_int64(A.nnz),
+            C.cast(C.c_void_p(A._order_t.data_ptr()), i64), C.cast(C.c_void_p(A._group_t.data_ptr()), i64),
+            _ptr(v), _ptr(out)))
         ctx.A = A
-        return torch.as_tensor(out, device=v.device)
+        return out
 
     @staticmethod
     def backward(ctx, g):
@@ -205,3 +213,151 @@ class _Eigsh(torch.autograd.Function):
         S._check(S.lib().sparsla_eig_backward(D.h, C.c_int64(len(g)), S._p(ctx.lam, S._f64p), _ptr(V),
                                               S._p(g, S._f64p), _ptr(gv), C.c_int32(S.MEM_DEVICE)))
         return gv, None, None, None, None, None
+
+
+class DSparseMatrix:
+    """One partition of a row-partitioned matrix, held by one process of a torch.distributed
+    job (PAPER.md:485-500; SPEC.md:417-544).  Every process passes the same global triplets;
+    it keeps the rows `part_of == my_partition` (partition_contiguous by default, RCB over
+    `coords`, or an explicit part_of array) and builds the distributed plan over them.
+    Transport: NCCL when the default process group is NCCL (one GPU per rank), else host
+    callbacks over the process group (gloo; ranks may share a GPU); with `fused` the Krylov
+    iterations run through peer-memory collectives.  `solve` is differentiable: the backward
+    is one distributed adjoint solve (dist_adjoint_solve); the gradient
+    w.r.t. the global values is this partition's rows' entries (zero elsewhere), so summing
+    it over ranks gives the full gradient."""
+
+    def __init__(self):
+        raise TypeError("use DSparseMatrix.from_global(...)")
+
+    @classmethod
+    def from_global(cls, values: torch.Tensor, row, col, shape, num_partitions: int, my_partition: int,
+                    part_of=None, coords=None, device: int | None = None, fused: bool = True, group=None):
+        import torch.distributed as dist
+        P, rank = int(num_partitions), int(my_partition)
+        if P < 1 or not 0 <= rank < P:
+            raise S.InvalidArgumentError(f"my_partition {rank} outside [0, {P})")
+        initialized = dist.is_available() and dist.is_initialized()
+        if initialized and dist.get_world_size(group) != P:
+            raise S.InvalidArgumentError("num_partitions must equal the process group's world size")
+        if not initialized and P != 1:
+            raise S.InvalidArgumentError("num_partitions > 1 needs an initialized torch.distributed group")
+        if initialized and dist.get_rank(group) != rank:
+            raise S.InvalidArgumentError("my_partition must equal this process's rank")
+        if device is None:
+            device = values.device.index if values.is_cuda else torch.cuda.current_device()
+        self = object.__new__(cls)
+        T = SparseTensor(values, row, col, shape, device=device)
+        n = T.shape[0]
+        if T.shape[0] != T.shape[1]:
+            raise S.DimensionError("DSparseMatrix needs a square matrix")
+        if part_of is not None:
+            part_of = np.ascontiguousarray(part_of, np.int32)
+            if len(part_of) != n:
+                raise S.DimensionError("part_of length must equal the number of rows")
+        elif coords is not None:
+            part_of = S.partition_rcb(coords[0], coords[1], P)
+        owned = (np.arange(n, dtype=np.int64) if part_of is None and P == 1 else
+                 np.nonzero((part_of if part_of is not None else S.partition_contiguous(n, P)) == rank)[0])
+        rp = T.csr.row_ptr
+        lens = np.diff(rp)[owned]
+        lrp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+        ent = (np.repeat(rp[owned] - lrp[:-1], lens) + np.arange(lrp[-1])) if len(owned) else np.zeros(0, np.int64)
+        self.T, self.owned, self.entries, self.n_global, self.device = T, owned, ent, n, device
+        self.part_of = part_of
+        self._ent_t = None
+        vals = T.canonical_values().detach().cpu().numpy()
+        rows = S.CsrMatrix(len(owned), n, lrp, T.csr.col_idx[ent], vals[ent])
+        if P == 1 and not initialized:
+            self._hub = S.LocalHub(1)
+            self.plan = S.DistPlan.create_local(self._hub, device, 0, rows, owned, part_of, n)
+        elif dist.get_backend(group) == "nccl":
+            uid = [S.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=dist.get_global_rank(group, 0) if group is not None else 0,
+                                       group=group)
+            self.plan = S.DistPlan.create_nccl(device, P, rank, uid[0], rows, owned, part_of, n)
+        else:
+            self.plan = S.DistPlan.create_host(device, P, rank, S.torch_host_transport(P, group), rows, owned,
+                                               part_of, n)
+        self.plan.set_fused(fused)
+        # value symmetry decides the default backend; A^T's values in the local entry order
+        # serve the nonsymmetric adjoint (the pattern is structurally symmetric)
+        keys = np.repeat(np.arange(n, dtype=np.int64), np.diff(rp)) * n + T.csr.col_idx
+        lr = np.repeat(owned, lens)
+        tpos = np.searchsorted(keys, T.csr.col_idx[ent] * n + lr)
+        vt = vals[np.minimum(tpos, max(len(keys) - 1, 0))] if len(ent) else np.zeros(0)
+        flag = torch.tensor([0.0 if np.array_equal(vt, vals[ent]) else 1.0])
+        if initialized:
+            fl = flag.to(f"cuda:{device}") if dist.get_backend(group) == "nccl" else flag
+            dist.all_reduce(fl, group=group)
+            flag = fl.cpu()
+        self.symmetric = float(flag[0]) == 0.0
+        self.vals_t = None if self.symmetric else np.ascontiguousarray(vt)
+        return self
+
+    @property
+    def n_owned(self):
+        return len(self.owned)
+
+    def solve(self, b_local: torch.Tensor, atol: float = 1e-10, rtol: float = 0.0, max_iter: int = 10000,
+              preconditioner: str = "jacobi", backend: str = "auto") -> torch.Tensor:
+        """Collective: x_local (this partition's owned rows, ascending global index)."""
+        if backend == "auto":
+            backend = "cg" if self.symmetric else "bicgstab"
+        opts = S.SolveOptions(atol=atol, rtol=rtol, max_iter=max_iter, preconditioner=preconditioner)
+        return _DSolve.apply(self.T.canonical_values(), b_local, self, opts, backend)
+
+    def gather(self, x_local: torch.Tensor):
+        """gather_solution: the global x on rank 0 (host numpy), None elsewhere."""
+        return self.plan.gather(x_local.detach().cpu().numpy())
+
+    def close(self):
+        self.plan.close()
+
+
+class _DSolve(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, vals, b, A: DSparseMatrix, opts: S.SolveOptions, backend: str):
+        dev = A.device
+        b = b.detach().to(f"cuda:{dev}", torch.float64).contiguous()
+        if b.numel() != A.n_owned:
+            raise S.DimensionError(f"b_local has {b.numel()} entries, this partition owns {A.n_owned} rows")
+        x = torch.empty_like(b)
+        rep = S._Report()
+        o = opts.c()
+        fn = S.lib().sparsla_dist_cg_solve if backend == "cg" else S.lib().sparsla_dist_bicgstab_solve
+        torch.cuda.current_stream(dev).synchronize()
+        S._check(fn(A.plan.h, _ptr(b), _ptr(x), C.byref(o), C.byref(rep), C.c_int32(S.MEM_DEVICE)))
+        r = S.SolveReport._from(rep)
+        if not r.converged:
+            raise S.Error(f"distributed solve did not converge: {r.diagnostic}")
+        ctx.A, ctx.opts, ctx.backend, ctx.n_vals = A, opts, backend, vals.numel()
+        ctx.save_for_backward(x)
+        ctx.report = r
+        return x
+
+    @staticmethod
+    def backward(ctx, gx):
+        (x,) = ctx.saved_tensors
+        A = ctx.A
+        gx = gx.detach().to(x.device, torch.float64).contiguous()
+        gb = torch.empty_like(x)
+        gv = torch.empty(len(A.entries), dtype=torch.float64, device=x.device)
+        vt = None
+        if A.vals_t is not None and ctx.backend != "cg":
+            vt = torch.as_tensor(A.vals_t, device=x.device)
+        rep = S._Report()
+        o = ctx.opts.c()
+        be = S.BACKEND_CG if ctx.backend == "cg" else S.BACKEND_BICGSTAB
+        torch.cuda.current_stream(x.device).synchronize()
+        S._check(S.lib().sparsla_dist_adjoint_backward(
+            A.plan.h, _ptr(x), _ptr(gx), None if vt is None else _ptr(vt), C.c_int32(be), C.byref(o), _ptr(gb),
+            _ptr(gv), C.byref(rep), C.c_int32(S.MEM_DEVICE)))
+        r = S.SolveReport._from(rep)
+        if not r.converged:
+            raise S.Error(f"distributed adjoint solve did not converge: {r.diagnostic}")
+        if A._ent_t is None:
+            A._ent_t = torch.as_tensor(A.entries, device=x.device)
+        gvals = torch.zeros(ctx.n_vals, dtype=torch.float64, device=x.device)
+        gvals[A._ent_t] = gv
+        return gvals, gb, None, None, None

@@ -95,3 +95,25 @@ def test_eigsh_autograd_eq4(S, O, gpu):
     ent = [0, 7, 100, len(v0) - 1]
     fd = O.eig_fd(A, 4, g.cpu().numpy(), entries=ent)
     assert np.max(np.abs(fd - ref[ent])) / np.max(np.abs(ref[ent])) < 1e-5
+
+
+@pytest.mark.parametrize("nnz", [5000, 300_000])  # host lexsort / GPU radix-sort patterns
+def test_duplicate_values_sum_in_input_order(S, gpu, nnz):
+    """Canonical values of triplets with duplicates come from the GPU group sum and equal the
+    host SparseCoo canonicalization (sparse.cpp:45-47 order) bit for bit; the gradient of
+    every duplicate is its canonical entry's gradient."""
+    import torch
+    from paper_2601_13994_b200.torch_sla import SparseTensor
+    rng = np.random.default_rng(7)
+    n = 64 if nnz < 10_000 else 400
+    r = rng.integers(0, n, nnz)
+    c = rng.integers(0, n, nnz)
+    v = rng.standard_normal(nnz) * 10.0 ** rng.integers(-8, 8, nnz)
+    ref = S.SparseCoo(r, c, v, (n, n))
+    vals = torch.tensor(v, device="cuda:0", requires_grad=True)
+    T = SparseTensor(vals, r, c, (n, n))
+    cv = T.canonical_values()
+    assert np.array_equal(bits(cv.detach().cpu().numpy()), bits(ref.vals))
+    w = torch.linspace(-1.0, 1.0, T.nnz, dtype=torch.float64, device="cuda:0")
+    (cv * w).sum().backward()
+    assert np.array_equal(vals.grad.cpu().numpy(), w.cpu().numpy()[T._group_of_input])

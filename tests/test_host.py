@@ -226,3 +226,16 @@ def test_eig_backward_argument_checks(S):
 def test_options_validation(S):
     with pytest.raises(S.InvalidArgumentError):
         S.SolveOptions(preconditioner="ilu").c()
+
+
+def test_dsparse_argument_errors(S):
+    """DSparseMatrix.from_global checks its partition arguments before touching a device."""
+    import torch
+    from paper_2601_13994_b200.torch_sla import DSparseMatrix
+    v = torch.ones(3, dtype=torch.float64)
+    with pytest.raises(S.InvalidArgumentError):
+        DSparseMatrix.from_global(v, [0, 1, 2], [0, 1, 2], (3, 3), num_partitions=2, my_partition=0)
+    with pytest.raises(S.InvalidArgumentError):
+        DSparseMatrix.from_global(v, [0, 1, 2], [0, 1, 2], (3, 3), num_partitions=1, my_partition=1)
+    with pytest.raises(TypeError):
+        DSparseMatrix()
