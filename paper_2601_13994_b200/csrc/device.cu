@@ -582,12 +582,33 @@ Solver::Solver(DevCsr* A_, int backend_, const sparsla_solve_options& o, DistCtx
         int coop = 0, sms = 0, per_sm = 0;
         CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, A->device));
         CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, A->device));
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cg_fused_kernel, kSpmvThreads, 0));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cg_fused_kernel<false>, kSpmvThreads, 0));
         const long long cap = (long long)sms * per_sm;
         fused_grid = (int)std::min<long long>(m, cap);
         fused = coop && cap > 0 && m <= cap;  // one chunk per CTA (measured: 2 per CTA ~ break-even)
         if (const char* e = getenv("SPARSLA_FUSED")) fused = coop && cap > 0 && atoi(e) != 0;
         if (fused) { fused_bar = dalloc<unsigned>(1); }
+        // resident chunk images when every chunk fits uint16 offsets / int16 column deltas and
+        // the whole grid stays co-resident with the larger shared-memory footprint
+        const char* re = getenv("SPARSLA_FUSED_RESIDENT");
+        if (fused && m <= cap && !(re && atoi(re) == 0)) {
+            int* chk = dalloc<int>(2);
+            int h[2] = {0, 0};
+            CK(cudaMemsetAsync(chk, 0, 8, stream));
+            fused_res_check_kernel<<<(unsigned)m, kSpmvThreads, 0, stream>>>(A->rp, A->ci, n, chk);
+            CK(cudaGetLastError());
+            CK(cudaMemcpyAsync(h, chk, 8, cudaMemcpyDeviceToHost, stream));
+            CK(cudaStreamSynchronize(stream));
+            cudaFree(chk);
+            if (h[0] <= 65535 && h[1] == 0) {
+                const int cap_e = (h[0] + 7) / 8 * 8;
+                const size_t bytes = fused_res_bytes(cap_e);
+                int rs = 0;
+                CK(cudaFuncSetAttribute(cg_fused_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&rs, cg_fused_kernel<true>, kSpmvThreads, bytes));
+                if ((long long)sms * rs >= m) { fused_res = cap_e; fused_grid = (int)m; }
+            }
+        }
     }
     tickets = dalloc<unsigned>(8);
     CK(cudaMemset(tickets, 0, 8 * sizeof(unsigned)));
@@ -822,8 +843,14 @@ void Solver::enqueue_fused(long long iters) {
         F.iters = (int)std::min<long long>(iters, 1 << 20);
         CK(cudaMemsetAsync(fused_bar, 0, sizeof(unsigned), stream));
         void* args[] = {&F};
-        CK(cudaLaunchCooperativeKernel((const void*)cg_fused_kernel, dim3(fused_grid), dim3(kSpmvThreads), args, 0,
-                                       stream));
+        if (fused_res > 0 && F.vidx) {
+            F.res_cap = fused_res;
+            CK(cudaLaunchCooperativeKernel((const void*)cg_fused_kernel<true>, dim3(fused_grid), dim3(kSpmvThreads),
+                                           args, fused_res_bytes(fused_res), stream));
+        } else {
+            CK(cudaLaunchCooperativeKernel((const void*)cg_fused_kernel<false>, dim3(fused_grid), dim3(kSpmvThreads),
+                                           args, 0, stream));
+        }
         iters -= F.iters;
     }
 }

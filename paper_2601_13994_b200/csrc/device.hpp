@@ -142,6 +142,7 @@ struct Solver {
     std::vector<void*> p2p_allocs, p2p_ipc_opened;
     int fused_grid = 0;
     unsigned* fused_bar = nullptr;
+    int fused_res = 0;               // > 0: resident chunk images of this many entries (cg_fused_kernel<true>)
 
     DistCtx* dist = nullptr;
     Solver(DevCsr* A, int backend, const sparsla_solve_options& o, DistCtx* dist = nullptr);

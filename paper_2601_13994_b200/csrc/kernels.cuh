@@ -1353,7 +1353,33 @@ struct FusedParams {
     unsigned* bar;     // grid barrier counter, zeroed before every launch
     KState* st;
     int iters;         // iterations this launch (stops earlier when the solve terminates)
+    int res_cap;       // RES: entry capacity of the chunk image in shared memory
 };
+
+// Resident chunk image (RES): the matrix does not change across iterations, so each CTA
+// keeps its chunk's structure in shared memory for the whole launch — uint16 local row
+// offsets, int16 column deltas (col - row) and the 1-byte dictionary indices — and the
+// SpMV's only global accesses are the p gathers (one L2 round trip per row instead of
+// three: row_ptr -> col/val -> p).
+__host__ __device__ constexpr size_t fused_res_bytes(int cap) {
+    return (((size_t)kChunk + 1) * 2 + 15) / 16 * 16 + ((size_t)cap * 2 + 15) / 16 * 16 + ((size_t)cap + 15) / 16 * 16;
+}
+
+// Host-side eligibility of the resident image: res[0] = max entries of a chunk, res[1] = 1
+// if some |col - row| exceeds the int16 range.
+static __global__ void __launch_bounds__(kSpmvThreads) fused_res_check_kernel(const int32_t* rp, const int32_t* ci,
+                                                                              long long n, int* res) {
+    const long long c = blockIdx.x, base = c * kChunk;
+    const long long end = base + kChunk < n ? base + kChunk : n;
+    if (threadIdx.x == 0) atomicMax(res, rp[end] - rp[base]);
+    bool far = false;
+    for (long long i = base + threadIdx.x; i < end; i += blockDim.x)
+        for (int k = rp[i]; k < rp[i + 1]; ++k) {
+            const long long d = (long long)ci[k] - i;
+            far |= d < -32768 || d > 32767;
+        }
+    if (far) atomicMax(res + 1, 1);
+}
 
 __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned& epoch) {
     __syncthreads();
@@ -1383,14 +1409,37 @@ __device__ __forceinline__ void fused_total(const double* partials, long long m,
     __syncthreads();
 }
 
+constexpr int kPairW = 6;  // RES: rows of <= kPairW entries are processed two at a time
+
+template <bool RES>
 static __global__ void __launch_bounds__(kSpmvThreads, 4) cg_fused_kernel(FusedParams P) {
     __shared__ KState S;
     __shared__ double sred[3 * (kSpmvThreads / 32)];
     __shared__ double sbc[4];
     __shared__ double s_vtab[256];
+    extern __shared__ __align__(16) unsigned char fres[];
     const int t = threadIdx.x;
     if (t == 0) S = *P.st;
     if (P.vidx) s_vtab[t] = P.vtab[t];  // kSpmvThreads == 256
+    [[maybe_unused]] uint16_t* s_rp = reinterpret_cast<uint16_t*>(fres);
+    [[maybe_unused]] int16_t* s_cd = reinterpret_cast<int16_t*>(fres + (((size_t)kChunk + 1) * 2 + 15) / 16 * 16);
+    [[maybe_unused]] uint8_t* s_vi =
+        fres + (((size_t)kChunk + 1) * 2 + 15) / 16 * 16 + ((size_t)P.res_cap * 2 + 15) / 16 * 16;
+    if constexpr (RES) {  // one chunk per CTA (gridDim.x == nch): load its image once
+        const long long base = (long long)blockIdx.x * kChunk;
+        const int e0 = __ldg(P.rp + base);
+        for (int li = t; li <= kChunk; li += kSpmvThreads) {
+            const long long row = base + li < P.n ? base + li : P.n;
+            s_rp[li] = (uint16_t)(__ldg(P.rp + row) - e0);
+        }
+        for (int li = t; li < kChunk && base + li < P.n; li += kSpmvThreads) {
+            const long long row = base + li;
+            for (int k = __ldg(P.rp + row); k < __ldg(P.rp + row + 1); ++k) {
+                s_cd[k - e0] = (int16_t)(__ldg(P.ci + k) - row);
+                s_vi[k - e0] = __ldg(P.vidx + k);  // RES implies the value dictionary
+            }
+        }
+    }
     __syncthreads();
     if (S.done) return;
     const uint8_t* __restrict__ vidx = P.vidx;
@@ -1398,7 +1447,65 @@ static __global__ void __launch_bounds__(kSpmvThreads, 4) cg_fused_kernel(FusedP
     const long long m = P.nch;
     for (int it = 0; it < P.iters; ++it) {
         // ---- SpMV q = A p (thread per row, L2-coherent gathers) + p.q chunk partials
-        for (long long c = blockIdx.x; c < m; c += gridDim.x) {
+        if constexpr (RES) {
+            const long long base = (long long)blockIdx.x * kChunk;
+            double acc[1] = {0.0};
+#pragma unroll 1
+            for (int r = 0; r < kChunkRounds; r += 2) {
+                // two rows per step: both rows' gathers are in flight together
+                const int la = r * kChunkSlots + t, lb = la + kChunkSlots;
+                const long long ra = base + la, rb = base + lb;
+                const int ka = s_rp[la], kea = s_rp[la + 1], kb = s_rp[lb], keb = s_rp[lb + 1];
+                if (rb < P.n && kea - ka <= kPairW && keb - kb <= kPairW) {
+                    double xa[kPairW], xb[kPairW];
+#pragma unroll
+                    for (int u = 0; u < kPairW; ++u) {
+                        if (ka + u < kea) xa[u] = __ldcg(P.p + ra + s_cd[ka + u]);
+                        if (kb + u < keb) xb[u] = __ldcg(P.p + rb + s_cd[kb + u]);
+                    }
+                    double ya = 0.0, yb = 0.0;
+#pragma unroll
+                    for (int u = 0; u < kPairW; ++u) {
+                        if (ka + u < kea)
+                            ya = __dadd_rn(ya, __dmul_rn(s_vtab[s_vi[ka + u]], xa[u]));
+                    }
+#pragma unroll
+                    for (int u = 0; u < kPairW; ++u) {
+                        if (kb + u < keb)
+                            yb = __dadd_rn(yb, __dmul_rn(s_vtab[s_vi[kb + u]], xb[u]));
+                    }
+                    P.q[ra] = ya;
+                    P.q[rb] = yb;
+                    acc[0] = __dadd_rn(acc[0], __dmul_rn(__ldcg(P.p + ra), ya));
+                    acc[0] = __dadd_rn(acc[0], __dmul_rn(__ldcg(P.p + rb), yb));
+                    continue;
+                }
+#pragma unroll 1
+                for (int h = 0; h < 2; ++h) {
+                const int li = h ? lb : la;
+                const long long row = base + li;
+                if (row < P.n) {
+                    const int kk = s_rp[li], ke = s_rp[li + 1];
+                    double y = 0.0;
+                    for (int k0 = kk; k0 < ke; k0 += 8) {
+                        double pr[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u)
+                            if (k0 + u < ke)
+                                pr[u] = __dmul_rn(s_vtab[s_vi[k0 + u]], __ldcg(P.p + row + s_cd[k0 + u]));
+#pragma unroll
+                        for (int u = 0; u < 8; ++u)
+                            if (k0 + u < ke) y = __dadd_rn(y, pr[u]);
+                    }
+                    P.q[row] = y;
+                    acc[0] = __dadd_rn(acc[0], __dmul_rn(__ldcg(P.p + row), y));
+                }
+                }
+            }
+            block_tree<kSpmvThreads, 1>(acc, sred);
+            if (t == 0) P.partials[blockIdx.x] = acc[0];
+        }
+        for (long long c = blockIdx.x; !RES && c < m; c += gridDim.x) {
             const long long base = c * kChunk;
             double acc[1] = {0.0};
             int kk = 0, ke = 0;
@@ -1458,13 +1565,7 @@ static __global__ void __launch_bounds__(kSpmvThreads, 4) cg_fused_kernel(FusedP
         }
         grid_barrier(P.bar, epoch);
         double rr2[2];
-        {
-            double a[1], b2[1];
-            fused_total<1>(P.partials + m, m, a, sred, sbc);
-            fused_total<1>(P.partials + 2 * m, m, b2, sred, sbc);
-            rr2[0] = a[0];
-            rr2[1] = b2[0];
-        }
+        fused_total<2>(P.partials + m, m, rr2, sred, sbc);  // per-dot trees: same bits as two calls
         if (t == 0) apply_scalar(SC_CG_RR, &S, rr2);
         __syncthreads();
         const bool live = !S.done;

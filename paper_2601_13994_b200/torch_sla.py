@@ -62,7 +62,10 @@ class SparseTensor:
         self._group_of_input = np.empty(len(row), np.int64)
         self._group_of_input[order] = group
         self._order = order
-        coo = S.SparseCoo(r_s[new], c_s[new], np.zeros(int(new.sum())), (n, m))  # pattern check
+        if len(row) >= (1 << 17):  # bounds checked and (row, col) sorted + unique on the GPU
+            coo = S.SparseCoo(r_s[new], c_s[new], np.zeros(int(new.sum())), (n, m), _canonical=True)
+        else:
+            coo = S.SparseCoo(r_s[new], c_s[new], np.zeros(int(new.sum())), (n, m))  # pattern check
         self.csr = S.CsrMatrix.from_coo(coo)
         self.shape = (n, m)
         self.values = values
@@ -70,6 +73,7 @@ class SparseTensor:
         self._dup = bool((~new).any())
         self._order_t = None
         self._group_t = None
+        self._gin_t = None
 
     @property
     def nnz(self):
@@ -123,8 +127,10 @@ class _DupSum(torch.autograd.Function):
 
     @staticmethod
     def backward(ctx, g):
-        idx = torch.as_tensor(ctx.A._group_of_input, device=g.device)
-        return g[idx], None
+        A = ctx.A
+        if A._gin_t is None or A._gin_t.device != g.device:
+            A._gin_t = torch.as_tensor(A._group_of_input, device=g.device)
+        return g[A._gin_t], None
 
 
 def _ptr(t: torch.Tensor):
