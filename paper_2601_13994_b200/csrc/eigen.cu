@@ -43,6 +43,7 @@ namespace {
 constexpr int kMaxK = 16;             // block size limit of the GPU LOBPCG
 constexpr int kMaxQ = 3 * kMaxK;      // basis columns [X | W | P]
 constexpr int kRedCTAs = 296;         // fixed reduction grid (device-independent result)
+constexpr int kPartRows = 4 * 148;     // >= kRedCTAs and the rr_apply grid (pinned readback rows)
 constexpr int kT = 256;
 
 template <class T>
@@ -817,6 +818,7 @@ struct Lobpcg {
     double* gout = nullptr;     // [kMaxQ*kMaxQ]
     unsigned* ticket = nullptr;
     double* h_pin = nullptr;    // pinned [kMaxQ*kMaxQ]
+    double* h_part = nullptr;   // pinned per-CTA partials read back for the residual norms
     long long* ipart = nullptr;
     long long spmm_count = 0;
 
@@ -832,6 +834,7 @@ struct Lobpcg {
         CK(cudaMemsetAsync(ticket, 0, sizeof(unsigned), s));
         ipart = dalloc<long long>((size_t)kRedCTAs * kMaxK);
         CK(cudaMallocHost(&h_pin, sizeof(double) * kMaxQ * kMaxQ));
+        CK(cudaMallocHost(&h_part, sizeof(double) * kPartRows * kMaxQ));
         // dynamic shared memory up to the opt-in limit minus each kernel's static part
         auto allow = [&](const void* f, const char* what) {
             int optin = 0;
@@ -853,6 +856,7 @@ struct Lobpcg {
         cudaFree(S); cudaFree(AS); cudaFree(Sn); cudaFree(ASn);
         cudaFree(partial); cudaFree(gout); cudaFree(ticket); cudaFree(ipart);
         if (h_pin) cudaFreeHost(h_pin);
+        if (h_part) cudaFreeHost(h_part);
     }
     unsigned grid() const { return (unsigned)((n + kT - 1) / kT); }
     unsigned tile_grid() const {  // persistent over row tiles, 4 CTAs per SM
@@ -899,8 +903,8 @@ struct Lobpcg {
         for (int j = 0; j < m; ++j) L.v[j] = lam[j];
         resid_kernel<<<kRedCTAs, kT, 0, s>>>(S, AS, ld, m, L, dinv, m, n, partial);
         CK(cudaGetLastError());
-        std::vector<double> h((size_t)kRedCTAs * m);
-        CK(cudaMemcpyAsync(h.data(), partial, h.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+        const double* h = h_part;  // pinned: no pageable staging copy on this per-iteration readback
+        CK(cudaMemcpyAsync(h_part, partial, (size_t)kRedCTAs * m * sizeof(double), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         std::vector<double> r(m, 0.0);
         for (int p = 0; p < kRedCTAs; ++p)
@@ -1011,8 +1015,8 @@ struct Lobpcg {
             else
                 rr_apply_kernel<64><<<g, 128, rr_apply_smem(ld), s>>>(S, AS, Sn, ASn, ld, B, m, n, C, L, dinv, partial);
             CK(cudaGetLastError());
-            std::vector<double> h((size_t)g * m);
-            CK(cudaMemcpyAsync(h.data(), partial, h.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+            const double* h = h_part;
+            CK(cudaMemcpyAsync(h_part, partial, (size_t)g * m * sizeof(double), cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
             for (unsigned p = 0; p < g; ++p)
                 for (int j = 0; j < m; ++j) res[j] += h[(size_t)p * m + j];
