@@ -26,7 +26,8 @@ def _port():
 
 
 def _triplets(O, kind, p1, c):
-    A = O.generate(kind, p1, 0, c) if kind == "convdiff3d" else O.generate(kind, p1)
+    A = (O.generate(kind, p1, 0, c) if kind == "convdiff3d" else
+         O.generate(kind, p1, 2601) if kind == "fem2d" else O.generate(kind, p1))
     rows = np.repeat(np.arange(A.nrows), np.diff(A.row_ptr))
     return A, rows
 
@@ -52,7 +53,7 @@ def test_single_partition_matches_oracle(O, gpu):
     D.close()
 
 
-def _rank(rank, world, port, kind, p1, c, outq):
+def _rank(rank, world, port, kind, p1, c, outq, rcb=False):
     try:
         sys.path.insert(0, ROOT)
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -70,8 +71,9 @@ def _rank(rank, world, port, kind, p1, c, outq):
         v = np.concatenate([np.where(diag, 0.5 * A.vals, A.vals), 0.5 * A.vals[diag]])  # exact halves
         perm = np.random.default_rng(5).permutation(len(r))
         vals = torch.tensor(v[perm], device="cuda:0", requires_grad=True)
+        coords = O.gen_coords(kind, p1, 2601) if rcb else None
         D = DSparseMatrix.from_global(vals, r[perm], cc[perm], (A.nrows, A.nrows), num_partitions=world,
-                                      my_partition=rank)
+                                      my_partition=rank, coords=coords)
         b = torch.ones(D.n_owned, dtype=torch.float64, device="cuda:0", requires_grad=True)
         x = D.solve(b, atol=0.0, rtol=1e-11)
         g = torch.as_tensor(np.cos(np.arange(A.nrows))[D.owned], device="cuda:0")
@@ -88,13 +90,14 @@ def _rank(rank, world, port, kind, p1, c, outq):
         outq.put((rank, "error", traceback.format_exc()))
 
 
-@pytest.mark.parametrize("kind,p1,c", [("poisson3d", 16, 0.0), ("convdiff3d", 14, 0.4)])
-def test_two_processes_solve_and_backward(O, gpu, kind, p1, c):
+@pytest.mark.parametrize("kind,p1,c,rcb", [("poisson3d", 16, 0.0, False), ("convdiff3d", 14, 0.4, False),
+                                           ("fem2d", 40, 0.0, True)])
+def test_two_processes_solve_and_backward(O, gpu, kind, p1, c, rcb):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_rank, args=(r, 2, port, kind, p1, c, q)) for r in range(2)]
+    procs = [ctx.Process(target=_rank, args=(r, 2, port, kind, p1, c, q, rcb)) for r in range(2)]
     for p in procs:
         p.start()
     res = [q.get(timeout=240) for _ in range(2)]
@@ -104,7 +107,7 @@ def test_two_processes_solve_and_backward(O, gpu, kind, p1, c):
         assert not isinstance(t[1], str), t[2]
     A, rows = _triplets(O, kind, p1, c)
     n = A.nrows
-    po = O.partition_contiguous(n, 2)
+    po = O.partition_rcb(*O.gen_coords(kind, p1, 2601), 2) if rcb else O.partition_contiguous(n, 2)
     nonsym = kind == "convdiff3d"
     xo, _, _ = O.dist_solve(A, np.ones(n), po, 2, kind="bicgstab" if nonsym else "cg", atol=0.0, rtol=1e-11)
     g = np.cos(np.arange(n))
