@@ -396,3 +396,42 @@ def test_value_dictionary_empty_rows_and_partial_rounds(S, O, gpu):
     y = S.spmv(D, x)
     assert_bitwise(y, O.spmv(B, x))
     assert np.all(y[np.diff(B.row_ptr) == 0] == 0.0)
+
+
+def _banded(O, n, offsets, diag, off, extra_vals=None):
+    """Symmetric diagonally dominant band matrix (CG-safe): diag on the diagonal, `off` on
+    +-offsets; extra_vals (optional) varies the off-diagonal values (more distinct values)."""
+    rows, cols, vals = [], [], []
+    for i in range(n):
+        for o in sorted([-d for d in offsets] + [0] + list(offsets)):
+            j = i + o
+            if 0 <= j < n:
+                rows.append(i)
+                cols.append(j)
+                v = diag if o == 0 else off
+                if extra_vals is not None and o != 0:
+                    v = off * (1.0 + extra_vals * ((min(i, j) * 7919) % 1000) / 1000.0)
+                vals.append(v)
+    return O.csr_from_triplets(n, n, rows, cols, vals)
+
+
+@pytest.mark.parametrize("case", ["resident", "far_columns", "dense_chunks", "no_dictionary"])
+def test_fused_cg_resident_images_and_fallbacks(S, O, gpu, case):
+    """The fused small-problem CG keeps chunk images resident in shared memory when every
+    entry is within 2^15 of the diagonal, a chunk holds <= 65535 entries and the values form
+    a dictionary; otherwise it runs the non-resident kernel.  Every case's trajectory equals
+    the oracle's bit for bit."""
+    if case == "resident":
+        A = _banded(O, 30000, (1, 150), 5.0, -1.0)
+    elif case == "far_columns":      # +-40000 > int16: no resident image
+        A = _banded(O, 90000, (1, 40000), 5.0, -1.0)
+    elif case == "dense_chunks":     # 2048 rows x 41 entries > 65535 per chunk
+        A = _banded(O, 6000, tuple(range(1, 21)), 45.0, -1.0)
+    else:                            # many distinct values: no dictionary, no image
+        A = _banded(O, 30000, (1, 150), 5.0, -1.0, extra_vals=0.2)
+    b = np.linspace(0.5, 1.5, A.nrows)
+    xo, ro = O.cg(A, b, atol=0.0, rtol=1e-10, max_iter=20000)
+    x, r = S.cg_solve(to_S(S, A), b, S.SolveOptions(atol=0.0, rtol=1e-10, max_iter=20000))
+    assert ro["converged"]
+    rep_eq(r, ro)
+    assert_bitwise(x, xo, case)
