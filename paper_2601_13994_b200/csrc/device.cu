@@ -93,8 +93,16 @@ struct VdVariant {
                (const void*)spmv_ws_kernel<SPMV_BICG_V, R, S, M, true, 8, false, true>,               \
                (const void*)spmv_ws_kernel<SPMV_BICG_T, R, S, M, true, 8, false, true>}}
 // Measured on config B (tools/vd_sweep.py, profiles/r01_value_dict.md): 3 CTAs/SM at 72
-// registers (no spills) is the best point; 4 CTAs/SM (56 registers) spills.
-static const VdVariant kVdVariants[] = {VDV(1, 3, 3), VDV(1, 4, 3), VDV(1, 3, 4)};
+// registers (no spills) is the best 8-wide point; 4 CTAs/SM (56 registers) spills.  For rows
+// of <= 7 entries the 7-wide kernel at 4 CTAs/SM (variant 3, 32 bytes of spills in CG mode)
+// is faster still: occupancy beats spill-free code for this gather-latency-bound loop.
+#define VDVW(R, S, M, W)                                                                             \
+    {R, S, M, {(const void*)spmv_ws_kernel<SPMV_PLAIN, R, S, M, true, W, false, true>,                \
+               (const void*)spmv_ws_kernel<SPMV_CG, R, S, M, true, W, false, true>,                   \
+               (const void*)spmv_ws_kernel<SPMV_BICG_V, R, S, M, true, W, false, true>,               \
+               (const void*)spmv_ws_kernel<SPMV_BICG_T, R, S, M, true, W, false, true>}}
+static const VdVariant kVdVariants[] = {VDV(1, 3, 3), VDV(1, 4, 3), VDV(1, 3, 4), VDVW(1, 3, 4, 7), VDVW(1, 3, 3, 7)};
+#undef VDVW
 #undef VDV
 constexpr int kNumVdVariants = sizeof(kVdVariants) / sizeof(kVdVariants[0]);
 static int vd_variant() {
@@ -289,6 +297,10 @@ DevCsr* DevCsr::create(int device, long long nrows, long long ncols, const I* h_
         mb = std::max<long long>(mb, (long long)h_rp[e] - (long long)h_rp[b]);
     }
     for (long long i = 0; i < nrows; ++i) mr = std::max<long long>(mr, (long long)h_rp[i + 1] - (long long)h_rp[i]);
+    // rows of <= 7 entries (7-point stencils): the 7-wide dictionary kernel at 4 CTAs/SM
+    // (56 registers) — more gathers in flight per SM than 8-wide at 3 CTAs/SM (config B
+    // SpMV 1.050 -> 0.967 ms, profiles/r01b_notes.md)
+    if (!getenv("SPARSLA_VD_VARIANT") && mr <= 7) A->vd_var = 3;
     long long mb32 = 0;
     for (long long b = 0; b < nrows; b += 32) {
         const long long e = std::min(b + 32, nrows);
@@ -343,6 +355,10 @@ DevCsr* DevCsr::create(int device, long long nrows, long long ncols, const I* h_
                 kWsVariants[v].rpt == 0 ? kSpmvThreads : kWsThreads, ws_smem_bytes(A.get(), v, vd)));
             A->ws_ctas[v] = sms * std::max(1, per_sm);
         }
+        int per_sm = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kVdVariants[0].fn[SPMV_BICG_T], kWsThreads,
+                                                         ws_smem_bytes(A.get(), 0, true)));
+        A->vdt_ctas = sms * std::max(1, per_sm);
     }
     CK(cudaDeviceSynchronize());
     return A.release();
@@ -440,9 +456,19 @@ DevCsr* DevCsr::get_transpose() {
 }
 
 // ------------------------------------------------------------------ launches -------
-unsigned spmv_grid(const DevCsr* A, long long nch) {
+// Dictionary variant per SpMV mode: the 7-wide 4-CTA kernel (variant 3) serves every mode
+// but BiCGStab's t = A s-hat, whose three fused dots spill it; that one keeps the 8-wide
+// 3-CTA kernel (config D: 0.69 vs 0.73 ms).
+static int vd_var_of(const DevCsr* A, int mode) {
+    return (mode == SPMV_BICG_T && A->vd_var == 3) ? 0 : A->vd_var;
+}
+
+unsigned spmv_grid(const DevCsr* A, long long nch, int mode) {
     if (nch <= 0) return 0;
-    if (A->staged) return (unsigned)std::min<long long>(nch, (long long)A->ws_ctas[A->ws_var]);
+    if (A->staged) {
+        const bool vdt = A->vd && A->ws_var == 0 && vd_var_of(A, mode) != A->vd_var;
+        return (unsigned)std::min<long long>(nch, (long long)(vdt ? A->vdt_ctas : A->ws_ctas[A->ws_var]));
+    }
     return (unsigned)nch;
 }
 
@@ -451,7 +477,7 @@ unsigned spmv_grid(const DevCsr* A, long long nch) {
 void launch_spmv_part(DevCsr* A, cudaStream_t s, int mode, const double* x, double* y, const double* aux,
                       const RedParams& red, int check_done, const int32_t* list, long long nch,
                       unsigned expected, const P2PCtx* p2p, long long n_interior, int halo_v) {
-    const unsigned grid = spmv_grid(A, nch);
+    const unsigned grid = spmv_grid(A, nch, mode);
     if (grid == 0) return;
     SpmvParams P{};
     P.rp = A->rp; P.ci = A->ci; P.val = A->val;
@@ -474,7 +500,7 @@ void launch_spmv_part(DevCsr* A, cudaStream_t s, int mode, const double* x, doub
         if (wp) { P.cap_v = A->cap_v32; P.cap_c = A->cap_c32; }
         void* args[] = {&P};
         const bool vd = A->vd && v == 0;
-        const void* fn = vd ? kVdVariants[A->vd_var].fn[mode]
+        const void* fn = vd ? kVdVariants[vd_var_of(A, mode)].fn[mode]
                             : (A->has_hub ? kWsVariants[v].fn_hub[mode] : kWsVariants[v].fn[mode]);
         CK(cudaLaunchKernel(fn, dim3(grid), dim3(wp ? kSpmvThreads : kWsThreads), args, ws_smem_bytes(A, v, vd), s));
     } else {
@@ -494,7 +520,7 @@ void launch_spmv(DevCsr* A, cudaStream_t s, int mode, const double* x, double* y
                  const RedParams& red, int check_done) {
     if (A->nrows == 0) return;
     const long long nch = nchunks_of(A->nrows);
-    launch_spmv_part(A, s, mode, x, y, aux, red, check_done, nullptr, nch, spmv_grid(A, nch));
+    launch_spmv_part(A, s, mode, x, y, aux, red, check_done, nullptr, nch, spmv_grid(A, nch, mode));
 }
 
 static int u1_group() {
@@ -672,7 +698,7 @@ void Solver::spmv_point(int mode, double* xin, double* y, const double* aux, int
     if (d_p2p && check_done) {  // fused peer collectives: one launch, halo pushed by the producer
         R.p2p = d_p2p;
         R.point = slot;
-        const unsigned gall = spmv_grid(A, dist->n_interior + dist->n_boundary);
+        const unsigned gall = spmv_grid(A, dist->n_interior + dist->n_boundary, mode);
         launch_spmv_part(A, stream, mode, xin, y, aux, R, check_done, dist->d_all_chunks,
                          dist->n_interior + dist->n_boundary, gall, d_p2p, dist->n_interior,
                          mode == SPMV_BICG_T ? 1 : 0);  // halo flag: p / p-hat = 0, s-hat = 1
@@ -680,7 +706,7 @@ void Solver::spmv_point(int mode, double* xin, double* y, const double* aux, int
     }
     if (nd > 0) R.red_out = dist->red_send + slot * 8;
     dist->exchange(stream, xin);
-    const unsigned gi = spmv_grid(A, dist->n_interior), gb = spmv_grid(A, dist->n_boundary);
+    const unsigned gi = spmv_grid(A, dist->n_interior, mode), gb = spmv_grid(A, dist->n_boundary, mode);
     launch_spmv_part(A, stream, mode, xin, y, aux, R, check_done, dist->d_interior, dist->n_interior, gi + gb);
     CK(cudaStreamWaitEvent(stream, dist->ev_halo, 0));
     launch_spmv_part(A, stream, mode, xin, y, aux, R, check_done, dist->d_boundary, dist->n_boundary, gi + gb);

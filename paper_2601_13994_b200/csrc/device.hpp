@@ -38,6 +38,7 @@ struct DevCsr {
     bool has_hub = false;  // rounds above the stage capacity exist (bypass kernels)
     bool local_layout = false;  // rank-local [owned | halo] columns (diagonal of row i is column i)
     int ws_ctas[8] = {0};  // persistent grid per staged-SpMV variant (SMs x resident CTAs)
+    int vdt_ctas = 0;      // persistent grid of the BiCGStab t-SpMV dictionary kernel (8-wide)
     double* dinv = nullptr;
     double* ones = nullptr;
     uint8_t* vidx = nullptr;  // value dictionary (<= 256 distinct values): 1-byte index per entry
@@ -75,7 +76,7 @@ void csr_transpose_device(int device, long long nrows, long long ncols, long lon
 
 void launch_spmv(DevCsr* A, cudaStream_t s, int mode, const double* x, double* y, const double* aux,
                  const RedParams& red, int check_done);
-unsigned spmv_grid(const DevCsr* A, long long nch);
+unsigned spmv_grid(const DevCsr* A, long long nch, int mode = 0);
 void launch_spmv_part(DevCsr* A, cudaStream_t s, int mode, const double* x, double* y, const double* aux,
                       const RedParams& red, int check_done, const int32_t* list, long long nch,
                       unsigned expected, const P2PCtx* p2p = nullptr, long long n_interior = 0,
