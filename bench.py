@@ -1,24 +1,41 @@
 #!/usr/bin/env python
 """bench.py — CG iterations/s and SpMV HBM GB/s on 3-D Poisson (BASELINE.json metric).
 
-Workload (N=1): BASELINE configs[1] = config B, 3-D 7-point Poisson 464^3
+Default workload (N=1): BASELINE configs[1] = config B, 3-D 7-point Poisson 464^3
 (n = 99,897,344, nnz = 697,989,632), fp64, Jacobi-PCG to rel-res 1e-8.  A "step" is one
-CG iteration of the hot loop (SpMV + fused p.q, fused x/r update + r.z/r.r, p update;
-device-side scalars) with every input resident in HBM; the matrix (8.4 GB) and vectors
-exceed the 126 MB L2, so no flush is needed between steps.
+Krylov iteration of the hot loop (CG: SpMV + fused p.q, fused x/r update + r.z/r.r, p
+update; device-side scalars) with every input resident in HBM; the matrix (8.4 GB) and
+vectors exceed the 126 MB L2, so no flush is needed between steps.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config B|D|E]
+
+  --config B  464^3 Poisson, strong-scaled over N GPUs (default; the metric's config)
+  --config D  368^3 convection-diffusion, right-Jacobi BiCGStab, over N GPUs.  DEVIATION:
+              measured at cell Peclet c = 0.1; SURVEY's c = 1.0 breaks down (rho) in plain
+              BiCGStab in the oracle as well as here, so it has no time to tolerance
+  --config E  weak scaling: 368 x 368 x (368 N) Poisson, one 368^3 z-slab per GPU
+
+--gpus N > 1 without torchrun: this script launches the N ranks itself (one process per
+GPU, RANK/LOCAL_RANK/WORLD_SIZE/MASTER_* set, 127.0.0.1); under torchrun it runs as the
+given rank.  Only rank 0 prints.
 
 Prints ONE JSON line (rank 0).  `e2e` is the same metric through the public C ABI call
-sparsla_cg_solve with pinned HOST b and x (H2D/D2H inside the timed region), solved to
-tolerance; `roofline` is the dominant kernel (the SpMV) against MEASURED_PEAKS.json;
-`cpu_baseline` is the oracle port timed on this host (rank 0, N=1).
+(sparsla_cg_solve / sparsla_bicgstab_solve, or the distributed plan's solve) with pinned
+HOST b and x (H2D/D2H inside the timed region), solved to tolerance; `e2e_cold` is the first
+such call on a fresh matrix handle (solver workspace allocation + graph capture included);
+`roofline` is the dominant kernel against MEASURED_PEAKS.json; `cpu_baseline` is the oracle
+port timed on this host (rank 0, N=1), all host threads and 1 thread; `parity_gate` checks
+the solution against tests/golden/fullsize.json (the CPU oracle run to tolerance on the same
+matrix: equal iteration count and bitwise-equal x) BEFORE the line is printed
+(SPEC.md:589-594); a mismatch exits nonzero after printing.
 """
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -31,6 +48,42 @@ sys.path.insert(0, ROOT)
 
 METRIC = "CG iters/s & SpMV HBM GB/s, 3D Poisson 100M DOF fp64, 1/2/4/8 B200"
 SPEC_PEAK_GBS = 8000.0
+GOLDEN = os.path.join(ROOT, "tests", "golden", "fullsize.json")
+D_DEVIATION = ("cell Peclet c = 0.1 instead of SURVEY's c = 1.0: at c = 1.0 plain right-Jacobi BiCGStab "
+               "hits the SPEC rho-breakdown (|rho| < 1e-30 ||b||^2) after its residual diverges, in the CPU "
+               "oracle bit-identically (tests/test_gpu_parity.py::test_config_D_c1_breakdown_matches_oracle)")
+
+
+# ---------------------------------------------------------------------------- configs ---
+def resolve_config(name, world, size=None):
+    """Generator parameters + the workload description shared by BOTH arms (so the
+    driver's same-config check compares identical dicts)."""
+    if name == "B":
+        N = size or 464
+        c = dict(kind="poisson3d", p1=N, p2=0, fparam=0.0, solver="cg", scaling="strong",
+                 golden={1: "B"} if N == 464 else {},
+                 workload=f"B: 3-D 7-pt Poisson {N}^3, Jacobi-PCG rtol 1e-8, x0 = 0, b = ones")
+    elif name == "D":
+        N = size or 368
+        c = dict(kind="convdiff3d", p1=N, p2=0, fparam=0.1, solver="bicgstab", scaling="strong",
+                 golden={1: "Dp"} if N == 368 else {}, deviation=D_DEVIATION,
+                 workload=f"D': 3-D upwind convection-diffusion {N}^3 (c = 0.1), right-Jacobi BiCGStab "
+                          "rtol 1e-8, x0 = 0, b = ones")
+    elif name == "E":
+        N = size or 368
+        c = dict(kind="poisson3d_box", p1=N, p2=N * world, fparam=0.0, solver="cg", scaling="weak",
+                 golden={1: "E1", 2: "E2"} if N == 368 else {},
+                 workload=f"E: 3-D 7-pt Poisson {N} x {N} x {N * world} ({N}^3 z-slab per GPU), "
+                          "Jacobi-PCG rtol 1e-8, x0 = 0, b = ones")
+    else:
+        raise ValueError(name)
+    c["name"] = name
+    return c
+
+
+def config_block(cfg, n, nnz, rtol):
+    return {"workload": cfg["workload"], "n": n, "nnz": nnz, "solver": cfg["solver"], "rtol": rtol,
+            "l2": "no flush: matrix + vectors exceed the 126 MB L2 (inputs larger than L2)"}
 
 
 def load_peak():
@@ -41,6 +94,58 @@ def load_peak():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def sha_bits(x) -> str:
+    return hashlib.sha256(np.ascontiguousarray(x, np.float64).view(np.uint8)).hexdigest()
+
+
+def golden_record(cfg, world):
+    key = cfg.get("golden", {}).get(world)
+    if not key or not os.path.exists(GOLDEN):
+        return None, None
+    with open(GOLDEN) as f:
+        g = json.load(f)
+    rec = g.get(key)
+    if rec and rec["kind"] == cfg["kind"] and rec["p1"] == cfg["p1"] and rec["p2"] == cfg["p2"] \
+            and rec["fparam"] == cfg["fparam"] and rec["solver"] == cfg["solver"]:
+        return key, rec
+    return None, None
+
+
+def parity_gate(cfg, world, rep, x, true_rel, rtol):
+    """verify against the serial CPU solver before reporting.  With a
+    golden record for this exact config and partition count: equal iteration count and
+    bitwise-equal x (sha256 of the bit patterns); otherwise north_star's k +-1 against the
+    serial record plus an independent true-residual check."""
+    key, rec = golden_record(cfg, world)
+    out = {"converged": bool(rep.converged), "iterations": rep.iterations,
+           "residual_norm": rep.residual_norm, "true_rel_residual": true_rel}
+    ok = bool(rep.converged) and true_rel <= 10 * rtol
+    if rec is not None:
+        k_ref = rec["report"]["iterations"]
+        out["golden"] = key
+        out["k_ref"] = k_ref
+        if x is not None:
+            h = sha_bits(x)
+            out["x_bitwise_equal"] = h == rec["x"]["sha256"]
+            idx = np.asarray(rec["x"]["sample_idx"], np.int64)
+            ref = np.asarray(rec["x"]["sample_bits"], np.int64).view(np.float64)
+            out["sample_max_rel_err"] = float(np.max(np.abs(x[idx] - ref)) / max(1e-300, np.max(np.abs(ref))))
+            ok = ok and out["x_bitwise_equal"] and rep.iterations == k_ref
+        else:
+            ok = ok and rep.iterations == k_ref
+        out["residual_norm_bitwise_equal"] = \
+            int(np.float64(rep.residual_norm).view(np.int64)) == rec["report"]["residual_norm_bits"]
+    else:
+        serial = golden_record(cfg, 1)[1] if world > 1 else None
+        if serial is not None:
+            out["k_ref_serial"] = serial["report"]["iterations"]
+            ok = ok and abs(rep.iterations - out["k_ref_serial"]) <= 1
+        out["golden"] = None
+    out["ok"] = bool(ok)
+    return out
+
+
+# ------------------------------------------------------------------------ clocks ---------
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled every 200 ms while running."""
 
@@ -51,6 +156,7 @@ class ClockSampler:
     def __init__(self, dev):
         self.dev = dev
         self.p = None
+        self.lines = []
 
     def __enter__(self):
         try:
@@ -68,8 +174,6 @@ class ClockSampler:
             self.p.terminate()
             out, _ = self.p.communicate(timeout=10)
             self.lines = [l for l in out.splitlines() if l.strip()]
-        else:
-            self.lines = []
 
     def summary(self):
         sm, mx, reasons, pw = [], 0.0, set(), []
@@ -94,152 +198,193 @@ class ClockSampler:
                 "samples": len(sm), "power_w_max": max(pw) if pw else None}
 
 
-def gen_config(args):
-    from paper_2601_13994_b200 import sparsla as S
-    t0 = time.time()
-    nr, n, rp, ci, v = S.generate_i32("poisson3d", args.size)
-    return n, rp, ci, v, time.time() - t0
-
-
-def iteration_bytes(n, nnz, value_dict=False, uniform_diag=False):
-    """Algorithmic bytes of THIS implementation's CG iteration in the storage format the
-    library chose (x += a p moved into update 2 so p is streamed once).  Plain CSR:
-    12 nnz + 100 n + 4; with the value dictionary the matrix stream is 5 nnz (+ a 2 KB
-    table); with a constant Jacobi diagonal the two vector passes skip d (-16 n).
-    SURVEY.md's canonical 3-pass CSR accounting, 12 nnz + 108 n + 4, is reported beside it."""
+# -------------------------------------------------------------- algorithmic bytes --------
+def kernel_bytes(solver, n, nnz, h, value_dict, uniform_diag):
+    """Per-launch algorithmic bytes of THIS implementation's kernels in the stored format in
+    use (value dictionary: 5 B/entry + a 2 KB table instead of 12 B/entry; constant Jacobi
+    diagonal: passed as a scalar, no d stream).  Returns [(kernel name, bytes)] in launch
+    order.  CG: x += a p is moved into update 2 (p streamed once per iteration)."""
     mat = (5 * nnz + 2048) if value_dict else 12 * nnz
-    spmv = mat + 4 * (n + 1) + 8 * n + 8 * n        # matrix, row_ptr, p (once), q write
-    u1 = (24 if uniform_diag else 32) * n           # read r q (d), write r
-    u2 = (40 if uniform_diag else 48) * n           # read x p r (d), write x p
-    return spmv, u1, u2
+    d = 0 if uniform_diag else 8 * n
+    rp = 4 * (n + 1)
+    if solver == "cg":
+        return [("spmv_cg", mat + rp + 8 * (n + h) + 8 * n),    # A, row_ptr, p gathered, q written
+                ("cg_update1", 24 * n + d),                      # read r q (d), write r
+                ("cg_update2", 40 * n + d)]                      # read x p r (d), write x p
+    return [("bicg_update1", 40 * n + d),                        # read r p v (d), write p ph
+            ("spmv_v", mat + rp + 8 * (n + h) + 16 * n),         # ph gathered, v written, rh read
+            ("bicg_update2", 32 * n + d),                        # read r v (d), write s sh
+            ("spmv_t", mat + rp + 8 * (n + h) + 16 * n),         # sh gathered, t written, s read
+            ("bicg_update3", 64 * n)]                            # read x ph s sh t rh, write x r
 
 
-def cpu_baseline(rp, ci, v, n, nnz, threads, budget_s=20.0):
-    """Oracle port (test infrastructure) on this host: per-iteration time of the same CG."""
+def canonical_bytes(solver, n, nnz, h=0):
+    """SURVEY.md §8(d) canonical CSR accounting per iteration."""
+    return 12 * nnz + 108 * n + 8 * h + 4 if solver == "cg" else 24 * nnz + 208 * n + 16 * h
+
+
+# ------------------------------------------------------------------ CPU baselines --------
+def _oracle():
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import pyoracle as O
+    return O
+
+
+def oracle_fixed(O, A, b, solver, iters):
+    """Oracle solve stopped after `iters` iterations (init included)."""
+    if solver == "cg":
+        O.cg_fixed(A, b, iters)
+    else:
+        O.bicgstab(A, b, atol=1e-300, rtol=0.0, max_iter=iters)  # never met: fixed count
+
+
+def time_oracle(O, A, b, solver, threads, budget_s, min_iters=2, max_iters=20):
+    """Per-iteration time of the oracle port: difference of a 1-iteration run and a
+    (1+m)-iteration run, m sized to the budget."""
     O.set_threads(threads)
-    A = O.Csr(n, n, rp.astype(np.int64), ci.astype(np.int64), v)
-    b = np.ones(n)
     t0 = time.perf_counter()
-    O.cg_fixed(A, b, 1)
+    oracle_fixed(O, A, b, solver, 1)
     t1 = time.perf_counter()
     per_guess = max(1e-3, (t1 - t0) / 2.0)
-    m = int(max(2, min(20, budget_s / per_guess)))
+    m = int(max(min_iters, min(max_iters, budget_s / per_guess)))
     t2 = time.perf_counter()
-    O.cg_fixed(A, b, 1 + m)
+    oracle_fixed(O, A, b, solver, 1 + m)
     t3 = time.perf_counter()
-    per_it = ((t3 - t2) - (t1 - t0)) / m
-    return {"value": 1.0 / per_it, "unit": "it/s", "cores": threads, "kind": "port",
-            "sample": f"{m} CG iterations of config B (full 99.9M-DOF matrix) with {threads} host "
-                      f"threads, oracle/liboracle.so (SpMV bit-identical to reference sparse.cpp)",
-            "s_per_iteration": per_it}
+    return ((t3 - t2) - (t1 - t0)) / m, m
+
+
+def cpu_baseline(A, b, cfg, threads):
+    """Oracle port (test infrastructure) on this host, all threads + 1 thread."""
+    O = _oracle()
+    per, m = time_oracle(O, A, b, cfg["solver"], threads, 20.0)
+    per1, m1 = time_oracle(O, A, b, cfg["solver"], 1, 12.0, min_iters=2, max_iters=5)
+    what = "CG" if cfg["solver"] == "cg" else "BiCGStab"
+    return {"value": 1.0 / per, "unit": "it/s", "cores": threads, "kind": "port",
+            "sample": f"{m} {what} iterations of config {cfg['name']} (full-size matrix) with {threads} host "
+                      "threads, oracle/liboracle.so (SpMV bit-identical to reference sparse.cpp)",
+            "s_per_iteration": per,
+            "single_thread": {"value": 1.0 / per1, "unit": "it/s", "cores": 1, "s_per_iteration": per1,
+                              "sample": f"{m1} iterations, 1 thread (the reference kernels are "
+                                        "single-threaded, SPEC.md:113, 199)"}}
 
 
 def run_reference(args):
-    """--impl reference: the reference's CPU path (oracle port of SPEC cg_solve over the
-    reference spmv semantics; the reference tree has no solver sources) on host cores."""
+    """--impl reference: the reference's CPU path on host cores.  The reference tree has no
+    solver sources, so this is the oracle port: reference spmv semantics
+    (sparse.cpp:135-154, checked bitwise against the compiled reference) + SPEC cg_solve /
+    bicgstab_solve.  The matrix comes from the oracle's own generator — nothing of the
+    product library is loaded in this arm."""
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     if rank != 0:
-        return
+        return 0
+    cfg = resolve_config(args.config, max(world, args.gpus), args.size)
     threads = os.cpu_count() or 1
-    n, rp, ci, v, tgen = gen_config(args)
-    nnz = int(rp[-1])
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import pyoracle as O
+    O = _oracle()
     O.set_threads(threads)
-    A = O.Csr(n, n, rp.astype(np.int64), ci.astype(np.int64), v)
-    del rp, ci
+    t0 = time.time()
+    A = O.generate_csr(cfg["kind"], cfg["p1"], cfg["p2"], cfg["fparam"])
+    tgen = time.time() - t0
+    n, nnz = A.nrows, A.nnz
     b = np.ones(n)
     t0 = time.perf_counter()
-    O.cg_fixed(A, b, args.warmup)        # init + W iterations
+    oracle_fixed(O, A, b, cfg["solver"], args.warmup)                 # init + W iterations
     t1 = time.perf_counter()
-    O.cg_fixed(A, b, args.warmup + args.steps)
+    oracle_fixed(O, A, b, cfg["solver"], args.warmup + args.steps)
     t2 = time.perf_counter()
     per = ((t2 - t1) - (t1 - t0)) / args.steps
     val = 1.0 / per
+    per1, m1 = time_oracle(O, A, b, cfg["solver"], 1, 12.0, min_iters=2, max_iters=5)
     line = {"metric": METRIC, "value": val, "unit": "it/s", "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic",
-            "config": {"workload": f"B: 3-D 7-pt Poisson {args.size}^3 ({n} DOF, nnz {nnz}), "
-                                   "Jacobi-PCG rtol 1e-8", "n": n, "nnz": nnz},
+            "higher_is_better": True, "scaling": cfg["scaling"], "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (generated, b = ones)",
+            "config": config_block(cfg, n, nnz, args.rtol),
             "cpu_baseline": {"value": val, "unit": "it/s", "cores": threads, "kind": "port",
-                             "sample": f"{args.steps} timed CG iterations after {args.warmup} warm-up "
-                                       "iterations (difference of two oracle runs)"},
-            "e2e": {"value": val, "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+                             "sample": f"{args.steps} timed iterations after {args.warmup} warm-up iterations "
+                                       "(difference of two oracle runs), all host threads",
+                             "single_thread": {"value": 1.0 / per1, "unit": "it/s", "cores": 1,
+                                               "sample": f"{m1} iterations, 1 thread"}},
+            "e2e": {"value": val, "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "setup_s": {"generate": tgen}}
+    if cfg.get("deviation"):
+        line["deviation"] = cfg["deviation"]
     print(json.dumps(line), flush=True)
+    return 0
 
 
+# ---------------------------------------------------------------- our arm, N = 1 ---------
 def run_ours(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1 or args.dist:
+        from paper_2601_13994_b200 import dist_bench
+        return dist_bench.run(args, METRIC, resolve_config(args.config, world, args.size))
+    import ctypes as C
     import torch
     from paper_2601_13994_b200 import sparsla as S
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    if world > 1 or args.gpus > 1 or args.dist:
-        from paper_2601_13994_b200 import dist_bench
-        return dist_bench.run(args, METRIC)
+    cfg = resolve_config(args.config, 1, args.size)
+    solver = cfg["solver"]
     dev = 0
     torch.cuda.set_device(dev)
     peak, peak_src = load_peak()
-    n, rp, ci, v, tgen = gen_config(args)
+    t0 = time.time()
+    nr, n, rp, ci, v = S.generate_i32(cfg["kind"], cfg["p1"], cfg["p2"], cfg["fparam"])
+    tgen = time.time() - t0
     nnz = int(rp[-1])
     t0 = time.time()
     D = S.DeviceCsr(None, dev, i32=(n, n, rp, ci, v))
     tup = time.time() - t0
-    info = D.info()
-    fmt = D.format()
+    info, fmt = D.info(), D.format()
     b_host = torch.ones(n, dtype=torch.float64).pin_memory()
     x_host = torch.empty(n, dtype=torch.float64).pin_memory()
     opts = S.SolveOptions(atol=0.0, rtol=args.rtol, max_iter=args.max_iter)
     lib = S.lib()
-    import ctypes as C
+    solve_fn = lib.sparsla_cg_solve if solver == "cg" else lib.sparsla_bicgstab_solve
+
+    def public_solve(o):
+        rep = S._Report()
+        oc = o.c()
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        S._check(solve_fn(D.h, C.cast(b_host.data_ptr(), S._f64p), C.cast(x_host.data_ptr(), S._f64p),
+                          C.byref(oc), C.byref(rep), C.c_int32(S.MEM_HOST)))
+        return S.SolveReport._from(rep), time.perf_counter() - t
 
     # ---------------- e2e: public C ABI call, host buffers, solve to tolerance ----------
-    # one untimed warm-up call (W iterations): the matrix handle's parked solver workspace
-    # and graphs are built there, as in any application that solves more than once
-    wo = S.SolveOptions(atol=0.0, rtol=args.rtol, max_iter=max(1, args.warmup)).c()
-    S._check(lib.sparsla_cg_solve(D.h, C.cast(b_host.data_ptr(), S._f64p), C.cast(x_host.data_ptr(), S._f64p),
-                                  C.byref(wo), C.byref(S._Report()), C.c_int32(S.MEM_HOST)))
+    # first call on the fresh handle: includes the solver workspace + CUDA-graph build
+    rep_cold, t_cold = public_solve(opts)
+    # steady state: the handle's parked solver is reused, as in any application that
+    # solves more than once (SPARSLA_SOLVER_CACHE=0 disables the parking)
     e2e_its, e2e_t, reps = 0, 0.0, []
     for _ in range(max(1, args.e2e_steps)):
-        rep = S._Report()
-        o = opts.c()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        S._check(lib.sparsla_cg_solve(D.h, C.cast(b_host.data_ptr(), S._f64p),
-                                      C.cast(x_host.data_ptr(), S._f64p), C.byref(o), C.byref(rep),
-                                      C.c_int32(S.MEM_HOST)))
-        dt = time.perf_counter() - t0
-        reps.append(S.SolveReport._from(rep))
+        rep, dt = public_solve(opts)
+        reps.append(rep)
         e2e_its += rep.iterations
         e2e_t += dt
     r0 = reps[0]
     k_tol = r0.iterations
-    # correctness gate before reporting (SPEC.md:592-593): true residual of the GPU solution
     x = x_host.numpy().copy()
     ax = S.spmv(D, x)
     true_rel = float(np.linalg.norm(1.0 - ax) / np.sqrt(n))
-    gate_ok = bool(r0.converged and true_rel <= 10 * args.rtol)
+    del ax
+    gate = parity_gate(cfg, 1, r0, x, true_rel, args.rtol)
 
     # ---------------- device-resident timed loop -----------------------------------------
-    sv = S.Solver(D, b_host.numpy(), "cg", opts)
+    sv = S.Solver(D, b_host.numpy(), solver, opts)
     stream = torch.cuda.ExternalStream(sv.stream())
     launches = sv.launches_per_iteration()
     budget = max(1, k_tol - 1)  # iterations available before the solve terminates
-    done = 0
-    resets = 0
+    st = {"done": 0, "resets": 0}
 
     def advance(k):
-        nonlocal done, resets
         while k > 0:
-            if done >= budget:
+            if st["done"] >= budget:
                 sv.reset()
-                resets += 1
-                done = 0
-            m = min(k, budget - done)
+                st["resets"] += 1
+                st["done"] = 0
+            m = min(k, budget - st["done"])
             sv.iterate(m)
-            done += m
+            st["done"] += m
             k -= m
 
     sv.reset()
@@ -248,32 +393,36 @@ def run_ours(args):
         torch.cuda.synchronize()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
-        resets_before = resets
+        resets_before = st["resets"]
         e0.record(stream)
         advance(args.steps)
         e1.record(stream)
         e1.synchronize()
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
-    timed_resets = resets - resets_before
-    rep_loop = sv.report()
+    timed_resets = st["resets"] - resets_before
     value = args.steps / (ms / 1e3)
-    # per-kernel durations (CUDA events around each kernel, individual launches)
+    # per-kernel durations (CUDA events around each kernel on the solver stream)
     sv.reset()
     sv.iterate(5)
     kms = sv.kernel_times(args.kernel_iters)
-    spmv_b, u1_b, u2_b = iteration_bytes(n, nnz, fmt["value_dict"], fmt["uniform_diag"])
-    it_bytes = spmv_b + u1_b + u2_b
-    spmv_gbs = spmv_b / (kms[0] * 1e-3) / 1e9
     sv.close()
+    kb = kernel_bytes(solver, n, nnz, 0, fmt["value_dict"], fmt["uniform_diag"])
+    it_bytes = sum(b for _, b in kb)
+    dom = max(range(len(kms)), key=lambda i: kms[i]) if solver == "cg" else \
+        max((i for i, (nm, _) in enumerate(kb) if nm.startswith("spmv")), key=lambda i: kms[i])
+    dom_name, dom_bytes = kb[dom]
+    dom_gbs = dom_bytes / (kms[dom] * 1e-3) / 1e9
+    kernel_gbs = {nm: b / (t * 1e-3) / 1e9 for (nm, b), t in zip(kb, kms)}
+    canon = canonical_bytes(solver, n, nnz)
     # plain-CSR reference point of the same loop (value dictionary and scalar diagonal off)
     plain = None
-    if args.plain_steps > 0:
+    if args.plain_steps > 0 and (fmt["value_dict"] or fmt["uniform_diag"]):
         os.environ["SPARSLA_VALUE_DICT"] = "0"
         os.environ["SPARSLA_UNIFORM_DIAG"] = "0"
         try:
             Dp = S.DeviceCsr(None, dev, i32=(n, n, rp, ci, v))
-            svp = S.Solver(Dp, b_host.numpy(), "cg", opts)
+            svp = S.Solver(Dp, b_host.numpy(), solver, opts)
             sp = torch.cuda.ExternalStream(svp.stream())
             svp.reset()
             svp.iterate(5)
@@ -285,11 +434,12 @@ def run_ours(args):
             q1.synchronize()
             pms = q0.elapsed_time(q1) / args.plain_steps
             pk = svp.kernel_times(10)
-            ps_b, pu1, pu2 = iteration_bytes(n, nnz)
+            pkb = kernel_bytes(solver, n, nnz, 0, False, False)
             plain = {"value": 1e3 / pms, "unit": "it/s", "steps": args.plain_steps, "ms_per_step": pms,
-                     "kernel_ms": {"spmv_cg": pk[0], "cg_update1": pk[1], "cg_update2": pk[2]},
-                     "spmv_gbs": ps_b / (pk[0] * 1e-3) / 1e9,
-                     "iteration_gbs": (ps_b + pu1 + pu2) / (pms * 1e-3) / 1e9,
+                     "kernel_ms": {nm: t for (nm, _), t in zip(pkb, pk)},
+                     "kernel_gbs": {nm: b / (t * 1e-3) / 1e9 for (nm, b), t in zip(pkb, pk)},
+                     "iteration_gbs": sum(b for _, b in pkb) / (pms * 1e-3) / 1e9,
+                     "iteration_frac": sum(b for _, b in pkb) / (pms * 1e-3) / 1e9 / peak,
                      "format": "plain CSR (int32 col, fp64 val), streamed Jacobi diagonal"}
             svp.close()
             del Dp
@@ -299,51 +449,98 @@ def run_ours(args):
     try:
         with open(os.path.join(ROOT, "profiles", "spmv_traffic.json")) as f:
             tj = json.load(f)
-        if tj.get("size") == args.size:
+        if tj.get("size") == cfg["p1"] and cfg["name"] == "B":
             traffic = tj["value_dict" if fmt["value_dict"] else "plain"]["dram_bytes_per_launch"]
     except Exception:
         pass
     line = {
         "metric": METRIC, "value": value, "unit": "it/s", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (generated 3-D Poisson, b = ones)",
-        "config": {"workload": f"B: 3-D 7-pt Poisson {args.size}^3 ({n} DOF, nnz {nnz}), Jacobi-PCG "
-                               f"rtol {args.rtol}, x0 = 0", "n": n, "nnz": nnz, "partition": "single GPU",
-                   "l2": "no flush: matrix + vectors (>12 GB) exceed the 126 MB L2",
-                   "spmv_variant": "tma-bulk-staged" if info["variant"] == 0 else "direct",
+        "scaling": cfg["scaling"], "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (generated, b = ones)",
+        "config": config_block(cfg, n, nnz, args.rtol),
+        "partition": "single GPU",
+        "format": {"spmv_variant": "tma-bulk-staged" if info["variant"] == 0 else "direct",
                    "storage": ("value dictionary (1-byte index into %d distinct fp64 values) + int32 col"
                                % fmt["distinct_values"]) if fmt["value_dict"] else "CSR int32 col + fp64 val",
                    "jacobi_diag": "constant (scalar)" if fmt["uniform_diag"] else "streamed"},
-        "spmv_gbs": spmv_gbs,
         "iteration_gbs": it_bytes / (ms / args.steps * 1e-3) / 1e9,
         "bytes_per_iteration": it_bytes,
-        "canonical_bytes_per_iteration": 12 * nnz + 108 * n + 4,
-        "canonical_iteration_gbs": (12 * nnz + 108 * n + 4) / (ms / args.steps * 1e-3) / 1e9,
-        "kernel_ms": {"spmv_cg": kms[0], "cg_update1": kms[1], "cg_update2": kms[2]},
-        "csr_equivalent_spmv_gbs": (12 * nnz + 20 * n + 4) / (kms[0] * 1e-3) / 1e9,
+        "canonical_bytes_per_iteration": canon,
+        "kernel_ms": {nm: t for (nm, _), t in zip(kb, kms)},
+        "kernel_gbs": kernel_gbs,
         "plain_csr": plain,
-        "roofline": {"bound": "hbm", "kernel": "spmv_ws_kernel<SPMV_CG,staged%s>" % (",value-dict" if fmt["value_dict"] else ""), "achieved": spmv_gbs,
-                     "peak": peak, "unit": "GB/s", "frac": spmv_gbs / peak, "traffic": traffic,
-                     "peak_source": peak_src, "frac_of_spec_8tbs": spmv_gbs / SPEC_PEAK_GBS,
-                     "algorithmic_bytes_per_launch": spmv_b,
-                     "bytes_basis": "bytes of the stored format (value dictionary: 5 B/entry)" if fmt["value_dict"]
-                                    else "CSR 12 B/entry",
+        "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": dom_gbs,
+                     "peak": peak, "unit": "GB/s", "frac": dom_gbs / peak, "traffic": traffic,
+                     "peak_source": peak_src, "frac_of_spec_8tbs": dom_gbs / SPEC_PEAK_GBS,
+                     "algorithmic_bytes_per_launch": dom_bytes,
+                     "bytes_basis": "bytes of the stored format (value dictionary: 5 B/entry + 2 KB table)"
+                                    if fmt["value_dict"] else "CSR 12 B/entry",
                      "iteration_frac": (it_bytes / (ms / args.steps * 1e-3) / 1e9) / peak},
         "time_to_tolerance_s": e2e_t / len(reps), "iterations_to_tolerance": k_tol,
         "e2e": {"value": e2e_its / e2e_t, "unit": "it/s", "h2d_bytes_per_step": 8 * n,
-                "d2h_bytes_per_step": 8 * n + 184, "step": "one sparsla_cg_solve call to rtol "
-                f"{args.rtol} with pinned host b/x", "steps": len(reps)},
+                "d2h_bytes_per_step": 8 * n + 184,
+                "step": f"one sparsla_{solver}_solve call to rtol {args.rtol:g} with pinned host b/x "
+                        "(matrix handle warm: parked solver reused)", "steps": len(reps)},
+        "e2e_cold": {"value": rep_cold.iterations / t_cold, "unit": "it/s", "time_s": t_cold,
+                     "iterations": rep_cold.iterations,
+                     "step": "first solve call on a fresh matrix handle (workspace + graph capture included)"},
         "gpu_launches": args.steps * launches + 2 * timed_resets,
         "clocks": clk.summary(),
-        "parity_gate": {"converged": r0.converged, "residual_norm": r0.residual_norm,
-                        "true_rel_residual": true_rel, "ok": gate_ok},
+        "parity_gate": gate,
         "setup_s": {"generate": tgen, "upload": tup},
     }
-    if not args.no_cpu_baseline and rank == 0:
-        del D, sv
-        line["cpu_baseline"] = cpu_baseline(rp, ci, v, n, nnz, os.cpu_count() or 1)
+    if cfg.get("deviation"):
+        line["deviation"] = cfg["deviation"]
+    if not args.no_cpu_baseline:
+        del D
+        O = _oracle()
+        A = O.Csr(n, n, rp.astype(np.int64), ci.astype(np.int64), v)
+        del rp, ci
+        line["cpu_baseline"] = cpu_baseline(A, np.ones(n), cfg, os.cpu_count() or 1)
     print(json.dumps(line), flush=True)
+    return 0 if gate["ok"] else 1
+
+
+# ------------------------------------------------------------------ launcher ------------
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def launch_ranks(argv, n):
+    """One process per GPU, without torchrun: rank r gets LOCAL_RANK r (its GPU) and the
+    127.0.0.1 rendezvous.  Only rank 0 prints; the exit code is the max over ranks."""
+    port = str(free_port())
+    procs = []
+    for r in range(n):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(n),
+                   LOCAL_WORLD_SIZE=str(n), MASTER_ADDR="127.0.0.1", MASTER_PORT=port)
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__)] + argv, env=env))
+    rcs = [p.wait() for p in procs]
+    return max(rcs)
+
+
+def run_dry(args):
+    """--dry-run: rank wiring only (gloo on CPU): each rank reports (rank, local_rank)."""
+    import torch
+    import torch.distributed as dist
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    t = torch.tensor([rank, int(os.environ.get("LOCAL_RANK", "0"))], dtype=torch.int64)
+    out = [torch.zeros(2, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(out, t)
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "ranks": [o.tolist() for o in out],
+                          "config": config_block(resolve_config(args.config, world, args.size), 0, 0, args.rtol)}),
+              flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+    return 0
 
 
 def main():
@@ -352,9 +549,10 @@ def main():
     ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--size", type=int, default=464)
-    ap.add_argument("--config", default="B", choices=["B", "E"],
-                    help="B: 464^3 strong-scaled over N GPUs; E: 368^2 x (368 N) weak scaling (368^3 per GPU)")
+    ap.add_argument("--config", default="B", choices=["B", "D", "E"],
+                    help="B: 464^3 strong-scaled over N GPUs; D: 368^3 convection-diffusion (c = 0.1) "
+                         "BiCGStab over N GPUs; E: 368^2 x (368 N) weak scaling (368^3 per GPU)")
+    ap.add_argument("--size", type=int, default=None, help="override the grid edge N of the config")
     ap.add_argument("--rtol", type=float, default=1e-8)
     ap.add_argument("--max-iter", type=int, default=100000)
     ap.add_argument("--e2e-steps", type=int, default=1)
@@ -364,14 +562,18 @@ def main():
     ap.add_argument("--dist", action="store_true", help="force the NCCL distributed path (also at N=1)")
     ap.add_argument("--fused", action="store_true",
                     help="N>1: fused peer-memory collectives inside the kernels instead of NCCL calls")
+    ap.add_argument("--dry-run", action="store_true", help="launcher wiring only (CPU, gloo)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        return launch_ranks(sys.argv[1:], args.gpus)
+    if args.dry_run:
+        return run_dry(args)
     if args.impl == "reference":
-        run_reference(args)
-    else:
-        run_ours(args)
+        return run_reference(args)
+    return run_ours(args)
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())

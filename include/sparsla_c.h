@@ -323,6 +323,11 @@ int sparsla_dist_reset_counters(sparsla_dist* D);
  * in-process ranks) with release/acquire epoch flags.  Must be set identically on all
  * ranks before a solve. */
 int sparsla_dist_set_fused(sparsla_dist* D, int32_t on);
+/* SparseCoo::with_values (sparse.hpp:58-61) on this rank's local matrix: new values in the
+ * local entry order of the sparsla_local it was built from (owned rows ascending, entries in
+ * global column order).  Collective (a barrier over the transport: no peer may still use a
+ * parked solver's peer mappings); drops the plan's parked solvers and the A^T values. */
+int sparsla_dist_set_values(sparsla_dist* D, const double* vals_local, int32_t mem);
 /* dist_spmv */
 int sparsla_dist_spmv(sparsla_dist* D, const double* x_owned, double* y_owned, int32_t mem);
 /* dist_cg (Alg. 4) / distributed BiCGStab, SolveOptions as cg_solve */

@@ -833,6 +833,103 @@ int orc_gen_triplets(int32_t kind, int64_t p1, int64_t p2, double fparam, int64_
     return 0;
 }
 
+int orc_gen_csr(int32_t kind, int64_t p1, int64_t p2, double fparam, int64_t* n_out,
+                int64_t* ntrip, int64_t* row_ptr, int64_t* col_idx, double* vals, int64_t* nnz) {
+    int rc = orc_gen_triplets(kind, p1, p2, fparam, n_out, ntrip, nullptr, nullptr, nullptr);
+    if (rc || !row_ptr) return rc;
+    const int64_t n = *n_out, nt = *ntrip;
+    if (kind != 3) {
+        // stencil emission is already canonical: rows ascending, columns ascending within a
+        // row, no duplicates (checked below) -- fill CSR in emission order
+        std::fill(row_ptr, row_ptr + n + 1, int64_t{0});
+        int64_t cnt = 0, last_r = -1, last_c = -1;
+        bool ok = true;
+        auto emit = [&](int64_t r, int64_t c, double v) {
+            if (r < last_r || (r == last_r && c <= last_c)) ok = false;
+            last_r = r; last_c = c;
+            ++row_ptr[r + 1];
+            col_idx[cnt] = c;
+            vals[cnt] = v;
+            ++cnt;
+        };
+        // the stencil loops of orc_gen_triplets, emitting into CSR (order asserted above)
+        if (kind == 0) {
+            const int64_t N = p1;
+            for (int64_t i = 0; i < N; ++i)
+                for (int64_t j = 0; j < N; ++j) {
+                    int64_t k = i * N + j;
+                    if (i > 0) emit(k, k - N, -1.0);
+                    if (j > 0) emit(k, k - 1, -1.0);
+                    emit(k, k, 4.0);
+                    if (j < N - 1) emit(k, k + 1, -1.0);
+                    if (i < N - 1) emit(k, k + N, -1.0);
+                }
+        } else {
+            const int64_t N = p1, Nz = kind == 4 ? p2 : p1;
+            const double c = kind == 2 ? fparam : 0.0;
+            const double diag = kind == 2 ? 6.0 + 3.0 * c : 6.0;
+            const double lo = kind == 2 ? -1.0 - c : -1.0;
+            for (int64_t z = 0; z < Nz; ++z)
+                for (int64_t y = 0; y < N; ++y)
+                    for (int64_t x = 0; x < N; ++x) {
+                        int64_t k = (z * N + y) * N + x;
+                        if (z > 0) emit(k, k - N * N, lo);
+                        if (y > 0) emit(k, k - N, lo);
+                        if (x > 0) emit(k, k - 1, lo);
+                        emit(k, k, diag);
+                        if (x < N - 1) emit(k, k + 1, -1.0);
+                        if (y < N - 1) emit(k, k + N, -1.0);
+                        if (z < Nz - 1) emit(k, k + N * N, -1.0);
+                    }
+        }
+        if (!ok || cnt != nt) return 7;
+        for (int64_t i = 0; i < n; ++i) row_ptr[i + 1] += row_ptr[i];
+        *nnz = cnt;
+        return 0;
+    }
+    // fem2d: stable bucket by row (emission order kept inside a row), then per row a stable
+    // insertion sort by column and an in-order duplicate sum (== SparseCoo semantics)
+    std::vector<int64_t> tr(static_cast<size_t>(nt)), tc(static_cast<size_t>(nt));
+    std::vector<double> tv(static_cast<size_t>(nt));
+    int64_t dummy_n, dummy_t;
+    orc_gen_triplets(kind, p1, p2, fparam, &dummy_n, &dummy_t, tr.data(), tc.data(), tv.data());
+    std::vector<int64_t> start(static_cast<size_t>(n) + 1, 0);
+    for (int64_t k = 0; k < nt; ++k) ++start[tr[k] + 1];
+    for (int64_t i = 0; i < n; ++i) start[i + 1] += start[i];
+    {
+        std::vector<int64_t> pos(start.begin(), start.end() - 1);
+        for (int64_t k = 0; k < nt; ++k) {
+            int64_t p = pos[tr[k]]++;
+            col_idx[p] = tc[k];
+            vals[p] = tv[k];
+        }
+    }
+    std::vector<int64_t>().swap(tr);
+    std::vector<int64_t>().swap(tc);
+    std::vector<double>().swap(tv);
+    int64_t out = 0;
+    row_ptr[0] = 0;
+    std::vector<std::pair<int64_t, double>> row;
+    for (int64_t i = 0; i < n; ++i) {
+        row.clear();
+        for (int64_t p = start[i]; p < start[i + 1]; ++p) row.emplace_back(col_idx[p], vals[p]);
+        std::stable_sort(row.begin(), row.end(),
+                         [](const auto& a, const auto& b) { return a.first < b.first; });
+        for (size_t q = 0; q < row.size(); ++q) {
+            if (out > row_ptr[i] && col_idx[out - 1] == row[q].first) {
+                vals[out - 1] += row[q].second;
+            } else {
+                col_idx[out] = row[q].first;
+                vals[out] = row[q].second;
+                ++out;
+            }
+        }
+        row_ptr[i + 1] = out;
+    }
+    *nnz = out;
+    return 0;
+}
+
 int orc_gen_coords(int32_t kind, int64_t p1, int64_t p2, double* xs, double* ys) {
     if (kind == 0) {
         const int64_t N = p1;

@@ -90,6 +90,16 @@ int orc_adjoint_backward(int64_t n, const int64_t* row_ptr, const int64_t* col_i
  * With rows==NULL: only *n and *ntrip are written. */
 int orc_gen_triplets(int32_t kind, int64_t p1, int64_t p2, double fparam, int64_t* n,
                      int64_t* ntrip, int64_t* rows, int64_t* cols, double* vals);
+/* ---- generators straight to canonical CSR (int64 row_ptr/col_idx, fp64 vals) ----
+ * Same matrices as orc_gen_triplets followed by the SparseCoo canonicalization
+ * (sparse.cpp:9-53: stable sort by (row, col), duplicates summed in input order), without
+ * the O(nnz log nnz) permutation sort: stencil kinds already emit canonical rows; fem2d is
+ * bucketed by row in emission order (stable), then each short row is stably ordered by
+ * column and its duplicates summed in emission order.  Used for full-size (>= 20M DOF)
+ * configs.  With row_ptr==NULL only *n and *ntrip (an upper bound on nnz) are written;
+ * otherwise col_idx/vals must hold *ntrip entries and *nnz receives the canonical count. */
+int orc_gen_csr(int32_t kind, int64_t p1, int64_t p2, double fparam, int64_t* n, int64_t* ntrip,
+                int64_t* row_ptr, int64_t* col_idx, double* vals, int64_t* nnz);
 /* node coordinates (x,y) for 2-D kinds (0: grid, 3: fem interior nodes) */
 int orc_gen_coords(int32_t kind, int64_t p1, int64_t p2, double* xs, double* ys);
 

@@ -254,6 +254,29 @@ def generate(kind, p1, p2=0, fparam=1.0) -> Csr:
     return csr_from_triplets(n, n, r, c, v)
 
 
+def generate_csr(kind, p1, p2=0, fparam=1.0) -> Csr:
+    """Same matrix as generate(), emitted straight into canonical CSR (orc_gen_csr) —
+    O(nnz), no permutation sort; used at the full BASELINE sizes."""
+    k = KIND[kind]
+    n, nt, nnz = C.c_int64(), C.c_int64(), C.c_int64()
+    L = lib()
+    rc = L.orc_gen_csr(C.c_int32(k), C.c_int64(p1), C.c_int64(p2), C.c_double(fparam), C.byref(n),
+                       C.byref(nt), None, None, None, None)
+    if rc:
+        raise ValueError("bad generator params")
+    rp = np.empty(n.value + 1, np.int64)
+    ci = np.empty(nt.value, np.int64)
+    v = np.empty(nt.value)
+    rc = L.orc_gen_csr(C.c_int32(k), C.c_int64(p1), C.c_int64(p2), C.c_double(fparam), C.byref(n),
+                       C.byref(nt), _p(rp, _i64p), _p(ci, _i64p), _p(v, _f64p), C.byref(nnz))
+    if rc:
+        raise RuntimeError(f"orc_gen_csr failed ({rc})")
+    m = nnz.value
+    if m != nt.value:
+        ci, v = ci[:m].copy(), v[:m].copy()
+    return Csr(n.value, n.value, rp, ci, v)
+
+
 def gen_coords(kind, p1, p2=0):
     n = p1 * p1 if kind == "poisson2d" else (p1 - 2) * (p1 - 2)
     xs, ys = np.empty(n), np.empty(n)

@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <atomic>
 #include <thread>
 #include <cmath>
@@ -630,7 +631,21 @@ Solver::Solver(DevCsr* A_, int backend_, const sparsla_solve_options& o, DistCtx
                 const int cap_e = (h[0] + 7) / 8 * 8;
                 const size_t bytes = fused_res_bytes(cap_e);
                 int rs = 0;
-                CK(cudaFuncSetAttribute(cg_fused_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+                // the attribute is process-wide: raise it once per device to the opt-in
+                // maximum (never lowered per solver, so a parked solver with a larger image
+                // keeps launching); occupancy below uses this solver's own footprint
+                {
+                    static std::mutex mu;
+                    static bool raised[64] = {false};
+                    std::lock_guard<std::mutex> lk(mu);
+                    if (A->device < 64 && !raised[A->device]) {
+                        int optin = 0;
+                        CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, A->device));
+                        CK(cudaFuncSetAttribute(cg_fused_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                optin));
+                        raised[A->device] = true;
+                    }
+                }
                 CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&rs, cg_fused_kernel<true>, kSpmvThreads, bytes));
                 if ((long long)sms * rs >= m) { fused_res = cap_e; fused_grid = (int)m; }
             }
@@ -904,18 +919,45 @@ void Solver::run() {
     h_flag[0] = h_flag[1] = 0;
     // All ranks of a distributed solve see identical device flags (same all-gathered
     // totals, same scalar step), so they stop after the same number of graph launches.
+    long long last = -1;
     for (long long i = 0; i < max_graphs; ++i) {
+        last = i;
         if (fused) enqueue_fused(4 * kGraphIters);
         else if (capturable()) CK(cudaGraphLaunch(g_many, stream));
         else for (int k = 0; k < kGraphIters; ++k) enqueue_iteration();
         CK(cudaMemcpyAsync(h_flag + (i & 1), &st->done, sizeof(int), cudaMemcpyDeviceToHost, stream));
         CK(cudaEventRecord(ev[i & 1], stream));
         if (i > 0) {
-            CK(cudaEventSynchronize(ev[(i - 1) & 1]));
+            wait_event(ev[(i - 1) & 1]);
             if (h_flag[(i - 1) & 1]) break;
         }
     }
+    if (last >= 0) wait_event(ev[last & 1]);
     CK(cudaStreamSynchronize(stream));
+}
+
+// Single GPU: a blocking event wait.  Distributed: poll the event and the transport
+// (NCCL asynchronous errors) meanwhile; a graph that makes no progress within the
+// collective timeout (+5 s, so the fused mode's device-side timeout reports first) aborts
+// the communicator and raises TransportError instead of hanging.
+void Solver::wait_event(cudaEvent_t e) {
+    if (!dist || !dist->tr) { CK(cudaEventSynchronize(e)); return; }
+    const auto t0 = std::chrono::steady_clock::now();
+    const double limit = transport_timeout_s() + 5.0;
+    for (unsigned k = 0;; ++k) {
+        const cudaError_t q = cudaEventQuery(e);
+        if (q == cudaSuccess) return;
+        if (q != cudaErrorNotReady) CK(q);
+        if ((k & 63) == 0) {
+            dist->tr->check();
+            if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > limit) {
+                dist->tr->abort();
+                fail(SPARSLA_ERR_TRANSPORT, "distributed iteration made no progress within " +
+                                                std::to_string(limit) + " s: collective timeout (SPEC.md:534)");
+            }
+        }
+        std::this_thread::sleep_for(std::chrono::microseconds(20));
+    }
 }
 
 void Solver::report(sparsla_solve_report* rep) {
@@ -938,6 +980,7 @@ void Solver::report(sparsla_solve_report* rep) {
         case ST_BD_RV: std::snprintf(rep->diagnostic, 128, "breakdown: rhat^T v = 0 at iteration %lld", k); break;
         case ST_BD_TT: std::snprintf(rep->diagnostic, 128, "breakdown: t^T t = 0 at iteration %lld", k); break;
         case ST_BD_OMEGA: std::snprintf(rep->diagnostic, 128, "breakdown: omega = 0 at iteration %lld", k); break;
+        case ST_TRANSPORT: std::snprintf(rep->diagnostic, 128, "transport timeout at iteration %lld", S.k); break;
     }
     if (S.status == ST_RUNNING && !S.converged) std::snprintf(rep->diagnostic, 128, "running");
 }
@@ -989,6 +1032,36 @@ double device_dot(int device, long long n, const double* a, const double* b, cud
     CK(cudaMemcpyAsync(&out, &S.st->scratch[0], sizeof(double), cudaMemcpyDeviceToHost, S.stream));
     CK(cudaStreamSynchronize(S.stream));
     return out;
+}
+
+// SparseCoo::with_values (sparse.hpp:58-61) on a device matrix: same pattern, new values.
+// Every value-dependent cache is dropped (parked solvers hold the old diagonal; the value
+// dictionary, the Jacobi diagonal, the symmetry verdict and A^T are rebuilt lazily).
+void devcsr_set_values(DevCsr* A, const double* vals, int32_t mem) {
+    DeviceGuard g(A->device);
+    CK(cudaMemcpyAsync(A->val, vals, A->nnz * sizeof(double),
+                       mem == SPARSLA_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, A->stream));
+    CK(cudaStreamSynchronize(A->stream));
+    A->drop_parked();
+    // value dictionary: rebuilt from host values (the scan stops at the 257th distinct
+    // value); device values are only downloaded when the matrix had a dictionary
+    if (A->ws_var == 0 && !A->has_hub && (mem != SPARSLA_MEM_DEVICE || A->vd)) {
+        if (mem != SPARSLA_MEM_DEVICE) {
+            build_value_dictionary(A, vals);
+        } else {
+            std::vector<double> hv((size_t)A->nnz);
+            CK(memcpy_sync(hv.data(), A->val, A->nnz * sizeof(double), cudaMemcpyDeviceToHost));
+            build_value_dictionary(A, hv.data());
+        }
+    } else {
+        drop_value_dictionary(A);
+    }
+    A->smem_bytes = ws_smem_bytes(A, A->ws_var, A->vd);
+    if (A->dinv) { cudaFree(A->dinv); A->dinv = nullptr; }
+    A->dinv_uniform = -1;
+    A->sym_checked = -1;
+    delete A->transpose;
+    A->transpose = nullptr;
 }
 
 }  // namespace sparsla_b200
@@ -1113,32 +1186,7 @@ int sparsla_dcsr_create_i32(int device, int64_t nrows, int64_t ncols, const int3
 int sparsla_dcsr_set_values(sparsla_dcsr* H, const double* vals, int32_t mem) {
     return guarded([&] {
         need(H, "matrix");
-        DevCsr* A = H->A;
-        DeviceGuard g(A->device);
-        CK(cudaMemcpyAsync(A->val, vals, A->nnz * sizeof(double),
-                           mem == SPARSLA_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, A->stream));
-        CK(cudaStreamSynchronize(A->stream));
-        // value-dependent caches are invalid now (parked solvers hold the old diagonal)
-        A->drop_parked();
-        // value dictionary: rebuilt from host values (the scan stops at the 257th distinct
-        // value); device values are only downloaded when the matrix had a dictionary
-        if (A->ws_var == 0 && !A->has_hub && (mem != SPARSLA_MEM_DEVICE || A->vd)) {
-            if (mem != SPARSLA_MEM_DEVICE) {
-                build_value_dictionary(A, vals);
-            } else {
-                std::vector<double> hv((size_t)A->nnz);
-                CK(memcpy_sync(hv.data(), A->val, A->nnz * sizeof(double), cudaMemcpyDeviceToHost));
-                build_value_dictionary(A, hv.data());
-            }
-        } else {
-            drop_value_dictionary(A);
-        }
-        A->smem_bytes = ws_smem_bytes(A, A->ws_var, A->vd);
-        if (A->dinv) { cudaFree(A->dinv); A->dinv = nullptr; }
-        A->dinv_uniform = -1;
-        A->sym_checked = -1;
-        delete A->transpose;
-        A->transpose = nullptr;
+        devcsr_set_values(H->A, vals, mem);
     });
 }
 

@@ -70,6 +70,9 @@ struct DevCsr {
     DevCsr* get_transpose();
 };
 
+// new values in A's entry order (host or device pointer); drops every value-dependent cache
+void devcsr_set_values(DevCsr* A, const double* vals, int32_t mem);
+
 // canonical A^T of a device CSR into host arrays (coo_device.cu)
 void csr_transpose_device(int device, long long nrows, long long ncols, long long nnz, const int32_t* rp,
                           const int32_t* ci, const double* val, int32_t* trp, int32_t* tci, double* tv);
@@ -140,6 +143,7 @@ struct Solver {
     long long values_version = 0;  // A->values_version when this solver was built
     // fused peer-memory collectives (distributed CG)
     P2PCtx* d_p2p = nullptr;
+    int* p2p_err = nullptr;      // device flag raised by a timed-out peer wait (P2PCtx::err)
     std::vector<void*> p2p_allocs, p2p_ipc_opened;
     int fused_grid = 0;
     unsigned* fused_bar = nullptr;
@@ -153,6 +157,7 @@ struct Solver {
     void reset();
     void iterate(long long iters);
     void run();
+    void wait_event(cudaEvent_t e);  // distributed: polls the transport, times out
     void report(sparsla_solve_report* rep);
     long long launches_per_iteration() const;
     void kernel_times(long long iters, double* ms);

@@ -227,6 +227,10 @@ void Solver::p2p_setup() {
     X.push_pos = (const long long*)upload(ppos.data(), ppos.size() * 8);
     X.peer_vec = (double**)upload(pv.data(), nn * sizeof(void*));
     X.peer_vec2 = (double**)upload(pv2.data(), nn * sizeof(void*));
+    const int zero = 0;
+    X.err = (int*)upload(&zero, sizeof(int));
+    p2p_err = X.err;
+    X.timeout_ns = (unsigned long long)(transport_timeout_s() * 1e9);
     d_p2p = (P2PCtx*)upload(&X, sizeof(X));
 }
 
@@ -236,6 +240,7 @@ void Solver::p2p_release() noexcept {
     p2p_ipc_opened.clear();
     p2p_allocs.clear();
     d_p2p = nullptr;
+    p2p_err = nullptr;
     cudaGetLastError();
 }
 
@@ -471,6 +476,11 @@ void dist_krylov(sparsla_dist* D, int backend, const double* b, double* x, const
     S.reset();
     S.run();
     S.report(rep);
+    int perr = 0;
+    if (S.p2p_err) CKD(memcpy_sync(&perr, S.p2p_err, sizeof(int), cudaMemcpyDeviceToHost));
+    if (S.h_st->status == ST_TRANSPORT || perr)
+        fail(SPARSLA_ERR_TRANSPORT, "fused peer collective timed out after " + std::to_string(transport_timeout_s()) +
+                                        " s: a peer rank stopped contributing (SPEC.md:534)");
     D->alg_exchanges += S.h_st->spmv_count;  // one halo exchange per SpMV (incl. the initial one)
     D->alg_allreduces += S.h_st->reductions;
     D->alg_messages += S.h_st->spmv_count * (long long)D->ctx->nbr.size();
@@ -584,6 +594,27 @@ int sparsla_dist_reset_counters(sparsla_dist* D) {
 }
 
 // dist_spmv: y_owned = owned rows of A x, bit-identical to serial rows.
+int sparsla_dist_set_values(sparsla_dist* D, const double* vals_local, int32_t mem) {
+    return guarded([&] {
+        if (!D) fail(SPARSLA_ERR_INVALID_ARGUMENT, "plan is null");
+        DevCsr* A = D->A;
+        DeviceGuard g(A->device);
+        cudaStream_t s = A->stream;
+        // barrier: every rank has left its previous solve before peer mappings go away
+        double* f = dmalloc<double>(1 + (size_t)D->tr->P);
+        CKD(cudaMemsetAsync(f, 0, 8, s));
+        D->tr->allgather(s, f, f + 1, 1);
+        CKD(cudaStreamSynchronize(s));
+        cudaFree(f);
+        D->tr->allgathers -= 1;
+        for (auto*& p : D->parked) { delete p; p = nullptr; }
+        devcsr_set_values(A, vals_local, mem);
+        delete D->AT;
+        D->AT = nullptr;
+        D->tr->check();
+    });
+}
+
 int sparsla_dist_spmv(sparsla_dist* D, const double* x_owned, double* y_owned, int32_t mem) {
     return guarded([&] {
         DevCsr* A = D->A;

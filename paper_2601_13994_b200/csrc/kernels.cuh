@@ -37,7 +37,8 @@ constexpr int kRpCopy = 260;  // row_ptr entries staged per round (257 needed, 1
 // ---------------------------------------------------------------- solver state -------
 enum Status : int {
     ST_RUNNING = 0, ST_CONVERGED = 1, ST_MAXITER = 2, ST_BD_PQ = 3, ST_BD_RHO = 4,
-    ST_BD_RV = 5, ST_BD_TT = 6, ST_BD_OMEGA = 7
+    ST_BD_RV = 5, ST_BD_TT = 6, ST_BD_OMEGA = 7,
+    ST_TRANSPORT = 8  // fused peer collectives: a peer flag did not arrive within the timeout
 };
 
 struct KState {
@@ -248,6 +249,8 @@ struct P2PCtx {
     const long long* push_pos;         // element offset in that neighbour's vector
     double** peer_vec;                 // [nnbr] -> neighbour's SpMV-input vector (p / BiCGStab p-hat)
     double** peer_vec2;                // [nnbr] -> neighbour's second SpMV input (BiCGStab s-hat)
+    int* err;                          // this rank's transport-error flag (host maps it to TransportError)
+    unsigned long long timeout_ns;     // SPEC.md:534 collective timeout (SPARSLA_TRANSPORT_TIMEOUT, 30 s)
 };
 
 
@@ -276,12 +279,44 @@ __device__ inline void p2p_push_totals(const P2PCtx* X, KState* st, int point, c
     for (int q = 0; q < X->P; ++q) st_release_sys(X->peer_mflag[q] + point * X->P + X->me, e);
 }
 
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Bounded spin on a peer flag (collectives time out -> TransportError).  Gives
+// up when the flag has not reached `e` within the timeout, or at once when another CTA of
+// this rank already gave up; the first to give up raises the rank's error flag.
+__device__ inline bool p2p_wait_flag(const P2PCtx* X, const unsigned long long* flag, unsigned long long e) {
+    if (ld_acquire_sys(flag) >= e) return true;
+    const unsigned long long t0 = globaltimer_ns();
+    unsigned spins = 0;
+    while (ld_acquire_sys(flag) < e) {
+        __nanosleep(32);
+        if ((++spins & 255) == 0) {
+            if (*(volatile int*)X->err) return false;
+            if (globaltimer_ns() - t0 > X->timeout_ns) {
+                atomicExch(X->err, 1);
+                __threadfence_system();
+                return false;
+            }
+        }
+    }
+    return true;
+}
+
 // one thread per CTA of a consumer kernel: wait for every rank's totals of `point`, sum
-// them in ascending rank order and apply the scalar step to S
+// them in ascending rank order and apply the scalar step to S.  A timed-out
+// wait ends the solve with ST_TRANSPORT instead (every kernel then exits at entry).
 __device__ inline void p2p_consume(const P2PCtx* X, KState* S, int point, int k, int which) {
     const unsigned long long e = S->ep[point];
     for (int q = 0; q < X->P; ++q)
-        while (ld_acquire_sys(X->my_mflag + point * X->P + q) < e) __nanosleep(32);
+        if (!p2p_wait_flag(X, X->my_mflag + point * X->P + q, e)) {
+            S->status = ST_TRANSPORT;
+            S->done = 1;
+            return;
+        }
     double t[4] = {0, 0, 0, 0};
     for (int j = 0; j < k; ++j) {
         double s = ld_relaxed_sys(X->my_mail + ((size_t)point * X->P) * 8 + j);
@@ -303,11 +338,12 @@ __device__ inline void p2p_raise_halo(const P2PCtx* X, KState* st, int v) {
     for (int a = 0; a < X->nnbr; ++a) st_release_sys(X->peer_hflag[X->nbr_rank[a]] + v * X->P + X->me, e);
 }
 
-// wait until every neighbour has pushed this epoch's halo of vector v
+// wait until every neighbour has pushed this epoch's halo of vector v (bounded: on a
+// timeout the SpMV proceeds on stale halo values and the next consume ends the solve)
 __device__ inline void p2p_wait_halo(const P2PCtx* X, int v, unsigned long long e) {
     for (int a = 0; a < X->nnbr; ++a) {
         const int q = X->nbr_rank[a];
-        while (ld_acquire_sys(X->my_hflag + v * X->P + q) < e) __nanosleep(32);
+        if (!p2p_wait_flag(X, X->my_hflag + v * X->P + q, e)) return;
     }
 }
 

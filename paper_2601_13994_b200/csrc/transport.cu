@@ -75,7 +75,22 @@ NcclTransport::~NcclTransport() {
     if (comm) nccl_api().CommDestroy(static_cast<ncclComm_t>(comm));
 }
 
+void NcclTransport::abort() {
+    if (comm) nccl_api().CommAbort(static_cast<ncclComm_t>(comm));
+    comm = nullptr;
+}
+
+double transport_timeout_s() {
+    static const double t = [] {
+        const char* e = getenv("SPARSLA_TRANSPORT_TIMEOUT");
+        const double v = e ? atof(e) : 30.0;
+        return v > 0.0 ? v : 30.0;
+    }();
+    return t;
+}
+
 void NcclTransport::check() {
+    if (!comm) fail(SPARSLA_ERR_TRANSPORT, "NCCL communicator was aborted after a transport timeout");
     ncclResult_t a = ncclSuccess;
     nccl_check(nccl_api().CommGetAsyncError(static_cast<ncclComm_t>(comm), &a), "ncclCommGetAsyncError");
     if (a != ncclSuccess && a != ncclInProgress) {
@@ -142,10 +157,7 @@ void HostTransport::allgather(cudaStream_t s, const double* send, double* recv, 
 
 // ---------------------------------------------------------------------- local ----
 void TimedBarrier::arrive_and_wait() {
-    static const double timeout_s = [] {
-        const char* e = getenv("SPARSLA_TRANSPORT_TIMEOUT");
-        return e ? atof(e) : 30.0;
-    }();
+    const double timeout_s = transport_timeout_s();
     std::unique_lock<std::mutex> lk(mu);
     if (broken) fail(SPARSLA_ERR_TRANSPORT, "collective aborted: a peer rank timed out earlier");
     const long long gen = generation;

@@ -40,7 +40,11 @@ struct Transport {
     virtual void allgather(cudaStream_t s, const double* send, double* recv, int count) = 0;
     virtual bool capturable() const = 0;
     virtual void check() {}
+    virtual void abort() {}  // tear the communicator down so device-side waits on it end
 };
+
+// SPEC.md:534 collective timeout in seconds (SPARSLA_TRANSPORT_TIMEOUT, default 30)
+double transport_timeout_s();
 
 // ---- NCCL ----
 struct NcclApi;
@@ -55,6 +59,7 @@ struct NcclTransport : Transport {
     void allgather(cudaStream_t s, const double* send, double* recv, int count) override;
     bool capturable() const override { return true; }
     void check() override;
+    void abort() override;
 };
 
 // ---- host callbacks (caller-provided collectives, e.g. torch.distributed gloo) ----

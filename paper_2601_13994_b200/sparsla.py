@@ -941,6 +941,17 @@ class DistPlan:
         _check(lib().sparsla_dist_format(self.h, _p(out, _i64p)))
         return {"value_dict": bool(out[0]), "distinct_values": int(out[1]), "uniform_diag": bool(out[2])}
 
+    def set_values(self, vals_local, mem=MEM_HOST):
+        """Collective: new values of this rank's local matrix (local entry order)."""
+        if mem == MEM_HOST:
+            v = _f64(vals_local)
+            if len(v) != self.nnz_local:
+                raise DimensionError(f"{len(v)} values for {self.nnz_local} local entries")
+            _check(lib().sparsla_dist_set_values(self.h, _p(v, _f64p), C.c_int32(MEM_HOST)))
+        else:
+            _check(lib().sparsla_dist_set_values(self.h, C.cast(C.c_void_p(vals_local), _f64p),
+                                                 C.c_int32(MEM_DEVICE)))
+
     def set_fused(self, on: bool = True):
         """Fused peer-memory collectives for CG (no NCCL call per iteration)."""
         _check(lib().sparsla_dist_set_fused(self.h, C.c_int32(1 if on else 0)))

@@ -286,24 +286,61 @@ class DSparseMatrix:
             self.plan = S.DistPlan.create_host(device, P, rank, S.torch_host_transport(P, group), rows, owned,
                                                part_of, n)
         self.plan.set_fused(fused)
-        # value symmetry decides the default backend; A^T's values in the local entry order
-        # serve the nonsymmetric adjoint (the pattern is structurally symmetric)
-        keys = np.repeat(np.arange(n, dtype=np.int64), np.diff(rp)) * n + T.csr.col_idx
-        lr = np.repeat(owned, lens)
-        tpos = np.searchsorted(keys, T.csr.col_idx[ent] * n + lr)
-        vt = vals[np.minimum(tpos, max(len(keys) - 1, 0))] if len(ent) else np.zeros(0)
-        flag = torch.tensor([0.0 if np.array_equal(vt, vals[ent]) else 1.0])
-        if initialized:
-            fl = flag.to(f"cuda:{device}") if dist.get_backend(group) == "nccl" else flag
-            dist.all_reduce(fl, group=group)
-            flag = fl.cpu()
-        self.symmetric = float(flag[0]) == 0.0
-        self.vals_t = None if self.symmetric else np.ascontiguousarray(vt)
+        self._group, self._initialized = group, initialized
+        self._local_vals = torch.as_tensor(vals[ent]).to(f"cuda:{device}")
+        self._refresh_symmetry(vals)
         return self
 
     @property
     def n_owned(self):
         return len(self.owned)
+
+    def _allreduce_max(self, v):
+        """Collective max of a small float vector over the plan's ranks."""
+        import torch.distributed as dist
+        t = torch.tensor(v, dtype=torch.float64)
+        if self._initialized:
+            t = t.to(f"cuda:{self.device}") if dist.get_backend(self._group) == "nccl" else t
+            dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self._group)
+        return t.cpu().tolist()
+
+    def _refresh_symmetry(self, vals):
+        """Value symmetry decides the default backend; A^T's values in the local entry order
+        serve the nonsymmetric adjoint.  The distributed path needs a structurally symmetric
+        pattern: a local entry (i, j) whose mirror (j, i) is absent is rejected
+        on every rank (the verdict is all-reduced, so no rank is left in a collective)."""
+        T, n, ent = self.T, self.n_global, self.entries
+        rp = T.csr.row_ptr
+        lens = np.diff(rp)[self.owned]
+        keys = np.repeat(np.arange(n, dtype=np.int64), np.diff(rp)) * n + T.csr.col_idx
+        want = T.csr.col_idx[ent] * n + np.repeat(self.owned, lens)
+        tpos = np.minimum(np.searchsorted(keys, want), max(len(keys) - 1, 0))
+        missing = bool(len(ent)) and not np.array_equal(keys[tpos], want)
+        vt = vals[tpos] if len(ent) else np.zeros(0)
+        asym = not np.array_equal(vt, vals[ent])
+        fl_asym, fl_missing = self._allreduce_max([1.0 if asym else 0.0, 1.0 if missing else 0.0])
+        if fl_missing:
+            raise S.UnsupportedInputError(
+                "DSparseMatrix needs a structurally symmetric pattern (SPEC.md:510): some entry (i, j) "
+                "has no (j, i)")
+        self.symmetric = fl_asym == 0.0
+        self.vals_t = None if self.symmetric else np.ascontiguousarray(vt)
+
+    def _sync_values(self, vals: torch.Tensor):
+        """Collective: push changed values (e.g. after an optimizer step) into the plan
+        before a solve, so forward and backward see the CURRENT matrix (the plan copies the
+        values at build time).  Every rank takes the same branch (all-reduced flag)."""
+        if self._ent_t is None:
+            self._ent_t = torch.as_tensor(self.entries, device=f"cuda:{self.device}")
+        cur = vals.detach().to(f"cuda:{self.device}", torch.float64)[self._ent_t].contiguous()
+        changed = cur.shape != self._local_vals.shape or not torch.equal(
+            cur.view(torch.int64), self._local_vals.view(torch.int64))
+        (any_changed,) = self._allreduce_max([1.0 if changed else 0.0])
+        if any_changed:
+            torch.cuda.current_stream(self.device).synchronize()
+            self.plan.set_values(cur.data_ptr(), mem=S.MEM_DEVICE)
+            self._local_vals = cur.clone()
+            self._refresh_symmetry(vals.detach().cpu().numpy())
 
     def solve(self, b_local: torch.Tensor, atol: float = 1e-10, rtol: float = 0.0, max_iter: int = 10000,
               preconditioner: str = "jacobi", backend: str = "auto") -> torch.Tensor:
@@ -325,6 +362,7 @@ class _DSolve(torch.autograd.Function):
     @staticmethod
     def forward(ctx, vals, b, A: DSparseMatrix, opts: S.SolveOptions, backend: str):
         dev = A.device
+        A._sync_values(vals)
         b = b.detach().to(f"cuda:{dev}", torch.float64).contiguous()
         if b.numel() != A.n_owned:
             raise S.DimensionError(f"b_local has {b.numel()} entries, this partition owns {A.n_owned} rows")

@@ -102,3 +102,49 @@ def test_two_processes_one_gpu_bicgstab_fused(O, gpu):
         assert k == ro["iterations"] and same
         assert c["raw_exchanges"] <= 4 and c["raw_allgathers"] <= 4, c
     assert np.array_equal(x.view(np.int64), xo.view(np.int64))
+
+
+def _rank_timeout(rank, world, port, outq):
+    """rank 1 stops contributing after 3 iterations (its own max_iter); rank 0's fused
+    peer-collective waits must give up after SPARSLA_TRANSPORT_TIMEOUT and raise
+    TransportError instead of spinning forever."""
+    try:
+        sys.path.insert(0, ROOT)
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), SPARSLA_TRANSPORT_TIMEOUT="2")
+        import time
+        import torch.distributed as dist
+        from paper_2601_13994_b200 import bootstrap, sparsla as S
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        rows, owned, n = bootstrap.local_rows("poisson3d", 24, 0, 0.0, world, rank)
+        plan = S.DistPlan.create_host(0, world, rank, S.torch_host_transport(world), rows, owned, None, n)
+        plan.set_fused(True)
+        t0 = time.time()
+        try:
+            _, rep = plan.cg(np.ones(len(owned)), S.SolveOptions(atol=0.0, rtol=1e-10,
+                                                                 max_iter=3 if rank == 1 else 5000))
+            out = ("ok", rep.iterations, rep.diagnostic)
+        except S.TransportError as e:
+            out = ("transport_error", str(e), None)
+        outq.put((rank, out, time.time() - t0))
+        dist.barrier()
+        dist.destroy_process_group()
+    except BaseException:  # noqa: BLE001
+        import traceback
+        outq.put((rank, ("error", traceback.format_exc(), None), 0.0))
+
+
+def test_fused_peer_wait_times_out_with_transport_error(gpu):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_rank_timeout, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict((r, (o, t)) for r, o, t in [q.get(timeout=240) for _ in range(2)])
+    for p in procs:
+        p.join(timeout=60)
+    assert res[1][0][0] == "ok" and res[1][0][1] == 3, res[1]
+    assert res[0][0][0] == "transport_error", res[0]
+    assert "timed out" in res[0][0][1]
+    assert res[0][1] < 30.0, res[0]  # bounded by the 2 s timeout, not a hang

@@ -435,3 +435,17 @@ def test_fused_cg_resident_images_and_fallbacks(S, O, gpu, case):
     assert ro["converged"]
     rep_eq(r, ro)
     assert_bitwise(x, xo, case)
+
+
+def test_config_D_c1_breakdown_matches_oracle(S, O, gpu):
+    """SURVEY config D as defined (cell Peclet c = 1.0) is not solvable by plain right-Jacobi
+    BiCGStab: from N = 128 the residual diverges and the SPEC rho-breakdown fires.  The GPU
+    must break down exactly where the oracle does, with the same bits — which is why the
+    bench measures D at c = 0.1 and says so (bench.py D_DEVIATION)."""
+    A = O.generate_csr("convdiff3d", 128, 0, 1.0)
+    b = np.ones(A.nrows)
+    xo, ro = O.bicgstab(A, b, atol=0.0, rtol=1e-8, max_iter=3000)
+    assert not ro["converged"] and ro["iterations"] < 3000  # breakdown, not max_iter
+    x, r = S.bicgstab_solve(to_S(S, A), b, S.SolveOptions(atol=0.0, rtol=1e-8, max_iter=3000))
+    rep_eq(r, ro)
+    assert_bitwise(x, xo, "convdiff c=1 N=128")

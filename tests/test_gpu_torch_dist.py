@@ -139,3 +139,45 @@ def test_two_processes_solve_and_backward(O, gpu, kind, p1, c, rcb):
         lt, _, _ = O.dist_solve(T, g, po, 2, kind="bicgstab", atol=0.0, rtol=1e-11)
         assert np.array_equal(bits(gb), bits(lt))
         assert np.array_equal(bits(gv_canon), bits(-(lt[rows] * xo[A.col_idx])))
+
+
+def test_values_changed_between_solves_are_used(O, gpu):
+    """The plan copies the values at build time; a later in-place change of the values
+    tensor (an optimizer step) must reach the next solve and its backward."""
+    import torch
+    from paper_2601_13994_b200.torch_sla import DSparseMatrix
+    A, rows = _triplets(O, "convdiff3d", 8, 0.3)
+    vals = torch.tensor(A.vals, device="cuda:0", requires_grad=True)
+    D = DSparseMatrix.from_global(vals, rows, A.col_idx, (A.nrows, A.nrows), num_partitions=1, my_partition=0)
+    b = torch.ones(A.nrows, dtype=torch.float64, device="cuda:0")
+    x1 = D.solve(b, atol=0.0, rtol=1e-12)
+    with torch.no_grad():
+        vals.mul_(2.0)                        # A -> 2A: x -> x/2, still nonsymmetric
+    x2 = D.solve(b, atol=0.0, rtol=1e-12)
+    A2 = O.Csr(A.nrows, A.ncols, A.row_ptr, A.col_idx, 2.0 * A.vals)
+    po = O.partition_contiguous(A.nrows, 1)
+    xo, _, _ = O.dist_solve(A2, np.ones(A.nrows), po, 1, kind="bicgstab", atol=0.0, rtol=1e-12)
+    assert np.array_equal(bits(x2.detach().cpu().numpy()), bits(xo))
+    assert not np.array_equal(bits(x1.detach().cpu().numpy()), bits(xo))
+    x2.sum().backward()
+    lam = np.linalg.solve(A2.dense().T, np.ones(A.nrows))       # dense adjoint of the NEW matrix
+    gv_ref = -(lam[rows] * xo[A.col_idx])
+    err = np.abs(vals.grad.cpu().numpy() - gv_ref).max() / np.abs(gv_ref).max()
+    assert err <= 1e-7, err
+    # symmetrising the values flips the default backend to CG on the next solve
+    with torch.no_grad():
+        vals.copy_(torch.as_tensor(O.generate("poisson3d", 8).vals))
+    D.solve(b, atol=1e-12)
+    assert D.symmetric
+    D.close()
+
+
+def test_structurally_nonsymmetric_pattern_rejected(O, gpu):
+    import torch
+    from paper_2601_13994_b200 import sparsla as S
+    from paper_2601_13994_b200.torch_sla import DSparseMatrix
+    rows = np.array([0, 0, 1, 1, 2])
+    cols = np.array([0, 1, 1, 2, 2])       # (0,1) and (1,2) have no mirror
+    vals = torch.tensor([4.0, -1.0, 4.0, -1.0, 4.0], dtype=torch.float64, device="cuda:0")
+    with pytest.raises(S.UnsupportedInputError):
+        DSparseMatrix.from_global(vals, rows, cols, (3, 3), num_partitions=1, my_partition=0)
