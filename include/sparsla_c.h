@@ -186,6 +186,10 @@ int sparsla_dcsr_destroy(sparsla_dcsr* A);
  * block [5]=max row length [6]=kernel variant used by spmv (0 staged, 1 long-row)
  * [7]=staged-SpMV variant index (8 entries) */
 int sparsla_dcsr_info(const sparsla_dcsr* A, int64_t* info);
+/* Long-row split chosen from the row-length histogram (single GPU): out[0]=rows summed
+ * warp-per-row, out[1]=their entries, out[2]=the length threshold (0: no split).
+ * SPARSLA_LONG_ROW=<n> forces the threshold at matrix creation, 0 disables. */
+int sparsla_dcsr_long_rows(const sparsla_dcsr* A, int64_t* out);
 /* Storage format chosen for the SpMV stream: fmt[0]=1 when the value dictionary is in use
  * (<= 256 distinct values: 1-byte index per entry instead of the 8-byte value), fmt[1]=number
  * of distinct values in it (0 otherwise), fmt[2]=1 when the Jacobi inverse diagonal is
@@ -307,6 +311,26 @@ int sparsla_local_hub_destroy(sparsla_local_hub* hub);
 int sparsla_dist_create_local(int device, sparsla_local_hub* hub, int rank, const sparsla_local* L,
                               sparsla_dist** out);
 int sparsla_dist_destroy(sparsla_dist* D);
+/* ---- Transport as a first-class object ----
+ * One per rank; plans built on it share it (and its counters).  Backings: NCCL (one rank per
+ * GPU), in-process ranks (threads on a sparsla_local_hub) and host callbacks (e.g.
+ * torch.distributed gloo). */
+typedef struct sparsla_transport sparsla_transport;
+int sparsla_transport_create_nccl(int device, int nranks, int rank, const unsigned char* nccl_id,
+                                  sparsla_transport** out);
+int sparsla_transport_create_local(int device, sparsla_local_hub* hub, int rank, sparsla_transport** out);
+int sparsla_transport_create_host(int device, int nranks, int rank, const sparsla_host_transport* T,
+                                  sparsla_transport** out);
+int sparsla_transport_destroy(sparsla_transport* T);
+/* all_reduce_sum: sum of every rank's scalar in ascending rank order. */
+int sparsla_transport_all_reduce_sum(sparsla_transport* T, double local, double* global);
+/* out[0]=nranks [1]=rank [2]=exchanges [3]=all-gathers [4]=messages (raw transport calls) */
+int sparsla_transport_info(const sparsla_transport* T, int64_t* out);
+/* build this rank's device plan for L on T's device (collective over T) */
+int sparsla_dist_create(sparsla_transport* T, const sparsla_local* L, sparsla_dist** out);
+/* halo_exchange: halo[n_halo] = the neighbours' owned values of this
+ * rank's halo nodes (ascending global index), from x_owned.  Collective. */
+int sparsla_dist_halo_exchange(sparsla_dist* D, const double* x_owned, double* halo, int32_t mem);
 /* info[0]=n_owned [1]=n_halo [2]=neighbors [3]=interior chunks [4]=boundary chunks [5]=P
  * [6]=rank [7]=zero-copy halo segments [8]=n_global */
 int sparsla_dist_info(const sparsla_dist* D, int64_t* info);

@@ -125,6 +125,29 @@ constexpr int kNumWsVariants = sizeof(kWsVariants) / sizeof(kWsVariants[0]);
 // Per-matrix choice (measured, profiles/r01_spmv_sweep.md): rows of <= 8 entries -> the
 // 8-wide register variant at 3 CTAs/SM; <= 12 -> the 12-wide variant at 2 CTAs/SM (FEM);
 // longer -> 8-wide with the held-stage tail path.  SPARSLA_WS_VARIANT overrides (sweeps).
+// Long-row split threshold (entries): rows longer than this are summed warp-per-row by
+// spmv_longrow_kernel.  Chosen from the row-length histogram: only when the longest row
+// exceeds kLongMin AND is far above the typical row (max > 16 x the 99th percentile), so
+// stencil / FEM matrices (max/mean ~ 1.3) never take it.  SPARSLA_LONG_ROW=<n> forces a
+// threshold, 0 disables.
+static constexpr long long kLongMin = 64;
+template <class I>
+static long long long_row_threshold(long long nrows, const I* h_rp, long long max_row) {
+    if (const char* e = getenv("SPARSLA_LONG_ROW")) return std::max(0LL, atoll(e));
+    if (max_row <= kLongMin || nrows == 0) return 0;
+    // 99th percentile of the row lengths (histogram up to kLongMin, the rest counted above)
+    std::vector<long long> hist(kLongMin + 2, 0);
+    for (long long i = 0; i < nrows; ++i)
+        ++hist[std::min<long long>((long long)h_rp[i + 1] - (long long)h_rp[i], kLongMin + 1)];
+    long long acc = 0, p99 = kLongMin + 1;
+    for (long long l = 0; l < kLongMin + 2; ++l) {
+        acc += hist[l];
+        if (acc * 100 >= nrows * 99) { p99 = l; break; }
+    }
+    if (max_row < 16 * std::max(1LL, p99)) return 0;
+    return std::max(kLongMin, 4 * std::max(1LL, p99));
+}
+
 static int choose_ws_variant(long long max_row) {
     if (const char* e = getenv("SPARSLA_WS_VARIANT")) {
         const int x = atoi(e);
@@ -167,6 +190,7 @@ DevCsr::~DevCsr() {
     DeviceGuard g(device, true);
     cudaFree(rp); cudaFree(ci); cudaFree(val); cudaFree(dinv); cudaFree(ones);
     cudaFree(vidx); cudaFree(vtab);
+    cudaFree(long_rows); cudaFree(long_bits); cudaFree(s_rp); cudaFree(s_ci); cudaFree(s_val);
     if (stream) cudaStreamDestroy(stream);
     delete transpose;
 }
@@ -291,13 +315,70 @@ DevCsr* DevCsr::create(int device, long long nrows, long long ncols, const I* h_
     CK(memcpy_sync(A->val, h_val, nnz * sizeof(double), cudaMemcpyHostToDevice));
     A->vd_var = vd_variant();
     build_value_dictionary(A.get(), h_val);
-    // row-length statistics -> SpMV variant and staging capacity
+    long long mr_all = 0;
+    for (long long i = 0; i < nrows; ++i) mr_all = std::max<long long>(mr_all, (long long)h_rp[i + 1] - (long long)h_rp[i]);
+    // long rows -> warp-per-row kernel + short-row view for the staged kernels
+    std::vector<long long> srp;  // short-view row_ptr (host), when long rows exist
+    if (!local_layout) {
+        const long long LT = long_row_threshold<I>(nrows, h_rp, mr_all);
+        std::vector<int32_t> lr;
+        if (LT > 0)
+            for (long long i = 0; i < nrows; ++i)
+                if ((long long)h_rp[i + 1] - (long long)h_rp[i] > LT) lr.push_back((int32_t)i);
+        if (!lr.empty()) {
+            std::stable_sort(lr.begin(), lr.end(), [&](int32_t a, int32_t b) {
+                return h_rp[a + 1] - h_rp[a] > h_rp[b + 1] - h_rp[b];
+            });
+            std::vector<uint32_t> bits((size_t)(nrows + 31) / 32, 0u);
+            for (int32_t r : lr) bits[(size_t)r >> 5] |= 1u << (r & 31);
+            srp.assign((size_t)nrows + 1, 0);
+            for (long long i = 0; i < nrows; ++i) {
+                const bool lg = (bits[(size_t)i >> 5] >> (i & 31)) & 1u;
+                srp[i + 1] = srp[i] + (lg ? 0 : (long long)h_rp[i + 1] - (long long)h_rp[i]);
+            }
+            const long long snz = srp[nrows];
+            std::vector<int32_t> hsrp((size_t)nrows + 1), hsci((size_t)snz);
+            std::vector<double> hsv((size_t)snz);
+            for (long long i = 0; i <= nrows; ++i) hsrp[i] = (int32_t)srp[i];
+            parallel_for(nrows, [&](int64_t a, int64_t b) {
+                for (int64_t i = a; i < b; ++i) {
+                    const long long o = (long long)h_rp[i], d = srp[i];
+                    for (long long k = 0; k < srp[i + 1] - d; ++k) {
+                        hsci[d + k] = (int32_t)h_ci[o + k];
+                        hsv[d + k] = h_val[o + k];
+                    }
+                }
+            });
+            A->nlong = (long long)lr.size();
+            A->long_nnz = nnz - snz;
+            A->long_threshold = LT;
+            A->long_rows = dalloc<int32_t>(lr.size());
+            A->long_bits = dalloc<uint32_t>(bits.size());
+            A->s_rp = dalloc<int32_t>(nrows + 1 + kRpCopy + 8);
+            A->s_ci = dalloc<int32_t>(snz + 8);
+            A->s_val = dalloc<double>(snz + 4);
+            CK(cudaMemset(A->s_rp, 0, (nrows + 1 + kRpCopy + 8) * sizeof(int32_t)));
+            CK(cudaMemset(A->s_ci + snz, 0, 8 * sizeof(int32_t)));
+            CK(cudaMemset(A->s_val + snz, 0, 4 * sizeof(double)));
+            CK(memcpy_sync(A->long_rows, lr.data(), lr.size() * 4, cudaMemcpyHostToDevice));
+            CK(memcpy_sync(A->long_bits, bits.data(), bits.size() * 4, cudaMemcpyHostToDevice));
+            CK(memcpy_sync(A->s_rp, hsrp.data(), hsrp.size() * 4, cudaMemcpyHostToDevice));
+            if (snz) {
+                CK(memcpy_sync(A->s_ci, hsci.data(), snz * 4, cudaMemcpyHostToDevice));
+                CK(memcpy_sync(A->s_val, hsv.data(), snz * 8, cudaMemcpyHostToDevice));
+            }
+            drop_value_dictionary(A.get());  // the dictionary indexes the full entry order
+        }
+    }
+    // row-length statistics (of the view the staged kernels stream) -> SpMV variant and
+    // staging capacity
+    auto rpv = [&](long long i) { return srp.empty() ? (long long)h_rp[i] : srp[i]; };
     long long mb = 0, mr = 0;
     for (long long b = 0; b < nrows; b += kChunkSlots) {
         const long long e = std::min(b + kChunkSlots, nrows);
-        mb = std::max<long long>(mb, (long long)h_rp[e] - (long long)h_rp[b]);
+        mb = std::max<long long>(mb, rpv(e) - rpv(b));
     }
-    for (long long i = 0; i < nrows; ++i) mr = std::max<long long>(mr, (long long)h_rp[i + 1] - (long long)h_rp[i]);
+    for (long long i = 0; i < nrows; ++i) mr = std::max<long long>(mr, rpv(i + 1) - rpv(i));
     // rows of <= 7 entries (7-point stencils): the 7-wide dictionary kernel at 4 CTAs/SM
     // (56 registers) — more gathers in flight per SM than 8-wide at 3 CTAs/SM (config B
     // SpMV 1.050 -> 0.967 ms, profiles/r01b_notes.md)
@@ -305,12 +386,12 @@ DevCsr* DevCsr::create(int device, long long nrows, long long ncols, const I* h_
     long long mb32 = 0;
     for (long long b = 0; b < nrows; b += 32) {
         const long long e = std::min(b + 32, nrows);
-        mb32 = std::max<long long>(mb32, (long long)h_rp[e] - (long long)h_rp[b]);
+        mb32 = std::max<long long>(mb32, rpv(e) - rpv(b));
     }
     A->cap_v32 = (int)(((mb32 + 2) + 1) & ~1LL);
     A->cap_c32 = (int)(((mb32 + 6) + 3) & ~3LL);
     A->max_block_nnz = mb;
-    A->max_row = mr;
+    A->max_row = mr_all;
     A->cap_v = (int)(((mb + 2) + 1) & ~1LL);
     A->cap_c = (int)(((mb + 6) + 3) & ~3LL);
     A->ws_var = choose_ws_variant(mr);
@@ -461,7 +542,8 @@ DevCsr* DevCsr::get_transpose() {
 // but BiCGStab's t = A s-hat, whose three fused dots spill it; that one keeps the 8-wide
 // 3-CTA kernel (config D: 0.69 vs 0.73 ms).
 static int vd_var_of(const DevCsr* A, int mode) {
-    return (mode == SPMV_BICG_T && A->vd_var == 3) ? 0 : A->vd_var;
+    static const bool t7 = [] { const char* e = getenv("SPARSLA_BICGT_VD7"); return e && atoi(e) != 0; }();
+    return (mode == SPMV_BICG_T && A->vd_var == 3 && !t7) ? 0 : A->vd_var;
 }
 
 unsigned spmv_grid(const DevCsr* A, long long nch, int mode) {
@@ -482,6 +564,17 @@ void launch_spmv_part(DevCsr* A, cudaStream_t s, int mode, const double* x, doub
     if (grid == 0) return;
     SpmvParams P{};
     P.rp = A->rp; P.ci = A->ci; P.val = A->val;
+    if (A->nlong > 0) {  // long rows first (warp per row), then the short-row view
+        LongRowParams L{A->rp, A->ci, A->val, x, y, A->long_rows, A->nlong, red.st, check_done && red.st};
+        int dev = 0, sms = 0;
+        CK(cudaGetDevice(&dev));
+        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        const long long want = (A->nlong + kLongWarps - 1) / kLongWarps;
+        spmv_longrow_kernel<<<(unsigned)std::min<long long>(want, (long long)sms * 8), kLongWarps * 32, 0, s>>>(L);
+        CK(cudaGetLastError());
+        P.rp = A->s_rp; P.ci = A->s_ci; P.val = A->s_val;
+        P.long_bits = A->long_bits;
+    }
     P.vidx = A->vidx; P.vtab = A->vtab;
     P.x = x; P.y = y; P.n = A->nrows; P.chunk0 = 0; P.aux = aux;
     P.nch = nch;
@@ -757,9 +850,10 @@ void Solver::vec_point(int scalar, int slot, int check_done) {
         launch_vec<OP>(stream, P, R);
         return;
     }
-    if (dist && nd > 0) R.red_out = dist->red_send + slot * 8;
+    constexpr bool reduces = nd > 0 && VecPublishOnly<OP>::row < 0;  // U2's s.s is reduced by the t-SpMV
+    if (dist && reduces) R.red_out = dist->red_send + slot * 8;
     launch_vec<OP>(stream, P, R);
-    if (dist && nd > 0) reduce_point(scalar, slot, nd);
+    if (dist && reduces) reduce_point(scalar, slot, nd);
 }
 
 void Solver::enqueue_init() {
@@ -1043,9 +1137,15 @@ void devcsr_set_values(DevCsr* A, const double* vals, int32_t mem) {
                        mem == SPARSLA_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, A->stream));
     CK(cudaStreamSynchronize(A->stream));
     A->drop_parked();
+    if (A->nlong > 0 && A->nrows > 0) {
+        short_view_values_kernel<<<grid_for(A->nrows, 256), 256, 0, A->stream>>>(A->rp, A->val, A->s_rp, A->s_val,
+                                                                                A->nrows);
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(A->stream));
+    }
     // value dictionary: rebuilt from host values (the scan stops at the 257th distinct
     // value); device values are only downloaded when the matrix had a dictionary
-    if (A->ws_var == 0 && !A->has_hub && (mem != SPARSLA_MEM_DEVICE || A->vd)) {
+    if (A->ws_var == 0 && !A->has_hub && A->nlong == 0 && (mem != SPARSLA_MEM_DEVICE || A->vd)) {
         if (mem != SPARSLA_MEM_DEVICE) {
             build_value_dictionary(A, vals);
         } else {
@@ -1195,6 +1295,13 @@ int sparsla_dcsr_destroy(sparsla_dcsr* H) {
         if (!H) return;
         delete H->A;
         delete H;
+    });
+}
+
+int sparsla_dcsr_long_rows(const sparsla_dcsr* H, int64_t* out) {
+    return guarded([&] {
+        need(H, "matrix"); need(out, "out");
+        out[0] = H->A->nlong; out[1] = H->A->long_nnz; out[2] = H->A->long_threshold;
     });
 }
 

@@ -49,6 +49,14 @@ struct DevCsr {
     int dinv_uniform = -1;    // 1: every dinv entry has the same bits (dinv_value); -1: unknown
     double dinv_value = 0.0;
     int sym_checked = -1;
+    // long rows (single GPU): one warp per row in spmv_longrow_kernel; the staged SpMV runs
+    // on a short-row view of the matrix in which those rows are empty
+    long long nlong = 0, long_nnz = 0, long_threshold = 0;
+    int32_t* long_rows = nullptr;    // [nlong], longest first
+    uint32_t* long_bits = nullptr;   // [ceil(n/32)]
+    int32_t* s_rp = nullptr;         // short-row view (same padding as rp/ci/val)
+    int32_t* s_ci = nullptr;
+    double* s_val = nullptr;
     DevCsr* transpose = nullptr;
     cudaStream_t stream = nullptr;
     std::mutex lazy_mu;  // guards the lazily built caches (dinv, ones, symmetry, transpose)

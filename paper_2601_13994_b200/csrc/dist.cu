@@ -250,8 +250,21 @@ using namespace sparsla_b200;
 
 struct sparsla_local_hub { std::shared_ptr<LocalHub> hub; };
 
+// A Transport handle shared by every plan built on it.
+struct sparsla_transport {
+    std::shared_ptr<Transport> tr;
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    double* buf = nullptr;  // [1 + P] all_reduce staging
+    ~sparsla_transport() {
+        DeviceGuard g(device, true);
+        cudaFree(buf);
+        if (stream) cudaStreamDestroy(stream);
+    }
+};
+
 struct sparsla_dist {
-    std::unique_ptr<Transport> tr;
+    std::shared_ptr<Transport> tr;
     std::unique_ptr<DistCtx> ctx;
     DevCsr* A = nullptr;
     DevCsr* AT = nullptr;            // transposed values in A's local pattern (adjoint)
@@ -288,7 +301,7 @@ bool contiguous_range(const std::vector<int64_t>& v, size_t b, size_t e, long lo
 }
 
 // Builds the device plan for one rank.  Collective over the transport (count handshake).
-sparsla_dist* build_plan(int device, std::unique_ptr<Transport> tr, const sparsla_local* L) {
+sparsla_dist* build_plan(int device, std::shared_ptr<Transport> tr, const sparsla_local* L) {
     DeviceGuard g(device);
     auto D = std::make_unique<sparsla_dist>();
     const long long no = (long long)L->owned.size(), nh = (long long)L->halo.size();
@@ -506,7 +519,7 @@ int sparsla_dist_create_nccl(int device, int nranks, int rank, const unsigned ch
     return guarded([&] {
         if (!L || !out || !id) fail(SPARSLA_ERR_INVALID_ARGUMENT, "null argument");
         DeviceGuard g(device);
-        std::unique_ptr<Transport> tr(new NcclTransport(nranks, rank, id));
+        std::shared_ptr<Transport> tr(new NcclTransport(nranks, rank, id));
         *out = build_plan(device, std::move(tr), L);
     });
 }
@@ -517,7 +530,7 @@ int sparsla_dist_create_host(int device, int nranks, int rank, const sparsla_hos
         if (!L || !out || !T || !T->allgather || !T->exchange) fail(SPARSLA_ERR_INVALID_ARGUMENT, "null argument");
         DeviceGuard g(device);
         HostCallbacks cb{T->user, T->allgather, T->exchange};
-        std::unique_ptr<Transport> tr(new HostTransport(nranks, rank, cb));
+        std::shared_ptr<Transport> tr(new HostTransport(nranks, rank, cb));
         *out = build_plan(device, std::move(tr), L);
     });
 }
@@ -539,8 +552,103 @@ int sparsla_dist_create_local(int device, sparsla_local_hub* hub, int rank, cons
     return guarded([&] {
         if (!L || !out || !hub) fail(SPARSLA_ERR_INVALID_ARGUMENT, "null argument");
         DeviceGuard g(device);
-        std::unique_ptr<Transport> tr(new LocalTransport(hub->hub, rank));
+        std::shared_ptr<Transport> tr(new LocalTransport(hub->hub, rank));
         *out = build_plan(device, std::move(tr), L);
+    });
+}
+
+// ---- first-class transports: one per rank, shared by its plans ----
+static sparsla_transport* wrap_transport(int device, std::shared_ptr<Transport> tr) {
+    auto T = std::make_unique<sparsla_transport>();
+    T->device = device;
+    T->tr = std::move(tr);
+    CKD(cudaStreamCreateWithFlags(&T->stream, cudaStreamNonBlocking));
+    T->buf = dmalloc<double>(1 + (size_t)T->tr->P + 1);
+    return T.release();
+}
+
+int sparsla_transport_create_nccl(int device, int nranks, int rank, const unsigned char* id, sparsla_transport** out) {
+    return guarded([&] {
+        if (!out || !id) fail(SPARSLA_ERR_INVALID_ARGUMENT, "null argument");
+        DeviceGuard g(device);
+        *out = wrap_transport(device, std::make_shared<NcclTransport>(nranks, rank, id));
+    });
+}
+
+int sparsla_transport_create_local(int device, sparsla_local_hub* hub, int rank, sparsla_transport** out) {
+    return guarded([&] {
+        if (!out || !hub) fail(SPARSLA_ERR_INVALID_ARGUMENT, "null argument");
+        DeviceGuard g(device);
+        *out = wrap_transport(device, std::make_shared<LocalTransport>(hub->hub, rank));
+    });
+}
+
+int sparsla_transport_create_host(int device, int nranks, int rank, const sparsla_host_transport* T,
+                                  sparsla_transport** out) {
+    return guarded([&] {
+        if (!out || !T || !T->allgather || !T->exchange) fail(SPARSLA_ERR_INVALID_ARGUMENT, "null argument");
+        DeviceGuard g(device);
+        HostCallbacks cb{T->user, T->allgather, T->exchange};
+        *out = wrap_transport(device, std::make_shared<HostTransport>(nranks, rank, cb));
+    });
+}
+
+int sparsla_transport_destroy(sparsla_transport* T) {
+    return guarded([&] { delete T; });
+}
+
+// all_reduce_sum: every rank's scalar, summed in ascending rank order.
+int sparsla_transport_all_reduce_sum(sparsla_transport* T, double local, double* global) {
+    return guarded([&] {
+        if (!T || !global) fail(SPARSLA_ERR_INVALID_ARGUMENT, "null argument");
+        DeviceGuard g(T->device);
+        const int P = T->tr->P;
+        CKD(cudaMemcpyAsync(T->buf, &local, 8, cudaMemcpyHostToDevice, T->stream));
+        T->tr->allgather(T->stream, T->buf, T->buf + 1, 1);
+        std::vector<double> all((size_t)P);
+        CKD(cudaMemcpyAsync(all.data(), T->buf + 1, (size_t)P * 8, cudaMemcpyDeviceToHost, T->stream));
+        CKD(cudaStreamSynchronize(T->stream));
+        double acc = all[0];
+        for (int q = 1; q < P; ++q) acc = acc + all[(size_t)q];
+        *global = acc;
+        T->tr->check();
+    });
+}
+
+int sparsla_transport_info(const sparsla_transport* T, int64_t* out) {
+    return guarded([&] {
+        if (!T || !out) fail(SPARSLA_ERR_INVALID_ARGUMENT, "null argument");
+        out[0] = T->tr->P; out[1] = T->tr->rank; out[2] = T->tr->exchanges; out[3] = T->tr->allgathers;
+        out[4] = T->tr->messages;
+    });
+}
+
+int sparsla_dist_create(sparsla_transport* T, const sparsla_local* L, sparsla_dist** out) {
+    return guarded([&] {
+        if (!T || !L || !out) fail(SPARSLA_ERR_INVALID_ARGUMENT, "null argument");
+        DeviceGuard g(T->device);
+        *out = build_plan(T->device, T->tr, L);
+    });
+}
+
+// halo_exchange: the neighbours' current owned values of this rank's halo
+// (ascending global index, the HaloMap's canonical order), from the owned slice.
+int sparsla_dist_halo_exchange(sparsla_dist* D, const double* x_owned, double* halo, int32_t mem) {
+    return guarded([&] {
+        DevCsr* A = D->A;
+        DistCtx* C = D->ctx.get();
+        DeviceGuard g(A->device);
+        cudaStream_t s = A->stream;
+        DVec X(x_owned, C->n_owned, C->vec_len - C->n_owned, mem, s);
+        C->exchange(s, X.d);
+        CKD(cudaStreamWaitEvent(s, C->ev_halo, 0));
+        if (C->n_halo)
+            CKD(cudaMemcpyAsync(halo, X.d + C->halo_base, C->n_halo * 8,
+                                mem == SPARSLA_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+        CKD(cudaStreamSynchronize(s));
+        D->alg_exchanges += 1;
+        D->alg_messages += (long long)C->nbr.size();
+        D->tr->check();
     });
 }
 

@@ -362,7 +362,9 @@ struct RedParams {
     const KState* s_loc;  // consumer kernels: CTA-local scalar state to write back first
 };
 
-template <int NT, int NDOT>
+// NFIN >= NDOT: the last CTA reduces NFIN partial rows; rows NDOT.. were published per
+// chunk by an earlier kernel of the same reduction point (BiCGStab: s.s by update 2).
+template <int NT, int NDOT, int NFIN = NDOT>
 __device__ void publish_and_finish(double (&part)[NDOT], long long chunk, const RedParams& R,
                                    double* sred) {
     __shared__ int s_last;
@@ -376,24 +378,24 @@ __device__ void publish_and_finish(double (&part)[NDOT], long long chunk, const 
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    double tot[NDOT];
-    final_reduce<NT, NDOT>(R.partials, R.nchunks, tot, sred);
+    double tot[NFIN];
+    final_reduce<NT, NFIN>(R.partials, R.nchunks, tot, sred);
     if (threadIdx.x == 0) {
         if (R.p2p) {
             if (R.s_loc) *R.st = *R.s_loc;
             if (!R.st->done) {
                 double t3[4] = {0, 0, 0, 0};
 #pragma unroll
-                for (int d = 0; d < NDOT; ++d) t3[d] = tot[d];
-                p2p_push_totals(R.p2p, R.st, R.point, t3, NDOT);
+                for (int d = 0; d < NFIN; ++d) t3[d] = tot[d];
+                p2p_push_totals(R.p2p, R.st, R.point, t3, NFIN);
             }
         } else if (R.red_out) {
 #pragma unroll
-            for (int d = 0; d < NDOT; ++d) R.red_out[d] = tot[d];
+            for (int d = 0; d < NFIN; ++d) R.red_out[d] = tot[d];
         } else {
             double t3[4] = {0, 0, 0, 0};
 #pragma unroll
-            for (int d = 0; d < NDOT; ++d) t3[d] = tot[d];
+            for (int d = 0; d < NFIN; ++d) t3[d] = tot[d];
             apply_scalar(R.scalar, R.st, t3);
         }
         *R.ticket = 0u;
@@ -403,7 +405,7 @@ __device__ void publish_and_finish(double (&part)[NDOT], long long chunk, const 
 
 // Persistent kernels: each CTA publishes several chunk partials, then takes ONE ticket;
 // the last CTA to finish reduces all chunks (same canonical result as publish_and_finish).
-template <int NT, int NDOT, int BAR>
+template <int NT, int NDOT, int BAR, int NFIN = NDOT>
 __device__ void ticket_and_finish(const RedParams& R, double* sred, int* s_flag) {
     if (threadIdx.x == 0) {
         __threadfence();
@@ -413,24 +415,24 @@ __device__ void ticket_and_finish(const RedParams& R, double* sred, int* s_flag)
     group_sync<BAR, NT>();
     if (!*s_flag) return;
     __threadfence();
-    double tot[NDOT];
-    final_reduce<NT, NDOT, BAR>(R.partials, R.nchunks, tot, sred);
+    double tot[NFIN];
+    final_reduce<NT, NFIN, BAR>(R.partials, R.nchunks, tot, sred);
     if (threadIdx.x == 0) {
         if (R.p2p) {
             if (R.s_loc) *R.st = *R.s_loc;
             if (!R.st->done) {
                 double t3[4] = {0, 0, 0, 0};
 #pragma unroll
-                for (int d = 0; d < NDOT; ++d) t3[d] = tot[d];
-                p2p_push_totals(R.p2p, R.st, R.point, t3, NDOT);
+                for (int d = 0; d < NFIN; ++d) t3[d] = tot[d];
+                p2p_push_totals(R.p2p, R.st, R.point, t3, NFIN);
             }
         } else if (R.red_out) {
 #pragma unroll
-            for (int d = 0; d < NDOT; ++d) R.red_out[d] = tot[d];
+            for (int d = 0; d < NFIN; ++d) R.red_out[d] = tot[d];
         } else {
             double t3[4] = {0, 0, 0, 0};
 #pragma unroll
-            for (int d = 0; d < NDOT; ++d) t3[d] = tot[d];
+            for (int d = 0; d < NFIN; ++d) t3[d] = tot[d];
             apply_scalar(R.scalar, R.st, t3);
         }
         *R.ticket = 0u;
@@ -494,7 +496,11 @@ enum SpmvMode : int { SPMV_PLAIN = 0, SPMV_CG = 1, SPMV_BICG_V = 2, SPMV_BICG_T 
 template <int MODE> struct SpmvDots { static constexpr int n = 0; };
 template <> struct SpmvDots<SPMV_CG> { static constexpr int n = 1; };
 template <> struct SpmvDots<SPMV_BICG_V> { static constexpr int n = 1; };
-template <> struct SpmvDots<SPMV_BICG_T> { static constexpr int n = 3; };
+template <> struct SpmvDots<SPMV_BICG_T> { static constexpr int n = 2; };  // t.t, t.s (s.s: update 2)
+// partial rows reduced at the SpMV's reduction point (BiCGStab t: t.t, t.s and s.s, whose
+// per-chunk partials bicg_update2 published when it produced s — same canonical shape)
+template <int MODE> struct SpmvFin { static constexpr int n = SpmvDots<MODE>::n; };
+template <> struct SpmvFin<SPMV_BICG_T> { static constexpr int n = 3; };
 
 struct SpmvParams {
     const int32_t* rp;
@@ -515,8 +521,18 @@ struct SpmvParams {
     int cap_v, cap_c;   // staged capacities (elements) per round
     int l2_keep;        // 1: matrix stream evict_last (working set fits L2), 0: evict_first
     int check_done;
+    const uint32_t* long_bits;  // rows summed by spmv_longrow_kernel (empty in this view): bit set
     RedParams red;
 };
+
+// A row that spmv_longrow_kernel already summed is empty in the short-row view, so its
+// staged sum is +0.0: take the long-row kernel's value instead (the bit is only read for
+// rows whose sum is exactly zero, and only when the matrix has long rows at all).
+__device__ __forceinline__ double long_row_fix(const SpmvParams& P, long long row, double y) {
+    if (P.long_bits != nullptr && y == 0.0 && ((__ldg(P.long_bits + (row >> 5)) >> (row & 31)) & 1u))
+        return __ldcg(P.y + row);
+    return y;
+}
 
 template <int MODE>
 __device__ __forceinline__ void spmv_epilogue(const SpmvParams& P, long long row, double y,
@@ -526,10 +542,8 @@ __device__ __forceinline__ void spmv_epilogue(const SpmvParams& P, long long row
     } else if constexpr (MODE == SPMV_BICG_V) {
         acc[0] = __dadd_rn(acc[0], __dmul_rn(__ldg(P.aux + row), y));
     } else if constexpr (MODE == SPMV_BICG_T) {
-        const double s = __ldg(P.aux + row);
         acc[0] = __dadd_rn(acc[0], __dmul_rn(y, y));
-        acc[1] = __dadd_rn(acc[1], __dmul_rn(y, s));
-        acc[2] = __dadd_rn(acc[2], __dmul_rn(s, s));
+        acc[1] = __dadd_rn(acc[1], __dmul_rn(y, __ldg(P.aux + row)));
     }
 }
 
@@ -578,19 +592,20 @@ __global__ void __launch_bounds__(kSpmvThreads, 2) spmv_direct_kernel(SpmvParams
     for (int r = 0; r < nrounds; ++r) {
         const long long row = base + (long long)r * kChunkSlots + t;
         if (row < P.n) {
-            const double y = row_sum(__ldg(P.rp + row), __ldg(P.rp + row + 1), P.x,
+            double y = row_sum(__ldg(P.rp + row), __ldg(P.rp + row + 1), P.x,
                                      [&](int k, int& c, double& v) {
                                          c = __ldg(P.ci + k);
                                          v = __ldg(P.val + k);
                                      });
+            y = long_row_fix(P, row, y);
             P.y[row] = y;
             spmv_epilogue<MODE>(P, row, y, acc);
         }
     }
     if constexpr (ND > 0) {
-        __shared__ double sred[ND * (kSpmvThreads / 32)];
+        __shared__ double sred[SpmvFin<MODE>::n * (kSpmvThreads / 32)];
         block_tree<kSpmvThreads, ND>(acc, sred);
-        publish_and_finish<kSpmvThreads, ND>(acc, chunk, P.red, sred);
+        publish_and_finish<kSpmvThreads, ND, SpmvFin<MODE>::n>(acc, chunk, P.red, sred);
     }
 }
 
@@ -685,7 +700,7 @@ __global__ void __launch_bounds__(kWsThreads, MINB) spmv_ws_kernel(SpmvParams P)
     }
 
     // ------------------------------------------------------------------ consumers ----
-    __shared__ double sred[NA * kConsumerWarps];
+    __shared__ double sred[(SpmvFin<MODE>::n > 0 ? SpmvFin<MODE>::n : 1) * kConsumerWarps];
     __shared__ int s_flag;
     static_assert(!VD || (RPT == 1 && !HUB), "value-dictionary kernels use the lean consumer");
     if constexpr (VD) {
@@ -767,7 +782,6 @@ __global__ void __launch_bounds__(kWsThreads, MINB) spmv_ws_kernel(SpmvParams P)
                     } else if constexpr (MODE == SPMV_BICG_T) {
                         acc[0] = __dadd_rn(acc[0], __dmul_rn(y, y));
                         acc[1] = __dadd_rn(acc[1], __dmul_rn(y, eop));
-                        acc[2] = __dadd_rn(acc[2], __dmul_rn(eop, eop));
                     } else {
                         spmv_epilogue<MODE>(P, row, y, acc);
                     }
@@ -782,7 +796,7 @@ __global__ void __launch_bounds__(kWsThreads, MINB) spmv_ws_kernel(SpmvParams P)
                 }
             }
         }
-        if constexpr (ND > 0) ticket_and_finish<kConsumerWarps * 32, ND, 1>(P.red, sred, &s_flag);
+        if constexpr (ND > 0) ticket_and_finish<kConsumerWarps * 32, ND, 1, SpmvFin<MODE>::n>(P.red, sred, &s_flag);
         return;
     }
     long long g = 0;
@@ -928,7 +942,11 @@ __global__ void __launch_bounds__(kWsThreads, MINB) spmv_ws_kernel(SpmvParams P)
 #pragma unroll
             for (int j = 0; j < RPT; ++j) {
                 const long long row = base + (long long)(r + j) * kChunkSlots + t;
-                if (j < cnt && row < P.n) { P.y[row] = y[j]; spmv_epilogue<MODE>(P, row, y[j], acc); }
+                if (j < cnt && row < P.n) {
+                    const double yj = long_row_fix(P, row, y[j]);
+                    P.y[row] = yj;
+                    spmv_epilogue<MODE>(P, row, yj, acc);
+                }
             }
             g += cnt;
         }
@@ -940,7 +958,7 @@ __global__ void __launch_bounds__(kWsThreads, MINB) spmv_ws_kernel(SpmvParams P)
             }
         }
     }
-    if constexpr (ND > 0) ticket_and_finish<kConsumerWarps * 32, ND, 1>(P.red, sred, &s_flag);
+    if constexpr (ND > 0) ticket_and_finish<kConsumerWarps * 32, ND, 1, SpmvFin<MODE>::n>(P.red, sred, &s_flag);
 }
 
 // Warp-pipelined staged variant (persistent, no producer/consumer hand-off).  Each warp
@@ -971,7 +989,7 @@ __global__ void __launch_bounds__(kSpmvThreads, MINB) spmv_wp_kernel(SpmvParams 
     const int t = threadIdx.x, w = t >> 5, lane = t & 31;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem) + w * D;
     unsigned char* ring = smem + 1024 + (size_t)w * D * L.stage;
-    __shared__ double sred[NA * NW];
+    __shared__ double sred[(SpmvFin<MODE>::n > 0 ? SpmvFin<MODE>::n : 1) * NW];
     __shared__ int s_flag;
     if (lane == 0) {
         for (int s = 0; s < D; ++s) mbar_init(&bars[s], 1);
@@ -1063,6 +1081,7 @@ __global__ void __launch_bounds__(kSpmvThreads, MINB) spmv_wp_kernel(SpmvParams 
                 issue_next();
             }
             if (row < P.n) {
+                y = long_row_fix(P, row, y);
                 P.y[row] = y;
                 spmv_epilogue<MODE>(P, row, y, acc);
             }
@@ -1075,7 +1094,7 @@ __global__ void __launch_bounds__(kSpmvThreads, MINB) spmv_wp_kernel(SpmvParams 
             }
         }
     }
-    if constexpr (ND > 0) ticket_and_finish<kSpmvThreads, ND, 1>(P.red, sred, &s_flag);
+    if constexpr (ND > 0) ticket_and_finish<kSpmvThreads, ND, 1, SpmvFin<MODE>::n>(P.red, sred, &s_flag);
 }
 
 // -------------------------------------------------------------- vector kernels -------
@@ -1118,6 +1137,93 @@ __device__ __forceinline__ double2 ldd(const double* d, double d_uni, long long 
 __device__ __forceinline__ double lane(const double2& v, int e) { return e ? v.y : v.x; }
 __device__ __forceinline__ void set_lane(double2& v, int e, double x) { if (e) v.y = x; else v.x = x; }
 
+// ------------------------------------------------------------------ long rows ------
+// Rows longer than the thread-per-row kernels handle well (power-law hubs; threshold from
+// the row-length histogram, DevCsr::create) get one warp each.  Lanes load col/val
+// coalesced, gather x and form the products in parallel (__dmul_rn); lane 0 then adds them
+// strictly left to right from 0.0 — the reference's per-row order (sparse.cpp:144-152),
+// bit-identical.  That dependent add chain is the floor of a bit-exact row sum, so the
+// loads are software-pipelined around it: while lane 0 runs the chain of batch b, the x
+// gathers of batch b+1 and the col/val loads of batch b+2 are in flight.  The list is
+// sorted longest first and walked grid-stride, so the longest chains start at once.
+// The staged SpMV then runs on the short-row view (long rows empty) and picks these sums
+// up (long_row_fix), keeping its fused dots in canonical order.
+constexpr int kLongWarps = 8;
+constexpr int kLongU = 4;                    // entries per lane per batch
+constexpr int kLongBatch = 32 * kLongU;      // 128 entries per batch
+
+struct LongRowParams {
+    const int32_t* rp;
+    const int32_t* ci;
+    const double* val;
+    const double* x;
+    double* y;
+    const int32_t* rows;  // long rows, longest first
+    long long nlong;
+    const KState* st;
+    int check_done;
+};
+
+static __global__ void __launch_bounds__(kLongWarps * 32) spmv_longrow_kernel(LongRowParams P) {
+    if (P.check_done && P.st->done) return;
+    __shared__ __align__(16) double prod[kLongWarps][kLongBatch];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (long long li = (long long)blockIdx.x * kLongWarps + w; li < P.nlong; li += (long long)gridDim.x * kLongWarps) {
+        const int row = __ldg(P.rows + li);
+        const int kb = __ldg(P.rp + row), ke = __ldg(P.rp + row + 1);
+        int cn[kLongU];
+        double vn[kLongU], vc[kLongU], xc[kLongU];
+        auto load_cv = [&](int k0) {
+#pragma unroll
+            for (int u = 0; u < kLongU; ++u) {
+                const int k = k0 + u * 32 + lane;
+                cn[u] = k < ke ? __ldcs(P.ci + k) : -1;
+                vn[u] = k < ke ? __ldcs(P.val + k) : 0.0;
+            }
+        };
+        auto gather = [&]() {
+#pragma unroll
+            for (int u = 0; u < kLongU; ++u) { xc[u] = cn[u] >= 0 ? __ldg(P.x + cn[u]) : 0.0; vc[u] = vn[u]; }
+        };
+        load_cv(kb);
+        gather();
+        load_cv(kb + kLongBatch);
+        double sum = 0.0;
+        for (int k0 = kb; k0 < ke; k0 += kLongBatch) {
+#pragma unroll
+            for (int u = 0; u < kLongU; ++u) prod[w][u * 32 + lane] = __dmul_rn(vc[u], xc[u]);
+            gather();                         // batch b+1: its columns arrived meanwhile
+            load_cv(k0 + 2 * kLongBatch);     // batch b+2
+            __syncwarp();
+            if (lane == 0) {
+                const int cnt = min(kLongBatch, ke - k0);
+                const double2* p2 = reinterpret_cast<const double2*>(prod[w]);
+                if (cnt == kLongBatch) {
+#pragma unroll 8
+                    for (int j = 0; j < kLongBatch / 2; ++j) {
+                        const double2 q = p2[j];
+                        sum = __dadd_rn(sum, q.x);
+                        sum = __dadd_rn(sum, q.y);
+                    }
+                } else {
+                    for (int j = 0; j < cnt; ++j) sum = __dadd_rn(sum, prod[w][j]);
+                }
+            }
+            __syncwarp();
+        }
+        if (lane == 0) P.y[row] = sum;
+    }
+}
+
+// short-row view values after set_values: copy every row that is not long
+static __global__ void short_view_values_kernel(const int32_t* rp, const double* val, const int32_t* s_rp,
+                                         double* s_val, long long n) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int b = s_rp[i], e = s_rp[i + 1], o = rp[i];
+    for (int k = b; k < e; ++k) s_val[k] = val[o + (k - b)];
+}
+
 enum VecOp : int { V_CG_INIT, V_CG_U1, V_CG_U2, V_BI_INIT, V_BI_U1, V_BI_U2, V_BI_U3 };
 // CG iteration split used by the solver: U1 = r -= a q, z = d r, {r.z, r.r} (reads r q d);
 // U2 = x += a p, then p = z + b p unless the solve just terminated (reads x p r d).  p is
@@ -1129,7 +1235,11 @@ template <> struct VecTraits<V_CG_U1>   { static constexpr int nin = 3, ndot = 2
 template <> struct VecTraits<V_CG_U2>   { static constexpr int nin = 4, ndot = 0; };  // x p r d
 template <> struct VecTraits<V_BI_INIT> { static constexpr int nin = 2, ndot = 3; };  // b v
 template <> struct VecTraits<V_BI_U1>   { static constexpr int nin = 4, ndot = 0; };  // r p v d
-template <> struct VecTraits<V_BI_U2>   { static constexpr int nin = 3, ndot = 0; };  // r v d
+template <> struct VecTraits<V_BI_U2>   { static constexpr int nin = 3, ndot = 1; };  // r v d; s.s
+// kernels whose chunk partials are reduced by a LATER kernel (no ticket, no finish): U2's
+// s.s partials land in row 2 of the t-SpMV's reduction point
+template <int OP> struct VecPublishOnly { static constexpr int row = -1; };
+template <> struct VecPublishOnly<V_BI_U2> { static constexpr int row = 2; };
 template <> struct VecTraits<V_BI_U3>   { static constexpr int nin = 6, ndot = 2; };  // x ph s sh t rh
 
 struct VecScalars {
@@ -1198,6 +1308,7 @@ __device__ __forceinline__ void vec_compute(const VecParams& P, const VecScalars
         if constexpr (OP == V_BI_U2) {  // s = r - alpha v; sh = d s
             const double s = __dsub_rn(lane(in[0], e), __dmul_rn(S.alpha, lane(in[1], e)));
             set_lane(o0, e, s); set_lane(o1, e, __dmul_rn(lane(in[2], e), s));
+            pr[0][e] = __dmul_rn(s, s);
         }
         if constexpr (OP == V_BI_U3) {
             if (S.half) {  // x += alpha ph; r = s
@@ -1311,7 +1422,9 @@ __global__ void __launch_bounds__(kVecThreads) vec_kernel(VecParams P) {
 #pragma unroll
         for (int d = 0; d < ND; ++d) v[d] = __dadd_rn(acc[d][0], acc[d][1]);  // slot pair
         block_tree<kVecThreads, ND>(v, sred);
-        if constexpr (PERSIST) {
+        if constexpr (VecPublishOnly<OP>::row >= 0) {
+            if (t == 0) P.red.partials[VecPublishOnly<OP>::row * P.red.nchunks + chunk] = v[0];
+        } else if constexpr (PERSIST) {
             if (t == 0) {
 #pragma unroll
                 for (int d = 0; d < ND; ++d) P.red.partials[d * P.red.nchunks + chunk] = v[d];
@@ -1323,7 +1436,7 @@ __global__ void __launch_bounds__(kVecThreads) vec_kernel(VecParams P) {
         }
     }
     }  // chunk loop
-    if constexpr (ND > 0 && PERSIST) {
+    if constexpr (ND > 0 && PERSIST && VecPublishOnly<OP>::row < 0) {
         RedParams R = P.red;
         if (P.p2p) { R.p2p = P.p2p; R.s_loc = &s_loc; }
         ticket_and_finish<kVecThreads, ND, 0>(R, sred, &s_flag);

@@ -268,6 +268,22 @@ class DeviceCsr:
         keys = ["nrows", "ncols", "nnz", "device_bytes", "max_block_nnz", "max_row", "variant", "ws_variant"]
         return {k: int(out[i]) for i, k in enumerate(keys)}
 
+    def set_values(self, vals, mem=MEM_HOST):
+        """SparseCoo::with_values (sparse.hpp:58-61): same pattern, new values."""
+        if mem == MEM_HOST:
+            v = _f64(vals)
+            if len(v) != self.nnz:
+                raise DimensionError(f"{len(v)} values for {self.nnz} entries")
+            _check(lib().sparsla_dcsr_set_values(self.h, _p(v, _f64p), C.c_int32(MEM_HOST)))
+        else:
+            _check(lib().sparsla_dcsr_set_values(self.h, C.cast(C.c_void_p(vals), _f64p), C.c_int32(MEM_DEVICE)))
+
+    def long_rows(self):
+        """Rows summed warp-per-row (power-law hubs): {rows, entries, threshold}."""
+        out = np.zeros(3, np.int64)
+        _check(lib().sparsla_dcsr_long_rows(self.h, _p(out, _i64p)))
+        return {"rows": int(out[0]), "entries": int(out[1]), "threshold": int(out[2])}
+
     def format(self):
         """SpMV storage format: value dictionary on / distinct values / constant Jacobi diagonal."""
         out = np.zeros(3, np.int64)

@@ -4,6 +4,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <thread>
 
 #include "sparsla/adjoint.hpp"
 #include "sparsla/distributed.hpp"
@@ -62,6 +63,13 @@ int main(int argc, char** argv) {
     SparseCoo chain({0, 0, 1, 1, 1, 2, 2, 2}, {0, 1, 0, 1, 2, 1, 2, 3}, {2, -1, -1, 2, -1, -1, 2, -1}, Shape{3, 6});
     LocalPartition L(6, &part, 2, 0, owned, CsrMatrix::from_coo(chain));
     CHECK(L.halo().size() == 1 && L.halo()[0] == 3 && L.send_idx()[0] == 2 && L.recv_idx()[0] == 3);
+    // SPEC build_local(A: SparseCoo, part_of, rank) on the Figure-1 chain
+    SparseCoo chain6({0, 0, 1, 1, 1, 2, 2, 2, 3, 3, 3, 4, 4, 4, 5, 5},
+                     {0, 1, 0, 1, 2, 1, 2, 3, 2, 3, 4, 3, 4, 5, 4, 5},
+                     {2, -1, -1, 2, -1, -1, 2, -1, -1, 2, -1, -1, 2, -1, -1, 2}, Shape{6, 6});
+    LocalPartition L0 = build_local(chain6, part, 0), L1 = build_local(chain6, part, 1);
+    CHECK(L0.owned().size() == 3 && L0.halo().size() == 1 && L0.halo()[0] == 3 && L0.neighbors()[0] == 1);
+    CHECK(L1.halo().size() == 1 && L1.halo()[0] == 2 && L1.send_idx()[0] == 0);
     if (!gpu) { std::printf("dropin cpu ok\n"); return 0; }
     // --- GPU path ---
     std::vector<double> ones(256, 1.0);
@@ -91,6 +99,52 @@ int main(int argc, char** argv) {
     CHECK(std::fabs(ge[0] - 0.5) < 1e-14 && std::fabs(ge[1] + 0.5) < 1e-14);
     auto ep = eig_smallest(P, 6, 1e-9);  // 2-D Poisson 16x16 through LOBPCG
     CHECK(ep.report.converged && std::fabs(ep.lambdas[0] - 2.0 * (2.0 - 2.0 * std::cos(M_PI / 17))) < 1e-8);
+    // --- SPEC-shaped distributed API: 2 in-process ranks on cuda:0 ---
+    {
+        const auto pc = partition_contiguous(256, 2);
+        const auto [xs, rs] = cg_solve(A, ones, SolveOptions{});
+        const auto ys = spmv(A, xs);
+        LocalHub hub(2);
+        int fails[2] = {0, 0};
+        auto worker = [&](int rank) {
+            try {
+                Transport T = Transport::in_process(hub, rank, 0);
+                LocalPartition L = build_local(P, pc, rank);
+                const auto& own = L.owned();
+                std::vector<double> xo(own.size());
+                for (std::size_t i = 0; i < own.size(); ++i) xo[i] = xs[own[i]];
+                auto halo = halo_exchange(L, T, xo);
+                for (std::size_t i = 0; i < halo.size(); ++i) fails[rank] += halo[i] != xs[L.halo()[i]];
+                auto yo = dist_spmv(L, T, xo);
+                for (std::size_t i = 0; i < own.size(); ++i) fails[rank] += yo[i] != ys[own[i]];
+                fails[rank] += all_reduce_sum(T, rank + 1.0) != 3.0;
+                std::vector<double> bo(own.size(), 1.0);
+                auto [xd, rd] = dist_cg(L, T, bo, 1e-10, 10000);
+                fails[rank] += !rd.converged || rd.iterations != rs.iterations;
+                double e = 0;
+                for (std::size_t i = 0; i < own.size(); ++i) e = std::fmax(e, std::fabs(xd[i] - xs[own[i]]));
+                fails[rank] += e > 1e-10;
+                auto g = dist_adjoint_solve(L, T, xd, bo);
+                fails[rank] += !g.report.converged || g.grad_b_owned.size() != own.size();
+                for (std::size_t i = 0; i < own.size(); ++i) fails[rank] += std::fabs(g.grad_b_owned[i] - xd[i]) > 1e-12;
+                auto xg = gather_solution(L, T, xd);
+                if (rank == 0) {
+                    fails[rank] += xg.size() != 256;
+                    for (std::size_t i = 0; i < xg.size(); ++i) fails[rank] += std::fabs(xg[i] - xs[i]) > 1e-10;
+                } else {
+                    fails[rank] += !xg.empty();
+                }
+                fails[rank] += T.all_reduces() <= 0;
+            } catch (const std::exception& ex) {
+                std::printf("rank %d: %s\n", rank, ex.what());
+                fails[rank] += 1000;
+            }
+        };
+        std::thread t0(worker, 0), t1(worker, 1);
+        t0.join();
+        t1.join();
+        CHECK(fails[0] == 0 && fails[1] == 0);
+    }
     std::printf("dropin gpu ok\n");
     return 0;
 }

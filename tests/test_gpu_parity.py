@@ -80,9 +80,11 @@ def test_spmv_random_rectangular_and_ragged(S, O, gpu, seed):
     assert_bitwise(S.spmv_transpose(D, y), O.spmv(O.transpose(A), y))
 
 
-def test_spmv_long_rows_hub_bypass(S, O, gpu):
+def test_spmv_long_rows_hub_bypass(S, O, gpu, monkeypatch):
     """Rounds larger than a ring stage (hub rows) bypass the smem ring inside the staged
-    kernel; everything stays bit-exact, incl. the fused dot and CG."""
+    kernel; everything stays bit-exact, incl. the fused dot and CG.  (Long-row split off, so
+    the staged kernel itself meets the hubs.)"""
+    monkeypatch.setenv("SPARSLA_LONG_ROW", "0")
     A = random_csr(O, 5000, 5000, 5, 3, long_rows={3: 4000, 500: 4500, 4999: 3000})
     D = to_S(S, A).device(0)
     assert D.info()["variant"] == 0
@@ -449,3 +451,59 @@ def test_config_D_c1_breakdown_matches_oracle(S, O, gpu):
     x, r = S.bicgstab_solve(to_S(S, A), b, S.SolveOptions(atol=0.0, rtol=1e-8, max_iter=3000))
     rep_eq(r, ro)
     assert_bitwise(x, xo, "convdiff c=1 N=128")
+
+
+def power_law_csr(O, n, seed, hubs, symmetric=True):
+    """Irregular matrix: Pareto row degrees plus a few hub rows of `hubs` entries each;
+    symmetric + diagonally dominant (SPD) unless symmetric=False."""
+    rng = np.random.default_rng(seed)
+    deg = np.minimum((rng.pareto(1.6, n) * 2).astype(np.int64) + 1, n // 4)
+    deg[rng.choice(n, len(hubs), replace=False)] = hubs
+    r = np.repeat(np.arange(n), deg)
+    c = rng.integers(0, n, len(r))
+    v = -rng.random(len(r))
+    if symmetric:
+        r, c, v = np.concatenate([r, c]), np.concatenate([c, r]), np.concatenate([v, v])
+    off = np.zeros(n)
+    np.add.at(off, r, np.abs(v))
+    r = np.concatenate([r, np.arange(n)])
+    c = np.concatenate([c, np.arange(n)])
+    v = np.concatenate([v, off + 1.0])
+    return O.csr_from_triplets(n, n, r, c, v)
+
+
+@pytest.mark.parametrize("threshold", [None, "32", "0"])
+def test_long_rows_warp_per_row_bitwise(S, O, gpu, monkeypatch, threshold):
+    """Power-law hubs (2e4-6e4 entries) summed warp-per-row with the reference's left-to-right
+    order: SpMV, CG (fused p.q over the short-row view) and set_values all bitwise."""
+    if threshold is not None:
+        monkeypatch.setenv("SPARSLA_LONG_ROW", threshold)
+    A = power_law_csr(O, 120_000, 7, [60_000, 41_000, 20_000, 20_000, 3000])
+    D = to_S(S, A).device(0)
+    lr = D.long_rows()
+    if threshold == "0":
+        assert lr["rows"] == 0
+    else:
+        assert lr["rows"] >= 5 and lr["entries"] >= 140_000, lr
+    x = np.random.default_rng(11).standard_normal(A.ncols)
+    assert_bitwise(S.spmv(D, x), O.spmv(A, x), "spmv")
+    b = np.ones(A.nrows)
+    xo, ro = O.cg(A, b, atol=0.0, rtol=1e-10, max_iter=3000)
+    xg, rg = S.cg_solve(D, b, S.SolveOptions(atol=0.0, rtol=1e-10, max_iter=3000))
+    rep_eq(rg, ro)
+    assert_bitwise(xg, xo, "cg")
+    v2 = A.vals * 1.5
+    D.set_values(v2)
+    A2 = O.Csr(A.nrows, A.ncols, A.row_ptr, A.col_idx, v2)
+    assert_bitwise(S.spmv(D, x), O.spmv(A2, x), "spmv after set_values")
+
+
+def test_long_rows_bicgstab_bitwise(S, O, gpu):
+    A = power_law_csr(O, 60_000, 5, [30_000, 8000], symmetric=False)
+    D = to_S(S, A).device(0)
+    assert D.long_rows()["rows"] >= 2
+    b = np.ones(A.nrows)
+    xo, ro = O.bicgstab(A, b, atol=0.0, rtol=1e-10, max_iter=2000)
+    xg, rg = S.bicgstab_solve(D, b, S.SolveOptions(atol=0.0, rtol=1e-10, max_iter=2000))
+    rep_eq(rg, ro)
+    assert_bitwise(xg, xo, "bicgstab")
