@@ -105,8 +105,11 @@ def golden_record(cfg, world):
     with open(GOLDEN) as f:
         g = json.load(f)
     rec = g.get(key)
+    # fparam is only a generator parameter of convection-diffusion (the Poisson generators
+    # ignore it; the golden records store the generator default 1.0 for them)
+    same_f = rec is not None and (cfg["kind"] != "convdiff3d" or rec["fparam"] == cfg["fparam"])
     if rec and rec["kind"] == cfg["kind"] and rec["p1"] == cfg["p1"] and rec["p2"] == cfg["p2"] \
-            and rec["fparam"] == cfg["fparam"] and rec["solver"] == cfg["solver"]:
+            and same_f and rec["solver"] == cfg["solver"]:
         return key, rec
     return None, None
 

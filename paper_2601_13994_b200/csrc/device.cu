@@ -22,6 +22,7 @@
 
 #include "common.hpp"
 #include "device.hpp"
+#include "spmv_xw.cuh"
 #include "kernels.cuh"
 #include "transport.hpp"
 
@@ -158,6 +159,53 @@ static int choose_ws_variant(long long max_row) {
     return 1;
 }
 
+// x-window kernels (spmv_xw.cuh), indexed by variant; `vd` selects the value stream.
+// SPARSLA_XW_VARIANT overrides the choice (sweeps).
+struct XwVariant {
+    bool vd;
+    int w, stg, minb;
+    const void* fn[4];  // per SpmvMode
+};
+#define XWV(VD, W, S, M)                                                                            \
+    {VD, W, S, M, {(const void*)spmv_xw_kernel<SPMV_PLAIN, S, M, W, VD>, (const void*)spmv_xw_kernel<SPMV_CG, S, M, W, VD>, \
+                   (const void*)spmv_xw_kernel<SPMV_BICG_V, S, M, W, VD>, (const void*)spmv_xw_kernel<SPMV_BICG_T, S, M, W, VD>}}
+static const XwVariant kXwVariants[] = {XWV(true, 8, 3, 3), XWV(true, 8, 2, 4), XWV(true, 8, 4, 2),
+                                        XWV(false, 8, 3, 2), XWV(false, 12, 3, 2), XWV(false, 12, 2, 3)};
+#undef XWV
+constexpr int kNumXwVariants = sizeof(kXwVariants) / sizeof(kXwVariants[0]);
+
+static size_t xw_smem_bytes(const DevCsr* A, int var, bool aux) {
+    const XwVariant& V = kXwVariants[var];
+    return 256 + (size_t)V.stg * XwLayout(A->cap_v, A->cap_c, A->cap_x, V.vd, aux).stage;
+}
+
+// Variant for the current value stream (dictionary or plain) and row lengths; -1 = none.
+static void choose_xw_variants(DevCsr* A) {
+    A->xw_var[0] = A->xw_var[1] = -1;
+    if (!A->xw) return;
+    A->xw_var[1] = 0;
+    A->xw_var[0] = A->max_row <= 8 ? 3 : 4;
+    if (const char* e = getenv("SPARSLA_XW_VARIANT")) {
+        const int x = atoi(e);
+        if (x >= 0 && x < kNumXwVariants) A->xw_var[kXwVariants[x].vd ? 1 : 0] = x;
+    }
+    int dev = A->device, sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    for (int d = 0; d < 2; ++d)
+        for (int aux = 0; aux < 2; ++aux) {
+            const int v = A->xw_var[d];
+            int per_sm = 0;
+            const size_t sm = xw_smem_bytes(A, v, aux);
+            if (sm <= 200 * 1024)
+                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kXwVariants[v].fn[aux ? SPMV_BICG_T : SPMV_CG],
+                                                                 kWsThreads, sm));
+            A->xw_ctas[d][aux] = sms * per_sm;
+        }
+    // the x-window path needs every mode to fit at least one CTA per SM
+    for (int d = 0; d < 2; ++d)
+        if (A->xw_ctas[d][0] == 0 || A->xw_ctas[d][1] == 0) A->xw_var[d] = -1;
+}
+
 size_t ws_smem_bytes(const DevCsr* A, int variant, bool vd = false) {
     if (vd) return 256 + (size_t)kVdVariants[A->vd_var].stg * StageLayout(A->cap_v, A->cap_c, true).stage;
     const WsVariant& V = kWsVariants[variant];
@@ -174,6 +222,9 @@ static void configure_ws_variants(int device) {
     for (int v = 0; v < kNumVdVariants; ++v)
         for (int m = 0; m < 4; ++m)
             CK(cudaFuncSetAttribute(kVdVariants[v].fn[m], cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    for (int v = 0; v < kNumXwVariants; ++v)
+        for (int m = 0; m < 4; ++m)
+            CK(cudaFuncSetAttribute(kXwVariants[v].fn[m], cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     (void)device;
 }
 
@@ -191,6 +242,7 @@ DevCsr::~DevCsr() {
     cudaFree(rp); cudaFree(ci); cudaFree(val); cudaFree(dinv); cudaFree(ones);
     cudaFree(vidx); cudaFree(vtab);
     cudaFree(long_rows); cudaFree(long_bits); cudaFree(s_rp); cudaFree(s_ci); cudaFree(s_val);
+    cudaFree(xw);
     if (stream) cudaStreamDestroy(stream);
     delete transpose;
 }
@@ -274,6 +326,121 @@ static void build_value_dictionary(DevCsr* A, const double* h_val) {
     CK(memcpy_sync(A->vtab, vt.data(), 256 * 8, cudaMemcpyHostToDevice));
     A->vd = true;
     A->nvals = (int)tab.size();
+}
+
+// x windows (spmv_xw.cuh): for every 256-row round, up to kXwMax contiguous segments of x
+// covering the round's columns.  Columns closer than kXwGap elements join one window; more
+// than kXwMax windows are merged across their smallest gaps; a round whose windows exceed
+// kXwCapMax elements keeps its most-referenced windows (the other entries read x from
+// global memory).  Windows are 16-byte granules inside x.  SPARSLA_XWIN: 0 = off, 1 = on
+// when it pays (>= 90% of the entries staged, staged elements <= entries), 2 = forced.
+static constexpr long long kXwGap = 32;
+static constexpr long long kXwCapMax = 2048;
+static int xwin_mode() {
+    const char* e = getenv("SPARSLA_XWIN");
+    return e ? atoi(e) : 1;
+}
+
+static void drop_xwin(DevCsr* A) {
+    cudaFree(A->xw);
+    A->xw = nullptr;
+    A->cap_x = 0;
+    A->xw_var[0] = A->xw_var[1] = -1;
+    A->xw_cover = 0.0;
+}
+
+template <class I>
+static void build_xwin(DevCsr* A, const I* h_rp, const I* h_ci) {
+    drop_xwin(A);
+    const int mode = xwin_mode();
+    if (mode == 0 || A->nrows == 0 || A->nnz == 0 || A->has_hub || A->nlong > 0 || !A->staged) return;
+    const long long nr = (A->nrows + kChunkSlots - 1) / kChunkSlots;
+    const long long ncx = A->ncols & ~1LL;
+    std::vector<int32_t> desc((size_t)nr * 2 * kXwMax, 0);
+    std::atomic<long long> covered{0}, staged{0};
+    std::atomic<int> capx{0};
+    parallel_for(nr, [&](int64_t a, int64_t b) {
+        std::vector<std::pair<long long, long long>> iv;
+        std::vector<long long> cnt;
+        long long cov = 0, stg = 0;
+        int cx = 0;
+        for (int64_t q = a; q < b; ++q) {
+            const long long rs = q * kChunkSlots, re = std::min<long long>(rs + kChunkSlots, A->nrows);
+            const long long k0 = (long long)h_rp[rs], k1 = (long long)h_rp[re];
+            iv.clear();
+            bool bad = false;
+            for (long long k = k0; k < k1 && !bad; ++k) {
+                const long long c = (long long)h_ci[k];
+                size_t j = 0;
+                while (j < iv.size() && iv[j].second + kXwGap < c) ++j;
+                if (j < iv.size() && iv[j].first - kXwGap <= c) {
+                    iv[j].first = std::min(iv[j].first, c);
+                    iv[j].second = std::max(iv[j].second, c + 1);
+                    if (j > 0 && iv[j - 1].second + kXwGap >= iv[j].first) {
+                        iv[j - 1].second = std::max(iv[j - 1].second, iv[j].second);
+                        iv.erase(iv.begin() + (long)j);
+                        --j;
+                    }
+                    while (j + 1 < iv.size() && iv[j + 1].first - kXwGap <= iv[j].second) {
+                        iv[j].second = std::max(iv[j].second, iv[j + 1].second);
+                        iv.erase(iv.begin() + (long)j + 1);
+                    }
+                } else {
+                    iv.insert(iv.begin() + (long)j, {c, c + 1});
+                    bad = iv.size() > 64;
+                }
+            }
+            if (bad) continue;  // scattered columns: this round gathers from global memory
+            while (iv.size() > (size_t)kXwMax) {  // merge across the smallest gap
+                size_t jm = 0;
+                for (size_t j = 1; j + 1 < iv.size(); ++j)
+                    if (iv[j + 1].first - iv[j].second < iv[jm + 1].first - iv[jm].second) jm = j;
+                iv[jm].second = iv[jm + 1].second;
+                iv.erase(iv.begin() + (long)jm + 1);
+            }
+            for (auto& w : iv) {  // 16-byte granules inside x
+                w.first &= ~1LL;
+                w.second = std::min((w.second + 1) & ~1LL, ncx);
+            }
+            iv.erase(std::remove_if(iv.begin(), iv.end(), [](auto& w) { return w.second <= w.first; }), iv.end());
+            cnt.assign(iv.size(), 0);
+            for (long long k = k0; k < k1; ++k) {
+                const long long c = (long long)h_ci[k];
+                for (size_t j = 0; j < iv.size(); ++j)
+                    if (c >= iv[j].first && c < iv[j].second) { ++cnt[j]; break; }
+            }
+            long long tot = 0;
+            for (auto& w : iv) tot += w.second - w.first;
+            while (tot > kXwCapMax && !iv.empty()) {  // keep the most-referenced windows
+                size_t jm = 0;
+                for (size_t j = 1; j < iv.size(); ++j)
+                    if (cnt[j] * (iv[jm].second - iv[jm].first) < cnt[jm] * (iv[j].second - iv[j].first)) jm = j;
+                tot -= iv[jm].second - iv[jm].first;
+                iv.erase(iv.begin() + (long)jm);
+                cnt.erase(cnt.begin() + (long)jm);
+            }
+            int32_t* d = desc.data() + (size_t)q * 2 * kXwMax;
+            for (size_t j = 0; j < iv.size(); ++j) {
+                d[j] = (int32_t)iv[j].first;
+                d[kXwMax + j] = (int32_t)(iv[j].second - iv[j].first);
+                cov += cnt[j];
+            }
+            stg += tot;
+            cx = std::max(cx, (int)tot);
+        }
+        covered += cov;
+        staged += stg;
+        int prev = capx.load();
+        while (cx > prev && !capx.compare_exchange_weak(prev, cx)) {}
+    });
+    const double cover = (double)covered.load() / (double)A->nnz;
+    if (mode == 1 && (cover < 0.9 || staged.load() > A->nnz)) return;
+    A->cap_x = std::max(16, (capx.load() + 15) & ~15);
+    A->xw_cover = cover;
+    A->xw = dalloc<int32_t>(desc.size());
+    CK(memcpy_sync(A->xw, desc.data(), desc.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    choose_xw_variants(A);
+    if (A->xw_var[0] < 0 && A->xw_var[1] < 0) drop_xwin(A);
 }
 
 template <class I>
@@ -426,6 +593,7 @@ DevCsr* DevCsr::create(int device, long long nrows, long long ncols, const I* h_
     A->smem_bytes = ws_smem_bytes(A.get(), A->ws_var, A->vd);
     A->staged = A->cap_v >= 512 && A->smem_bytes <= 200 * 1024;  // else: direct kernel
     if (const char* e = getenv("SPARSLA_SPMV_DIRECT")) if (atoi(e)) A->staged = false;
+    build_xwin<I>(A.get(), h_rp, h_ci);
     {
         int sms = 0;
         CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
@@ -546,8 +714,20 @@ static int vd_var_of(const DevCsr* A, int mode) {
     return (mode == SPMV_BICG_T && A->vd_var == 3 && !t7) ? 0 : A->vd_var;
 }
 
-unsigned spmv_grid(const DevCsr* A, long long nch, int mode) {
+// x-window kernel variant for the matrix's current value stream, or -1
+static int xw_pick(const DevCsr* A) {
+    if (!A->staged || !A->xw) return -1;
+    return A->xw_var[(A->vd && A->ws_var == 0) ? 1 : 0];
+}
+static bool xw_aligned(const double* x, const double* aux) {  // TMA sources: 16-byte aligned
+    return ((uintptr_t)x & 15) == 0 && ((uintptr_t)aux & 15) == 0;
+}
+static bool mode_has_aux(int mode) { return mode == SPMV_BICG_V || mode == SPMV_BICG_T; }
+
+unsigned spmv_grid(const DevCsr* A, long long nch, int mode, bool xw_ok) {
     if (nch <= 0) return 0;
+    if (xw_ok && xw_pick(A) >= 0)
+        return (unsigned)std::min<long long>(nch, (long long)A->xw_ctas[(A->vd && A->ws_var == 0) ? 1 : 0][mode_has_aux(mode)]);
     if (A->staged) {
         const bool vdt = A->vd && A->ws_var == 0 && vd_var_of(A, mode) != A->vd_var;
         return (unsigned)std::min<long long>(nch, (long long)(vdt ? A->vdt_ctas : A->ws_ctas[A->ws_var]));
@@ -560,7 +740,8 @@ unsigned spmv_grid(const DevCsr* A, long long nch, int mode) {
 void launch_spmv_part(DevCsr* A, cudaStream_t s, int mode, const double* x, double* y, const double* aux,
                       const RedParams& red, int check_done, const int32_t* list, long long nch,
                       unsigned expected, const P2PCtx* p2p, long long n_interior, int halo_v) {
-    const unsigned grid = spmv_grid(A, nch, mode);
+    const bool xw_ok = xw_aligned(x, aux);
+    const unsigned grid = spmv_grid(A, nch, mode, xw_ok);
     if (grid == 0) return;
     SpmvParams P{};
     P.rp = A->rp; P.ci = A->ci; P.val = A->val;
@@ -588,7 +769,14 @@ void launch_spmv_part(DevCsr* A, cudaStream_t s, int mode, const double* x, doub
     P.red = red;
     P.red.nchunks = nchunks_of(A->nrows);
     P.red.expected = expected;
-    if (A->staged) {
+    const int xv = xw_ok ? xw_pick(A) : -1;
+    if (xv >= 0) {
+        P.xw = A->xw;
+        P.cap_x = A->cap_x;
+        void* args[] = {&P};
+        CK(cudaLaunchKernel(kXwVariants[xv].fn[mode], dim3(grid), dim3(kWsThreads), args,
+                            xw_smem_bytes(A, xv, mode_has_aux(mode)), s));
+    } else if (A->staged) {
         const int v = A->ws_var;
         const bool wp = kWsVariants[v].rpt == 0;
         if (wp) { P.cap_v = A->cap_v32; P.cap_c = A->cap_c32; }
@@ -614,7 +802,7 @@ void launch_spmv(DevCsr* A, cudaStream_t s, int mode, const double* x, double* y
                  const RedParams& red, int check_done) {
     if (A->nrows == 0) return;
     const long long nch = nchunks_of(A->nrows);
-    launch_spmv_part(A, s, mode, x, y, aux, red, check_done, nullptr, nch, spmv_grid(A, nch, mode));
+    launch_spmv_part(A, s, mode, x, y, aux, red, check_done, nullptr, nch, spmv_grid(A, nch, mode, xw_aligned(x, aux)));
 }
 
 static int u1_group() {
@@ -705,7 +893,9 @@ Solver::Solver(DevCsr* A_, int backend_, const sparsla_solve_options& o, DistCtx
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cg_fused_kernel<false>, kSpmvThreads, 0));
         const long long cap = (long long)sms * per_sm;
         fused_grid = (int)std::min<long long>(m, cap);
-        fused = coop && cap > 0 && m <= cap;  // one chunk per CTA (measured: 2 per CTA ~ break-even)
+        // one chunk per CTA (measured: 2 per CTA ~ break-even); thread-per-row, so never for
+        // matrices with long (hub) rows — those take the warp-per-row split of the SpMV
+        fused = coop && cap > 0 && m <= cap && A->nlong == 0 && A->max_row <= kLongMin;
         if (const char* e = getenv("SPARSLA_FUSED")) fused = coop && cap > 0 && atoi(e) != 0;
         if (fused) { fused_bar = dalloc<unsigned>(1); }
         // resident chunk images when every chunk fits uint16 offsets / int16 column deltas and
@@ -734,8 +924,10 @@ Solver::Solver(DevCsr* A_, int backend_, const sparsla_solve_options& o, DistCtx
                     if (A->device < 64 && !raised[A->device]) {
                         int optin = 0;
                         CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, A->device));
+                        cudaFuncAttributes fa{};
+                        CK(cudaFuncGetAttributes(&fa, cg_fused_kernel<true>));  // minus its static smem
                         CK(cudaFuncSetAttribute(cg_fused_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                optin));
+                                                optin - (int)fa.sharedSizeBytes));
                         raised[A->device] = true;
                     }
                 }
@@ -1313,6 +1505,16 @@ int sparsla_dcsr_info(const sparsla_dcsr* H, int64_t* info) {
         info[3] = (A->nrows + 1) * 4 + A->nnz * 12;
         info[4] = A->max_block_nnz; info[5] = A->max_row; info[6] = A->staged ? 0 : 1;
         info[7] = A->ws_var;
+    });
+}
+
+int sparsla_dcsr_xwin(const sparsla_dcsr* H, int64_t* out) {
+    return guarded([&] {
+        need(H, "matrix"); need(out, "out");
+        const DevCsr* A = H->A;
+        out[0] = xw_pick(A);
+        out[1] = A->cap_x;
+        out[2] = (int64_t)(A->xw_cover * 1e6 + 0.5);
     });
 }
 

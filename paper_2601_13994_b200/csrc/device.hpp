@@ -57,6 +57,13 @@ struct DevCsr {
     int32_t* s_rp = nullptr;         // short-row view (same padding as rp/ci/val)
     int32_t* s_ci = nullptr;
     double* s_val = nullptr;
+    // x windows (spmv_xw.cuh): per-round descriptors of the x segments the staged SpMV
+    // streams into shared memory next to the matrix (banded / mesh-ordered matrices)
+    int32_t* xw = nullptr;     // [rounds][16]: start[8], len[8]
+    int cap_x = 0;             // max staged x elements per round
+    int xw_var[2] = {-1, -1};  // x-window kernel variant, [plain, dictionary]; -1: not used
+    int xw_ctas[2][2] = {{0, 0}, {0, 0}};  // persistent grid [dictionary][aux vector staged]
+    double xw_cover = 0.0;     // fraction of entries whose x operand is staged
     DevCsr* transpose = nullptr;
     cudaStream_t stream = nullptr;
     std::mutex lazy_mu;  // guards the lazily built caches (dinv, ones, symmetry, transpose)
@@ -87,7 +94,7 @@ void csr_transpose_device(int device, long long nrows, long long ncols, long lon
 
 void launch_spmv(DevCsr* A, cudaStream_t s, int mode, const double* x, double* y, const double* aux,
                  const RedParams& red, int check_done);
-unsigned spmv_grid(const DevCsr* A, long long nch, int mode = 0);
+unsigned spmv_grid(const DevCsr* A, long long nch, int mode = 0, bool xw_ok = true);
 void launch_spmv_part(DevCsr* A, cudaStream_t s, int mode, const double* x, double* y, const double* aux,
                       const RedParams& red, int check_done, const int32_t* list, long long nch,
                       unsigned expected, const P2PCtx* p2p = nullptr, long long n_interior = 0,

@@ -522,6 +522,8 @@ struct SpmvParams {
     int l2_keep;        // 1: matrix stream evict_last (working set fits L2), 0: evict_first
     int check_done;
     const uint32_t* long_bits;  // rows summed by spmv_longrow_kernel (empty in this view): bit set
+    const int32_t* xw;  // x-window kernels (spmv_xw.cuh): per-round window descriptors
+    int cap_x;          //   staged x elements per round
     RedParams red;
 };
 

@@ -284,6 +284,13 @@ class DeviceCsr:
         _check(lib().sparsla_dcsr_long_rows(self.h, _p(out, _i64p)))
         return {"rows": int(out[0]), "entries": int(out[1]), "threshold": int(out[2])}
 
+    def xwin(self):
+        """x-window staging: {variant (-1 = off), cap_x (elements per round), cover (fraction
+        of entries whose x operand is staged)}."""
+        out = np.zeros(3, np.int64)
+        _check(lib().sparsla_dcsr_xwin(self.h, _p(out, _i64p)))
+        return {"variant": int(out[0]), "cap_x": int(out[1]), "cover": out[2] / 1e6}
+
     def format(self):
         """SpMV storage format: value dictionary on / distinct values / constant Jacobi diagonal."""
         out = np.zeros(3, np.int64)

@@ -1,0 +1,123 @@
+"""x-window staged SpMV (csrc/spmv_xw.cuh): the x operand of each 256-row round is streamed
+into shared memory by TMA as a few contiguous windows; columns outside every window are read
+from global memory.  The arithmetic is the reference's row-ordered sum (sparse.cpp:144-152),
+so every result must stay bit-identical to the oracle, for every kernel variant, value
+stream (dictionary / plain), mode (plain / CG p.q / BiCGStab r-hat.v, t.t + t.s) and window
+coverage (full, partial, forced on scattered columns)."""
+import numpy as np
+import pytest
+
+from test_gpu_parity import _banded, assert_bitwise, random_csr, rep_eq, to_S
+
+pytestmark = pytest.mark.gpu
+
+N_XW_VARIANTS = 6  # kXwVariants in csrc/device.cu (0-2 dictionary, 3-5 plain)
+
+
+def _gen(O, case):
+    if case == "poisson3d":
+        return O.generate("poisson3d", 40)
+    if case == "poisson2d":
+        return O.generate("poisson2d", 300)
+    if case == "convdiff3d":
+        return O.generate("convdiff3d", 30, 0, 0.3)
+    if case == "fem2d":
+        return O.generate("fem2d", 200, 2601, 0.0)
+    if case == "banded_far":   # windows far apart, > 8 of them merged across the smallest gaps
+        return _banded(O, 70000, (1, 5, 300, 2000, 9000, 20000), 20.0, -1.0)
+    raise ValueError(case)
+
+
+CASES = ["poisson3d", "poisson2d", "convdiff3d", "fem2d", "banded_far"]
+
+
+def test_xwin_selection(S, O, gpu, monkeypatch):
+    """On by default for stencil / mesh matrices (>= 90% of entries staged), off for
+    scattered columns unless forced; SPARSLA_XWIN=0 disables."""
+    P = to_S(S, O.generate("poisson3d", 40)).device(0)
+    xw = P.xwin()
+    assert xw["variant"] >= 0 and xw["cover"] >= 0.9 and 0 < xw["cap_x"] <= 2048, xw
+    R = random_csr(O, 20000, 20000, 9, 1)
+    assert to_S(S, R).device(0).xwin()["variant"] == -1
+    monkeypatch.setenv("SPARSLA_XWIN", "2")
+    assert to_S(S, R).device(0).xwin()["variant"] >= 0
+    monkeypatch.setenv("SPARSLA_XWIN", "0")
+    assert to_S(S, O.generate("poisson3d", 40)).device(0).xwin()["variant"] == -1
+
+
+@pytest.mark.parametrize("variant", range(N_XW_VARIANTS))
+@pytest.mark.parametrize("case", CASES)
+def test_xwin_spmv_bitwise(S, O, gpu, monkeypatch, case, variant):
+    if variant < 3 and case in ("fem2d", "banded_far"):
+        pytest.skip("no value dictionary (distinct values / rows > 8): dictionary variants unused")
+    A = _gen(O, case)
+    monkeypatch.setenv("SPARSLA_XWIN", "2")
+    monkeypatch.setenv("SPARSLA_XW_VARIANT", str(variant))
+    if variant >= 3:
+        monkeypatch.setenv("SPARSLA_VALUE_DICT", "0")
+    D = to_S(S, A).device(0)
+    assert D.xwin()["variant"] == variant, (D.xwin(), D.format())
+    x = np.random.default_rng(3).standard_normal(A.ncols)
+    assert_bitwise(S.spmv(D, x), O.spmv(A, x), f"{case} variant {variant}")
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_xwin_forced_on_scattered_and_rectangular(S, O, gpu, monkeypatch, seed):
+    """Forced on a random rectangular matrix with empty / ragged rows: most columns fall
+    outside the windows and take the global fallback — still bitwise."""
+    monkeypatch.setenv("SPARSLA_XWIN", "2")
+    A = random_csr(O, 5001 + seed, 4003, 14, seed)
+    D = to_S(S, A).device(0)
+    assert D.xwin()["variant"] >= 0
+    x = np.random.default_rng(seed).standard_normal(A.ncols)
+    assert_bitwise(S.spmv(D, x), O.spmv(A, x), "rectangular")
+
+
+@pytest.mark.parametrize("dictionary", [True, False])
+@pytest.mark.parametrize("case", ["poisson3d", "fem2d", "banded_far"])
+def test_xwin_cg_trajectory_bitwise(S, O, gpu, monkeypatch, case, dictionary):
+    """CG through the x-window SpMV (fused p.q operand read from the centre window)."""
+    monkeypatch.setenv("SPARSLA_FUSED", "0")  # small problems would run the fused CG kernel
+    if not dictionary:
+        monkeypatch.setenv("SPARSLA_VALUE_DICT", "0")
+    A = _gen(O, case)
+    D = to_S(S, A).device(0)
+    assert D.xwin()["variant"] >= 0
+    b = np.linspace(0.5, 1.5, A.nrows)
+    xo, ro = O.cg(A, b, atol=0.0, rtol=1e-10, max_iter=20000)
+    x, r = S.cg_solve(D, b, S.SolveOptions(atol=0.0, rtol=1e-10, max_iter=20000))
+    assert ro["converged"]
+    rep_eq(r, ro)
+    assert_bitwise(x, xo, case)
+
+
+@pytest.mark.parametrize("dictionary", [True, False])
+@pytest.mark.parametrize("case", ["convdiff3d", "fem2d"])
+def test_xwin_bicgstab_trajectory_bitwise(S, O, gpu, monkeypatch, case, dictionary):
+    """BiCGStab: r-hat and s segments staged next to the windows (aux stream)."""
+    if not dictionary:
+        monkeypatch.setenv("SPARSLA_VALUE_DICT", "0")
+    A = _gen(O, case)
+    D = to_S(S, A).device(0)
+    assert D.xwin()["variant"] >= 0
+    b = np.ones(A.nrows)
+    xo, ro = O.bicgstab(A, b, atol=0.0, rtol=1e-9, max_iter=5000)
+    x, r = S.bicgstab_solve(D, b, S.SolveOptions(atol=0.0, rtol=1e-9, max_iter=5000))
+    assert ro["converged"]
+    rep_eq(r, ro)
+    assert_bitwise(x, xo, case)
+
+
+def test_xwin_set_values_keeps_windows(S, O, gpu):
+    """Windows depend on the pattern only: set_values (dictionary dropped / rebuilt) keeps
+    the staged path and the bits."""
+    A = O.generate("poisson3d", 40)
+    D = to_S(S, A).device(0)
+    x = np.random.default_rng(9).standard_normal(A.ncols)
+    v2 = A.vals * (1.0 + 1e-3 * np.arange(A.nnz) / A.nnz)  # > 256 distinct values
+    D.set_values(v2)
+    assert not D.format()["value_dict"] and D.xwin()["variant"] >= 0
+    assert_bitwise(S.spmv(D, x), O.spmv(O.Csr(A.nrows, A.ncols, A.row_ptr, A.col_idx, v2), x))
+    D.set_values(A.vals)
+    assert D.format()["value_dict"] and D.xwin()["variant"] >= 0
+    assert_bitwise(S.spmv(D, x), O.spmv(A, x))
