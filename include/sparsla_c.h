@@ -195,10 +195,12 @@ int sparsla_dcsr_long_rows(const sparsla_dcsr* A, int64_t* out);
  * of distinct values in it (0 otherwise), fmt[2]=1 when the Jacobi inverse diagonal is
  * constant (the CG/BiCGStab vector kernels then take it as a scalar). */
 int sparsla_dcsr_format(sparsla_dcsr* A, int64_t* fmt);
-/* x-window staging of the SpMV (banded / mesh-ordered matrices): out[0]=kernel variant in
- * use for the current value stream (-1: x gathered from global memory), out[1]=staged x
- * elements per 256-row round, out[2]=parts per million of the entries whose x operand is
- * staged.  SPARSLA_XWIN=0 disables at matrix creation, 2 forces it. */
+/* x-window staging of the SpMV (banded / mesh-ordered matrices): out[0]=x-window kernel
+ * variant for the current value stream (-1: none built), out[1]=staged x elements per
+ * 256-row round, out[2]=parts per million of the entries whose x operand is staged,
+ * out[3]=bit m set when SpMV mode m (0 plain, 1 CG p.q, 2 BiCGStab r-hat.v, 3 BiCGStab
+ * t.t/t.s) runs the x-window kernel.  SPARSLA_XWIN at matrix creation: 0 disables, 1 (the
+ * default) stages when it pays, 2 forces every mode. */
 int sparsla_dcsr_xwin(const sparsla_dcsr* A, int64_t* out);
 
 /* y = A x (sparse.cpp:135-154): rows accumulated left to right from 0.0, separate

@@ -169,14 +169,14 @@ struct XwVariant {
 #define XWV(VD, W, S, M)                                                                            \
     {VD, W, S, M, {(const void*)spmv_xw_kernel<SPMV_PLAIN, S, M, W, VD>, (const void*)spmv_xw_kernel<SPMV_CG, S, M, W, VD>, \
                    (const void*)spmv_xw_kernel<SPMV_BICG_V, S, M, W, VD>, (const void*)spmv_xw_kernel<SPMV_BICG_T, S, M, W, VD>}}
-static const XwVariant kXwVariants[] = {XWV(true, 8, 3, 3), XWV(true, 8, 2, 4), XWV(true, 8, 4, 2),
+static const XwVariant kXwVariants[] = {XWV(true, 8, 3, 3), XWV(true, 8, 2, 4), XWV(true, 8, 3, 4),
                                         XWV(false, 8, 3, 2), XWV(false, 12, 3, 2), XWV(false, 12, 2, 3)};
 #undef XWV
 constexpr int kNumXwVariants = sizeof(kXwVariants) / sizeof(kXwVariants[0]);
 
 static size_t xw_smem_bytes(const DevCsr* A, int var, bool aux) {
     const XwVariant& V = kXwVariants[var];
-    return 256 + (size_t)V.stg * XwLayout(A->cap_v, A->cap_c, A->cap_x, V.vd, aux).stage;
+    return kXwHead + (size_t)V.stg * XwLayout(A->cap_v, A->cap_c, A->cap_x, V.vd, aux).stage;
 }
 
 // Variant for the current value stream (dictionary or plain) and row lengths; -1 = none.
@@ -184,7 +184,7 @@ static void choose_xw_variants(DevCsr* A) {
     A->xw_var[0] = A->xw_var[1] = -1;
     if (!A->xw) return;
     A->xw_var[1] = 0;
-    A->xw_var[0] = A->max_row <= 8 ? 3 : 4;
+    A->xw_var[0] = 5;  // plain stream: 12-wide, 2 stages, 3 CTAs/SM (fastest on FEM and stencils)
     if (const char* e = getenv("SPARSLA_XW_VARIANT")) {
         const int x = atoi(e);
         if (x >= 0 && x < kNumXwVariants) A->xw_var[kXwVariants[x].vd ? 1 : 0] = x;
@@ -242,7 +242,7 @@ DevCsr::~DevCsr() {
     cudaFree(rp); cudaFree(ci); cudaFree(val); cudaFree(dinv); cudaFree(ones);
     cudaFree(vidx); cudaFree(vtab);
     cudaFree(long_rows); cudaFree(long_bits); cudaFree(s_rp); cudaFree(s_ci); cudaFree(s_val);
-    cudaFree(xw);
+    cudaFree(xw); cudaFree(xwo);
     if (stream) cudaStreamDestroy(stream);
     delete transpose;
 }
@@ -333,7 +333,8 @@ static void build_value_dictionary(DevCsr* A, const double* h_val) {
 // than kXwMax windows are merged across their smallest gaps; a round whose windows exceed
 // kXwCapMax elements keeps its most-referenced windows (the other entries read x from
 // global memory).  Windows are 16-byte granules inside x.  SPARSLA_XWIN: 0 = off, 1 = on
-// when it pays (>= 90% of the entries staged, staged elements <= entries), 2 = forced.
+// when it pays (default: >= 90% of the entries staged, staged elements <= entries; see
+// xw_pick for the per-stream choice), 2 = forced (every mode, every stream).
 static constexpr long long kXwGap = 32;
 static constexpr long long kXwCapMax = 2048;
 static int xwin_mode() {
@@ -343,7 +344,9 @@ static int xwin_mode() {
 
 static void drop_xwin(DevCsr* A) {
     cudaFree(A->xw);
+    cudaFree(A->xwo);
     A->xw = nullptr;
+    A->xwo = nullptr;
     A->cap_x = 0;
     A->xw_var[0] = A->xw_var[1] = -1;
     A->xw_cover = 0.0;
@@ -356,17 +359,23 @@ static void build_xwin(DevCsr* A, const I* h_rp, const I* h_ci) {
     if (mode == 0 || A->nrows == 0 || A->nnz == 0 || A->has_hub || A->nlong > 0 || !A->staged) return;
     const long long nr = (A->nrows + kChunkSlots - 1) / kChunkSlots;
     const long long ncx = A->ncols & ~1LL;
-    std::vector<int32_t> desc((size_t)nr * 2 * kXwMax, 0);
+    std::vector<int32_t> desc((size_t)nchunks_of(A->nrows) * kChunkRounds * kXwDescInts, 0);
+    std::vector<uint16_t> xoff((size_t)A->nnz + kXwPad, kXwNone);
+    std::fill(xoff.end() - kXwPad, xoff.end(), (uint16_t)0);  // read as spares, never used
     std::atomic<long long> covered{0}, staged{0};
     std::atomic<int> capx{0};
     parallel_for(nr, [&](int64_t a, int64_t b) {
         std::vector<std::pair<long long, long long>> iv;
-        std::vector<long long> cnt;
+        std::vector<long long> cnt, off;
         long long cov = 0, stg = 0;
         int cx = 0;
         for (int64_t q = a; q < b; ++q) {
             const long long rs = q * kChunkSlots, re = std::min<long long>(rs + kChunkSlots, A->nrows);
             const long long k0 = (long long)h_rp[rs], k1 = (long long)h_rp[re];
+            int32_t* d = desc.data() + (size_t)q * kXwDescInts;
+            d[12] = (int32_t)k0;
+            d[13] = (int32_t)k1;
+            d[14] = -1;
             iv.clear();
             bool bad = false;
             for (long long k = k0; k < k1 && !bad; ++k) {
@@ -403,11 +412,15 @@ static void build_xwin(DevCsr* A, const I* h_rp, const I* h_ci) {
                 w.second = std::min((w.second + 1) & ~1LL, ncx);
             }
             iv.erase(std::remove_if(iv.begin(), iv.end(), [](auto& w) { return w.second <= w.first; }), iv.end());
+            auto find = [&](long long c) -> int {
+                for (size_t j = 0; j < iv.size(); ++j)
+                    if (c >= iv[j].first && c < iv[j].second) return (int)j;
+                return -1;
+            };
             cnt.assign(iv.size(), 0);
             for (long long k = k0; k < k1; ++k) {
-                const long long c = (long long)h_ci[k];
-                for (size_t j = 0; j < iv.size(); ++j)
-                    if (c >= iv[j].first && c < iv[j].second) { ++cnt[j]; break; }
+                const int j = find((long long)h_ci[k]);
+                if (j >= 0) ++cnt[(size_t)j];
             }
             long long tot = 0;
             for (auto& w : iv) tot += w.second - w.first;
@@ -419,12 +432,22 @@ static void build_xwin(DevCsr* A, const I* h_rp, const I* h_ci) {
                 iv.erase(iv.begin() + (long)jm);
                 cnt.erase(cnt.begin() + (long)jm);
             }
-            int32_t* d = desc.data() + (size_t)q * 2 * kXwMax;
+            off.assign(iv.size(), 0);
             for (size_t j = 0; j < iv.size(); ++j) {
+                off[j] = j ? off[j - 1] + (iv[j - 1].second - iv[j - 1].first) : 0;
                 d[j] = (int32_t)iv[j].first;
-                d[kXwMax + j] = (int32_t)(iv[j].second - iv[j].first);
+                d[8 + j / 2] |= (int32_t)((uint32_t)(iv[j].second - iv[j].first) << (16 * (j & 1)));
                 cov += cnt[j];
+                if (iv[j].first <= rs && re <= iv[j].second) d[14] = (int32_t)(off[j] + rs - iv[j].first);
             }
+            bool all = true;
+            for (long long k = k0; k < k1; ++k) {
+                const long long c = (long long)h_ci[k];
+                const int j = find(c);
+                if (j >= 0) xoff[(size_t)k] = (uint16_t)(off[(size_t)j] + c - iv[(size_t)j].first);
+                else all = false;
+            }
+            d[15] = all ? 1 : 0;
             stg += tot;
             cx = std::max(cx, (int)tot);
         }
@@ -435,10 +458,13 @@ static void build_xwin(DevCsr* A, const I* h_rp, const I* h_ci) {
     });
     const double cover = (double)covered.load() / (double)A->nnz;
     if (mode == 1 && (cover < 0.9 || staged.load() > A->nnz)) return;
+    A->xw_mode = mode;
     A->cap_x = std::max(16, (capx.load() + 15) & ~15);
     A->xw_cover = cover;
     A->xw = dalloc<int32_t>(desc.size());
+    A->xwo = dalloc<uint16_t>(xoff.size());
     CK(memcpy_sync(A->xw, desc.data(), desc.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    CK(memcpy_sync(A->xwo, xoff.data(), xoff.size() * sizeof(uint16_t), cudaMemcpyHostToDevice));
     choose_xw_variants(A);
     if (A->xw_var[0] < 0 && A->xw_var[1] < 0) drop_xwin(A);
 }
@@ -714,10 +740,16 @@ static int vd_var_of(const DevCsr* A, int mode) {
     return (mode == SPMV_BICG_T && A->vd_var == 3 && !t7) ? 0 : A->vd_var;
 }
 
-// x-window kernel variant for the matrix's current value stream, or -1
-static int xw_pick(const DevCsr* A) {
+// x-window kernel variant for the matrix's current value stream and this SpMV mode, or -1.
+// Measured on B200 (tools/xw_sweep.py, profiles/r02_xwin.md): with the plain fp64 value
+// stream the x-window kernel wins everywhere (FEM config C 0.407 -> 0.31 ms; plain 7-point
+// stencil 1.78 -> 1.35 ms at 464^3); with the 1-byte value dictionary the gather kernel is
+// as fast or faster except for BiCGStab's t = A s-hat (0.615 -> 0.589 ms at 368^3).
+static int xw_pick(const DevCsr* A, int mode) {
     if (!A->staged || !A->xw) return -1;
-    return A->xw_var[(A->vd && A->ws_var == 0) ? 1 : 0];
+    const bool vd = A->vd && A->ws_var == 0;
+    if (vd && mode != SPMV_BICG_T && A->xw_mode < 2) return -1;
+    return A->xw_var[vd ? 1 : 0];
 }
 static bool xw_aligned(const double* x, const double* aux) {  // TMA sources: 16-byte aligned
     return ((uintptr_t)x & 15) == 0 && ((uintptr_t)aux & 15) == 0;
@@ -726,7 +758,7 @@ static bool mode_has_aux(int mode) { return mode == SPMV_BICG_V || mode == SPMV_
 
 unsigned spmv_grid(const DevCsr* A, long long nch, int mode, bool xw_ok) {
     if (nch <= 0) return 0;
-    if (xw_ok && xw_pick(A) >= 0)
+    if (xw_ok && xw_pick(A, mode) >= 0)
         return (unsigned)std::min<long long>(nch, (long long)A->xw_ctas[(A->vd && A->ws_var == 0) ? 1 : 0][mode_has_aux(mode)]);
     if (A->staged) {
         const bool vdt = A->vd && A->ws_var == 0 && vd_var_of(A, mode) != A->vd_var;
@@ -769,9 +801,10 @@ void launch_spmv_part(DevCsr* A, cudaStream_t s, int mode, const double* x, doub
     P.red = red;
     P.red.nchunks = nchunks_of(A->nrows);
     P.red.expected = expected;
-    const int xv = xw_ok ? xw_pick(A) : -1;
+    const int xv = xw_ok ? xw_pick(A, mode) : -1;
     if (xv >= 0) {
         P.xw = A->xw;
+        P.xwo = A->xwo;
         P.cap_x = A->cap_x;
         void* args[] = {&P};
         CK(cudaLaunchKernel(kXwVariants[xv].fn[mode], dim3(grid), dim3(kWsThreads), args,
@@ -1512,9 +1545,11 @@ int sparsla_dcsr_xwin(const sparsla_dcsr* H, int64_t* out) {
     return guarded([&] {
         need(H, "matrix"); need(out, "out");
         const DevCsr* A = H->A;
-        out[0] = xw_pick(A);
+        out[0] = A->xw ? A->xw_var[(A->vd && A->ws_var == 0) ? 1 : 0] : -1;
         out[1] = A->cap_x;
         out[2] = (int64_t)(A->xw_cover * 1e6 + 0.5);
+        out[3] = 0;
+        for (int m = 0; m < 4; ++m) out[3] |= (xw_pick(A, m) >= 0 ? 1 : 0) << m;
     });
 }
 

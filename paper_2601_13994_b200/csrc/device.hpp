@@ -59,8 +59,10 @@ struct DevCsr {
     double* s_val = nullptr;
     // x windows (spmv_xw.cuh): per-round descriptors of the x segments the staged SpMV
     // streams into shared memory next to the matrix (banded / mesh-ordered matrices)
-    int32_t* xw = nullptr;     // [rounds][16]: start[8], len[8]
+    int32_t* xw = nullptr;     // [chunks * 8 rounds][kXwDescInts] window descriptors
+    uint16_t* xwo = nullptr;   // [nnz + kXwPad] entry -> offset in its round's staged windows
     int cap_x = 0;             // max staged x elements per round
+    int xw_mode = 0;           // SPARSLA_XWIN at creation (2: every mode and stream)
     int xw_var[2] = {-1, -1};  // x-window kernel variant, [plain, dictionary]; -1: not used
     int xw_ctas[2][2] = {{0, 0}, {0, 0}};  // persistent grid [dictionary][aux vector staged]
     double xw_cover = 0.0;     // fraction of entries whose x operand is staged

@@ -522,8 +522,9 @@ struct SpmvParams {
     int l2_keep;        // 1: matrix stream evict_last (working set fits L2), 0: evict_first
     int check_done;
     const uint32_t* long_bits;  // rows summed by spmv_longrow_kernel (empty in this view): bit set
-    const int32_t* xw;  // x-window kernels (spmv_xw.cuh): per-round window descriptors
-    int cap_x;          //   staged x elements per round
+    const int32_t* xw;    // x-window kernels (spmv_xw.cuh): per-round window descriptors
+    const uint16_t* xwo;  //   per-entry offsets into the round's staged windows
+    int cap_x;            //   staged x elements per round
     RedParams red;
 };
 

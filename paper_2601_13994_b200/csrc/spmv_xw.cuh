@@ -2,22 +2,33 @@
 //
 // Same arithmetic as spmv_ws_kernel (row-ordered __dmul_rn/__dadd_rn sums in stored column
 // order, the same fused dots in the same canonical chunk shape) — bit-identical — but the x
-// operand is no longer gathered by the consumer threads.  For each 256-row round a setup
-// pass (DevCsr::create, build_xwin) records up to kXwMax contiguous windows of x that cover
-// the round's columns (for a 7-point stencil: the z-1 plane, y-1 line, centre, y+1 line and
-// z+1 plane segments, ~260 elements each).  The producer warp streams those windows into the
-// stage with TMA bulk copies next to the round's row_ptr / col_idx / value stream (and, for
-// BiCGStab, the epilogue vector's segment), so the leading-plane DRAM latency is hidden by
-// the ring instead of by consumer registers, and consumers only read shared memory.  A
-// column outside every window (boundary rows, truncated windows) is read from global
-// memory, so any window set is correct; the windows only decide how fast.
+// operand is not gathered by the consumer threads.  For each 256-row round a setup pass
+// (DevCsr::create, build_xwin) records up to kXwMax contiguous windows of x covering the
+// round's columns (7-point stencil: the z-1 plane, y-1 line, centre, y+1 line and z+1 plane
+// segments, ~260 elements each), and re-expresses every entry's column as a 16-bit offset
+// into the round's staged windows (0xFFFF: outside every window).  The producer warp
+// streams, per round, the row_ptr segment, the value stream (fp64 values or 1-byte
+// dictionary indices), the 16-bit window offsets (instead of the 4-byte columns) and the x
+// windows themselves (plus, for BiCGStab, the epilogue vector's segment) into the stage with
+// TMA bulk copies, so the leading-plane DRAM latency is covered by the ring instead of by
+// consumer registers, and a consumer entry costs two shared-memory reads.  Entries outside
+// the windows read their column and x from global memory, so any window set is correct;
+// the windows only decide how fast.  The per-round descriptors are themselves prefetched a
+// whole chunk ahead into shared memory by TMA.
 #pragma once
 
 #include "kernels.cuh"
 
 namespace sparsla_b200 {
 
-constexpr int kXwMax = 8;  // windows per round; descriptor = int32 start[8], len[8] (elements)
+constexpr int kXwMax = 8;       // windows per round
+constexpr int kXwDescInts = 16; // per-round descriptor (64 B):
+//   [0..7]  window start (x element index)     [8..11] window lengths, 2 x uint16 per int
+//   [12]    row_ptr[rs]  [13] row_ptr[re]       [14] staged offset of x[rs] when rows
+//   [rs, re) lie inside one window (CG's p.q operand), else -1      [15] 1: every entry of
+//   the round is staged (the consumer skips the per-entry fallback test)
+constexpr uint16_t kXwNone = 0xFFFFu;
+constexpr int kXwPad = 32;  // offsets past the last entry (bulk-copy granule slack)
 
 __device__ __forceinline__ void fence_proxy_async_global() {
     asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -32,35 +43,26 @@ __device__ __forceinline__ void bulk_g2s_plain(void* dst, const void* src, uint3
 }
 
 struct XwLayout {
-    size_t vbytes, cbytes, rbytes, dbytes, xbytes, abytes, stage;
-    size_t coff, roff, doff, xoff, aoff;
+    size_t vbytes, obytes, rbytes, xbytes, abytes, stage;
+    size_t ooff, roff, xoff, aoff;
     __host__ __device__ XwLayout(int cap_v, int cap_c, int cap_x, bool vd, bool aux) {
         vbytes = ((size_t)cap_v * (vd ? 1 : 8) + (vd ? 32 : 0) + 127) & ~size_t(127);
-        cbytes = ((size_t)cap_c * 4 + 127) & ~size_t(127);
+        obytes = ((size_t)cap_c * 2 + 64 + 127) & ~size_t(127);  // 16-bit window offsets (+ spares)
         rbytes = (kRpCopy * 4 + 127) & ~size_t(127);
-        dbytes = 128;  // consumer view of the windows: start[8], end[8], base[8]
         xbytes = ((size_t)cap_x * 8 + 127) & ~size_t(127);
         abytes = aux ? (size_t)kChunkSlots * 8 : 0;
-        coff = vbytes;
-        roff = coff + cbytes;
-        doff = roff + rbytes;
-        xoff = doff + dbytes;
+        ooff = vbytes;
+        roff = ooff + obytes;
+        xoff = roff + rbytes;
         aoff = xoff + xbytes;
         stage = aoff + abytes;
     }
 };
+// shared memory in front of the stages: full/empty barriers, descriptor barriers, and the
+// double-buffered per-chunk descriptor block [2][kChunkRounds][kXwDescInts]
+constexpr size_t kXwHead = 1024 + 2 * kChunkRounds * kXwDescInts * 4;
 
 template <int MODE> struct XwAux { static constexpr bool on = (MODE == SPMV_BICG_V || MODE == SPMV_BICG_T); };
-
-// Window lookup for column c, walking from window w (monotone within a row; restarts when a
-// column precedes the current window, e.g. the relabelled halo columns of a local matrix).
-__device__ __forceinline__ double xw_load(const int32_t* D, const double* sx, const double* __restrict__ x,
-                                          int c, int& w) {
-    if (c < D[w]) w = 0;
-    while (w < kXwMax - 1 && c >= D[kXwMax + w]) ++w;
-    if (c >= D[w] && c < D[kXwMax + w]) return sx[c + D[2 * kXwMax + w]];
-    return __ldg(x + c);
-}
 
 template <int MODE, int STG, int MINB, int W, bool VD>
 __global__ void __launch_bounds__(kWsThreads, MINB) spmv_xw_kernel(SpmvParams P) {
@@ -76,8 +78,10 @@ __global__ void __launch_bounds__(kWsThreads, MINB) spmv_xw_kernel(SpmvParams P)
     }
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);
     uint64_t* empty = full + STG;
+    uint64_t* dbar = empty + STG;  // [2]
+    int32_t* dbuf = reinterpret_cast<int32_t*>(smem + 1024);
     const XwLayout L(P.cap_v, P.cap_c, P.cap_x, VD, AUX);
-    unsigned char* stage0 = smem + 256;
+    unsigned char* stage0 = smem + kXwHead;
     const int t = threadIdx.x;
     const int warp = t >> 5, lane = t & 31;
     if (t == 0) {
@@ -85,6 +89,8 @@ __global__ void __launch_bounds__(kWsThreads, MINB) spmv_xw_kernel(SpmvParams P)
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], kConsumerWarps);
         }
+        mbar_init(&dbar[0], 1);
+        mbar_init(&dbar[1], 1);
         fence_mbar_init();
     }
     __syncthreads();
@@ -92,9 +98,23 @@ __global__ void __launch_bounds__(kWsThreads, MINB) spmv_xw_kernel(SpmvParams P)
     if (warp == kConsumerWarps) {  // ------------------------------- producer warp ----
         if (lane == 0) {
             const uint64_t pol = P.l2_keep ? policy_evict_last() : policy_evict_first();
+            constexpr uint32_t kDescBytes = kChunkRounds * kXwDescInts * 4;
+            auto chunk_of = [&](long long c) { return P.chunk_list ? (long long)P.chunk_list[c] : P.chunk0 + c; };
+            auto fetch_desc = [&](long long c, int b) {
+                mbar_arrive_expect_tx(&dbar[b], kDescBytes);
+                bulk_g2s(dbuf + b * kChunkRounds * kXwDescInts, P.xw + chunk_of(c) * kChunkRounds * kXwDescInts,
+                         kDescBytes, &dbar[b], pol);
+            };
+            if ((long long)blockIdx.x < P.nch) fetch_desc(blockIdx.x, 0);
             bool halo_ok = P.p2p == nullptr;
             long long g = 0;
-            for (long long c = blockIdx.x; c < P.nch; c += gridDim.x) {
+            int ci = 0;
+            for (long long c = blockIdx.x; c < P.nch; c += gridDim.x, ++ci) {
+                const int b = ci & 1;
+                if (c + gridDim.x < P.nch) {  // one chunk ahead (buffer b^1 was read last chunk)
+                    fence_proxy_async_smem();
+                    fetch_desc(c + gridDim.x, b ^ 1);
+                }
                 if (!halo_ok && c >= P.n_interior) {
                     // the boundary rounds' x windows include halo values pushed by the peers:
                     // wait for them, then order the async-proxy reads after the acquire
@@ -102,52 +122,45 @@ __global__ void __launch_bounds__(kWsThreads, MINB) spmv_xw_kernel(SpmvParams P)
                     fence_proxy_async_global();
                     halo_ok = true;
                 }
-                const long long chunk = P.chunk_list ? (long long)P.chunk_list[c] : P.chunk0 + c;
-                const long long base = chunk * kChunk;
+                mbar_wait(&dbar[b], (uint32_t)((ci >> 1) & 1));
+                const long long base = chunk_of(c) * kChunk;
                 const long long rem = (P.n - base + kChunkSlots - 1) / kChunkSlots;
                 const int nr = rem < kChunkRounds ? (int)rem : kChunkRounds;
                 for (int r = 0; r < nr; ++r, ++g) {
                     const int s = (int)(g % STG);
+                    const int32_t* d = dbuf + (b * kChunkRounds + r) * kXwDescInts;
                     const long long rs = base + (long long)r * kChunkSlots;
                     const long long re = min(rs + kChunkSlots, P.n);
-                    // this round's loads go out before the wait for a free stage
-                    const int nz0 = __ldg(P.rp + rs), nz1 = __ldg(P.rp + re);
-                    const int4* dsc = reinterpret_cast<const int4*>(P.xw + (chunk * kChunkRounds + r) * (2 * kXwMax));
-                    const int4 st0 = __ldg(dsc), st1 = __ldg(dsc + 1), ln0 = __ldg(dsc + 2), ln1 = __ldg(dsc + 3);
-                    mbar_wait(&empty[s], (uint32_t)(((g / STG) & 1) ^ 1));
+                    const int nz0 = d[12], nz1 = d[13];
                     const int a0 = nz0 & ~(VALIGN - 1), a1 = (nz1 + VALIGN - 1) & ~(VALIGN - 1);
-                    const int c0 = nz0 & ~3, c1 = (nz1 + 3) & ~3;
+                    const int o0 = nz0 & ~7, o1 = (nz1 + 7) & ~7;
                     const uint32_t vb = (uint32_t)(a1 - a0) * (VD ? 1u : 8u);
-                    const uint32_t cb = (uint32_t)(c1 - c0) * 4u;
-                    unsigned char* st = stage0 + s * L.stage;
-                    const int ws[kXwMax] = {st0.x, st0.y, st0.z, st0.w, st1.x, st1.y, st1.z, st1.w};
-                    const int wl[kXwMax] = {ln0.x, ln0.y, ln0.z, ln0.w, ln1.x, ln1.y, ln1.z, ln1.w};
-                    int32_t* D = reinterpret_cast<int32_t*>(st + L.doff);
+                    const uint32_t ob = (uint32_t)(o1 - o0) * 2u;
                     uint32_t xb = 0;
 #pragma unroll
-                    for (int w = 0; w < kXwMax; ++w) {
-                        const int xo = (int)(xb >> 3);
-                        D[w] = wl[w] ? ws[w] : 0x7fffffff;
-                        D[kXwMax + w] = wl[w] ? ws[w] + wl[w] : 0x7fffffff;
-                        D[2 * kXwMax + w] = xo - ws[w];
-                        xb += (uint32_t)wl[w] * 8u;
-                    }
+                    for (int w = 0; w < kXwMax; ++w) xb += ((uint32_t)d[8 + w / 2] >> (16 * (w & 1)) & 0xffffu) * 8u;
                     const uint32_t ab = AUX ? (uint32_t)((re - rs) & ~1LL) * 8u : 0u;
-                    mbar_arrive_expect_tx(&full[s], (uint32_t)(kRpCopy * 4) + vb + cb + xb + ab);
+                    mbar_wait(&empty[s], (uint32_t)(((g / STG) & 1) ^ 1));
+                    unsigned char* st = stage0 + s * L.stage;
+                    reinterpret_cast<int32_t*>(st + L.roff)[kRpCopy] = d[14];      // staged x[rs] offset
+                    reinterpret_cast<int32_t*>(st + L.roff)[kRpCopy + 1] = d[15];  // every entry staged
+                    mbar_arrive_expect_tx(&full[s], (uint32_t)(kRpCopy * 4) + vb + ob + xb + ab);
                     bulk_g2s(st + L.roff, P.rp + rs, kRpCopy * 4, &full[s], pol);
                     if constexpr (VD) {
                         if (vb) bulk_g2s(st, P.vidx + a0, vb, &full[s], pol);
                     } else {
                         if (vb) bulk_g2s(st, P.val + a0, vb, &full[s], pol);
                     }
-                    if (cb) bulk_g2s(st + L.coff, P.ci + c0, cb, &full[s], pol);
+                    if (ob) bulk_g2s(st + L.ooff, P.xwo + o0, ob, &full[s], pol);
                     uint32_t xo = 0;
 #pragma unroll
-                    for (int w = 0; w < kXwMax; ++w)
-                        if (wl[w]) {
-                            bulk_g2s_plain(st + L.xoff + xo, P.x + ws[w], (uint32_t)wl[w] * 8u, &full[s]);
-                            xo += (uint32_t)wl[w] * 8u;
+                    for (int w = 0; w < kXwMax; ++w) {
+                        const uint32_t len = ((uint32_t)d[8 + w / 2] >> (16 * (w & 1))) & 0xffffu;
+                        if (len) {
+                            bulk_g2s_plain(st + L.xoff + xo, P.x + d[w], len * 8u, &full[s]);
+                            xo += len * 8u;
                         }
+                    }
                     if constexpr (AUX)
                         if (ab) bulk_g2s(st + L.aoff, P.aux + rs, ab, &full[s], pol);
                 }
@@ -179,7 +192,6 @@ __global__ void __launch_bounds__(kWsThreads, MINB) spmv_xw_kernel(SpmvParams P)
             mbar_wait(&full[s], ph);
             const unsigned char* A = stage0 + s * L.stage;
             const int32_t* rps = reinterpret_cast<const int32_t*>(A + L.roff);
-            const int32_t* D = reinterpret_cast<const int32_t*>(A + L.doff);
             const double* sx = reinterpret_cast<const double*>(A + L.xoff);
             const long long rs = base + (long long)r * kChunkSlots;
             const long long row = rs + t;
@@ -187,41 +199,42 @@ __global__ void __launch_bounds__(kWsThreads, MINB) spmv_xw_kernel(SpmvParams P)
             const int o0 = rps[0];
             const int kb = live ? rps[t] : o0, ke = live ? rps[t + 1] : o0;
             const int len = ke - kb;
-            const int32_t* cp = reinterpret_cast<const int32_t*>(A + L.coff) + (kb - (o0 & ~3));
+            const uint16_t* xo = reinterpret_cast<const uint16_t*>(A + L.ooff) + (kb - (o0 & ~7));
             const uint8_t* vp = A + (kb - (o0 & ~(VALIGN - 1)));
             const double* vs = reinterpret_cast<const double*>(A) + (kb - (o0 & ~(VALIGN - 1)));
             auto value = [&](int u) -> double {
                 if constexpr (VD) return s_vtab[vp[u]];
                 else return vs[u];
             };
+            auto xval = [&](int u) -> double {
+                const uint32_t o = xo[u];
+                return o != kXwNone ? sx[o] : __ldg(P.x + __ldg(P.ci + kb + u));
+            };
             double y = 0.0;
-            int w = 0;
-            if (__all_sync(0xffffffffu, len <= W)) {
-                double xv[W];
+            const bool all_staged = rps[kRpCopy + 1] != 0;  // round-uniform
+            if (all_staged && __all_sync(0xffffffffu, len <= W)) {
+                // common case: every x operand of the round is in the staged windows (the
+                // per-entry guards stay branches: reading all W slots unconditionally was
+                // measured slower — shared-memory bandwidth, profiles/r02_xwin.md)
+                double pr[W];
 #pragma unroll
                 for (int u = 0; u < W; ++u)
-                    if (u < len) xv[u] = xw_load(D, sx, P.x, cp[u], w);
+                    if (u < len) pr[u] = __dmul_rn(value(u), sx[xo[u]]);
 #pragma unroll
                 for (int u = 0; u < W; ++u)
-                    if (u < len) y = __dadd_rn(y, __dmul_rn(value(u), xv[u]));
+                    if (u < len) y = __dadd_rn(y, pr[u]);
             } else {
-                for (int k0 = 0; k0 < len; k0 += W) {
-                    double pr[W];
-#pragma unroll
-                    for (int u = 0; u < W; ++u)
-                        if (k0 + u < len) pr[u] = __dmul_rn(value(k0 + u), xw_load(D, sx, P.x, cp[k0 + u], w));
-#pragma unroll
-                    for (int u = 0; u < W; ++u)
-                        if (k0 + u < len) y = __dadd_rn(y, pr[u]);
-                }
+                // rounds with unstaged entries or long rows: one entry at a time, same order
+#pragma unroll 1
+                for (int k = 0; k < len; ++k) y = __dadd_rn(y, __dmul_rn(value(k), xval(k)));
             }
-            // the fused dot's operand: p[row] (CG, usually inside the centre window) or the
-            // staged r-hat / s segment (BiCGStab)
+            // the fused dot's operand: p[row] (CG: staged when the round's rows lie inside
+            // one window) or the staged r-hat / s segment (BiCGStab)
             double eop = 0.0;
             if (live) {
                 if constexpr (MODE == SPMV_CG) {
-                    int w2 = 0;
-                    eop = xw_load(D, sx, P.x, (int)row, w2);
+                    const int xr = rps[kRpCopy];
+                    eop = xr >= 0 ? sx[xr + t] : __ldg(P.x + row);
                 } else if constexpr (AUX) {
                     const double* sa = reinterpret_cast<const double*>(A + L.aoff);
                     eop = t < (int)((min(rs + kChunkSlots, P.n) - rs) & ~1LL) ? sa[t] : __ldg(P.aux + row);

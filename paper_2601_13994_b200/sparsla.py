@@ -285,11 +285,12 @@ class DeviceCsr:
         return {"rows": int(out[0]), "entries": int(out[1]), "threshold": int(out[2])}
 
     def xwin(self):
-        """x-window staging: {variant (-1 = off), cap_x (elements per round), cover (fraction
-        of entries whose x operand is staged)}."""
-        out = np.zeros(3, np.int64)
+        """x-window staging: {variant (-1 = none), cap_x (elements per round), cover (fraction
+        of entries whose x operand is staged), modes (SpMV modes that use it)}."""
+        out = np.zeros(4, np.int64)
         _check(lib().sparsla_dcsr_xwin(self.h, _p(out, _i64p)))
-        return {"variant": int(out[0]), "cap_x": int(out[1]), "cover": out[2] / 1e6}
+        return {"variant": int(out[0]), "cap_x": int(out[1]), "cover": out[2] / 1e6,
+                "modes": [m for m in range(4) if (int(out[3]) >> m) & 1]}
 
     def format(self):
         """SpMV storage format: value dictionary on / distinct values / constant Jacobi diagonal."""

@@ -23,32 +23,59 @@ def _gen(O, case):
         return O.generate("convdiff3d", 30, 0, 0.3)
     if case == "fem2d":
         return O.generate("fem2d", 200, 2601, 0.0)
-    if case == "banded_far":   # windows far apart, > 8 of them merged across the smallest gaps
-        return _banded(O, 70000, (1, 5, 300, 2000, 9000, 20000), 20.0, -1.0)
+    if case == "banded_far":   # 7 windows far apart (SPD: CG-safe)
+        return _banded(O, 70000, (1, 300, 2000), 20.0, -1.0)
+    if case == "two_band":     # even / odd rows on different bands: 11 windows per round, merged to 8
+        n = 80000
+        rows, cols, vals = [], [], []
+        for i in range(n):
+            offs = (0, 400, 4000, 15000, 30000, 45000) if i % 2 == 0 else (0, 1200, 8000, 22000, 37000, 52000)
+            for o in offs:
+                if i + o < n:
+                    rows.append(i)
+                    cols.append(i + o)
+                    vals.append(4.0 if o == 0 else -0.5 - 1e-3 * (o % 7))
+        return O.csr_from_triplets(n, n, rows, cols, vals)
     raise ValueError(case)
 
 
-CASES = ["poisson3d", "poisson2d", "convdiff3d", "fem2d", "banded_far"]
+CASES = ["poisson3d", "poisson2d", "convdiff3d", "fem2d", "banded_far", "two_band"]
+
+
+@pytest.fixture(autouse=True)
+def _xwin_on(monkeypatch):
+    """The x-window path is opt-in (SPARSLA_XWIN=1: when it pays, 2: forced); these tests
+    exercise it."""
+    monkeypatch.setenv("SPARSLA_XWIN", "1")
 
 
 def test_xwin_selection(S, O, gpu, monkeypatch):
-    """On by default for stencil / mesh matrices (>= 90% of entries staged), off for
-    scattered columns unless forced; SPARSLA_XWIN=0 disables."""
+    """SPARSLA_XWIN=1 (the default) stages stencil / mesh matrices (>= 90% of entries
+    staged) but not scattered columns unless forced (2); 0 disables.  With the 1-byte value
+    dictionary only BiCGStab's t-SpMV (mode 3) takes it; the plain fp64 stream uses it in
+    every mode."""
     P = to_S(S, O.generate("poisson3d", 40)).device(0)
     xw = P.xwin()
     assert xw["variant"] >= 0 and xw["cover"] >= 0.9 and 0 < xw["cap_x"] <= 2048, xw
+    assert P.format()["value_dict"] and xw["modes"] == [3], xw
+    monkeypatch.setenv("SPARSLA_VALUE_DICT", "0")
+    assert to_S(S, O.generate("poisson3d", 40)).device(0).xwin()["modes"] == [0, 1, 2, 3]
+    monkeypatch.delenv("SPARSLA_VALUE_DICT")
     R = random_csr(O, 20000, 20000, 9, 1)
     assert to_S(S, R).device(0).xwin()["variant"] == -1
     monkeypatch.setenv("SPARSLA_XWIN", "2")
     assert to_S(S, R).device(0).xwin()["variant"] >= 0
+    assert to_S(S, O.generate("poisson3d", 40)).device(0).xwin()["modes"] == [0, 1, 2, 3]
     monkeypatch.setenv("SPARSLA_XWIN", "0")
     assert to_S(S, O.generate("poisson3d", 40)).device(0).xwin()["variant"] == -1
+    monkeypatch.delenv("SPARSLA_XWIN")
+    assert to_S(S, O.generate("poisson3d", 40)).device(0).xwin()["variant"] >= 0
 
 
 @pytest.mark.parametrize("variant", range(N_XW_VARIANTS))
 @pytest.mark.parametrize("case", CASES)
 def test_xwin_spmv_bitwise(S, O, gpu, monkeypatch, case, variant):
-    if variant < 3 and case in ("fem2d", "banded_far"):
+    if variant < 3 and case in ("fem2d", "two_band"):
         pytest.skip("no value dictionary (distinct values / rows > 8): dictionary variants unused")
     A = _gen(O, case)
     monkeypatch.setenv("SPARSLA_XWIN", "2")
@@ -78,6 +105,7 @@ def test_xwin_forced_on_scattered_and_rectangular(S, O, gpu, monkeypatch, seed):
 def test_xwin_cg_trajectory_bitwise(S, O, gpu, monkeypatch, case, dictionary):
     """CG through the x-window SpMV (fused p.q operand read from the centre window)."""
     monkeypatch.setenv("SPARSLA_FUSED", "0")  # small problems would run the fused CG kernel
+    monkeypatch.setenv("SPARSLA_XWIN", "2")   # every mode, both value streams
     if not dictionary:
         monkeypatch.setenv("SPARSLA_VALUE_DICT", "0")
     A = _gen(O, case)
@@ -95,6 +123,7 @@ def test_xwin_cg_trajectory_bitwise(S, O, gpu, monkeypatch, case, dictionary):
 @pytest.mark.parametrize("case", ["convdiff3d", "fem2d"])
 def test_xwin_bicgstab_trajectory_bitwise(S, O, gpu, monkeypatch, case, dictionary):
     """BiCGStab: r-hat and s segments staged next to the windows (aux stream)."""
+    monkeypatch.setenv("SPARSLA_XWIN", "2")
     if not dictionary:
         monkeypatch.setenv("SPARSLA_VALUE_DICT", "0")
     A = _gen(O, case)

@@ -62,7 +62,7 @@ def main():
         kind, p1, p2, fp, backend = CFG[name]
         arrays = S.generate_i32(kind, p1, p2, fp)
         run(name, arrays, "gather", {"SPARSLA_XWIN": "0"})
-        run(name, arrays, "xwin-default", {})
+        run(name, arrays, "xwin-1", {"SPARSLA_XWIN": "1"})
         for var in variants or []:
             env = {"SPARSLA_XWIN": "2", "SPARSLA_XW_VARIANT": str(var)}
             if var >= 3:
@@ -70,7 +70,7 @@ def main():
             run(name, arrays, f"xwin-v{var}", env)
         if name != "C":  # plain CSR beside the dictionary
             run(name, arrays, "gather-plain", {"SPARSLA_XWIN": "0", "SPARSLA_VALUE_DICT": "0"})
-            run(name, arrays, "xwin-plain", {"SPARSLA_VALUE_DICT": "0"})
+            run(name, arrays, "xwin-plain", {"SPARSLA_XWIN": "1", "SPARSLA_VALUE_DICT": "0"})
 
 
 if __name__ == "__main__":
