@@ -202,23 +202,43 @@ class ClockSampler:
 
 
 # -------------------------------------------------------------- algorithmic bytes --------
-def kernel_bytes(solver, n, nnz, h, value_dict, uniform_diag):
+def kernel_bytes(solver, n, nnz, h, value_dict, uniform_diag, xw_modes=(), pair=False):
     """Per-launch algorithmic bytes of THIS implementation's kernels in the stored format in
     use (value dictionary: 5 B/entry + a 2 KB table instead of 12 B/entry; constant Jacobi
-    diagonal: passed as a scalar, no d stream).  Returns [(kernel name, bytes)] in launch
-    order.  CG: x += a p is moved into update 2 (p streamed once per iteration)."""
-    mat = (5 * nnz + 2048) if value_dict else 12 * nnz
+    diagonal: passed as a scalar, no d stream; x-window SpMV (modes in xw_modes): the 4-byte
+    column becomes a 2-byte offset into the round's TMA-staged x windows, + a 64-byte
+    descriptor per 256-row round, x still counted once).  Returns [(kernel name, bytes)] in
+    launch order.  CG: x += a p is moved into update 2 (p streamed once per iteration)."""
+    rounds = (n + 255) // 256
+
+    def mat(mode):
+        if mode not in xw_modes:
+            return (5 * nnz + 2048) if value_dict else 12 * nnz
+        vb = 0 if pair else (1 if value_dict else 8)
+        return (vb + 2) * nnz + (2048 if value_dict else 0) + 64 * rounds
+
     d = 0 if uniform_diag else 8 * n
     rp = 4 * (n + 1)
     if solver == "cg":
-        return [("spmv_cg", mat + rp + 8 * (n + h) + 8 * n),    # A, row_ptr, p gathered, q written
+        return [("spmv_cg", mat(1) + rp + 8 * (n + h) + 8 * n),  # A, row_ptr, p gathered, q written
                 ("cg_update1", 24 * n + d),                      # read r q (d), write r
                 ("cg_update2", 40 * n + d)]                      # read x p r (d), write x p
     return [("bicg_update1", 40 * n + d),                        # read r p v (d), write p ph
-            ("spmv_v", mat + rp + 8 * (n + h) + 16 * n),         # ph gathered, v written, rh read
+            ("spmv_v", mat(2) + rp + 8 * (n + h) + 16 * n),      # ph gathered, v written, rh read
             ("bicg_update2", 32 * n + d),                        # read r v (d), write s sh
-            ("spmv_t", mat + rp + 8 * (n + h) + 16 * n),         # sh gathered, t written, s read
+            ("spmv_t", mat(3) + rp + 8 * (n + h) + 16 * n),      # sh gathered, t written, s read
             ("bicg_update3", 64 * n)]                            # read x ph s sh t rh, write x r
+
+
+def format_text(fmt, xw):
+    vals = ("value dictionary (1-byte index into %d distinct fp64 values)" % fmt["distinct_values"]) \
+        if fmt["value_dict"] else "fp64 values"
+    if xw["modes"]:
+        names = {0: "plain", 1: "cg", 2: "bicg_v", 3: "bicg_t"}
+        return (vals + " + int32 col; SpMV modes %s: x-window kernel (16-bit offsets into TMA-staged x windows, "
+                "%d staged elements per round, %.3f of entries staged)"
+                % ([names[m] for m in xw["modes"]], xw["cap_x"], xw["cover"]))
+    return vals + " + int32 col"
 
 
 def canonical_bytes(solver, n, nnz, h=0):
@@ -337,7 +357,7 @@ def run_ours(args):
     t0 = time.time()
     D = S.DeviceCsr(None, dev, i32=(n, n, rp, ci, v))
     tup = time.time() - t0
-    info, fmt = D.info(), D.format()
+    info, fmt, xw = D.info(), D.format(), D.xwin()
     b_host = torch.ones(n, dtype=torch.float64).pin_memory()
     x_host = torch.empty(n, dtype=torch.float64).pin_memory()
     opts = S.SolveOptions(atol=0.0, rtol=args.rtol, max_iter=args.max_iter)
@@ -410,7 +430,7 @@ def run_ours(args):
     sv.iterate(5)
     kms = sv.kernel_times(args.kernel_iters)
     sv.close()
-    kb = kernel_bytes(solver, n, nnz, 0, fmt["value_dict"], fmt["uniform_diag"])
+    kb = kernel_bytes(solver, n, nnz, 0, fmt["value_dict"], fmt["uniform_diag"], xw["modes"], xw["variant"] >= 6)
     it_bytes = sum(b for _, b in kb)
     dom = max(range(len(kms)), key=lambda i: kms[i]) if solver == "cg" else \
         max((i for i, (nm, _) in enumerate(kb) if nm.startswith("spmv")), key=lambda i: kms[i])
@@ -418,13 +438,16 @@ def run_ours(args):
     dom_gbs = dom_bytes / (kms[dom] * 1e-3) / 1e9
     kernel_gbs = {nm: b / (t * 1e-3) / 1e9 for (nm, b), t in zip(kb, kms)}
     canon = canonical_bytes(solver, n, nnz)
-    # plain-CSR reference point of the same loop (value dictionary and scalar diagonal off)
-    plain = None
-    if args.plain_steps > 0 and (fmt["value_dict"] or fmt["uniform_diag"]):
-        os.environ["SPARSLA_VALUE_DICT"] = "0"
-        os.environ["SPARSLA_UNIFORM_DIAG"] = "0"
+    # plain reference points of the same loop (value dictionary and scalar diagonal off): the
+    # north star's CSR (int32 col + fp64 val, x gathered) and the same values through the
+    # x-window kernel (the default for the fp64 value stream)
+    def plain_point(xwin):
+        env = {"SPARSLA_VALUE_DICT": "0", "SPARSLA_UNIFORM_DIAG": "0", "SPARSLA_XWIN": "1" if xwin else "0"}
+        saved = {k: os.environ.get(k) for k in env}
+        os.environ.update(env)
         try:
             Dp = S.DeviceCsr(None, dev, i32=(n, n, rp, ci, v))
+            xwp = Dp.xwin()
             svp = S.Solver(Dp, b_host.numpy(), solver, opts)
             sp = torch.cuda.ExternalStream(svp.stream())
             svp.reset()
@@ -437,17 +460,27 @@ def run_ours(args):
             q1.synchronize()
             pms = q0.elapsed_time(q1) / args.plain_steps
             pk = svp.kernel_times(10)
-            pkb = kernel_bytes(solver, n, nnz, 0, False, False)
-            plain = {"value": 1e3 / pms, "unit": "it/s", "steps": args.plain_steps, "ms_per_step": pms,
-                     "kernel_ms": {nm: t for (nm, _), t in zip(pkb, pk)},
-                     "kernel_gbs": {nm: b / (t * 1e-3) / 1e9 for (nm, b), t in zip(pkb, pk)},
-                     "iteration_gbs": sum(b for _, b in pkb) / (pms * 1e-3) / 1e9,
-                     "iteration_frac": sum(b for _, b in pkb) / (pms * 1e-3) / 1e9 / peak,
-                     "format": "plain CSR (int32 col, fp64 val), streamed Jacobi diagonal"}
+            pkb = kernel_bytes(solver, n, nnz, 0, False, False, xwp["modes"])
+            out = {"value": 1e3 / pms, "unit": "it/s", "steps": args.plain_steps, "ms_per_step": pms,
+                   "kernel_ms": {nm: t for (nm, _), t in zip(pkb, pk)},
+                   "kernel_gbs": {nm: b / (t * 1e-3) / 1e9 for (nm, b), t in zip(pkb, pk)},
+                   "iteration_gbs": sum(b for _, b in pkb) / (pms * 1e-3) / 1e9,
+                   "iteration_frac": sum(b for _, b in pkb) / (pms * 1e-3) / 1e9 / peak,
+                   "format": format_text({"value_dict": False}, xwp) + ", streamed Jacobi diagonal"}
             svp.close()
             del Dp
+            return out
         finally:
-            del os.environ["SPARSLA_VALUE_DICT"], os.environ["SPARSLA_UNIFORM_DIAG"]
+            for k, val in saved.items():
+                if val is None:
+                    os.environ.pop(k, None)
+                else:
+                    os.environ[k] = val
+
+    plain = plain_xw = None
+    if args.plain_steps > 0 and (fmt["value_dict"] or fmt["uniform_diag"]):
+        plain = plain_point(False)
+        plain_xw = plain_point(True)
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "spmv_traffic.json")) as f:
@@ -464,8 +497,7 @@ def run_ours(args):
         "config": config_block(cfg, n, nnz, args.rtol),
         "partition": "single GPU",
         "format": {"spmv_variant": "tma-bulk-staged" if info["variant"] == 0 else "direct",
-                   "storage": ("value dictionary (1-byte index into %d distinct fp64 values) + int32 col"
-                               % fmt["distinct_values"]) if fmt["value_dict"] else "CSR int32 col + fp64 val",
+                   "storage": format_text(fmt, xw),
                    "jacobi_diag": "constant (scalar)" if fmt["uniform_diag"] else "streamed"},
         "iteration_gbs": it_bytes / (ms / args.steps * 1e-3) / 1e9,
         "bytes_per_iteration": it_bytes,
@@ -473,12 +505,12 @@ def run_ours(args):
         "kernel_ms": {nm: t for (nm, _), t in zip(kb, kms)},
         "kernel_gbs": kernel_gbs,
         "plain_csr": plain,
+        "plain_values_xwin": plain_xw,
         "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": dom_gbs,
                      "peak": peak, "unit": "GB/s", "frac": dom_gbs / peak, "traffic": traffic,
                      "peak_source": peak_src, "frac_of_spec_8tbs": dom_gbs / SPEC_PEAK_GBS,
                      "algorithmic_bytes_per_launch": dom_bytes,
-                     "bytes_basis": "bytes of the stored format (value dictionary: 5 B/entry + 2 KB table)"
-                                    if fmt["value_dict"] else "CSR 12 B/entry",
+                     "bytes_basis": "bytes of the stored format: " + format_text(fmt, xw),
                      "iteration_frac": (it_bytes / (ms / args.steps * 1e-3) / 1e9) / peak},
         "time_to_tolerance_s": e2e_t / len(reps), "iterations_to_tolerance": k_tol,
         "e2e": {"value": e2e_its / e2e_t, "unit": "it/s", "h2d_bytes_per_step": 8 * n,

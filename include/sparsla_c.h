@@ -343,6 +343,8 @@ int sparsla_dist_halo_exchange(sparsla_dist* D, const double* x_owned, double* h
 int sparsla_dist_info(const sparsla_dist* D, int64_t* info);
 /* this rank's local-matrix storage format (same fields as sparsla_dcsr_format) */
 int sparsla_dist_format(sparsla_dist* D, int64_t* fmt);
+/* this rank's local-matrix x-window staging (same fields as sparsla_dcsr_xwin) */
+int sparsla_dist_xwin(const sparsla_dist* D, int64_t* out);
 /* counters[0]=halo exchanges [1]=all_reduce points [2]=p2p messages performed by the live
  * algorithm (SPEC.md:524 accounting); [3..5] = raw transport calls of the same kinds (they
  * also include the no-op tail replayed after convergence).  6 entries. */

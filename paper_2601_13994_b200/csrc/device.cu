@@ -162,36 +162,38 @@ static int choose_ws_variant(long long max_row) {
 // x-window kernels (spmv_xw.cuh), indexed by variant; `vd` selects the value stream.
 // SPARSLA_XW_VARIANT overrides the choice (sweeps).
 struct XwVariant {
-    bool vd;
+    int vs;  // value stream: 0 fp64 values, 1 dictionary indices, 2 pair (index in the offset)
     int w, stg, minb;
     const void* fn[4];  // per SpmvMode
 };
-#define XWV(VD, W, S, M)                                                                            \
-    {VD, W, S, M, {(const void*)spmv_xw_kernel<SPMV_PLAIN, S, M, W, VD>, (const void*)spmv_xw_kernel<SPMV_CG, S, M, W, VD>, \
-                   (const void*)spmv_xw_kernel<SPMV_BICG_V, S, M, W, VD>, (const void*)spmv_xw_kernel<SPMV_BICG_T, S, M, W, VD>}}
-static const XwVariant kXwVariants[] = {XWV(true, 8, 3, 3), XWV(true, 8, 2, 4), XWV(true, 8, 3, 4),
-                                        XWV(false, 8, 3, 2), XWV(false, 12, 3, 2), XWV(false, 12, 2, 3)};
+#define XWV(VS, W, S, M)                                                                            \
+    {VS, W, S, M, {(const void*)spmv_xw_kernel<SPMV_PLAIN, S, M, W, VS>, (const void*)spmv_xw_kernel<SPMV_CG, S, M, W, VS>, \
+                   (const void*)spmv_xw_kernel<SPMV_BICG_V, S, M, W, VS>, (const void*)spmv_xw_kernel<SPMV_BICG_T, S, M, W, VS>}}
+static const XwVariant kXwVariants[] = {XWV(1, 8, 3, 3), XWV(1, 8, 2, 4), XWV(1, 8, 3, 4),
+                                        XWV(0, 8, 3, 2), XWV(0, 12, 3, 2), XWV(0, 12, 2, 3),
+                                        XWV(2, 8, 3, 3), XWV(2, 8, 2, 4), XWV(2, 8, 3, 4)};
 #undef XWV
 constexpr int kNumXwVariants = sizeof(kXwVariants) / sizeof(kXwVariants[0]);
 
 static size_t xw_smem_bytes(const DevCsr* A, int var, bool aux) {
     const XwVariant& V = kXwVariants[var];
-    return kXwHead + (size_t)V.stg * XwLayout(A->cap_v, A->cap_c, A->cap_x, V.vd, aux).stage;
+    return kXwHead + (size_t)V.stg * XwLayout(A->cap_v, A->cap_c, A->cap_x, V.vs, aux).stage;
 }
 
-// Variant for the current value stream (dictionary or plain) and row lengths; -1 = none.
+// Variant per value stream and row lengths; -1 = none.
 static void choose_xw_variants(DevCsr* A) {
-    A->xw_var[0] = A->xw_var[1] = -1;
+    for (int d = 0; d < 3; ++d) A->xw_var[d] = -1;
     if (!A->xw) return;
-    A->xw_var[1] = 0;
     A->xw_var[0] = 5;  // plain stream: 12-wide, 2 stages, 3 CTAs/SM (fastest on FEM and stencils)
+    A->xw_var[1] = 0;
+    A->xw_var[2] = 8;
     if (const char* e = getenv("SPARSLA_XW_VARIANT")) {
         const int x = atoi(e);
-        if (x >= 0 && x < kNumXwVariants) A->xw_var[kXwVariants[x].vd ? 1 : 0] = x;
+        if (x >= 0 && x < kNumXwVariants) A->xw_var[kXwVariants[x].vs] = x;
     }
     int dev = A->device, sms = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    for (int d = 0; d < 2; ++d)
+    for (int d = 0; d < 3; ++d) {
         for (int aux = 0; aux < 2; ++aux) {
             const int v = A->xw_var[d];
             int per_sm = 0;
@@ -201,9 +203,9 @@ static void choose_xw_variants(DevCsr* A) {
                                                                  kWsThreads, sm));
             A->xw_ctas[d][aux] = sms * per_sm;
         }
-    // the x-window path needs every mode to fit at least one CTA per SM
-    for (int d = 0; d < 2; ++d)
+        // every mode must fit at least one CTA per SM
         if (A->xw_ctas[d][0] == 0 || A->xw_ctas[d][1] == 0) A->xw_var[d] = -1;
+    }
 }
 
 size_t ws_smem_bytes(const DevCsr* A, int variant, bool vd = false) {
@@ -242,7 +244,7 @@ DevCsr::~DevCsr() {
     cudaFree(rp); cudaFree(ci); cudaFree(val); cudaFree(dinv); cudaFree(ones);
     cudaFree(vidx); cudaFree(vtab);
     cudaFree(long_rows); cudaFree(long_bits); cudaFree(s_rp); cudaFree(s_ci); cudaFree(s_val);
-    cudaFree(xw); cudaFree(xwo);
+    cudaFree(xw); cudaFree(xwo); cudaFree(xvo);
     if (stream) cudaStreamDestroy(stream);
     delete transpose;
 }
@@ -342,13 +344,17 @@ static int xwin_mode() {
     return e ? atoi(e) : 1;
 }
 
+static void build_xw_pair(DevCsr* A);
+
 static void drop_xwin(DevCsr* A) {
     cudaFree(A->xw);
     cudaFree(A->xwo);
+    cudaFree(A->xvo);
     A->xw = nullptr;
     A->xwo = nullptr;
+    A->xvo = nullptr;
     A->cap_x = 0;
-    A->xw_var[0] = A->xw_var[1] = -1;
+    A->xw_var[0] = A->xw_var[1] = A->xw_var[2] = -1;
     A->xw_cover = 0.0;
 }
 
@@ -466,7 +472,8 @@ static void build_xwin(DevCsr* A, const I* h_rp, const I* h_ci) {
     CK(memcpy_sync(A->xw, desc.data(), desc.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
     CK(memcpy_sync(A->xwo, xoff.data(), xoff.size() * sizeof(uint16_t), cudaMemcpyHostToDevice));
     choose_xw_variants(A);
-    if (A->xw_var[0] < 0 && A->xw_var[1] < 0) drop_xwin(A);
+    if (A->xw_var[0] < 0 && A->xw_var[1] < 0 && A->xw_var[2] < 0) drop_xwin(A);
+    build_xw_pair(A);
 }
 
 template <class I>
@@ -740,6 +747,32 @@ static int vd_var_of(const DevCsr* A, int mode) {
     return (mode == SPMV_BICG_T && A->vd_var == 3 && !t7) ? 0 : A->vd_var;
 }
 
+// pair stream: the dictionary index in the top 5 bits of the 16-bit window offset (one
+// 2-byte stream per entry instead of 1 + 2 bytes); needs <= 32 distinct values and
+// <= 2032 staged elements per round.  Rebuilt on the device whenever the dictionary is.
+// Same products in the same order: bit-identical to the other streams.
+static void build_xw_pair(DevCsr* A) {
+    cudaFree(A->xvo);
+    A->xvo = nullptr;
+    // opt-in (SPARSLA_XW_PAIR=1): measured slower than the gather dictionary kernel at
+    // configs B / D' / E (profiles/r02_xwin.md)
+    const char* pe = getenv("SPARSLA_XW_PAIR");
+    if (!pe || atoi(pe) == 0) return;
+    if (!A->xw || !A->vd || A->nvals > (1 << (16 - kXwPairBits)) || A->cap_x > (int)kXwPairMask - 15) return;
+    if (A->xw_var[2] < 0) return;
+    const long long m = A->nnz + kXwPad;
+    A->xvo = dalloc<uint16_t>(m);
+    xw_pair_kernel<<<grid_for(m, 256), 256, 0, A->stream>>>(A->vidx, A->xwo, A->xvo, m);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(A->stream));
+}
+
+// value stream of the x-window path: 0 fp64 values, 1 dictionary indices, 2 pair
+static int xw_stream(const DevCsr* A) {
+    if (!(A->vd && A->ws_var == 0)) return 0;
+    return A->xvo ? 2 : 1;
+}
+
 // x-window kernel variant for the matrix's current value stream and this SpMV mode, or -1.
 // Measured on B200 (tools/xw_sweep.py, profiles/r02_xwin.md): with the plain fp64 value
 // stream the x-window kernel wins everywhere (FEM config C 0.407 -> 0.31 ms; plain 7-point
@@ -747,19 +780,27 @@ static int vd_var_of(const DevCsr* A, int mode) {
 // as fast or faster except for BiCGStab's t = A s-hat (0.615 -> 0.589 ms at 368^3).
 static int xw_pick(const DevCsr* A, int mode) {
     if (!A->staged || !A->xw) return -1;
-    const bool vd = A->vd && A->ws_var == 0;
-    if (vd && mode != SPMV_BICG_T && A->xw_mode < 2) return -1;
-    return A->xw_var[vd ? 1 : 0];
+    const int vs = xw_stream(A);
+    if (vs == 1 && mode != SPMV_BICG_T && A->xw_mode < 2) return -1;
+    return A->xw_var[vs];
 }
 static bool xw_aligned(const double* x, const double* aux) {  // TMA sources: 16-byte aligned
     return ((uintptr_t)x & 15) == 0 && ((uintptr_t)aux & 15) == 0;
 }
 static bool mode_has_aux(int mode) { return mode == SPMV_BICG_V || mode == SPMV_BICG_T; }
 
+void devcsr_xwin_info(const DevCsr* A, int64_t* out) {
+    out[0] = A->xw ? A->xw_var[xw_stream(A)] : -1;
+    out[1] = A->cap_x;
+    out[2] = (int64_t)(A->xw_cover * 1e6 + 0.5);
+    out[3] = 0;
+    for (int m = 0; m < 4; ++m) out[3] |= (xw_pick(A, m) >= 0 ? 1 : 0) << m;
+}
+
 unsigned spmv_grid(const DevCsr* A, long long nch, int mode, bool xw_ok) {
     if (nch <= 0) return 0;
     if (xw_ok && xw_pick(A, mode) >= 0)
-        return (unsigned)std::min<long long>(nch, (long long)A->xw_ctas[(A->vd && A->ws_var == 0) ? 1 : 0][mode_has_aux(mode)]);
+        return (unsigned)std::min<long long>(nch, (long long)A->xw_ctas[xw_stream(A)][mode_has_aux(mode)]);
     if (A->staged) {
         const bool vdt = A->vd && A->ws_var == 0 && vd_var_of(A, mode) != A->vd_var;
         return (unsigned)std::min<long long>(nch, (long long)(vdt ? A->vdt_ctas : A->ws_ctas[A->ws_var]));
@@ -804,7 +845,7 @@ void launch_spmv_part(DevCsr* A, cudaStream_t s, int mode, const double* x, doub
     const int xv = xw_ok ? xw_pick(A, mode) : -1;
     if (xv >= 0) {
         P.xw = A->xw;
-        P.xwo = A->xwo;
+        P.xwo = xw_stream(A) == 2 ? A->xvo : A->xwo;
         P.cap_x = A->cap_x;
         void* args[] = {&P};
         CK(cudaLaunchKernel(kXwVariants[xv].fn[mode], dim3(grid), dim3(kWsThreads), args,
@@ -1382,6 +1423,7 @@ void devcsr_set_values(DevCsr* A, const double* vals, int32_t mem) {
         drop_value_dictionary(A);
     }
     A->smem_bytes = ws_smem_bytes(A, A->ws_var, A->vd);
+    build_xw_pair(A);  // the pair stream carries dictionary indices
     if (A->dinv) { cudaFree(A->dinv); A->dinv = nullptr; }
     A->dinv_uniform = -1;
     A->sym_checked = -1;
@@ -1544,12 +1586,7 @@ int sparsla_dcsr_info(const sparsla_dcsr* H, int64_t* info) {
 int sparsla_dcsr_xwin(const sparsla_dcsr* H, int64_t* out) {
     return guarded([&] {
         need(H, "matrix"); need(out, "out");
-        const DevCsr* A = H->A;
-        out[0] = A->xw ? A->xw_var[(A->vd && A->ws_var == 0) ? 1 : 0] : -1;
-        out[1] = A->cap_x;
-        out[2] = (int64_t)(A->xw_cover * 1e6 + 0.5);
-        out[3] = 0;
-        for (int m = 0; m < 4; ++m) out[3] |= (xw_pick(A, m) >= 0 ? 1 : 0) << m;
+        devcsr_xwin_info(H->A, out);
     });
 }
 

@@ -63,8 +63,9 @@ struct DevCsr {
     uint16_t* xwo = nullptr;   // [nnz + kXwPad] entry -> offset in its round's staged windows
     int cap_x = 0;             // max staged x elements per round
     int xw_mode = 0;           // SPARSLA_XWIN at creation (2: every mode and stream)
-    int xw_var[2] = {-1, -1};  // x-window kernel variant, [plain, dictionary]; -1: not used
-    int xw_ctas[2][2] = {{0, 0}, {0, 0}};  // persistent grid [dictionary][aux vector staged]
+    uint16_t* xvo = nullptr;   // [nnz + kXwPad] pair stream: dictionary index << 11 | offset
+    int xw_var[3] = {-1, -1, -1};  // x-window kernel variant per value stream [plain, dictionary, pair]
+    int xw_ctas[3][2] = {{0, 0}, {0, 0}, {0, 0}};  // persistent grid [stream][aux vector staged]
     double xw_cover = 0.0;     // fraction of entries whose x operand is staged
     DevCsr* transpose = nullptr;
     cudaStream_t stream = nullptr;
@@ -86,6 +87,9 @@ struct DevCsr {
     bool exactly_symmetric();
     DevCsr* get_transpose();
 };
+
+// x-window staging summary (sparsla_dcsr_xwin layout)
+void devcsr_xwin_info(const DevCsr* A, int64_t* out);
 
 // new values in A's entry order (host or device pointer); drops every value-dependent cache
 void devcsr_set_values(DevCsr* A, const double* vals, int32_t mem);

@@ -28,6 +28,18 @@ constexpr int kXwDescInts = 16; // per-round descriptor (64 B):
 //   [rs, re) lie inside one window (CG's p.q operand), else -1      [15] 1: every entry of
 //   the round is staged (the consumer skips the per-entry fallback test)
 constexpr uint16_t kXwNone = 0xFFFFu;
+// pair stream: (dictionary index << 11) | window offset; offset 0x7FF = not staged
+constexpr int kXwPairBits = 11;
+constexpr uint32_t kXwPairMask = (1u << kXwPairBits) - 1u;
+
+// pair stream from the dictionary indices and the window offsets (device, after every
+// dictionary (re)build)
+static __global__ void xw_pair_kernel(const uint8_t* vidx, const uint16_t* xwo, uint16_t* xvo, long long m) {
+    const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= m) return;
+    const uint32_t o = xwo[k];
+    xvo[k] = (uint16_t)(((uint32_t)vidx[k] << kXwPairBits) | (o == kXwNone ? kXwPairMask : o));
+}
 constexpr int kXwPad = 32;  // offsets past the last entry (bulk-copy granule slack)
 
 __device__ __forceinline__ void fence_proxy_async_global() {
@@ -45,8 +57,10 @@ __device__ __forceinline__ void bulk_g2s_plain(void* dst, const void* src, uint3
 struct XwLayout {
     size_t vbytes, obytes, rbytes, xbytes, abytes, stage;
     size_t ooff, roff, xoff, aoff;
-    __host__ __device__ XwLayout(int cap_v, int cap_c, int cap_x, bool vd, bool aux) {
-        vbytes = ((size_t)cap_v * (vd ? 1 : 8) + (vd ? 32 : 0) + 127) & ~size_t(127);
+    // vs: value stream 0 = fp64 values, 1 = 1-byte dictionary indices, 2 = none (the value
+    // index travels in the top 5 bits of the 16-bit offset: "pair" stream)
+    __host__ __device__ XwLayout(int cap_v, int cap_c, int cap_x, int vs, bool aux) {
+        vbytes = vs == 2 ? 0 : ((size_t)cap_v * (vs ? 1 : 8) + (vs ? 32 : 0) + 127) & ~size_t(127);
         obytes = ((size_t)cap_c * 2 + 64 + 127) & ~size_t(127);  // 16-bit window offsets (+ spares)
         rbytes = (kRpCopy * 4 + 127) & ~size_t(127);
         xbytes = ((size_t)cap_x * 8 + 127) & ~size_t(127);
@@ -64,8 +78,10 @@ constexpr size_t kXwHead = 1024 + 2 * kChunkRounds * kXwDescInts * 4;
 
 template <int MODE> struct XwAux { static constexpr bool on = (MODE == SPMV_BICG_V || MODE == SPMV_BICG_T); };
 
-template <int MODE, int STG, int MINB, int W, bool VD>
+template <int MODE, int STG, int MINB, int W, int VS>
 __global__ void __launch_bounds__(kWsThreads, MINB) spmv_xw_kernel(SpmvParams P) {
+    constexpr bool VD = VS != 0;     // values from the dictionary table
+    constexpr bool PAIR = VS == 2;   // ... indexed by the top bits of the offset stream
     constexpr int ND = SpmvDots<MODE>::n;
     constexpr int NA = ND > 0 ? ND : 1;
     constexpr bool AUX = XwAux<MODE>::on;
@@ -80,7 +96,7 @@ __global__ void __launch_bounds__(kWsThreads, MINB) spmv_xw_kernel(SpmvParams P)
     uint64_t* empty = full + STG;
     uint64_t* dbar = empty + STG;  // [2]
     int32_t* dbuf = reinterpret_cast<int32_t*>(smem + 1024);
-    const XwLayout L(P.cap_v, P.cap_c, P.cap_x, VD, AUX);
+    const XwLayout L(P.cap_v, P.cap_c, P.cap_x, VS, AUX);
     unsigned char* stage0 = smem + kXwHead;
     const int t = threadIdx.x;
     const int warp = t >> 5, lane = t & 31;
@@ -134,7 +150,7 @@ __global__ void __launch_bounds__(kWsThreads, MINB) spmv_xw_kernel(SpmvParams P)
                     const int nz0 = d[12], nz1 = d[13];
                     const int a0 = nz0 & ~(VALIGN - 1), a1 = (nz1 + VALIGN - 1) & ~(VALIGN - 1);
                     const int o0 = nz0 & ~7, o1 = (nz1 + 7) & ~7;
-                    const uint32_t vb = (uint32_t)(a1 - a0) * (VD ? 1u : 8u);
+                    const uint32_t vb = PAIR ? 0u : (uint32_t)(a1 - a0) * (VD ? 1u : 8u);
                     const uint32_t ob = (uint32_t)(o1 - o0) * 2u;
                     uint32_t xb = 0;
 #pragma unroll
@@ -203,12 +219,18 @@ __global__ void __launch_bounds__(kWsThreads, MINB) spmv_xw_kernel(SpmvParams P)
             const uint8_t* vp = A + (kb - (o0 & ~(VALIGN - 1)));
             const double* vs = reinterpret_cast<const double*>(A) + (kb - (o0 & ~(VALIGN - 1)));
             auto value = [&](int u) -> double {
-                if constexpr (VD) return s_vtab[vp[u]];
+                if constexpr (PAIR) return s_vtab[xo[u] >> kXwPairBits];
+                else if constexpr (VD) return s_vtab[vp[u]];
                 else return vs[u];
             };
             auto xval = [&](int u) -> double {
-                const uint32_t o = xo[u];
-                return o != kXwNone ? sx[o] : __ldg(P.x + __ldg(P.ci + kb + u));
+                if constexpr (PAIR) {
+                    const uint32_t o = xo[u] & kXwPairMask;
+                    return o != kXwPairMask ? sx[o] : __ldg(P.x + __ldg(P.ci + kb + u));
+                } else {
+                    const uint32_t o = xo[u];
+                    return o != kXwNone ? sx[o] : __ldg(P.x + __ldg(P.ci + kb + u));
+                }
             };
             double y = 0.0;
             const bool all_staged = rps[kRpCopy + 1] != 0;  // round-uniform
@@ -219,7 +241,14 @@ __global__ void __launch_bounds__(kWsThreads, MINB) spmv_xw_kernel(SpmvParams P)
                 double pr[W];
 #pragma unroll
                 for (int u = 0; u < W; ++u)
-                    if (u < len) pr[u] = __dmul_rn(value(u), sx[xo[u]]);
+                    if (u < len) {
+                        if constexpr (PAIR) {
+                            const uint32_t e = xo[u];
+                            pr[u] = __dmul_rn(s_vtab[e >> kXwPairBits], sx[e & kXwPairMask]);
+                        } else {
+                            pr[u] = __dmul_rn(value(u), sx[xo[u]]);
+                        }
+                    }
 #pragma unroll
                 for (int u = 0; u < W; ++u)
                     if (u < len) y = __dadd_rn(y, pr[u]);

@@ -965,6 +965,13 @@ class DistPlan:
         _check(lib().sparsla_dist_format(self.h, _p(out, _i64p)))
         return {"value_dict": bool(out[0]), "distinct_values": int(out[1]), "uniform_diag": bool(out[2])}
 
+    def xwin(self):
+        """This rank's local-matrix x-window staging (see DeviceCsr.xwin)."""
+        out = np.zeros(4, np.int64)
+        _check(lib().sparsla_dist_xwin(self.h, _p(out, _i64p)))
+        return {"variant": int(out[0]), "cap_x": int(out[1]), "cover": out[2] / 1e6,
+                "modes": [m for m in range(4) if (int(out[3]) >> m) & 1]}
+
     def set_values(self, vals_local, mem=MEM_HOST):
         """Collective: new values of this rank's local matrix (local entry order)."""
         if mem == MEM_HOST:

@@ -11,7 +11,7 @@ from test_gpu_parity import _banded, assert_bitwise, random_csr, rep_eq, to_S
 
 pytestmark = pytest.mark.gpu
 
-N_XW_VARIANTS = 6  # kXwVariants in csrc/device.cu (0-2 dictionary, 3-5 plain)
+N_XW_VARIANTS = 9  # kXwVariants in csrc/device.cu (0-2 dictionary, 3-5 plain, 6-8 pair)
 
 
 def _gen(O, case):
@@ -51,13 +51,18 @@ def _xwin_on(monkeypatch):
 
 def test_xwin_selection(S, O, gpu, monkeypatch):
     """SPARSLA_XWIN=1 (the default) stages stencil / mesh matrices (>= 90% of entries
-    staged) but not scattered columns unless forced (2); 0 disables.  With the 1-byte value
-    dictionary only BiCGStab's t-SpMV (mode 3) takes it; the plain fp64 stream uses it in
-    every mode."""
+    staged) but not scattered columns unless forced (2); 0 disables.  The plain fp64 stream
+    uses it in every mode; with the 1-byte dictionary stream only BiCGStab's t-SpMV (mode 3)
+    takes it; the opt-in pair stream (SPARSLA_XW_PAIR=1: dictionary index inside the 16-bit
+    offset) in every mode."""
     P = to_S(S, O.generate("poisson3d", 40)).device(0)
     xw = P.xwin()
-    assert xw["variant"] >= 0 and xw["cover"] >= 0.9 and 0 < xw["cap_x"] <= 2048, xw
+    assert xw["variant"] in (0, 1, 2) and xw["cover"] >= 0.9 and 0 < xw["cap_x"] <= 2048, xw
     assert P.format()["value_dict"] and xw["modes"] == [3], xw
+    monkeypatch.setenv("SPARSLA_XW_PAIR", "1")
+    xw = to_S(S, O.generate("poisson3d", 40)).device(0).xwin()
+    assert xw["variant"] >= 6 and xw["modes"] == [0, 1, 2, 3], xw
+    monkeypatch.delenv("SPARSLA_XW_PAIR")
     monkeypatch.setenv("SPARSLA_VALUE_DICT", "0")
     assert to_S(S, O.generate("poisson3d", 40)).device(0).xwin()["modes"] == [0, 1, 2, 3]
     monkeypatch.delenv("SPARSLA_VALUE_DICT")
@@ -75,13 +80,15 @@ def test_xwin_selection(S, O, gpu, monkeypatch):
 @pytest.mark.parametrize("variant", range(N_XW_VARIANTS))
 @pytest.mark.parametrize("case", CASES)
 def test_xwin_spmv_bitwise(S, O, gpu, monkeypatch, case, variant):
-    if variant < 3 and case in ("fem2d", "two_band"):
+    if (variant < 3 or variant >= 6) and case in ("fem2d", "two_band"):
         pytest.skip("no value dictionary (distinct values / rows > 8): dictionary variants unused")
     A = _gen(O, case)
     monkeypatch.setenv("SPARSLA_XWIN", "2")
     monkeypatch.setenv("SPARSLA_XW_VARIANT", str(variant))
-    if variant >= 3:
+    if 3 <= variant < 6:
         monkeypatch.setenv("SPARSLA_VALUE_DICT", "0")
+    if variant >= 6:
+        monkeypatch.setenv("SPARSLA_XW_PAIR", "1")
     D = to_S(S, A).device(0)
     assert D.xwin()["variant"] == variant, (D.xwin(), D.format())
     x = np.random.default_rng(3).standard_normal(A.ncols)
@@ -100,14 +107,20 @@ def test_xwin_forced_on_scattered_and_rectangular(S, O, gpu, monkeypatch, seed):
     assert_bitwise(S.spmv(D, x), O.spmv(A, x), "rectangular")
 
 
-@pytest.mark.parametrize("dictionary", [True, False])
+def _stream(monkeypatch, stream):
+    if stream == "plain":
+        monkeypatch.setenv("SPARSLA_VALUE_DICT", "0")
+    elif stream == "pair":
+        monkeypatch.setenv("SPARSLA_XW_PAIR", "1")
+
+
+@pytest.mark.parametrize("stream", ["pair", "dict", "plain"])
 @pytest.mark.parametrize("case", ["poisson3d", "fem2d", "banded_far"])
-def test_xwin_cg_trajectory_bitwise(S, O, gpu, monkeypatch, case, dictionary):
+def test_xwin_cg_trajectory_bitwise(S, O, gpu, monkeypatch, case, stream):
     """CG through the x-window SpMV (fused p.q operand read from the centre window)."""
     monkeypatch.setenv("SPARSLA_FUSED", "0")  # small problems would run the fused CG kernel
-    monkeypatch.setenv("SPARSLA_XWIN", "2")   # every mode, both value streams
-    if not dictionary:
-        monkeypatch.setenv("SPARSLA_VALUE_DICT", "0")
+    monkeypatch.setenv("SPARSLA_XWIN", "2")   # every mode, every value stream
+    _stream(monkeypatch, stream)
     A = _gen(O, case)
     D = to_S(S, A).device(0)
     assert D.xwin()["variant"] >= 0
@@ -119,13 +132,12 @@ def test_xwin_cg_trajectory_bitwise(S, O, gpu, monkeypatch, case, dictionary):
     assert_bitwise(x, xo, case)
 
 
-@pytest.mark.parametrize("dictionary", [True, False])
+@pytest.mark.parametrize("stream", ["pair", "dict", "plain"])
 @pytest.mark.parametrize("case", ["convdiff3d", "fem2d"])
-def test_xwin_bicgstab_trajectory_bitwise(S, O, gpu, monkeypatch, case, dictionary):
+def test_xwin_bicgstab_trajectory_bitwise(S, O, gpu, monkeypatch, case, stream):
     """BiCGStab: r-hat and s segments staged next to the windows (aux stream)."""
     monkeypatch.setenv("SPARSLA_XWIN", "2")
-    if not dictionary:
-        monkeypatch.setenv("SPARSLA_VALUE_DICT", "0")
+    _stream(monkeypatch, stream)
     A = _gen(O, case)
     D = to_S(S, A).device(0)
     assert D.xwin()["variant"] >= 0
@@ -137,9 +149,10 @@ def test_xwin_bicgstab_trajectory_bitwise(S, O, gpu, monkeypatch, case, dictiona
     assert_bitwise(x, xo, case)
 
 
-def test_xwin_set_values_keeps_windows(S, O, gpu):
-    """Windows depend on the pattern only: set_values (dictionary dropped / rebuilt) keeps
-    the staged path and the bits."""
+def test_xwin_set_values_keeps_windows(S, O, gpu, monkeypatch):
+    """Windows depend on the pattern only: set_values (dictionary dropped / rebuilt, pair
+    stream rebuilt on the device) keeps the staged path and the bits."""
+    monkeypatch.setenv("SPARSLA_XW_PAIR", "1")
     A = O.generate("poisson3d", 40)
     D = to_S(S, A).device(0)
     x = np.random.default_rng(9).standard_normal(A.ncols)
@@ -148,5 +161,9 @@ def test_xwin_set_values_keeps_windows(S, O, gpu):
     assert not D.format()["value_dict"] and D.xwin()["variant"] >= 0
     assert_bitwise(S.spmv(D, x), O.spmv(O.Csr(A.nrows, A.ncols, A.row_ptr, A.col_idx, v2), x))
     D.set_values(A.vals)
-    assert D.format()["value_dict"] and D.xwin()["variant"] >= 0
+    assert D.format()["value_dict"] and D.xwin()["variant"] >= 6  # pair stream rebuilt
     assert_bitwise(S.spmv(D, x), O.spmv(A, x))
+    v3 = np.where(A.vals < 0, -1.5, A.vals)  # new dictionary values, same pattern
+    D.set_values(v3)
+    assert D.xwin()["variant"] >= 6
+    assert_bitwise(S.spmv(D, x), O.spmv(O.Csr(A.nrows, A.ncols, A.row_ptr, A.col_idx, v3), x))

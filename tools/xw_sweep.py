@@ -25,7 +25,7 @@ CFG = {"B": ("poisson3d", 464, 0, 0.0, "cg"), "E": ("poisson3d", 368, 0, 0.0, "c
 def run(name, arrays, setting, env):
     kind, p1, p2, fp, backend = CFG[name]
     nr, n, rp, ci, v = arrays
-    for k in ("SPARSLA_XWIN", "SPARSLA_XW_VARIANT", "SPARSLA_VALUE_DICT"):
+    for k in ("SPARSLA_XWIN", "SPARSLA_XW_VARIANT", "SPARSLA_VALUE_DICT", "SPARSLA_XW_PAIR"):
         os.environ.pop(k, None)
     os.environ.update(env)
     D = S.DeviceCsr(None, 0, i32=(n, n, rp, ci, v))
@@ -65,8 +65,10 @@ def main():
         run(name, arrays, "xwin-1", {"SPARSLA_XWIN": "1"})
         for var in variants or []:
             env = {"SPARSLA_XWIN": "2", "SPARSLA_XW_VARIANT": str(var)}
-            if var >= 3:
+            if 3 <= var < 6:
                 env["SPARSLA_VALUE_DICT"] = "0"
+            if var >= 6:
+                env["SPARSLA_XW_PAIR"] = "1"
             run(name, arrays, f"xwin-v{var}", env)
         if name != "C":  # plain CSR beside the dictionary
             run(name, arrays, "gather-plain", {"SPARSLA_XWIN": "0", "SPARSLA_VALUE_DICT": "0"})
