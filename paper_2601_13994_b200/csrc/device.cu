@@ -245,6 +245,9 @@ DevCsr::~DevCsr() {
     cudaFree(vidx); cudaFree(vtab);
     cudaFree(long_rows); cudaFree(long_bits); cudaFree(s_rp); cudaFree(s_ci); cudaFree(s_val);
     cudaFree(xw); cudaFree(xwo); cudaFree(xvo);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (side) cudaStreamDestroy(side);
     if (stream) cudaStreamDestroy(stream);
     delete transpose;
 }
@@ -818,14 +821,7 @@ void launch_spmv_part(DevCsr* A, cudaStream_t s, int mode, const double* x, doub
     if (grid == 0) return;
     SpmvParams P{};
     P.rp = A->rp; P.ci = A->ci; P.val = A->val;
-    if (A->nlong > 0) {  // long rows first (warp per row), then the short-row view
-        LongRowParams L{A->rp, A->ci, A->val, x, y, A->long_rows, A->nlong, red.st, check_done && red.st};
-        int dev = 0, sms = 0;
-        CK(cudaGetDevice(&dev));
-        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        const long long want = (A->nlong + kLongWarps - 1) / kLongWarps;
-        spmv_longrow_kernel<<<(unsigned)std::min<long long>(want, (long long)sms * 8), kLongWarps * 32, 0, s>>>(L);
-        CK(cudaGetLastError());
+    if (A->nlong > 0) {  // short-row view (long rows empty, summed by launch_spmv's fork)
         P.rp = A->s_rp; P.ci = A->s_ci; P.val = A->s_val;
         P.long_bits = A->long_bits;
     }
@@ -872,9 +868,57 @@ void launch_spmv_part(DevCsr* A, cudaStream_t s, int mode, const double* x, doub
     CK(cudaGetLastError());
 }
 
+// Long rows (single GPU): fork a side stream for the warp-per-row kernel, run the staged
+// kernel over the short-row view in SPMV_PLAIN mode meanwhile, join, then form the fused
+// dots with spmv_dots_kernel (same canonical reduction, same bits).  Stream-ordered and
+// capturable (the fork/join becomes graph edges).
+static void launch_spmv_longsplit(DevCsr* A, cudaStream_t s, int mode, const double* x, double* y,
+                                  const double* aux, const RedParams& red, int check_done) {
+    {
+        std::lock_guard<std::mutex> lk(A->lazy_mu);
+        if (!A->side) {
+            CK(cudaStreamCreateWithFlags(&A->side, cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&A->ev_fork, cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&A->ev_join, cudaEventDisableTiming));
+        }
+    }
+    std::lock_guard<std::mutex> lk(A->split_mu);  // one fork in flight per matrix on the host
+    CK(cudaEventRecord(A->ev_fork, s));
+    CK(cudaStreamWaitEvent(A->side, A->ev_fork, 0));
+    LongRowParams L{A->rp, A->ci, A->val, x, y, A->long_rows, A->nlong, red.st, check_done && red.st};
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, A->device));
+    const long long want = (A->nlong + kLongWarps - 1) / kLongWarps;
+    spmv_longrow_kernel<<<(unsigned)std::min<long long>(want, (long long)sms * 16), kLongWarps * 32, 0, A->side>>>(L);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(A->ev_join, A->side));
+    const long long nch = nchunks_of(A->nrows);
+    RedParams none{};
+    none.st = red.st;
+    launch_spmv_part(A, s, SPMV_PLAIN, x, y, aux, none, check_done && red.st, nullptr, nch,
+                     spmv_grid(A, nch, SPMV_PLAIN, xw_aligned(x, aux)));
+    CK(cudaStreamWaitEvent(s, A->ev_join, 0));
+    if (mode == SPMV_PLAIN) return;
+    SpmvParams P{};
+    P.x = x; P.y = y; P.aux = aux; P.n = A->nrows; P.check_done = check_done;
+    P.red = red;
+    P.red.nchunks = nch;
+    P.red.expected = (unsigned)nch;
+    switch (mode) {
+        case SPMV_CG: spmv_dots_kernel<SPMV_CG><<<(unsigned)nch, kSpmvThreads, 0, s>>>(P); break;
+        case SPMV_BICG_V: spmv_dots_kernel<SPMV_BICG_V><<<(unsigned)nch, kSpmvThreads, 0, s>>>(P); break;
+        case SPMV_BICG_T: spmv_dots_kernel<SPMV_BICG_T><<<(unsigned)nch, kSpmvThreads, 0, s>>>(P); break;
+    }
+    CK(cudaGetLastError());
+}
+
 void launch_spmv(DevCsr* A, cudaStream_t s, int mode, const double* x, double* y, const double* aux,
                  const RedParams& red, int check_done) {
     if (A->nrows == 0) return;
+    if (A->nlong > 0) {
+        launch_spmv_longsplit(A, s, mode, x, y, aux, red, check_done);
+        return;
+    }
     const long long nch = nchunks_of(A->nrows);
     launch_spmv_part(A, s, mode, x, y, aux, red, check_done, nullptr, nch, spmv_grid(A, nch, mode, xw_aligned(x, aux)));
 }

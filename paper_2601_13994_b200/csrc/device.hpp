@@ -54,6 +54,9 @@ struct DevCsr {
     long long nlong = 0, long_nnz = 0, long_threshold = 0;
     int32_t* long_rows = nullptr;    // [nlong], longest first
     uint32_t* long_bits = nullptr;   // [ceil(n/32)]
+    cudaStream_t side = nullptr;     // forked stream of the long-row kernel (launch_spmv)
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    std::mutex split_mu;
     int32_t* s_rp = nullptr;         // short-row view (same padding as rp/ci/val)
     int32_t* s_ci = nullptr;
     double* s_val = nullptr;

@@ -528,13 +528,13 @@ struct SpmvParams {
     RedParams red;
 };
 
-// A row that spmv_longrow_kernel already summed is empty in the short-row view, so its
-// staged sum is +0.0: take the long-row kernel's value instead (the bit is only read for
-// rows whose sum is exactly zero, and only when the matrix has long rows at all).
-__device__ __forceinline__ double long_row_fix(const SpmvParams& P, long long row, double y) {
-    if (P.long_bits != nullptr && y == 0.0 && ((__ldg(P.long_bits + (row >> 5)) >> (row & 31)) & 1u))
-        return __ldcg(P.y + row);
-    return y;
+// A row that spmv_longrow_kernel sums (concurrently, on a forked stream) is empty in the
+// short-row view, so its staged sum is +0.0: the short-row kernel must not store it (the
+// bit is only read for rows whose sum is exactly zero, and only when the matrix has long
+// rows at all).  Long-row SpMVs run the short-row kernel in SPMV_PLAIN mode; their fused
+// dots come from spmv_dots_kernel after the join.
+__device__ __forceinline__ bool long_row_skip(const SpmvParams& P, long long row, double y) {
+    return P.long_bits != nullptr && y == 0.0 && ((__ldg(P.long_bits + (row >> 5)) >> (row & 31)) & 1u);
 }
 
 template <int MODE>
@@ -600,8 +600,7 @@ __global__ void __launch_bounds__(kSpmvThreads, 2) spmv_direct_kernel(SpmvParams
                                          c = __ldg(P.ci + k);
                                          v = __ldg(P.val + k);
                                      });
-            y = long_row_fix(P, row, y);
-            P.y[row] = y;
+            if (!long_row_skip(P, row, y)) P.y[row] = y;
             spmv_epilogue<MODE>(P, row, y, acc);
         }
     }
@@ -946,9 +945,8 @@ __global__ void __launch_bounds__(kWsThreads, MINB) spmv_ws_kernel(SpmvParams P)
             for (int j = 0; j < RPT; ++j) {
                 const long long row = base + (long long)(r + j) * kChunkSlots + t;
                 if (j < cnt && row < P.n) {
-                    const double yj = long_row_fix(P, row, y[j]);
-                    P.y[row] = yj;
-                    spmv_epilogue<MODE>(P, row, yj, acc);
+                    if (!long_row_skip(P, row, y[j])) P.y[row] = y[j];
+                    spmv_epilogue<MODE>(P, row, y[j], acc);
                 }
             }
             g += cnt;
@@ -1084,8 +1082,7 @@ __global__ void __launch_bounds__(kSpmvThreads, MINB) spmv_wp_kernel(SpmvParams 
                 issue_next();
             }
             if (row < P.n) {
-                y = long_row_fix(P, row, y);
-                P.y[row] = y;
+                if (!long_row_skip(P, row, y)) P.y[row] = y;
                 spmv_epilogue<MODE>(P, row, y, acc);
             }
         }
@@ -1149,9 +1146,14 @@ __device__ __forceinline__ void set_lane(double2& v, int e, double x) { if (e) v
 // loads are software-pipelined around it: while lane 0 runs the chain of batch b, the x
 // gathers of batch b+1 and the col/val loads of batch b+2 are in flight.  The list is
 // sorted longest first and walked grid-stride, so the longest chains start at once.
-// The staged SpMV then runs on the short-row view (long rows empty) and picks these sums
-// up (long_row_fix), keeping its fused dots in canonical order.
-constexpr int kLongWarps = 8;
+// The staged SpMV runs concurrently (forked stream) on the short-row view, where the long
+// rows are empty and not stored (long_row_skip); after the join spmv_dots_kernel forms the
+// fused dots in canonical order.  So the SpMV costs max(longest chain, short rows) + one
+// 16-24 B/row dot pass instead of their sum.
+// one warp per CTA: the long-row kernel runs beside the persistent short-row kernel, so its
+// CTAs must fit in the register / shared-memory slack that kernel leaves on each SM (an
+// 8-warp CTA holding a hub row kept a short-row CTA off its SM for the whole hub chain)
+constexpr int kLongWarps = 1;
 constexpr int kLongU = 4;                    // entries per lane per batch
 constexpr int kLongBatch = 32 * kLongU;      // 128 entries per batch
 
@@ -1216,6 +1218,30 @@ static __global__ void __launch_bounds__(kLongWarps * 32) spmv_longrow_kernel(Lo
         }
         if (lane == 0) P.y[row] = sum;
     }
+}
+
+// Fused dots of an SpMV whose rows were summed by two concurrent kernels (long rows warp-
+// per-row, the rest staged): one CTA per 2048-row chunk re-reads y (and the dot operand)
+// and reduces them in the canonical chunk shape (slot t, rounds 0..7, then the block tree)
+// — the same bits as the staged kernels' fused epilogue; the last CTA runs the scalar step.
+template <int MODE>
+static __global__ void __launch_bounds__(kSpmvThreads) spmv_dots_kernel(SpmvParams P) {
+    constexpr int ND = SpmvDots<MODE>::n;
+    if (P.check_done && P.red.st->done) return;
+    const int t = threadIdx.x;
+    const long long chunk = blockIdx.x;
+    const long long base = chunk * kChunk;
+    double acc[ND];
+#pragma unroll
+    for (int d = 0; d < ND; ++d) acc[d] = 0.0;
+#pragma unroll
+    for (int r = 0; r < kChunkRounds; ++r) {
+        const long long row = base + (long long)r * kChunkSlots + t;
+        if (row < P.n) spmv_epilogue<MODE>(P, row, __ldg(P.y + row), acc);
+    }
+    __shared__ double sred[SpmvFin<MODE>::n * (kSpmvThreads / 32)];
+    block_tree<kSpmvThreads, ND>(acc, sred);
+    publish_and_finish<kSpmvThreads, ND, SpmvFin<MODE>::n>(acc, chunk, P.red, sred);
 }
 
 // short-row view values after set_values: copy every row that is not long

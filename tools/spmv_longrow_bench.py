@@ -4,7 +4,8 @@ diagonally dominant).  The SpMV is timed inside the CG loop (kernel_times: the S
 long-row kernel + staged kernel on the short-row view, CUDA events on the solver stream);
 bytes = 12 nnz + 4 (n+1) + 24 n (gathered x once, q written, p read for p.q).
 
-    python tools/spmv_longrow_bench.py [n]
+    python tools/spmv_longrow_bench.py [n] [threshold ...]   (thresholds: auto | <entries> | 0 = off;
+                                                             default: auto 0)
 """
 import json
 import os
@@ -36,7 +37,8 @@ def main():
     x = np.random.default_rng(1).standard_normal(n)
     yref = O.spmv(A, x)
     b = np.ones(n)
-    for thr in (None, "0"):
+    thrs = [None if t == "auto" else t for t in sys.argv[2:]] or [None, "0"]
+    for thr in thrs:
         if thr is None:
             os.environ.pop("SPARSLA_LONG_ROW", None)
         else:
@@ -50,7 +52,7 @@ def main():
         sv.close()
         byt = 12 * A.nnz + 4 * (n + 1) + 24 * n
         lr = D.long_rows()
-        print(json.dumps({"n": n, "nnz": int(A.nnz), "max_row": int(lens.max()), "p99_row": float(np.percentile(lens, 99)),
+        print(json.dumps({"n": n, "nnz": int(A.nnz), "threshold_env": thr or "auto", "max_row": int(lens.max()), "p99_row": float(np.percentile(lens, 99)),
                           "long_rows": lr, "mode": "warp-per-row split" if lr["rows"] else "staged + hub bypass",
                           "spmv_ms": kms[0], "spmv_gbs": byt / (kms[0] * 1e-3) / 1e9,
                           "frac": byt / (kms[0] * 1e-3) / 1e9 / PEAK, "bitwise_vs_oracle": bool(ok),
