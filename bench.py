@@ -430,7 +430,7 @@ def run_ours(args):
     sv.iterate(5)
     kms = sv.kernel_times(args.kernel_iters)
     sv.close()
-    kb = kernel_bytes(solver, n, nnz, 0, fmt["value_dict"], fmt["uniform_diag"], xw["modes"], xw["variant"] >= 6)
+    kb = kernel_bytes(solver, n, nnz, 0, fmt["value_dict"], fmt["uniform_diag"], xw["modes"], xw["stream"] == 2)
     it_bytes = sum(b for _, b in kb)
     dom = max(range(len(kms)), key=lambda i: kms[i]) if solver == "cg" else \
         max((i for i, (nm, _) in enumerate(kb) if nm.startswith("spmv")), key=lambda i: kms[i])
@@ -486,7 +486,9 @@ def run_ours(args):
         with open(os.path.join(ROOT, "profiles", "spmv_traffic.json")) as f:
             tj = json.load(f)
         if tj.get("size") == cfg["p1"] and cfg["name"] == "B":
-            traffic = tj["value_dict" if fmt["value_dict"] else "plain"]["dram_bytes_per_launch"]
+            key = ("pair_xwin" if xw["stream"] == 2 else "xwin") if 1 in xw["modes"] else \
+                ("value_dict" if fmt["value_dict"] else "plain")
+            traffic = tj[key]["dram_bytes_per_launch"] if key in tj else None
     except Exception:
         pass
     line = {

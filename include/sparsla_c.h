@@ -199,8 +199,10 @@ int sparsla_dcsr_format(sparsla_dcsr* A, int64_t* fmt);
  * variant for the current value stream (-1: none built), out[1]=staged x elements per
  * 256-row round, out[2]=parts per million of the entries whose x operand is staged,
  * out[3]=bit m set when SpMV mode m (0 plain, 1 CG p.q, 2 BiCGStab r-hat.v, 3 BiCGStab
- * t.t/t.s) runs the x-window kernel.  SPARSLA_XWIN at matrix creation: 0 disables, 1 (the
- * default) stages when it pays, 2 forces every mode. */
+ * t.t/t.s) runs the x-window kernel, out[4]=its value stream (0 fp64 values, 1 1-byte
+ * dictionary indices, 2 "pair": the dictionary index inside the 16-bit offset).  out has 5
+ * entries.  SPARSLA_XWIN at matrix creation: 0 disables, 1 (the default) stages when it
+ * pays, 2 forces every mode. */
 int sparsla_dcsr_xwin(const sparsla_dcsr* A, int64_t* out);
 
 /* y = A x (sparse.cpp:135-154): rows accumulated left to right from 0.0, separate

@@ -171,7 +171,8 @@ struct XwVariant {
                    (const void*)spmv_xw_kernel<SPMV_BICG_V, S, M, W, VS>, (const void*)spmv_xw_kernel<SPMV_BICG_T, S, M, W, VS>}}
 static const XwVariant kXwVariants[] = {XWV(1, 8, 3, 3), XWV(1, 8, 2, 4), XWV(1, 8, 3, 4),
                                         XWV(0, 8, 3, 2), XWV(0, 12, 3, 2), XWV(0, 12, 2, 3),
-                                        XWV(2, 8, 3, 3), XWV(2, 8, 2, 4), XWV(2, 8, 3, 4)};
+                                        XWV(2, 8, 3, 3), XWV(2, 8, 2, 4), XWV(2, 8, 3, 4),
+                                        XWV(1, 7, 3, 4), XWV(2, 7, 3, 4), XWV(0, 7, 2, 3)};
 #undef XWV
 constexpr int kNumXwVariants = sizeof(kXwVariants) / sizeof(kXwVariants[0]);
 
@@ -184,9 +185,13 @@ static size_t xw_smem_bytes(const DevCsr* A, int var, bool aux) {
 static void choose_xw_variants(DevCsr* A) {
     for (int d = 0; d < 3; ++d) A->xw_var[d] = -1;
     if (!A->xw) return;
-    A->xw_var[0] = 5;  // plain stream: 12-wide, 2 stages, 3 CTAs/SM (fastest on FEM and stencils)
-    A->xw_var[1] = 0;
-    A->xw_var[2] = 8;
+    // measured on B200 (tools/xw_sweep.py, profiles/r02_xwin.md): rows of <= 7 entries take the
+    // 7-wide kernels, whose warps of exactly-7-entry rows run the guard-free path; longer rows:
+    // plain 12-wide 2-stage 3 CTAs/SM, dictionary 8-wide 3 stages 3 CTAs/SM
+    const bool w7 = A->max_row <= 7;
+    A->xw_var[0] = w7 ? 11 : 5;
+    A->xw_var[1] = w7 ? 9 : 0;
+    A->xw_var[2] = w7 ? 10 : 8;
     if (const char* e = getenv("SPARSLA_XW_VARIANT")) {
         const int x = atoi(e);
         if (x >= 0 && x < kNumXwVariants) A->xw_var[kXwVariants[x].vs] = x;
@@ -757,10 +762,12 @@ static int vd_var_of(const DevCsr* A, int mode) {
 static void build_xw_pair(DevCsr* A) {
     cudaFree(A->xvo);
     A->xvo = nullptr;
-    // opt-in (SPARSLA_XW_PAIR=1): measured slower than the gather dictionary kernel at
-    // configs B / D' / E (profiles/r02_xwin.md)
+    // default for rows of <= 7 entries (the 7-wide guard-free kernel: config B SpMV 0.962 ->
+    // 0.840 ms); with longer rows the 8-wide pair kernel is slower than the gather dictionary
+    // kernel (profiles/r02_xwin.md).  SPARSLA_XW_PAIR=0 disables, =1 forces it.
     const char* pe = getenv("SPARSLA_XW_PAIR");
-    if (!pe || atoi(pe) == 0) return;
+    const int pm = pe ? atoi(pe) : -1;
+    if (pm == 0 || (pm < 0 && A->max_row > 7)) return;
     if (!A->xw || !A->vd || A->nvals > (1 << (16 - kXwPairBits)) || A->cap_x > (int)kXwPairMask - 15) return;
     if (A->xw_var[2] < 0) return;
     const long long m = A->nnz + kXwPad;
@@ -798,6 +805,7 @@ void devcsr_xwin_info(const DevCsr* A, int64_t* out) {
     out[2] = (int64_t)(A->xw_cover * 1e6 + 0.5);
     out[3] = 0;
     for (int m = 0; m < 4; ++m) out[3] |= (xw_pick(A, m) >= 0 ? 1 : 0) << m;
+    out[4] = xw_stream(A);
 }
 
 unsigned spmv_grid(const DevCsr* A, long long nch, int mode, bool xw_ok) {

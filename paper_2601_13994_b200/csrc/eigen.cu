@@ -342,6 +342,135 @@ __global__ void __launch_bounds__(kT) gram_kernel(const double* __restrict__ U, 
     if (tid == 0) *ticket = 0u;
 }
 
+// Warp-specialised Gram block (same result, same fixed grid and combination order as
+// gram_kernel): warp kGwConsumers is the producer — lane 0 streams the CTA's 64-row tiles
+// of U (and V) into a kGwStages-deep ring by TMA, re-arming a stage once every consumer warp
+// has released it (empty mbarrier) — and the consumer warps never meet at a CTA barrier
+// inside the tile loop.  gram_kernel's per-tile __syncthreads was its largest stall
+// (profiles/r02_lobpcg.md).
+constexpr int kGwConsumers = 7;  // + 1 producer warp = 256 threads: 2 CTAs/SM at <= 128 registers
+constexpr int kGwMaxStages = 8;
+__global__ void __launch_bounds__((kGwConsumers + 1) * 32, 2) gram_ws_kernel(const double* __restrict__ U,
+                                                                          const double* __restrict__ V, int ld,
+                                                                          Cols uc, Cols vc, long long n,
+                                                                          double* partial, unsigned* ticket,
+                                                                          double* out, int nst) {
+    constexpr int R = kTileR;
+    constexpr int NT = kGwConsumers * 32;
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem);  // [nst <= kGwMaxStages]
+    uint64_t* empty = full + kGwMaxStages;                // [nst]
+    int* s_uc = reinterpret_cast<int*>(smem + 256);
+    int* s_vc = s_uc + kMaxQ;
+    double* red = reinterpret_cast<double*>(smem + 512);
+    double* ring = red + kMaxQ * kMaxQ;
+    const bool two = U != V;
+    const size_t te = (size_t)kTR * ld, st_el = two ? 2 * te : te;
+    const int a = uc.n, b = vc.n, ab = a * b;
+    const int TI = (a + R - 1) / R, TJ = (b + R - 1) / R, tiles = TI * TJ;
+    const int ngroups = min(kTR, max(1, NT / tiles));
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int grp = tid / tiles, tt = tid - grp * tiles;
+    const bool act = warp < kGwConsumers && grp < ngroups;
+    const int ti = tt / TJ, tj = tt - ti * TJ;
+    stage_cols(uc, s_uc);
+    stage_cols(vc, s_vc);
+    const TileWalk<kTR> W(n, ld);
+    if (tid == 0) {
+        for (int s = 0; s < nst; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kGwConsumers);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (warp == kGwConsumers) {  // producer
+        if (lane == 0) {
+            for (long long j = 0; j < W.mine; ++j) {
+                const int s = (int)(j % nst);
+                mbar_wait(&empty[s], (uint32_t)(((j / nst) & 1) ^ 1));
+                W.issue(j, s, full, ring + s * st_el, U, two ? V : nullptr);
+            }
+        }
+    } else {
+        int cu[R], cv[R];
+#pragma unroll
+        for (int x = 0; x < R; ++x) {
+            cu[x] = ti * R + x < a ? s_uc[ti * R + x] : 0;
+            cv[x] = tj * R + x < b ? s_vc[tj * R + x] : 0;
+        }
+        double acc[R][R];
+#pragma unroll
+        for (int x = 0; x < R; ++x)
+#pragma unroll
+            for (int y = 0; y < R; ++y) acc[x][y] = 0.0;
+        for (long long j = 0; j < W.mine; ++j) {
+            const int s = (int)(j % nst);
+            mbar_wait(&full[s], (uint32_t)((j / nst) & 1));
+            const double* Ut = ring + s * st_el;
+            const double* Vt = two ? Ut + te : Ut;
+            const int nr = W.rows(j);
+            if (act) {
+                for (int r = grp; r < nr; r += ngroups) {
+                    double u[R], v[R];
+#pragma unroll
+                    for (int x = 0; x < R; ++x) u[x] = Ut[r * ld + cu[x]];
+#pragma unroll
+                    for (int y = 0; y < R; ++y) v[y] = Vt[r * ld + cv[y]];
+#pragma unroll
+                    for (int x = 0; x < R; ++x)
+#pragma unroll
+                        for (int y = 0; y < R; ++y) acc[x][y] = fma(u[x], v[y], acc[x][y]);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+        }
+        // consumers finished reading the ring: reuse it for the row-group combination
+        asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+        double* gbuf = ring;
+        if (act) {
+#pragma unroll
+            for (int x = 0; x < R; ++x)
+#pragma unroll
+                for (int y = 0; y < R; ++y) {
+                    const int i = ti * R + x, k = tj * R + y;
+                    if (i < a && k < b) gbuf[(size_t)grp * ab + i * b + k] = acc[x][y];
+                }
+        }
+    }
+    __syncthreads();
+    for (int e = tid; e < ab; e += blockDim.x) {
+        double sum = 0.0;
+        for (int g = 0; g < ngroups; ++g) sum += ring[(size_t)g * ab + e];
+        red[e] = sum;
+    }
+    __syncthreads();
+    for (int e = tid; e < ab; e += blockDim.x) partial[(size_t)blockIdx.x * ab + e] = red[e];
+    __shared__ int s_last;
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    const int P = gridDim.x;
+    for (int e = tid; e < ab; e += blockDim.x) {
+        double sum = 0.0;
+        int p = 0;
+        for (; p + 8 <= P; p += 8) {
+            double t[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) t[q] = __ldcg(partial + (size_t)(p + q) * ab + e);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) sum += t[q];
+        }
+        for (; p < P; ++p) sum += __ldcg(partial + (size_t)p * ab + e);
+        out[e] = sum;
+    }
+    if (tid == 0) *ticket = 0u;
+}
+
 // In-place block transform of whole rows: S[:, out_j] = sum_l S[:, in_l] M[l, j]
 // (a = in.n <= 48 inputs, c = out.n <= 32 outputs).  One thread per row (kTRa rows per
 // tile): the coefficients are warp-uniform constant-bank reads; the row's inputs are read
@@ -531,6 +660,23 @@ __global__ void __launch_bounds__(2 * TR) rr_apply_kernel(const double* S, const
 
 // The ring doubles as the row-group reduction buffer after the tile loop.
 int gram_stages(int, bool) { return kEStages; }  // deeper rings measured slower (profiles/)
+bool gram_ws_on() {
+    static const bool on = [] { const char* e = std::getenv("SPARSLA_GRAM_WS"); return !e || std::atoi(e) != 0; }();
+    return on;
+}
+// warp-specialised Gram: as many stages (<= 8) as fit two CTAs per SM (the fixed 296-CTA
+// grid is then one wave)
+int gram_ws_stages(int ld, bool two) {
+    const size_t per = (size_t)kTR * ld * 8 * (two ? 2 : 1);
+    const size_t room = 92 * 1024;
+    return (int)std::max<size_t>(2, std::min<size_t>(kGwMaxStages, room / per));
+}
+size_t gram_ws_smem(int ld, bool two, int a, int b) {
+    const int tiles = ((a + kTileR - 1) / kTileR) * ((b + kTileR - 1) / kTileR);
+    const int ngroups = std::min(kTR, std::max(1, kGwConsumers * 32 / std::max(1, tiles)));
+    const size_t ring = (size_t)gram_ws_stages(ld, two) * kTR * ld * 8 * (two ? 2 : 1);
+    return 512 + kMaxQ * kMaxQ * 8 + std::max(ring, (size_t)ngroups * a * b * 8);
+}
 size_t gram_smem(int ld, bool two, int a, int b) {
     const int tiles = ((a + kTileR - 1) / kTileR) * ((b + kTileR - 1) / kTileR);
     const int ngroups = std::min(kTR, std::max(1, kT / std::max(1, tiles)));
@@ -845,6 +991,7 @@ struct Lobpcg {
                                             optin - (int)fa.sharedSizeBytes), what);
         };
         allow((const void*)gram_kernel, "gram smem");
+        allow((const void*)gram_ws_kernel, "gram smem");
 #define SPARSLA_ALLOW(C) allow((const void*)apply_kernel<C>, "apply smem");
         SPARSLA_FOR_1_32(SPARSLA_ALLOW)
 #undef SPARSLA_ALLOW
@@ -869,8 +1016,12 @@ struct Lobpcg {
         const int ab = uc.n * vc.n;
         std::vector<double> G(ab, 0.0);
         if (ab == 0 || n == 0) return G;
-        gram_kernel<<<kRedCTAs, kT, gram_smem(ld, U != V, uc.n, vc.n), s>>>(U, V, ld, uc, vc, n, partial, ticket, gout,
-                                                                      gram_stages(ld, U != V));
+        if (gram_ws_on())
+            gram_ws_kernel<<<kRedCTAs, (kGwConsumers + 1) * 32, gram_ws_smem(ld, U != V, uc.n, vc.n), s>>>(
+                U, V, ld, uc, vc, n, partial, ticket, gout, gram_ws_stages(ld, U != V));
+        else
+            gram_kernel<<<kRedCTAs, kT, gram_smem(ld, U != V, uc.n, vc.n), s>>>(U, V, ld, uc, vc, n, partial, ticket,
+                                                                          gout, gram_stages(ld, U != V));
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(h_pin, gout, ab * sizeof(double), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));

@@ -234,7 +234,26 @@ __global__ void __launch_bounds__(kWsThreads, MINB) spmv_xw_kernel(SpmvParams P)
             };
             double y = 0.0;
             const bool all_staged = rps[kRpCopy + 1] != 0;  // round-uniform
-            if (all_staged && __all_sync(0xffffffffu, len <= W)) {
+            auto product = [&](int u) -> double {
+                if constexpr (PAIR) {
+                    const uint32_t e = xo[u];
+                    return __dmul_rn(s_vtab[e >> kXwPairBits], sx[e & kXwPairMask]);
+                } else {
+                    return __dmul_rn(value(u), sx[xo[u]]);
+                }
+            };
+            const bool exact = __all_sync(0xffffffffu, len == W || !live);  // warp-uniform
+            if (all_staged && exact) {
+                // every live row of the warp has exactly W entries (stencil interiors with
+                // the W = 7 variants): straight-line code, no per-entry guards (idle lanes
+                // read the round's first row, always staged, and discard the sum)
+                double pr[W];
+#pragma unroll
+                for (int u = 0; u < W; ++u) pr[u] = product(u);
+#pragma unroll
+                for (int u = 0; u < W; ++u) y = __dadd_rn(y, pr[u]);
+                if (!live) y = 0.0;
+            } else if (all_staged && __all_sync(0xffffffffu, len <= W)) {
                 // common case: every x operand of the round is in the staged windows (the
                 // per-entry guards stay branches: reading all W slots unconditionally was
                 // measured slower — shared-memory bandwidth, profiles/r02_xwin.md)

@@ -106,7 +106,7 @@ def run(args, metric, cfg):
     no, nh = info["n_owned"], info["n_halo"]
     xw = plan.xwin()
     kb = B.kernel_bytes(solver, no, nnz_local, nh, fmt["value_dict"], fmt["uniform_diag"], xw["modes"],
-                        xw["variant"] >= 6)
+                        xw["stream"] == 2)
     it_bytes = sum(x for _, x in kb)
     nnz_t = torch.tensor([nnz_local], dtype=torch.int64)
     dist.all_reduce(nnz_t)

@@ -287,10 +287,10 @@ class DeviceCsr:
     def xwin(self):
         """x-window staging: {variant (-1 = none), cap_x (elements per round), cover (fraction
         of entries whose x operand is staged), modes (SpMV modes that use it)}."""
-        out = np.zeros(4, np.int64)
+        out = np.zeros(5, np.int64)
         _check(lib().sparsla_dcsr_xwin(self.h, _p(out, _i64p)))
         return {"variant": int(out[0]), "cap_x": int(out[1]), "cover": out[2] / 1e6,
-                "modes": [m for m in range(4) if (int(out[3]) >> m) & 1]}
+                "modes": [m for m in range(4) if (int(out[3]) >> m) & 1], "stream": int(out[4])}
 
     def format(self):
         """SpMV storage format: value dictionary on / distinct values / constant Jacobi diagonal."""
@@ -967,10 +967,10 @@ class DistPlan:
 
     def xwin(self):
         """This rank's local-matrix x-window staging (see DeviceCsr.xwin)."""
-        out = np.zeros(4, np.int64)
+        out = np.zeros(5, np.int64)
         _check(lib().sparsla_dist_xwin(self.h, _p(out, _i64p)))
         return {"variant": int(out[0]), "cap_x": int(out[1]), "cover": out[2] / 1e6,
-                "modes": [m for m in range(4) if (int(out[3]) >> m) & 1]}
+                "modes": [m for m in range(4) if (int(out[3]) >> m) & 1], "stream": int(out[4])}
 
     def set_values(self, vals_local, mem=MEM_HOST):
         """Collective: new values of this rank's local matrix (local entry order)."""

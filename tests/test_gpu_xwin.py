@@ -11,7 +11,9 @@ from test_gpu_parity import _banded, assert_bitwise, random_csr, rep_eq, to_S
 
 pytestmark = pytest.mark.gpu
 
-N_XW_VARIANTS = 9  # kXwVariants in csrc/device.cu (0-2 dictionary, 3-5 plain, 6-8 pair)
+# kXwVariants in csrc/device.cu: value stream per variant (0 plain fp64, 1 dictionary, 2 pair)
+XW_STREAM = [1, 1, 1, 0, 0, 0, 2, 2, 2, 1, 2, 0]
+N_XW_VARIANTS = len(XW_STREAM)
 
 
 def _gen(O, case):
@@ -51,17 +53,18 @@ def _xwin_on(monkeypatch):
 
 def test_xwin_selection(S, O, gpu, monkeypatch):
     """SPARSLA_XWIN=1 (the default) stages stencil / mesh matrices (>= 90% of entries
-    staged) but not scattered columns unless forced (2); 0 disables.  The plain fp64 stream
-    uses it in every mode; with the 1-byte dictionary stream only BiCGStab's t-SpMV (mode 3)
-    takes it; the opt-in pair stream (SPARSLA_XW_PAIR=1: dictionary index inside the 16-bit
-    offset) in every mode."""
+    staged) but not scattered columns unless forced (2); 0 disables.  Rows of <= 7 entries
+    with <= 32 distinct values take the pair stream (dictionary index inside the 16-bit
+    offset) in every mode; the plain fp64 stream uses it in every mode; the separate 1-byte
+    dictionary stream (SPARSLA_XW_PAIR=0, or rows of 8 entries) only in BiCGStab's t-SpMV
+    (mode 3)."""
     P = to_S(S, O.generate("poisson3d", 40)).device(0)
     xw = P.xwin()
-    assert xw["variant"] in (0, 1, 2) and xw["cover"] >= 0.9 and 0 < xw["cap_x"] <= 2048, xw
-    assert P.format()["value_dict"] and xw["modes"] == [3], xw
-    monkeypatch.setenv("SPARSLA_XW_PAIR", "1")
+    assert XW_STREAM[xw["variant"]] == 2 and xw["cover"] >= 0.9 and 0 < xw["cap_x"] <= 2048, xw
+    assert P.format()["value_dict"] and xw["modes"] == [0, 1, 2, 3] and xw["stream"] == 2, xw
+    monkeypatch.setenv("SPARSLA_XW_PAIR", "0")
     xw = to_S(S, O.generate("poisson3d", 40)).device(0).xwin()
-    assert xw["variant"] >= 6 and xw["modes"] == [0, 1, 2, 3], xw
+    assert XW_STREAM[xw["variant"]] == 1 and xw["modes"] == [3] and xw["stream"] == 1, xw
     monkeypatch.delenv("SPARSLA_XW_PAIR")
     monkeypatch.setenv("SPARSLA_VALUE_DICT", "0")
     assert to_S(S, O.generate("poisson3d", 40)).device(0).xwin()["modes"] == [0, 1, 2, 3]
@@ -80,15 +83,15 @@ def test_xwin_selection(S, O, gpu, monkeypatch):
 @pytest.mark.parametrize("variant", range(N_XW_VARIANTS))
 @pytest.mark.parametrize("case", CASES)
 def test_xwin_spmv_bitwise(S, O, gpu, monkeypatch, case, variant):
-    if (variant < 3 or variant >= 6) and case in ("fem2d", "two_band"):
+    vs = XW_STREAM[variant]
+    if vs != 0 and case in ("fem2d", "two_band"):
         pytest.skip("no value dictionary (distinct values / rows > 8): dictionary variants unused")
     A = _gen(O, case)
     monkeypatch.setenv("SPARSLA_XWIN", "2")
     monkeypatch.setenv("SPARSLA_XW_VARIANT", str(variant))
-    if 3 <= variant < 6:
+    if vs == 0:
         monkeypatch.setenv("SPARSLA_VALUE_DICT", "0")
-    if variant >= 6:
-        monkeypatch.setenv("SPARSLA_XW_PAIR", "1")
+    monkeypatch.setenv("SPARSLA_XW_PAIR", "1" if vs == 2 else "0")
     D = to_S(S, A).device(0)
     assert D.xwin()["variant"] == variant, (D.xwin(), D.format())
     x = np.random.default_rng(3).standard_normal(A.ncols)
@@ -112,6 +115,8 @@ def _stream(monkeypatch, stream):
         monkeypatch.setenv("SPARSLA_VALUE_DICT", "0")
     elif stream == "pair":
         monkeypatch.setenv("SPARSLA_XW_PAIR", "1")
+    else:
+        monkeypatch.setenv("SPARSLA_XW_PAIR", "0")
 
 
 @pytest.mark.parametrize("stream", ["pair", "dict", "plain"])
@@ -161,9 +166,9 @@ def test_xwin_set_values_keeps_windows(S, O, gpu, monkeypatch):
     assert not D.format()["value_dict"] and D.xwin()["variant"] >= 0
     assert_bitwise(S.spmv(D, x), O.spmv(O.Csr(A.nrows, A.ncols, A.row_ptr, A.col_idx, v2), x))
     D.set_values(A.vals)
-    assert D.format()["value_dict"] and D.xwin()["variant"] >= 6  # pair stream rebuilt
+    assert D.format()["value_dict"] and XW_STREAM[D.xwin()["variant"]] == 2  # pair stream rebuilt
     assert_bitwise(S.spmv(D, x), O.spmv(A, x))
     v3 = np.where(A.vals < 0, -1.5, A.vals)  # new dictionary values, same pattern
     D.set_values(v3)
-    assert D.xwin()["variant"] >= 6
+    assert XW_STREAM[D.xwin()["variant"]] == 2
     assert_bitwise(S.spmv(D, x), O.spmv(O.Csr(A.nrows, A.ncols, A.row_ptr, A.col_idx, v3), x))

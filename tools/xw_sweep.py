@@ -18,6 +18,7 @@ from paper_2601_13994_b200 import sparsla as S  # noqa: E402
 
 PEAK = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
     if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
+XW_STREAM = [1, 1, 1, 0, 0, 0, 2, 2, 2, 1, 2, 0]  # value stream of kXwVariants (device.cu)
 CFG = {"B": ("poisson3d", 464, 0, 0.0, "cg"), "E": ("poisson3d", 368, 0, 0.0, "cg"),
        "D": ("convdiff3d", 368, 0, 0.1, "bicgstab"), "C": ("fem2d", 4474, 2601, 0.0, "cg")}
 
@@ -65,10 +66,10 @@ def main():
         run(name, arrays, "xwin-1", {"SPARSLA_XWIN": "1"})
         for var in variants or []:
             env = {"SPARSLA_XWIN": "2", "SPARSLA_XW_VARIANT": str(var)}
-            if 3 <= var < 6:
+            vs = XW_STREAM[var]
+            if vs == 0:
                 env["SPARSLA_VALUE_DICT"] = "0"
-            if var >= 6:
-                env["SPARSLA_XW_PAIR"] = "1"
+            env["SPARSLA_XW_PAIR"] = "1" if vs == 2 else "0"
             run(name, arrays, f"xwin-v{var}", env)
         if name != "C":  # plain CSR beside the dictionary
             run(name, arrays, "gather-plain", {"SPARSLA_XWIN": "0", "SPARSLA_VALUE_DICT": "0"})
