@@ -850,6 +850,8 @@ void launch_spmv_part(DevCsr* A, cudaStream_t s, int mode, const double* x, doub
     if (xv >= 0) {
         P.xw = A->xw;
         P.xwo = xw_stream(A) == 2 ? A->xvo : A->xwo;
+        static const int xpol = [] { const char* e = getenv("SPARSLA_XW_XPOL"); return e ? atoi(e) : 0; }();
+        P.xw_xpol = xpol;
         P.cap_x = A->cap_x;
         void* args[] = {&P};
         CK(cudaLaunchKernel(kXwVariants[xv].fn[mode], dim3(grid), dim3(kWsThreads), args,

@@ -114,6 +114,7 @@ __global__ void __launch_bounds__(kWsThreads, MINB) spmv_xw_kernel(SpmvParams P)
     if (warp == kConsumerWarps) {  // ------------------------------- producer warp ----
         if (lane == 0) {
             const uint64_t pol = P.l2_keep ? policy_evict_last() : policy_evict_first();
+            const uint64_t xpol = P.xw_xpol == 2 ? policy_evict_first() : policy_evict_last();
             constexpr uint32_t kDescBytes = kChunkRounds * kXwDescInts * 4;
             auto chunk_of = [&](long long c) { return P.chunk_list ? (long long)P.chunk_list[c] : P.chunk0 + c; };
             auto fetch_desc = [&](long long c, int b) {
@@ -173,7 +174,8 @@ __global__ void __launch_bounds__(kWsThreads, MINB) spmv_xw_kernel(SpmvParams P)
                     for (int w = 0; w < kXwMax; ++w) {
                         const uint32_t len = ((uint32_t)d[8 + w / 2] >> (16 * (w & 1))) & 0xffffu;
                         if (len) {
-                            bulk_g2s_plain(st + L.xoff + xo, P.x + d[w], len * 8u, &full[s]);
+                            if (P.xw_xpol == 0) bulk_g2s_plain(st + L.xoff + xo, P.x + d[w], len * 8u, &full[s]);
+                            else bulk_g2s(st + L.xoff + xo, P.x + d[w], len * 8u, &full[s], xpol);
                             xo += len * 8u;
                         }
                     }
