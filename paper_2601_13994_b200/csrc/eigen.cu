@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -886,7 +887,31 @@ void launch_spmm(const DevCsr* A, const double* X, int ldx, const Cols& in, doub
 // eigenvalues ascending in w and the matching orthonormal eigenvectors as the COLUMNS of
 // V (row-major q x q).  Quadratically convergent, accurate to working precision for the
 // small Rayleigh-Ritz and Gram problems of LOBPCG.
+// SPARSLA_EIG_TIMING=1: host-time breakdown of the LOBPCG driver (printed to stderr)
+struct EigTiming {
+    bool on = false;
+    double eig_s = 0, sync_s = 0;
+    long long eigs = 0, syncs = 0;
+    EigTiming() { const char* e = std::getenv("SPARSLA_EIG_TIMING"); on = e && std::atoi(e) != 0; }
+};
+EigTiming& eig_timing() { static EigTiming t; return t; }
+double now_s() { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); }
+
+void sym_eig_impl(int q, std::vector<double> A, std::vector<double>& w, std::vector<double>& V);
 void sym_eig(int q, std::vector<double> A, std::vector<double>& w, std::vector<double>& V) {
+    EigTiming& T = eig_timing();
+    const double t0 = T.on ? now_s() : 0.0;
+    sym_eig_impl(q, std::move(A), w, V);
+    if (T.on) { T.eig_s += now_s() - t0; ++T.eigs; }
+}
+void stream_sync_timed(cudaStream_t s) {
+    EigTiming& T = eig_timing();
+    const double t0 = T.on ? now_s() : 0.0;
+    CK(cudaStreamSynchronize(s));
+    if (T.on) { T.sync_s += now_s() - t0; ++T.syncs; }
+}
+
+void sym_eig_impl(int q, std::vector<double> A, std::vector<double>& w, std::vector<double>& V) {
     V.assign((size_t)q * q, 0.0);
     for (int i = 0; i < q; ++i) V[(size_t)i * q + i] = 1.0;
     auto a = [&](int i, int j) -> double& { return A[(size_t)i * q + j]; };
@@ -1024,7 +1049,7 @@ struct Lobpcg {
                                                                           gout, gram_stages(ld, U != V));
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(h_pin, gout, ab * sizeof(double), cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
+        stream_sync_timed(s);
         std::memcpy(G.data(), h_pin, ab * sizeof(double));
         return G;
     }
@@ -1168,7 +1193,7 @@ struct Lobpcg {
             CK(cudaGetLastError());
             const double* h = h_part;
             CK(cudaMemcpyAsync(h_part, partial, (size_t)g * m * sizeof(double), cudaMemcpyDeviceToHost, s));
-            CK(cudaStreamSynchronize(s));
+            stream_sync_timed(s);
             for (unsigned p = 0; p < g; ++p)
                 for (int j = 0; j < m; ++j) res[j] += h[(size_t)p * m + j];
             for (auto& v : res) v = std::sqrt(v);
@@ -1322,6 +1347,11 @@ void eig_smallest(DevCsr* A, int k, double tol, long long max_iter, uint64_t see
     o.iters = it;
     o.lam = lam;
     finish(L, k, tol, dinv, o, V);
+    if (eig_timing().on) {
+        EigTiming& T = eig_timing();
+        std::fprintf(stderr, "[eig timing] host sym_eig %.3f ms (%lld calls), stream syncs %.3f ms (%lld), iterations %lld\n",
+                     T.eig_s * 1e3, T.eigs, T.sync_s * 1e3, T.syncs, it);
+    }
     char buf[128];
     std::snprintf(buf, sizeof buf, "lobpcg: %lld iterations, block %d (k %d), %s", it, m, k,
                   o.all_conv ? "all pairs converged" : "not all pairs converged");

@@ -172,3 +172,38 @@ def test_xwin_set_values_keeps_windows(S, O, gpu, monkeypatch):
     D.set_values(v3)
     assert XW_STREAM[D.xwin()["variant"]] == 2
     assert_bitwise(S.spmv(D, x), O.spmv(O.Csr(A.nrows, A.ncols, A.row_ptr, A.col_idx, v3), x))
+
+
+@pytest.mark.parametrize("fused", [False, True])
+@pytest.mark.parametrize("stream", ["pair", "dict", "plain"])
+@pytest.mark.parametrize("kind,p1,P,part,solver", [("poisson3d", 24, 3, "contig", "cg"),
+                                                   ("convdiff3d", 20, 2, "contig", "bicgstab"),
+                                                   ("fem2d", 60, 4, "rcb", "cg")])
+def test_xwin_distributed_bitwise(S, O, gpu, monkeypatch, kind, p1, P, part, solver, stream, fused):
+    """Rank-local matrices ([owned | halo] columns) through the x-window kernels: interior
+    chunks while the halo is in flight (transport path) or the producer warp waiting for the
+    peers' halo pushes before staging a boundary round (fused peer-memory path) — bitwise
+    equal to the oracle's distributed solve."""
+    from test_gpu_dist import Ocsr, bits, make_plans, partition
+    if stream != "plain" and kind == "fem2d":
+        pytest.skip("FEM values are all distinct: no dictionary")
+    monkeypatch.setenv("SPARSLA_XWIN", "2")
+    _stream(monkeypatch, stream)
+    A = S.generate(kind, p1, 2601 if kind == "fem2d" else 0, 0.3 if kind == "convdiff3d" else 1.0)
+    po = partition(S, kind, p1, A, P, part)
+    hub, plans, owned = make_plans(S, A, po, P)
+    for p in plans:
+        xw = p.xwin()
+        assert xw["variant"] >= 0 and xw["modes"] == [0, 1, 2, 3], xw
+        assert xw["stream"] == {"plain": 0, "dict": 1, "pair": 2}[stream], xw
+        p.set_fused(fused)
+    b = np.ones(A.nrows)
+    opts = S.SolveOptions(atol=0.0, rtol=1e-9, max_iter=5000)
+    res = S.run_ranks(P, lambda r: (plans[r].cg if solver == "cg" else plans[r].bicgstab)(b[owned[r]], opts))
+    xd = np.empty(A.nrows)
+    for r in range(P):
+        xd[owned[r]] = res[r][0]
+    xo, ro, co = O.dist_solve(Ocsr(O, A), b, po, P, kind=solver, atol=0.0, rtol=1e-9, max_iter=5000)
+    rep = res[0][1]
+    assert rep.converged and rep.iterations == ro["iterations"], (rep, ro)
+    assert np.array_equal(bits(xd), bits(xo))
