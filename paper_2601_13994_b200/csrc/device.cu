@@ -755,9 +755,9 @@ static int vd_var_of(const DevCsr* A, int mode) {
     return (mode == SPMV_BICG_T && A->vd_var == 3 && !t7) ? 0 : A->vd_var;
 }
 
-// pair stream: the dictionary index in the top 5 bits of the 16-bit window offset (one
-// 2-byte stream per entry instead of 1 + 2 bytes); needs <= 32 distinct values and
-// <= 2032 staged elements per round.  Rebuilt on the device whenever the dictionary is.
+// pair stream: the dictionary index in the low 3 bits of the 16-bit window offset (one
+// 2-byte stream per entry instead of 1 + 2 bytes); needs <= 8 distinct values and
+// <= 8176 staged elements per round.  Rebuilt on the device whenever the dictionary is.
 // Same products in the same order: bit-identical to the other streams.
 static void build_xw_pair(DevCsr* A) {
     cudaFree(A->xvo);
@@ -768,7 +768,7 @@ static void build_xw_pair(DevCsr* A) {
     const char* pe = getenv("SPARSLA_XW_PAIR");
     const int pm = pe ? atoi(pe) : -1;
     if (pm == 0 || (pm < 0 && A->max_row > 7)) return;
-    if (!A->xw || !A->vd || A->nvals > (1 << (16 - kXwPairBits)) || A->cap_x > (int)kXwPairMask - 15) return;
+    if (!A->xw || !A->vd || A->nvals > (1 << kXwPairValBits) || A->cap_x > (int)kXwPairNone - 15) return;
     if (A->xw_var[2] < 0) return;
     const long long m = A->nnz + kXwPad;
     A->xvo = dalloc<uint16_t>(m);
@@ -850,8 +850,6 @@ void launch_spmv_part(DevCsr* A, cudaStream_t s, int mode, const double* x, doub
     if (xv >= 0) {
         P.xw = A->xw;
         P.xwo = xw_stream(A) == 2 ? A->xvo : A->xwo;
-        static const int xpol = [] { const char* e = getenv("SPARSLA_XW_XPOL"); return e ? atoi(e) : 0; }();
-        P.xw_xpol = xpol;
         P.cap_x = A->cap_x;
         void* args[] = {&P};
         CK(cudaLaunchKernel(kXwVariants[xv].fn[mode], dim3(grid), dim3(kWsThreads), args,

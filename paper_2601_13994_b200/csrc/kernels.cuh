@@ -520,7 +520,6 @@ struct SpmvParams {
     const double* vtab;   // ... into this table of the matrix's <= 256 distinct values
     int cap_v, cap_c;   // staged capacities (elements) per round
     int l2_keep;        // 1: matrix stream evict_last (working set fits L2), 0: evict_first
-    int xw_xpol;        // x-window kernels: L2 policy of the x windows (0 normal, 1 evict_last, 2 evict_first)
     int check_done;
     const uint32_t* long_bits;  // rows summed by spmv_longrow_kernel (empty in this view): bit set
     const int32_t* xw;    // x-window kernels (spmv_xw.cuh): per-round window descriptors

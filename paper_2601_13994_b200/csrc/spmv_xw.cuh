@@ -28,9 +28,12 @@ constexpr int kXwDescInts = 16; // per-round descriptor (64 B):
 //   [rs, re) lie inside one window (CG's p.q operand), else -1      [15] 1: every entry of
 //   the round is staged (the consumer skips the per-entry fallback test)
 constexpr uint16_t kXwNone = 0xFFFFu;
-// pair stream: (dictionary index << 11) | window offset; offset 0x7FF = not staged
-constexpr int kXwPairBits = 11;
-constexpr uint32_t kXwPairMask = (1u << kXwPairBits) - 1u;
+// pair stream: (window offset << 3) | dictionary index (<= 8 values); offset 0x1FFF = not
+// staged.  With the index in the low bits, e & ~7 is the byte offset of x in the staged
+// windows and (e & 7) * 8 the byte offset of the value in the table: one mask per address.
+constexpr int kXwPairValBits = 3;
+constexpr uint32_t kXwPairValMask = (1u << kXwPairValBits) - 1u;
+constexpr uint32_t kXwPairNone = 0xFFFFu >> kXwPairValBits;  // offset field of an unstaged entry
 
 // pair stream from the dictionary indices and the window offsets (device, after every
 // dictionary (re)build)
@@ -38,9 +41,10 @@ static __global__ void xw_pair_kernel(const uint8_t* vidx, const uint16_t* xwo, 
     const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= m) return;
     const uint32_t o = xwo[k];
-    xvo[k] = (uint16_t)(((uint32_t)vidx[k] << kXwPairBits) | (o == kXwNone ? kXwPairMask : o));
+    xvo[k] = (uint16_t)(((o == kXwNone ? kXwPairNone : o) << kXwPairValBits) | vidx[k]);
 }
 constexpr int kXwPad = 32;  // offsets past the last entry (bulk-copy granule slack)
+
 
 __device__ __forceinline__ void fence_proxy_async_global() {
     asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -112,73 +116,83 @@ __global__ void __launch_bounds__(kWsThreads, MINB) spmv_xw_kernel(SpmvParams P)
     __syncthreads();
 
     if (warp == kConsumerWarps) {  // ------------------------------- producer warp ----
-        if (lane == 0) {
-            const uint64_t pol = P.l2_keep ? policy_evict_last() : policy_evict_first();
-            const uint64_t xpol = P.xw_xpol == 2 ? policy_evict_first() : policy_evict_last();
-            constexpr uint32_t kDescBytes = kChunkRounds * kXwDescInts * 4;
-            auto chunk_of = [&](long long c) { return P.chunk_list ? (long long)P.chunk_list[c] : P.chunk0 + c; };
-            auto fetch_desc = [&](long long c, int b) {
-                mbar_arrive_expect_tx(&dbar[b], kDescBytes);
-                bulk_g2s(dbuf + b * kChunkRounds * kXwDescInts, P.xw + chunk_of(c) * kChunkRounds * kXwDescInts,
-                         kDescBytes, &dbar[b], pol);
-            };
-            if ((long long)blockIdx.x < P.nch) fetch_desc(blockIdx.x, 0);
-            bool halo_ok = P.p2p == nullptr;
-            long long g = 0;
-            int ci = 0;
-            for (long long c = blockIdx.x; c < P.nch; c += gridDim.x, ++ci) {
-                const int b = ci & 1;
-                if (c + gridDim.x < P.nch) {  // one chunk ahead (buffer b^1 was read last chunk)
-                    fence_proxy_async_smem();
-                    fetch_desc(c + gridDim.x, b ^ 1);
-                }
-                if (!halo_ok && c >= P.n_interior) {
-                    // the boundary rounds' x windows include halo values pushed by the peers:
-                    // wait for them, then order the async-proxy reads after the acquire
+        // Lane-parallel issue: per round, lanes 0-7 copy the x windows (one each), lane 8 the
+        // row_ptr segment, lane 9 the value stream, lane 10 the offset stream, lane 11 the
+        // epilogue vector segment — one SIMT bulk-copy instruction instead of ~8 serial ones
+        // (the producer sits on the critical path: a few extra scalar instructions per
+        // window measurably slowed the kernel).
+        const uint64_t pol = P.l2_keep ? policy_evict_last() : policy_evict_first();
+        constexpr uint32_t kDescBytes = kChunkRounds * kXwDescInts * 4;
+        auto chunk_of = [&](long long c) { return P.chunk_list ? (long long)P.chunk_list[c] : P.chunk0 + c; };
+        auto fetch_desc = [&](long long c, int b) {
+            mbar_arrive_expect_tx(&dbar[b], kDescBytes);
+            bulk_g2s(dbuf + b * kChunkRounds * kXwDescInts, P.xw + chunk_of(c) * kChunkRounds * kXwDescInts,
+                     kDescBytes, &dbar[b], pol);
+        };
+        if (lane == 0 && (long long)blockIdx.x < P.nch) fetch_desc(blockIdx.x, 0);
+        bool halo_ok = P.p2p == nullptr;
+        long long g = 0;
+        int ci = 0;
+        for (long long c = blockIdx.x; c < P.nch; c += gridDim.x, ++ci) {
+            const int b = ci & 1;
+            if (lane == 0 && c + gridDim.x < P.nch) {  // one chunk ahead (buffer b^1 was read last chunk)
+                fence_proxy_async_smem();
+                fetch_desc(c + gridDim.x, b ^ 1);
+            }
+            if (!halo_ok && c >= P.n_interior) {
+                // the boundary rounds' x windows include halo values pushed by the peers:
+                // wait for them, then order the async-proxy reads after the acquire
+                if (lane == 0) {
                     p2p_wait_halo(P.p2p, P.halo_v, P.red.st->ep_halo[P.halo_v]);
                     fence_proxy_async_global();
-                    halo_ok = true;
                 }
-                mbar_wait(&dbar[b], (uint32_t)((ci >> 1) & 1));
-                const long long base = chunk_of(c) * kChunk;
-                const long long rem = (P.n - base + kChunkSlots - 1) / kChunkSlots;
-                const int nr = rem < kChunkRounds ? (int)rem : kChunkRounds;
-                for (int r = 0; r < nr; ++r, ++g) {
-                    const int s = (int)(g % STG);
-                    const int32_t* d = dbuf + (b * kChunkRounds + r) * kXwDescInts;
-                    const long long rs = base + (long long)r * kChunkSlots;
-                    const long long re = min(rs + kChunkSlots, P.n);
-                    const int nz0 = d[12], nz1 = d[13];
-                    const int a0 = nz0 & ~(VALIGN - 1), a1 = (nz1 + VALIGN - 1) & ~(VALIGN - 1);
-                    const int o0 = nz0 & ~7, o1 = (nz1 + 7) & ~7;
-                    const uint32_t vb = PAIR ? 0u : (uint32_t)(a1 - a0) * (VD ? 1u : 8u);
-                    const uint32_t ob = (uint32_t)(o1 - o0) * 2u;
-                    uint32_t xb = 0;
+                __syncwarp();
+                halo_ok = true;
+            }
+            mbar_wait(&dbar[b], (uint32_t)((ci >> 1) & 1));
+            const long long base = chunk_of(c) * kChunk;
+            const long long rem = (P.n - base + kChunkSlots - 1) / kChunkSlots;
+            const int nr = rem < kChunkRounds ? (int)rem : kChunkRounds;
+            for (int r = 0; r < nr; ++r, ++g) {
+                const int s = (int)(g % STG);
+                const int32_t* d = dbuf + (b * kChunkRounds + r) * kXwDescInts;
+                const long long rs = base + (long long)r * kChunkSlots;
+                // this lane's window (lanes 0-7) and its offset in the staged x: shuffle scan
+                const uint32_t wlen = lane < kXwMax ? ((uint32_t)d[8 + lane / 2] >> (16 * (lane & 1))) & 0xffffu : 0u;
+                uint32_t incl = wlen;
 #pragma unroll
-                    for (int w = 0; w < kXwMax; ++w) xb += ((uint32_t)d[8 + w / 2] >> (16 * (w & 1)) & 0xffffu) * 8u;
-                    const uint32_t ab = AUX ? (uint32_t)((re - rs) & ~1LL) * 8u : 0u;
-                    mbar_wait(&empty[s], (uint32_t)(((g / STG) & 1) ^ 1));
-                    unsigned char* st = stage0 + s * L.stage;
+                for (int o = 1; o < kXwMax; o <<= 1) {
+                    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += v;
+                }
+                const uint32_t xb = __shfl_sync(0xffffffffu, incl, kXwMax - 1) * 8u;
+                const int nz0 = d[12], nz1 = d[13];
+                const int a0 = nz0 & ~(VALIGN - 1), a1 = (nz1 + VALIGN - 1) & ~(VALIGN - 1);
+                const int o0 = nz0 & ~7, o1 = (nz1 + 7) & ~7;
+                const uint32_t vb = PAIR ? 0u : (uint32_t)(a1 - a0) * (VD ? 1u : 8u);
+                const uint32_t ob = (uint32_t)(o1 - o0) * 2u;
+                const uint32_t ab = AUX ? (uint32_t)((min(rs + kChunkSlots, P.n) - rs) & ~1LL) * 8u : 0u;
+                mbar_wait(&empty[s], (uint32_t)(((g / STG) & 1) ^ 1));
+                unsigned char* st = stage0 + s * L.stage;
+                if (lane == 0) {
                     reinterpret_cast<int32_t*>(st + L.roff)[kRpCopy] = d[14];      // staged x[rs] offset
                     reinterpret_cast<int32_t*>(st + L.roff)[kRpCopy + 1] = d[15];  // every entry staged
                     mbar_arrive_expect_tx(&full[s], (uint32_t)(kRpCopy * 4) + vb + ob + xb + ab);
+                }
+                __syncwarp();
+                if (lane < kXwMax) {
+                    if (wlen) bulk_g2s_plain(st + L.xoff + (incl - wlen) * 8u, P.x + d[lane], wlen * 8u, &full[s]);
+                } else if (lane == kXwMax) {
                     bulk_g2s(st + L.roff, P.rp + rs, kRpCopy * 4, &full[s], pol);
+                } else if (lane == kXwMax + 1) {
                     if constexpr (VD) {
                         if (vb) bulk_g2s(st, P.vidx + a0, vb, &full[s], pol);
                     } else {
                         if (vb) bulk_g2s(st, P.val + a0, vb, &full[s], pol);
                     }
+                } else if (lane == kXwMax + 2) {
                     if (ob) bulk_g2s(st + L.ooff, P.xwo + o0, ob, &full[s], pol);
-                    uint32_t xo = 0;
-#pragma unroll
-                    for (int w = 0; w < kXwMax; ++w) {
-                        const uint32_t len = ((uint32_t)d[8 + w / 2] >> (16 * (w & 1))) & 0xffffu;
-                        if (len) {
-                            if (P.xw_xpol == 0) bulk_g2s_plain(st + L.xoff + xo, P.x + d[w], len * 8u, &full[s]);
-                            else bulk_g2s(st + L.xoff + xo, P.x + d[w], len * 8u, &full[s], xpol);
-                            xo += len * 8u;
-                        }
-                    }
+                } else if (lane == kXwMax + 3) {
                     if constexpr (AUX)
                         if (ab) bulk_g2s(st + L.aoff, P.aux + rs, ab, &full[s], pol);
                 }
@@ -221,14 +235,14 @@ __global__ void __launch_bounds__(kWsThreads, MINB) spmv_xw_kernel(SpmvParams P)
             const uint8_t* vp = A + (kb - (o0 & ~(VALIGN - 1)));
             const double* vs = reinterpret_cast<const double*>(A) + (kb - (o0 & ~(VALIGN - 1)));
             auto value = [&](int u) -> double {
-                if constexpr (PAIR) return s_vtab[xo[u] >> kXwPairBits];
+                if constexpr (PAIR) return s_vtab[xo[u] & kXwPairValMask];
                 else if constexpr (VD) return s_vtab[vp[u]];
                 else return vs[u];
             };
             auto xval = [&](int u) -> double {
                 if constexpr (PAIR) {
-                    const uint32_t o = xo[u] & kXwPairMask;
-                    return o != kXwPairMask ? sx[o] : __ldg(P.x + __ldg(P.ci + kb + u));
+                    const uint32_t o = (uint32_t)xo[u] >> kXwPairValBits;
+                    return o != kXwPairNone ? sx[o] : __ldg(P.x + __ldg(P.ci + kb + u));
                 } else {
                     const uint32_t o = xo[u];
                     return o != kXwNone ? sx[o] : __ldg(P.x + __ldg(P.ci + kb + u));
@@ -239,7 +253,7 @@ __global__ void __launch_bounds__(kWsThreads, MINB) spmv_xw_kernel(SpmvParams P)
             auto product = [&](int u) -> double {
                 if constexpr (PAIR) {
                     const uint32_t e = xo[u];
-                    return __dmul_rn(s_vtab[e >> kXwPairBits], sx[e & kXwPairMask]);
+                    return __dmul_rn(s_vtab[e & kXwPairValMask], sx[e >> kXwPairValBits]);
                 } else {
                     return __dmul_rn(value(u), sx[xo[u]]);
                 }
@@ -265,7 +279,7 @@ __global__ void __launch_bounds__(kWsThreads, MINB) spmv_xw_kernel(SpmvParams P)
                     if (u < len) {
                         if constexpr (PAIR) {
                             const uint32_t e = xo[u];
-                            pr[u] = __dmul_rn(s_vtab[e >> kXwPairBits], sx[e & kXwPairMask]);
+                            pr[u] = __dmul_rn(s_vtab[e & kXwPairValMask], sx[e >> kXwPairValBits]);
                         } else {
                             pr[u] = __dmul_rn(value(u), sx[xo[u]]);
                         }
