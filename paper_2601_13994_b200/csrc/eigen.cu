@@ -926,6 +926,17 @@ void sym_eig_impl(int q, std::vector<double> A, std::vector<double>& w, std::vec
             for (int r = p + 1; r < q; ++r) {
                 const double apr = a(p, r);
                 if (apr == 0.0) continue;
+                // after the first sweeps, an element too small to change either diagonal
+                // entry in floating point is zeroed without a rotation (the classic cyclic
+                // Jacobi threshold rule): the converged sweeps cost O(q^2) instead of O(q^3)
+                if (sweep >= 3) {
+                    const double g = 100.0 * std::fabs(apr);
+                    if (std::fabs(a(p, p)) + g == std::fabs(a(p, p)) && std::fabs(a(r, r)) + g == std::fabs(a(r, r))) {
+                        a(p, r) = 0.0;
+                        a(r, p) = 0.0;
+                        continue;
+                    }
+                }
                 const double theta = (a(r, r) - a(p, p)) / (2.0 * apr);
                 const double t = (theta >= 0 ? 1.0 : -1.0) / (std::fabs(theta) + std::sqrt(theta * theta + 1.0));
                 const double c = 1.0 / std::sqrt(t * t + 1.0), s = t * c;
