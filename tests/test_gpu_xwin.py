@@ -54,7 +54,7 @@ def _xwin_on(monkeypatch):
 def test_xwin_selection(S, O, gpu, monkeypatch):
     """SPARSLA_XWIN=1 (the default) stages stencil / mesh matrices (>= 90% of entries
     staged) but not scattered columns unless forced (2); 0 disables.  Rows of <= 7 entries
-    with <= 32 distinct values take the pair stream (dictionary index inside the 16-bit
+    with <= 8 distinct values take the pair stream (dictionary index inside the 16-bit
     offset) in every mode; the plain fp64 stream uses it in every mode; the separate 1-byte
     dictionary stream (SPARSLA_XW_PAIR=0, or rows of 8 entries) only in BiCGStab's t-SpMV
     (mode 3)."""
