@@ -192,34 +192,46 @@ __device__ __forceinline__ void block_tree(double (&v)[NDOT], double* sred) {
 }
 
 // Level-2 reduction over m chunk partials per dot (layout [NDOT][m]); called by every
-// thread of the last CTA; result valid on thread 0.
+// thread of the last CTA; result valid on thread 0.  Slot s sums partials s, s + 1024, ...
+// from 0.0 in that order; the loop walks the 1024-wide rows of partials so that every slot
+// of every dot of this thread has its next load in flight at once (one L2 round trip per
+// row instead of one per four partials of one slot — this tail runs on a single CTA after
+// the whole grid, so its latency is on the iteration's critical path).
 template <int NT, int NDOT, int BAR = 0>
 __device__ void final_reduce(const double* partials, long long m, double (&out)[NDOT], double* sred) {
     constexpr int SPT = kFinalSlots / NT;  // consecutive slots per thread
     const int t = threadIdx.x;
+    double s[NDOT][SPT];
+#pragma unroll
+    for (int d = 0; d < NDOT; ++d)
+#pragma unroll
+        for (int j = 0; j < SPT; ++j) s[d][j] = 0.0;
+    const long long rows = m / kFinalSlots;  // complete rows of 1024 partials
+    const double* P0 = partials + (long long)t * SPT;
+    for (long long c = 0; c < rows; ++c) {
+        double a[NDOT][SPT];
+#pragma unroll
+        for (int d = 0; d < NDOT; ++d)
+#pragma unroll
+            for (int j = 0; j < SPT; ++j) a[d][j] = __ldcg(P0 + d * m + c * kFinalSlots + j);
+#pragma unroll
+        for (int d = 0; d < NDOT; ++d)
+#pragma unroll
+            for (int j = 0; j < SPT; ++j) s[d][j] = __dadd_rn(s[d][j], a[d][j]);
+    }
+    const long long tail = m - rows * kFinalSlots;  // last, partial row
+#pragma unroll
+    for (int d = 0; d < NDOT; ++d)
+#pragma unroll
+        for (int j = 0; j < SPT; ++j)
+            if ((long long)t * SPT + j < tail) s[d][j] = __dadd_rn(s[d][j], __ldcg(P0 + d * m + rows * kFinalSlots + j));
 #pragma unroll
     for (int d = 0; d < NDOT; ++d) {
-        const double* P = partials + d * m;
-        double s[SPT];
-#pragma unroll
-        for (int j = 0; j < SPT; ++j) {
-            const long long slot = (long long)t * SPT + j;
-            double acc = 0.0;
-            long long c = slot;
-            for (; c + 3 * kFinalSlots < m; c += 4 * kFinalSlots) {
-                const double a0 = __ldcg(P + c), a1 = __ldcg(P + c + kFinalSlots);
-                const double a2 = __ldcg(P + c + 2 * kFinalSlots), a3 = __ldcg(P + c + 3 * kFinalSlots);
-                acc = __dadd_rn(acc, a0); acc = __dadd_rn(acc, a1);
-                acc = __dadd_rn(acc, a2); acc = __dadd_rn(acc, a3);
-            }
-            for (; c < m; c += kFinalSlots) acc = __dadd_rn(acc, __ldcg(P + c));
-            s[j] = acc;
-        }
 #pragma unroll
         for (int w = 1; w < SPT; w *= 2)
 #pragma unroll
-            for (int i = 0; i + w < SPT; i += 2 * w) s[i] = __dadd_rn(s[i], s[i + w]);
-        out[d] = s[0];
+            for (int i = 0; i + w < SPT; i += 2 * w) s[d][i] = __dadd_rn(s[d][i], s[d][i + w]);
+        out[d] = s[d][0];
     }
     block_tree<NT, NDOT, BAR>(out, sred);
 }
