@@ -208,16 +208,29 @@ __device__ void final_reduce(const double* partials, long long m, double (&out)[
         for (int j = 0; j < SPT; ++j) s[d][j] = 0.0;
     const long long rows = m / kFinalSlots;  // complete rows of 1024 partials
     const double* P0 = partials + (long long)t * SPT;
-    for (long long c = 0; c < rows; ++c) {
-        double a[NDOT][SPT];
+    // two rows per step when the loads fit the register budget (same per-slot order)
+    constexpr int RR = NDOT * SPT <= 8 ? 2 : 1;
+    long long c = 0;
+    for (; c + RR <= rows; c += RR) {
+        double a[RR][NDOT][SPT];
+#pragma unroll
+        for (int q = 0; q < RR; ++q)
+#pragma unroll
+            for (int d = 0; d < NDOT; ++d)
+#pragma unroll
+                for (int j = 0; j < SPT; ++j) a[q][d][j] = __ldcg(P0 + d * m + (c + q) * kFinalSlots + j);
+#pragma unroll
+        for (int q = 0; q < RR; ++q)
+#pragma unroll
+            for (int d = 0; d < NDOT; ++d)
+#pragma unroll
+                for (int j = 0; j < SPT; ++j) s[d][j] = __dadd_rn(s[d][j], a[q][d][j]);
+    }
+    for (; c < rows; ++c) {
 #pragma unroll
         for (int d = 0; d < NDOT; ++d)
 #pragma unroll
-            for (int j = 0; j < SPT; ++j) a[d][j] = __ldcg(P0 + d * m + c * kFinalSlots + j);
-#pragma unroll
-        for (int d = 0; d < NDOT; ++d)
-#pragma unroll
-            for (int j = 0; j < SPT; ++j) s[d][j] = __dadd_rn(s[d][j], a[d][j]);
+            for (int j = 0; j < SPT; ++j) s[d][j] = __dadd_rn(s[d][j], __ldcg(P0 + d * m + c * kFinalSlots + j));
     }
     const long long tail = m - rows * kFinalSlots;  // last, partial row
 #pragma unroll
