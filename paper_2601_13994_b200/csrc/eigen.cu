@@ -29,6 +29,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <numeric>
 #include <string>
 #include <vector>
@@ -75,6 +76,19 @@ struct Vec16 {
     double v[kMaxK];
 };
 
+// Coefficient matrices of the block transforms live in constant memory (warp-uniform
+// broadcast reads, usable as direct FMA operands): the host path copies them in before each
+// launch, the device-resident iteration copies them from the small-problem kernels' output
+// with device-to-device memcpy nodes of the captured graph.  One LOBPCG runs at a time per
+// process (eig_mutex).
+__constant__ double c_coef[kMaxQ * 2 * kMaxK];  // apply_kernel: a x C (row-major)
+__constant__ double c_rrC[kMaxQ * kMaxK];       // rr_apply_kernel: q x m
+__constant__ double c_rrlam[kMaxK];             // rr_apply_kernel: the m Ritz values
+
+// device-resident iteration: kernels of a captured iteration exit at entry once the solve
+// has stopped (or this step is skipped)
+__device__ __forceinline__ bool halted(const int* stop) { return stop && *(volatile const int*)stop; }
+
 __host__ __device__ inline uint64_t splitmix64(uint64_t z) {
     z += 0x9e3779b97f4a7c15ULL;
     z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
@@ -115,7 +129,8 @@ template <int NW, bool VEC>
 __global__ void __launch_bounds__(kT) spmm_kernel(const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
                                                   const double* __restrict__ val, long long n,
                                                   const double* __restrict__ S, int lds, Cols in, double* Y,
-                                                  int ldy, Cols out) {
+                                                  int ldy, Cols out, const int* stop) {
+    if (halted(stop)) return;
     __shared__ int s_in[kMaxQ], s_out[kMaxQ];
     stage_cols(in, s_in);
     stage_cols(out, s_out);
@@ -165,7 +180,8 @@ template <int NW>
 __global__ void __launch_bounds__(kT) spmm_lanes_kernel(const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
                                                         const double* __restrict__ val, long long n,
                                                         const double* __restrict__ S, int lds, int c_in,
-                                                        double* Y, int ldy, int c_out) {
+                                                        double* Y, int ldy, int c_out, const int* stop) {
+    if (halted(stop)) return;
     constexpr int L = NW / 2, RPW = 32 / L;
     const int lane = threadIdx.x & 31, sub = lane / L, part = lane - sub * L;
     const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -237,7 +253,8 @@ struct TileWalk {
 // The grid is fixed (kRedCTAs), so the result is deterministic and device-independent.
 __global__ void __launch_bounds__(kT) gram_kernel(const double* __restrict__ U, const double* __restrict__ V, int ld,
                                                   Cols uc, Cols vc, long long n, double* partial,
-                                                  unsigned* ticket, double* out, int nst) {
+                                                  unsigned* ticket, double* out, int nst, const int* stop) {
+    if (halted(stop)) return;
     constexpr int R = kTileR;
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem);  // [nst <= 8]
@@ -355,7 +372,8 @@ __global__ void __launch_bounds__((kGwConsumers + 1) * 32, 2) gram_ws_kernel(con
                                                                           const double* __restrict__ V, int ld,
                                                                           Cols uc, Cols vc, long long n,
                                                                           double* partial, unsigned* ticket,
-                                                                          double* out, int nst) {
+                                                                          double* out, int nst, const int* stop) {
+    if (halted(stop)) return;
     constexpr int R = kTileR;
     constexpr int NT = kGwConsumers * 32;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -477,8 +495,13 @@ __global__ void __launch_bounds__((kGwConsumers + 1) * 32, 2) gram_ws_kernel(con
 // tile): the coefficients are warp-uniform constant-bank reads; the row's inputs are read
 // from the staged tile before its outputs are written back into it, then the whole rows
 // are bulk-stored.
-template <int C>
-__global__ void __launch_bounds__(kTRa) apply_kernel(double* S, int ld, Cols in, Cols out, long long n, const Mat M) {
+// DEV: coefficients from the c_coef symbol (device-resident iteration) instead of the
+// kernel parameter M (host driver)
+template <int C, bool DEV>
+__global__ void __launch_bounds__(kTRa) apply_kernel(double* S, int ld, Cols in, Cols out, long long n,
+                                                     const Mat M, const int* stop) {
+    if (halted(stop)) return;
+    const double* Mc = DEV ? c_coef : M.v;
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
     int* s_in = reinterpret_cast<int*>(smem + 64);
@@ -509,7 +532,7 @@ __global__ void __launch_bounds__(kTRa) apply_kernel(double* S, int ld, Cols in,
             for (int q = 0; q < C; ++q) acc[q] = 0.0;
             for (int l = 0; l < a; ++l) {  // warp-uniform coefficient row l
                 const double u = t[s_in[l]];
-                const double* Ml = M.v + l * C;
+                const double* Ml = Mc + l * C;
 #pragma unroll
                 for (int q = 0; q < C; ++q) acc[q] = fma(u, Ml[q], acc[q]);
             }
@@ -539,11 +562,14 @@ __global__ void __launch_bounds__(kTRa) apply_kernel(double* S, int ld, Cols in,
 // before they are read).
 constexpr int kRRStages = 2;
 constexpr int kHalfK = kMaxK / 2;
-template <int TR>
+template <int TR, bool DEV>
 __global__ void __launch_bounds__(2 * TR) rr_apply_kernel(const double* S, const double* AS, double* Sn, double* ASn,
                                                           int ld, Cols B, int m, long long n, const Mat C,
-                                                          const Vec16 lam, const double* __restrict__ dinv,
-                                                          double* rpart) {
+                                                          const Vec16 lam, const int* stop,
+                                                          const double* __restrict__ dinv, double* rpart) {
+    if (halted(stop)) return;
+    const double* Cc = DEV ? c_rrC : C.v;
+    const double* lamc = DEV ? c_rrlam : lam.v;
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
     int* s_b = reinterpret_cast<int*>(smem + 64);
@@ -557,7 +583,7 @@ __global__ void __launch_bounds__(2 * TR) rr_apply_kernel(const double* S, const
     const int row = threadIdx.x >> 1, half = threadIdx.x & 1;
     double lk[kHalfK];  // lambda of this thread's columns (constant-index parameter reads)
 #pragma unroll
-    for (int i = 0; i < kHalfK; ++i) lk[i] = half ? lam.v[2 * i + 1] : lam.v[2 * i];
+    for (int i = 0; i < kHalfK; ++i) lk[i] = half ? lamc[2 * i + 1] : lamc[2 * i];
     double racc[kHalfK];  // ||R_k||^2 of this thread's columns over its rows
 #pragma unroll
     for (int i = 0; i < kHalfK; ++i) racc[i] = 0.0;
@@ -586,8 +612,8 @@ __global__ void __launch_bounds__(2 * TR) rr_apply_kernel(const double* S, const
                 for (int i = 0; i < kHalfK; ++i) {
                     const int k = half + 2 * i;
                     if (k < m) {
-                        xs[i] = fma(u, C.v[l * m + k], xs[i]);
-                        xa[i] = fma(v, C.v[l * m + k], xa[i]);
+                        xs[i] = fma(u, Cc[l * m + k], xs[i]);
+                        xa[i] = fma(v, Cc[l * m + k], xa[i]);
                     }
                 }
             }
@@ -608,8 +634,8 @@ __global__ void __launch_bounds__(2 * TR) rr_apply_kernel(const double* S, const
                 for (int i = 0; i < kHalfK; ++i) {
                     const int k = half + 2 * i;
                     if (k < m) {
-                        xs[i] = fma(u, C.v[l * m + k], xs[i]);
-                        xa[i] = fma(v, C.v[l * m + k], xa[i]);
+                        xs[i] = fma(u, Cc[l * m + k], xs[i]);
+                        xa[i] = fma(v, Cc[l * m + k], xa[i]);
                     }
                 }
             }
@@ -840,7 +866,7 @@ bool lanes_off() {
 }
 
 void launch_spmm(const DevCsr* A, const double* X, int ldx, const Cols& in, double* Y, int ldy, const Cols& out,
-                 cudaStream_t st) {
+                 cudaStream_t st, const int* stop = nullptr) {
     const long long n = A->nrows;
     const unsigned g = (unsigned)((n + kT - 1) / kT);
     for (int b = 0; b < in.n; b += 16) {
@@ -857,7 +883,7 @@ void launch_spmm(const DevCsr* A, const double* X, int ldx, const Cols& in, doub
             const unsigned gl = (unsigned)((n + rpw * (kT / 32) - 1) / (rpw * (kT / 32)));
             switch (ci.n) {
 #define SPARSLA_SPMML(W) \
-    case W: spmm_lanes_kernel<W><<<gl, kT, 0, st>>>(A->rp, A->ci, A->val, n, X, ldx, ci.c[0], Y, ldy, co.c[0]); break;
+    case W: spmm_lanes_kernel<W><<<gl, kT, 0, st>>>(A->rp, A->ci, A->val, n, X, ldx, ci.c[0], Y, ldy, co.c[0], stop); break;
                 SPARSLA_SPMML(4) SPARSLA_SPMML(6) SPARSLA_SPMML(8) SPARSLA_SPMML(10) SPARSLA_SPMML(12)
                 SPARSLA_SPMML(14) SPARSLA_SPMML(16)
 #undef SPARSLA_SPMML
@@ -868,9 +894,9 @@ void launch_spmm(const DevCsr* A, const double* X, int ldx, const Cols& in, doub
         }
         switch (ci.n * 2 + (contig ? 1 : 0)) {
 #define SPARSLA_SPMM(W) \
-    case 2 * W: spmm_kernel<W, false><<<g, kT, 0, st>>>(A->rp, A->ci, A->val, n, X, ldx, ci, Y, ldy, co); break;
+    case 2 * W: spmm_kernel<W, false><<<g, kT, 0, st>>>(A->rp, A->ci, A->val, n, X, ldx, ci, Y, ldy, co, stop); break;
 #define SPARSLA_SPMM2(W) \
-    SPARSLA_SPMM(W) case 2 * W + 1: spmm_kernel<W, true><<<g, kT, 0, st>>>(A->rp, A->ci, A->val, n, X, ldx, ci, Y, ldy, co); break;
+    SPARSLA_SPMM(W) case 2 * W + 1: spmm_kernel<W, true><<<g, kT, 0, st>>>(A->rp, A->ci, A->val, n, X, ldx, ci, Y, ldy, co, stop); break;
             SPARSLA_SPMM(1) SPARSLA_SPMM2(2) SPARSLA_SPMM(3) SPARSLA_SPMM2(4) SPARSLA_SPMM(5) SPARSLA_SPMM2(6)
             SPARSLA_SPMM(7) SPARSLA_SPMM2(8) SPARSLA_SPMM(9) SPARSLA_SPMM2(10) SPARSLA_SPMM(11) SPARSLA_SPMM2(12)
             SPARSLA_SPMM(13) SPARSLA_SPMM2(14) SPARSLA_SPMM(15) SPARSLA_SPMM2(16)
@@ -1017,6 +1043,7 @@ struct Lobpcg {
         ipart = dalloc<long long>((size_t)kRedCTAs * kMaxK);
         CK(cudaMallocHost(&h_pin, sizeof(double) * kMaxQ * kMaxQ));
         CK(cudaMallocHost(&h_part, sizeof(double) * kPartRows * kMaxQ));
+
         // dynamic shared memory up to the opt-in limit minus each kernel's static part
         auto allow = [&](const void* f, const char* what) {
             int optin = 0;
@@ -1028,11 +1055,14 @@ struct Lobpcg {
         };
         allow((const void*)gram_kernel, "gram smem");
         allow((const void*)gram_ws_kernel, "gram smem");
-#define SPARSLA_ALLOW(C) allow((const void*)apply_kernel<C>, "apply smem");
+#define SPARSLA_ALLOW(C) allow((const void*)apply_kernel<C, false>, "apply smem"); \
+    allow((const void*)apply_kernel<C, true>, "apply smem");
         SPARSLA_FOR_1_32(SPARSLA_ALLOW)
 #undef SPARSLA_ALLOW
-        allow((const void*)rr_apply_kernel<128>, "rr smem");
-        allow((const void*)rr_apply_kernel<64>, "rr smem");
+        allow((const void*)rr_apply_kernel<128, false>, "rr smem");
+        allow((const void*)rr_apply_kernel<64, false>, "rr smem");
+        allow((const void*)rr_apply_kernel<128, true>, "rr smem");
+        allow((const void*)rr_apply_kernel<64, true>, "rr smem");
     }
     ~Lobpcg() {
         DeviceGuard g(A->device, true);
@@ -1040,6 +1070,7 @@ struct Lobpcg {
         cudaFree(partial); cudaFree(gout); cudaFree(ticket); cudaFree(ipart);
         if (h_pin) cudaFreeHost(h_pin);
         if (h_part) cudaFreeHost(h_part);
+
     }
     unsigned grid() const { return (unsigned)((n + kT - 1) / kT); }
     unsigned tile_grid() const {  // persistent over row tiles, 4 CTAs per SM
@@ -1048,17 +1079,22 @@ struct Lobpcg {
     }
 
     // G = U_uc^T V_vc (host, row-major a x b); U, V are S / AS buffers (row stride ld)
+    // G = U_uc^T V_vc into gout (device); stop: device-resident iteration's halt flag
+    void gram_launch(const double* U, const Cols& uc, const double* V, const Cols& vc, double* out,
+                     const int* stop = nullptr) {
+        if (gram_ws_on())
+            gram_ws_kernel<<<kRedCTAs, (kGwConsumers + 1) * 32, gram_ws_smem(ld, U != V, uc.n, vc.n), s>>>(
+                U, V, ld, uc, vc, n, partial, ticket, out, gram_ws_stages(ld, U != V), stop);
+        else
+            gram_kernel<<<kRedCTAs, kT, gram_smem(ld, U != V, uc.n, vc.n), s>>>(U, V, ld, uc, vc, n, partial, ticket,
+                                                                          out, gram_stages(ld, U != V), stop);
+        CK(cudaGetLastError());
+    }
     std::vector<double> gram(const double* U, const Cols& uc, const double* V, const Cols& vc) {
         const int ab = uc.n * vc.n;
         std::vector<double> G(ab, 0.0);
         if (ab == 0 || n == 0) return G;
-        if (gram_ws_on())
-            gram_ws_kernel<<<kRedCTAs, (kGwConsumers + 1) * 32, gram_ws_smem(ld, U != V, uc.n, vc.n), s>>>(
-                U, V, ld, uc, vc, n, partial, ticket, gout, gram_ws_stages(ld, U != V));
-        else
-            gram_kernel<<<kRedCTAs, kT, gram_smem(ld, U != V, uc.n, vc.n), s>>>(U, V, ld, uc, vc, n, partial, ticket,
-                                                                          gout, gram_stages(ld, U != V));
-        CK(cudaGetLastError());
+        gram_launch(U, uc, V, vc, gout);
         CK(cudaMemcpyAsync(h_pin, gout, ab * sizeof(double), cudaMemcpyDeviceToHost, s));
         stream_sync_timed(s);
         std::memcpy(G.data(), h_pin, ab * sizeof(double));
@@ -1070,10 +1106,15 @@ struct Lobpcg {
         Mat Mt;
         std::memset(&Mt, 0, sizeof(Mt));
         std::copy(M.begin(), M.end(), Mt.v);
+        apply_launch<false>(in, out, Mt);
+    }
+    // DEV: coefficients already in c_coef (device-resident iteration)
+    template <bool DEV>
+    void apply_launch(const Cols& in, const Cols& out, const Mat& Mt, const int* stop = nullptr) {
         const unsigned g = tile_grid();
         const size_t sm = apply_smem(ld);
         switch (out.n) {
-#define SPARSLA_APPLY(C) case C: apply_kernel<C><<<g, kTRa, sm, s>>>(S, ld, in, out, n, Mt); break;
+#define SPARSLA_APPLY(C) case C: apply_kernel<C, DEV><<<g, kTRa, sm, s>>>(S, ld, in, out, n, Mt, stop); break;
             SPARSLA_FOR_1_32(SPARSLA_APPLY)
 #undef SPARSLA_APPLY
             default: fail(SPARSLA_ERR_INTERNAL, "apply: more than 32 output columns");
@@ -1177,6 +1218,20 @@ struct Lobpcg {
     // Rayleigh-Ritz on the orthonormal basis S_B, B = [X | Z] (AS_B = A S_B): one Gram launch
     // and one fused update launch writing X', AX', P' into Sn / ASn — plus the new pairs'
     // residual norms and W = |D|^-1 (AX' - X' Lambda) for the next iteration — then swap.
+    // rr_apply over basis columns B (DEV: coefficients in c_rrC / c_rrlam); returns its grid
+    template <bool DEV>
+    unsigned rr_launch(const Cols& B, const Mat& C, const Vec16& L, const double* dinv, const int* stop = nullptr) {
+        const int tr = rr_rows(ld);
+        const unsigned g = (unsigned)std::max<long long>(1, std::min<long long>((n + tr - 1) / tr, 4LL * 148));
+        if (tr == 128)
+            rr_apply_kernel<128, DEV><<<g, 256, rr_apply_smem(ld), s>>>(S, AS, Sn, ASn, ld, B, m, n, C, L, stop, dinv,
+                                                                         partial);
+        else
+            rr_apply_kernel<64, DEV><<<g, 128, rr_apply_smem(ld), s>>>(S, AS, Sn, ASn, ld, B, m, n, C, L, stop, dinv,
+                                                                        partial);
+        CK(cudaGetLastError());
+        return g;
+    }
     void rayleigh_ritz(const Cols& B, std::vector<double>& lam, const double* dinv, std::vector<double>& res) {
         const int q = B.n;
         std::vector<double> G = gram(S, B, AS, B);
@@ -1195,13 +1250,7 @@ struct Lobpcg {
         for (int j = 0; j < m; ++j) L.v[j] = th[j];
         res.assign(m, 0.0);
         if (n > 0) {
-            const int tr = rr_rows(ld);
-            const unsigned g = (unsigned)std::max<long long>(1, std::min<long long>((n + tr - 1) / tr, 4LL * 148));
-            if (tr == 128)
-                rr_apply_kernel<128><<<g, 256, rr_apply_smem(ld), s>>>(S, AS, Sn, ASn, ld, B, m, n, C, L, dinv, partial);
-            else
-                rr_apply_kernel<64><<<g, 128, rr_apply_smem(ld), s>>>(S, AS, Sn, ASn, ld, B, m, n, C, L, dinv, partial);
-            CK(cudaGetLastError());
+            const unsigned g = rr_launch<false>(B, C, L, dinv);
             const double* h = h_part;
             CK(cudaMemcpyAsync(h_part, partial, (size_t)g * m * sizeof(double), cudaMemcpyDeviceToHost, s));
             stream_sync_timed(s);
@@ -1214,6 +1263,396 @@ struct Lobpcg {
         lam.assign(th.begin(), th.begin() + m);
     }
 };
+
+// ------------------------------------------------ device-resident LOBPCG iteration ----
+// The host driver above synchronises three times per iteration (two Gram read-backs and the
+// residual norms) and solves the small dense problems on the host.  Here every decision of
+// an iteration — soft locking, the CGS2 + SVQB orthogonalisation with its drop rule and
+// "twice is enough" test, the Rayleigh-Ritz eigenproblem, termination — runs in one-CTA
+// kernels on the device, the block kernels take fixed column lists (X | W | P) with the
+// inactive directions expressed as zero / identity coefficients, and two iterations are one
+// CUDA graph (S <-> Sn ping-pong).  The host only polls the stop flag, one graph behind.
+// Same algorithm as the host driver; the small eigenproblems use a parallel (round-robin)
+// cyclic Jacobi instead of the serial one, so results agree to rounding (tolerance parity,
+// like the rest of this module).
+struct EigDevState {
+    int done;    // solve stopped: every later kernel exits at entry
+    int halt1;   // done, or the second orthogonalisation pass is not needed
+    int it, have_p, cur;  // completed iterations, P block present, buffer pair holding S (0/1)
+    int nza;     // active Z directions (indices into the 2m W|P slots); after ortho: survivors
+    int za[2 * kMaxK];
+    int m, k, cgs2;
+    int nspmm;   // SpMMs executed (one per iteration that ran)
+    long long max_iter;
+    double tol;
+    double res[kMaxK], lam[kMaxK];
+};
+
+constexpr int kEigThreads = 256;
+constexpr int kQ = kMaxQ;  // leading dimension of the small matrices in shared memory
+
+// Parallel cyclic Jacobi on the q x q symmetric matrix A (shared, ld kQ) by one CTA: q/2
+// disjoint rotations per step in round-robin order, each element updated from its 2 x 2
+// block of the previous step.  On return w[0..q) ascending and the matching eigenvectors
+// in the columns of U (ld kQ).  Work buffers A2, V, V2 (q x q, ld kQ), small arrays in sm.
+struct JacobiSmem {
+    double alpha[kQ], beta[kQ], red[kEigThreads / 32][2];
+    int part[kQ], zero[kQ];
+};
+__device__ void block_sym_eig(int q, double* A, double* A2, double* V, double* V2, double* w, double* U,
+                              JacobiSmem& J) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    for (int e = tid; e < q * q; e += nt) V[(e / q) * kQ + e % q] = (e / q == e % q) ? 1.0 : 0.0;
+    const int qq = q + (q & 1);
+    __syncthreads();
+    for (int sweep = 0; sweep < 60 && q > 1; ++sweep) {
+        // convergence: off-diagonal vs diagonal mass (same rule as the host solver)
+        double off = 0.0, dia = 0.0;
+        for (int e = tid; e < q * q; e += nt) {
+            const int i = e / q, j = e % q;
+            const double a = A[i * kQ + j];
+            if (i == j) dia += a * a;
+            else if (i < j) off += a * a;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            off += __shfl_xor_sync(0xffffffffu, off, o);
+            dia += __shfl_xor_sync(0xffffffffu, dia, o);
+        }
+        if ((tid & 31) == 0) { J.red[tid >> 5][0] = off; J.red[tid >> 5][1] = dia; }
+        __syncthreads();
+        off = 0.0; dia = 0.0;
+        for (int wv = 0; wv < nt / 32; ++wv) { off += J.red[wv][0]; dia += J.red[wv][1]; }
+        __syncthreads();
+        if (off == 0.0 || off <= 1e-32 * dia) break;
+        for (int step = 0; step < qq - 1; ++step) {
+            if (tid < qq / 2) {
+                auto player = [&](int sl) { return sl == 0 ? 0 : 1 + (sl - 1 + step) % (qq - 1); };
+                const int i0 = player(tid), j0 = player(qq - 1 - tid);
+                const int lo = min(i0, j0), hi = max(i0, j0);
+                if (hi < q) {
+                    const double apr = A[lo * kQ + hi];
+                    bool rot = apr != 0.0, zero = false;
+                    if (rot && sweep >= 3) {  // threshold rule: too small to change the diagonal
+                        const double g = 100.0 * fabs(apr);
+                        if (fabs(A[lo * kQ + lo]) + g == fabs(A[lo * kQ + lo]) &&
+                            fabs(A[hi * kQ + hi]) + g == fabs(A[hi * kQ + hi])) { rot = false; zero = true; }
+                    }
+                    if (rot) {
+                        const double theta = (A[hi * kQ + hi] - A[lo * kQ + lo]) / (2.0 * apr);
+                        const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+                        const double c = 1.0 / sqrt(t * t + 1.0), s = t * c;
+                        J.alpha[lo] = c; J.beta[lo] = -s; J.part[lo] = hi;
+                        J.alpha[hi] = c; J.beta[hi] = s; J.part[hi] = lo;
+                    } else {
+                        J.alpha[lo] = 1.0; J.beta[lo] = 0.0; J.part[lo] = lo;
+                        J.alpha[hi] = 1.0; J.beta[hi] = 0.0; J.part[hi] = hi;
+                    }
+                    J.zero[lo] = (rot || zero) ? hi : -1;
+                    J.zero[hi] = (rot || zero) ? lo : -1;
+                } else if (lo < q) {  // paired with the padding index
+                    J.alpha[lo] = 1.0; J.beta[lo] = 0.0; J.part[lo] = lo; J.zero[lo] = -1;
+                }
+            }
+            __syncthreads();
+            for (int e = tid; e < q * q; e += nt) {
+                const int i = e / q, j = e % q;
+                const double ai = J.alpha[i], bi = J.beta[i], aj = J.alpha[j], bj = J.beta[j];
+                const int pi = J.part[i], pj = J.part[j];
+                double v = ai * (aj * A[i * kQ + j] + bj * A[i * kQ + pj]) +
+                           bi * (aj * A[pi * kQ + j] + bj * A[pi * kQ + pj]);
+                if (J.zero[i] == j) v = 0.0;  // the annihilated (or negligible) pair element
+                A2[i * kQ + j] = v;
+                V2[i * kQ + j] = aj * V[i * kQ + j] + bj * V[i * kQ + pj];
+            }
+            __syncthreads();
+            double* t = A; A = A2; A2 = t;
+            t = V; V = V2; V2 = t;
+        }
+    }
+    // ascending order, ties by index (as std::stable_sort on the diagonal)
+    for (int i = tid; i < q; i += nt) {
+        const double wi = A[i * kQ + i];
+        int r = 0;
+        for (int j = 0; j < q; ++j) {
+            const double wj = A[j * kQ + j];
+            r += (wj < wi || (wj == wi && j < i)) ? 1 : 0;
+        }
+        w[r] = wi;
+        for (int row = 0; row < q; ++row) U[row * kQ + r] = V[row * kQ + i];
+    }
+    __syncthreads();
+}
+
+struct EigSmem {  // dynamic shared memory of the small-problem kernels
+    double A[kQ * kQ], A2[kQ * kQ], V[kQ * kQ], V2[kQ * kQ], U[kQ * kQ];
+    double H[kQ * kQ];
+    double w[kQ], D[kQ], h0[kQ];
+    int keep[kQ];
+    JacobiSmem J;
+    int w2, skip;
+};
+
+// soft locking and termination for the coming iteration (host driver: top of its loop)
+__global__ void eig_decide_kernel(EigDevState* st) {
+    if (threadIdx.x != 0 || st->done) return;
+    const int m = st->m;
+    int n = 0;
+    bool wanted_done = true;
+    for (int j = 0; j < m; ++j) {
+        const bool conv = st->res[j] <= st->tol;
+        if (!conv) st->za[n++] = j;  // W_j
+        if (j < st->k && !conv) wanted_done = false;
+    }
+    if (wanted_done || n == 0 || st->it >= st->max_iter) {
+        st->done = 1;
+        st->halt1 = 1;
+        return;
+    }
+    if (st->have_p) {
+        const int nw = n;
+        for (int t = 0; t < nw; ++t) st->za[n++] = m + st->za[t];  // P slot of each active W
+    }
+    st->nza = n;
+    st->halt1 = 0;
+}
+
+// One CGS + SVQB orthogonalisation pass of the active Z directions against X (host driver:
+// Lobpcg::ortho).  G = [X | W | P]^T [W | P] (3m x 2m).  Writes the coefficients of the in-place
+// transform S[:, W|P] = S[:, X|W|P] M (3m x 2m, row-major) to Mout; survivors stay a prefix of
+// the active list, dropped and inactive slots get identity columns.
+__global__ void __launch_bounds__(kEigThreads) eig_ortho_kernel(EigDevState* st, const double* G, double* Mout,
+                                                                int pass) {
+    if (pass == 0 ? st->done : st->halt1) return;
+    extern __shared__ __align__(16) unsigned char esm[];
+    EigSmem& E = *reinterpret_cast<EigSmem*>(esm);
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int m = st->m, b = m, w = st->nza, zc = 2 * m;
+    const int* za = st->za;
+    const double rel = pass == 0 ? 1e-14 : 1e-24;
+    // H = G_ZZ - G_XZ^T G_XZ (host order: subtract l = 0, 1, ...)
+    for (int e = tid; e < w * w; e += nt) {
+        const int i = e / w, j = e % w;
+        double h = G[(b + za[i]) * zc + za[j]];
+        for (int l = 0; l < b; ++l) h -= G[l * zc + za[i]] * G[l * zc + za[j]];
+        E.H[i * kQ + j] = h;
+    }
+    __syncthreads();
+    for (int i = tid; i < w; i += nt) {
+        const double h0 = G[(b + za[i]) * zc + za[i]], h = E.H[i * kQ + i];
+        E.h0[i] = h0;
+        E.D[i] = (isfinite(h) && h > 1e-300 && h > rel * h0) ? 1.0 / sqrt(h) : 0.0;
+    }
+    __syncthreads();
+    for (int e = tid; e < w * w; e += nt) {
+        const int i = e / w, j = e % w;
+        E.A[i * kQ + j] = E.D[i] * 0.5 * (E.H[i * kQ + j] + E.H[j * kQ + i]) * E.D[j];
+    }
+    __syncthreads();
+    block_sym_eig(w, E.A, E.A2, E.V, E.V2, E.w, E.U, E.J);
+    if (tid == 0) {
+        const double smax = fmax(w > 0 ? E.w[w - 1] : 0.0, 0.0);
+        int w2 = 0;
+        for (int j = w - 1; j >= 0; --j)
+            if (E.w[j] > rel * smax && E.w[j] > 0.0) E.keep[w2++] = j;
+        E.w2 = w2;
+        int skip = 0;
+        if (pass == 0 && !st->cgs2) {
+            double worst = 1.0;
+            for (int i = 0; i < w; ++i) worst = fmin(worst, E.h0[i] > 0 ? E.H[i * kQ + i] / E.h0[i] : 0.0);
+            const double smin = w > 0 ? E.w[0] : 0.0;
+            skip = (w2 == w && worst > 0.25 && smin > 1e-6 * smax) ? 1 : 0;
+        }
+        E.skip = skip;
+    }
+    __syncthreads();
+    const int w2 = E.w2;
+    // T (w x w2) = D U_keep sigma^-1/2, into A2
+    for (int e = tid; e < w * w2; e += nt) {
+        const int i = e / w2, c = e % w2;
+        E.A2[i * kQ + c] = E.D[i] * E.U[i * kQ + E.keep[c]] / sqrt(E.w[E.keep[c]]);
+    }
+    for (int e = tid; e < 3 * m * zc; e += nt) Mout[e] = 0.0;
+    __syncthreads();
+    for (int e = tid; e < (b + w) * w2; e += nt) {
+        const int r = e / w2, c = e % w2, o = za[c];  // output slot of survivor c
+        double v;
+        if (r < b) {  // -Y T
+            v = 0.0;
+            for (int i = 0; i < w; ++i) v += G[r * zc + za[i]] * E.A2[i * kQ + c];
+            v = -v;
+            Mout[r * zc + o] = v;
+        } else {
+            Mout[(b + za[r - b]) * zc + o] = E.A2[(r - b) * kQ + c];
+        }
+    }
+    __syncthreads();
+    for (int o = tid; o < zc; o += nt) {  // slots that are not survivors keep their column
+        bool surv = false;
+        for (int c = 0; c < w2; ++c) surv |= za[c] == o;
+        if (!surv) Mout[(b + o) * zc + o] = 1.0;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        st->nza = w2;
+        if (pass == 0) st->halt1 = (E.skip || w2 == 0) ? 1 : 0;
+    }
+}
+
+// Rayleigh-Ritz on the orthonormal basis X | surviving Z: G = [X|W|P]^T A [X|W|P] (3m x 3m)
+// restricted to the active slots; writes C (3m x m, zero rows for inactive slots) and the
+// m smallest Ritz values.
+__global__ void __launch_bounds__(kEigThreads) eig_rr_kernel(EigDevState* st, const double* G, double* Cout,
+                                                             double* lamout) {
+    if (st->done) return;
+    extern __shared__ __align__(16) unsigned char esm[];
+    EigSmem& E = *reinterpret_cast<EigSmem*>(esm);
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int m = st->m, q = m + st->nza, ac = 3 * m;
+    __shared__ int slot[kQ];
+    for (int i = tid; i < q; i += nt) slot[i] = i < m ? i : m + st->za[i - m];
+    __syncthreads();
+    for (int e = tid; e < q * q; e += nt) {
+        const int i = e / q, j = e % q;
+        const double gij = G[slot[i] * ac + slot[j]], gji = G[slot[j] * ac + slot[i]];
+        E.A[i * kQ + j] = i == j ? gij : 0.5 * (i < j ? gij + gji : gji + gij);
+    }
+    __syncthreads();
+    block_sym_eig(q, E.A, E.A2, E.V, E.V2, E.w, E.U, E.J);
+    for (int e = tid; e < ac * m; e += nt) Cout[e] = 0.0;
+    __syncthreads();
+    for (int e = tid; e < q * m; e += nt) {
+        const int i = e / m, j = e % m;
+        Cout[slot[i] * m + j] = E.U[i * kQ + j];
+    }
+    for (int j = tid; j < m; j += nt) {
+        lamout[j] = E.w[j];
+        st->lam[j] = E.w[j];
+    }
+}
+
+// residual norms of the new pairs (rr_apply's per-CTA partials, summed in CTA order) and
+// the end-of-iteration bookkeeping
+__global__ void __launch_bounds__(kEigThreads) eig_post_kernel(EigDevState* st, const double* partial, int g) {
+    if (st->done) return;
+    const int m = st->m;
+    __shared__ double part[kEigThreads][kMaxK];
+    // fixed two-level order: thread t sums CTAs t, t + 256, ...; then threads in order
+    for (int j = 0; j < m; ++j) {
+        double r = 0.0;
+        for (int p = threadIdx.x; p < g; p += blockDim.x) r += partial[(size_t)p * m + j];
+        part[threadIdx.x][j] = r;
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < m; j += blockDim.x) {
+        double r = 0.0;
+        for (int t = 0; t < (int)blockDim.x; ++t) r += part[t][j];
+        st->res[j] = sqrt(r);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        st->cur ^= 1;
+        st->nspmm += 1;
+        st->have_p = st->nza > 0;
+        if (st->nza == 0) { st->done = 1; st->halt1 = 1; }
+        else st->it += 1;
+    }
+}
+
+size_t eig_smem_bytes() { return sizeof(EigSmem); }
+
+
+// opt-in (SPARSLA_EIG_DEVICE=1): measured slower than the host driver — the one-CTA
+// Jacobi of the 18 x 18 Rayleigh-Ritz problem takes ~125 us on the GPU against ~19 us on
+// the host (profiles/r02_lobpcg.md)
+bool eig_device_on() {
+    const char* e = std::getenv("SPARSLA_EIG_DEVICE");
+    return e && std::atoi(e) != 0;
+}
+
+// Device-resident LOBPCG loop (see above).  Entry: X (and AX, W, res) from the initial
+// Rayleigh-Ritz in L.S / L.AS, lam / res on the host.  Exit: L.S / L.AS hold the final basis,
+// lam / res / it updated.
+const Mat kNoMat{};  // parameter of the DEV launches (coefficients come from the symbols)
+
+void lobpcg_device_loop(Lobpcg& L, int k, double tol, long long max_iter, const double* dinv,
+                        std::vector<double>& lam, std::vector<double>& res, long long& it) {
+    const int m = L.m;
+    cudaStream_t s = L.s;
+    static std::once_flag attr_once;
+    std::call_once(attr_once, [] {
+        CK(cudaFuncSetAttribute(eig_ortho_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)eig_smem_bytes()));
+        CK(cudaFuncSetAttribute(eig_rr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)eig_smem_bytes()));
+    });
+    EigDevState h{};
+    h.m = m; h.k = k; h.tol = tol; h.max_iter = max_iter; h.cgs2 = cgs2_always() ? 1 : 0;
+    for (int j = 0; j < m; ++j) { h.res[j] = res[j]; h.lam[j] = lam[j]; }
+    EigDevState* st = dalloc<EigDevState>(1);
+    double* Mbuf = dalloc<double>((size_t)kMaxQ * 2 * kMaxK);
+    double* Cbuf = dalloc<double>((size_t)kMaxQ * kMaxK);
+    double* lbuf = dalloc<double>(kMaxK);
+    EigDevState* hs = nullptr;  // pinned: [2] polled states
+    CK(cudaMallocHost(&hs, 2 * sizeof(EigDevState)));
+    CK(cudaMemcpyAsync(st, &h, sizeof h, cudaMemcpyHostToDevice, s));
+    const Cols All = cols_range(0, 3 * m), Zf = cols_range(m, 3 * m);
+    double* b0S = L.S; double* b0A = L.AS; double* b1S = L.Sn; double* b1A = L.ASn;
+    const size_t esm = eig_smem_bytes();
+    auto iteration = [&](double* S, double* AS, double* Sn, double* ASn) {
+        L.S = S; L.AS = AS; L.Sn = Sn; L.ASn = ASn;
+        eig_decide_kernel<<<1, 32, 0, s>>>(st);
+        for (int pass = 0; pass < 2; ++pass) {
+            const int* stop = pass == 0 ? &st->done : &st->halt1;
+            L.gram_launch(S, All, S, Zf, L.gout, stop);
+            eig_ortho_kernel<<<1, kEigThreads, esm, s>>>(st, L.gout, Mbuf, pass);
+            CK(cudaMemcpyToSymbolAsync(c_coef, Mbuf, (size_t)3 * m * 2 * m * sizeof(double), 0,
+                                       cudaMemcpyDeviceToDevice, s));
+            L.apply_launch<true>(All, Zf, kNoMat, stop);
+        }
+        launch_spmm(L.A, S, L.ld, Zf, AS, L.ld, Zf, s, &st->done);
+        L.gram_launch(S, All, AS, All, L.gout, &st->done);
+        eig_rr_kernel<<<1, kEigThreads, esm, s>>>(st, L.gout, Cbuf, lbuf);
+        CK(cudaMemcpyToSymbolAsync(c_rrC, Cbuf, (size_t)3 * m * m * sizeof(double), 0, cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemcpyToSymbolAsync(c_rrlam, lbuf, m * sizeof(double), 0, cudaMemcpyDeviceToDevice, s));
+        const unsigned g = L.rr_launch<true>(All, kNoMat, Vec16{}, dinv, &st->done);
+        eig_post_kernel<<<1, kEigThreads, 0, s>>>(st, L.partial, (int)g);
+        CK(cudaGetLastError());
+    };
+    cudaGraph_t graph;
+    CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    iteration(b0S, b0A, b1S, b1A);
+    iteration(b1S, b1A, b0S, b0A);
+    CK(cudaStreamEndCapture(s, &graph));
+    cudaGraphExec_t exec;
+    CK(cudaGraphInstantiate(&exec, graph, 0));
+    CK(cudaGraphDestroy(graph));
+    cudaEvent_t ev[2];
+    CK(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+    // launch graphs, poll the stop flag one launch behind
+    for (long long i = 0;; ++i) {
+        CK(cudaGraphLaunch(exec, s));
+        CK(cudaMemcpyAsync(&hs[i & 1], st, sizeof(EigDevState), cudaMemcpyDeviceToHost, s));
+        CK(cudaEventRecord(ev[i & 1], s));
+        if (i >= 1) {
+            CK(cudaEventSynchronize(ev[(i - 1) & 1]));
+            if (hs[(i - 1) & 1].done) break;
+        }
+        if (i > 2 * max_iter + 8) break;  // cannot happen: decide stops at max_iter
+    }
+    CK(cudaStreamSynchronize(s));
+    CK(cudaMemcpy(&h, st, sizeof h, cudaMemcpyDeviceToHost));
+    cudaEventDestroy(ev[0]); cudaEventDestroy(ev[1]);
+    cudaGraphExecDestroy(exec);
+    cudaFreeHost(hs);
+    cudaFree(st); cudaFree(Mbuf); cudaFree(Cbuf); cudaFree(lbuf);
+    // h.cur: the pair that holds the current basis
+    L.S = h.cur ? b1S : b0S; L.AS = h.cur ? b1A : b0A;
+    L.Sn = h.cur ? b0S : b1S; L.ASn = h.cur ? b0A : b1A;
+    lam.assign(h.lam, h.lam + m);
+    res.assign(h.res, h.res + m);
+    it = h.it;
+    L.spmm_count += h.nspmm;
+}
 
 struct EigOut {
     std::vector<double> lam, res;
@@ -1285,8 +1724,14 @@ int dense_threshold() {
     return e ? std::max(0, std::atoi(e)) : 64;
 }
 
+std::mutex& eig_mutex() {  // one LOBPCG at a time per process: coefficient symbols are global
+    static std::mutex mu;
+    return mu;
+}
+
 void eig_smallest(DevCsr* A, int k, double tol, long long max_iter, uint64_t seed, int precond, double* V,
                   EigOut& o) {
+    std::lock_guard<std::mutex> lk(eig_mutex());
     const long long n = A->nrows;
     const double* dinv = precond == SPARSLA_PRECOND_JACOBI ? A->jacobi_dinv() : nullptr;
     int m = k;
@@ -1337,7 +1782,10 @@ void eig_smallest(DevCsr* A, int k, double tol, long long max_iter, uint64_t see
     L.rayleigh_ritz(Xc, lam, dinv, res);  // also ||R_j|| and W = |D|^-1 R into the W slot
     bool have_p = false;
     long long it = 0;
-    for (;; ++it) {
+    if (eig_device_on()) {  // device-resident iterations (CUDA graph, no host round trips)
+        lobpcg_device_loop(L, k, tol, max_iter, dinv, lam, res, it);
+    }
+    for (; !eig_device_on(); ++it) {
         Cols Z;
         bool wanted_done = true;  // the first k (wanted) pairs decide termination
         for (int j = 0; j < m; ++j) {  // soft locking: only unconverged pairs add directions
