@@ -207,3 +207,26 @@ def test_xwin_distributed_bitwise(S, O, gpu, monkeypatch, kind, p1, P, part, sol
     rep = res[0][1]
     assert rep.converged and rep.iterations == ro["iterations"], (rep, ro)
     assert np.array_equal(bits(xd), bits(xo))
+
+
+@pytest.mark.parametrize("offset", [0, 1])
+def test_xwin_user_device_pointers(S, O, gpu, offset):
+    """sparsla_spmv with caller-owned device buffers: a 16-byte aligned x goes through the
+    TMA windows; an x (or y) that is only 8-byte aligned falls back to the gather kernel
+    (TMA bulk copies need 16-byte aligned sources) — bitwise either way."""
+    import ctypes as C
+    import torch
+    A = O.generate("poisson3d", 40)
+    D = to_S(S, A).device(0)
+    assert 0 in D.xwin()["modes"]  # plain-mode SpMV takes the x-window kernel (pair stream)
+    x = np.random.default_rng(7).standard_normal(A.ncols)
+    xt = torch.zeros(A.ncols + 2, dtype=torch.float64, device="cuda:0")
+    yt = torch.zeros(A.nrows + 2, dtype=torch.float64, device="cuda:0")
+    xv, yv = xt[offset:offset + A.ncols], yt[offset:offset + A.nrows]
+    xv.copy_(torch.from_numpy(x))
+    torch.cuda.synchronize()
+    assert (xv.data_ptr() % 16 == 0) == (offset == 0)
+    S._check(S.lib().sparsla_spmv(D.h, C.cast(C.c_void_p(xv.data_ptr()), S._f64p),
+                                  C.cast(C.c_void_p(yv.data_ptr()), S._f64p), C.c_int32(S.MEM_DEVICE)))
+    torch.cuda.synchronize()
+    assert_bitwise(yv.cpu().numpy(), O.spmv(A, x), f"device pointers, offset {offset}")
