@@ -504,6 +504,10 @@ def run_ours(args):
         "iteration_gbs": it_bytes / (ms / args.steps * 1e-3) / 1e9,
         "bytes_per_iteration": it_bytes,
         "canonical_bytes_per_iteration": canon,
+        # SURVEY.md §8(d) "SpMV-only GB/s" on the canonical fp64 CSR accounting (12 nnz + 20 n
+        # bytes) — an equivalent rate, not a bandwidth: the stored format moves fewer bytes
+        # (roofline.achieved above uses the stored bytes)
+        "spmv_canonical_csr_rate_gbs": (12 * nnz + 20 * n) / (kms[[nm for nm, _ in kb].index(dom_name)] * 1e-3) / 1e9,
         "kernel_ms": {nm: t for (nm, _), t in zip(kb, kms)},
         "kernel_gbs": kernel_gbs,
         "plain_csr": plain,
