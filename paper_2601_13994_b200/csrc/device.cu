@@ -825,9 +825,11 @@ unsigned spmv_grid(const DevCsr* A, long long nch, int mode, bool xw_ok) {
 // number of CTAs of every launch of this reduction point (interior + boundary).
 void launch_spmv_part(DevCsr* A, cudaStream_t s, int mode, const double* x, double* y, const double* aux,
                       const RedParams& red, int check_done, const int32_t* list, long long nch,
-                      unsigned expected, const P2PCtx* p2p, long long n_interior, int halo_v) {
+                      unsigned expected, const P2PCtx* p2p, long long n_interior, int halo_v,
+                      unsigned grid_cap) {
     const bool xw_ok = xw_aligned(x, aux);
-    const unsigned grid = spmv_grid(A, nch, mode, xw_ok);
+    unsigned grid = spmv_grid(A, nch, mode, xw_ok);
+    if (grid_cap && A->staged && grid > grid_cap) grid = grid_cap;  // persistent kernels only
     if (grid == 0) return;
     SpmvParams P{};
     P.rp = A->rp; P.ci = A->ci; P.val = A->val;
@@ -1134,8 +1136,23 @@ void Solver::spmv_point(int mode, double* xin, double* y, const double* aux, int
     }
     if (nd > 0) R.red_out = dist->red_send + slot * 8;
     dist->exchange(stream, xin);
-    const unsigned gi = spmv_grid(A, dist->n_interior, mode), gb = spmv_grid(A, dist->n_boundary, mode);
-    launch_spmv_part(A, stream, mode, xin, y, aux, R, check_done, dist->d_interior, dist->n_interior, gi + gb);
+    // The interior launch runs while the halo moves: with peers, cap its persistent grid two
+    // SMs short of the device so the transport's kernels (NCCL send/recv) are not queued
+    // behind a GPU-filling grid.  (The persistent kernels loop over their chunks, so any grid
+    // works; the ticket count `expected` uses the same capped grid.)
+    unsigned cap = 0;
+    if (dist->tr && dist->tr->P > 1 && A->staged) {
+        int sms = 0;
+        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, A->device));
+        const unsigned full = spmv_grid(A, 1LL << 40, mode);
+        const unsigned per_sm = std::max(1u, full / (unsigned)std::max(1, sms));
+        if (full > 4 * per_sm) cap = full - 2 * per_sm;
+    }
+    unsigned gi = spmv_grid(A, dist->n_interior, mode);
+    if (cap && gi > cap) gi = cap;
+    const unsigned gb = spmv_grid(A, dist->n_boundary, mode);
+    launch_spmv_part(A, stream, mode, xin, y, aux, R, check_done, dist->d_interior, dist->n_interior, gi + gb,
+                     nullptr, 0, 0, cap);
     CK(cudaStreamWaitEvent(stream, dist->ev_halo, 0));
     launch_spmv_part(A, stream, mode, xin, y, aux, R, check_done, dist->d_boundary, dist->n_boundary, gi + gb);
     if (nd > 0) reduce_point(scalar, slot, nd);

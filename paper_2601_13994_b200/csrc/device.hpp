@@ -107,7 +107,7 @@ unsigned spmv_grid(const DevCsr* A, long long nch, int mode = 0, bool xw_ok = tr
 void launch_spmv_part(DevCsr* A, cudaStream_t s, int mode, const double* x, double* y, const double* aux,
                       const RedParams& red, int check_done, const int32_t* list, long long nch,
                       unsigned expected, const P2PCtx* p2p = nullptr, long long n_interior = 0,
-                      int halo_v = 0);
+                      int halo_v = 0, unsigned grid_cap = 0);
 
 struct Transport;
 
