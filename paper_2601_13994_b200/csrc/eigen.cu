@@ -1283,6 +1283,7 @@ struct EigDevState {
     int za[2 * kMaxK];
     int m, k, cgs2;
     int nspmm;   // SpMMs executed (one per iteration that ran)
+    int jac_sweeps_max;  // largest Jacobi sweep count of the small solves (diagnostics)
     long long max_iter;
     double tol;
     double res[kMaxK], lam[kMaxK];
@@ -1298,14 +1299,17 @@ constexpr int kQ = kMaxQ;  // leading dimension of the small matrices in shared 
 struct JacobiSmem {
     double alpha[kQ], beta[kQ], red[kEigThreads / 32][2];
     int part[kQ], zero[kQ];
+    int sweeps;
 };
+constexpr int kJacobiSweeps = 30;
 __device__ void block_sym_eig(int q, double* A, double* A2, double* V, double* V2, double* w, double* U,
                               JacobiSmem& J) {
     const int tid = threadIdx.x, nt = blockDim.x;
     for (int e = tid; e < q * q; e += nt) V[(e / q) * kQ + e % q] = (e / q == e % q) ? 1.0 : 0.0;
+    if (tid == 0) J.sweeps = 0;
     const int qq = q + (q & 1);
     __syncthreads();
-    for (int sweep = 0; sweep < 60 && q > 1; ++sweep) {
+    for (int sweep = 0; sweep < kJacobiSweeps && q > 1; ++sweep) {
         // convergence: off-diagonal vs diagonal mass (same rule as the host solver)
         double off = 0.0, dia = 0.0;
         for (int e = tid; e < q * q; e += nt) {
@@ -1324,7 +1328,8 @@ __device__ void block_sym_eig(int q, double* A, double* A2, double* V, double* V
         off = 0.0; dia = 0.0;
         for (int wv = 0; wv < nt / 32; ++wv) { off += J.red[wv][0]; dia += J.red[wv][1]; }
         __syncthreads();
-        if (off == 0.0 || off <= 1e-32 * dia) break;
+        if (off == 0.0 || off <= 1e-30 * dia) break;  // off-diagonal below 1e-15 of the diagonal (norm)
+        if (tid == 0) J.sweeps = sweep + 1;
         for (int step = 0; step < qq - 1; ++step) {
             if (tid < qq / 2) {
                 auto player = [&](int sl) { return sl == 0 ? 0 : 1 + (sl - 1 + step) % (qq - 1); };
@@ -1519,6 +1524,7 @@ __global__ void __launch_bounds__(kEigThreads) eig_rr_kernel(EigDevState* st, co
     }
     __syncthreads();
     block_sym_eig(q, E.A, E.A2, E.V, E.V2, E.w, E.U, E.J);
+    if (tid == 0) st->jac_sweeps_max = max(st->jac_sweeps_max, E.J.sweeps);
     for (int e = tid; e < ac * m; e += nt) Cout[e] = 0.0;
     __syncthreads();
     for (int e = tid; e < q * m; e += nt) {
@@ -1652,6 +1658,7 @@ void lobpcg_device_loop(Lobpcg& L, int k, double tol, long long max_iter, const 
     res.assign(h.res, h.res + m);
     it = h.it;
     L.spmm_count += h.nspmm;
+    if (eig_timing().on) std::fprintf(stderr, "[eig device] max Jacobi sweeps of the Rayleigh-Ritz solves: %d\n", h.jac_sweeps_max);
 }
 
 struct EigOut {
