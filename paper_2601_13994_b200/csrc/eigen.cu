@@ -336,28 +336,7 @@ __global__ void __launch_bounds__(kT) gram_kernel(const double* __restrict__ U, 
     }
     __syncthreads();
     for (int e = tid; e < ab; e += kT) partial[(size_t)blockIdx.x * ab + e] = red[e];
-    __shared__ int s_last;
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    const int P = gridDim.x;
-    for (int e = tid; e < ab; e += kT) {
-        double sum = 0.0;
-        int p = 0;
-        for (; p + 8 <= P; p += 8) {
-            double t[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) t[q] = __ldcg(partial + (size_t)(p + q) * ab + e);
-#pragma unroll
-            for (int q = 0; q < 8; ++q) sum += t[q];
-        }
-        for (; p < P; ++p) sum += __ldcg(partial + (size_t)p * ab + e);
-        out[e] = sum;
-    }
-    if (tid == 0) *ticket = 0u;
+    (void)ticket; (void)out;  // the CTA partials are summed by gram_finish_kernel
 }
 
 // Warp-specialised Gram block (same result, same fixed grid and combination order as
@@ -466,28 +445,36 @@ __global__ void __launch_bounds__((kGwConsumers + 1) * 32, 2) gram_ws_kernel(con
     }
     __syncthreads();
     for (int e = tid; e < ab; e += blockDim.x) partial[(size_t)blockIdx.x * ab + e] = red[e];
-    __shared__ int s_last;
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    const int P = gridDim.x;
-    for (int e = tid; e < ab; e += blockDim.x) {
-        double sum = 0.0;
-        int p = 0;
-        for (; p + 8 <= P; p += 8) {
-            double t[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) t[q] = __ldcg(partial + (size_t)(p + q) * ab + e);
-#pragma unroll
-            for (int q = 0; q < 8; ++q) sum += t[q];
+    (void)ticket; (void)out;  // the CTA partials are summed by gram_finish_kernel
+}
+
+// Sum of the Gram kernels' CTA partials (partial[p * ab + e], p < P) into out[e].  One
+// last CTA summing P x ab partials with 8 loads in flight per thread was a ~30 us serial
+// tail; here 32 entries per block, 8 warps each summing a residue class of p (coalesced
+// rows), combined in warp order: deterministic, independent of the device.
+__global__ void __launch_bounds__(256) gram_finish_kernel(const double* __restrict__ partial, int P, int ab,
+                                                          double* out, const int* stop) {
+    if (halted(stop)) return;
+    __shared__ double red[8][33];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int e = blockIdx.x * 32 + lane;
+    double sum = 0.0;
+    if (e < ab) {
+        int p = w;
+        for (; p + 24 < P; p += 32) {
+            const double a0 = __ldcg(partial + (size_t)p * ab + e), a1 = __ldcg(partial + (size_t)(p + 8) * ab + e);
+            const double a2 = __ldcg(partial + (size_t)(p + 16) * ab + e), a3 = __ldcg(partial + (size_t)(p + 24) * ab + e);
+            sum += a0; sum += a1; sum += a2; sum += a3;
         }
-        for (; p < P; ++p) sum += __ldcg(partial + (size_t)p * ab + e);
-        out[e] = sum;
+        for (; p < P; p += 8) sum += __ldcg(partial + (size_t)p * ab + e);
     }
-    if (tid == 0) *ticket = 0u;
+    red[w][lane] = sum;
+    __syncthreads();
+    if (w == 0 && e < ab) {
+        double t = red[0][lane];
+        for (int q = 1; q < 8; ++q) t += red[q][lane];
+        out[e] = t;
+    }
 }
 
 // In-place block transform of whole rows: S[:, out_j] = sum_l S[:, in_l] M[l, j]
@@ -1088,6 +1075,8 @@ struct Lobpcg {
         else
             gram_kernel<<<kRedCTAs, kT, gram_smem(ld, U != V, uc.n, vc.n), s>>>(U, V, ld, uc, vc, n, partial, ticket,
                                                                           out, gram_stages(ld, U != V), stop);
+        const int ab = uc.n * vc.n;
+        gram_finish_kernel<<<(unsigned)((ab + 31) / 32), 256, 0, s>>>(partial, kRedCTAs, ab, out, stop);
         CK(cudaGetLastError());
     }
     std::vector<double> gram(const double* U, const Cols& uc, const double* V, const Cols& vc) {
