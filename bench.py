@@ -202,13 +202,15 @@ class ClockSampler:
 
 
 # -------------------------------------------------------------- algorithmic bytes --------
-def kernel_bytes(solver, n, nnz, h, value_dict, uniform_diag, xw_modes=(), pair=False):
+def kernel_bytes(solver, n, nnz, h, value_dict, uniform_diag, xw_modes=(), pair=False, defer_x=False):
     """Per-launch algorithmic bytes of THIS implementation's kernels in the stored format in
     use (value dictionary: 5 B/entry + a 2 KB table instead of 12 B/entry; constant Jacobi
     diagonal: passed as a scalar, no d stream; x-window SpMV (modes in xw_modes): the 4-byte
     column becomes a 2-byte offset into the round's TMA-staged x windows, + a 64-byte
     descriptor per 256-row round, x still counted once).  Returns [(kernel name, bytes)] in
-    launch order.  CG: x += a p is moved into update 2 (p streamed once per iteration)."""
+    launch order.  CG: x += a p is moved into update 2 (p streamed once per iteration);
+    defer_x (single-GPU multi-kernel CG): x is read and written every other iteration from two
+    alternating direction buffers — update 2 averages 36 instead of 40 bytes per row."""
     rounds = (n + 255) // 256
 
     def mat(mode):
@@ -222,7 +224,7 @@ def kernel_bytes(solver, n, nnz, h, value_dict, uniform_diag, xw_modes=(), pair=
     if solver == "cg":
         return [("spmv_cg", mat(1) + rp + 8 * (n + h) + 8 * n),  # A, row_ptr, p gathered, q written
                 ("cg_update1", 24 * n + d),                      # read r q (d), write r
-                ("cg_update2", 40 * n + d)]                      # read x p r (d), write x p
+                ("cg_update2", (36 if defer_x else 40) * n + d)]  # read x p r (d), write x p (x: every other)
     return [("bicg_update1", 40 * n + d),                        # read r p v (d), write p ph
             ("spmv_v", mat(2) + rp + 8 * (n + h) + 16 * n),      # ph gathered, v written, rh read
             ("bicg_update2", 32 * n + d),                        # read r v (d), write s sh
@@ -430,7 +432,8 @@ def run_ours(args):
     sv.iterate(5)
     kms = sv.kernel_times(args.kernel_iters)
     sv.close()
-    kb = kernel_bytes(solver, n, nnz, 0, fmt["value_dict"], fmt["uniform_diag"], xw["modes"], xw["stream"] == 2)
+    kb = kernel_bytes(solver, n, nnz, 0, fmt["value_dict"], fmt["uniform_diag"], xw["modes"], xw["stream"] == 2,
+                      defer_x=solver == "cg" and os.environ.get("SPARSLA_CG_DEFER_X", "1") != "0")
     it_bytes = sum(b for _, b in kb)
     dom = max(range(len(kms)), key=lambda i: kms[i]) if solver == "cg" else \
         max((i for i, (nm, _) in enumerate(kb) if nm.startswith("spmv")), key=lambda i: kms[i])
@@ -460,7 +463,8 @@ def run_ours(args):
             q1.synchronize()
             pms = q0.elapsed_time(q1) / args.plain_steps
             pk = svp.kernel_times(10)
-            pkb = kernel_bytes(solver, n, nnz, 0, False, False, xwp["modes"])
+            pkb = kernel_bytes(solver, n, nnz, 0, False, False, xwp["modes"],
+                               defer_x=solver == "cg" and os.environ.get("SPARSLA_CG_DEFER_X", "1") != "0")
             out = {"value": 1e3 / pms, "unit": "it/s", "steps": args.plain_steps, "ms_per_step": pms,
                    "kernel_ms": {nm: t for (nm, _), t in zip(pkb, pk)},
                    "kernel_gbs": {nm: b / (t * 1e-3) / 1e9 for (nm, b), t in zip(pkb, pk)},

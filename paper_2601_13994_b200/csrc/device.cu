@@ -1015,6 +1015,12 @@ Solver::Solver(DevCsr* A_, int backend_, const sparsla_solve_options& o, DistCtx
         sh = dalloc<double>(nh); t = dalloc<double>(nv);
     }
     partials = dalloc<double>(3 * m);
+    // single-GPU CG: x updated every other iteration from two alternating direction
+    // buffers (bit-identical; SPARSLA_CG_DEFER_X=0 disables).  Not with the fused kernel.
+    {
+        const char* e = getenv("SPARSLA_CG_DEFER_X");
+        defer_x = !dist && backend == SPARSLA_BACKEND_CG && n > 0 && !(e && atoi(e) == 0);
+    }
     // small single-GPU CG problems: whole iterations in one cooperative kernel
     if (!dist && backend == SPARSLA_BACKEND_CG && n > 0) {
         int coop = 0, sms = 0, per_sm = 0;
@@ -1027,7 +1033,7 @@ Solver::Solver(DevCsr* A_, int backend_, const sparsla_solve_options& o, DistCtx
         // matrices with long (hub) rows — those take the warp-per-row split of the SpMV
         fused = coop && cap > 0 && m <= cap && A->nlong == 0 && A->max_row <= kLongMin;
         if (const char* e = getenv("SPARSLA_FUSED")) fused = coop && cap > 0 && atoi(e) != 0;
-        if (fused) { fused_bar = dalloc<unsigned>(1); }
+        if (fused) { fused_bar = dalloc<unsigned>(1); defer_x = false; }
         // resident chunk images when every chunk fits uint16 offsets / int16 column deltas and
         // the whole grid stays co-resident with the larger shared-memory footprint
         const char* re = getenv("SPARSLA_FUSED_RESIDENT");
@@ -1066,6 +1072,7 @@ Solver::Solver(DevCsr* A_, int backend_, const sparsla_solve_options& o, DistCtx
             }
         }
     }
+    if (defer_x) p2 = dalloc<double>(nh);
     tickets = dalloc<unsigned>(8);
     CK(cudaMemset(tickets, 0, 8 * sizeof(unsigned)));
     st = dalloc<KState>(1);
@@ -1086,14 +1093,15 @@ void Solver::release() noexcept {
     p2p_release();
     if (g_many) cudaGraphExecDestroy(g_many);
     if (g_one) cudaGraphExecDestroy(g_one);
-    for (double* v : {x_own, b_own, r, p, q, rh, ph, s, sh, t}) cudaFree(v);
+    if (g_one_odd) cudaGraphExecDestroy(g_one_odd);
+    for (double* v : {x_own, b_own, r, p, p2, q, rh, ph, s, sh, t}) cudaFree(v);
     cudaFree(partials); cudaFree(tickets); cudaFree(st); cudaFree(fused_bar);
     if (h_st) cudaFreeHost(h_st);
     if (h_flag) cudaFreeHost(h_flag);
     if (ev[0]) cudaEventDestroy(ev[0]);
     if (ev[1]) cudaEventDestroy(ev[1]);
-    g_many = g_one = nullptr;
-    x_own = b_own = r = p = q = rh = ph = s = sh = t = nullptr;
+    g_many = g_one = g_one_odd = nullptr;
+    x_own = b_own = r = p = p2 = q = rh = ph = s = sh = t = nullptr;
     partials = nullptr; tickets = nullptr; st = nullptr; fused_bar = nullptr;
     h_st = nullptr; h_flag = nullptr; ev[0] = ev[1] = nullptr;
     cudaGetLastError();
@@ -1109,7 +1117,9 @@ RedParams Solver::red(int which, int slot) const {
 
 VecParams Solver::vparams() const {
     VecParams P{};
-    P.n = n; P.d = d_is_uniform ? nullptr : dinv; P.d_uni = d_uniform; P.x = x; P.r = r; P.p = p; P.q = q;
+    P.n = n; P.d = d_is_uniform ? nullptr : dinv; P.d_uni = d_uniform; P.x = x; P.r = r; P.q = q;
+    P.p = swap_p ? p2 : p;   // deferred x update, odd iterations: the current direction is in p2
+    P.p2 = swap_p ? p : p2;
     P.rh = rh; P.ph = ph; P.v = q; P.s = s; P.sh = sh; P.tt = t; P.b = b;
     P.check_done = 1;
     return P;
@@ -1224,11 +1234,20 @@ void Solver::enqueue_init() {
     }
 }
 
-void Solver::enqueue_iteration(cudaEvent_t* evs) {
-    // evs (optional): launches_per_iteration()+1 events recorded around every kernel
+void Solver::enqueue_iteration(cudaEvent_t* evs, int par) {
+    // evs (optional): launches_per_iteration()+1 events recorded around every kernel;
+    // par: iteration parity (deferred x update: which direction buffer is current)
     auto mark = [&](int i) { if (evs) CK(cudaEventRecord(evs[i], stream)); };
     mark(0);
-    if (backend == SPARSLA_BACKEND_CG) {
+    if (backend == SPARSLA_BACKEND_CG && defer_x) {
+        swap_p = par != 0;
+        spmv_point(SPMV_CG, swap_p ? p2 : p, q, nullptr, SC_CG_PQ, 1, 1); mark(1);
+        vec_point<V_CG_U1>(SC_CG_RR, 2, 1); mark(2);
+        if (par == 0) vec_point<V_CG_U2E>(SC_NONE, 3, 1);
+        else vec_point<V_CG_U2O>(SC_NONE, 3, 1);
+        mark(3);
+        swap_p = false;
+    } else if (backend == SPARSLA_BACKEND_CG) {
         spmv_point(SPMV_CG, p, q, nullptr, SC_CG_PQ, 1, 1); mark(1);
         vec_point<V_CG_U1>(SC_CG_RR, 2, 1); mark(2);
         vec_point<V_CG_U2>(SC_NONE, 3, 1); mark(3);
@@ -1260,7 +1279,10 @@ void Solver::kernel_times(long long iters, double* ms) {
     }
     std::vector<cudaEvent_t> evs((size_t)iters * (L + 1));
     for (auto& e : evs) CK(cudaEventCreate(&e));
-    for (long long it = 0; it < iters; ++it) enqueue_iteration(evs.data() + it * (L + 1));
+    for (long long it = 0; it < iters; ++it) {
+        enqueue_iteration(evs.data() + it * (L + 1), parity);
+        if (defer_x) parity ^= 1;
+    }
     CK(cudaStreamSynchronize(stream));
     for (int k = 0; k < L; ++k) ms[k] = 0.0;
     for (long long it = 0; it < iters; ++it)
@@ -1276,18 +1298,19 @@ long long Solver::launches_per_iteration() const { return backend == SPARSLA_BAC
 
 void Solver::build_graphs() {
     if (g_many || !capturable()) return;
-    auto capture = [&](int iters) {
+    auto capture = [&](int iters, int par0) {  // deferred x: parities alternate from par0
         cudaGraph_t graph;
         CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
-        for (int i = 0; i < iters; ++i) enqueue_iteration();
+        for (int i = 0; i < iters; ++i) enqueue_iteration(nullptr, defer_x ? (par0 + i) & 1 : 0);
         CK(cudaStreamEndCapture(stream, &graph));
         cudaGraphExec_t exec;
         CK(cudaGraphInstantiate(&exec, graph, 0));
         CK(cudaGraphDestroy(graph));
         return exec;
     };
-    g_many = capture(kGraphIters);
-    g_one = capture(1);
+    g_many = capture(kGraphIters, 0);  // even length: starts and ends on an even iteration
+    g_one = capture(1, 0);
+    if (defer_x) g_one_odd = capture(1, 1);
 }
 
 void Solver::set_b(const double* src, int mem) {
@@ -1296,10 +1319,30 @@ void Solver::set_b(const double* src, int mem) {
     else { b = b_own; CK(cudaMemcpyAsync(b_own, src, n * sizeof(double), cudaMemcpyHostToDevice, stream)); }
 }
 
+// Deferred x update: after an even number of iterations x lacks alpha_prev * p_prev (p_prev
+// is in p: even iterations leave the next direction in p2).  Apply it before x is read
+// mid-solve; the flag is cleared so the next odd iteration does not apply it again.
+static __global__ void cg_flush_x_kernel(double* x, const double* pprev, long long n, double a) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) x[i] = __dadd_rn(x[i], __dmul_rn(a, pprev[i]));
+}
+void Solver::flush_x() {
+    if (!defer_x) return;
+    CK(cudaMemcpyAsync(h_st, st, sizeof(KState), cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    if (!h_st->x_lag) return;
+    cg_flush_x_kernel<<<grid_for(n, 256), 256, 0, stream>>>(x, p, n, h_st->alpha_prev);
+    CK(cudaGetLastError());
+    const int zero = 0;
+    CK(cudaMemcpyAsync(&st->x_lag, &zero, sizeof(int), cudaMemcpyHostToDevice, stream));
+    CK(cudaStreamSynchronize(stream));
+}
+
 void Solver::reset() {
     DeviceGuard g(A->device);
     build_graphs();
     enqueue_init();
+    parity = 0;
 }
 
 bool Solver::capturable() const { return !fused && (!dist || dist->tr->capturable()); }
@@ -1335,11 +1378,18 @@ void Solver::iterate(long long iters) {
         return;
     }
     if (!capturable()) {
-        while (iters-- > 0) enqueue_iteration();
+        while (iters-- > 0) {
+            enqueue_iteration(nullptr, parity);
+            if (defer_x) parity ^= 1;
+        }
         return;
     }
+    if (parity && iters > 0) { CK(cudaGraphLaunch(g_one_odd, stream)); --iters; parity = 0; }
     while (iters >= kGraphIters) { CK(cudaGraphLaunch(g_many, stream)); iters -= kGraphIters; }
-    while (iters-- > 0) CK(cudaGraphLaunch(g_one, stream));
+    while (iters-- > 0) {
+        CK(cudaGraphLaunch(parity ? g_one_odd : g_one, stream));
+        if (defer_x) parity ^= 1;
+    }
 }
 
 void Solver::run() {
@@ -1354,8 +1404,15 @@ void Solver::run() {
     for (long long i = 0; i < max_graphs; ++i) {
         last = i;
         if (fused) enqueue_fused(4 * kGraphIters);
-        else if (capturable()) CK(cudaGraphLaunch(g_many, stream));
-        else for (int k = 0; k < kGraphIters; ++k) enqueue_iteration();
+        else if (capturable()) {
+            if (parity) { CK(cudaGraphLaunch(g_one_odd, stream)); parity = 0; }  // back to even
+            CK(cudaGraphLaunch(g_many, stream));
+        } else {
+            for (int k = 0; k < kGraphIters; ++k) {
+                enqueue_iteration(nullptr, parity);
+                if (defer_x) parity ^= 1;
+            }
+        }
         CK(cudaMemcpyAsync(h_flag + (i & 1), &st->done, sizeof(int), cudaMemcpyDeviceToHost, stream));
         CK(cudaEventRecord(ev[i & 1], stream));
         if (i > 0) {
@@ -1804,6 +1861,7 @@ int sparsla_solver_get_x(sparsla_solver* S, double* x, int32_t mem) {
     return guarded([&] {
         Solver* s = S->S;
         DeviceGuard g(s->A->device);
+        s->flush_x();
         CK(cudaMemcpyAsync(x, s->x, s->n * sizeof(double),
                            mem == SPARSLA_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s->stream));
         CK(cudaStreamSynchronize(s->stream));

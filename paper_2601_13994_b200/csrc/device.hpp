@@ -155,6 +155,12 @@ struct Solver {
     double* x = nullptr;
     double *x_own = nullptr, *b_own = nullptr;
     double *r = nullptr, *p = nullptr, *q = nullptr;
+    // deferred x update (single-GPU CG, kernels.cuh V_CG_U2E / V_CG_U2O): second direction
+    // buffer, host-side iteration parity, and which buffer holds the current direction
+    double* p2 = nullptr;
+    bool defer_x = false;
+    int parity = 0;
+    bool swap_p = false;
     double *rh = nullptr, *ph = nullptr, *s = nullptr, *sh = nullptr, *t = nullptr;
     double* partials = nullptr;
     unsigned* tickets = nullptr;
@@ -162,7 +168,7 @@ struct Solver {
     KState* h_st = nullptr;
     int* h_flag = nullptr;
     cudaEvent_t ev[2] = {nullptr, nullptr};
-    cudaGraphExec_t g_many = nullptr, g_one = nullptr;
+    cudaGraphExec_t g_many = nullptr, g_one = nullptr, g_one_odd = nullptr;
     bool fused = false;          // small CG: cg_fused_kernel runs whole iterations
     long long values_version = 0;  // A->values_version when this solver was built
     // fused peer-memory collectives (distributed CG)
@@ -183,6 +189,7 @@ struct Solver {
     void run();
     void wait_event(cudaEvent_t e);  // distributed: polls the transport, times out
     void report(sparsla_solve_report* rep);
+    void flush_x();  // deferred x update: complete x before it is read mid-solve
     long long launches_per_iteration() const;
     void kernel_times(long long iters, double* ms);
 
@@ -199,7 +206,7 @@ struct Solver {
     void p2p_setup();     // collective (dist.cu)
     void p2p_release() noexcept;
     void enqueue_fused(long long iters);
-    void enqueue_iteration(cudaEvent_t* evs = nullptr);
+    void enqueue_iteration(cudaEvent_t* evs = nullptr, int par = 0);
     void build_graphs();
 };
 

@@ -48,6 +48,8 @@ struct KState {
     long long k, spmv_count, breakdown_iter;
     long long reductions;  // reduction points applied while the solve was live
     int pending_x;         // CG: alpha of this iteration computed, x += alpha p still to apply
+    int x_lag;             // CG, deferred x update: x still lacks alpha_prev * p_prev (U2E -> U2O)
+    double alpha_prev;
     unsigned long long ep[8];       // fused peer collectives: epochs pushed per reduction point
     unsigned long long ep_halo[4];  // ... and per halo-pushed vector
     int done, converged, status, halfstep;
@@ -1132,6 +1134,7 @@ struct VecParams {
     const double* d;  // Jacobi inverse diagonal; nullptr: uniform diagonal d_uni (not streamed)
     double d_uni;
     double *x, *r, *p, *q;
+    double* p2;  // CG deferred x update: the other direction buffer (previous / next p)
     double *rh, *ph, *v, *s, *sh, *tt;
     const double* b;
     int check_done;
@@ -1278,7 +1281,12 @@ static __global__ void short_view_values_kernel(const int32_t* rp, const double*
     for (int k = b; k < e; ++k) s_val[k] = val[o + (k - b)];
 }
 
-enum VecOp : int { V_CG_INIT, V_CG_U1, V_CG_U2, V_BI_INIT, V_BI_U1, V_BI_U2, V_BI_U3 };
+enum VecOp : int { V_CG_INIT, V_CG_U1, V_CG_U2, V_BI_INIT, V_BI_U1, V_BI_U2, V_BI_U3, V_CG_U2E, V_CG_U2O };
+// Deferred x update (single GPU CG): two p buffers alternate.  Even iterations (U2E) only
+// form the next direction p' = z + beta p into the other buffer — x keeps lagging alpha p;
+// odd iterations (U2O) apply both steps, x = (x + alpha_prev p_prev) + alpha p, then form p'.
+// The same two roundings in the same order as updating x every iteration (bit-identical),
+// with x streamed every other iteration: 36 instead of 40 bytes per row per iteration.
 // CG iteration split used by the solver: U1 = r -= a q, z = d r, {r.z, r.r} (reads r q d);
 // U2 = x += a p, then p = z + b p unless the solve just terminated (reads x p r d).  p is
 // streamed once per iteration instead of twice (100 n instead of 108 n bytes); the x update
@@ -1287,6 +1295,8 @@ template <int OP> struct VecTraits;
 template <> struct VecTraits<V_CG_INIT> { static constexpr int nin = 3, ndot = 3; };  // b q d
 template <> struct VecTraits<V_CG_U1>   { static constexpr int nin = 3, ndot = 2; };  // r q d
 template <> struct VecTraits<V_CG_U2>   { static constexpr int nin = 4, ndot = 0; };  // x p r d
+template <> struct VecTraits<V_CG_U2E>  { static constexpr int nin = 4, ndot = 0; };  // p r d (x only at the end)
+template <> struct VecTraits<V_CG_U2O>  { static constexpr int nin = 5, ndot = 0; };  // x p_prev p r d
 template <> struct VecTraits<V_BI_INIT> { static constexpr int nin = 2, ndot = 3; };  // b v
 template <> struct VecTraits<V_BI_U1>   { static constexpr int nin = 4, ndot = 0; };  // r p v d
 template <> struct VecTraits<V_BI_U2>   { static constexpr int nin = 3, ndot = 1; };  // r v d; s.s
@@ -1297,13 +1307,22 @@ template <> struct VecPublishOnly<V_BI_U2> { static constexpr int row = 2; };
 template <> struct VecTraits<V_BI_U3>   { static constexpr int nin = 6, ndot = 2; };  // x ph s sh t rh
 
 struct VecScalars {
-    double alpha, beta, omega;
-    int first, half, live;
+    double alpha, beta, omega, alpha_prev;
+    int first, half, live, lag, pend;
 };
 
 template <int OP>
-__device__ __forceinline__ void vec_load(const VecParams& P, long long i, double2 (&in)[VecTraits<OP>::nin]) {
+__device__ __forceinline__ void vec_load(const VecParams& P, const VecScalars& S, long long i,
+                                         double2 (&in)[VecTraits<OP>::nin]) {
     const long long n = P.n;
+    if constexpr (OP == V_CG_U2E) {  // x only when the solve ends here (apply alpha p at once)
+        in[0] = ld2(P.p, i, n); in[1] = ld2(P.r, i, n); in[2] = ldd(P.d, P.d_uni, i, n);
+        in[3] = S.live ? make_double2(0.0, 0.0) : ld2(P.x, i, n);
+    }
+    if constexpr (OP == V_CG_U2O) {
+        in[0] = ld2(P.x, i, n); in[1] = ld2(P.p2, i, n); in[2] = ld2(P.p, i, n); in[3] = ld2(P.r, i, n);
+        in[4] = ldd(P.d, P.d_uni, i, n);
+    }
     if constexpr (OP == V_CG_INIT) { in[0] = ld2(P.b, i, n); in[1] = ld2(P.q, i, n); in[2] = ldd(P.d, P.d_uni, i, n); }
     if constexpr (OP == V_CG_U1) { in[0] = ld2(P.r, i, n); in[1] = ld2(P.q, i, n); in[2] = ldd(P.d, P.d_uni, i, n); }
     if constexpr (OP == V_CG_U2) {
@@ -1347,6 +1366,22 @@ __device__ __forceinline__ void vec_compute(const VecParams& P, const VecScalars
             const double z = __dmul_rn(lane(in[3], e), lane(in[2], e));
             set_lane(o1, e, __dadd_rn(z, __dmul_rn(S.beta, lane(in[1], e))));
         }
+        if constexpr (OP == V_CG_U2E) {  // p' = z + beta p (x lags alpha p), or x += alpha p at the end
+            if (S.live) {
+                const double z = __dmul_rn(lane(in[2], e), lane(in[1], e));
+                set_lane(o1, e, __dadd_rn(z, __dmul_rn(S.beta, lane(in[0], e))));
+            } else {
+                set_lane(o0, e, __dadd_rn(lane(in[3], e), __dmul_rn(S.alpha, lane(in[0], e))));
+            }
+        }
+        if constexpr (OP == V_CG_U2O) {  // x = (x + a_prev p_prev) + a p; p' = z + beta p
+            double xn = lane(in[0], e);
+            if (S.lag) xn = __dadd_rn(xn, __dmul_rn(S.alpha_prev, lane(in[1], e)));
+            if (S.pend) xn = __dadd_rn(xn, __dmul_rn(S.alpha, lane(in[2], e)));
+            set_lane(o0, e, xn);
+            const double z = __dmul_rn(lane(in[4], e), lane(in[3], e));
+            set_lane(o1, e, __dadd_rn(z, __dmul_rn(S.beta, lane(in[2], e))));
+        }
         if constexpr (OP == V_BI_INIT) {  // r = b - v; rhat = r; {rh.r, r.r, b.b}
             const double b = lane(in[0], e);
             const double r = __dsub_rn(b, lane(in[1], e));
@@ -1384,6 +1419,14 @@ __device__ __forceinline__ void vec_compute(const VecParams& P, const VecScalars
         st2(P.x, i, n, o0);
         if (S.live) st2(P.p, i, n, o1);  // the solve continues: new direction
     }
+    if constexpr (OP == V_CG_U2E) {
+        if (S.live) st2(P.p2, i, n, o1);
+        else st2(P.x, i, n, o0);
+    }
+    if constexpr (OP == V_CG_U2O) {
+        st2(P.x, i, n, o0);
+        if (S.live) st2(P.p2, i, n, o1);  // overwrites p_prev, read above by this thread
+    }
     if constexpr (OP == V_BI_INIT) { st2(P.r, i, n, o0); st2(P.rh, i, n, o0); }
     if constexpr (OP == V_BI_U1) { st2(P.p, i, n, o0); st2(P.ph, i, n, o1); }
     if constexpr (OP == V_BI_U2) { st2(P.s, i, n, o0); st2(P.sh, i, n, o1); }
@@ -1396,7 +1439,11 @@ __global__ void __launch_bounds__(kVecThreads) vec_kernel(VecParams P) {
     constexpr int ND = VecTraits<OP>::ndot;
     constexpr int NA = ND > 0 ? ND : 1;
     KState* st = P.red.st;
-    if constexpr (OP == V_CG_U2) {
+    if constexpr (OP == V_CG_U2E) {
+        if (!st->pending_x) return;
+    } else if constexpr (OP == V_CG_U2O) {
+        if (!st->pending_x && !st->x_lag) return;  // also after a breakdown: the lagging step
+    } else if constexpr (OP == V_CG_U2) {
         if (!st->pending_x) return;  // runs once more after termination to apply x += a p
     } else {
         if (P.check_done && st->done) return;
@@ -1425,6 +1472,11 @@ __global__ void __launch_bounds__(kVecThreads) vec_kernel(VecParams P) {
     VecScalars S;
     if constexpr (OP == V_CG_U1 || OP == V_BI_U2) S.alpha = sc->alpha;
     if constexpr (OP == V_CG_U2) { S.alpha = sc->alpha; S.beta = sc->beta; S.live = !sc->done; }
+    if constexpr (OP == V_CG_U2E) { S.alpha = sc->alpha; S.beta = sc->beta; S.live = !sc->done; }
+    if constexpr (OP == V_CG_U2O) {
+        S.alpha = sc->alpha; S.beta = sc->beta; S.alpha_prev = sc->alpha_prev; S.live = !sc->done;
+        S.lag = sc->x_lag; S.pend = sc->pending_x;
+    }
     if constexpr (OP == V_BI_U1) { S.beta = sc->beta; S.omega = sc->omega; S.first = sc->k == 0; }
     if constexpr (OP == V_BI_U3) { S.alpha = sc->alpha; S.omega = sc->omega; S.half = sc->halfstep; }
     const int t = threadIdx.x;
@@ -1441,7 +1493,7 @@ __global__ void __launch_bounds__(kVecThreads) vec_kernel(VecParams P) {
     for (int g = 0; g < kChunkRounds; g += G) {
         double2 in[G][NIN];
 #pragma unroll
-        for (int u = 0; u < G; ++u) vec_load<OP>(P, base + (long long)(g + u) * kChunkSlots + 2 * t, in[u]);
+        for (int u = 0; u < G; ++u) vec_load<OP>(P, S, base + (long long)(g + u) * kChunkSlots + 2 * t, in[u]);
 #pragma unroll
         for (int u = 0; u < G; ++u) {
             const long long i = base + (long long)(g + u) * kChunkSlots + 2 * t;
@@ -1526,6 +1578,23 @@ __global__ void __launch_bounds__(kVecThreads) vec_kernel(VecParams P) {
                 } else {
                     st->pending_x = 0;
                 }
+                *P.red.ticket = 0u;
+                __threadfence();
+            }
+        }
+    } else if constexpr (OP == V_CG_U2E || OP == V_CG_U2O) {
+        // the last CTA (every CTA has read the scalars) updates the deferral state: after an
+        // even step that continues, x lags alpha p; after an odd step x is complete
+        __syncthreads();
+        if (t == 0) {
+            __threadfence();
+            if (atomicAdd(P.red.ticket, 1u) == P.red.expected - 1) {
+                if constexpr (OP == V_CG_U2E) {
+                    if (S.live) { st->alpha_prev = S.alpha; st->x_lag = 1; }
+                } else {
+                    st->x_lag = 0;
+                }
+                st->pending_x = 0;
                 *P.red.ticket = 0u;
                 __threadfence();
             }

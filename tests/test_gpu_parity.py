@@ -266,17 +266,29 @@ def test_config_A_full(S, O, gpu):
     assert_bitwise(x, xo)
 
 
-def test_persistent_solver_fixed_iterations(S, O, gpu):
-    """Solver.iterate(k) after reset == oracle CG truncated at k iterations, bitwise."""
+@pytest.mark.parametrize("fused", ["1", "0"])
+def test_persistent_solver_fixed_iterations(S, O, gpu, monkeypatch, fused):
+    """Solver.iterate(k) after reset == oracle CG truncated at k iterations, bitwise.  With
+    the multi-kernel loop (SPARSLA_FUSED=0) x is updated every other iteration from two
+    direction buffers: odd k leave a lagging step that reading x must flush, and the solve
+    must continue bit-exactly after such a mid-solve read."""
+    monkeypatch.setenv("SPARSLA_FUSED", fused)
     A = O.generate("poisson3d", 64)
     b = np.ones(A.nrows)
     sv = S.Solver(to_S(S, A), b, "cg", S.SolveOptions(atol=0.0, rtol=1e-30, max_iter=10**6))
-    for k in (1, 7, 40):
+    for k in (1, 2, 7, 40):
         sv.reset()
         sv.iterate(k)
         xo, _ = O.cg_fixed(A, b, k)
         assert sv.report().iterations == k
         assert_bitwise(sv.x(), xo, f"k={k}")
+    sv.reset()
+    for k0, k in ((3, 3), (4, 7), (17, 24), (1, 25)):  # reads after odd and even counts
+        sv.iterate(k0)
+        xo, _ = O.cg_fixed(A, b, k)
+        assert_bitwise(sv.x(), xo, f"resumed k={k}")
+    rep = sv.report()
+    assert rep.iterations == 25
 
 
 @pytest.mark.parametrize("kind,p1,p2,fp,backend", [("poisson3d", 40, 0, 0.0, "cg"), ("poisson2d", 200, 0, 0.0, "cg"),
