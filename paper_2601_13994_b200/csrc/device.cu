@@ -165,22 +165,29 @@ struct XwVariant {
     int vs;  // value stream: 0 fp64 values, 1 dictionary indices, 2 pair (index in the offset)
     int w, stg, minb;
     const void* fn[4];  // per SpmvMode
+    bool fix;           // compile-time stage layout (kXwFixCapC / kXwFixCapX)
 };
 #define XWV(VS, W, S, M)                                                                            \
     {VS, W, S, M, {(const void*)spmv_xw_kernel<SPMV_PLAIN, S, M, W, VS>, (const void*)spmv_xw_kernel<SPMV_CG, S, M, W, VS>, \
-                   (const void*)spmv_xw_kernel<SPMV_BICG_V, S, M, W, VS>, (const void*)spmv_xw_kernel<SPMV_BICG_T, S, M, W, VS>}}
+                   (const void*)spmv_xw_kernel<SPMV_BICG_V, S, M, W, VS>, (const void*)spmv_xw_kernel<SPMV_BICG_T, S, M, W, VS>}, false}
+#define XWVF(VS, W, S, M)                                                                           \
+    {VS, W, S, M, {(const void*)spmv_xw_kernel<SPMV_PLAIN, S, M, W, VS, true>, (const void*)spmv_xw_kernel<SPMV_CG, S, M, W, VS, true>, \
+                   (const void*)spmv_xw_kernel<SPMV_BICG_V, S, M, W, VS, true>, (const void*)spmv_xw_kernel<SPMV_BICG_T, S, M, W, VS, true>}, true}
 static const XwVariant kXwVariants[] = {XWV(1, 8, 3, 3), XWV(1, 8, 2, 4), XWV(1, 8, 3, 4),
                                         XWV(0, 8, 3, 2), XWV(0, 12, 3, 2), XWV(0, 12, 2, 3),
                                         XWV(2, 8, 3, 3), XWV(2, 8, 2, 4), XWV(2, 8, 3, 4),
-                                        XWV(1, 7, 3, 4), XWV(2, 7, 3, 4), XWV(0, 7, 2, 3)};
+                                        XWV(1, 7, 3, 4), XWV(2, 7, 3, 4), XWV(0, 7, 2, 3),
+                                        XWVF(2, 7, 3, 4)};
 // (measured and dropped: pair 7-wide at 4 stages / 3 CTAs per SM 0.840 ms and at 2 stages /
 // 5 CTAs per SM, 40 registers with spills, 0.999 ms — vs 0.792 ms for 3 stages / 4 CTAs)
 #undef XWV
+#undef XWVF
 constexpr int kNumXwVariants = sizeof(kXwVariants) / sizeof(kXwVariants[0]);
 
 static size_t xw_smem_bytes(const DevCsr* A, int var, bool aux) {
     const XwVariant& V = kXwVariants[var];
-    return kXwHead + (size_t)V.stg * XwLayout(A->cap_v, A->cap_c, A->cap_x, V.vs, aux).stage;
+    const XwLayout L = V.fix ? XwLayout(0, kXwFixCapC, kXwFixCapX, V.vs, aux) : XwLayout(A->cap_v, A->cap_c, A->cap_x, V.vs, aux);
+    return kXwHead + (size_t)V.stg * L.stage;
 }
 
 // Variant per value stream and row lengths; -1 = none.
@@ -194,9 +201,12 @@ static void choose_xw_variants(DevCsr* A) {
     A->xw_var[0] = w7 ? 11 : 5;
     A->xw_var[1] = w7 ? 9 : 0;
     A->xw_var[2] = w7 ? 10 : 8;
+    // compile-time layout when the rounds fit it (7-point stencils up to 464^3 and beyond)
+    if (w7 && A->cap_c <= kXwFixCapC && A->cap_x <= kXwFixCapX && !getenv("SPARSLA_XW_NOFIX")) A->xw_var[2] = 12;
     if (const char* e = getenv("SPARSLA_XW_VARIANT")) {
         const int x = atoi(e);
-        if (x >= 0 && x < kNumXwVariants) A->xw_var[kXwVariants[x].vs] = x;
+        const bool fits = !kXwVariants[x].fix || (A->cap_c <= kXwFixCapC && A->cap_x <= kXwFixCapX);
+        if (x >= 0 && x < kNumXwVariants && fits) A->xw_var[kXwVariants[x].vs] = x;
     }
     int dev = A->device, sms = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));

@@ -63,7 +63,8 @@ struct XwLayout {
     size_t ooff, roff, xoff, aoff;
     // vs: value stream 0 = fp64 values, 1 = 1-byte dictionary indices, 2 = none (the value
     // index travels in the top 5 bits of the 16-bit offset: "pair" stream)
-    __host__ __device__ XwLayout(int cap_v, int cap_c, int cap_x, int vs, bool aux) {
+    __host__ __device__ constexpr XwLayout(int cap_v, int cap_c, int cap_x, int vs, bool aux)
+        : vbytes(0), obytes(0), rbytes(0), xbytes(0), abytes(0), stage(0), ooff(0), roff(0), xoff(0), aoff(0) {
         vbytes = vs == 2 ? 0 : ((size_t)cap_v * (vs ? 1 : 8) + (vs ? 32 : 0) + 127) & ~size_t(127);
         obytes = ((size_t)cap_c * 2 + 64 + 127) & ~size_t(127);  // 16-bit window offsets (+ spares)
         rbytes = (kRpCopy * 4 + 127) & ~size_t(127);
@@ -82,7 +83,12 @@ constexpr size_t kXwHead = 1024 + 2 * kChunkRounds * kXwDescInts * 4;
 
 template <int MODE> struct XwAux { static constexpr bool on = (MODE == SPMV_BICG_V || MODE == SPMV_BICG_T); };
 
-template <int MODE, int STG, int MINB, int W, int VS>
+// FIX: compile-time stage layout for matrices whose rounds fit kXwFixCapC offsets and
+// kXwFixCapX staged x elements (stencils): the per-round stage addressing folds into
+// immediates instead of being rematerialised from the parameters at 56 registers
+constexpr int kXwFixCapC = 2016;  // (2016 * 2 + 64) bytes = 4 KB of offsets
+constexpr int kXwFixCapX = 1536;
+template <int MODE, int STG, int MINB, int W, int VS, bool FIX = false>
 __global__ void __launch_bounds__(kWsThreads, MINB) spmv_xw_kernel(SpmvParams P) {
     constexpr bool VD = VS != 0;     // values from the dictionary table
     constexpr bool PAIR = VS == 2;   // ... indexed by the top bits of the offset stream
@@ -100,7 +106,7 @@ __global__ void __launch_bounds__(kWsThreads, MINB) spmv_xw_kernel(SpmvParams P)
     uint64_t* empty = full + STG;
     uint64_t* dbar = empty + STG;  // [2]
     int32_t* dbuf = reinterpret_cast<int32_t*>(smem + 1024);
-    const XwLayout L(P.cap_v, P.cap_c, P.cap_x, VS, AUX);
+    const XwLayout L = FIX ? XwLayout(0, kXwFixCapC, kXwFixCapX, VS, AUX) : XwLayout(P.cap_v, P.cap_c, P.cap_x, VS, AUX);
     unsigned char* stage0 = smem + kXwHead;
     const int t = threadIdx.x;
     const int warp = t >> 5, lane = t & 31;

@@ -12,7 +12,7 @@ from test_gpu_parity import _banded, assert_bitwise, random_csr, rep_eq, to_S
 pytestmark = pytest.mark.gpu
 
 # kXwVariants in csrc/device.cu: value stream per variant (0 plain fp64, 1 dictionary, 2 pair)
-XW_STREAM = [1, 1, 1, 0, 0, 0, 2, 2, 2, 1, 2, 0]
+XW_STREAM = [1, 1, 1, 0, 0, 0, 2, 2, 2, 1, 2, 0, 2]
 N_XW_VARIANTS = len(XW_STREAM)
 
 

@@ -18,7 +18,7 @@ from paper_2601_13994_b200 import sparsla as S  # noqa: E402
 
 PEAK = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
     if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
-XW_STREAM = [1, 1, 1, 0, 0, 0, 2, 2, 2, 1, 2, 0]  # value stream of kXwVariants (device.cu)
+XW_STREAM = [1, 1, 1, 0, 0, 0, 2, 2, 2, 1, 2, 0, 2]  # value stream of kXwVariants (device.cu)
 CFG = {"B": ("poisson3d", 464, 0, 0.0, "cg"), "E": ("poisson3d", 368, 0, 0.0, "cg"),
        "D": ("convdiff3d", 368, 0, 0.1, "bicgstab"), "C": ("fem2d", 4474, 2601, 0.0, "cg")}
 
