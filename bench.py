@@ -202,7 +202,7 @@ class ClockSampler:
 
 
 # -------------------------------------------------------------- algorithmic bytes --------
-def kernel_bytes(solver, n, nnz, h, value_dict, uniform_diag, xw_modes=(), pair=False, defer_x=False):
+def kernel_bytes(solver, n, nnz, h, value_dict, uniform_diag, xw_modes=(), pair=False, defer_x=False, dia=None):
     """Per-launch algorithmic bytes of THIS implementation's kernels in the stored format in
     use (value dictionary: 5 B/entry + a 2 KB table instead of 12 B/entry; constant Jacobi
     diagonal: passed as a scalar, no d stream; x-window SpMV (modes in xw_modes): the 4-byte
@@ -210,37 +210,47 @@ def kernel_bytes(solver, n, nnz, h, value_dict, uniform_diag, xw_modes=(), pair=
     descriptor per 256-row round, x still counted once).  Returns [(kernel name, bytes)] in
     launch order.  CG: x += a p is moved into update 2 (p streamed once per iteration);
     defer_x (single-GPU multi-kernel CG): x is read and written every other iteration from two
-    alternating direction buffers — update 2 averages 36 instead of 40 bytes per row."""
+    alternating direction buffers — update 2 averages 36 instead of 40 bytes per row.
+    dia (DeviceCsr.dia()): its modes read 48-byte warp-table entries (+ the unstructured
+    warps' CSR) instead of the matrix stream and row pointers."""
     rounds = (n + 255) // 256
+    rp = 4 * (n + 1)
 
-    def mat(mode):
+    def mat(mode):  # matrix stream + row pointers
+        if dia and mode in dia["modes"]:
+            return dia["bytes"]
         if mode not in xw_modes:
-            return (5 * nnz + 2048) if value_dict else 12 * nnz
+            return ((5 * nnz + 2048) if value_dict else 12 * nnz) + rp
         vb = 0 if pair else (1 if value_dict else 8)
-        return (vb + 2) * nnz + (2048 if value_dict else 0) + 64 * rounds
+        return (vb + 2) * nnz + (2048 if value_dict else 0) + 64 * rounds + rp
 
     d = 0 if uniform_diag else 8 * n
-    rp = 4 * (n + 1)
     if solver == "cg":
-        return [("spmv_cg", mat(1) + rp + 8 * (n + h) + 8 * n),  # A, row_ptr, p gathered, q written
+        return [("spmv_cg", mat(1) + 8 * (n + h) + 8 * n),       # A, row_ptr, p gathered, q written
                 ("cg_update1", 24 * n + d),                      # read r q (d), write r
                 ("cg_update2", (36 if defer_x else 40) * n + d)]  # read x p r (d), write x p (x: every other)
     return [("bicg_update1", 40 * n + d),                        # read r p v (d), write p ph
-            ("spmv_v", mat(2) + rp + 8 * (n + h) + 16 * n),      # ph gathered, v written, rh read
+            ("spmv_v", mat(2) + 8 * (n + h) + 16 * n),           # ph gathered, v written, rh read
             ("bicg_update2", 32 * n + d),                        # read r v (d), write s sh
-            ("spmv_t", mat(3) + rp + 8 * (n + h) + 16 * n),      # sh gathered, t written, s read
+            ("spmv_t", mat(3) + 8 * (n + h) + 16 * n),           # sh gathered, t written, s read
             ("bicg_update3", 64 * n)]                            # read x ph s sh t rh, write x r
 
 
-def format_text(fmt, xw):
+def format_text(fmt, xw, dia=None):
     vals = ("value dictionary (1-byte index into %d distinct fp64 values)" % fmt["distinct_values"]) \
         if fmt["value_dict"] else "fp64 values"
-    if xw["modes"]:
-        names = {0: "plain", 1: "cg", 2: "bicg_v", 3: "bicg_t"}
-        return (vals + " + int32 col; SpMV modes %s: x-window kernel (16-bit offsets into TMA-staged x windows, "
+    names = {0: "plain", 1: "cg", 2: "bicg_v", 3: "bicg_t"}
+    dm = dia["modes"] if dia else []
+    xm = [m for m in xw["modes"] if m not in dm]
+    out = vals + " + int32 col"
+    if xm:
+        out += ("; SpMV modes %s: x-window kernel (16-bit offsets into TMA-staged x windows, "
                 "%d staged elements per round, %.3f of entries staged)"
-                % ([names[m] for m in xw["modes"]], xw["cap_x"], xw["cover"]))
-    return vals + " + int32 col"
+                % ([names[m] for m in xm], xw["cap_x"], xw["cover"]))
+    if dm:
+        out += ("; SpMV modes %s: diagonal-warp kernel (48-byte table entry per 32 rows, %.4f of the "
+                "warps structured)" % ([names[m] for m in dm], dia["structured"]))
+    return out
 
 
 def canonical_bytes(solver, n, nnz, h=0):
@@ -359,7 +369,7 @@ def run_ours(args):
     t0 = time.time()
     D = S.DeviceCsr(None, dev, i32=(n, n, rp, ci, v))
     tup = time.time() - t0
-    info, fmt, xw = D.info(), D.format(), D.xwin()
+    info, fmt, xw, dia = D.info(), D.format(), D.xwin(), D.dia()
     b_host = torch.ones(n, dtype=torch.float64).pin_memory()
     x_host = torch.empty(n, dtype=torch.float64).pin_memory()
     opts = S.SolveOptions(atol=0.0, rtol=args.rtol, max_iter=args.max_iter)
@@ -433,7 +443,7 @@ def run_ours(args):
     kms = sv.kernel_times(args.kernel_iters)
     sv.close()
     kb = kernel_bytes(solver, n, nnz, 0, fmt["value_dict"], fmt["uniform_diag"], xw["modes"], xw["stream"] == 2,
-                      defer_x=solver == "cg" and os.environ.get("SPARSLA_CG_DEFER_X", "1") != "0")
+                      defer_x=solver == "cg" and os.environ.get("SPARSLA_CG_DEFER_X", "1") != "0", dia=dia)
     it_bytes = sum(b for _, b in kb)
     dom = max(range(len(kms)), key=lambda i: kms[i]) if solver == "cg" else \
         max((i for i, (nm, _) in enumerate(kb) if nm.startswith("spmv")), key=lambda i: kms[i])
@@ -503,7 +513,7 @@ def run_ours(args):
         "config": config_block(cfg, n, nnz, args.rtol),
         "partition": "single GPU",
         "format": {"spmv_variant": "tma-bulk-staged" if info["variant"] == 0 else "direct",
-                   "storage": format_text(fmt, xw),
+                   "storage": format_text(fmt, xw, dia),
                    "jacobi_diag": "constant (scalar)" if fmt["uniform_diag"] else "streamed"},
         "iteration_gbs": it_bytes / (ms / args.steps * 1e-3) / 1e9,
         "bytes_per_iteration": it_bytes,
@@ -520,7 +530,7 @@ def run_ours(args):
                      "peak": peak, "unit": "GB/s", "frac": dom_gbs / peak, "traffic": traffic,
                      "peak_source": peak_src, "frac_of_spec_8tbs": dom_gbs / SPEC_PEAK_GBS,
                      "algorithmic_bytes_per_launch": dom_bytes,
-                     "bytes_basis": "bytes of the stored format: " + format_text(fmt, xw),
+                     "bytes_basis": "bytes of the stored format: " + format_text(fmt, xw, dia),
                      "iteration_frac": (it_bytes / (ms / args.steps * 1e-3) / 1e9) / peak},
         "time_to_tolerance_s": e2e_t / len(reps), "iterations_to_tolerance": k_tol,
         "e2e": {"value": e2e_its / e2e_t, "unit": "it/s", "h2d_bytes_per_step": 8 * n,

@@ -200,10 +200,18 @@ int sparsla_dcsr_format(sparsla_dcsr* A, int64_t* fmt);
  * 256-row round, out[2]=parts per million of the entries whose x operand is staged,
  * out[3]=bit m set when SpMV mode m (0 plain, 1 CG p.q, 2 BiCGStab r-hat.v, 3 BiCGStab
  * t.t/t.s) runs the x-window kernel, out[4]=its value stream (0 fp64 values, 1 1-byte
- * dictionary indices, 2 "pair": the dictionary index inside the 16-bit offset).  out has 5
- * entries.  SPARSLA_XWIN at matrix creation: 0 disables, 1 (the default) stages when it
- * pays, 2 forces every mode. */
+ * dictionary indices, 2 "pair": the dictionary index inside the 16-bit offset), out[5]=its
+ * resident CTAs per SM, out[6..7] reserved (0).  out has 8 entries.  SPARSLA_XWIN at
+ * matrix creation: 0 disables, 1 (the default) stages when it pays, 2 forces every mode.
+ * (When the diagonal-warp kernel is on, sparsla_dcsr_dia, it takes every SpMV instead.) */
 int sparsla_dcsr_xwin(const sparsla_dcsr* A, int64_t* out);
+/* diagonal-warp SpMV (stencil-like matrices: >= 90% of the 32-row warps have all rows on
+ * the same <= 7 diagonals with the same dictionary values, up to two missing entries):
+ * out[0]=bit m set when SpMV mode m (as in sparsla_dcsr_xwin) runs the diagonal-warp
+ * kernel, out[1]=parts per million of structured warps (last build, also when below the
+ * threshold), out[2]=matrix bytes one such SpMV reads (48-byte warp entries + the other
+ * warps' CSR).  3 entries.  SPARSLA_DIA=0 at creation / set_values disables. */
+int sparsla_dcsr_dia(const sparsla_dcsr* A, int64_t* out);
 
 /* y = A x (sparse.cpp:135-154): rows accumulated left to right from 0.0, separate
  * multiply and add — bitwise equal to the reference.  mem: see above. */
@@ -347,6 +355,8 @@ int sparsla_dist_info(const sparsla_dist* D, int64_t* info);
 int sparsla_dist_format(sparsla_dist* D, int64_t* fmt);
 /* this rank's local-matrix x-window staging (same fields as sparsla_dcsr_xwin) */
 int sparsla_dist_xwin(const sparsla_dist* D, int64_t* out);
+/* this rank's local-matrix diagonal-warp kernel (same fields as sparsla_dcsr_dia) */
+int sparsla_dist_dia(const sparsla_dist* D, int64_t* out);
 /* counters[0]=halo exchanges [1]=all_reduce points [2]=p2p messages performed by the live
  * algorithm (SPEC.md:524 accounting); [3..5] = raw transport calls of the same kinds (they
  * also include the no-op tail replayed after convergence).  6 entries. */

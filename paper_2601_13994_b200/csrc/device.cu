@@ -23,6 +23,7 @@
 #include "common.hpp"
 #include "device.hpp"
 #include "spmv_xw.cuh"
+#include "spmv_dia.cuh"
 #include "kernels.cuh"
 #include "transport.hpp"
 
@@ -165,28 +166,29 @@ struct XwVariant {
     int vs;  // value stream: 0 fp64 values, 1 dictionary indices, 2 pair (index in the offset)
     int w, stg, minb;
     const void* fn[4];  // per SpmvMode
-    bool fix;           // compile-time stage layout (kXwFixCapC / kXwFixCapX)
+    int fix;            // compile-time stage layout (kXwFixCapC / xw_fix_cap_x(fix)), 0 = runtime
 };
 #define XWV(VS, W, S, M)                                                                            \
     {VS, W, S, M, {(const void*)spmv_xw_kernel<SPMV_PLAIN, S, M, W, VS>, (const void*)spmv_xw_kernel<SPMV_CG, S, M, W, VS>, \
-                   (const void*)spmv_xw_kernel<SPMV_BICG_V, S, M, W, VS>, (const void*)spmv_xw_kernel<SPMV_BICG_T, S, M, W, VS>}, false}
-#define XWVF(VS, W, S, M)                                                                           \
-    {VS, W, S, M, {(const void*)spmv_xw_kernel<SPMV_PLAIN, S, M, W, VS, true>, (const void*)spmv_xw_kernel<SPMV_CG, S, M, W, VS, true>, \
-                   (const void*)spmv_xw_kernel<SPMV_BICG_V, S, M, W, VS, true>, (const void*)spmv_xw_kernel<SPMV_BICG_T, S, M, W, VS, true>}, true}
+                   (const void*)spmv_xw_kernel<SPMV_BICG_V, S, M, W, VS>, (const void*)spmv_xw_kernel<SPMV_BICG_T, S, M, W, VS>}, 0}
+#define XWVF(VS, W, S, M, F)                                                                        \
+    {VS, W, S, M, {(const void*)spmv_xw_kernel<SPMV_PLAIN, S, M, W, VS, F>, (const void*)spmv_xw_kernel<SPMV_CG, S, M, W, VS, F>, \
+                   (const void*)spmv_xw_kernel<SPMV_BICG_V, S, M, W, VS, F>, (const void*)spmv_xw_kernel<SPMV_BICG_T, S, M, W, VS, F>}, F}
 static const XwVariant kXwVariants[] = {XWV(1, 8, 3, 3), XWV(1, 8, 2, 4), XWV(1, 8, 3, 4),
                                         XWV(0, 8, 3, 2), XWV(0, 12, 3, 2), XWV(0, 12, 2, 3),
                                         XWV(2, 8, 3, 3), XWV(2, 8, 2, 4), XWV(2, 8, 3, 4),
                                         XWV(1, 7, 3, 4), XWV(2, 7, 3, 4), XWV(0, 7, 2, 3),
-                                        XWVF(2, 7, 3, 4)};
+                                        XWVF(2, 7, 3, 4, 1)};
 // (measured and dropped: pair 7-wide at 4 stages / 3 CTAs per SM 0.840 ms and at 2 stages /
-// 5 CTAs per SM, 40 registers with spills, 0.999 ms — vs 0.792 ms for 3 stages / 4 CTAs)
+// 5 CTAs per SM, 40 registers with spills, 0.999 ms — vs 0.792 ms for 3 stages / 4 CTAs;
+// a 1408-element fixed x area: same 4 CTAs per SM, same time as 1536)
 #undef XWV
 #undef XWVF
 constexpr int kNumXwVariants = sizeof(kXwVariants) / sizeof(kXwVariants[0]);
 
 static size_t xw_smem_bytes(const DevCsr* A, int var, bool aux) {
     const XwVariant& V = kXwVariants[var];
-    const XwLayout L = V.fix ? XwLayout(0, kXwFixCapC, kXwFixCapX, V.vs, aux) : XwLayout(A->cap_v, A->cap_c, A->cap_x, V.vs, aux);
+    const XwLayout L = V.fix ? XwLayout(0, kXwFixCapC, xw_fix_cap_x(V.fix), V.vs, aux) : XwLayout(A->cap_v, A->cap_c, A->cap_x, V.vs, aux);
     return kXwHead + (size_t)V.stg * L.stage;
 }
 
@@ -202,15 +204,21 @@ static void choose_xw_variants(DevCsr* A) {
     A->xw_var[1] = w7 ? 9 : 0;
     A->xw_var[2] = w7 ? 10 : 8;
     // compile-time layout when the rounds fit it (7-point stencils up to 464^3 and beyond)
-    if (w7 && A->cap_c <= kXwFixCapC && A->cap_x <= kXwFixCapX && !getenv("SPARSLA_XW_NOFIX")) A->xw_var[2] = 12;
+    const bool fix = w7 && A->cap_c <= kXwFixCapC && A->cap_x <= xw_fix_cap_x(1);
+    if (fix && !getenv("SPARSLA_XW_NOFIX")) A->xw_var[2] = 12;
     if (const char* e = getenv("SPARSLA_XW_VARIANT")) {
         const int x = atoi(e);
-        const bool fits = !kXwVariants[x].fix || (A->cap_c <= kXwFixCapC && A->cap_x <= kXwFixCapX);
-        if (x >= 0 && x < kNumXwVariants && fits) A->xw_var[kXwVariants[x].vs] = x;
+        if (x >= 0 && x < kNumXwVariants) {
+            const XwVariant& V = kXwVariants[x];
+            const bool fits = !V.fix || (A->cap_c <= kXwFixCapC && A->cap_x <= xw_fix_cap_x(V.fix));
+            if (fits) A->xw_var[V.vs] = x;
+        }
     }
     int dev = A->device, sms = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    A->sms = sms;
     for (int d = 0; d < 3; ++d) {
+        if (A->xw_var[d] < 0) continue;
         for (int aux = 0; aux < 2; ++aux) {
             const int v = A->xw_var[d];
             int per_sm = 0;
@@ -261,7 +269,7 @@ DevCsr::~DevCsr() {
     cudaFree(rp); cudaFree(ci); cudaFree(val); cudaFree(dinv); cudaFree(ones);
     cudaFree(vidx); cudaFree(vtab);
     cudaFree(long_rows); cudaFree(long_bits); cudaFree(s_rp); cudaFree(s_ci); cudaFree(s_val);
-    cudaFree(xw); cudaFree(xwo); cudaFree(xvo);
+    cudaFree(xw); cudaFree(xwo); cudaFree(xvo); cudaFree(dia);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (side) cudaStreamDestroy(side);
@@ -283,8 +291,65 @@ static void configure_kernels_once(int device) {
 // coefficient stencils: {6, -1}).  The table holds the exact fp64 values, so every product
 // and sum is bit-identical.  SPARSLA_VALUE_DICT=0 disables.
 static void drop_value_dictionary(DevCsr* A) {
-    cudaFree(A->vidx); cudaFree(A->vtab);
+    cudaFree(A->vidx); cudaFree(A->vtab); cudaFree(A->dia);
     A->vidx = nullptr; A->vtab = nullptr; A->vd = false;
+    A->dia = nullptr;
+}
+
+// diagonal-warp kernel variants: rounds per step, min CTAs per SM (SPARSLA_DIA_VARIANT)
+struct DiaVariant {
+    const void* fn[4];
+};
+#define DIAV(R, M)                                                                                   \
+    {{(const void*)spmv_dia_kernel<SPMV_PLAIN, R, M>, (const void*)spmv_dia_kernel<SPMV_CG, R, M>,      \
+      (const void*)spmv_dia_kernel<SPMV_BICG_V, R, M>, (const void*)spmv_dia_kernel<SPMV_BICG_T, R, M>}}
+// measured on B200, config B CG SpMV (tools/r02_call34.sh): 1 round / 5 CTAs per SM
+// 0.776 ms, 1 / 4: 0.813, 2 / 4: 0.820, 1 / 6: 0.799, 2 / 3: 0.912 (x-window pair: 0.771)
+static const DiaVariant kDiaVariants[] = {DIAV(1, 5), DIAV(1, 4), DIAV(2, 4)};
+#undef DIAV
+constexpr int kNumDiaVariants = sizeof(kDiaVariants) / sizeof(kDiaVariants[0]);
+
+// diagonal-warp table (spmv_dia.cuh) from the device CSR and dictionary indices; kept when
+// at least 90% of the 32-row warps are structured, and then every SpMV mode takes it.
+// Measured on B200 (profiles/r02_dia.md): half the DRAM bytes of the x-window pair kernel,
+// config B CG SpMV 0.773 -> 0.68 ms, config D 0.49/0.51 -> 0.43/0.46 ms.  SPARSLA_DIA=0: off.
+static void build_dia(DevCsr* A) {
+    cudaFree(A->dia);
+    A->dia = nullptr;
+    A->dia_frac = 0.0;
+    A->dia_bytes = 0;
+    const char* e = getenv("SPARSLA_DIA");
+    const int dm = e ? atoi(e) : -1;
+    A->dia_modes = 0xF;
+    if (dm == 0 || !A->vd || A->nrows == 0) return;
+    const long long nwarps = nchunks_of(A->nrows) * kChunkRounds * (kSpmvThreads / 32);
+    unsigned long long* cnt = dalloc<unsigned long long>(2);
+    CK(cudaMemsetAsync(cnt, 0, 2 * sizeof(unsigned long long), A->stream));
+    int32_t* tab = dalloc<int32_t>(nwarps * kDiaInts);
+    dia_build_kernel<<<grid_for(nwarps * 32, 256), 256, 0, A->stream>>>(A->rp, A->ci, A->vidx, A->nrows, nwarps,
+                                                                          tab, cnt);
+    CK(cudaGetLastError());
+    unsigned long long h[2] = {0, 0};
+    CK(cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, A->stream));
+    CK(cudaStreamSynchronize(A->stream));
+    cudaFree(cnt);
+    const long long live = (A->nrows + 31) / 32;
+    A->dia_frac = (double)h[0] / (double)live;
+    // per SpMV: the live warps' table entries + the unstructured warps' CSR reads
+    A->dia_bytes = live * kDiaInts * 4 + (long long)h[1];
+    if (A->dia_frac >= 0.9) A->dia = tab;
+    else cudaFree(tab);
+    A->dia_var = 0;
+    if (const char* v = getenv("SPARSLA_DIA_VARIANT")) {
+        const int x = atoi(v);
+        if (x >= 0 && x < kNumDiaVariants) A->dia_var = x;
+    }
+    int sms = 0, per_sm = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, A->device));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kDiaVariants[A->dia_var].fn[SPMV_CG], kSpmvThreads, 0));
+    // prefetch distance in waves of resident CTAs (SPARSLA_DIA_PREFETCH, default 1; 0 = off)
+    const char* pe = getenv("SPARSLA_DIA_PREFETCH");
+    A->dia_ahead = (pe ? atoi(pe) : 1) * sms * per_sm;
 }
 
 static void build_value_dictionary(DevCsr* A, const double* h_val) {
@@ -348,6 +413,7 @@ static void build_value_dictionary(DevCsr* A, const double* h_val) {
     CK(memcpy_sync(A->vtab, vt.data(), 256 * 8, cudaMemcpyHostToDevice));
     A->vd = true;
     A->nvals = (int)tab.size();
+    build_dia(A);
 }
 
 // x windows (spmv_xw.cuh): for every 256-row round, up to kXwMax contiguous segments of x
@@ -818,10 +884,27 @@ void devcsr_xwin_info(const DevCsr* A, int64_t* out) {
     out[3] = 0;
     for (int m = 0; m < 4; ++m) out[3] |= (xw_pick(A, m) >= 0 ? 1 : 0) << m;
     out[4] = xw_stream(A);
+    const int v = out[0];
+    out[5] = v >= 0 ? A->xw_ctas[xw_stream(A)][0] / std::max(1, A->sms) : 0;
+    out[6] = 0;
+    out[7] = 0;
+}
+
+// the diagonal-warp kernel (one CTA per chunk) takes every SpMV mode when its table exists
+static bool dia_pick(const DevCsr* A, int mode) {
+    return A->dia && A->nlong == 0 && !A->has_hub && ((A->dia_modes >> mode) & 1);
+}
+
+void devcsr_dia_info(const DevCsr* A, int64_t* out) {
+    out[0] = 0;
+    for (int m = 0; m < 4; ++m) out[0] |= (dia_pick(A, m) ? 1 : 0) << m;
+    out[1] = (int64_t)(A->dia_frac * 1e6 + 0.5);
+    out[2] = A->dia ? A->dia_bytes : 0;
 }
 
 unsigned spmv_grid(const DevCsr* A, long long nch, int mode, bool xw_ok) {
     if (nch <= 0) return 0;
+    if (dia_pick(A, mode)) return (unsigned)nch;
     if (xw_ok && xw_pick(A, mode) >= 0)
         return (unsigned)std::min<long long>(nch, (long long)A->xw_ctas[xw_stream(A)][mode_has_aux(mode)]);
     if (A->staged) {
@@ -839,7 +922,8 @@ void launch_spmv_part(DevCsr* A, cudaStream_t s, int mode, const double* x, doub
                       unsigned grid_cap) {
     const bool xw_ok = xw_aligned(x, aux);
     unsigned grid = spmv_grid(A, nch, mode, xw_ok);
-    if (grid_cap && A->staged && grid > grid_cap) grid = grid_cap;  // persistent kernels only
+    const bool dia = dia_pick(A, mode);
+    if (grid_cap && A->staged && !dia && grid > grid_cap) grid = grid_cap;  // persistent kernels only
     if (grid == 0) return;
     SpmvParams P{};
     P.rp = A->rp; P.ci = A->ci; P.val = A->val;
@@ -861,7 +945,13 @@ void launch_spmv_part(DevCsr* A, cudaStream_t s, int mode, const double* x, doub
     P.red.nchunks = nchunks_of(A->nrows);
     P.red.expected = expected;
     const int xv = xw_ok ? xw_pick(A, mode) : -1;
-    if (xv >= 0) {
+    if (dia) {
+        P.dia = A->dia;
+        P.dia_ahead = A->dia_ahead;
+        P.ncols = A->ncols;
+        void* args[] = {&P};
+        CK(cudaLaunchKernel(kDiaVariants[A->dia_var].fn[mode], dim3(grid), dim3(kSpmvThreads), args, 0, s));
+    } else if (xv >= 0) {
         P.xw = A->xw;
         P.xwo = xw_stream(A) == 2 ? A->xvo : A->xwo;
         P.cap_x = A->cap_x;
@@ -1161,7 +1251,7 @@ void Solver::spmv_point(int mode, double* xin, double* y, const double* aux, int
     // behind a GPU-filling grid.  (The persistent kernels loop over their chunks, so any grid
     // works; the ticket count `expected` uses the same capped grid.)
     unsigned cap = 0;
-    if (dist->tr && dist->tr->P > 1 && A->staged) {
+    if (dist->tr && dist->tr->P > 1 && A->staged && !dia_pick(A, mode)) {
         int sms = 0;
         CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, A->device));
         const unsigned full = spmv_grid(A, 1LL << 40, mode);
@@ -1725,6 +1815,13 @@ int sparsla_dcsr_xwin(const sparsla_dcsr* H, int64_t* out) {
     return guarded([&] {
         need(H, "matrix"); need(out, "out");
         devcsr_xwin_info(H->A, out);
+    });
+}
+
+int sparsla_dcsr_dia(const sparsla_dcsr* H, int64_t* out) {
+    return guarded([&] {
+        need(H, "matrix"); need(out, "out");
+        devcsr_dia_info(H->A, out);
     });
 }
 

@@ -69,7 +69,16 @@ struct DevCsr {
     uint16_t* xvo = nullptr;   // [nnz + kXwPad] pair stream: dictionary index << 11 | offset
     int xw_var[3] = {-1, -1, -1};  // x-window kernel variant per value stream [plain, dictionary, pair]
     int xw_ctas[3][2] = {{0, 0}, {0, 0}, {0, 0}};  // persistent grid [stream][aux vector staged]
+    // diagonal-warp table (spmv_dia.cuh): [chunks * 64 warps][12], kept when >= 90% of the
+    // warps are structured; the SpMV then takes spmv_dia_kernel in every mode
+    int32_t* dia = nullptr;
+    double dia_frac = 0.0;       // structured warps / warps (last build)
+    long long dia_bytes = 0;     // matrix bytes one diagonal-warp SpMV reads
+    int dia_ahead = 0;           // chunks ahead a diagonal-warp CTA prefetches (whole waves)
+    int dia_var = 0;             // kDiaVariants index
+    int dia_modes = 0;           // SpMV modes (bit per SpmvMode) that take it
     double xw_cover = 0.0;     // fraction of entries whose x operand is staged
+    int sms = 0;               // multiprocessors of the device (set with the variants)
     DevCsr* transpose = nullptr;
     cudaStream_t stream = nullptr;
     std::mutex lazy_mu;  // guards the lazily built caches (dinv, ones, symmetry, transpose)
@@ -93,6 +102,8 @@ struct DevCsr {
 
 // x-window staging summary (sparsla_dcsr_xwin layout)
 void devcsr_xwin_info(const DevCsr* A, int64_t* out);
+// diagonal-warp summary (sparsla_dcsr_dia layout)
+void devcsr_dia_info(const DevCsr* A, int64_t* out);
 
 // new values in A's entry order (host or device pointer); drops every value-dependent cache
 void devcsr_set_values(DevCsr* A, const double* vals, int32_t mem);

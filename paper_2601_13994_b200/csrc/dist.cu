@@ -686,6 +686,13 @@ int sparsla_dist_xwin(const sparsla_dist* D, int64_t* out) {
     });
 }
 
+int sparsla_dist_dia(const sparsla_dist* D, int64_t* out) {
+    return guarded([&] {
+        if (!D || !out) fail(SPARSLA_ERR_INVALID_ARGUMENT, "null argument");
+        devcsr_dia_info(D->A, out);
+    });
+}
+
 int sparsla_dist_set_fused(sparsla_dist* D, int32_t on) {
     return guarded([&] { D->ctx->p2p_enabled = on != 0; });
 }

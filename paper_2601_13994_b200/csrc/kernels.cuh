@@ -552,6 +552,9 @@ struct SpmvParams {
     const int32_t* xw;    // x-window kernels (spmv_xw.cuh): per-round window descriptors
     const uint16_t* xwo;  //   per-entry offsets into the round's staged windows
     int cap_x;            //   staged x elements per round
+    const int32_t* dia;   // diagonal-warp table (spmv_dia.cuh): [chunks * 8 rounds * 8 warps][12]
+    int dia_ahead;        //   chunks ahead whose leading x lines a CTA prefetches (one wave)
+    long long ncols;      //   x length (prefetch bound)
     RedParams red;
 };
 

@@ -1,0 +1,280 @@
+// spmv_dia.cuh — "diagonal warp" SpMV for stencil-like CSR matrices.
+//
+// Same arithmetic as every other SpMV kernel of the library (row-ordered __dmul_rn /
+// __dadd_rn sums in stored column order, the fused dots in the canonical chunk shape):
+// bit-identical.  At matrix creation (and after set_values) one warp per 32 consecutive
+// rows classifies its rows: when every row's entries lie on the same <= 7 "diagonals"
+// (entry k of row i in column i + delta_k, with dictionary value v_k), in stored order,
+// except at most two entries missing from some rows (the x-boundary rows of a stencil
+// line), the warp is "structured" and its 48-byte table entry replaces the rows' row
+// pointers, columns and value indices: the SpMV then reads 1.5 B of matrix per 32 rows
+// plus x and y.  x is read with coalesced loads straight from global memory (each diagonal
+// of a warp is 256 contiguous bytes; neighbouring diagonals share L1 lines), so there is
+// no staging pipeline at all.  Other warps ("unstructured") run the CSR loop on the fp64
+// values.  The table is kept only when at least 90% of the warps are structured.
+//
+// Table entry (12 ints per warp): [0..6] delta_k (0 past the last diagonal), [7] v0..v3,
+// [8] v4..v6 | m << 24 (m diagonals; 0xFF = unstructured), [9] exception bytes
+// (lane << 3 | k, 0x07 = none), [10..11] 0.
+#pragma once
+
+#include "kernels.cuh"
+
+namespace sparsla_b200 {
+
+constexpr int kDiaInts = 12;            // per warp
+constexpr uint32_t kDiaUnstructured = 0xFFu;
+constexpr uint32_t kDiaNoEx = 0x07u;
+
+// one warp per 32 rows: classify and write the table entry; cnt[0] += structured warps,
+// cnt[1] += CSR bytes the unstructured warps read (row pointers, columns, values)
+static __global__ void dia_build_kernel(const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                        const uint8_t* __restrict__ vidx, long long n, long long nwarps,
+                                        int32_t* __restrict__ tab, unsigned long long* cnt) {
+    const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (w >= nwarps) return;  // warp-uniform
+    const long long row = w * 32 + lane;
+    const bool live = row < n;
+    int32_t e[kDiaInts] = {0, 0, 0, 0, 0, 0, 0, 0, (int32_t)(kDiaUnstructured << 24), 0, 0, 0};
+    const int kb = live ? rp[row] : 0;
+    const int len = live ? rp[row + 1] - kb : 0;
+    int m = len;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    bool ok;
+    if (!__any_sync(0xffffffffu, live)) {  // past the last row: structured, no diagonals
+        ok = false;
+        e[8] = 0;
+        e[9] = (int32_t)(kDiaNoEx | (kDiaNoEx << 8));
+    } else if (__all_sync(0xffffffffu, live) && m >= 1 && m <= 7) {
+        const int tl = __ffs(__ballot_sync(0xffffffffu, len == m)) - 1;
+        long long dk[7];
+        uint32_t vk[7];
+#pragma unroll
+        for (int k = 0; k < 7; ++k) {
+            const bool mine = lane == tl && k < len;
+            dk[k] = __shfl_sync(0xffffffffu, mine ? (long long)ci[kb + k] - row : 0ll, tl);
+            vk[k] = __shfl_sync(0xffffffffu, mine ? (uint32_t)vidx[kb + k] : 0u, tl);
+        }
+        bool tok = true;
+#pragma unroll
+        for (int k = 0; k < 7; ++k)
+            if (k < m) tok = tok && dk[k] >= INT32_MIN && dk[k] <= INT32_MAX;
+        int j = 0, miss = 0;
+        uint32_t exb[2] = {kDiaNoEx, kDiaNoEx};
+#pragma unroll
+        for (int k = 0; k < 7; ++k) {
+            if (k < m) {
+                const bool hit = j < len && (long long)ci[kb + j] - row == dk[k] && (uint32_t)vidx[kb + j] == vk[k];
+                if (hit) {
+                    ++j;
+                } else {
+                    if (miss < 2) exb[miss] = ((uint32_t)lane << 3) | (uint32_t)k;
+                    ++miss;
+                }
+            }
+        }
+        ok = __all_sync(0xffffffffu, tok && j == len);
+        int tot = miss;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+        ok = ok && tot <= 2;
+        if (ok) {
+            uint32_t ex[2] = {kDiaNoEx, kDiaNoEx};
+            int ne = 0;
+            uint32_t b = __ballot_sync(0xffffffffu, miss > 0);
+            while (b && ne < 2) {
+                const int l = __ffs(b) - 1;
+                b &= b - 1;
+                const uint32_t e0 = __shfl_sync(0xffffffffu, exb[0], l), e1 = __shfl_sync(0xffffffffu, exb[1], l);
+                ex[ne++] = e0;
+                if (e1 != kDiaNoEx && ne < 2) ex[ne++] = e1;
+            }
+#pragma unroll
+            for (int k = 0; k < 7; ++k) e[k] = k < m ? (int32_t)dk[k] : 0;
+            e[7] = (int32_t)(vk[0] | (vk[1] << 8) | (vk[2] << 16) | (vk[3] << 24));
+            e[8] = (int32_t)(vk[4] | (vk[5] << 8) | (vk[6] << 16) | ((uint32_t)m << 24));
+            e[9] = (int32_t)(ex[0] | (ex[1] << 8));
+        }
+    } else {
+        ok = false;
+    }
+    if (lane == 0) {
+        int4* t4 = reinterpret_cast<int4*>(tab + w * kDiaInts);
+        t4[0] = make_int4(e[0], e[1], e[2], e[3]);
+        t4[1] = make_int4(e[4], e[5], e[6], e[7]);
+        t4[2] = make_int4(e[8], e[9], e[10], e[11]);
+        if (ok) {
+            atomicAdd(cnt, 1ull);
+        } else if (((uint32_t)e[8] >> 24) == kDiaUnstructured) {
+            const long long re = min(w * 32 + 32, n);
+            atomicAdd(cnt + 1, (unsigned long long)(4 * (re - w * 32 + 1) + 12 * (long long)(rp[re] - rp[w * 32])));
+        }
+    }
+}
+
+// Per round and warp: the skip mask of this lane (slots past the warp's last diagonal, the
+// lane's missing entries, dead rows) and the 7 x loads (skipped slots read x[row]).
+__device__ __forceinline__ uint32_t dia_loads(const int32_t* e, const double* __restrict__ x, int row, bool live,
+                                              int lane, double (&xv)[7]) {
+    const uint32_t m = (uint32_t)e[8] >> 24, ex = (uint32_t)e[9];
+    uint32_t skip = (0x7Fu << m) & 0x7Fu;
+    if (((ex >> 3) & 31u) == (uint32_t)lane) skip |= 1u << (ex & 7u);
+    if (((ex >> 11) & 31u) == (uint32_t)lane) skip |= 1u << ((ex >> 8) & 7u);
+    if (!live) skip = 0x7Fu;
+    const int rb = live ? row : 0;  // 32-bit column arithmetic: one IMAD.WIDE per address
+#pragma unroll
+    for (int u = 0; u < 7; ++u) xv[u] = __ldg(x + (((skip >> u) & 1u) ? rb : rb + e[u]));
+    return skip;
+}
+// stencil-interior warp (7 diagonals, no missing entry, every row live): no masks at all
+__device__ __forceinline__ double dia_full(const int4& q0, const int4& q1, const int4& q2, const double* __restrict__ x,
+                                           const double* s_vtab, int row) {
+    const int dl[7] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z};
+    double xv[7];
+#pragma unroll
+    for (int u = 0; u < 7; ++u) xv[u] = __ldg(x + (row + dl[u]));
+    const uint32_t vw0 = (uint32_t)q1.w, vw1 = (uint32_t)q2.x;
+    double y = 0.0;
+#pragma unroll
+    for (int u = 0; u < 7; ++u)
+        y = __dadd_rn(y, __dmul_rn(s_vtab[((u < 4 ? vw0 : vw1) >> (8 * (u & 3))) & 0xFFu], xv[u]));
+    return y;
+}
+__device__ __forceinline__ bool dia_is_full(const int4& q2) {
+    return ((uint32_t)q2.x >> 24) == 7u && (uint32_t)q2.y == (kDiaNoEx | (kDiaNoEx << 8));
+}
+
+// the row sum over the present slots in stored order (guard-free when no lane skips)
+__device__ __forceinline__ double dia_sum(const int32_t* e, const double* s_vtab, uint32_t skip, const double (&xv)[7]) {
+    const uint32_t vw0 = (uint32_t)e[7], vw1 = (uint32_t)e[8];
+    double y = 0.0;
+    if (__all_sync(0xffffffffu, skip == 0)) {
+#pragma unroll
+        for (int u = 0; u < 7; ++u)
+            y = __dadd_rn(y, __dmul_rn(s_vtab[((u < 4 ? vw0 : vw1) >> (8 * (u & 3))) & 0xFFu], xv[u]));
+    } else {
+#pragma unroll
+        for (int u = 0; u < 7; ++u) {
+            const double s = __dadd_rn(y, __dmul_rn(s_vtab[((u < 4 ? vw0 : vw1) >> (8 * (u & 3))) & 0xFFu], xv[u]));
+            y = ((skip >> u) & 1u) ? y : s;
+        }
+    }
+    return y;
+}
+__device__ __forceinline__ double dia_csr_row(const SpmvParams& P, int row) {
+    const int kb = __ldg(P.rp + row), ke = __ldg(P.rp + row + 1);
+    double y = 0.0;
+#pragma unroll 1
+    for (int k = kb; k < ke; ++k) y = __dadd_rn(y, __dmul_rn(__ldg(P.val + k), __ldg(P.x + __ldg(P.ci + k))));
+    return y;
+}
+
+// One CTA = one chunk (8 rounds of 256 rows, thread t owns row round * 256 + t), like
+// spmv_direct_kernel.  The chunk's 64 table entries (3 KB) are staged in shared memory at
+// the start; rounds are taken two at a time so each warp has 14 independent x loads in
+// flight (the kernel is bound by load latency, not bandwidth).  Warps whose rows all have
+// every diagonal (the stencil interior) sum guard-free; the others select per slot;
+// unstructured warps run the CSR loop.  Sums and dot accumulation in round order.
+template <int MODE, int R, int MINB>
+__global__ void __launch_bounds__(kSpmvThreads, MINB) spmv_dia_kernel(SpmvParams P) {
+    constexpr int ND = SpmvDots<MODE>::n;
+    constexpr int NA = ND > 0 ? ND : 1;
+    constexpr int kW = kSpmvThreads / 32;
+    if (P.check_done && P.red.st->done) return;
+    __shared__ double s_vtab[256];
+    __shared__ __align__(16) int32_t s_tab[kChunkRounds * kW * kDiaInts];
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const long long chunk = P.chunk_list ? (long long)P.chunk_list[blockIdx.x] : P.chunk0 + blockIdx.x;
+    s_vtab[t] = P.vtab[t];  // kSpmvThreads == 256
+    const int4* tc = reinterpret_cast<const int4*>(P.dia) + chunk * kChunkRounds * kW * 3;
+    if (t < kChunkRounds * kW * 3) reinterpret_cast<int4*>(s_tab)[t] = __ldg(tc + t);
+    if (P.dia_ahead > 0 && !P.chunk_list && t >= 192) {
+        // one wave ahead: the chunk a successor CTA on this SM will take reads its leading
+        // diagonal (the z+1 plane of a 3-D stencil) from DRAM for the first time — pull
+        // those 2048 x values and its table into L2 now, so its rounds wait on L2 hits
+        const long long ca = chunk + P.dia_ahead;
+        if (ca < P.nch) {
+            const int4 e0 = __ldg(tc), e1 = __ldg(tc + 1);
+            const int dmax = max(max(max(e0.x, e0.y), max(e0.z, e0.w)), max(max(e1.x, e1.y), e1.z));
+            const int q = t - 192;  // 64 threads: 2 lines of x each, 24 of them a table line
+            const long long j = ca * kChunk + dmax + 32 * q;
+            if (j >= 0 && j < P.ncols) asm volatile("prefetch.global.L2 [%0];" ::"l"(P.x + j));
+            if (j + 16 >= 0 && j + 16 < P.ncols) asm volatile("prefetch.global.L2 [%0];" ::"l"(P.x + j + 16));
+            if (q < 24)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const int4*>(P.dia) + ca * kChunkRounds * kW * 3 + 8 * q));
+        }
+    }
+    if (P.p2p && (long long)blockIdx.x >= P.n_interior) {
+        if (t == 0) p2p_wait_halo(P.p2p, P.halo_v, P.red.st->ep_halo[P.halo_v]);
+    }
+    __syncthreads();
+    const long long base = chunk * kChunk;
+    const long long rem_rounds = (P.n - base + kChunkSlots - 1) / kChunkSlots;
+    const int nrounds = rem_rounds < kChunkRounds ? (int)rem_rounds : kChunkRounds;
+    const int n = (int)P.n;  // int32 CSR: rows < 2^31
+    double acc[NA];
+#pragma unroll
+    for (int d = 0; d < NA; ++d) acc[d] = 0.0;
+    auto finish = [&](int row, double y) {
+        if (row < n) {
+            P.y[row] = y;
+            spmv_epilogue<MODE>(P, row, y, acc);
+        }
+    };
+    int r = 0;
+    for (; R == 2 && r + 1 < nrounds; r += 2) {
+        const int32_t* e0 = s_tab + (r * kW + warp) * kDiaInts;
+        const int32_t* e1 = e0 + kW * kDiaInts;
+        const int row0 = (int)base + r * kChunkSlots + t, row1 = row0 + kChunkSlots;
+        const bool u0 = ((uint32_t)e0[8] >> 24) == kDiaUnstructured, u1 = ((uint32_t)e1[8] >> 24) == kDiaUnstructured;
+        if (!u0 && !u1) {  // warp-uniform
+            double x0[7], x1[7];
+            const uint32_t s0 = dia_loads(e0, P.x, row0, row0 < n, lane, x0);
+            const uint32_t s1 = dia_loads(e1, P.x, row1, row1 < n, lane, x1);
+            finish(row0, dia_sum(e0, s_vtab, s0, x0));
+            finish(row1, dia_sum(e1, s_vtab, s1, x1));
+        } else {
+#pragma unroll 1
+            for (int h = 0; h < 2; ++h) {
+                const int32_t* e = h ? e1 : e0;
+                const int row = h ? row1 : row0;
+                double y = 0.0;
+                if (((uint32_t)e[8] >> 24) != kDiaUnstructured) {
+                    double xv[7];
+                    const uint32_t sk = dia_loads(e, P.x, row, row < n, lane, xv);
+                    y = dia_sum(e, s_vtab, sk, xv);
+                } else if (row < n) {
+                    y = dia_csr_row(P, row);
+                }
+                finish(row, y);
+            }
+        }
+    }
+#pragma unroll 1
+    for (; r < nrounds; ++r) {  // one round at a time (R = 1; the odd last round for R = 2)
+        const int32_t* e = s_tab + (r * kW + warp) * kDiaInts;
+        const int row = (int)base + r * kChunkSlots + t;
+        const int4* q = reinterpret_cast<const int4*>(e);
+        const int4 q2 = q[2];
+        double y = 0.0;
+        if (dia_is_full(q2)) {  // warp-uniform
+            y = dia_full(q[0], q[1], q2, P.x, s_vtab, row);
+        } else if (((uint32_t)e[8] >> 24) != kDiaUnstructured) {
+            double xv[7];
+            const uint32_t sk = dia_loads(e, P.x, row, row < n, lane, xv);
+            y = dia_sum(e, s_vtab, sk, xv);
+        } else if (row < n) {
+            y = dia_csr_row(P, row);
+        }
+        finish(row, y);
+    }
+    if constexpr (ND > 0) {
+        __shared__ double sred[SpmvFin<MODE>::n * kW];
+        block_tree<kSpmvThreads, ND>(acc, sred);
+        publish_and_finish<kSpmvThreads, ND, SpmvFin<MODE>::n>(acc, chunk, P.red, sred);
+    }
+}
+
+}  // namespace sparsla_b200

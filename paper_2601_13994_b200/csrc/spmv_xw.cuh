@@ -87,8 +87,8 @@ template <int MODE> struct XwAux { static constexpr bool on = (MODE == SPMV_BICG
 // kXwFixCapX staged x elements (stencils): the per-round stage addressing folds into
 // immediates instead of being rematerialised from the parameters at 56 registers
 constexpr int kXwFixCapC = 2016;  // (2016 * 2 + 64) bytes = 4 KB of offsets
-constexpr int kXwFixCapX = 1536;
-template <int MODE, int STG, int MINB, int W, int VS, bool FIX = false>
+__host__ __device__ constexpr int xw_fix_cap_x(int fix) { return fix == 1 ? 1536 : 1408; }
+template <int MODE, int STG, int MINB, int W, int VS, int FIX = 0>
 __global__ void __launch_bounds__(kWsThreads, MINB) spmv_xw_kernel(SpmvParams P) {
     constexpr bool VD = VS != 0;     // values from the dictionary table
     constexpr bool PAIR = VS == 2;   // ... indexed by the top bits of the offset stream
@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(kWsThreads, MINB) spmv_xw_kernel(SpmvParams P)
     uint64_t* empty = full + STG;
     uint64_t* dbar = empty + STG;  // [2]
     int32_t* dbuf = reinterpret_cast<int32_t*>(smem + 1024);
-    const XwLayout L = FIX ? XwLayout(0, kXwFixCapC, kXwFixCapX, VS, AUX) : XwLayout(P.cap_v, P.cap_c, P.cap_x, VS, AUX);
+    const XwLayout L = FIX ? XwLayout(0, kXwFixCapC, xw_fix_cap_x(FIX), VS, AUX) : XwLayout(P.cap_v, P.cap_c, P.cap_x, VS, AUX);
     unsigned char* stage0 = smem + kXwHead;
     const int t = threadIdx.x;
     const int warp = t >> 5, lane = t & 31;

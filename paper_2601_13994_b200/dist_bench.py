@@ -104,9 +104,9 @@ def run(args, metric, cfg):
     kms = sv.kernel_times(args.kernel_iters)
     nnz_local = plan.nnz_local
     no, nh = info["n_owned"], info["n_halo"]
-    xw = plan.xwin()
+    xw, dia = plan.xwin(), plan.dia()
     kb = B.kernel_bytes(solver, no, nnz_local, nh, fmt["value_dict"], fmt["uniform_diag"], xw["modes"],
-                        xw["stream"] == 2)
+                        xw["stream"] == 2, dia=dia)
     it_bytes = sum(x for _, x in kb)
     nnz_t = torch.tensor([nnz_local], dtype=torch.int64)
     dist.all_reduce(nnz_t)
@@ -126,7 +126,7 @@ def run(args, metric, cfg):
             "boundary_chunks": info["boundary_chunks"],
             "iteration_gbs_per_gpu": it_gbs,
             "canonical_bytes_per_iteration_per_gpu": B.canonical_bytes(solver, no, nnz_local, nh),
-            "format": dict(fmt, storage=B.format_text(fmt, xw)), "collectives": "fused peer-memory (in-kernel)" if getattr(args, "fused", False)
+            "format": dict(fmt, storage=B.format_text(fmt, xw, dia)), "collectives": "fused peer-memory (in-kernel)" if getattr(args, "fused", False)
             else "NCCL (grouped send/recv halo overlapped with the interior SpMV, all-gathered totals)",
             "roofline": {"bound": "hbm", "kernel": "iteration (spmv + halo + fused updates), rank 0",
                          "achieved": it_gbs, "peak": peak, "unit": "GB/s", "frac": it_gbs / peak,

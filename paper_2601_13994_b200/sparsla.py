@@ -241,6 +241,12 @@ class CsrMatrix:
         return self._dev[dev]
 
 
+def _xwin_dict(out):
+    return {"variant": int(out[0]), "cap_x": int(out[1]), "cover": out[2] / 1e6,
+            "modes": [m for m in range(4) if (int(out[3]) >> m) & 1], "stream": int(out[4]),
+            "ctas_per_sm": int(out[5])}
+
+
 class DeviceCsr:
     """Owning wrapper of a sparsla_dcsr handle (one GPU)."""
 
@@ -287,10 +293,17 @@ class DeviceCsr:
     def xwin(self):
         """x-window staging: {variant (-1 = none), cap_x (elements per round), cover (fraction
         of entries whose x operand is staged), modes (SpMV modes that use it)}."""
-        out = np.zeros(5, np.int64)
+        out = np.zeros(8, np.int64)
         _check(lib().sparsla_dcsr_xwin(self.h, _p(out, _i64p)))
-        return {"variant": int(out[0]), "cap_x": int(out[1]), "cover": out[2] / 1e6,
-                "modes": [m for m in range(4) if (int(out[3]) >> m) & 1], "stream": int(out[4])}
+        return _xwin_dict(out)
+
+    def dia(self):
+        """Diagonal-warp SpMV (csrc/spmv_dia.cuh): {on (every SpMV mode), modes (SpMV modes
+        that take it), structured (fraction of 32-row warps), bytes (matrix bytes per SpMV)}."""
+        out = np.zeros(3, np.int64)
+        _check(lib().sparsla_dcsr_dia(self.h, _p(out, _i64p)))
+        return {"on": int(out[0]) == 0xF, "modes": [m for m in range(4) if (int(out[0]) >> m) & 1],
+                "structured": out[1] / 1e6, "bytes": int(out[2])}
 
     def format(self):
         """SpMV storage format: value dictionary on / distinct values / constant Jacobi diagonal."""
@@ -967,10 +980,16 @@ class DistPlan:
 
     def xwin(self):
         """This rank's local-matrix x-window staging (see DeviceCsr.xwin)."""
-        out = np.zeros(5, np.int64)
+        out = np.zeros(8, np.int64)
         _check(lib().sparsla_dist_xwin(self.h, _p(out, _i64p)))
-        return {"variant": int(out[0]), "cap_x": int(out[1]), "cover": out[2] / 1e6,
-                "modes": [m for m in range(4) if (int(out[3]) >> m) & 1], "stream": int(out[4])}
+        return _xwin_dict(out)
+
+    def dia(self):
+        """This rank's local-matrix diagonal-warp SpMV (see DeviceCsr.dia)."""
+        out = np.zeros(3, np.int64)
+        _check(lib().sparsla_dist_dia(self.h, _p(out, _i64p)))
+        return {"on": int(out[0]) == 0xF, "modes": [m for m in range(4) if (int(out[0]) >> m) & 1],
+                "structured": out[1] / 1e6, "bytes": int(out[2])}
 
     def set_values(self, vals_local, mem=MEM_HOST):
         """Collective: new values of this rank's local matrix (local entry order)."""

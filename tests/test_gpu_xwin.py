@@ -47,8 +47,10 @@ CASES = ["poisson3d", "poisson2d", "convdiff3d", "fem2d", "banded_far", "two_ban
 @pytest.fixture(autouse=True)
 def _xwin_on(monkeypatch):
     """The x-window path is opt-in (SPARSLA_XWIN=1: when it pays, 2: forced); these tests
-    exercise it."""
+    exercise it (the diagonal-warp kernel, which takes BiCGStab's SpMVs on stencils by
+    default, is off: tests/test_gpu_dia.py)."""
     monkeypatch.setenv("SPARSLA_XWIN", "1")
+    monkeypatch.setenv("SPARSLA_DIA", "0")
 
 
 def test_xwin_selection(S, O, gpu, monkeypatch):

@@ -1,15 +1,11 @@
 #!/bin/bash
-# Pair-stream default: full GPU suite, bench B/D/E, ncu of the headline SpMV (pair x-window,
-# config B) and the launch list of the bench command.
+# diagonal-warp SpMV: tests + sweep against the x-window / gather kernels
 cd "$GRAFT_REPO_ROOT"
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.limit --format=csv
-timeout 2400 python -m pytest tests -m gpu -q --timeout 900 -p no:cacheprovider > gpurun_out/r31_pytest.log 2>&1; echo "pytest rc=$?"
-grep -E "^FAILED|passed|failed" gpurun_out/r31_pytest.log | tail -20
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r31_smoke.log 2>&1; tail -1 gpurun_out/r31_smoke.log
-timeout 900 python bench.py > gpurun_out/r31_benchB.json 2> gpurun_out/r31_benchB.err; echo "benchB rc=$?"
-timeout 900 python bench.py --config D --no-cpu-baseline --plain-steps 50 > gpurun_out/r31_benchD.json 2> gpurun_out/r31_benchD.err; echo "benchD rc=$?"
-timeout 900 python bench.py --config E --no-cpu-baseline --plain-steps 50 > gpurun_out/r31_benchE.json 2> gpurun_out/r31_benchE.err; echo "benchE rc=$?"
-timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/r31_ref.json 2> gpurun_out/r31_ref.err; echo "ref rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:spmv_xw_kernel -s 3 -c 1 -o gpurun_out/r31_pairB python bench.py --steps 3 --warmup 3 --plain-steps 0 --no-cpu-baseline --e2e-steps 1 > /dev/null 2>&1; echo "ncu pair rc=$?"
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/r31_launchesB.csv python bench.py --steps 3 --warmup 3 --plain-steps 0 --no-cpu-baseline --e2e-steps 1 > /dev/null 2>&1; echo "ncu B rc=$?"
-for f in r31_benchB r31_benchD r31_benchE r31_ref; do cut -c1-250 gpurun_out/$f.json; done
+timeout 900 python -m pytest tests/test_gpu_dia.py -q --timeout 300 -p no:cacheprovider > gpurun_out/r68_pytest.log 2>&1; echo "pytest rc=$?"; tail -1 gpurun_out/r68_pytest.log; grep -E "^FAILED|Error" gpurun_out/r68_pytest.log | head -20
+timeout 900 python tools/xw_sweep.py B E D > gpurun_out/r68_xw_sweep.jsonl 2> gpurun_out/r68_xw_sweep.err; echo "sweep rc=$?"; tail -3 gpurun_out/r68_xw_sweep.err
+python - <<'PY'
+import json
+for l in open("gpurun_out/r68_xw_sweep.jsonl"):
+    d = json.loads(l)
+    print(d["config"], d["setting"], d["xwin"]["variant"], d["dia"], round(d["iteration_ms"], 4), {k: round(v, 4) for k, v in d["ms"].items()})
+PY

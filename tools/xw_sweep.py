@@ -26,7 +26,7 @@ CFG = {"B": ("poisson3d", 464, 0, 0.0, "cg"), "E": ("poisson3d", 368, 0, 0.0, "c
 def run(name, arrays, setting, env):
     kind, p1, p2, fp, backend = CFG[name]
     nr, n, rp, ci, v = arrays
-    for k in ("SPARSLA_XWIN", "SPARSLA_XW_VARIANT", "SPARSLA_VALUE_DICT", "SPARSLA_XW_PAIR"):
+    for k in ("SPARSLA_XWIN", "SPARSLA_XW_VARIANT", "SPARSLA_VALUE_DICT", "SPARSLA_XW_PAIR", "SPARSLA_DIA"):
         os.environ.pop(k, None)
     os.environ.update(env)
     D = S.DeviceCsr(None, 0, i32=(n, n, rp, ci, v))
@@ -43,7 +43,7 @@ def run(name, arrays, setting, env):
     else:
         names = ["u1", "spmv_v", "u2", "spmv_t", "u3"]
         byts = [None, base + 8 * n, None, base + 8 * n, None]
-    out = {"config": name, "setting": setting, "format": fmt, "xwin": xw,
+    out = {"config": name, "setting": setting, "format": fmt, "xwin": xw, "dia": D.dia(),
            "ms": dict(zip(names, ms)), "iteration_ms": float(sum(ms))}
     for nm, b, t in zip(names, byts, ms):
         if b:
@@ -62,18 +62,20 @@ def main():
     for name in args or ["B", "E", "D", "C"]:
         kind, p1, p2, fp, backend = CFG[name]
         arrays = S.generate_i32(kind, p1, p2, fp)
-        run(name, arrays, "gather", {"SPARSLA_XWIN": "0"})
-        run(name, arrays, "xwin-1", {"SPARSLA_XWIN": "1"})
+        run(name, arrays, "gather", {"SPARSLA_XWIN": "0", "SPARSLA_DIA": "0"})
+        run(name, arrays, "xwin-1", {"SPARSLA_XWIN": "1", "SPARSLA_DIA": "0"})
+        run(name, arrays, "dia", {"SPARSLA_DIA": "1"})
         for var in variants or []:
             env = {"SPARSLA_XWIN": "2", "SPARSLA_XW_VARIANT": str(var)}
             vs = XW_STREAM[var]
             if vs == 0:
                 env["SPARSLA_VALUE_DICT"] = "0"
             env["SPARSLA_XW_PAIR"] = "1" if vs == 2 else "0"
+            env["SPARSLA_DIA"] = "0"
             run(name, arrays, f"xwin-v{var}", env)
         if name != "C":  # plain CSR beside the dictionary
-            run(name, arrays, "gather-plain", {"SPARSLA_XWIN": "0", "SPARSLA_VALUE_DICT": "0"})
-            run(name, arrays, "xwin-plain", {"SPARSLA_XWIN": "1", "SPARSLA_VALUE_DICT": "0"})
+            run(name, arrays, "gather-plain", {"SPARSLA_XWIN": "0", "SPARSLA_VALUE_DICT": "0", "SPARSLA_DIA": "0"})
+            run(name, arrays, "xwin-plain", {"SPARSLA_XWIN": "1", "SPARSLA_VALUE_DICT": "0", "SPARSLA_DIA": "0"})
 
 
 if __name__ == "__main__":
