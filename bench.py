@@ -500,7 +500,8 @@ def run_ours(args):
         with open(os.path.join(ROOT, "profiles", "spmv_traffic.json")) as f:
             tj = json.load(f)
         if tj.get("size") == cfg["p1"] and cfg["name"] == "B":
-            key = ("pair_xwin" if xw["stream"] == 2 else "xwin") if 1 in xw["modes"] else \
+            key = "dia" if dia and 1 in dia["modes"] else \
+                ("pair_xwin" if xw["stream"] == 2 else "xwin") if 1 in xw["modes"] else \
                 ("value_dict" if fmt["value_dict"] else "plain")
             traffic = tj[key]["dram_bytes_per_launch"] if key in tj else None
     except Exception:

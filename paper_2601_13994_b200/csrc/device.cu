@@ -305,8 +305,13 @@ struct DiaVariant {
       (const void*)spmv_dia_kernel<SPMV_BICG_V, R, M>, (const void*)spmv_dia_kernel<SPMV_BICG_T, R, M>}}
 // measured on B200, config B CG SpMV (tools/r02_call34.sh): 1 round / 5 CTAs per SM
 // 0.776 ms, 1 / 4: 0.813, 2 / 4: 0.820, 1 / 6: 0.799, 2 / 3: 0.912 (x-window pair: 0.771)
-static const DiaVariant kDiaVariants[] = {DIAV(1, 5), DIAV(1, 4), DIAV(2, 4)};
+#define DIARV(M)                                                                                     \
+    {{(const void*)spmv_diar_kernel<SPMV_PLAIN, M>, (const void*)spmv_diar_kernel<SPMV_CG, M>,          \
+      (const void*)spmv_diar_kernel<SPMV_BICG_V, M>, (const void*)spmv_diar_kernel<SPMV_BICG_T, M>}}
+// 3..5: register-pattern kernel (spmv_diar_kernel) at 4 / 5 / 3 CTAs per SM
+static const DiaVariant kDiaVariants[] = {DIAV(1, 5), DIAV(1, 4), DIAV(2, 4), DIARV(4), DIARV(5), DIARV(3)};
 #undef DIAV
+#undef DIARV
 constexpr int kNumDiaVariants = sizeof(kDiaVariants) / sizeof(kDiaVariants[0]);
 
 // diagonal-warp table (spmv_dia.cuh) from the device CSR and dictionary indices; kept when
@@ -328,6 +333,8 @@ static void build_dia(DevCsr* A) {
     int32_t* tab = dalloc<int32_t>(nwarps * kDiaInts);
     dia_build_kernel<<<grid_for(nwarps * 32, 256), 256, 0, A->stream>>>(A->rp, A->ci, A->vidx, A->nrows, nwarps,
                                                                           tab, cnt);
+    CK(cudaGetLastError());
+    dia_link_kernel<<<grid_for(nwarps, 256), 256, 0, A->stream>>>(tab, nwarps);
     CK(cudaGetLastError());
     unsigned long long h[2] = {0, 0};
     CK(cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, A->stream));

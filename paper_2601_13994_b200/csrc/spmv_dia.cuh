@@ -15,7 +15,7 @@
 //
 // Table entry (12 ints per warp): [0..6] delta_k (0 past the last diagonal), [7] v0..v3,
 // [8] v4..v6 | m << 24 (m diagonals; 0xFF = unstructured), [9] exception bytes
-// (lane << 3 | k, 0x07 = none), [10..11] 0.
+// (lane << 3 | k, 0x07 = none), [10] link flag (dia_link_kernel), [11] 0.
 #pragma once
 
 #include "kernels.cuh"
@@ -269,6 +269,182 @@ __global__ void __launch_bounds__(kSpmvThreads, MINB) spmv_dia_kernel(SpmvParams
             y = dia_csr_row(P, row);
         }
         finish(row, y);
+    }
+    if constexpr (ND > 0) {
+        __shared__ double sred[SpmvFin<MODE>::n * kW];
+        block_tree<kSpmvThreads, ND>(acc, sred);
+        publish_and_finish<kSpmvThreads, ND, SpmvFin<MODE>::n>(acc, chunk, P.red, sred);
+    }
+}
+
+// Second build pass: e[10] = kDiaSame when the entry's diagonals and values (words 0..8)
+// equal those of the same warp slot one round earlier in the same chunk and both are
+// structured — spmv_diar_kernel then keeps that round's registers instead of re-decoding.
+constexpr int32_t kDiaSame = 1;
+static __global__ void dia_link_kernel(int32_t* __restrict__ tab, long long nwarps) {
+    const long long w = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= nwarps) return;
+    constexpr int kW = kSpmvThreads / 32;
+    const int r = (int)((w / kW) % kChunkRounds);
+    int32_t* e = tab + w * kDiaInts;
+    int same = 0;
+    if (r > 0) {
+        const int32_t* p = e - kW * kDiaInts;
+        same = ((uint32_t)e[8] >> 24) != kDiaUnstructured && ((uint32_t)p[8] >> 24) != kDiaUnstructured;
+        for (int k = 0; k < 9 && same; ++k) same = e[k] == p[k];
+    }
+    e[10] = same ? kDiaSame : 0;
+}
+
+// v = x[a] when p (one predicated ld.global.nc: the compiler would branch around a guarded
+// __ldg per slot)
+__device__ __forceinline__ void ldg_pred(double& v, const double* a, bool p) {
+    asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.global.nc.f64 %0, [%1];\n\t}"
+                 : "+d"(v) : "l"(a), "r"((unsigned)p));
+}
+
+// The 7 x operands of a row.  C > 0: slots C-1, C, C+1 are the diagonals -1, 0, +1 (a
+// canonical stencil row), taken from x[row] and its neighbouring lanes (one predicated
+// load at each warp edge); C == 0: any pattern.  Other slots load x[row + delta], skipped
+// slots (missing entry, past the last diagonal, dead row) load nothing.
+template <int C>
+__device__ __forceinline__ void dia_gather(const int (&dl)[7], uint32_t skip, const double* __restrict__ x, int rb,
+                                           int lane, double xc, double (&xv)[7]) {
+    if constexpr (C > 0) {
+        // every load is issued before the shuffles, which wait on x[row]
+        double em = 0.0, ep = 0.0;  // (no copy of xc: a predicated load would wait on it)
+        ldg_pred(em, x + (rb - 1), lane == 0 && !((skip >> (C - 1)) & 1u));
+        ldg_pred(ep, x + (rb + 1), lane == 31 && !((skip >> (C + 1)) & 1u));
+#pragma unroll
+        for (int u = 0; u < 7; ++u) {
+            if (u < C - 1 || u > C + 1) {
+                xv[u] = 0.0;  // skipped slots are masked out of the sum
+                ldg_pred(xv[u], x + (rb + dl[u]), !((skip >> u) & 1u));
+            }
+        }
+        const double sm = __shfl_up_sync(0xffffffffu, xc, 1), sp = __shfl_down_sync(0xffffffffu, xc, 1);
+        xv[C - 1] = lane == 0 ? em : sm;
+        xv[C] = xc;
+        xv[C + 1] = lane == 31 ? ep : sp;
+    } else {
+#pragma unroll
+        for (int u = 0; u < 7; ++u) {
+            xv[u] = 0.0;
+            ldg_pred(xv[u], x + (rb + dl[u]), !((skip >> u) & 1u));
+        }
+    }
+}
+
+// Register-pattern variant.  The l1tex data pipe was the limiter of spmv_dia_kernel (76%
+// of its wavefronts: ~16 per warp-row were uniform shared-memory reads of the table entry
+// and the 7 dictionary values).  Here a warp decodes its entry into registers (7 deltas, 7
+// fp64 values) only when it differs from the previous round's (e[10]), reads one 8-byte
+// word per round otherwise, takes x[row] once (reused by the diagonal-0 slot and the CG
+// epilogue) and forms the +-1 diagonals by warp shuffles of it (one single-lane load at the
+// warp edge).  Same products and sums in the same order: bit-identical.
+template <int MODE, int MINB>
+__global__ void __launch_bounds__(kSpmvThreads, MINB) spmv_diar_kernel(SpmvParams P) {
+    constexpr int ND = SpmvDots<MODE>::n;
+    constexpr int NA = ND > 0 ? ND : 1;
+    constexpr int kW = kSpmvThreads / 32;
+    if (P.check_done && P.red.st->done) return;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const long long chunk = P.chunk_list ? (long long)P.chunk_list[blockIdx.x] : P.chunk0 + blockIdx.x;
+    const int4* tc = reinterpret_cast<const int4*>(P.dia) + chunk * kChunkRounds * kW * 3;
+    if (P.dia_ahead > 0 && !P.chunk_list && t >= 192) {  // as spmv_dia_kernel
+        const long long ca = chunk + P.dia_ahead;
+        if (ca < P.nch) {
+            const int4 e0 = __ldg(tc), e1 = __ldg(tc + 1);
+            const int dmax = max(max(max(e0.x, e0.y), max(e0.z, e0.w)), max(max(e1.x, e1.y), e1.z));
+            const int q = t - 192;
+            const long long j = ca * kChunk + dmax + 32 * q;
+            if (j >= 0 && j < P.ncols) asm volatile("prefetch.global.L2 [%0];" ::"l"(P.x + j));
+            if (j + 16 >= 0 && j + 16 < P.ncols) asm volatile("prefetch.global.L2 [%0];" ::"l"(P.x + j + 16));
+            if (q < 24)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const int4*>(P.dia) + ca * kChunkRounds * kW * 3 + 8 * q));
+        }
+    }
+    if (P.p2p && (long long)blockIdx.x >= P.n_interior) {  // CTA-uniform
+        if (t == 0) p2p_wait_halo(P.p2p, P.halo_v, P.red.st->ep_halo[P.halo_v]);
+        __syncthreads();
+    }
+    // no shared-memory staging: this warp's entries are read straight from the table (L1),
+    // word 2 (diagonal count, exceptions, link flag) one round ahead
+    const int4* tw = tc + warp * 3;
+    const long long base = chunk * kChunk;
+    const long long rem_rounds = (P.n - base + kChunkSlots - 1) / kChunkSlots;
+    const int nrounds = rem_rounds < kChunkRounds ? (int)rem_rounds : kChunkRounds;
+    const int n = (int)P.n;  // int32 CSR: rows < 2^31
+    const double* __restrict__ x = P.x;
+    double acc[NA];
+#pragma unroll
+    for (int d = 0; d < NA; ++d) acc[d] = 0.0;
+    int dl[7];
+    double vv[7];
+    uint32_t full = 0;  // 0x7F >> (7 - m): slots present in a row with no missing entry
+    int cls = 0;        // dia_gather shape of the decoded pattern
+#pragma unroll
+    for (int u = 0; u < 7; ++u) { dl[u] = 0; vv[u] = 0.0; }
+    int4 q2n = __ldg(tw + 2);
+#pragma unroll 1
+    for (int r = 0; r < nrounds; ++r) {
+        const int4* te = tw + r * kW * 3;
+        const int4 q2 = q2n;
+        if (r + 1 < nrounds) q2n = __ldg(te + kW * 3 + 2);
+        const int row = (int)base + r * kChunkSlots + t;
+        const bool live = row < n;
+        const uint32_t w8 = (uint32_t)q2.x;
+        double y = 0.0, xc = 0.0;
+        if ((w8 >> 24) == kDiaUnstructured) {  // warp-uniform: CSR loop on the fp64 values
+            if (live) {
+                y = dia_csr_row(P, row);
+                if constexpr (MODE == SPMV_CG) xc = __ldg(x + row);
+            }
+        } else {
+            if (!(q2.z & kDiaSame)) {  // decode: deltas and values into registers
+                const int4 q0 = __ldg(te), q1 = __ldg(te + 1);
+                dl[0] = q0.x; dl[1] = q0.y; dl[2] = q0.z; dl[3] = q0.w; dl[4] = q1.x; dl[5] = q1.y; dl[6] = q1.z;
+                const uint32_t vw0 = (uint32_t)q1.w;
+#pragma unroll
+                for (int u = 0; u < 7; ++u) vv[u] = __ldg(P.vtab + (((u < 4 ? vw0 : w8) >> (8 * (u & 3))) & 0xFFu));
+                const int m = (int)(w8 >> 24);
+                full = 0x7Fu >> (7 - m);
+                cls = 0;
+#pragma unroll
+                for (int c = 1; c <= 3; ++c)
+                    if (c + 1 < m && dl[c - 1] == -1 && dl[c] == 0 && dl[c + 1] == 1) cls = c;
+            }
+            const uint32_t ex = (uint32_t)q2.y;
+            uint32_t skip = ~full & 0x7Fu;
+            if (ex != (kDiaNoEx | (kDiaNoEx << 8))) {  // warp-uniform: a row misses entries
+                if (((ex >> 3) & 31u) == (uint32_t)lane) skip |= 1u << (ex & 7u);
+                if (((ex >> 11) & 31u) == (uint32_t)lane) skip |= 1u << ((ex >> 8) & 7u);
+                skip &= 0x7Fu;  // (a lone exception's "none" byte names slot 7)
+            }
+            if (!live) skip = 0x7Fu;
+            const int rb = live ? row : 0;
+            xc = __ldg(x + rb);
+            double xv[7];
+            if (cls == 3) dia_gather<3>(dl, skip, x, rb, lane, xc, xv);  // warp-uniform
+            else if (cls == 2) dia_gather<2>(dl, skip, x, rb, lane, xc, xv);
+            else if (cls == 1) dia_gather<1>(dl, skip, x, rb, lane, xc, xv);
+            else dia_gather<0>(dl, skip, x, rb, lane, xc, xv);
+            if (__all_sync(0xffffffffu, skip == 0)) {  // 7 diagonals, nothing missing
+#pragma unroll
+                for (int u = 0; u < 7; ++u) y = __dadd_rn(y, __dmul_rn(vv[u], xv[u]));
+            } else {
+#pragma unroll
+                for (int u = 0; u < 7; ++u) {
+                    const double s = __dadd_rn(y, __dmul_rn(vv[u], xv[u]));
+                    y = ((skip >> u) & 1u) ? y : s;
+                }
+            }
+        }
+        if (live) {
+            P.y[row] = y;
+            if constexpr (MODE == SPMV_CG) acc[0] = __dadd_rn(acc[0], __dmul_rn(xc, y));
+            else spmv_epilogue<MODE>(P, row, y, acc);
+        }
     }
     if constexpr (ND > 0) {
         __shared__ double sred[SpmvFin<MODE>::n * kW];

@@ -41,11 +41,11 @@ def _dia_on(monkeypatch):
     monkeypatch.setenv("SPARSLA_DIA", "1")
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5])
 def test_dia_variants_bitwise(S, O, gpu, monkeypatch, variant):
     """Every kDiaVariants entry (1 or 2 rounds per step, occupancy), odd round counts."""
     monkeypatch.setenv("SPARSLA_DIA_VARIANT", str(variant))
-    for case in ("poisson3d_odd", "perturbed"):
+    for case in CASES:
         A = _gen(O, case)
         D = to_S(S, A).device(0)
         assert D.dia()["on"]
