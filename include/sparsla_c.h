@@ -210,7 +210,9 @@ int sparsla_dcsr_xwin(const sparsla_dcsr* A, int64_t* out);
  * out[0]=bit m set when SpMV mode m (as in sparsla_dcsr_xwin) runs the diagonal-warp
  * kernel, out[1]=parts per million of structured warps (last build, also when below the
  * threshold), out[2]=matrix bytes one such SpMV reads (48-byte warp entries + the other
- * warps' CSR).  3 entries.  SPARSLA_DIA=0 at creation / set_values disables. */
+ * warps' CSR), out[3]=distinct patterns when the pattern-table kernel runs (a 4-byte word
+ * per 32-row warp; the <= 64 patterns travel as a kernel parameter), else 0.  4 entries.
+ * SPARSLA_DIA=0 at creation / set_values disables. */
 int sparsla_dcsr_dia(const sparsla_dcsr* A, int64_t* out);
 
 /* y = A x (sparse.cpp:135-154): rows accumulated left to right from 0.0, separate

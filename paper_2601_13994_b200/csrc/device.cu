@@ -269,7 +269,8 @@ DevCsr::~DevCsr() {
     cudaFree(rp); cudaFree(ci); cudaFree(val); cudaFree(dinv); cudaFree(ones);
     cudaFree(vidx); cudaFree(vtab);
     cudaFree(long_rows); cudaFree(long_bits); cudaFree(s_rp); cudaFree(s_ci); cudaFree(s_val);
-    cudaFree(xw); cudaFree(xwo); cudaFree(xvo); cudaFree(dia);
+    cudaFree(xw); cudaFree(xwo); cudaFree(xvo); cudaFree(dia); cudaFree(diaw);
+    delete[] diac;
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (side) cudaStreamDestroy(side);
@@ -291,14 +292,16 @@ static void configure_kernels_once(int device) {
 // coefficient stencils: {6, -1}).  The table holds the exact fp64 values, so every product
 // and sum is bit-identical.  SPARSLA_VALUE_DICT=0 disables.
 static void drop_value_dictionary(DevCsr* A) {
-    cudaFree(A->vidx); cudaFree(A->vtab); cudaFree(A->dia);
+    cudaFree(A->vidx); cudaFree(A->vtab); cudaFree(A->dia); cudaFree(A->diaw);
+    delete[] A->diac;
     A->vidx = nullptr; A->vtab = nullptr; A->vd = false;
-    A->dia = nullptr;
+    A->dia = nullptr; A->diaw = nullptr; A->diac = nullptr; A->dia_npat = 0;
 }
 
 // diagonal-warp kernel variants: rounds per step, min CTAs per SM (SPARSLA_DIA_VARIANT)
 struct DiaVariant {
     const void* fn[4];
+    bool pattern = false;  // spmv_diac_kernel: second argument = the DiaConst patterns
 };
 #define DIAV(R, M)                                                                                   \
     {{(const void*)spmv_dia_kernel<SPMV_PLAIN, R, M>, (const void*)spmv_dia_kernel<SPMV_CG, R, M>,      \
@@ -308,19 +311,99 @@ struct DiaVariant {
 #define DIARV(M)                                                                                     \
     {{(const void*)spmv_diar_kernel<SPMV_PLAIN, M>, (const void*)spmv_diar_kernel<SPMV_CG, M>,          \
       (const void*)spmv_diar_kernel<SPMV_BICG_V, M>, (const void*)spmv_diar_kernel<SPMV_BICG_T, M>}}
-// 3..5: register-pattern kernel (spmv_diar_kernel) at 4 / 5 / 3 CTAs per SM
-static const DiaVariant kDiaVariants[] = {DIAV(1, 5), DIAV(1, 4), DIAV(2, 4), DIARV(4), DIARV(5), DIARV(3)};
+#define DIACV(M)                                                                                     \
+    {{(const void*)spmv_diac_kernel<SPMV_PLAIN, M>, (const void*)spmv_diac_kernel<SPMV_CG, M>,          \
+      (const void*)spmv_diac_kernel<SPMV_BICG_V, M>, (const void*)spmv_diac_kernel<SPMV_BICG_T, M>}, true}
+// 3..5: register-pattern kernel (spmv_diar_kernel) at 4 / 5 / 3 CTAs per SM; 6..8: pattern-
+// table kernel (spmv_diac_kernel) at 5 / 6 / 4 / 8 CTAs per SM
+static const DiaVariant kDiaVariants[] = {DIAV(1, 5), DIAV(1, 4), DIAV(2, 4), DIARV(4), DIARV(5), DIARV(3),
+                                          DIACV(5), DIACV(6), DIACV(4), DIACV(8)};
 #undef DIAV
 #undef DIARV
+#undef DIACV
 constexpr int kNumDiaVariants = sizeof(kDiaVariants) / sizeof(kDiaVariants[0]);
 
 // diagonal-warp table (spmv_dia.cuh) from the device CSR and dictionary indices; kept when
 // at least 90% of the 32-row warps are structured, and then every SpMV mode takes it.
 // Measured on B200 (profiles/r02_dia.md): half the DRAM bytes of the x-window pair kernel,
 // config B CG SpMV 0.773 -> 0.68 ms, config D 0.49/0.51 -> 0.43/0.46 ms.  SPARSLA_DIA=0: off.
+// Pattern table (spmv_diac_kernel): deduplicate the structured entries by a 64-bit hash of
+// their diagonals and values, verify every entry against its slot's representative, and keep
+// a 32-bit word per warp plus <= kDiaPatterns patterns (deltas, fp64 values) for the kernel
+// parameter.  Any overflow or collision leaves the pattern table off.
+static void build_dia_patterns(DevCsr* A, const int32_t* tab, long long nwarps) {
+    cudaFree(A->diaw);
+    delete[] A->diac;
+    A->diaw = nullptr;
+    A->diac = nullptr;
+    A->dia_npat = 0;
+    cudaStream_t s = A->stream;
+    unsigned long long* keys = dalloc<unsigned long long>(2 * kDiaHashSlots);
+    unsigned long long* rep = keys + kDiaHashSlots;
+    int* flags = dalloc<int>(2 + kDiaHashSlots);  // overflow, collision, pid per slot
+    int16_t* slot = dalloc<int16_t>(nwarps);
+    CK(cudaMemsetAsync(keys, 0, kDiaHashSlots * 8, s));
+    CK(cudaMemsetAsync(rep, 0xFF, kDiaHashSlots * 8, s));
+    CK(cudaMemsetAsync(flags, 0, 2 * sizeof(int), s));
+    dia_hash_kernel<<<grid_for(nwarps, 256), 256, 0, s>>>(tab, nwarps, keys, rep, slot, flags);
+    CK(cudaGetLastError());
+    std::vector<unsigned long long> hk(2 * kDiaHashSlots);
+    int hf[2] = {0, 0};
+    CK(cudaMemcpyAsync(hk.data(), keys, hk.size() * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hf, flags, sizeof(hf), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    std::vector<std::pair<unsigned long long, int>> used;  // (representative warp, slot)
+    for (int i = 0; i < kDiaHashSlots; ++i)
+        if (hk[i] != 0ull) used.push_back({hk[kDiaHashSlots + i], i});
+    std::sort(used.begin(), used.end());
+    bool ok = !hf[0] && !used.empty() && (int)used.size() <= kDiaPatterns;
+    if (ok) {
+        std::vector<int> pid_of(kDiaHashSlots, (int)kDiaPidUnstructured);
+        std::vector<double> vt(256);
+        CK(cudaMemcpyAsync(vt.data(), A->vtab, 256 * 8, cudaMemcpyDeviceToHost, s));
+        auto* C = new DiaConst();
+        std::memset(C, 0, sizeof(DiaConst));
+        for (size_t p = 0; p < used.size(); ++p) {
+            int32_t e[kDiaInts];
+            CK(cudaMemcpyAsync(e, tab + (long long)used[p].first * kDiaInts, sizeof(e), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            const int m = (int)((uint32_t)e[8] >> 24);
+            for (int u = 0; u < 7; ++u) {
+                C->pat[p].d[u] = e[u];
+                const uint32_t w = u < 4 ? (uint32_t)e[7] : (uint32_t)e[8];
+                C->pat[p].v[u] = vt[(w >> (8 * (u & 3))) & 0xFFu];
+            }
+            C->pat[p].d[7] = m;
+            pid_of[used[p].second] = (int)p;
+        }
+        CK(cudaMemcpyAsync(flags + 2, pid_of.data(), kDiaHashSlots * sizeof(int), cudaMemcpyHostToDevice, s));
+        uint32_t* words = dalloc<uint32_t>(nwarps);
+        dia_compact_kernel<<<grid_for(nwarps, 256), 256, 0, s>>>(tab, nwarps, slot, rep, flags + 2, words, flags + 1);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(hf, flags, sizeof(hf), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (hf[1] == 0) {
+            A->diaw = words;
+            A->diac = reinterpret_cast<unsigned char*>(C);
+            A->dia_npat = (int)used.size();
+        } else {
+            cudaFree(words);
+            delete C;
+        }
+    }
+    cudaFree(keys);
+    cudaFree(flags);
+    cudaFree(slot);
+}
+
 static void build_dia(DevCsr* A) {
     cudaFree(A->dia);
+    cudaFree(A->diaw);
+    delete[] A->diac;
     A->dia = nullptr;
+    A->diaw = nullptr;
+    A->diac = nullptr;
+    A->dia_npat = 0;
     A->dia_frac = 0.0;
     A->dia_bytes = 0;
     const char* e = getenv("SPARSLA_DIA");
@@ -346,11 +429,15 @@ static void build_dia(DevCsr* A) {
     A->dia_bytes = live * kDiaInts * 4 + (long long)h[1];
     if (A->dia_frac >= 0.9) A->dia = tab;
     else cudaFree(tab);
-    A->dia_var = 0;
+    if (A->dia) build_dia_patterns(A, A->dia, nwarps);
+    // default: the pattern-table kernel at 8 CTAs/SM when the patterns fit (measured on B200,
+    // profiles/r02_dia.md: config B CG SpMV 0.573 -> 0.488 ms, D' 0.40/0.43 -> 0.33/0.37 ms)
+    A->dia_var = A->diac ? 9 : 0;
     if (const char* v = getenv("SPARSLA_DIA_VARIANT")) {
         const int x = atoi(v);
         if (x >= 0 && x < kNumDiaVariants) A->dia_var = x;
     }
+    if (kDiaVariants[A->dia_var].pattern && !A->diac) A->dia_var = 0;  // no pattern table
     int sms = 0, per_sm = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, A->device));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kDiaVariants[A->dia_var].fn[SPMV_CG], kSpmvThreads, 0));
@@ -907,6 +994,11 @@ void devcsr_dia_info(const DevCsr* A, int64_t* out) {
     for (int m = 0; m < 4; ++m) out[0] |= (dia_pick(A, m) ? 1 : 0) << m;
     out[1] = (int64_t)(A->dia_frac * 1e6 + 0.5);
     out[2] = A->dia ? A->dia_bytes : 0;
+    out[3] = 0;
+    if (A->dia && kDiaVariants[A->dia_var].pattern) {  // 4-byte words instead of 48-byte entries
+        out[2] -= ((A->nrows + 31) / 32) * (kDiaInts * 4 - 4);
+        out[3] = A->dia_npat;
+    }
 }
 
 unsigned spmv_grid(const DevCsr* A, long long nch, int mode, bool xw_ok) {
@@ -957,7 +1049,13 @@ void launch_spmv_part(DevCsr* A, cudaStream_t s, int mode, const double* x, doub
         P.dia_ahead = A->dia_ahead;
         P.ncols = A->ncols;
         void* args[] = {&P};
-        CK(cudaLaunchKernel(kDiaVariants[A->dia_var].fn[mode], dim3(grid), dim3(kSpmvThreads), args, 0, s));
+        if (kDiaVariants[A->dia_var].pattern) {
+            P.diaw = A->diaw;
+            void* args2[] = {&P, A->diac};
+            CK(cudaLaunchKernel(kDiaVariants[A->dia_var].fn[mode], dim3(grid), dim3(kSpmvThreads), args2, 0, s));
+        } else {
+            CK(cudaLaunchKernel(kDiaVariants[A->dia_var].fn[mode], dim3(grid), dim3(kSpmvThreads), args, 0, s));
+        }
     } else if (xv >= 0) {
         P.xw = A->xw;
         P.xwo = xw_stream(A) == 2 ? A->xvo : A->xwo;

@@ -77,6 +77,9 @@ struct DevCsr {
     int dia_ahead = 0;           // chunks ahead a diagonal-warp CTA prefetches (whole waves)
     int dia_var = 0;             // kDiaVariants index
     int dia_modes = 0;           // SpMV modes (bit per SpmvMode) that take it
+    uint32_t* diaw = nullptr;    // pattern-table kernel: [chunks * 64 warps] pattern id + exceptions
+    unsigned char* diac = nullptr;  // host DiaConst (the deduplicated patterns), kernel parameter
+    int dia_npat = 0;            // distinct patterns (0: no pattern table)
     double xw_cover = 0.0;     // fraction of entries whose x operand is staged
     int sms = 0;               // multiprocessors of the device (set with the variants)
     DevCsr* transpose = nullptr;

@@ -554,6 +554,7 @@ struct SpmvParams {
     int cap_x;            //   staged x elements per round
     const int32_t* dia;   // diagonal-warp table (spmv_dia.cuh): [chunks * 8 rounds * 8 warps][12]
     int dia_ahead;        //   chunks ahead whose leading x lines a CTA prefetches (one wave)
+    const uint32_t* diaw; //   pattern-table kernel: one 32-bit word per 32-row warp
     long long ncols;      //   x length (prefetch bound)
     RedParams red;
 };

@@ -454,3 +454,162 @@ __global__ void __launch_bounds__(kSpmvThreads, MINB) spmv_diar_kernel(SpmvParam
 }
 
 }  // namespace sparsla_b200
+
+namespace sparsla_b200 {
+
+// ---------------------------------------------------------------------------------------
+// Pattern-table variant (spmv_diac_kernel).  The distinct structured table entries of a
+// matrix ("patterns": diagonals + values; a 3-D stencil has ~10: interior, boundary planes
+// and lines) are deduplicated at build time and passed by value as a __grid_constant__
+// kernel parameter, so a warp's per-round description shrinks to one 32-bit word (pattern
+// id + exceptions: 4 B per 32 rows instead of 48) and the deltas and fp64 values are read
+// through the constant cache (LDC) instead of the l1tex pipe that bounds spmv_dia_kernel.
+constexpr int kDiaPatterns = 64;
+constexpr uint32_t kDiaPidUnstructured = 0xFFu;
+struct DiaPattern {
+    int d[8];      // deltas of the m diagonals (0 past the last), d[7] = m
+    double v[8];   // their fp64 values (v[7] unused)
+};
+struct DiaConst {
+    DiaPattern pat[kDiaPatterns];
+};
+constexpr int kDiaHashSlots = 512;
+
+// build pass 1: hash each structured entry's words 0..8 into an open-addressed table of
+// kDiaHashSlots 64-bit keys; the lowest warp index of a slot is its representative
+static __global__ void dia_hash_kernel(const int32_t* __restrict__ tab, long long nwarps,
+                                       unsigned long long* keys, unsigned long long* rep, int16_t* slot,
+                                       int* overflow) {
+    const long long w = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= nwarps) return;
+    const int32_t* e = tab + w * kDiaInts;
+    if (((uint32_t)e[8] >> 24) == kDiaUnstructured) { slot[w] = -1; return; }
+    unsigned long long h = 1469598103934665603ull;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) h = (h ^ (uint32_t)e[k]) * 1099511628211ull;
+    h |= 1ull;  // 0 marks an empty slot
+    int i = (int)(h % kDiaHashSlots);
+    for (int probe = 0; probe < kDiaHashSlots; ++probe) {
+        const unsigned long long prev = atomicCAS(keys + i, 0ull, h);
+        if (prev == 0ull || prev == h) {
+            atomicMin(rep + i, (unsigned long long)w);
+            slot[w] = (int16_t)i;
+            return;
+        }
+        i = (i + 1) % kDiaHashSlots;
+    }
+    slot[w] = -2;
+    atomicExch(overflow, 1);
+}
+
+// build pass 2: per warp the 32-bit word [pid | ex0 << 8 | ex1 << 16]; an entry that differs
+// from its slot's representative (a hash collision) raises *bad (the host then keeps the
+// 48-byte table kernel)
+static __global__ void dia_compact_kernel(const int32_t* __restrict__ tab, long long nwarps,
+                                          const int16_t* __restrict__ slot, const unsigned long long* __restrict__ rep,
+                                          const int* __restrict__ pid_of, uint32_t* __restrict__ words, int* bad) {
+    const long long w = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= nwarps) return;
+    const int32_t* e = tab + w * kDiaInts;
+    const int s = slot[w];
+    uint32_t pid = kDiaPidUnstructured;
+    if (s >= 0) {
+        const int32_t* r = tab + (long long)rep[s] * kDiaInts;
+        for (int k = 0; k < 9; ++k)
+            if (e[k] != r[k]) atomicExch(bad, 1);
+        pid = (uint32_t)pid_of[s];
+    } else if (s == -2) {
+        atomicExch(bad, 1);
+    }
+    words[w] = pid | (((uint32_t)e[9] & 0xFFFFu) << 8);
+}
+
+template <int MODE, int MINB>
+__global__ void __launch_bounds__(kSpmvThreads, MINB) spmv_diac_kernel(SpmvParams P, const __grid_constant__ DiaConst C) {
+    constexpr int ND = SpmvDots<MODE>::n;
+    constexpr int NA = ND > 0 ? ND : 1;
+    constexpr int kW = kSpmvThreads / 32;
+    if (P.check_done && P.red.st->done) return;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const long long chunk = P.chunk_list ? (long long)P.chunk_list[blockIdx.x] : P.chunk0 + blockIdx.x;
+    const uint32_t* wc = P.diaw + chunk * kChunkRounds * kW;
+    const long long base = chunk * kChunk;
+    const long long rem_rounds = (P.n - base + kChunkSlots - 1) / kChunkSlots;
+    const int nrounds = rem_rounds < kChunkRounds ? (int)rem_rounds : kChunkRounds;
+    // lane r holds this warp's word of round r
+    const uint32_t wpre = lane < nrounds ? __ldg(wc + lane * kW + warp) : kDiaPidUnstructured;
+    if (P.dia_ahead > 0 && !P.chunk_list && t >= 192) {
+        // one wave ahead: the leading diagonal of the chunk a successor CTA will take (the
+        // largest delta of this chunk's first pattern), pulled into L2
+        const long long ca = chunk + P.dia_ahead;
+        if (ca < P.nch) {
+            const uint32_t p0 = __ldg(wc) & 0xFFu;
+            int dmax = 0;
+            if (p0 != kDiaPidUnstructured) {
+#pragma unroll
+                for (int u = 0; u < 7; ++u) dmax = max(dmax, C.pat[p0].d[u]);
+            }
+            const int q = t - 192;
+            const long long j = ca * kChunk + dmax + 32 * q;
+            if (j >= 0 && j < P.ncols) asm volatile("prefetch.global.L2 [%0];" ::"l"(P.x + j));
+            if (j + 16 >= 0 && j + 16 < P.ncols) asm volatile("prefetch.global.L2 [%0];" ::"l"(P.x + j + 16));
+            if (q < 2) asm volatile("prefetch.global.L2 [%0];" ::"l"(P.diaw + ca * kChunkRounds * kW + 32 * q));
+        }
+    }
+    if (P.p2p && (long long)blockIdx.x >= P.n_interior) {  // CTA-uniform
+        if (t == 0) p2p_wait_halo(P.p2p, P.halo_v, P.red.st->ep_halo[P.halo_v]);
+        __syncthreads();
+    }
+    const int n = (int)P.n;  // int32 CSR: rows < 2^31
+    const double* __restrict__ x = P.x;
+    double acc[NA];
+#pragma unroll
+    for (int d = 0; d < NA; ++d) acc[d] = 0.0;
+#pragma unroll 1
+    for (int r = 0; r < nrounds; ++r) {
+        const uint32_t wd = __shfl_sync(0xffffffffu, wpre, r);
+        const uint32_t pid = wd & 0xFFu;
+        const int row = (int)base + r * kChunkSlots + t;
+        const bool live = row < n;
+        double y = 0.0;
+        if (pid == kDiaPidUnstructured) {  // warp-uniform: CSR loop on the fp64 values
+            if (live) y = dia_csr_row(P, row);
+        } else {
+            const DiaPattern& pt = C.pat[pid];
+            const int m = pt.d[7];
+            const uint32_t ex = wd >> 8;
+            const int rb = live ? row : 0;
+            double xv[7];
+            if (m == 7 && ex == (kDiaNoEx | (kDiaNoEx << 8)) && __all_sync(0xffffffffu, live)) {
+#pragma unroll
+                for (int u = 0; u < 7; ++u) xv[u] = __ldg(x + (rb + pt.d[u]));
+#pragma unroll
+                for (int u = 0; u < 7; ++u) y = __dadd_rn(y, __dmul_rn(pt.v[u], xv[u]));
+            } else {
+                uint32_t skip = (0x7Fu << m) & 0x7Fu;
+                if (((ex >> 3) & 31u) == (uint32_t)lane) skip |= 1u << (ex & 7u);
+                if (((ex >> 11) & 31u) == (uint32_t)lane) skip |= 1u << ((ex >> 8) & 7u);
+                skip &= 0x7Fu;
+                if (!live) skip = 0x7Fu;
+#pragma unroll
+                for (int u = 0; u < 7; ++u) xv[u] = __ldg(x + (((skip >> u) & 1u) ? rb : rb + pt.d[u]));
+#pragma unroll
+                for (int u = 0; u < 7; ++u) {
+                    const double s = __dadd_rn(y, __dmul_rn(pt.v[u], xv[u]));
+                    y = ((skip >> u) & 1u) ? y : s;
+                }
+            }
+        }
+        if (live) {
+            P.y[row] = y;
+            spmv_epilogue<MODE>(P, row, y, acc);
+        }
+    }
+    if constexpr (ND > 0) {
+        __shared__ double sred[SpmvFin<MODE>::n * kW];
+        block_tree<kSpmvThreads, ND>(acc, sred);
+        publish_and_finish<kSpmvThreads, ND, SpmvFin<MODE>::n>(acc, chunk, P.red, sred);
+    }
+}
+
+}  // namespace sparsla_b200

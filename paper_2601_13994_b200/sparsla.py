@@ -299,11 +299,12 @@ class DeviceCsr:
 
     def dia(self):
         """Diagonal-warp SpMV (csrc/spmv_dia.cuh): {on (every SpMV mode), modes (SpMV modes
-        that take it), structured (fraction of 32-row warps), bytes (matrix bytes per SpMV)}."""
-        out = np.zeros(3, np.int64)
+        that take it), structured (fraction of 32-row warps), bytes (matrix bytes per SpMV),
+        patterns (distinct patterns of the pattern-table kernel, 0 = 48-byte table kernel)}."""
+        out = np.zeros(4, np.int64)
         _check(lib().sparsla_dcsr_dia(self.h, _p(out, _i64p)))
         return {"on": int(out[0]) == 0xF, "modes": [m for m in range(4) if (int(out[0]) >> m) & 1],
-                "structured": out[1] / 1e6, "bytes": int(out[2])}
+                "structured": out[1] / 1e6, "bytes": int(out[2]), "patterns": int(out[3])}
 
     def format(self):
         """SpMV storage format: value dictionary on / distinct values / constant Jacobi diagonal."""
@@ -986,10 +987,10 @@ class DistPlan:
 
     def dia(self):
         """This rank's local-matrix diagonal-warp SpMV (see DeviceCsr.dia)."""
-        out = np.zeros(3, np.int64)
+        out = np.zeros(4, np.int64)
         _check(lib().sparsla_dist_dia(self.h, _p(out, _i64p)))
         return {"on": int(out[0]) == 0xF, "modes": [m for m in range(4) if (int(out[0]) >> m) & 1],
-                "structured": out[1] / 1e6, "bytes": int(out[2])}
+                "structured": out[1] / 1e6, "bytes": int(out[2]), "patterns": int(out[3])}
 
     def set_values(self, vals_local, mem=MEM_HOST):
         """Collective: new values of this rank's local matrix (local entry order)."""

@@ -41,7 +41,7 @@ def _dia_on(monkeypatch):
     monkeypatch.setenv("SPARSLA_DIA", "1")
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5, 6, 7, 8, 9])
 def test_dia_variants_bitwise(S, O, gpu, monkeypatch, variant):
     """Every kDiaVariants entry (1 or 2 rounds per step, occupancy), odd round counts."""
     monkeypatch.setenv("SPARSLA_DIA_VARIANT", str(variant))
@@ -66,6 +66,9 @@ def test_dia_selection(S, O, gpu, monkeypatch):
     monkeypatch.delenv("SPARSLA_DIA")
     d = to_S(S, O.generate("poisson3d", 40)).device(0).dia()
     assert d["on"] and d["modes"] == [0, 1, 2, 3], d
+    # default kernel: the pattern table (a 3-D stencil has a handful of diagonal/value
+    # patterns: interior, boundary planes and lines), 4 bytes per warp
+    assert 1 <= d["patterns"] <= 64, d
     monkeypatch.setenv("SPARSLA_DIA", "0")
     d = to_S(S, O.generate("poisson3d", 40)).device(0).dia()
     assert d["modes"] == [] and d["structured"] == 0, d
