@@ -302,6 +302,7 @@ static void drop_value_dictionary(DevCsr* A) {
 struct DiaVariant {
     const void* fn[4];
     bool pattern = false;  // spmv_diac_kernel: second argument = the DiaConst patterns
+    bool pers = false;     // resident grid looping over chunks (one ticket per CTA)
 };
 #define DIAV(R, M)                                                                                   \
     {{(const void*)spmv_dia_kernel<SPMV_PLAIN, R, M>, (const void*)spmv_dia_kernel<SPMV_CG, R, M>,      \
@@ -311,16 +312,23 @@ struct DiaVariant {
 #define DIARV(M)                                                                                     \
     {{(const void*)spmv_diar_kernel<SPMV_PLAIN, M>, (const void*)spmv_diar_kernel<SPMV_CG, M>,          \
       (const void*)spmv_diar_kernel<SPMV_BICG_V, M>, (const void*)spmv_diar_kernel<SPMV_BICG_T, M>}}
-#define DIACV(M)                                                                                     \
-    {{(const void*)spmv_diac_kernel<SPMV_PLAIN, M>, (const void*)spmv_diac_kernel<SPMV_CG, M>,          \
-      (const void*)spmv_diac_kernel<SPMV_BICG_V, M>, (const void*)spmv_diac_kernel<SPMV_BICG_T, M>}, true}
+#define DIACV(M, U)                                                                                  \
+    {{(const void*)spmv_diac_kernel<SPMV_PLAIN, M, U>, (const void*)spmv_diac_kernel<SPMV_CG, M, U>,    \
+      (const void*)spmv_diac_kernel<SPMV_BICG_V, M, U>, (const void*)spmv_diac_kernel<SPMV_BICG_T, M, U>}, true}
+#define DIACP(M)                                                                                     \
+    {{(const void*)spmv_diac_kernel<SPMV_PLAIN, M, 1, true>, (const void*)spmv_diac_kernel<SPMV_CG, M, 1, true>, \
+      (const void*)spmv_diac_kernel<SPMV_BICG_V, M, 1, true>,                                         \
+      (const void*)spmv_diac_kernel<SPMV_BICG_T, M, 1, true>}, true, true}
 // 3..5: register-pattern kernel (spmv_diar_kernel) at 4 / 5 / 3 CTAs per SM; 6..8: pattern-
-// table kernel (spmv_diac_kernel) at 5 / 6 / 4 / 8 CTAs per SM
+// table kernel (spmv_diac_kernel) at 5 / 6 / 4 / 8 CTAs per SM; 10, 11: rounds unrolled by 2
+// at 6 / 5 CTAs per SM; 12, 13: persistent at 6 / 8 CTAs per SM
 static const DiaVariant kDiaVariants[] = {DIAV(1, 5), DIAV(1, 4), DIAV(2, 4), DIARV(4), DIARV(5), DIARV(3),
-                                          DIACV(5), DIACV(6), DIACV(4), DIACV(8)};
+                                          DIACV(5, 1), DIACV(6, 1), DIACV(4, 1), DIACV(8, 1), DIACV(6, 2), DIACV(5, 2),
+                                          DIACP(6), DIACP(8)};
 #undef DIAV
 #undef DIARV
 #undef DIACV
+#undef DIACP
 constexpr int kNumDiaVariants = sizeof(kDiaVariants) / sizeof(kDiaVariants[0]);
 
 // diagonal-warp table (spmv_dia.cuh) from the device CSR and dictionary indices; kept when
@@ -430,9 +438,9 @@ static void build_dia(DevCsr* A) {
     if (A->dia_frac >= 0.9) A->dia = tab;
     else cudaFree(tab);
     if (A->dia) build_dia_patterns(A, A->dia, nwarps);
-    // default: the pattern-table kernel at 8 CTAs/SM when the patterns fit (measured on B200,
-    // profiles/r02_dia.md: config B CG SpMV 0.573 -> 0.488 ms, D' 0.40/0.43 -> 0.33/0.37 ms)
-    A->dia_var = A->diac ? 9 : 0;
+    // default: the pattern-table kernel at 6 CTAs/SM when the patterns fit (measured on B200,
+    // profiles/r02_dia.md: config B CG SpMV 0.573 -> 0.487 ms, D' 0.40/0.43 -> 0.30/0.33 ms)
+    A->dia_var = A->diac ? 7 : 0;
     if (const char* v = getenv("SPARSLA_DIA_VARIANT")) {
         const int x = atoi(v);
         if (x >= 0 && x < kNumDiaVariants) A->dia_var = x;
@@ -444,6 +452,7 @@ static void build_dia(DevCsr* A) {
     // prefetch distance in waves of resident CTAs (SPARSLA_DIA_PREFETCH, default 1; 0 = off)
     const char* pe = getenv("SPARSLA_DIA_PREFETCH");
     A->dia_ahead = (pe ? atoi(pe) : 1) * sms * per_sm;
+    A->dia_ctas = sms * per_sm;
 }
 
 static void build_value_dictionary(DevCsr* A, const double* h_val) {
@@ -1003,7 +1012,8 @@ void devcsr_dia_info(const DevCsr* A, int64_t* out) {
 
 unsigned spmv_grid(const DevCsr* A, long long nch, int mode, bool xw_ok) {
     if (nch <= 0) return 0;
-    if (dia_pick(A, mode)) return (unsigned)nch;
+    if (dia_pick(A, mode))
+        return kDiaVariants[A->dia_var].pers ? (unsigned)std::min<long long>(nch, (long long)A->dia_ctas) : (unsigned)nch;
     if (xw_ok && xw_pick(A, mode) >= 0)
         return (unsigned)std::min<long long>(nch, (long long)A->xw_ctas[xw_stream(A)][mode_has_aux(mode)]);
     if (A->staged) {

@@ -80,6 +80,7 @@ struct DevCsr {
     uint32_t* diaw = nullptr;    // pattern-table kernel: [chunks * 64 warps] pattern id + exceptions
     unsigned char* diac = nullptr;  // host DiaConst (the deduplicated patterns), kernel parameter
     int dia_npat = 0;            // distinct patterns (0: no pattern table)
+    int dia_ctas = 0;            // resident CTAs of the diagonal-warp variant (persistent grid)
     double xw_cover = 0.0;     // fraction of entries whose x operand is staged
     int sms = 0;               // multiprocessors of the device (set with the variants)
     DevCsr* transpose = nullptr;

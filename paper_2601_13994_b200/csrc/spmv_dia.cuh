@@ -524,14 +524,21 @@ static __global__ void dia_compact_kernel(const int32_t* __restrict__ tab, long 
     words[w] = pid | (((uint32_t)e[9] & 0xFFFFu) << 8);
 }
 
-template <int MODE, int MINB>
+// PERS: a resident grid loops over the launch's chunks (list index i = blockIdx.x, + gridDim.x,
+// ...), stores one partial per chunk and takes ONE reduction ticket at the end (no per-chunk
+// atomic round trip holding the CTA slot); otherwise one chunk per CTA.
+template <int MODE, int MINB, int UNR = 1, bool PERS = false>
 __global__ void __launch_bounds__(kSpmvThreads, MINB) spmv_diac_kernel(SpmvParams P, const __grid_constant__ DiaConst C) {
     constexpr int ND = SpmvDots<MODE>::n;
     constexpr int NA = ND > 0 ? ND : 1;
     constexpr int kW = kSpmvThreads / 32;
     if (P.check_done && P.red.st->done) return;
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    const long long chunk = P.chunk_list ? (long long)P.chunk_list[blockIdx.x] : P.chunk0 + blockIdx.x;
+    __shared__ double sred[(SpmvFin<MODE>::n > 0 ? SpmvFin<MODE>::n : 1) * kW];
+    __shared__ int s_flag;
+    bool halo_ok = false;
+    for (long long li = blockIdx.x; li < (PERS ? P.nch : (long long)blockIdx.x + 1); li += gridDim.x) {
+    const long long chunk = P.chunk_list ? (long long)P.chunk_list[li] : P.chunk0 + li;
     const uint32_t* wc = P.diaw + chunk * kChunkRounds * kW;
     const long long base = chunk * kChunk;
     const long long rem_rounds = (P.n - base + kChunkSlots - 1) / kChunkSlots;
@@ -556,22 +563,27 @@ __global__ void __launch_bounds__(kSpmvThreads, MINB) spmv_diac_kernel(SpmvParam
             if (q < 2) asm volatile("prefetch.global.L2 [%0];" ::"l"(P.diaw + ca * kChunkRounds * kW + 32 * q));
         }
     }
-    if (P.p2p && (long long)blockIdx.x >= P.n_interior) {  // CTA-uniform
+    if (P.p2p && li >= P.n_interior && !halo_ok) {  // CTA-uniform
         if (t == 0) p2p_wait_halo(P.p2p, P.halo_v, P.red.st->ep_halo[P.halo_v]);
         __syncthreads();
+        halo_ok = true;
     }
     const int n = (int)P.n;  // int32 CSR: rows < 2^31
     const double* __restrict__ x = P.x;
     double acc[NA];
 #pragma unroll
     for (int d = 0; d < NA; ++d) acc[d] = 0.0;
-#pragma unroll 1
+#pragma unroll UNR
     for (int r = 0; r < nrounds; ++r) {
         const uint32_t wd = __shfl_sync(0xffffffffu, wpre, r);
         const uint32_t pid = wd & 0xFFu;
         const int row = (int)base + r * kChunkSlots + t;
         const bool live = row < n;
         double y = 0.0;
+        // the epilogue operand, loaded with the row's x operands (not after the sum)
+        double ea = 0.0;
+        if constexpr (MODE == SPMV_CG) ea = live ? __ldg(x + row) : 0.0;
+        if constexpr (MODE == SPMV_BICG_V || MODE == SPMV_BICG_T) ea = live ? __ldg(P.aux + row) : 0.0;
         if (pid == kDiaPidUnstructured) {  // warp-uniform: CSR loop on the fp64 values
             if (live) y = dia_csr_row(P, row);
         } else {
@@ -602,14 +614,27 @@ __global__ void __launch_bounds__(kSpmvThreads, MINB) spmv_diac_kernel(SpmvParam
         }
         if (live) {
             P.y[row] = y;
-            spmv_epilogue<MODE>(P, row, y, acc);
+            if constexpr (MODE == SPMV_CG || MODE == SPMV_BICG_V) {  // as spmv_epilogue
+                acc[0] = __dadd_rn(acc[0], __dmul_rn(ea, y));
+            } else if constexpr (MODE == SPMV_BICG_T) {
+                acc[0] = __dadd_rn(acc[0], __dmul_rn(y, y));
+                acc[1] = __dadd_rn(acc[1], __dmul_rn(y, ea));
+            }
         }
     }
     if constexpr (ND > 0) {
-        __shared__ double sred[SpmvFin<MODE>::n * kW];
         block_tree<kSpmvThreads, ND>(acc, sred);
-        publish_and_finish<kSpmvThreads, ND, SpmvFin<MODE>::n>(acc, chunk, P.red, sred);
+        if constexpr (PERS) {
+            if (t == 0) {
+#pragma unroll
+                for (int d = 0; d < ND; ++d) P.red.partials[d * P.red.nchunks + chunk] = acc[d];
+            }
+        } else {
+            publish_and_finish<kSpmvThreads, ND, SpmvFin<MODE>::n>(acc, chunk, P.red, sred);
+        }
     }
+    }  // chunk loop
+    if constexpr (PERS && ND > 0) ticket_and_finish<kSpmvThreads, ND, 0, SpmvFin<MODE>::n>(P.red, sred, &s_flag);
 }
 
 }  // namespace sparsla_b200

@@ -41,7 +41,7 @@ def _dia_on(monkeypatch):
     monkeypatch.setenv("SPARSLA_DIA", "1")
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5, 6, 7, 8, 9])
+@pytest.mark.parametrize("variant", list(range(14)))
 def test_dia_variants_bitwise(S, O, gpu, monkeypatch, variant):
     """Every kDiaVariants entry (1 or 2 rounds per step, occupancy), odd round counts."""
     monkeypatch.setenv("SPARSLA_DIA_VARIANT", str(variant))
