@@ -1288,8 +1288,10 @@ Solver::Solver(DevCsr* A_, int backend_, const sparsla_solve_options& o, DistCtx
         }
     }
     if (defer_x) p2 = dalloc<double>(nh);
-    tickets = dalloc<unsigned>(8);
-    CK(cudaMemset(tickets, 0, 8 * sizeof(unsigned)));
+    tickets = dalloc<unsigned>(16);  // [0, 8): per reduction point; [8, 16): multi_finish
+    CK(cudaMemset(tickets, 0, 16 * sizeof(unsigned)));
+    if (!getenv("SPARSLA_MULTI_FINISH") || atoi(getenv("SPARSLA_MULTI_FINISH")) != 0)
+        slotsum = dalloc<double>(4 * kFinalSlots);
     st = dalloc<KState>(1);
     CK(cudaMallocHost(&h_st, sizeof(KState)));
     CK(cudaMallocHost(&h_flag, 2 * sizeof(int)));
@@ -1310,14 +1312,14 @@ void Solver::release() noexcept {
     if (g_one) cudaGraphExecDestroy(g_one);
     if (g_one_odd) cudaGraphExecDestroy(g_one_odd);
     for (double* v : {x_own, b_own, r, p, p2, q, rh, ph, s, sh, t}) cudaFree(v);
-    cudaFree(partials); cudaFree(tickets); cudaFree(st); cudaFree(fused_bar);
+    cudaFree(partials); cudaFree(tickets); cudaFree(st); cudaFree(fused_bar); cudaFree(slotsum);
     if (h_st) cudaFreeHost(h_st);
     if (h_flag) cudaFreeHost(h_flag);
     if (ev[0]) cudaEventDestroy(ev[0]);
     if (ev[1]) cudaEventDestroy(ev[1]);
     g_many = g_one = g_one_odd = nullptr;
     x_own = b_own = r = p = p2 = q = rh = ph = s = sh = t = nullptr;
-    partials = nullptr; tickets = nullptr; st = nullptr; fused_bar = nullptr;
+    partials = nullptr; tickets = nullptr; st = nullptr; fused_bar = nullptr; slotsum = nullptr;
     h_st = nullptr; h_flag = nullptr; ev[0] = ev[1] = nullptr;
     cudaGetLastError();
 }
@@ -1327,6 +1329,7 @@ Solver::~Solver() { release(); }
 RedParams Solver::red(int which, int slot) const {
     RedParams R{};
     R.partials = partials; R.ticket = tickets + slot; R.st = st; R.red_out = nullptr; R.scalar = which;
+    R.slotsum = slotsum; R.ticket2 = tickets + 8 + slot;
     return R;
 }
 
@@ -1424,7 +1427,7 @@ void Solver::enqueue_init() {
     h.spmv_count = 1;
     *h_st = h;
     CK(cudaMemcpyAsync(st, h_st, sizeof(KState), cudaMemcpyHostToDevice, stream));
-    CK(cudaMemsetAsync(tickets, 0, 8 * sizeof(unsigned), stream));
+    CK(cudaMemsetAsync(tickets, 0, 16 * sizeof(unsigned), stream));
     CK(cudaMemsetAsync(x, 0, n * sizeof(double), stream));
     // initial residual r0 = b - A x0 (one SpMV, spmv_count = 1); x0 = 0 lives in p's storage
     // for the distributed case so the halo exchange has its slots

@@ -179,6 +179,7 @@ struct Solver {
     double *rh = nullptr, *ph = nullptr, *s = nullptr, *sh = nullptr, *t = nullptr;
     double* partials = nullptr;
     unsigned* tickets = nullptr;
+    double* slotsum = nullptr;   // multi_finish scratch [4][kFinalSlots] (SPARSLA_MULTI_FINISH=0: off)
     KState* st = nullptr;
     KState* h_st = nullptr;
     int* h_flag = nullptr;

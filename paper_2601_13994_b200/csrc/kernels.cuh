@@ -387,7 +387,73 @@ struct RedParams {
     const P2PCtx* p2p;    // fused peer collectives: push the totals of `point` instead
     int point;
     const KState* s_loc;  // consumer kernels: CTA-local scalar state to write back first
+    double* slotsum;      // [4][kFinalSlots] scratch: the last kFinishers CTAs split the
+    unsigned* ticket2;    //   level-2 slot sums (multi_finish); nullptr = one finishing CTA
 };
+
+// Parallel level-2 reduction.  The CTAs that draw the last kFinishers tickets of a
+// reduction point each wait until every CTA has published its partials, then sum 1/K of
+// the kFinalSlots slots (slot s: 0.0 + partials s, s + 1024, ... in that order, 8 loads in
+// flight) into `slotsum`; the last of them combines the slot sums exactly as final_reduce
+// does (4 consecutive slots per thread, pairwise, then block_tree) — the same additions in
+// the same order, bit-identical, but the ~48 sequential L2 round trips of one CTA become ~6
+// per finisher.  Returns true on the CTA whose thread 0 then holds the totals in `out`.
+constexpr int kFinishers = 8;
+// Only for a reduction point that is ONE launch (the finishers wait on CTAs of their own
+// grid, which free SM slots always let run: an interior/boundary split whose second launch
+// waits for the first would deadlock) and without fused peer collectives (a same-GPU peer's
+// kernel spinning on this rank's totals could hold the slots the remaining CTAs need).
+__device__ __forceinline__ bool multi_ok(const RedParams& R) {
+    return R.slotsum != nullptr && R.p2p == nullptr && R.expected >= (unsigned)kFinishers &&
+           R.expected == gridDim.x;
+}
+template <int NT, int NFIN, int BAR = 0>
+__device__ bool multi_finish(const RedParams& R, int fin, double (&out)[NFIN], double* sred, int* s_flag) {
+    constexpr int SPF = kFinalSlots / kFinishers;  // slots per finisher
+    const int t = threadIdx.x;
+    const long long m = R.nchunks;
+    if (t == 0) {
+        while (*reinterpret_cast<volatile unsigned*>(R.ticket) < R.expected) __nanosleep(64);
+    }
+    group_sync<BAR, NT>();
+    __threadfence();
+    for (int it = t; it < NFIN * SPF; it += NT) {
+        const int d = it / SPF, sl = fin * SPF + it % SPF;
+        const double* pp = R.partials + d * m;
+        double acc = 0.0;
+        long long c = sl;
+        for (; c + 7 * kFinalSlots < m; c += 8 * kFinalSlots) {
+            double a[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) a[q] = __ldcg(pp + c + q * kFinalSlots);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) acc = __dadd_rn(acc, a[q]);
+        }
+        for (; c < m; c += kFinalSlots) acc = __dadd_rn(acc, __ldcg(pp + c));
+        R.slotsum[d * kFinalSlots + sl] = acc;
+    }
+    __threadfence();
+    group_sync<BAR, NT>();
+    if (t == 0) *s_flag = atomicAdd(R.ticket2, 1u) == kFinishers - 1;
+    group_sync<BAR, NT>();
+    if (!*s_flag) return false;
+    __threadfence();
+    constexpr int SPT = kFinalSlots / NT;
+#pragma unroll
+    for (int d = 0; d < NFIN; ++d) {
+        double v[SPT];
+#pragma unroll
+        for (int j = 0; j < SPT; ++j) v[j] = __ldcg(R.slotsum + d * kFinalSlots + t * SPT + j);
+#pragma unroll
+        for (int w = 1; w < SPT; w *= 2)
+#pragma unroll
+            for (int i = 0; i + w < SPT; i += 2 * w) v[i] = __dadd_rn(v[i], v[i + w]);
+        out[d] = v[0];
+    }
+    block_tree<NT, NFIN, BAR>(out, sred);
+    if (t == 0) *R.ticket2 = 0u;
+    return true;
+}
 
 // NFIN >= NDOT: the last CTA reduces NFIN partial rows; rows NDOT.. were published per
 // chunk by an earlier kernel of the same reduction point (BiCGStab: s.s by update 2).
@@ -395,18 +461,26 @@ template <int NT, int NDOT, int NFIN = NDOT>
 __device__ void publish_and_finish(double (&part)[NDOT], long long chunk, const RedParams& R,
                                    double* sred) {
     __shared__ int s_last;
+    __shared__ int s_fin;
+    const bool multi = multi_ok(R);
     if (threadIdx.x == 0) {
 #pragma unroll
         for (int d = 0; d < NDOT; ++d) R.partials[d * R.nchunks + chunk] = part[d];
         __threadfence();
         const unsigned prev = atomicAdd(R.ticket, 1u);
         s_last = (prev == R.expected - 1);
+        s_fin = multi && prev >= R.expected - kFinishers ? (int)(prev - (R.expected - kFinishers)) : -1;
     }
     __syncthreads();
-    if (!s_last) return;
-    __threadfence();
     double tot[NFIN];
-    final_reduce<NT, NFIN>(R.partials, R.nchunks, tot, sred);
+    if (multi) {
+        if (s_fin < 0) return;
+        if (!multi_finish<NT, NFIN>(R, s_fin, tot, sred, &s_last)) return;
+    } else {
+        if (!s_last) return;
+        __threadfence();
+        final_reduce<NT, NFIN>(R.partials, R.nchunks, tot, sred);
+    }
     if (threadIdx.x == 0) {
         if (R.p2p) {
             if (R.s_loc) *R.st = *R.s_loc;
@@ -434,16 +508,24 @@ __device__ void publish_and_finish(double (&part)[NDOT], long long chunk, const 
 // the last CTA to finish reduces all chunks (same canonical result as publish_and_finish).
 template <int NT, int NDOT, int BAR, int NFIN = NDOT>
 __device__ void ticket_and_finish(const RedParams& R, double* sred, int* s_flag) {
+    const bool multi = multi_ok(R);
+    __shared__ int s_fin;
     if (threadIdx.x == 0) {
         __threadfence();
         const unsigned prev = atomicAdd(R.ticket, 1u);
         *s_flag = (prev == R.expected - 1);
+        s_fin = multi && prev >= R.expected - kFinishers ? (int)(prev - (R.expected - kFinishers)) : -1;
     }
     group_sync<BAR, NT>();
-    if (!*s_flag) return;
-    __threadfence();
     double tot[NFIN];
-    final_reduce<NT, NFIN, BAR>(R.partials, R.nchunks, tot, sred);
+    if (multi) {
+        if (s_fin < 0) return;
+        if (!multi_finish<NT, NFIN, BAR>(R, s_fin, tot, sred, s_flag)) return;
+    } else {
+        if (!*s_flag) return;
+        __threadfence();
+        final_reduce<NT, NFIN, BAR>(R.partials, R.nchunks, tot, sred);
+    }
     if (threadIdx.x == 0) {
         if (R.p2p) {
             if (R.s_loc) *R.st = *R.s_loc;
