@@ -60,3 +60,21 @@ def test_kernel_bytes_match_canonical_accounting():
     assert cg == bench.canonical_bytes("cg", n, nnz) - 8 * n
     bi = sum(b for _, b in bench.kernel_bytes("bicgstab", n, nnz, 0, False, False))
     assert bi == 24 * nnz + 8 * (n + 1) + 200 * n
+
+
+def test_diagonal_warp_bytes_and_format_text():
+    """The diagonal-warp SpMV's stored bytes replace the matrix stream and row pointers in
+    every mode it takes; the format text names the pattern table when it is the kernel."""
+    sys.path.insert(0, ROOT)
+    import bench
+    n, nnz = 4096, 7 * 4096
+    dia = {"modes": [0, 1, 2, 3], "bytes": 4 * (n // 32), "structured": 1.0, "patterns": 9}
+    kb = dict(bench.kernel_bytes("cg", n, nnz, 0, True, True, dia=dia, defer_x=True))
+    assert kb["spmv_cg"] == 4 * (n // 32) + 16 * n
+    assert kb["cg_update1"] == 24 * n and kb["cg_update2"] == 36 * n
+    kbb = dict(bench.kernel_bytes("bicgstab", n, nnz, 0, True, True, dia=dia))
+    assert kbb["spmv_v"] == kbb["spmv_t"] == 4 * (n // 32) + 24 * n
+    fmt = {"value_dict": True, "distinct_values": 2}
+    xw = {"modes": [], "cap_x": 0, "cover": 0.0, "stream": 0}
+    assert "pattern table" in bench.format_text(fmt, xw, dia) and "9 diagonal/value patterns" in bench.format_text(fmt, xw, dia)
+    assert "48-byte table entry" in bench.format_text(fmt, xw, dict(dia, patterns=0))
