@@ -315,20 +315,27 @@ struct DiaVariant {
 #define DIACV(M, U)                                                                                  \
     {{(const void*)spmv_diac_kernel<SPMV_PLAIN, M, U>, (const void*)spmv_diac_kernel<SPMV_CG, M, U>,    \
       (const void*)spmv_diac_kernel<SPMV_BICG_V, M, U>, (const void*)spmv_diac_kernel<SPMV_BICG_T, M, U>}, true}
+#define DIACN(M)                                                                                     \
+    {{(const void*)spmv_diac_kernel<SPMV_PLAIN, M, 1, false, true>,                                   \
+      (const void*)spmv_diac_kernel<SPMV_CG, M, 1, false, true>,                                      \
+      (const void*)spmv_diac_kernel<SPMV_BICG_V, M, 1, false, true>,                                  \
+      (const void*)spmv_diac_kernel<SPMV_BICG_T, M, 1, false, true>}, true}
 #define DIACP(M)                                                                                     \
     {{(const void*)spmv_diac_kernel<SPMV_PLAIN, M, 1, true>, (const void*)spmv_diac_kernel<SPMV_CG, M, 1, true>, \
       (const void*)spmv_diac_kernel<SPMV_BICG_V, M, 1, true>,                                         \
       (const void*)spmv_diac_kernel<SPMV_BICG_T, M, 1, true>}, true, true}
 // 3..5: register-pattern kernel (spmv_diar_kernel) at 4 / 5 / 3 CTAs per SM; 6..8: pattern-
 // table kernel (spmv_diac_kernel) at 5 / 6 / 4 / 8 CTAs per SM; 10, 11: rounds unrolled by 2
-// at 6 / 5 CTAs per SM; 12, 13: persistent at 6 / 8 CTAs per SM
+// at 6 / 5 CTAs per SM; 12, 13: persistent at 6 / 8 CTAs per SM; 14, 15: far diagonals
+// without L1 allocation at 6 / 8 CTAs per SM
 static const DiaVariant kDiaVariants[] = {DIAV(1, 5), DIAV(1, 4), DIAV(2, 4), DIARV(4), DIARV(5), DIARV(3),
                                           DIACV(5, 1), DIACV(6, 1), DIACV(4, 1), DIACV(8, 1), DIACV(6, 2), DIACV(5, 2),
-                                          DIACP(6), DIACP(8)};
+                                          DIACP(6), DIACP(8), DIACN(6), DIACN(8)};
 #undef DIAV
 #undef DIARV
 #undef DIACV
 #undef DIACP
+#undef DIACN
 constexpr int kNumDiaVariants = sizeof(kDiaVariants) / sizeof(kDiaVariants[0]);
 
 // diagonal-warp table (spmv_dia.cuh) from the device CSR and dictionary indices; kept when

@@ -527,7 +527,23 @@ static __global__ void dia_compact_kernel(const int32_t* __restrict__ tab, long 
 // PERS: a resident grid loops over the launch's chunks (list index i = blockIdx.x, + gridDim.x,
 // ...), stores one partial per chunk and takes ONE reduction ticket at the end (no per-chunk
 // atomic round trip holding the CTA slot); otherwise one chunk per CTA.
-template <int MODE, int MINB, int UNR = 1, bool PERS = false>
+// x operand of one diagonal: NA: diagonals farther than kDiaFar rows (the +-plane ones of a
+// 3-D stencil, never re-read from L1) bypass L1 allocation so the near diagonals' lines
+// (+-1, +-line, re-read by the rows a line later) stay resident
+constexpr int kDiaFar = 4096;
+template <bool NA>
+__device__ __forceinline__ double dia_x(const double* __restrict__ a, int d) {
+    if constexpr (NA) {
+        if (d >= kDiaFar || d <= -kDiaFar) {  // warp-uniform
+            double v;
+            asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(a));
+            return v;
+        }
+    }
+    return __ldg(a);
+}
+
+template <int MODE, int MINB, int UNR = 1, bool PERS = false, bool L1NA = false>
 __global__ void __launch_bounds__(kSpmvThreads, MINB) spmv_diac_kernel(SpmvParams P, const __grid_constant__ DiaConst C) {
     constexpr int ND = SpmvDots<MODE>::n;
     constexpr int NA = ND > 0 ? ND : 1;
@@ -594,7 +610,7 @@ __global__ void __launch_bounds__(kSpmvThreads, MINB) spmv_diac_kernel(SpmvParam
             double xv[7];
             if (m == 7 && ex == (kDiaNoEx | (kDiaNoEx << 8)) && __all_sync(0xffffffffu, live)) {
 #pragma unroll
-                for (int u = 0; u < 7; ++u) xv[u] = __ldg(x + (rb + pt.d[u]));
+                for (int u = 0; u < 7; ++u) xv[u] = dia_x<L1NA>(x + (rb + pt.d[u]), pt.d[u]);
 #pragma unroll
                 for (int u = 0; u < 7; ++u) y = __dadd_rn(y, __dmul_rn(pt.v[u], xv[u]));
             } else {
@@ -604,7 +620,7 @@ __global__ void __launch_bounds__(kSpmvThreads, MINB) spmv_diac_kernel(SpmvParam
                 skip &= 0x7Fu;
                 if (!live) skip = 0x7Fu;
 #pragma unroll
-                for (int u = 0; u < 7; ++u) xv[u] = __ldg(x + (((skip >> u) & 1u) ? rb : rb + pt.d[u]));
+                for (int u = 0; u < 7; ++u) xv[u] = dia_x<L1NA>(x + (((skip >> u) & 1u) ? rb : rb + pt.d[u]), pt.d[u]);
 #pragma unroll
                 for (int u = 0; u < 7; ++u) {
                     const double s = __dadd_rn(y, __dmul_rn(pt.v[u], xv[u]));
