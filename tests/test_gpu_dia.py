@@ -162,3 +162,40 @@ def test_dia_distributed_bitwise(S, O, gpu, kind, p1, P, solver, fused):
     rep = res[0][1]
     assert rep.converged and rep.iterations == ro["iterations"], (rep, ro)
     assert np.array_equal(bits(xd), bits(xo))
+
+
+def _many_patterns(O, n, npat):
+    """Tridiagonal, every 32-row warp with its own off-diagonal value (npat distinct, cycling;
+    nonsymmetric, diagonally dominant): warps share diagonals but not values -> npat distinct
+    structured patterns."""
+    rows, cols, vals = [], [], []
+    for i in range(n):
+        for j in (i - 1, i, i + 1):
+            if 0 <= j < n:
+                rows.append(i)
+                cols.append(j)
+                vals.append(4.0 if i == j else -(1.0 + ((i // 32) % npat) / 128.0))
+    return O.csr_from_triplets(n, n, rows, cols, vals)
+
+
+@pytest.mark.parametrize("npat", [40, 100])
+def test_dia_pattern_table_limit(S, O, gpu, monkeypatch, npat):
+    """<= 64 distinct patterns: the pattern-table kernel; more: the 48-byte-entry kernel
+    (patterns == 0).  Both bit-identical to the oracle (SpMV and a BiCGStab trajectory)."""
+    monkeypatch.delenv("SPARSLA_DIA_VARIANT", raising=False)
+    A = _many_patterns(O, 32 * 300 + 17, npat)
+    D = to_S(S, A).device(0)
+    d = D.dia()
+    assert d["on"], d
+    if npat <= 64:
+        assert 1 <= d["patterns"] <= 64, d
+    else:
+        assert d["patterns"] == 0, d
+    x = np.random.default_rng(npat).standard_normal(A.ncols)
+    assert_bitwise(S.spmv(D, x), O.spmv(A, x), f"{npat} patterns")
+    b = np.linspace(0.5, 1.5, A.nrows)
+    xo, ro = O.bicgstab(A, b, atol=0.0, rtol=1e-10, max_iter=5000)
+    xg, rg = S.bicgstab_solve(D, b, S.SolveOptions(atol=0.0, rtol=1e-10, max_iter=5000))
+    assert ro["converged"]
+    rep_eq(rg, ro)
+    assert_bitwise(xg, xo, f"{npat} patterns BiCGStab")
