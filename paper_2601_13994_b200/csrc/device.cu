@@ -320,6 +320,11 @@ struct DiaVariant {
       (const void*)spmv_diac_kernel<SPMV_CG, M, 1, false, true>,                                      \
       (const void*)spmv_diac_kernel<SPMV_BICG_V, M, 1, false, true>,                                  \
       (const void*)spmv_diac_kernel<SPMV_BICG_T, M, 1, false, true>}, true}
+#define DIACS(M)                                                                                     \
+    {{(const void*)spmv_diac_kernel<SPMV_PLAIN, M, 1, false, false, true>,                            \
+      (const void*)spmv_diac_kernel<SPMV_CG, M, 1, false, false, true>,                               \
+      (const void*)spmv_diac_kernel<SPMV_BICG_V, M, 1, false, false, true>,                           \
+      (const void*)spmv_diac_kernel<SPMV_BICG_T, M, 1, false, false, true>}, true}
 #define DIACP(M)                                                                                     \
     {{(const void*)spmv_diac_kernel<SPMV_PLAIN, M, 1, true>, (const void*)spmv_diac_kernel<SPMV_CG, M, 1, true>, \
       (const void*)spmv_diac_kernel<SPMV_BICG_V, M, 1, true>,                                         \
@@ -327,15 +332,17 @@ struct DiaVariant {
 // 3..5: register-pattern kernel (spmv_diar_kernel) at 4 / 5 / 3 CTAs per SM; 6..8: pattern-
 // table kernel (spmv_diac_kernel) at 5 / 6 / 4 / 8 CTAs per SM; 10, 11: rounds unrolled by 2
 // at 6 / 5 CTAs per SM; 12, 13: persistent at 6 / 8 CTAs per SM; 14, 15: far diagonals
-// without L1 allocation at 6 / 8 CTAs per SM
+// without L1 allocation at 6 / 8 CTAs per SM; 16, 17: round 0 loaded speculatively with the
+// most frequent pattern at 6 / 5 CTAs per SM
 static const DiaVariant kDiaVariants[] = {DIAV(1, 5), DIAV(1, 4), DIAV(2, 4), DIARV(4), DIARV(5), DIARV(3),
                                           DIACV(5, 1), DIACV(6, 1), DIACV(4, 1), DIACV(8, 1), DIACV(6, 2), DIACV(5, 2),
-                                          DIACP(6), DIACP(8), DIACN(6), DIACN(8)};
+                                          DIACP(6), DIACP(8), DIACN(6), DIACN(8), DIACS(6), DIACS(5)};
 #undef DIAV
 #undef DIARV
 #undef DIACV
 #undef DIACP
 #undef DIACN
+#undef DIACS
 constexpr int kNumDiaVariants = sizeof(kDiaVariants) / sizeof(kDiaVariants[0]);
 
 // diagonal-warp table (spmv_dia.cuh) from the device CSR and dictionary indices; kept when
@@ -360,17 +367,26 @@ static void build_dia_patterns(DevCsr* A, const int32_t* tab, long long nwarps) 
     CK(cudaMemsetAsync(keys, 0, kDiaHashSlots * 8, s));
     CK(cudaMemsetAsync(rep, 0xFF, kDiaHashSlots * 8, s));
     CK(cudaMemsetAsync(flags, 0, 2 * sizeof(int), s));
-    dia_hash_kernel<<<grid_for(nwarps, 256), 256, 0, s>>>(tab, nwarps, keys, rep, slot, flags);
+    unsigned* count = dalloc<unsigned>(kDiaHashSlots);
+    CK(cudaMemsetAsync(count, 0, kDiaHashSlots * sizeof(unsigned), s));
+    dia_hash_kernel<<<grid_for(nwarps, 256), 256, 0, s>>>(tab, nwarps, keys, rep, slot, flags, count);
     CK(cudaGetLastError());
     std::vector<unsigned long long> hk(2 * kDiaHashSlots);
+    std::vector<unsigned> hc(kDiaHashSlots);
     int hf[2] = {0, 0};
+    CK(cudaMemcpyAsync(hc.data(), count, kDiaHashSlots * sizeof(unsigned), cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(hk.data(), keys, hk.size() * 8, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(hf, flags, sizeof(hf), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    std::vector<std::pair<unsigned long long, int>> used;  // (representative warp, slot)
+    // (representative warp, slot), most frequent pattern first (ties: lowest warp) — the
+    // speculative variant loads round 0 with pattern 0
+    std::vector<std::pair<unsigned long long, int>> used;
     for (int i = 0; i < kDiaHashSlots; ++i)
         if (hk[i] != 0ull) used.push_back({hk[kDiaHashSlots + i], i});
-    std::sort(used.begin(), used.end());
+    std::sort(used.begin(), used.end(), [&](const std::pair<unsigned long long, int>& a,
+                                            const std::pair<unsigned long long, int>& b) {
+        return hc[a.second] != hc[b.second] ? hc[a.second] > hc[b.second] : a.first < b.first;
+    });
     bool ok = !hf[0] && !used.empty() && (int)used.size() <= kDiaPatterns;
     if (ok) {
         std::vector<int> pid_of(kDiaHashSlots, (int)kDiaPidUnstructured);
@@ -409,6 +425,7 @@ static void build_dia_patterns(DevCsr* A, const int32_t* tab, long long nwarps) 
     cudaFree(keys);
     cudaFree(flags);
     cudaFree(slot);
+    cudaFree(count);
 }
 
 static void build_dia(DevCsr* A) {

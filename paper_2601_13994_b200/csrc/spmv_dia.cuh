@@ -479,7 +479,7 @@ constexpr int kDiaHashSlots = 512;
 // kDiaHashSlots 64-bit keys; the lowest warp index of a slot is its representative
 static __global__ void dia_hash_kernel(const int32_t* __restrict__ tab, long long nwarps,
                                        unsigned long long* keys, unsigned long long* rep, int16_t* slot,
-                                       int* overflow) {
+                                       int* overflow, unsigned* count) {
     const long long w = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (w >= nwarps) return;
     const int32_t* e = tab + w * kDiaInts;
@@ -493,6 +493,7 @@ static __global__ void dia_hash_kernel(const int32_t* __restrict__ tab, long lon
         const unsigned long long prev = atomicCAS(keys + i, 0ull, h);
         if (prev == 0ull || prev == h) {
             atomicMin(rep + i, (unsigned long long)w);
+            atomicAdd(count + i, 1u);
             slot[w] = (int16_t)i;
             return;
         }
@@ -543,7 +544,10 @@ __device__ __forceinline__ double dia_x(const double* __restrict__ a, int d) {
     return __ldg(a);
 }
 
-template <int MODE, int MINB, int UNR = 1, bool PERS = false, bool L1NA = false>
+// SPEC: round 0's x operands are loaded with pattern 0 (the most frequent: patterns are
+// numbered by count) at CTA start, in parallel with the load of the warp's pattern words —
+// used when round 0 turns out to be a pattern-0 interior warp, otherwise reloaded.
+template <int MODE, int MINB, int UNR = 1, bool PERS = false, bool L1NA = false, bool SPEC = false>
 __global__ void __launch_bounds__(kSpmvThreads, MINB) spmv_diac_kernel(SpmvParams P, const __grid_constant__ DiaConst C) {
     constexpr int ND = SpmvDots<MODE>::n;
     constexpr int NA = ND > 0 ? ND : 1;
@@ -586,6 +590,16 @@ __global__ void __launch_bounds__(kSpmvThreads, MINB) spmv_diac_kernel(SpmvParam
     }
     const int n = (int)P.n;  // int32 CSR: rows < 2^31
     const double* __restrict__ x = P.x;
+    double xs[7];
+    if constexpr (SPEC) {  // after the halo wait: the operands may be halo values
+        const int rs = (int)base + t;
+#pragma unroll
+        for (int u = 0; u < 7; ++u) {
+            const int c = rs + C.pat[0].d[u];
+            xs[u] = 0.0;
+            ldg_pred(xs[u], x + c, rs < n && c >= 0 && (long long)c < P.ncols);
+        }
+    }
     double acc[NA];
 #pragma unroll
     for (int d = 0; d < NA; ++d) acc[d] = 0.0;
@@ -609,8 +623,13 @@ __global__ void __launch_bounds__(kSpmvThreads, MINB) spmv_diac_kernel(SpmvParam
             const int rb = live ? row : 0;
             double xv[7];
             if (m == 7 && ex == (kDiaNoEx | (kDiaNoEx << 8)) && __all_sync(0xffffffffu, live)) {
+                if (SPEC && r == 0 && pid == 0) {
 #pragma unroll
-                for (int u = 0; u < 7; ++u) xv[u] = dia_x<L1NA>(x + (rb + pt.d[u]), pt.d[u]);
+                    for (int u = 0; u < 7; ++u) xv[u] = xs[u];
+                } else {
+#pragma unroll
+                    for (int u = 0; u < 7; ++u) xv[u] = dia_x<L1NA>(x + (rb + pt.d[u]), pt.d[u]);
+                }
 #pragma unroll
                 for (int u = 0; u < 7; ++u) y = __dadd_rn(y, __dmul_rn(pt.v[u], xv[u]));
             } else {

@@ -41,7 +41,7 @@ def _dia_on(monkeypatch):
     monkeypatch.setenv("SPARSLA_DIA", "1")
 
 
-@pytest.mark.parametrize("variant", list(range(16)))
+@pytest.mark.parametrize("variant", list(range(18)))
 def test_dia_variants_bitwise(S, O, gpu, monkeypatch, variant):
     """Every kDiaVariants entry (1 or 2 rounds per step, occupancy), odd round counts."""
     monkeypatch.setenv("SPARSLA_DIA_VARIANT", str(variant))
